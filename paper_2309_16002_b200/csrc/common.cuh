@@ -1,0 +1,54 @@
+// common.cuh — internal definitions shared by the librbrp kernels (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/rbrp.h"
+
+namespace rbrp {
+
+constexpr int kChunk = RBRP_CHUNK;   // rows per sampling chunk
+constexpr int kMaxB = RBRP_MAX_B;    // largest block size
+constexpr int64_t kJMax = 1 << 20;   // cap on draws per block (R6)
+
+// Loop state kept on the device so that every decision of Alg. 2 (stop test,
+// b_t, b') is taken by a kernel and the host only reads it once per block.
+struct DevState {
+  double D0;          // ||d^(0)||_1 (Alg. 2 l.2)
+  double total;       // ||d^(t)||_1 (fixed-order chunk prefix, last entry)
+  double tau;         // tolerance (<= 0: fixed rank)
+  double tau_b;       // filter tolerance (< 0: 1/b_t)
+  int64_t k;          // |S|
+  int64_t k_cap;      // capacity / fixed rank
+  int64_t npos;       // rows with d > 0
+  int32_t t;          // block counter (l.4)
+  int32_t b;          // block size parameter
+  int32_t b_t;        // candidates in the current block
+  int32_t b_prime;    // kept by the filter (l.8)
+  int32_t stop;       // 1: loop ended
+  uint32_t flags;     // RBRP_F_* bits
+  int32_t nonfinite;  // set by k_init_norms
+  int32_t draws;      // Philox draws consumed by the current block
+  int32_t rank_def;   // pivoted Cholesky hit a non-positive pivot
+  int32_t pad;
+};
+
+// fp64 warp reduction in a fixed butterfly order (bitwise deterministic)
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <typename T> struct VecT;
+template <> struct VecT<double> { using v2 = double2; };
+template <> struct VecT<float> { using v2 = float2; };
+
+inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+// padded block-width bucket used to instantiate the projection kernels
+__host__ __device__ inline int bucket_of(int bp) {
+  return bp <= 16 ? 16 : bp <= 32 ? 32 : bp <= 64 ? 64 : 128;
+}
+
+}  // namespace rbrp

@@ -1,0 +1,105 @@
+// k_formw.cu — a6 interpolation matrix, Alg. 3.
+//
+// L_1 = L(S,:) is exactly lower-triangular in selection order (reading R13), so
+// L_2 L_1^{-1} is a triangular solve (north_star step 6).  We form
+// L_1^{-1} once (k_trinv: one warp per column, forward substitution in fp64), then
+// W = L L_1^{-1} for all local rows with the tile GEMM (k_gemm_nt, B = L_1^{-T}), and
+// finally W(S,:) = I exactly (Alg. 3 l.2).  W_CLIPPED is reported when
+// min |diag L_1| < 1e-12 max |diag L_1| (Remark 5.2, reading R17).
+#include <float.h>
+
+#include "launch.cuh"
+
+namespace rbrp {
+
+template <typename T>
+__global__ void k_gather_L1(const T* __restrict__ L, int64_t ldl, const int64_t* __restrict__ S,
+                            int64_t k, int64_t n_local, int64_t row_offset, double* __restrict__ L1) {
+  const int64_t i = blockIdx.x;
+  const int64_t r = S[i] - row_offset;
+  for (int64_t j = threadIdx.x; j < k; j += blockDim.x)
+    L1[i * k + j] = (r >= 0 && r < n_local) ? (double)L[r * ldl + j] : 0.0;
+}
+
+template <typename T>
+cudaError_t launch_gather_L1(const T* L, int64_t ldl, const int64_t* S, int64_t k, int64_t n_local,
+                             int64_t row_offset, double* L1, cudaStream_t s) {
+  if (k <= 0) return cudaSuccess;
+  k_gather_L1<T><<<(unsigned)k, 256, 0, s>>>(L, ldl, S, k, n_local, row_offset, L1);
+  return cudaGetLastError();
+}
+
+constexpr int kTrinvWarps = 4;
+
+// Column j of L_1^{-1}: x_j = 1/L(j,j); x_i = -(sum_{j<=m<i} L(i,m) x_m) / L(i,i).
+// Written transposed: LinvT(j, m) = x_m (zeros for m < j).
+template <typename T>
+__global__ void __launch_bounds__(32 * kTrinvWarps) k_trinv(const double* __restrict__ L1, int64_t k,
+                                                            T* __restrict__ LinvT, DevState* st) {
+  extern __shared__ double xs[];   // [kTrinvWarps][k]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t j = (int64_t)blockIdx.x * kTrinvWarps + w;
+  if (blockIdx.x == 0 && w == 0) {
+    double mx = 0.0, mn = DBL_MAX;
+    for (int64_t i = lane; i < k; i += 32) {
+      const double a = fabs(L1[i * k + i]);
+      mx = fmax(mx, a);
+      mn = fmin(mn, a);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    }
+    if (lane == 0 && mn < 1e-12 * mx) atomicOr(&st->flags, (uint32_t)RBRP_F_W_CLIPPED);
+  }
+  if (j >= k) return;
+  double* x = xs + (int64_t)w * k;
+  if (lane == 0) x[j] = 1.0 / L1[j * k + j];
+  __syncwarp();
+  for (int64_t i = j + 1; i < k; ++i) {
+    double s = 0.0;
+    for (int64_t m = j + lane; m < i; m += 32) s += L1[i * k + m] * x[m];
+    s = warp_sum(s);
+    if (lane == 0) x[i] = -s / L1[i * k + i];
+    __syncwarp();
+  }
+  for (int64_t m = lane; m < k; m += 32) LinvT[j * k + m] = (m < j) ? T(0) : (T)x[m];
+}
+
+template <typename T>
+cudaError_t launch_trinv(const double* L1, int64_t k, T* LinvT, DevState* st, cudaStream_t s) {
+  if (k <= 0) return cudaSuccess;
+  size_t smem = (size_t)kTrinvWarps * k * sizeof(double);
+  cudaFuncSetAttribute(k_trinv<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_trinv<T><<<ceil_div(k, kTrinvWarps), 32 * kTrinvWarps, smem, s>>>(L1, k, LinvT, st);
+  return cudaGetLastError();
+}
+
+template <typename T>
+__global__ void k_w_identity(T* __restrict__ W, int64_t ldw, const int64_t* __restrict__ S,
+                             int64_t k, int64_t n_local, int64_t row_offset) {
+  const int64_t i = blockIdx.x;
+  const int64_t r = S[i] - row_offset;
+  if (r < 0 || r >= n_local) return;
+  for (int64_t j = threadIdx.x; j < k; j += blockDim.x) W[r * ldw + j] = (j == i) ? T(1) : T(0);
+}
+
+template <typename T>
+cudaError_t launch_w_identity(T* W, int64_t ldw, const int64_t* S, int64_t k, int64_t n_local,
+                              int64_t row_offset, cudaStream_t s) {
+  if (k <= 0) return cudaSuccess;
+  k_w_identity<T><<<(unsigned)k, 256, 0, s>>>(W, ldw, S, k, n_local, row_offset);
+  return cudaGetLastError();
+}
+
+#define INSTW(T)                                                                                  \
+  template cudaError_t launch_gather_L1<T>(const T*, int64_t, const int64_t*, int64_t, int64_t,  \
+                                           int64_t, double*, cudaStream_t);                      \
+  template cudaError_t launch_trinv<T>(const double*, int64_t, T*, DevState*, cudaStream_t);     \
+  template cudaError_t launch_w_identity<T>(T*, int64_t, const int64_t*, int64_t, int64_t,       \
+                                            int64_t, cudaStream_t);
+INSTW(double)
+INSTW(float)
+
+}  // namespace rbrp

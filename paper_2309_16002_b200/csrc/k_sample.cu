@@ -1,0 +1,203 @@
+// k_sample.cu — a2 sample + a5 stop test (Alg. 2 l.3-5).
+//
+// One CTA.  (1) Inclusive prefix over the per-chunk totals in a fixed order (warp 0),
+// giving ||d||_1 bit-identically on every rank; (2) the stop test of l.3 (reading R1:
+// continue while ||d||_1 > tau ||d^(0)||_1, or |S| < k in fixed-rank mode) and l.4's
+// b_t = min(b, k - |S|) (reading R15); (3) S_t ~ d/||d||_1 without replacement
+// (Eq. 2.2; reading R6): rounds of 256 Philox draws (counter (j, t, 0, 0)),
+// each resolved by binary search over the chunk prefix and then over the chunk-local
+// prefix of d (reading R8), repeats rejected in draw order.  Small support (reading
+// R7): all positive rows in row order.
+#include "launch.cuh"
+#include "philox.cuh"
+
+namespace rbrp {
+
+constexpr int kSampleThreads = 256;
+
+// smallest local row r of global chunk q with cpre[r] > tq; falls back to the last
+// positive row of the chunk when tq is past the chunk's end (rounding).
+__device__ int64_t resolve_in_chunk(int q, double tq, const double* __restrict__ cpre,
+                                    const double* __restrict__ dvec, int64_t n_local,
+                                    int64_t row_offset) {
+  int64_t lo = (int64_t)q * kChunk - row_offset;
+  int64_t hi = lo + kChunk;
+  if (hi > n_local) hi = n_local;
+  if (lo < 0 || lo >= n_local) return -1;   // chunk owned by another rank
+  int64_t a = lo, b = hi;                    // search in [a, b)
+  while (a < b) {
+    int64_t m = (a + b) >> 1;
+    if (cpre[m] > tq) b = m; else a = m + 1;
+  }
+  if (a >= hi) {
+    a = hi - 1;
+    while (a > lo && !(dvec[a] > 0.0)) --a;
+  }
+  return a + row_offset;
+}
+
+__global__ void __launch_bounds__(kSampleThreads) k_sample(SampleArgs A) {
+  DevState* st = A.st;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  __shared__ int s_stop, s_bt, s_c, s_new;
+  __shared__ double s_total;
+  __shared__ int64_t s_np;
+  __shared__ int64_t chosen[kMaxB];
+  __shared__ int64_t cand[kSampleThreads];
+  __shared__ int wcount[kSampleThreads / 32];
+
+  // the previous block's kept skeletons become part of S (Alg. 2 l.14)
+  // (1) chunk prefix, fixed order: lane l sums a contiguous range of chunks
+  if (w == 0) {
+    const int nch = A.nchunks;
+    const int per = (nch + 31) / 32;
+    const int c0 = lane * per, c1 = min(nch, c0 + per);
+    double s = 0.0;
+    long long np = 0;
+    for (int c = c0; c < c1; ++c) { s += A.ctot[c]; np += A.cpos[c]; }
+    double incl = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      double y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    double p = __shfl_up_sync(0xffffffffu, incl, 1);
+    if (lane == 0) p = 0.0;
+    for (int c = c0; c < c1; ++c) { p += A.ctot[c]; A.cprefix[c] = p; }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) np += __shfl_xor_sync(0xffffffffu, np, o);
+    __syncwarp();
+    if (lane == 0) {
+      s_total = A.cprefix[nch - 1];
+      s_np = np;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const double total = s_total;
+    st->k += st->b_prime;          // l.14: S <- S u S'_t of the previous block
+    st->b_prime = 0;
+    st->total = total;
+    st->npos = s_np;
+    if (A.first) st->D0 = total;
+    const bool fixed = !(st->tau > 0.0);
+    bool stop = st->stop != 0;
+    if (!stop && st->k >= st->k_cap) {
+      stop = true;
+      if (!fixed && total > st->tau * st->D0) st->flags |= RBRP_F_TOL_UNREACHED;
+    }
+    if (!stop && !fixed && !(total > st->tau * st->D0)) stop = true;   // l.3
+    if (!stop && s_np == 0) {
+      stop = true;
+      st->flags |= RBRP_F_SUPPORT_EXHAUSTED;
+    }
+    if (!stop && A.replay_len == -2) stop = true;   // replay log exhausted
+    int bt = 0;
+    if (!stop) {
+      st->t += 1;                                                     // l.4
+      int64_t room = st->k_cap - st->k;
+      bt = (int)(st->b < room ? st->b : room);
+    }
+    st->stop = stop ? 1 : 0;
+    s_stop = stop;
+    s_bt = bt;
+    s_c = 0;
+  }
+  __syncthreads();
+  if (s_stop) return;
+  if (A.replay_len >= 0) {
+    if (tid == 0) { st->b_t = A.replay_len; st->draws = 0; }
+    return;
+  }
+  const int bt = s_bt;
+  if (s_np <= bt) {
+    // reading R7: every positive-weight row, in row order (local rows; single GPU)
+    for (int64_t r0 = 0; r0 < A.n_local; r0 += kSampleThreads) {
+      int64_t r = r0 + tid;
+      int f = (r < A.n_local && A.dvec[r] > 0.0) ? 1 : 0;
+      unsigned m = __ballot_sync(0xffffffffu, f);
+      if (lane == 0) wcount[w] = __popc(m);
+      __syncthreads();
+      int off = s_c;
+      for (int q = 0; q < w; ++q) off += wcount[q];
+      off += __popc(m & ((1u << lane) - 1u));
+      if (f && off < kMaxB) chosen[off] = r + A.row_offset;
+      __syncthreads();
+      if (tid == 0) {
+        int tot = 0;
+        for (int q = 0; q < kSampleThreads / 32; ++q) tot += wcount[q];
+        s_c += tot;
+      }
+      __syncthreads();
+    }
+    const int c = min(s_c, kMaxB);
+    for (int i = tid; i < c; i += kSampleThreads) A.S_t[i] = chosen[i];
+    if (tid == 0) {
+      st->b_t = c;
+      st->draws = 0;
+      st->flags |= RBRP_F_SUPPORT_EXHAUSTED;
+    }
+    return;
+  }
+  // (3) rejection rounds
+  const double total = s_total;
+  const uint2 key = make_uint2((uint32_t)(A.seed & 0xffffffffu), (uint32_t)(A.seed >> 32));
+  const uint32_t t = (uint32_t)st->t;
+  int64_t jb = 0;
+  for (; jb < kJMax; jb += kSampleThreads) {
+    const int c = s_c;
+    if (c >= bt) break;
+    const uint32_t j = (uint32_t)(jb + tid);
+    const double u = u53(philox4x32_10(make_uint4(j, t, 0u, 0u), key));
+    const double target = u * total;
+    // first chunk q with cprefix[q] > target
+    int a = 0, b = A.nchunks;
+    while (a < b) {
+      int m = (a + b) >> 1;
+      if (A.cprefix[m] > target) b = m; else a = m + 1;
+    }
+    int64_t row;
+    if (a >= A.nchunks) {
+      // past the end (rounding): last positive row overall
+      int q = A.nchunks - 1;
+      while (q > 0 && A.cpos[q] == 0) --q;
+      row = resolve_in_chunk(q, 1e308, A.cpre, A.dvec, A.n_local, A.row_offset);
+    } else {
+      const double tq = target - (a > 0 ? A.cprefix[a - 1] : 0.0);
+      row = resolve_in_chunk(a, tq, A.cpre, A.dvec, A.n_local, A.row_offset);
+    }
+    cand[tid] = row;
+    __syncthreads();
+    int isnew = row >= 0;
+    for (int m = 0; m < c && isnew; ++m) isnew = chosen[m] != row;
+    for (int m = 0; m < tid && isnew; ++m) isnew = cand[m] != row;
+    unsigned msk = __ballot_sync(0xffffffffu, isnew);
+    if (lane == 0) wcount[w] = __popc(msk);
+    __syncthreads();
+    int off = 0;
+    for (int q = 0; q < w; ++q) off += wcount[q];
+    off += __popc(msk & ((1u << lane) - 1u));
+    if (isnew && c + off < bt) chosen[c + off] = row;
+    if (isnew && c + off == bt - 1) s_new = (int)(jb + tid + 1);   // draws consumed
+    __syncthreads();
+    if (tid == 0) {
+      int tot = 0;
+      for (int q = 0; q < kSampleThreads / 32; ++q) tot += wcount[q];
+      s_c = min(bt, c + tot);
+    }
+    __syncthreads();
+  }
+  const int c = s_c;
+  for (int i = tid; i < c; i += kSampleThreads) A.S_t[i] = chosen[i];
+  if (tid == 0) {
+    st->b_t = c;
+    st->draws = (c == bt) ? s_new : (int)jb;
+  }
+}
+
+cudaError_t launch_sample(const SampleArgs& a, cudaStream_t s) {
+  k_sample<<<1, kSampleThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace rbrp

@@ -1,0 +1,232 @@
+"""Thin ctypes binding of librbrp.so (include/rbrp.h).
+
+Argument marshalling only: torch supplies device memory (workspace, W) and the
+current CUDA stream; every step of RBRP runs in the library's sm_100a kernels.
+There is no CPU or PyTorch fallback: if the library cannot be loaded, every
+call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import os
+from typing import List, Optional, Sequence
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "librbrp.so")
+
+RBRP_F32, RBRP_F64 = 0, 1
+RBRP_INPLACE, RBRP_NO_W, RBRP_FORM_PAPER = 1, 2, 4
+F_TOL_UNREACHED, F_ZERO_BLOCK, F_W_CLIPPED, F_SUPPORT_EXHAUSTED, F_NEAR_TIE = 1, 2, 4, 8, 16
+CHUNK = 4096
+MAX_B = 128
+
+STATUS = {0: "RBRP_OK", -1: "RBRP_EINVAL", -2: "RBRP_ENONFINITE", -3: "RBRP_EDEGENERATE",
+          -4: "RBRP_ENOMEM", -5: "RBRP_ECUDA", -6: "RBRP_ENCCL", -7: "RBRP_EREPLAY",
+          -8: "RBRP_ENOTSUP"}
+
+EXPORTED = ["rbrp_version", "rbrp_strerror", "rbrp_workspace_size", "rbrp_id",
+            "rbrp_comm_unique_id", "rbrp_comm_init", "rbrp_comm_destroy"]
+
+
+class Problem(ctypes.Structure):
+    _fields_ = [("dtype", ctypes.c_int), ("n_global", ctypes.c_int64), ("n_local", ctypes.c_int64),
+                ("row_offset", ctypes.c_int64), ("d", ctypes.c_int64), ("ld", ctypes.c_int64),
+                ("tol", ctypes.c_double), ("k_max", ctypes.c_int64), ("b", ctypes.c_int32),
+                ("tau_b", ctypes.c_double), ("greedy", ctypes.c_int32), ("seed", ctypes.c_uint64),
+                ("flags", ctypes.c_uint32), ("replay_blocks", ctypes.POINTER(ctypes.c_int64)),
+                ("replay_lens", ctypes.POINTER(ctypes.c_int32)),
+                ("replay_pivots", ctypes.POINTER(ctypes.c_int32)),
+                ("replay_nblocks", ctypes.c_int32)]
+
+
+class Report(ctypes.Structure):
+    _fields_ = [("k", ctypes.c_int64), ("resid_rel", ctypes.c_double), ("fro2", ctypes.c_double),
+                ("nblocks", ctypes.c_int32), ("flags", ctypes.c_uint32),
+                ("max_blocks", ctypes.c_int32), ("b_t", ctypes.POINTER(ctypes.c_int32)),
+                ("b_prime", ctypes.POINTER(ctypes.c_int32)), ("rho", ctypes.POINTER(ctypes.c_double)),
+                ("block_idx", ctypes.POINTER(ctypes.c_int64)),
+                ("block_piv", ctypes.POINTER(ctypes.c_int32)), ("ms_total", ctypes.c_float)]
+
+
+class RBRPError(RuntimeError):
+    def __init__(self, status: int, what: str = ""):
+        self.status = status
+        super().__init__(f"{STATUS.get(status, status)}{': ' + what if what else ''}")
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load librbrp.so (raises if it is missing: there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"librbrp.so not built ({LIB_PATH}); run __graft_entry__.build()")
+        L = ctypes.CDLL(LIB_PATH)
+        L.rbrp_version.restype = ctypes.c_int
+        L.rbrp_strerror.restype = ctypes.c_char_p
+        L.rbrp_strerror.argtypes = [ctypes.c_int]
+        L.rbrp_workspace_size.argtypes = [ctypes.POINTER(Problem), ctypes.POINTER(ctypes.c_size_t)]
+        L.rbrp_workspace_size.restype = ctypes.c_int
+        L.rbrp_id.argtypes = [ctypes.POINTER(Problem), ctypes.c_void_p, ctypes.c_void_p,
+                              ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p,
+                              ctypes.POINTER(ctypes.c_int64), ctypes.c_void_p, ctypes.POINTER(Report)]
+        L.rbrp_id.restype = ctypes.c_int
+        L.rbrp_comm_unique_id.argtypes = [ctypes.c_void_p]
+        L.rbrp_comm_init.argtypes = [ctypes.POINTER(ctypes.c_void_p), ctypes.c_void_p, ctypes.c_int,
+                                     ctypes.c_int, ctypes.c_int]
+        L.rbrp_comm_destroy.argtypes = [ctypes.c_void_p]
+        _lib = L
+    return _lib
+
+
+@dataclasses.dataclass
+class Result:
+    S: torch.Tensor                 # int64 [k] on CPU, selection order
+    W: Optional[torch.Tensor]       # [n_local, k] on the device (None with with_W=False)
+    k: int
+    resid_rel: float                # ||d||_1 / ||d0||_1 = errskel / ||X||_F^2
+    fro2: float
+    flags: int
+    nblocks: int
+    b_t: List[int]
+    b_prime: List[int]
+    rho: List[float]
+    blocks: List[List[int]]         # candidate blocks S_t (global ids, draw order)
+    pivots: List[List[int]]         # local pivot orders
+    ms: float                       # device time of the call (CUDA events), ms
+
+
+def _problem(X: torch.Tensor, tol, k, b, seed, k_max, tau_b, flags, n_global, row_offset, greedy):
+    if X.dim() != 2 or X.stride(1) != 1:
+        raise ValueError("X must be a 2-D row-major tensor (stride(1) == 1)")
+    if X.dtype not in (torch.float32, torch.float64):
+        raise ValueError("X must be float32 or float64")
+    p = Problem()
+    p.dtype = RBRP_F64 if X.dtype == torch.float64 else RBRP_F32
+    p.n_local = X.shape[0]
+    p.n_global = n_global if n_global is not None else X.shape[0]
+    p.row_offset = row_offset
+    p.d = X.shape[1]
+    p.ld = X.stride(0) if X.shape[0] > 1 else X.shape[1]
+    if k is not None:
+        p.tol = 0.0
+        p.k_max = int(k)
+    else:
+        p.tol = float(tol)
+        p.k_max = int(k_max or 0)
+    p.b = int(b)
+    p.tau_b = float(tau_b)
+    p.greedy = int(bool(greedy))
+    p.seed = int(seed) & 0xFFFFFFFFFFFFFFFF
+    p.flags = flags
+    p.replay_nblocks = 0
+    return p
+
+
+def workspace_size(X: torch.Tensor, tol=None, k=None, b=16, k_max=0, tau_b=-1.0, with_W=True,
+                   inplace=False, n_global=None, row_offset=0) -> int:
+    flags = (0 if with_W else RBRP_NO_W) | (RBRP_INPLACE if inplace else 0)
+    p = _problem(X, tol, k, b, 0, k_max, tau_b, flags, n_global, row_offset, False)
+    sz = ctypes.c_size_t()
+    rc = lib().rbrp_workspace_size(ctypes.byref(p), ctypes.byref(sz))
+    if rc:
+        raise RBRPError(rc)
+    return sz.value
+
+
+def id(X: torch.Tensor, tol: Optional[float] = None, k: Optional[int] = None, b: int = 16,
+       seed: int = 0, k_max: int = 0, tau_b: float = -1.0, with_W: bool = True,
+       inplace: bool = False, greedy: bool = False,
+       replay_blocks: Optional[Sequence[Sequence[int]]] = None,
+       replay_pivots: Optional[Sequence[Sequence[int]]] = None,
+       max_blocks: int = 1024, log_blocks: bool = True, workspace: Optional[torch.Tensor] = None,
+       comm=None, n_global: Optional[int] = None, row_offset: int = 0) -> Result:
+    """RBRP interpolative decomposition X ~ W X_S of a CUDA tensor X (n x d).
+
+    tol: tau, relative to ||X||_F^2 (for an (r, eps)-ID pass tol = (1+eps) eta_r,
+    PAPER.md l.86); or k: fixed rank.  b: block size; seed: Philox key;
+    tau_b < 0 -> 1/b_t.  Returns S (CPU int64, selection order), W (device,
+    n x k, W[S] = I) and the per-block log."""
+    if not X.is_cuda:
+        raise ValueError("X must be a CUDA tensor (use id_host for host buffers)")
+    if tol is None and k is None:
+        raise ValueError("need tol or k")
+    L = lib()
+    flags = (0 if with_W else RBRP_NO_W) | (RBRP_INPLACE if inplace else 0)
+    p = _problem(X, tol, k, b, seed, k_max, tau_b, flags, n_global, row_offset, greedy)
+    keep = []
+    if replay_blocks is not None:
+        flat = [int(i) for blk in replay_blocks for i in blk]
+        lens = [len(blk) for blk in replay_blocks]
+        arr = (ctypes.c_int64 * max(1, len(flat)))(*flat)
+        la = (ctypes.c_int32 * max(1, len(lens)))(*lens)
+        p.replay_blocks = ctypes.cast(arr, ctypes.POINTER(ctypes.c_int64))
+        p.replay_lens = ctypes.cast(la, ctypes.POINTER(ctypes.c_int32))
+        p.replay_nblocks = len(lens)
+        keep += [arr, la]
+        if replay_pivots is not None:
+            fp = [int(i) for blk in replay_pivots for i in blk]
+            pa = (ctypes.c_int32 * max(1, len(fp)))(*fp)
+            p.replay_pivots = ctypes.cast(pa, ctypes.POINTER(ctypes.c_int32))
+            keep.append(pa)
+    sz = ctypes.c_size_t()
+    rc = L.rbrp_workspace_size(ctypes.byref(p), ctypes.byref(sz))
+    if rc:
+        raise RBRPError(rc, "workspace_size")
+    if workspace is None or workspace.numel() < sz.value:
+        workspace = torch.empty(sz.value, dtype=torch.uint8, device=X.device)
+    k_cap = p.k_max if p.k_max > 0 else min(p.n_global, p.d)
+    W = torch.empty((X.shape[0], k_cap), dtype=X.dtype, device=X.device) if with_W else None
+    S = torch.empty(k_cap, dtype=torch.int64)
+    rep = Report()
+    mb = max_blocks
+    b_t = (ctypes.c_int32 * mb)()
+    b_pr = (ctypes.c_int32 * mb)()
+    rho = (ctypes.c_double * mb)()
+    rep.max_blocks = mb
+    rep.b_t = ctypes.cast(b_t, ctypes.POINTER(ctypes.c_int32))
+    rep.b_prime = ctypes.cast(b_pr, ctypes.POINTER(ctypes.c_int32))
+    rep.rho = ctypes.cast(rho, ctypes.POINTER(ctypes.c_double))
+    if log_blocks:
+        bidx = (ctypes.c_int64 * (mb * b))()
+        bpiv = (ctypes.c_int32 * (mb * b))()
+        rep.block_idx = ctypes.cast(bidx, ctypes.POINTER(ctypes.c_int64))
+        rep.block_piv = ctypes.cast(bpiv, ctypes.POINTER(ctypes.c_int32))
+    stream = torch.cuda.current_stream(X.device).cuda_stream
+    rc = L.rbrp_id(ctypes.byref(p), ctypes.c_void_p(X.data_ptr()),
+                   ctypes.c_void_p(workspace.data_ptr()), sz.value,
+                   ctypes.c_void_p(comm) if comm else None, ctypes.c_void_p(stream),
+                   ctypes.cast(S.data_ptr(), ctypes.POINTER(ctypes.c_int64)),
+                   ctypes.c_void_p(W.data_ptr()) if W is not None else None, ctypes.byref(rep))
+    if rc:
+        raise RBRPError(rc, L.rbrp_strerror(rc).decode())
+    kk = rep.k
+    nb = min(rep.nblocks, mb)
+    blocks, pivots = [], []
+    if log_blocks:
+        for t in range(nb):
+            bt = b_t[t]
+            blocks.append([bidx[t * b + i] for i in range(bt)])
+            pivots.append([bpiv[t * b + i] for i in range(bt)])
+    return Result(S=S[:kk].clone(), W=W[:, :kk] if W is not None else None, k=kk,
+                  resid_rel=rep.resid_rel, fro2=rep.fro2, flags=rep.flags, nblocks=rep.nblocks,
+                  b_t=list(b_t[:nb]), b_prime=list(b_pr[:nb]), rho=list(rho[:nb]),
+                  blocks=blocks, pivots=pivots, ms=rep.ms_total)
+
+
+def id_host(X_host: torch.Tensor, device="cuda", **kw):
+    """End-to-end entry with a HOST input: copies X (pinned host -> HBM), runs
+    id(), and copies W back to pinned host memory.  Returns (Result, W_host)."""
+    Xd = X_host.to(device, non_blocking=True)
+    res = id(Xd, **kw)
+    W_host = None
+    if res.W is not None:
+        W_host = torch.empty(res.W.shape, dtype=res.W.dtype, pin_memory=True)
+        W_host.copy_(res.W, non_blocking=True)
+    torch.cuda.current_stream(Xd.device).synchronize()
+    return res, W_host

@@ -1,0 +1,229 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Tolerances (DESIGN.md §3 R23/R24, north_star): per-block rho_t absolutely within
+1e-10 (fp64) / 1e-4 (fp32); W within max(tol, 10 kappa(L_1) u) relative in
+Frobenius norm; skeletons and filtered ranks exact (integer results).
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import rbrp as O
+from oracle import referee as R
+from workloads import CONFIGS, make, small_config
+
+pytestmark = pytest.mark.gpu
+
+cuda = pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")
+
+
+def _rb():
+    import paper_2309_16002_b200 as rb
+    return rb
+
+
+def _tol(dtype):
+    return 1e-10 if dtype == np.float64 else 1e-4
+
+
+def _check_W(Xnp, res, ores, dtype):
+    W = res.W.double().cpu().numpy()
+    Wo, kappa, _ = O.form_W(ores.L, ores.S, method="trsm")
+    u = 1.1e-16 if dtype == np.float64 else 6e-8
+    tol = max(_tol(dtype), 10 * kappa * u)
+    assert np.linalg.norm(W - Wo) <= tol * np.linalg.norm(Wo)
+    S = res.S.numpy()
+    assert np.array_equal(W[S], np.eye(len(S)))           # Alg. 3 l.2: exactly I
+
+
+def _same_seed(cfg, tau=None, k=None, seed=0, **kw):
+    rb = _rb()
+    X = make(cfg)
+    Xnp = X.numpy()
+    ores = O.rbrp(Xnp, tau=tau, k=k, b=cfg.b, seed=seed, **kw)
+    res = rb.id(X.cuda(), tol=tau, k=k, b=cfg.b, seed=seed, **kw)
+    return Xnp, ores, res
+
+
+@cuda
+def test_c1_same_seed_end_to_end():
+    """c1 full size, seeds 0..9: same Philox protocol -> identical S on >= 8/10
+    seeds, rho_t within 1e-10, the (r, eps) bound met by both (R24)."""
+    cfg = CONFIGS["c1"]
+    X = make(cfg)
+    Xnp = X.numpy()
+    tail = R.tail(Xnp, cfg.r)
+    tau = (1 + cfg.eps) * R.eta(Xnp, cfg.r)
+    rb = _rb()
+    Xd = X.cuda()
+    same = 0
+    for seed in range(10):
+        ores = O.rbrp(Xnp, tau=tau, b=cfg.b, seed=seed)
+        res = rb.id(Xd, tol=tau, b=cfg.b, seed=seed)
+        assert res.resid_rel <= tau and ores.rho <= tau
+        assert abs(res.k - ores.k) <= cfg.b
+        eid = R.errid(Xnp, res.S.tolist(), res.W.cpu().numpy())
+        assert eid <= (1 + cfg.eps) * tail * (1 + 1e-9)
+        assert abs(eid - R.errskel(Xnp, res.S.tolist())) <= 1e-10 * res.fro2
+        if res.S.tolist() == ores.S:
+            same += 1
+            for a, b in zip(res.rho, [blk.rho for blk in ores.blocks]):
+                assert abs(a - b) <= 1e-10
+            assert res.b_prime == [blk.b_prime for blk in ores.blocks]
+            _check_W(Xnp, res, ores, np.float64)
+    assert same >= 8
+
+
+@cuda
+def test_c1_first_block_candidates_match_oracle():
+    """Philox + chunked CDF sampler: block 1's candidates equal the oracle's."""
+    cfg = CONFIGS["c1"]
+    X = make(cfg)
+    rb = _rb()
+    for seed in range(5):
+        ores = O.rbrp(X.numpy(), k=16, b=16, seed=seed)
+        res = rb.id(X.cuda(), k=16, b=16, seed=seed)
+        assert res.blocks[0] == ores.blocks[0].S_t
+
+
+def _replay(Xnp, ores, dtype, b, with_pivots=True):
+    rb = _rb()
+    blocks = [blk.S_t for blk in ores.blocks]
+    piv = [blk.piv for blk in ores.blocks] if with_pivots else None
+    X = torch.from_numpy(Xnp).cuda()
+    res = rb.id(X, k=ores.k, b=b, replay_blocks=blocks, replay_pivots=piv)
+    assert res.S.tolist() == ores.S
+    assert res.b_prime == [blk.b_prime for blk in ores.blocks]
+    for a, blk in zip(res.rho, ores.blocks):
+        assert abs(a - blk.rho) <= _tol(dtype)
+    _check_W(Xnp, res, ores, dtype)
+    return res
+
+
+@cuda
+@pytest.mark.parametrize("name,kw", [
+    ("c1", {}),
+    ("c2", dict(n=6000, d=260, rank=24, b=8)),
+    ("c3", dict(n=12000, d=64, n_heavy_dirs=20, n_heavy_rows=6000, b=16)),
+    ("c5", dict(n=9000, d=96, n_centres=24, b=16)),
+])
+def test_replay_parity_fp64(name, kw):
+    """Forced-pivot replay driven by the oracle's candidate blocks: S and b'
+    exact, rho_t within 1e-10, W within tolerance (north_star)."""
+    cfg = CONFIGS[name] if not kw else small_config(name, **kw)
+    Xnp = make(cfg).numpy()
+    if cfg.tau is not None:
+        tau = cfg.tau
+    else:
+        tau = (1 + cfg.eps) * R.eta(Xnp, min(cfg.r, Xnp.shape[1] // 2))
+    ores = O.rbrp(Xnp, tau=tau, b=cfg.b, seed=0)
+    _replay(Xnp, ores, np.float64, cfg.b)
+
+
+@cuda
+def test_replay_parity_fp32_c4_small():
+    cfg = small_config("c4", n=20000, d=192, b=16)
+    Xnp = make(cfg).numpy()
+    ores = O.rbrp(Xnp, tau=1e-3, b=16, seed=0)
+    _replay(Xnp, ores, np.float32, 16)
+
+
+@cuda
+def test_replay_without_forced_pivots_c1():
+    """Replay of candidate blocks only: the GPU's own pivoted Cholesky picks
+    the same pivots as the oracle's Householder CPQR (no near-ties in c1)."""
+    cfg = CONFIGS["c1"]
+    Xnp = make(cfg).numpy()
+    ores = O.rbrp(Xnp, k=60, b=16, seed=3)
+    assert min(blk.pivot_gap for blk in ores.blocks) > 1e-9
+    _replay(Xnp, ores, np.float64, 16, with_pivots=False)
+
+
+@cuda
+def test_exact_rank_stop_c2_small():
+    cfg = small_config("c2", n=8192 + 123, d=300, rank=40, b=16)
+    X = make(cfg)
+    res = _rb().id(X.cuda(), tol=1e-12, b=16, seed=1)
+    assert res.k == 40 and res.resid_rel <= 1e-12
+    assert R.errskel(X.numpy(), res.S.tolist()) / res.fro2 <= 1e-12
+
+
+@cuda
+def test_ragged_shapes_and_odd_d():
+    """n and d not multiples of any tile, d odd (scalar load path), b = 1."""
+    rng = np.random.default_rng(0)
+    rb = _rb()
+    for (n, d, b) in [(777, 33, 5), (4097, 17, 1), (130, 201, 16), (5000, 64, 32)]:
+        Xnp = rng.standard_normal((n, min(d, 12))) @ rng.standard_normal((min(d, 12), d))
+        Xnp += 1e-3 * rng.standard_normal((n, d))
+        ores = O.rbrp(Xnp, k=min(12, d), b=b, seed=2)
+        _replay(Xnp, ores, np.float64, b)
+
+
+@cuda
+def test_b1_matches_srp():
+    """b = 1: RBRP reduces to SRP (Alg. 1); same skeletons as the oracle's SRP."""
+    cfg = small_config("c1", n=600, d=80)
+    X = make(cfg)
+    S, L, _ = O.srp(X.numpy(), k=20, seed=4)
+    res = _rb().id(X.cuda(), k=20, b=1, seed=4)
+    assert res.S.tolist() == S
+
+
+@cuda
+def test_edge_cases():
+    rb = _rb()
+    dev = torch.device("cuda")
+    # NaN -> ENONFINITE; zero -> EDEGENERATE
+    X = torch.randn(300, 20, dtype=torch.float64, device=dev)
+    X[7, 3] = float("nan")
+    with pytest.raises(rb.RBRPError) as e:
+        rb.id(X, tol=0.1, b=8)
+    assert e.value.status == -2
+    with pytest.raises(rb.RBRPError) as e:
+        rb.id(torch.zeros(50, 10, dtype=torch.float64, device=dev), tol=0.1, b=8)
+    assert e.value.status == -3
+    # k_max cap before tau -> TOL_UNREACHED
+    X = torch.randn(500, 40, dtype=torch.float64, device=dev)
+    res = rb.id(X, tol=1e-6, k_max=10, b=4)
+    assert res.k == 10 and (res.flags & rb.rbrp.F_TOL_UNREACHED)
+    # support smaller than b: 3 nonzero rows
+    Z = torch.zeros(100, 10, dtype=torch.float64, device=dev)
+    Z[[5, 50, 90]] = torch.randn(3, 10, dtype=torch.float64, device=dev)
+    res = rb.id(Z, tol=1e-14, b=8)
+    assert sorted(res.S.tolist()) == [5, 50, 90]
+    assert res.flags & rb.rbrp.F_SUPPORT_EXHAUSTED
+    # exact duplicates never both selected
+    base = torch.randn(10, 30, dtype=torch.float64, device=dev)
+    D = base.repeat(40, 1)
+    res = rb.id(D, tol=1e-12, b=16)
+    assert res.k == 10 and len({s % 10 for s in res.S.tolist()}) == 10
+    # in-place mode gives the same answer
+    Y = torch.randn(3000, 50, dtype=torch.float64, device=dev) @ torch.randn(50, 50, dtype=torch.float64, device=dev)
+    a = rb.id(Y.clone(), k=30, b=16, seed=5)
+    bb = rb.id(Y.clone(), k=30, b=16, seed=5, inplace=True)
+    assert a.S.tolist() == bb.S.tolist()
+    assert torch.equal(a.W, bb.W)
+    # n < b
+    res = rb.id(torch.randn(5, 9, dtype=torch.float64, device=dev), tol=1e-12, b=16)
+    assert res.k == 5
+
+
+@cuda
+def test_full_c2_bench_config():
+    """c2 at BASELINE size (the bench workload): stops at |S| = 128 exactly,
+    rho <= 1e-12; trace = errskel by the referee; sampled W rows equal the
+    least-squares interpolation X X_S^+ (Eq. 5.1)."""
+    cfg = CONFIGS["c2"]
+    X = make(cfg, device="cuda")
+    res = _rb().id(X, tol=cfg.tau, b=cfg.b, seed=0)
+    assert res.k == 128 and res.resid_rel <= 1e-12
+    Xnp = X.cpu().numpy()
+    S = res.S.tolist()
+    assert abs(R.errskel(Xnp, S) / res.fro2 - res.resid_rel) <= 1e-13
+    rows = np.random.default_rng(0).choice(cfg.n, 64, replace=False)
+    Xs = Xnp[S]
+    Wls = np.linalg.lstsq(Xs.T, Xnp[rows].T, rcond=None)[0].T
+    W = res.W.cpu().numpy()
+    assert np.linalg.norm(W[rows] - Wls) <= 1e-9 * np.linalg.norm(Wls)
+    assert np.array_equal(W[S], np.eye(128))
