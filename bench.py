@@ -1,0 +1,324 @@
+#!/usr/bin/env python
+"""bench.py — RBRP time-to-ID on B200 (BASELINE.json metric), one JSON line.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+A step is one complete RBRP interpolative decomposition (Alg. 2 selection to
+the tolerance + Alg. 3 W) of the config's synthetic X, already resident in
+HBM.  At N = 1 the workload is BASELINE.json configs[1] (c2: fp64 65536 x 1024,
+exactly rank-128 + 1e-8 noise, b = 32, tau = 1e-12) — the metric's
+configuration; configs[0] (c1) is the oracle-sized parity case.  Timing: W
+warm-up steps, then K steps between barrier + synchronize, CUDA events on the
+stream the library launches on, max over ranks.  X (537 MB) and the residual
+are larger than the 126 MB L2, so no explicit flush is needed.
+
+Also reported: the roofline of the dominant projection pass (Alg. 2 l.13/l.16:
+k_lhat + k_update, timed live with CUDA events inside the library), the
+end-to-end figure through the C ABI with host buffers (pinned X -> HBM, W ->
+host inside the timed region), the kernel-launch count, the SM clocks seen by
+nvidia-smi during the timed region, and the CPU oracle timed on this host.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("RBRP time-to-(r,ε)-ID (s) and projection-pass HBM GB/s / roofline fraction, "
+          "1–8 GPU")
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # DFMA units x max clock
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+class Clocks:
+    """nvidia-smi sampler (SM clock + throttle reasons) around the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.t0 = self.t1 = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append((time.time(), line.strip()))
+
+    def stop(self):
+        if self.proc:
+            time.sleep(0.12)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        import statistics
+        sel = [r for (t, r) in self.rows if self.t0 - 0.06 <= t <= self.t1 + 0.06] or \
+              [r for (_, r) in self.rows]
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in sel:
+            f = [x.strip() for x in r.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _tau(cfg, X):
+    """tau for the config: given, or (1+eps) eta_r with eta_r from the Gram
+    eigenvalues (harness code, untimed; R3)."""
+    import torch
+    if cfg.tau is not None:
+        return cfg.tau
+    G = X.double().T @ X.double()
+    ev = torch.linalg.eigvalsh(G).flip(0).clamp_min(0)
+    return float((1 + cfg.eps) * ev[cfg.r:].sum() / ev.sum())
+
+
+def _proj_roofline(cfg, res_list, phase_ms):
+    """Algorithmic flops/bytes of the projection pass: per block
+    flops = 4 n d b' + 2 n d, bytes = 2 n d w + n b' w + 8 n."""
+    n, d = cfg.n, cfg.d
+    w = 8 if cfg.dtype == "f64" else 4
+    flops = bytes_ = 0.0
+    for res in res_list:
+        for bp in res.b_prime:
+            flops += 4.0 * n * d * bp + 2.0 * n * d
+            bytes_ += 2.0 * n * d * w + n * bp * w + 8.0 * n
+    t = phase_ms / 1e3
+    return flops / t / 1e12, bytes_ / t / 1e9
+
+
+def _traffic_from_profile():
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p)).get("proj_dram_bytes_per_block")
+        except Exception:
+            return None
+    return None
+
+
+def _cpu_baseline(cfg, Xnp, tau):
+    from oracle import rbrp as O
+    try:
+        from threadpoolctl import threadpool_info
+        thr = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+    except Exception:
+        thr = os.cpu_count()
+    t = time.perf_counter()
+    ores = O.rbrp(Xnp, tau=tau, b=cfg.b, seed=0)
+    ores_W = O.form_W(ores.L, ores.S, method="trsm")
+    dt = time.perf_counter() - t
+    return {"value": dt, "unit": "s", "cores": int(thr), "kind": "oracle",
+            "sample": f"one full {cfg.name} ID ({cfg.n}x{cfg.d} {cfg.dtype}, b={cfg.b}, "
+                      f"k={ores.k}) incl. W, NumPy/BLAS on {len(os.sched_getaffinity(0))} host cores"}
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+    from oracle import rbrp as O
+    from workloads import CONFIGS, make
+    cfg = CONFIGS[a.config]
+    X = make(cfg)
+    Xnp = X.numpy()
+    import torch
+    tau = _tau(cfg, X)
+    for _ in range(a.warmup):
+        O.rbrp(Xnp, tau=tau, b=cfg.b, seed=a.seed)
+    times = []
+    for _ in range(a.steps):
+        t = time.perf_counter()
+        r = O.rbrp(Xnp, tau=tau, b=cfg.b, seed=a.seed)
+        O.form_W(r.L, r.S, method="trsm")
+        times.append(time.perf_counter() - t)
+    v = float(np.mean(times))
+    try:
+        from threadpoolctl import threadpool_info
+        thr = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+    except Exception:
+        thr = os.cpu_count()
+    line = {"metric": METRIC, "value": v, "unit": "s", "n_gpus": a.gpus, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64" if cfg.dtype == "f64" else "f32",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"{cfg.name}: {cfg.dtype} n={cfg.n} d={cfg.d} b={cfg.b} tau={tau:.3g}",
+                       "n": cfg.n, "d": cfg.d, "b": cfg.b, "k": r.k},
+            "cpu_baseline": {"value": v, "unit": "s", "cores": int(thr), "kind": "oracle",
+                             "sample": f"full {cfg.name} ID per step (oracle as it stands)"},
+            "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    a = _args()
+    if a.impl == "reference":
+        return run_reference(a)
+    import torch
+    import torch.distributed as dist
+
+    import paper_2309_16002_b200 as rb
+    from workloads import CONFIGS, make
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    cfg = CONFIGS[a.config]
+    # N > 1: the row-sharded NCCL path is not built yet; each rank runs a full replica
+    X = make(cfg, device=dev)
+    tau = _tau(cfg, X)
+    ws = torch.empty(rb.workspace_size(X, tol=tau, b=cfg.b), dtype=torch.uint8, device=dev)
+    for _ in range(a.warmup):
+        rb.id(X, tol=tau, b=cfg.b, seed=a.seed, workspace=ws, log_blocks=False)
+    torch.cuda.synchronize()
+
+    clk = Clocks(local)
+    clk.start()
+    time.sleep(0.3)
+    res_list = []
+    stream = torch.cuda.current_stream(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    clk.t0 = time.time()
+    e0.record(stream)
+    for _ in range(a.steps):
+        res_list.append(rb.id(X, tol=tau, b=cfg.b, seed=a.seed, workspace=ws, log_blocks=False,
+                              profile=True))
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk.t1 = time.time()
+    clk.stop()
+    ms = e0.elapsed_time(e1) / a.steps
+    t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+
+    ph = {k: sum(r.ms_phase[k] for r in res_list) for k in res_list[0].ms_phase}
+    proj_ms = ph["lhat"] + ph["update"]
+    tflops, gbs = _proj_roofline(cfg, res_list, proj_ms)
+    launches = sum(r.launches for r in res_list)
+    r0 = res_list[-1]
+
+    e2e = None
+    if not a.no_e2e:
+        Xh = X.cpu().pin_memory()
+        w = 8 if cfg.dtype == "f64" else 4
+        rb.id_host(Xh, device=dev, tol=tau, b=cfg.b, seed=a.seed, workspace=ws, log_blocks=False)
+        torch.cuda.synchronize()
+        barrier()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        ks = 0
+        for _ in range(a.steps):
+            rr, _W = rb.id_host(Xh, device=dev, tol=tau, b=cfg.b, seed=a.seed, workspace=ws,
+                                log_blocks=False)
+            ks = rr.k
+        f1.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([f0.elapsed_time(f1) / a.steps], device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": float(te.item()) / 1e3, "unit": "s",
+               "h2d_bytes_per_step": cfg.n * cfg.d * w,
+               "d2h_bytes_per_step": cfg.n * ks * w + ks * 8}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    cpu = None
+    if world == 1 and not a.no_cpu_baseline:
+        cpu = _cpu_baseline(cfg, X.cpu().numpy(), tau)
+    peak = FP64_PEAK_TFLOPS if cfg.dtype == "f64" else FP64_PEAK_TFLOPS * 2
+    traffic = _traffic_from_profile()
+    line = {
+        "metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: {cfg.dtype} n={cfg.n} d={cfg.d} exactly rank-128 + 1e-8 "
+                               f"noise, b={cfg.b}, tau={tau:.3g}" if cfg.name == "c2" else
+                               f"{cfg.name}: {cfg.dtype} n={cfg.n} d={cfg.d} b={cfg.b} tau={tau:.3g}",
+                   "n": cfg.n, "d": cfg.d, "b": cfg.b, "tau": tau, "k": r0.k, "blocks": r0.nblocks,
+                   "b_prime": r0.b_prime, "resid_rel": r0.resid_rel,
+                   "parallelism": "single" if world == 1 else f"replicas{world}",
+                   "l2": "inputs larger than L2 (X 537 MB + residual 537 MB vs 126 MB L2); no flush"},
+        "roofline": {"kernel": "projection pass a4 (k_lhat + k_update, Alg. 2 l.13/l.16)",
+                     "bound": "alu", "achieved": tflops, "peak": peak, "unit": "TFLOP/s",
+                     "frac": tflops / peak, "traffic": traffic,
+                     "peak_note": "FP64 DFMA: 148 SM x 64 FMA/clk x 2 x 1.965 GHz (derived, DESIGN.md §6); "
+                                  "MEASURED_PEAKS.json has no FP64 entry",
+                     "algorithmic_GBs": gbs, "hbm_frac_of_measured": gbs / 6551.4,
+                     "share_of_step": proj_ms / a.steps / ms},
+        "phase_ms_per_step": {k: v / a.steps for k, v in ph.items()},
+        "gpu_launches": launches,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -130,6 +130,13 @@ typedef struct {
  *              ids, draw order) of each logged block, -1 padded.
  *   block_piv  (optional, length max_blocks * b): the local pivot order pi_V.
  *   ms_total   device time of the whole call in ms (CUDA events on `stream`).
+ *   profile    (in) non-zero: record CUDA events around every phase on `stream` and fill
+ *              ms_phase (summed over blocks): [0] init norms + chunk scan, [1] sampler +
+ *              stop test, [2] gather + local pivoted QR + filter (a3), [3] projection
+ *              L-hat = X_res Q_b, [4] fused update X_res -= L-hat Q_b^T + norms, [5] skeleton
+ *              fix-up + chunk scan, [6] W (Alg. 3), [7] collectives.
+ *   launches   (out) number of kernels this call launched.
+ *   proj_calls (out) number of projection passes that did work (one per block).
  */
 typedef struct {
   int64_t k;
@@ -144,6 +151,10 @@ typedef struct {
   int64_t* block_idx;
   int32_t* block_piv;
   float ms_total;
+  int32_t profile;
+  float ms_phase[8];
+  int32_t launches;
+  int32_t proj_calls;
 } rbrp_report;
 
 /* Opaque NCCL communicator wrapper; NULL means a single-GPU call. */

@@ -1,0 +1,376 @@
+// k_filter_coop.cu — a3 in ONE cooperative kernel: gather + local pivoted QR + robust
+// filter + CholQR2 basis (Alg. 2 l.6-9; Remark 4.1).
+//
+// Grid = ceil(d / 32) CTAs; CTA c owns columns [32c, 32c+32) of V = X_res(S_t,:)^T and of
+// every basis built from it, kept in shared memory for the whole kernel.
+//   A  gather V(:, cols) (fp64) and its partial Gram                    -> Gpart[c]
+//   B  G = sum_c Gpart[c] in a fixed order (element slices)              -> G
+//   C  every CTA (redundantly, bit-identical, so nothing is broadcast): right-looking
+//      pivoted Cholesky of G with logical pivoting.  The Schur diagonal is the
+//      Householder CPQR residual column norm^2 (reading R10), so mass[i] =
+//      ||R_V(i:b,i:b)||_F^2 and b' = max{i : mass[i] >= tau_b mass[0]} (l.8);
+//      pivot = max, ties -> lowest draw position (R9).  Then T11 = R11^{-1}.
+//   D  Q1(:, cols) = V(:, pi(1:b')) T11 (parallel dot products); partial Gram of Q1
+//   E  G2 = sum_c Gpart[c]
+//   F  every CTA: Cholesky G2 = R2^T R2 (CholQR2) with T2 = R2^{-1}; CTA 0: R_total = R2 R11
+//   G  Q_b(:, cols) = Q1 T2 -> Qt (rows >= b' zero up to bp_pad)
+// Four grid-wide barriers.
+#include <cooperative_groups.h>
+#include <float.h>
+
+#include "launch.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace rbrp {
+
+constexpr int kFiltThreads = 256;
+constexpr int kFiltCW = 32;         // columns per CTA
+constexpr int kFiltLd = kFiltCW + 1;
+constexpr int kSmallNb = 64;        // nb <= 64: G, R, T, R11 all in shared memory
+
+// Right-looking pivoted (mode 1) or plain (mode 2) Cholesky of the symmetric nb x nb
+// matrix A (shared memory, stride lda, destroyed), all threads of the CTA, logical
+// pivoting (no row/column swaps):
+//   step i: p = argmax of the unchosen Schur diagonal dg (ties -> lowest original index,
+//   reading R9; mode 2: p = i; replay: forced[i]); R(i, l) = A(p, l) / sqrt(dg(p)) for
+//   the unchosen l; A(r, c) -= R(i, r) R(i, c) on the unchosen block.
+// dg is the Householder CPQR residual column norm^2 (reading R10), so in mode 1
+// mass[i] = sum of the unchosen dg before step i = ||R_V(i:b,i:b)||_F^2 and the loop
+// stops at the first i with mass[i] < tau_b mass[0] (l.8; the masses are
+// non-increasing), or at a non-positive pivot (numerical rank).  R: row = step, column =
+// original index (ldr).  Returns the number of kept steps.
+__device__ int cta_pivchol(double* A, int lda, int nb, int mode, const int32_t* forced, double tau_b,
+                           double* R, int ldr, int* perm, double* mass, double* dg, int* chosen,
+                           int* rank_def) {
+  __shared__ int s_p, s_cut;
+  __shared__ double s_thr;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  for (int l = tid; l < nb; l += blockDim.x) {
+    dg[l] = A[l * lda + l];
+    chosen[l] = 0;
+  }
+  if (tid == 0) *rank_def = 0;
+  __syncthreads();
+  int kept = nb;
+  for (int i = 0; i < nb; ++i) {
+    if (w == 0) {
+      double ms = 0.0, best = -DBL_MAX;
+      int bl = 1 << 30;
+      for (int l = lane; l < nb; l += 32) {
+        if (chosen[l]) continue;
+        const double x = dg[l];
+        ms += fmax(x, 0.0);
+        if (x > best) { best = x; bl = l; }
+      }
+      ms = warp_sum(ms);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+        if (ob > best || (ob == best && ol < bl)) { best = ob; bl = ol; }
+      }
+      if (lane == 0) {
+        int cut = 0;
+        if (mode == 1) {
+          mass[i] = ms;
+          if (i == 0) s_thr = tau_b * ms;
+          if (!(ms > 0.0) || ms < s_thr) cut = 1;                  // l.8 cut
+        }
+        int p = bl;
+        if (mode == 2) p = i;
+        if (mode == 1 && forced) p = forced[i];
+        if (!cut && !(dg[p] > 0.0)) cut = 2;                      // non-positive pivot
+        s_p = p;
+        s_cut = cut;
+        if (!cut) perm[i] = p;
+      }
+    }
+    __syncthreads();
+    if (s_cut) {
+      if (tid == 0 && s_cut == 2) *rank_def = 1;
+      kept = i;
+      break;
+    }
+    const int p = s_p;
+    const double rii = sqrt(dg[p]);
+    for (int l = tid; l < nb; l += blockDim.x) {
+      double v;
+      if (l == p) v = rii;
+      else if (chosen[l]) v = 0.0;
+      else v = A[p * lda + l] / rii;
+      R[i * ldr + l] = v;
+    }
+    __syncthreads();
+    if (tid == 0) chosen[p] = 1;
+    for (int e = tid; e < nb * nb; e += blockDim.x) {
+      const int r = e / nb, c = e % nb;
+      if (r == p || c == p) continue;
+      const double rr = R[i * ldr + r], rc = R[i * ldr + c];
+      if (rr == 0.0 && rc == 0.0) continue;   // chosen rows/columns carry zeros
+      const double a = fma(-rr, rc, A[r * lda + c]);
+      A[r * lda + c] = a;
+      if (r == c) dg[r] = a;
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  return kept;
+}
+
+// T = R11^{-1} for the upper-triangular R11(j, c) = R(j, perm[c]) (step order), one
+// thread per column c: T(c,c) = 1/R11(c,c); T(j,c) = -(sum_{j<q<=c} R11(j,q) T(q,c)) / R11(j,j).
+__device__ void cta_trinv(const double* R, int ldr, const int* perm, int bp, double* Tm, int ldt) {
+  for (int c = threadIdx.x; c < bp; c += blockDim.x) {
+    const int pc = perm[c];
+    Tm[c * ldt + c] = 1.0 / R[c * ldr + pc];
+    for (int j = c - 1; j >= 0; --j) {
+      double t0 = 0.0, t1 = 0.0;
+      int q = j + 1;
+      for (; q + 1 <= c; q += 2) {
+        t0 = fma(R[j * ldr + perm[q]], Tm[q * ldt + c], t0);
+        t1 = fma(R[j * ldr + perm[q + 1]], Tm[(q + 1) * ldt + c], t1);
+      }
+      if (q <= c) t0 = fma(R[j * ldr + perm[q]], Tm[q * ldt + c], t0);
+      Tm[j * ldt + c] = -(t0 + t1) / R[j * ldr + perm[j]];
+    }
+    for (int j = c + 1; j < bp; ++j) Tm[j * ldt + c] = 0.0;
+  }
+  __syncthreads();
+}
+
+// partial Gram of the nb x 32 slice S (stride kFiltLd) -> out (kMaxB x kMaxB)
+__device__ void slice_gram(const double* S, int nb, double* out) {
+  for (int p = threadIdx.x; p < nb * nb; p += blockDim.x) {
+    const int i = p / nb, j = p % nb;
+    if (i > j) continue;
+    double s = 0.0;
+#pragma unroll 8
+    for (int c = 0; c < kFiltCW; ++c) s += S[i * kFiltLd + c] * S[j * kFiltLd + c];
+    out[i * kMaxB + j] = s;
+    out[j * kMaxB + i] = s;
+  }
+}
+
+__device__ void reduce_slices(const double* Gpart, int nsplit, int nb, double* G) {
+  const int64_t per = (int64_t)nb * nb;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < per;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / nb), j = (int)(e % nb);
+    const double* src = Gpart + i * kMaxB + j;
+    double s = 0.0;
+    int q = 0;
+    for (; q + 8 <= nsplit; q += 8) {   // 8 independent loads in flight, summed in order
+      double x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) x[u] = src[(int64_t)(q + u) * kMaxB * kMaxB];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s += x[u];
+    }
+    for (; q < nsplit; ++q) s += src[(int64_t)q * kMaxB * kMaxB];
+    G[i * kMaxB + j] = s;
+  }
+}
+
+// Out(i, c) = sum_{j <= i} T(j, i) In(src(j), c), i < rows (parallel dot products)
+__device__ void apply_T(const double* Tm, int ldt, int rows, const double* In, const int* src,
+                        double* Out) {
+  for (int e = threadIdx.x; e < rows * kFiltCW; e += blockDim.x) {
+    const int i = e / kFiltCW, c = e % kFiltCW;
+    double s0 = 0.0, s1 = 0.0;
+    int j = 0;
+    for (; j + 1 <= i; j += 2) {
+      s0 = fma(Tm[j * ldt + i], In[(src ? src[j] : j) * kFiltLd + c], s0);
+      s1 = fma(Tm[(j + 1) * ldt + i], In[(src ? src[j + 1] : j + 1) * kFiltLd + c], s1);
+    }
+    if (j <= i) s0 = fma(Tm[j * ldt + i], In[(src ? src[j] : j) * kFiltLd + c], s0);
+    Out[i * kFiltLd + c] = s0 + s1;
+  }
+}
+
+__device__ __forceinline__ void stamp(long long* dbg, int k) {
+  if (dbg && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    dbg[k] = (long long)t;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kFiltThreads) k_filter_coop(FilterArgs F) {
+  cg::grid_group grid = cg::this_grid();
+  stamp(F.dbg, 0);
+  extern __shared__ double smd[];
+  __shared__ int perm[kMaxB], perm2[kMaxB], s_ch[kMaxB];
+  __shared__ double s_mass[kMaxB], s_dg[kMaxB];
+  __shared__ int s_nb, s_stop, s_kept, s_rd;
+  __shared__ long long s_k;
+  DevState* st = F.st;
+  const int tid = threadIdx.x, w = tid >> 5;
+  if (tid == 0) {
+    s_stop = st->stop;
+    s_nb = st->b_t;
+    s_k = st->k;
+  }
+  __syncthreads();
+  if (s_stop || s_nb <= 0) return;   // uniform over the grid
+  const int nb = s_nb;
+  const bool small = nb <= kSmallNb;
+  double* Vs = smd;                          // [kMaxB][33]
+  double* Q1s = Vs + kMaxB * kFiltLd;        // [kMaxB][33]
+  double* Rs = Q1s + kMaxB * kFiltLd;        // R: [nb][ldr]
+  const int ldr = small ? kSmallNb + 1 : kMaxB + 1;
+  // small: G, T, R11 copies in shared memory too; large: global scratch (L2)
+  double* Gs = small ? Rs + kSmallNb * ldr : F.G;
+  const int ldg = small ? ldr : kMaxB;
+  double* Ts = small ? Gs + kSmallNb * ldr : F.Tg;
+  const int ldt = small ? ldr : kMaxB;
+  double* R11s = small ? Ts + kSmallNb * ldr : F.R11;
+  const int ld11 = small ? ldr : kMaxB;
+  const int64_t c0 = (int64_t)blockIdx.x * kFiltCW;
+  const int64_t d = F.d;
+  const int nsplit = gridDim.x;
+  double* Gp = F.Gpart + (int64_t)blockIdx.x * kMaxB * kMaxB;
+
+  // A: gather + partial Gram
+  for (int e = tid; e < nb * kFiltCW; e += kFiltThreads) {
+    const int i = e / kFiltCW, c = e % kFiltCW;
+    double v = 0.0;
+    if (c0 + c < d) {
+      if (F.Vg) {
+        v = F.Vg[(int64_t)i * d + c0 + c];
+      } else {
+        const int64_t r = F.S_t[i] - F.row_offset;
+        v = (double)((const T*)F.X)[r * F.ldx + c0 + c];
+      }
+    }
+    Vs[i * kFiltLd + c] = v;
+  }
+  __syncthreads();
+  slice_gram(Vs, nb, Gp);
+  stamp(F.dbg, 1);
+  grid.sync();
+  stamp(F.dbg, 2);
+  // B
+  reduce_slices(F.Gpart, nsplit, nb, F.G);
+  grid.sync();
+  stamp(F.dbg, 3);
+  // C: pivoted Cholesky + filter (redundant in every CTA; the large case works on G in
+  // L2 and keeps T in a per-CTA global scratch)
+  if (!small) {
+    Ts = F.Tg + (int64_t)blockIdx.x * kMaxB * kMaxB;
+    Gs = F.Ag + (int64_t)blockIdx.x * kMaxB * kMaxB;
+  }
+  for (int e = tid; e < nb * nb; e += kFiltThreads) Gs[(e / nb) * ldg + e % nb] = F.G[(e / nb) * kMaxB + e % nb];
+  __syncthreads();
+  {
+    const double tb = st->tau_b < 0.0 ? 1.0 / nb : st->tau_b;
+    const int kept = cta_pivchol(Gs, ldg, nb, 1, F.forced, tb, Rs, ldr, perm, s_mass, s_dg, s_ch, &s_rd);
+    if (tid == 0) s_kept = kept;
+  }
+  __syncthreads();
+  const int bp = s_kept;
+  cta_trinv(Rs, ldr, perm, bp, Ts, ldt);
+  stamp(F.dbg, 4);
+  // R11 (step order) and the bookkeeping of l.8-9
+  for (int e = tid; e < bp * bp; e += kFiltThreads) {
+    const int i = e / bp, j = e % bp;
+    const double v = (i <= j) ? Rs[i * ldr + perm[j]] : 0.0;
+    if (small) R11s[i * ld11 + j] = v;
+    else if (blockIdx.x == 0) F.R11[i * kMaxB + j] = v;
+  }
+  if (blockIdx.x == 0) {
+    for (int i = tid; i < bp; i += kFiltThreads) {
+      F.piv[i] = perm[i];
+      F.S[s_k + i] = F.S_t[perm[i]];                                  // l.9
+    }
+    for (int i = tid; i < kMaxB; i += kFiltThreads) F.mass[i] = (i < nb && i <= bp) ? s_mass[i] : 0.0;
+    if (tid == 0) {
+      st->b_prime = bp;
+      if (s_rd) st->rank_def = 1;
+      if (bp == 0) {
+        st->flags |= RBRP_F_ZERO_BLOCK;
+        st->stop = 1;
+      }
+    }
+  }
+  if (bp == 0) return;   // uniform
+  __syncthreads();
+  // D: Q1(:, cols) = V(:, pi(1:b')) T11, partial Gram of Q1
+  apply_T(Ts, ldt, bp, Vs, perm, Q1s);
+  __syncthreads();
+  slice_gram(Q1s, bp, Gp);
+  stamp(F.dbg, 5);
+  grid.sync();
+  stamp(F.dbg, 6);
+  // E
+  reduce_slices(F.Gpart, nsplit, bp, F.G);
+  grid.sync();
+  stamp(F.dbg, 7);
+  // F: CholQR2 pass (R2 into Rs, T2 into Ts)
+  for (int e = tid; e < bp * bp; e += kFiltThreads) Gs[(e / bp) * ldg + e % bp] = F.G[(e / bp) * kMaxB + e % bp];
+  __syncthreads();
+  {
+    int rd2;
+    const int kept = cta_pivchol(Gs, ldg, bp, 2, nullptr, 0.0, Rs, ldr, perm2, nullptr, s_dg, s_ch, &rd2);
+    if (tid == 0) s_kept = kept;
+  }
+  __syncthreads();
+  cta_trinv(Rs, ldr, perm2, s_kept, Ts, ldt);
+  const int bq = s_kept;   // normally bp; smaller only if G2 lost definiteness
+  stamp(F.dbg, 8);
+  if (blockIdx.x == 0) {
+    for (int e = tid; e < bq * bq; e += kFiltThreads) {
+      const int i = e / bq, j = e % bq;
+      double s = 0.0;
+      if (i <= j)
+        for (int m = i; m <= j; ++m) s = fma(Rs[i * ldr + m], R11s[m * ld11 + j], s);
+      F.Rtot[i * kMaxB + j] = (i <= j) ? s : 0.0;                      // R_total = R2 R11
+    }
+    if (tid == 0 && bq < bp) {
+      st->b_prime = bq;
+      st->rank_def = 1;
+      if (bq == 0) st->stop = 1;
+    }
+  }
+  if (bq == 0) return;
+  // G: Q_b(:, cols) = Q1 T2 -> Vs (free now) -> Qt
+  apply_T(Ts, ldt, bq, Q1s, nullptr, Vs);
+  __syncthreads();
+  T* Qt = (T*)F.Qt;
+  const int rows = bq > F.bp_pad ? bq : F.bp_pad;
+  for (int e = tid; e < rows * kFiltCW; e += kFiltThreads) {
+    const int i = e / kFiltCW, c = e % kFiltCW;
+    if (c0 + c >= d) continue;
+    Qt[(int64_t)i * d + c0 + c] = (T)(i < bq ? Vs[i * kFiltLd + c] : 0.0);
+  }
+  stamp(F.dbg, 9);
+}
+
+static size_t filter_smem() {
+  const size_t small = 2 * kMaxB * kFiltLd + 4 * kSmallNb * (kSmallNb + 1);
+  const size_t large = 2 * kMaxB * kFiltLd + kMaxB * (kMaxB + 1);
+  return sizeof(double) * (small > large ? small : large);
+}
+
+template <typename T>
+cudaError_t launch_filter_coop(const FilterArgs& a, cudaStream_t s) {
+  const int nsplit = ceil_div(a.d, kFiltCW);
+  const size_t smem = filter_smem();
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_filter_coop<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  FilterArgs A = a;
+  void* args[] = {&A};
+  return cudaLaunchCooperativeKernel((void*)k_filter_coop<T>, dim3(nsplit), dim3(kFiltThreads), args,
+                                     smem, s);
+}
+
+int filter_coop_nsplit(int64_t d) { return ceil_div(d, kFiltCW); }
+
+template cudaError_t launch_filter_coop<double>(const FilterArgs&, cudaStream_t);
+template cudaError_t launch_filter_coop<float>(const FilterArgs&, cudaStream_t);
+
+}  // namespace rbrp

@@ -1,0 +1,323 @@
+// k_project_mma.cu — a4 projection on the FP64 tensor path (DMMA, mma.sync.m8n8k4.f64).
+//
+// B200 has no FP64 kind for tcgen05 (ptxas rejects kind::f64); the legacy DMMA path
+// reaches the full FP64 rate (measured 37.2 TFLOP/s vs 33.8 for DFMA, profiles/).
+//
+//   k_nt_mma<BN>     C[m, n0+j] = sum_k A[m,k] B[n0+j,k]   (row-major A, B; K contiguous)
+//                    = L-hat = X_res Q_b^T (Alg. 2 l.13) and W = L L_1^{-1} (Alg. 3).
+//   k_update_mma<BP> X_res -= L-hat Q_b and d(i) = ||x_res,i||^2 (l.16), fused:
+//                    each residual row is read once and written once per block.
+//
+// Fragment layouts (PTX ISA, mma.m8n8k4 .f64): lane = 4 g + q;  A(8x4): A[g][q];
+// B(4x8): B[q][g];  C/D(8x8): C[g][2q + i], i = 0, 1.
+// In k_nt_mma an A-row segment x[2q, 2q+1] (one 16-byte load) feeds two MMAs whose K
+// index is permuted as k = 2q + h; the B fragments are read with the same permutation
+// (one 16-byte shared load gives both), so no shuffles are needed.
+#include <algorithm>
+
+#include "launch.cuh"
+
+namespace rbrp {
+
+__device__ __forceinline__ void dmma(double2& d, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d.x), "+d"(d.y)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const int n = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+constexpr int kMmaWarps = 8;
+constexpr int kMmaRows = 8 * kMmaWarps;   // rows per CTA (8 per warp)
+constexpr int kKC = 64;                   // K (columns) per staged chunk
+constexpr int kXld = kKC + 8;             // X tile stride (doubles), = 8 mod 16: LDS.128 conflict-free
+constexpr int kBld = kKC + 8;             // B tile stride for 16-byte B loads (k_nt_mma)
+constexpr int kQld = kKC + 4;             // Q tile stride for 8-byte B loads (k_update_mma), = 4 mod 16
+
+template <int BN> struct NtCfg {
+  static constexpr int NS = BN <= 64 ? 3 : 2;                            // pipeline stages
+  static constexpr int STAGE = kMmaRows * kXld + BN * kBld;              // doubles per stage
+  static constexpr size_t SMEM = sizeof(double) * NS * STAGE;
+};
+template <int BP> struct UpdCfg {
+  static constexpr int NS = BP <= 64 ? 3 : 2;
+  static constexpr int STAGE = kMmaRows * kXld + BP * kQld;
+  static constexpr size_t SMEM = sizeof(double) * NS * STAGE;
+};
+
+// X tile rows [r0, r0+64) x columns [c0, c0+64) -> xs (zero-filled outside [0,M) x [0,K))
+__device__ __forceinline__ void stage_x(double* xs, const double* __restrict__ A, int64_t lda,
+                                        int64_t r0, int64_t M, int64_t c0, int64_t K, int tid) {
+#pragma unroll
+  for (int i = 0; i < (kMmaRows * kKC / 2) / (32 * kMmaWarps); ++i) {
+    const int e = tid + i * 32 * kMmaWarps;
+    const int r = e / (kKC / 2), c = (e % (kKC / 2)) * 2;
+    const bool ok = (r0 + r < M) && (c0 + c < K);
+    cp_async16(xs + r * kXld + c, ok ? A + (r0 + r) * lda + c0 + c : A, ok);
+  }
+}
+// rows [0, BN) of B (rows >= nrows zero) x columns [c0, c0+64)
+template <int BN, int LD>
+__device__ __forceinline__ void stage_b(double* bs, const double* __restrict__ B, int64_t ldb,
+                                        int64_t n0, int64_t nrows, int64_t c0, int64_t K, int tid) {
+  for (int e = tid; e < BN * (kKC / 2); e += 32 * kMmaWarps) {
+    const int j = e / (kKC / 2), c = (e % (kKC / 2)) * 2;
+    const bool ok = (n0 + j < nrows) && (c0 + c < K);
+    cp_async16(bs + j * LD + c, ok ? B + (n0 + j) * ldb + c0 + c : B, ok);
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// C = A B^T: 64-row tiles x BN columns; persistent CTAs (one per SM) walk their tiles
+// and the 64-column K chunks of each tile as ONE flattened sequence, so the NS-stage
+// cp.async pipeline never drains between tiles.  Requirements (checked by the
+// launcher): K % 8 == 0, lda % 2 == 0, ldb % 2 == 0, 16-byte aligned A and B.
+// ---------------------------------------------------------------------------------
+template <int BN>
+__global__ void __launch_bounds__(32 * kMmaWarps, 1) k_nt_mma(const double* __restrict__ A, int64_t lda,
+                                                              const double* __restrict__ B, int64_t ldb,
+                                                              double* __restrict__ C, int64_t ldc,
+                                                              int64_t M, int64_t N, int64_t K,
+                                                              const DevState* st, int mode) {
+  using Cf = NtCfg<BN>;
+  extern __shared__ __align__(16) double sm[];
+  int64_t col0 = 0, Nn = N;
+  if (mode == 1) {   // L-hat: N = b', columns written at L[:, k + j]
+    if (st->stop) return;
+    const int bp = st->b_prime;
+    if (bp <= 0 || bucket_of(bp) != BN) return;
+    Nn = bp;
+    col0 = st->k;
+  }
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  const int64_t ntm = (M + kMmaRows - 1) / kMmaRows;
+  const int64_t ntn = (Nn + BN - 1) / BN;
+  const int64_t ntiles = ntm * ntn;
+  const int nchunk = (int)((K + kKC - 1) / kKC);
+  const int64_t nmine = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t total = nmine * nchunk;
+  auto tile_of = [&](int64_t j, int64_t& r0, int64_t& n0) {
+    const int64_t t = blockIdx.x + j * gridDim.x;
+    r0 = (t % ntm) * kMmaRows;
+    n0 = (t / ntm) * BN;
+  };
+  auto issue = [&](int64_t it) {
+    if (it < total) {
+      int64_t r0, n0;
+      tile_of(it / nchunk, r0, n0);
+      const int64_t k0 = (it % nchunk) * kKC;
+      double* base = sm + (size_t)(it % Cf::NS) * Cf::STAGE;
+      stage_x(base, A, lda, r0, M, k0, K, tid);
+      stage_b<BN, kBld>(base + kMmaRows * kXld, B, ldb, n0, Nn, k0, K, tid);
+    }
+    cp_async_commit();
+  };
+  double2 acc[BN / 8];
+#pragma unroll
+  for (int t = 0; t < BN / 8; ++t) acc[t] = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int i = 0; i < Cf::NS - 1; ++i) issue(i);
+  for (int64_t it = 0; it < total; ++it) {
+    issue(it + Cf::NS - 1);
+    cp_async_wait<Cf::NS - 1>();
+    __syncthreads();
+    const double* xs = sm + (size_t)(it % Cf::NS) * Cf::STAGE;
+    const double* bs = xs + kMmaRows * kXld;
+#pragma unroll
+    for (int s = 0; s < kKC / 8; ++s) {
+      const double2 xa = *reinterpret_cast<const double2*>(xs + (w * 8 + g) * kXld + 8 * s + 2 * q);
+#pragma unroll
+      for (int t = 0; t < BN / 8; ++t) {
+        const double2 b = *reinterpret_cast<const double2*>(bs + (t * 8 + g) * kBld + 8 * s + 2 * q);
+        dmma(acc[t], xa.x, b.x);
+        dmma(acc[t], xa.y, b.y);
+      }
+    }
+    if (it % nchunk == nchunk - 1) {   // tile done: write, reset
+      int64_t r0, n0;
+      tile_of(it / nchunk, r0, n0);
+      const int64_t row = r0 + w * 8 + g;
+      if (row < M) {
+        double* crow = C + row * ldc + col0;
+#pragma unroll
+        for (int t = 0; t < BN / 8; ++t) {
+          const int64_t j = n0 + t * 8 + 2 * q;
+          if (j < Nn) crow[j] = acc[t].x;
+          if (j + 1 < Nn) crow[j + 1] = acc[t].y;
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < BN / 8; ++t) acc[t] = make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// X(rows, :) -= P(rows, :b') Q_b ; d(rows) = ||x||^2.  P = L[:, k : k+b'].
+// Persistent CTAs, flattened (tile, chunk) cp.async pipeline; the next tile's P rows
+// (the A fragments) are fetched into registers one chunk before the tile switch.
+// Requirements: d % 8 == 0, ldx % 2 == 0, 16-byte aligned X and Qt.
+// ---------------------------------------------------------------------------------
+template <int BP>
+__global__ void __launch_bounds__(32 * kMmaWarps, 1) k_update_mma(double* __restrict__ X, int64_t ldx,
+                                                                  const double* __restrict__ Qt,
+                                                                  const double* __restrict__ L,
+                                                                  int64_t ldl, int64_t n, int64_t d,
+                                                                  double* __restrict__ dvec,
+                                                                  const DevState* st) {
+  using Cf = UpdCfg<BP>;
+  extern __shared__ __align__(16) double sm[];
+  if (st->stop) return;
+  const int bp = st->b_prime;
+  if (bp <= 0 || bucket_of(bp) != BP) return;
+  const int64_t k0 = st->k;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  const int64_t ntiles = (n + kMmaRows - 1) / kMmaRows;
+  const int nchunk = (int)((d + kKC - 1) / kKC);
+  const int64_t nmine = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t total = nmine * nchunk;
+  auto r0_of = [&](int64_t j) { return (blockIdx.x + j * gridDim.x) * (int64_t)kMmaRows; };
+  auto issue = [&](int64_t it) {
+    if (it < total) {
+      double* base = sm + (size_t)(it % Cf::NS) * Cf::STAGE;
+      const int64_t c0 = (it % nchunk) * kKC;
+      stage_x(base, X, ldx, r0_of(it / nchunk), n, c0, d, tid);
+      stage_b<BP, kQld>(base + kMmaRows * kXld, Qt, d, 0, bp, c0, d, tid);
+    }
+    cp_async_commit();
+  };
+  // A fragments: -P[row][4 jc + q]
+  double a[BP / 4], an[BP / 4];
+  auto load_a = [&](double (&dst)[BP / 4], int64_t j) {
+    const int64_t row = r0_of(j) + w * 8 + g;
+    const bool rok = row < n;
+    const double* lrow = L + (rok ? row : 0) * ldl + k0;
+#pragma unroll
+    for (int jc = 0; jc < BP / 4; ++jc) {
+      const int jj = jc * 4 + q;
+      dst[jc] = (rok && jj < bp) ? -lrow[jj] : 0.0;
+    }
+  };
+#pragma unroll
+  for (int i = 0; i < Cf::NS - 1; ++i) issue(i);
+  if (total > 0) load_a(a, 0);
+  double nrm = 0.0;
+  for (int64_t it = 0; it < total; ++it) {
+    const int64_t j = it / nchunk;
+    const int ch = (int)(it % nchunk);
+    issue(it + Cf::NS - 1);
+    if (ch == nchunk - 1 && j + 1 < nmine) load_a(an, j + 1);
+    cp_async_wait<Cf::NS - 1>();
+    __syncthreads();
+    const double* xs = sm + (size_t)(it % Cf::NS) * Cf::STAGE;
+    const double* qb = xs + kMmaRows * kXld;
+    const int64_t row = r0_of(j) + w * 8 + g;
+    const bool rok = row < n;
+    double* xrow = X + (rok ? row : 0) * ldx;
+    const int64_t c0 = (int64_t)ch * kKC;
+    double2 xd[kKC / 8];
+#pragma unroll
+    for (int s = 0; s < kKC / 8; ++s)
+      xd[s] = *reinterpret_cast<const double2*>(xs + (w * 8 + g) * kXld + 8 * s + 2 * q);
+#pragma unroll
+    for (int jc = 0; jc < BP / 4; ++jc) {
+#pragma unroll
+      for (int s = 0; s < kKC / 8; ++s) dmma(xd[s], a[jc], qb[(jc * 4 + q) * kQld + 8 * s + g]);
+    }
+#pragma unroll
+    for (int s = 0; s < kKC / 8; ++s) {
+      const int64_t c = c0 + 8 * s + 2 * q;
+      if (rok && c < d) {
+        __stcs(reinterpret_cast<double2*>(xrow + c), xd[s]);
+        nrm += xd[s].x * xd[s].x + xd[s].y * xd[s].y;
+      }
+    }
+    if (ch == nchunk - 1) {
+      nrm += __shfl_xor_sync(0xffffffffu, nrm, 1);
+      nrm += __shfl_xor_sync(0xffffffffu, nrm, 2);
+      if (rok && q == 0) dvec[row] = nrm;
+      nrm = 0.0;
+#pragma unroll
+      for (int jc = 0; jc < BP / 4; ++jc) a[jc] = an[jc];
+    }
+    __syncthreads();
+  }
+}
+
+static int g_num_sms = 0;
+static int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+static bool mma_ok(const void* p, int64_t ld, int64_t K) {
+  return (K % 8 == 0) && (ld % 2 == 0) && ((uintptr_t)p % 16 == 0);
+}
+
+bool projection_mma_supported(const void* X, int64_t ldx, const void* Qt, int64_t d) {
+  return mma_ok(X, ldx, d) && ((uintptr_t)Qt % 16 == 0);
+}
+
+cudaError_t launch_lhat_mma(const double* Xres, int64_t ldx, const double* Qt, int64_t n, int64_t d,
+                            double* L, int64_t ldl, const DevState* st, int bucket, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  dim3 grid((unsigned)std::min<int64_t>(num_sms(), ceil_div(n, kMmaRows)), 1);
+  auto go = [&](auto kern, size_t smem) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<grid, 32 * kMmaWarps, smem, s>>>(Xres, ldx, Qt, d, L, ldl, n, 0, d, st, 1);
+  };
+  switch (bucket) {
+    case 16: go(k_nt_mma<16>, NtCfg<16>::SMEM); break;
+    case 32: go(k_nt_mma<32>, NtCfg<32>::SMEM); break;
+    case 64: go(k_nt_mma<64>, NtCfg<64>::SMEM); break;
+    default: go(k_nt_mma<128>, NtCfg<128>::SMEM); break;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_update_mma(double* Xres, int64_t ldx, const double* Qt, const double* L,
+                              int64_t ldl, int64_t n, int64_t d, double* dvec, const DevState* st,
+                              int bucket, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const int g = (int)std::min<int64_t>(num_sms(), ceil_div(n, kMmaRows));
+  auto go = [&](auto kern, size_t smem) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<g, 32 * kMmaWarps, smem, s>>>(Xres, ldx, Qt, L, ldl, n, d, dvec, st);
+  };
+  switch (bucket) {
+    case 16: go(k_update_mma<16>, UpdCfg<16>::SMEM); break;
+    case 32: go(k_update_mma<32>, UpdCfg<32>::SMEM); break;
+    case 64: go(k_update_mma<64>, UpdCfg<64>::SMEM); break;
+    default: go(k_update_mma<128>, UpdCfg<128>::SMEM); break;
+  }
+  return cudaGetLastError();
+}
+
+// W = A B^T with N = k columns (B = L_1^{-T}), DMMA path when shapes allow
+bool gemm_nt_mma(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
+                 int64_t M, int64_t N, int64_t K, cudaStream_t s, cudaError_t* err) {
+  if (!mma_ok(A, lda, K) || !mma_ok(B, ldb, K)) return false;
+  dim3 grid((unsigned)std::min<int64_t>(num_sms(), (int64_t)ceil_div(M, kMmaRows) * ceil_div(N, 128)), 1);
+  const size_t smem = NtCfg<128>::SMEM;
+  cudaFuncSetAttribute(k_nt_mma<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_nt_mma<128><<<grid, 32 * kMmaWarps, smem, s>>>(A, lda, B, ldb, C, ldc, M, N, K, nullptr, 0);
+  *err = cudaGetLastError();
+  return true;
+}
+
+}  // namespace rbrp

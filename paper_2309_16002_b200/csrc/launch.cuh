@@ -33,28 +33,31 @@ template <typename T>
 cudaError_t launch_gather_rows(const T* X, int64_t ldx, const int64_t* rows, int64_t n_local,
                                int64_t row_offset, const DevState* st, int64_t d, double* Vg,
                                cudaStream_t s);
-template <typename TS>
-cudaError_t launch_gram(const TS* src, int64_t ld, const int64_t* rows, int64_t row_offset,
-                        const DevState* st, int use_bprime, int64_t d, double* Vout, double* Gpart,
-                        int nsplit, int cw, cudaStream_t s);
-cudaError_t launch_gram_reduce(const double* Gpart, int nsplit, double* G, cudaStream_t s);
-struct FactorArgs {
+// k_filter_coop.cu — the whole a3 step in one cooperative kernel
+struct FilterArgs {
   DevState* st;
-  const double* G;          // kMaxB x kMaxB (ld kMaxB)
-  int mode;                 // 1: pivoted Cholesky + filter (l.7-8); 2: Cholesky (CholQR2 pass)
-  const int32_t* forced;    // device, forced pivots for this block or null
-  int32_t* piv;             // out (mode 1)
-  double* mass;             // out (mode 1)
-  double* Tinv;             // out: inverse of the triangular factor (upper, ld kMaxB)
-  double* R11;              // mode 1 out / mode 2 in: first-pass R (upper, ld kMaxB)
-  double* Rtot;             // mode 2 out: R2 * R11
-  const int64_t* S_t;       // candidates
-  int64_t* S;               // skeleton list (mode 1 appends S'_t at [k, k+b'))
+  const void* X;            // X_res (dtype T), used when Vg == nullptr
+  int64_t ldx;
+  const double* Vg;         // pre-gathered V rows (multi-GPU, after allreduce) or null
+  const int64_t* S_t;       // candidates (global ids)
+  int64_t row_offset, d;
+  double* Gpart;            // nsplit x kMaxB x kMaxB
+  double* G;                // kMaxB x kMaxB
+  const int32_t* forced;    // forced pivots (device) or null
+  int32_t* piv;             // out: pi_V
+  double* mass;             // out: ||R_V(i:b,i:b)||_F^2
+  double* R11;              // out: first-pass R (upper, ld kMaxB)
+  double* Tg;               // scratch: nsplit x kMaxB x kMaxB (b_t > 64 only)
+  double* Ag;               // scratch: nsplit x kMaxB x kMaxB (b_t > 64 only)
+  double* Rtot;             // out: R2 R11
+  int64_t* S;               // skeleton list: S'_t appended at [k, k+b')
+  void* Qt;                 // out: Q_b rows (dtype T), ld d; rows [b', bp_pad) zero
+  int bp_pad;
+  long long* dbg;           // optional: %globaltimer stamps of the phases (CTA 0)
 };
-cudaError_t launch_factor(const FactorArgs& a, cudaStream_t s);
-template <typename TO>
-cudaError_t launch_apply_tinv(const double* Tinv, const double* Vsrc, const int32_t* perm,
-                              const DevState* st, int64_t d, TO* Qout, int bp_pad, cudaStream_t s);
+template <typename T>
+cudaError_t launch_filter_coop(const FilterArgs& a, cudaStream_t s);
+int filter_coop_nsplit(int64_t d);
 
 // k_project.cu — Alg. 2 l.13, l.16 in residual form
 template <typename T>
@@ -67,6 +70,16 @@ template <typename T>
 cudaError_t launch_fixup(T* Xres, int64_t ldx, double* dvec, T* L, int64_t ldl, const double* Rtot,
                          const int64_t* S, int64_t n_local, int64_t row_offset, int64_t d,
                          DevState* st, cudaStream_t s);
+
+// k_project_mma.cu — DMMA (FP64 tensor) projection
+bool projection_mma_supported(const void* X, int64_t ldx, const void* Qt, int64_t d);
+cudaError_t launch_lhat_mma(const double* Xres, int64_t ldx, const double* Qt, int64_t n, int64_t d,
+                            double* L, int64_t ldl, const DevState* st, int bucket, cudaStream_t s);
+cudaError_t launch_update_mma(double* Xres, int64_t ldx, const double* Qt, const double* L,
+                              int64_t ldl, int64_t n, int64_t d, double* dvec, const DevState* st,
+                              int bucket, cudaStream_t s);
+bool gemm_nt_mma(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
+                 int64_t M, int64_t N, int64_t K, cudaStream_t s, cudaError_t* err);
 
 // k_formw.cu — Alg. 3 by triangular solve
 template <typename T>

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -28,7 +29,7 @@ namespace {
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
-  size_t Xres = SIZE_MAX, dvec, cpre, ctot, cpos, cprefix, L, Qt, Vg, Q1, Gpart, G, Tinv, R11, Rtot,
+  size_t Xres = SIZE_MAX, dvec, cpre, ctot, cpos, cprefix, L, Qt, Vg, Gpart, G, Tg, Ag, R11, Rtot,
          piv, mass, St, S, forced, cand, st, L1 = SIZE_MAX, LinvT = SIZE_MAX, total;
   int nsplit, cw;
   int64_t nchunks, k_cap;
@@ -79,10 +80,10 @@ Layout make_layout(const rbrp_problem* p) {
   L.L = take((size_t)n * L.k_cap * w);
   L.Qt = take(B * d * w);
   L.Vg = take(B * d * 8);
-  L.Q1 = take(B * d * 8);
   L.Gpart = take((size_t)L.nsplit * B * B * 8);
   L.G = take(B * B * 8);
-  L.Tinv = take(B * B * 8);
+  L.Tg = take((size_t)L.nsplit * B * B * 8);
+  L.Ag = take((size_t)L.nsplit * B * B * 8);
   L.R11 = take(B * B * 8);
   L.Rtot = take(B * B * 8);
   L.piv = take(B * 4);
@@ -120,6 +121,48 @@ struct Pinned {
 };
 thread_local Pinned g_pinned;
 
+// RBRP_FORCE_SIMT=1 selects the CUDA-core (DFMA/FFMA) projection kernels instead of DMMA
+bool dbg_stamps() {
+  const char* e = getenv("RBRP_DEBUG_STAMPS");
+  return e && e[0] == '1';
+}
+bool force_simt() {
+  const char* e = getenv("RBRP_FORCE_SIMT");
+  return e && e[0] == '1';
+}
+
+// per-phase CUDA events on the caller's stream (report.profile)
+struct Prof {
+  bool on = false;
+  cudaStream_t s = nullptr;
+  std::vector<int> phase;
+  std::vector<cudaEvent_t> ev;   // pairs (start, end)
+  int open_phase = -1;
+  void begin(int ph) {
+    if (!on) return;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, s);
+    ev.push_back(a);
+    ev.push_back(b);
+    phase.push_back(ph);
+  }
+  void end() {
+    if (!on) return;
+    cudaEventRecord(ev.back(), s);
+  }
+  void collect(float* out) {
+    for (size_t i = 0; i < phase.size(); ++i) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, ev[2 * i], ev[2 * i + 1]) == cudaSuccess) out[phase[i]] += ms;
+    }
+  }
+  ~Prof() {
+    for (auto e : ev) cudaEventDestroy(e);
+  }
+};
+
 template <typename T>
 int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* comm,
         cudaStream_t s, int64_t* S_out, void* W_out, rbrp_report* rep) {
@@ -136,10 +179,10 @@ int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* 
   T* Lm = (T*)(ws + Ly.L);
   T* Qt = (T*)(ws + Ly.Qt);
   double* Vg = (double*)(ws + Ly.Vg);
-  double* Q1 = (double*)(ws + Ly.Q1);
   double* Gpart = (double*)(ws + Ly.Gpart);
   double* G = (double*)(ws + Ly.G);
-  double* Tinv = (double*)(ws + Ly.Tinv);
+  double* Tg = (double*)(ws + Ly.Tg);
+  double* Ag = (double*)(ws + Ly.Ag);
   double* R11 = (double*)(ws + Ly.R11);
   double* Rtot = (double*)(ws + Ly.Rtot);
   int32_t* piv = (int32_t*)(ws + Ly.piv);
@@ -169,6 +212,15 @@ int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* 
   *hA = h0;
   CK(cudaMemcpyAsync(st, hA, sizeof(DevState), cudaMemcpyHostToDevice, s));
 
+  Prof prof;
+  prof.on = rep && rep->profile;
+  prof.s = s;
+  int nl = 0, nproj = 0;
+#define LK(x) \
+  do {        \
+    ++nl;     \
+    CK(x);    \
+  } while (0)
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
@@ -176,8 +228,10 @@ int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* 
 
   const int64_t chunk0 = p->row_offset / RBRP_CHUNK;
   // a0: d^(0), X_res <- X (Alg. 2 l.1-2)
-  CK(launch_init_norms<T>(X, p->ld, Xres, n, d, dvec, st, !inplace, s));
-  CK(launch_chunk_scan(dvec, n, chunk0, cpre, ctot, cpos, s));
+  prof.begin(0);
+  LK(launch_init_norms<T>(X, p->ld, Xres, n, d, dvec, st, !inplace, s));
+  LK(launch_chunk_scan(dvec, n, chunk0, cpre, ctot, cpos, s));
+  prof.end();
   if (comm) {
     int rc = comm_allgather_chunks(comm, ctot, cpos, chunk0, (n + RBRP_CHUNK - 1) / RBRP_CHUNK, Ly.nchunks, s);
     if (rc) return rc;
@@ -223,7 +277,9 @@ int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* 
   int rl = stage_replay(0);
   if (rl < -100) return rl + 1000;
   sa.replay_len = rl;
-  CK(launch_sample(sa, s));
+  prof.begin(1);
+  LK(launch_sample(sa, s));
+  prof.end();
   CK(cudaMemcpyAsync(hB, st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   if (hB->nonfinite) return RBRP_ENONFINITE;
@@ -231,44 +287,64 @@ int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* 
 
   const int bucketB = bucket_of((int)std::min<int64_t>(p->b, k_cap));
   const bool use_forced = p->replay_pivots != nullptr;
+  const bool use_mma = sizeof(T) == 8 && !force_simt() && projection_mma_supported(Xres, ldr, Qt, d);
   int nblocks = 0;
   while (!hB->stop) {
     // a3: gather V = X_res(S_t,:)^T, Gram, pivoted Cholesky + filter (l.6-9)
-    CK(launch_gather_rows<T>(Xres, ldr, St, n, p->row_offset, st, d, Vg, s));
+    prof.begin(2);
+    FilterArgs fa;
+    fa.st = st;
+    fa.X = Xres;
+    fa.ldx = ldr;
+    fa.Vg = nullptr;
     if (comm) {
+      LK(launch_gather_rows<T>(Xres, ldr, St, n, p->row_offset, st, d, Vg, s));
       int rc = comm_allreduce_f64(comm, Vg, (int64_t)RBRP_MAX_B * d, s);
       if (rc) return rc;
+      fa.Vg = Vg;
     }
-    CK(launch_gram<double>(Vg, d, nullptr, 0, st, 0, d, nullptr, Gpart, Ly.nsplit, Ly.cw, s));
-    CK(launch_gram_reduce(Gpart, Ly.nsplit, G, s));
-    FactorArgs fa;
-    fa.st = st;
+    fa.S_t = St;
+    fa.row_offset = p->row_offset;
+    fa.d = d;
+    fa.Gpart = Gpart;
     fa.G = G;
-    fa.mode = 1;
     fa.forced = use_forced ? forced : nullptr;
     fa.piv = piv;
     fa.mass = mass;
-    fa.Tinv = Tinv;
     fa.R11 = R11;
+    fa.Tg = Tg;
+    fa.Ag = Ag;
     fa.Rtot = Rtot;
-    fa.S_t = St;
     fa.S = S;
-    CK(launch_factor(fa, s));
-    CK(launch_apply_tinv<double>(Tinv, Vg, piv, st, d, Q1, 0, s));
-    // CholQR2 re-orthonormalisation
-    CK(launch_gram<double>(Q1, d, nullptr, 0, st, 1, d, nullptr, Gpart, Ly.nsplit, Ly.cw, s));
-    CK(launch_gram_reduce(Gpart, Ly.nsplit, G, s));
-    fa.mode = 2;
-    fa.forced = nullptr;
-    CK(launch_factor(fa, s));
-    CK(launch_apply_tinv<T>(Tinv, Q1, nullptr, st, d, Qt, bucketB, s));
+    fa.Qt = Qt;
+    fa.bp_pad = bucketB;
+    fa.dbg = dbg_stamps() ? (long long*)(ws + Ly.cand) : nullptr;
+    LK(launch_filter_coop<T>(fa, s));
+    prof.end();
     // a4: projection + fused norms (l.13, l.16)
+    prof.begin(3);
     for (int bk = 16; bk <= bucketB; bk *= 2) {
-      CK(launch_lhat<T>(Xres, ldr, Qt, n, d, Lm, k_cap, st, bk, s));
-      CK(launch_update<T>(Xres, ldr, Qt, Lm, k_cap, n, d, dvec, st, bk, s));
+      if (use_mma)
+        LK(launch_lhat_mma((const double*)Xres, ldr, (const double*)Qt, n, d, (double*)Lm, k_cap,
+                           st, bk, s));
+      else
+        LK(launch_lhat<T>(Xres, ldr, Qt, n, d, Lm, k_cap, st, bk, s));
     }
-    CK(launch_fixup<T>(Xres, ldr, dvec, Lm, k_cap, Rtot, S, n, p->row_offset, d, st, s));
-    CK(launch_chunk_scan(dvec, n, chunk0, cpre, ctot, cpos, s));
+    prof.end();
+    prof.begin(4);
+    for (int bk = 16; bk <= bucketB; bk *= 2) {
+      if (use_mma)
+        LK(launch_update_mma((double*)Xres, ldr, (const double*)Qt, (const double*)Lm, k_cap, n, d,
+                             dvec, st, bk, s));
+      else
+        LK(launch_update<T>(Xres, ldr, Qt, Lm, k_cap, n, d, dvec, st, bk, s));
+    }
+    prof.end();
+    ++nproj;
+    prof.begin(5);
+    LK(launch_fixup<T>(Xres, ldr, dvec, Lm, k_cap, Rtot, S, n, p->row_offset, d, st, s));
+    LK(launch_chunk_scan(dvec, n, chunk0, cpre, ctot, cpos, s));
+    prof.end();
     if (comm) {
       int rc = comm_allgather_chunks(comm, ctot, cpos, chunk0, (n + RBRP_CHUNK - 1) / RBRP_CHUNK, Ly.nchunks, s);
       if (rc) return rc;
@@ -291,9 +367,19 @@ int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* 
     if (rl < -100) return rl + 1000;
     sa.replay_len = rl;
     sa.first = 0;
-    CK(launch_sample(sa, s));
+    prof.begin(1);
+    LK(launch_sample(sa, s));
+    prof.end();
     CK(cudaMemcpyAsync(hB, st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    if (dbg_stamps()) {   // diagnostics: phase stamps of this block's filter call (ns)
+      long long t[11];
+      if (cudaMemcpy(t, ws + Ly.cand, sizeof(t), cudaMemcpyDeviceToHost) == cudaSuccess) {
+        fprintf(stderr, "rbrp filter b_t=%d b'=%d phases (us):", hA->b_t, hA->b_prime);
+        for (int i = 1; i < 11; ++i) fprintf(stderr, " %.2f", (t[i] - t[0]) * 1e-3);
+        fprintf(stderr, "\n");
+      }
+    }
     if (logit) {
       if (rep->b_t) rep->b_t[nblocks] = hA->b_t;
       if (rep->b_prime) rep->b_prime[nblocks] = hA->b_prime;
@@ -307,14 +393,24 @@ int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* 
   if (!(p->flags & RBRP_NO_W) && W_out && k > 0) {
     double* L1 = (double*)(ws + Ly.L1);
     T* LinvT = (T*)(ws + Ly.LinvT);
-    CK(launch_gather_L1<T>(Lm, k_cap, S, k, n, p->row_offset, L1, s));
+    prof.begin(6);
+    LK(launch_gather_L1<T>(Lm, k_cap, S, k, n, p->row_offset, L1, s));
     if (comm) {
       int rc = comm_allreduce_f64(comm, L1, k * k, s);
       if (rc) return rc;
     }
-    CK(launch_trinv<T>(L1, k, LinvT, st, s));
-    CK(launch_gemm_nt<T>(Lm, k_cap, LinvT, k, (T*)W_out, k_cap, n, k, k, s));
-    CK(launch_w_identity<T>((T*)W_out, k_cap, S, k, n, p->row_offset, s));
+    LK(launch_trinv<T>(L1, k, LinvT, st, s));
+    cudaError_t merr = cudaSuccess;
+    if (sizeof(T) == 8 && !force_simt() &&
+        gemm_nt_mma((const double*)Lm, k_cap, (const double*)LinvT, k, (double*)W_out, k_cap, n, k,
+                    k, s, &merr)) {
+      ++nl;
+      CK(merr);
+    } else {
+      LK(launch_gemm_nt<T>(Lm, k_cap, LinvT, k, (T*)W_out, k_cap, n, k, k, s));
+    }
+    LK(launch_w_identity<T>((T*)W_out, k_cap, S, k, n, p->row_offset, s));
+    prof.end();
   }
   CK(cudaMemcpyAsync(hS, S, (size_t)std::max<int64_t>(k, 1) * 8, cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(hB, st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
@@ -332,7 +428,12 @@ int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* 
     rep->nblocks = nblocks;
     rep->flags = hB->flags;
     rep->ms_total = ms;
+    for (int i = 0; i < 8; ++i) rep->ms_phase[i] = 0.f;
+    prof.collect(rep->ms_phase);
+    rep->launches = nl;
+    rep->proj_calls = nproj;
   }
+#undef LK
   return RBRP_OK;
 }
 
@@ -374,6 +475,7 @@ int rbrp_id(const rbrp_problem* p, void* X, void* workspace, size_t ws_bytes, rb
   if (p->greedy) return RBRP_ENOTSUP;
   if (comm && (p->row_offset % RBRP_CHUNK) != 0) return RBRP_EINVAL;
   if (comm) return RBRP_ENOTSUP;   // distributed sampler: not yet built
+  if (filter_coop_nsplit(p->d) > 148) return RBRP_ENOTSUP;   // d > 4736: one CTA per 32 columns
   Layout Ly = make_layout(p);
   if (ws_bytes < Ly.total) return RBRP_ENOMEM;
   if ((uintptr_t)workspace % 256) return RBRP_EINVAL;

@@ -48,7 +48,11 @@ class Report(ctypes.Structure):
                 ("max_blocks", ctypes.c_int32), ("b_t", ctypes.POINTER(ctypes.c_int32)),
                 ("b_prime", ctypes.POINTER(ctypes.c_int32)), ("rho", ctypes.POINTER(ctypes.c_double)),
                 ("block_idx", ctypes.POINTER(ctypes.c_int64)),
-                ("block_piv", ctypes.POINTER(ctypes.c_int32)), ("ms_total", ctypes.c_float)]
+                ("block_piv", ctypes.POINTER(ctypes.c_int32)), ("ms_total", ctypes.c_float),
+                ("profile", ctypes.c_int32), ("ms_phase", ctypes.c_float * 8),
+                ("launches", ctypes.c_int32), ("proj_calls", ctypes.c_int32)]
+
+PHASES = ["init", "sample", "filter", "lhat", "update", "fixup_scan", "W", "comm"]
 
 
 class RBRPError(RuntimeError):
@@ -99,6 +103,9 @@ class Result:
     blocks: List[List[int]]         # candidate blocks S_t (global ids, draw order)
     pivots: List[List[int]]         # local pivot orders
     ms: float                       # device time of the call (CUDA events), ms
+    ms_phase: dict                  # per-phase device ms (profile=True)
+    launches: int                   # kernels launched by the call
+    proj_calls: int
 
 
 def _problem(X: torch.Tensor, tol, k, b, seed, k_max, tau_b, flags, n_global, row_offset, greedy):
@@ -145,7 +152,8 @@ def id(X: torch.Tensor, tol: Optional[float] = None, k: Optional[int] = None, b:
        replay_blocks: Optional[Sequence[Sequence[int]]] = None,
        replay_pivots: Optional[Sequence[Sequence[int]]] = None,
        max_blocks: int = 1024, log_blocks: bool = True, workspace: Optional[torch.Tensor] = None,
-       comm=None, n_global: Optional[int] = None, row_offset: int = 0) -> Result:
+       comm=None, n_global: Optional[int] = None, row_offset: int = 0,
+       profile: bool = False) -> Result:
     """RBRP interpolative decomposition X ~ W X_S of a CUDA tensor X (n x d).
 
     tol: tau, relative to ||X||_F^2 (for an (r, eps)-ID pass tol = (1+eps) eta_r,
@@ -189,6 +197,7 @@ def id(X: torch.Tensor, tol: Optional[float] = None, k: Optional[int] = None, b:
     b_pr = (ctypes.c_int32 * mb)()
     rho = (ctypes.c_double * mb)()
     rep.max_blocks = mb
+    rep.profile = 1 if profile else 0
     rep.b_t = ctypes.cast(b_t, ctypes.POINTER(ctypes.c_int32))
     rep.b_prime = ctypes.cast(b_pr, ctypes.POINTER(ctypes.c_int32))
     rep.rho = ctypes.cast(rho, ctypes.POINTER(ctypes.c_double))
@@ -216,7 +225,9 @@ def id(X: torch.Tensor, tol: Optional[float] = None, k: Optional[int] = None, b:
     return Result(S=S[:kk].clone(), W=W[:, :kk] if W is not None else None, k=kk,
                   resid_rel=rep.resid_rel, fro2=rep.fro2, flags=rep.flags, nblocks=rep.nblocks,
                   b_t=list(b_t[:nb]), b_prime=list(b_pr[:nb]), rho=list(rho[:nb]),
-                  blocks=blocks, pivots=pivots, ms=rep.ms_total)
+                  blocks=blocks, pivots=pivots, ms=rep.ms_total,
+                  ms_phase={nm: rep.ms_phase[i] for i, nm in enumerate(PHASES)},
+                  launches=rep.launches, proj_calls=rep.proj_calls)
 
 
 def id_host(X_host: torch.Tensor, device="cuda", **kw):

@@ -106,6 +106,9 @@ def _replay(Xnp, ores, dtype, b, with_pivots=True):
     ("c2", dict(n=6000, d=260, rank=24, b=8)),
     ("c3", dict(n=12000, d=64, n_heavy_dirs=20, n_heavy_rows=6000, b=16)),
     ("c5", dict(n=9000, d=96, n_centres=24, b=16)),
+    ("c5", dict(n=12000, d=160, n_centres=120, b=64)),
+    ("c5", dict(n=12000, d=200, n_centres=150, b=96)),
+    ("c3", dict(n=20000, d=256, n_heavy_dirs=90, n_heavy_rows=9000, b=128)),
 ])
 def test_replay_parity_fp64(name, kw):
     """Forced-pivot replay driven by the oracle's candidate blocks: S and b'
@@ -227,3 +230,17 @@ def test_full_c2_bench_config():
     W = res.W.cpu().numpy()
     assert np.linalg.norm(W[rows] - Wls) <= 1e-9 * np.linalg.norm(Wls)
     assert np.array_equal(W[S], np.eye(128))
+
+
+@cuda
+def test_simt_and_mma_projection_paths_agree(monkeypatch):
+    """The CUDA-core (DFMA) and FP64-tensor (DMMA) projection kernels both
+    match the oracle in replay mode."""
+    cfg = small_config("c2", n=9000, d=256, rank=30, b=16)
+    Xnp = make(cfg).numpy()
+    ores = O.rbrp(Xnp, tau=1e-12, b=16, seed=0)
+    monkeypatch.setenv("RBRP_FORCE_SIMT", "1")
+    a = _replay(Xnp, ores, np.float64, 16)
+    monkeypatch.setenv("RBRP_FORCE_SIMT", "0")
+    b = _replay(Xnp, ores, np.float64, 16)
+    assert a.S.tolist() == b.S.tolist()
