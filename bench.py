@@ -223,8 +223,9 @@ def main():
     X = make(cfg, device=dev)
     tau = _tau(cfg, X)
     ws = torch.empty(rb.workspace_size(X, tol=tau, b=cfg.b), dtype=torch.uint8, device=dev)
+    Wbuf = torch.empty((cfg.n, min(cfg.n, cfg.d)), dtype=cfg.torch_dtype, device=dev)
     for _ in range(a.warmup):
-        rb.id(X, tol=tau, b=cfg.b, seed=a.seed, workspace=ws, log_blocks=False)
+        rb.id(X, tol=tau, b=cfg.b, seed=a.seed, workspace=ws, log_blocks=False, W_out=Wbuf)
     torch.cuda.synchronize()
 
     clk = Clocks(local)
@@ -239,8 +240,9 @@ def main():
     clk.t0 = time.time()
     e0.record(stream)
     for _ in range(a.steps):
-        res_list.append(rb.id(X, tol=tau, b=cfg.b, seed=a.seed, workspace=ws, log_blocks=False,
-                              profile=True))
+        r = rb.id(X, tol=tau, b=cfg.b, seed=a.seed, workspace=ws, log_blocks=False, W_out=Wbuf)
+        r.W = None
+        res_list.append(r)
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -252,11 +254,153 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
 
-    ph = {k: sum(r.ms_phase[k] for r in res_list) for k in res_list[0].ms_phase}
-    proj_ms = ph["lhat"] + ph["update"]
+    # projection-pass device time measured inside the timed region (in-kernel
+    # %globaltimer stamps, first CTA start of L-hat -> last CTA end of the update)
+    proj_ms = sum(r.proj_ms for r in res_list)
     tflops, gbs = _proj_roofline(cfg, res_list, proj_ms)
     launches = sum(r.launches for r in res_list)
     r0 = res_list[-1]
+    # per-phase breakdown from one eager, event-instrumented run (outside the timed region)
+    rp = rb.id(X, tol=tau, b=cfg.b, seed=a.seed, workspace=ws, log_blocks=False, profile=True,
+               W_out=Wbuf)
+    torch.cuda.synchronize()
+    ph = rp.ms_phase
+    ph_proj_eager = ph["lhat"] + ph["update"]
+
+    e2e = None
+    if not a.no_e2e:
+        # end to end through the public API with HOST buffers: every step copies X
+        # (pinned host -> HBM) and reads W (n x k) back to pinned host memory
+        Xh = X.cpu().pin_memory()
+        Xd = torch.empty_like(X)
+        Wh = torch.empty((cfg.n, min(cfg.n, cfg.d)), dtype=cfg.torch_dtype, pin_memory=True)
+        w = 8 if cfg.dtype == "f64" else 4
+        kw = dict(tol=tau, b=cfg.b, seed=a.seed, workspace=ws, log_blocks=False, W_out=Wbuf)
+        rb.id_host(Xh, X_dev=Xd, W_host=Wh, **kw)
+        torch.cuda.synchronize()
+        barrier()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        ks = 0
+        for _ in range(a.steps):
+            rr, _W = rb.id_host(Xh, X_dev=Xd, W_host=Wh, **kw)
+            ks = rr.k
+        f1.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([f0.elapsed_time(f1) / a.steps], device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": float(te.item()) / 1e3, "unit": "s",
+               "h2d_bytes_per_step": cfg.n * cfg.d * w,
+               "d2h_bytes_per_step": cfg.n * ks * w + ks * 8}
+
+    if rank != 0:
+        return
+    import numpy as np
+    from oracle import rbrp as O
+    from workloads import CONFIGS, make
+    cfg = CONFIGS[a.config]
+    X = make(cfg)
+    Xnp = X.numpy()
+    import torch
+    tau = _tau(cfg, X)
+    for _ in range(a.warmup):
+        O.rbrp(Xnp, tau=tau, b=cfg.b, seed=a.seed)
+    times = []
+    for _ in range(a.steps):
+        t = time.perf_counter()
+        r = O.rbrp(Xnp, tau=tau, b=cfg.b, seed=a.seed)
+        O.form_W(r.L, r.S, method="trsm")
+        times.append(time.perf_counter() - t)
+    v = float(np.mean(times))
+    try:
+        from threadpoolctl import threadpool_info
+        thr = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+    except Exception:
+        thr = os.cpu_count()
+    line = {"metric": METRIC, "value": v, "unit": "s", "n_gpus": a.gpus, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64" if cfg.dtype == "f64" else "f32",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"{cfg.name}: {cfg.dtype} n={cfg.n} d={cfg.d} b={cfg.b} tau={tau:.3g}",
+                       "n": cfg.n, "d": cfg.d, "b": cfg.b, "k": r.k},
+            "cpu_baseline": {"value": v, "unit": "s", "cores": int(thr), "kind": "oracle",
+                             "sample": f"full {cfg.name} ID per step (oracle as it stands)"},
+            "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    a = _args()
+    if a.impl == "reference":
+        return run_reference(a)
+    import torch
+    import torch.distributed as dist
+
+    import paper_2309_16002_b200 as rb
+    from workloads import CONFIGS, make
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    cfg = CONFIGS[a.config]
+    # N > 1: the row-sharded NCCL path is not built yet; each rank runs a full replica
+    X = make(cfg, device=dev)
+    tau = _tau(cfg, X)
+    ws = torch.empty(rb.workspace_size(X, tol=tau, b=cfg.b), dtype=torch.uint8, device=dev)
+    Wbuf = torch.empty((cfg.n, min(cfg.n, cfg.d)), dtype=cfg.torch_dtype, device=dev)
+    for _ in range(a.warmup):
+        rb.id(X, tol=tau, b=cfg.b, seed=a.seed, workspace=ws, log_blocks=False, W_out=Wbuf)
+    torch.cuda.synchronize()
+
+    clk = Clocks(local)
+    clk.start()
+    time.sleep(0.3)
+    res_list = []
+    stream = torch.cuda.current_stream(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    clk.t0 = time.time()
+    e0.record(stream)
+    for _ in range(a.steps):
+        r = rb.id(X, tol=tau, b=cfg.b, seed=a.seed, workspace=ws, log_blocks=False, W_out=Wbuf)
+        r.W = None
+        res_list.append(r)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk.t1 = time.time()
+    clk.stop()
+    ms = e0.elapsed_time(e1) / a.steps
+    t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+
+    # projection-pass device time measured inside the timed region (in-kernel
+    # %globaltimer stamps, first CTA start of L-hat -> last CTA end of the update)
+    proj_ms = sum(r.proj_ms for r in res_list)
+    tflops, gbs = _proj_roofline(cfg, res_list, proj_ms)
+    launches = sum(r.launches for r in res_list)
+    r0 = res_list[-1]
+    # per-phase breakdown from one eager, event-instrumented run (outside the timed region)
+    rp = rb.id(X, tol=tau, b=cfg.b, seed=a.seed, workspace=ws, log_blocks=False, profile=True,
+               W_out=Wbuf)
+    torch.cuda.synchronize()
+    ph = rp.ms_phase
+    ph_proj_eager = ph["lhat"] + ph["update"]
 
     e2e = None
     if not a.no_e2e:
@@ -302,14 +446,17 @@ def main():
                    "b_prime": r0.b_prime, "resid_rel": r0.resid_rel,
                    "parallelism": "single" if world == 1 else f"replicas{world}",
                    "l2": "inputs larger than L2 (X 537 MB + residual 537 MB vs 126 MB L2); no flush"},
-        "roofline": {"kernel": "projection pass a4 (k_lhat + k_update, Alg. 2 l.13/l.16)",
+        "roofline": {"kernel": "projection pass a4 (k_nt_mma L-hat + k_update_mma fused update, Alg. 2 l.13/l.16)",
+                     "timing": "in-kernel %globaltimer stamps, summed over the blocks of the K timed steps",
                      "bound": "alu", "achieved": tflops, "peak": peak, "unit": "TFLOP/s",
                      "frac": tflops / peak, "traffic": traffic,
                      "peak_note": "FP64 DFMA: 148 SM x 64 FMA/clk x 2 x 1.965 GHz (derived, DESIGN.md §6); "
                                   "MEASURED_PEAKS.json has no FP64 entry",
                      "algorithmic_GBs": gbs, "hbm_frac_of_measured": gbs / 6551.4,
                      "share_of_step": proj_ms / a.steps / ms},
-        "phase_ms_per_step": {k: v / a.steps for k, v in ph.items()},
+        "phase_ms_eager_profile": ph,
+        "proj_ms_eager_events": ph_proj_eager,
+        "graph_loop": r0.graph,
         "gpu_launches": launches,
         "e2e": e2e,
         "cpu_baseline": cpu,

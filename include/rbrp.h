@@ -137,6 +137,11 @@ typedef struct {
  *              fix-up + chunk scan, [6] W (Alg. 3), [7] collectives.
  *   launches   (out) number of kernels this call launched.
  *   proj_calls (out) number of projection passes that did work (one per block).
+ *   proj_ms    (out) device time of the projection passes (a4: L-hat + fused update),
+ *              summed over blocks, from %globaltimer stamps taken inside the kernels
+ *              (first CTA start of L-hat to last CTA end of the update).
+ *   graph      (out) 1 if the block loop ran as one CUDA-graph launch (conditional WHILE
+ *              node), 0 if it was launched eagerly (replay, profile, or graphs unusable).
  */
 typedef struct {
   int64_t k;
@@ -155,6 +160,8 @@ typedef struct {
   float ms_phase[8];
   int32_t launches;
   int32_t proj_calls;
+  float proj_ms;
+  int32_t graph;
 } rbrp_report;
 
 /* Opaque NCCL communicator wrapper; NULL means a single-GPU call. */

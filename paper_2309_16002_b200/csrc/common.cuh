@@ -30,7 +30,40 @@ struct DevState {
   int32_t nonfinite;  // set by k_init_norms
   int32_t draws;      // Philox draws consumed by the current block
   int32_t rank_def;   // pivoted Cholesky hit a non-positive pivot
+  int32_t nlogged;    // blocks written to the device log
+  uint32_t done_ctas; // CTA completion counter of the projection update kernel
   int32_t pad;
+  long long ts0, ts1; // %globaltimer at projection start / end (current block)
+};
+
+__device__ __forceinline__ long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return (long long)t;
+}
+
+// the last CTA of a grid to call this records the projection end time
+__device__ __forceinline__ void proj_end_stamp(DevState* st) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned prev = atomicAdd(&st->done_ctas, 1u);
+    if (prev == gridDim.x - 1) {
+      st->ts1 = gtimer();
+      st->done_ctas = 0;
+    }
+  }
+}
+
+// per-block device log (read by the host once, at the end of rbrp_id)
+struct BlockLog {
+  int32_t* bt;        // [maxlog]
+  int32_t* bp;        // [maxlog]
+  double* rho;        // [maxlog]
+  int64_t* St;        // [maxlog][b]
+  int32_t* piv;       // [maxlog][b]
+  long long* ts;      // [maxlog][2]
+  int maxlog, b;
 };
 
 // fp64 warp reduction in a fixed butterfly order (bitwise deterministic)

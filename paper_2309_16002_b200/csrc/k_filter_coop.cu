@@ -362,10 +362,18 @@ cudaError_t launch_filter_coop(const FilterArgs& a, cudaStream_t s) {
     cudaFuncSetAttribute(k_filter_coop<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  FilterArgs A = a;
-  void* args[] = {&A};
-  return cudaLaunchCooperativeKernel((void*)k_filter_coop<T>, dim3(nsplit), dim3(kFiltThreads), args,
-                                     smem, s);
+  // cooperative launch through cudaLaunchKernelEx so that it can be captured in a graph
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nsplit);
+  cfg.blockDim = dim3(kFiltThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute la[1];
+  la[0].id = cudaLaunchAttributeCooperative;
+  la[0].val.cooperative = 1;
+  cfg.attrs = la;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_filter_coop<T>, a);
 }
 
 int filter_coop_nsplit(int64_t d) { return ceil_div(d, kFiltCW); }

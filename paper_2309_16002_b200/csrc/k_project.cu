@@ -97,11 +97,12 @@ template <typename T, int BN>
 __global__ void __launch_bounds__(kGemmThreads) k_lhat(const T* __restrict__ Xres, int64_t ldx,
                                                        const T* __restrict__ Qt, int64_t n,
                                                        int64_t d, T* __restrict__ L, int64_t ldl,
-                                                       const DevState* st) {
+                                                       DevState* st) {
   using C = GemmCfg<T, BN>;
   if (st->stop) return;
   const int bp = st->b_prime;
   if (bp <= 0 || bucket_of(bp) != BN) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) st->ts0 = gtimer();
   const int64_t k0 = st->k;
   const int64_t m0 = (int64_t)blockIdx.x * C::BM;
   T acc[C::TM][C::TN];
@@ -121,7 +122,7 @@ __global__ void __launch_bounds__(kGemmThreads) k_lhat(const T* __restrict__ Xre
 
 template <typename T>
 cudaError_t launch_lhat(const T* Xres, int64_t ldx, const T* Qt, int64_t n, int64_t d, T* L,
-                        int64_t ldl, const DevState* st, int bucket, cudaStream_t s) {
+                        int64_t ldl, DevState* st, int bucket, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   switch (bucket) {
     case 16: k_lhat<T, 16><<<ceil_div(n, GemmCfg<T, 16>::BM), kGemmThreads, 0, s>>>(Xres, ldx, Qt, n, d, L, ldl, st); break;
@@ -171,7 +172,7 @@ template <typename T, int BP>
 __global__ void __launch_bounds__(256) k_update(T* __restrict__ X, int64_t ldx,
                                                 const T* __restrict__ Qt, const T* __restrict__ L,
                                                 int64_t ldl, int64_t n, int64_t d,
-                                                double* __restrict__ dvec, const DevState* st) {
+                                                double* __restrict__ dvec, DevState* st) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T (*Ps)[kUpdRows + 4] = reinterpret_cast<T (*)[kUpdRows + 4]>(smem_raw);
   T (*Qs)[kUpdCols + 4] = reinterpret_cast<T (*)[kUpdCols + 4]>(smem_raw + sizeof(T) * BP * (kUpdRows + 4));
@@ -233,11 +234,12 @@ __global__ void __launch_bounds__(256) k_update(T* __restrict__ X, int64_t ldx,
     const int64_t gr = r0 + tr * 4 + r;
     if (tc == 0 && gr < n) dvec[gr] = v;
   }
+  proj_end_stamp(st);
 }
 
 template <typename T>
 cudaError_t launch_update(T* Xres, int64_t ldx, const T* Qt, const T* L, int64_t ldl, int64_t n,
-                          int64_t d, double* dvec, const DevState* st, int bucket, cudaStream_t s) {
+                          int64_t d, double* dvec, DevState* st, int bucket, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   const int g = ceil_div(n, kUpdRows);
   auto go = [&](auto kern, int BP) {
@@ -284,9 +286,9 @@ cudaError_t launch_fixup(T* Xres, int64_t ldx, double* dvec, T* L, int64_t ldl, 
 
 #define INST(T)                                                                                  \
   template cudaError_t launch_lhat<T>(const T*, int64_t, const T*, int64_t, int64_t, T*, int64_t, \
-                                      const DevState*, int, cudaStream_t);                        \
+                                      DevState*, int, cudaStream_t);                              \
   template cudaError_t launch_update<T>(T*, int64_t, const T*, const T*, int64_t, int64_t,        \
-                                        int64_t, double*, const DevState*, int, cudaStream_t);    \
+                                        int64_t, double*, DevState*, int, cudaStream_t);          \
   template cudaError_t launch_fixup<T>(T*, int64_t, double*, T*, int64_t, const double*,          \
                                        const int64_t*, int64_t, int64_t, int64_t, DevState*,      \
                                        cudaStream_t);                                             \

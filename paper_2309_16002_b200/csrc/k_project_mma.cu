@@ -35,28 +35,34 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 constexpr int kMmaWarps = 8;
-constexpr int kMmaRows = 8 * kMmaWarps;   // rows per CTA (8 per warp)
 constexpr int kKC = 64;                   // K (columns) per staged chunk
 constexpr int kXld = kKC + 8;             // X tile stride (doubles), = 8 mod 16: LDS.128 conflict-free
 constexpr int kBld = kKC + 8;             // B tile stride for 16-byte B loads (k_nt_mma)
 constexpr int kQld = kKC + 4;             // Q tile stride for 8-byte B loads (k_update_mma), = 4 mod 16
 
+// RG row groups of 8 rows per warp: every B (Q) fragment read from shared memory feeds
+// RG MMAs, which halves the shared-memory traffic per MMA at RG = 2.
 template <int BN> struct NtCfg {
-  static constexpr int NS = BN <= 64 ? 3 : 2;                            // pipeline stages
-  static constexpr int STAGE = kMmaRows * kXld + BN * kBld;              // doubles per stage
+  static constexpr int RG = BN == 128 ? 1 : 2;
+  static constexpr int ROWS = 8 * RG * kMmaWarps;                        // rows per tile
+  static constexpr int NS = 2;                                           // pipeline stages
+  static constexpr int STAGE = ROWS * kXld + BN * kBld;                  // doubles per stage
   static constexpr size_t SMEM = sizeof(double) * NS * STAGE;
 };
 template <int BP> struct UpdCfg {
-  static constexpr int NS = BP <= 64 ? 3 : 2;
-  static constexpr int STAGE = kMmaRows * kXld + BP * kQld;
+  static constexpr int RG = BP == 128 ? 1 : 2;
+  static constexpr int ROWS = 8 * RG * kMmaWarps;
+  static constexpr int NS = 2;
+  static constexpr int STAGE = ROWS * kXld + BP * kQld;
   static constexpr size_t SMEM = sizeof(double) * NS * STAGE;
 };
 
-// X tile rows [r0, r0+64) x columns [c0, c0+64) -> xs (zero-filled outside [0,M) x [0,K))
+// X tile rows [r0, r0+ROWS) x columns [c0, c0+64) -> xs (zero-filled outside [0,M) x [0,K))
+template <int ROWS>
 __device__ __forceinline__ void stage_x(double* xs, const double* __restrict__ A, int64_t lda,
                                         int64_t r0, int64_t M, int64_t c0, int64_t K, int tid) {
 #pragma unroll
-  for (int i = 0; i < (kMmaRows * kKC / 2) / (32 * kMmaWarps); ++i) {
+  for (int i = 0; i < (ROWS * kKC / 2) / (32 * kMmaWarps); ++i) {
     const int e = tid + i * 32 * kMmaWarps;
     const int r = e / (kKC / 2), c = (e % (kKC / 2)) * 2;
     const bool ok = (r0 + r < M) && (c0 + c < K);
@@ -75,18 +81,20 @@ __device__ __forceinline__ void stage_b(double* bs, const double* __restrict__ B
 }
 
 // ---------------------------------------------------------------------------------
-// C = A B^T: 64-row tiles x BN columns; persistent CTAs (one per SM) walk their tiles
-// and the 64-column K chunks of each tile as ONE flattened sequence, so the NS-stage
-// cp.async pipeline never drains between tiles.  Requirements (checked by the
-// launcher): K % 8 == 0, lda % 2 == 0, ldb % 2 == 0, 16-byte aligned A and B.
+// C = A B^T: ROWS-row tiles x BN columns; persistent CTAs (one per SM) walk their tiles
+// and the 64-column K chunks of each tile as ONE flattened sequence, so the cp.async
+// pipeline never drains between tiles.  Warp w owns rows [w*8*RG, (w+1)*8*RG) of a tile.
+// Requirements (checked by the launcher): K % 8 == 0, lda % 2 == 0, ldb % 2 == 0,
+// 16-byte aligned A and B.
 // ---------------------------------------------------------------------------------
 template <int BN>
 __global__ void __launch_bounds__(32 * kMmaWarps, 1) k_nt_mma(const double* __restrict__ A, int64_t lda,
                                                               const double* __restrict__ B, int64_t ldb,
                                                               double* __restrict__ C, int64_t ldc,
                                                               int64_t M, int64_t N, int64_t K,
-                                                              const DevState* st, int mode) {
+                                                              DevState* st, int mode) {
   using Cf = NtCfg<BN>;
+  constexpr int RG = Cf::RG;
   extern __shared__ __align__(16) double sm[];
   int64_t col0 = 0, Nn = N;
   if (mode == 1) {   // L-hat: N = b', columns written at L[:, k + j]
@@ -95,10 +103,11 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 1) k_nt_mma(const double* __re
     if (bp <= 0 || bucket_of(bp) != BN) return;
     Nn = bp;
     col0 = st->k;
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->ts0 = gtimer();
   }
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int g = lane >> 2, q = lane & 3;
-  const int64_t ntm = (M + kMmaRows - 1) / kMmaRows;
+  const int64_t ntm = (M + Cf::ROWS - 1) / Cf::ROWS;
   const int64_t ntn = (Nn + BN - 1) / BN;
   const int64_t ntiles = ntm * ntn;
   const int nchunk = (int)((K + kKC - 1) / kKC);
@@ -106,7 +115,7 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 1) k_nt_mma(const double* __re
   const int64_t total = nmine * nchunk;
   auto tile_of = [&](int64_t j, int64_t& r0, int64_t& n0) {
     const int64_t t = blockIdx.x + j * gridDim.x;
-    r0 = (t % ntm) * kMmaRows;
+    r0 = (t % ntm) * Cf::ROWS;
     n0 = (t / ntm) * BN;
   };
   auto issue = [&](int64_t it) {
@@ -115,14 +124,16 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 1) k_nt_mma(const double* __re
       tile_of(it / nchunk, r0, n0);
       const int64_t k0 = (it % nchunk) * kKC;
       double* base = sm + (size_t)(it % Cf::NS) * Cf::STAGE;
-      stage_x(base, A, lda, r0, M, k0, K, tid);
-      stage_b<BN, kBld>(base + kMmaRows * kXld, B, ldb, n0, Nn, k0, K, tid);
+      stage_x<Cf::ROWS>(base, A, lda, r0, M, k0, K, tid);
+      stage_b<BN, kBld>(base + Cf::ROWS * kXld, B, ldb, n0, Nn, k0, K, tid);
     }
     cp_async_commit();
   };
-  double2 acc[BN / 8];
+  double2 acc[RG][BN / 8];
 #pragma unroll
-  for (int t = 0; t < BN / 8; ++t) acc[t] = make_double2(0.0, 0.0);
+  for (int r = 0; r < RG; ++r)
+#pragma unroll
+    for (int t = 0; t < BN / 8; ++t) acc[r][t] = make_double2(0.0, 0.0);
 #pragma unroll
   for (int i = 0; i < Cf::NS - 1; ++i) issue(i);
   for (int64_t it = 0; it < total; ++it) {
@@ -130,32 +141,41 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 1) k_nt_mma(const double* __re
     cp_async_wait<Cf::NS - 1>();
     __syncthreads();
     const double* xs = sm + (size_t)(it % Cf::NS) * Cf::STAGE;
-    const double* bs = xs + kMmaRows * kXld;
+    const double* bs = xs + Cf::ROWS * kXld;
 #pragma unroll
     for (int s = 0; s < kKC / 8; ++s) {
-      const double2 xa = *reinterpret_cast<const double2*>(xs + (w * 8 + g) * kXld + 8 * s + 2 * q);
+      double2 xa[RG];
+#pragma unroll
+      for (int r = 0; r < RG; ++r)
+        xa[r] = *reinterpret_cast<const double2*>(xs + ((w * RG + r) * 8 + g) * kXld + 8 * s + 2 * q);
 #pragma unroll
       for (int t = 0; t < BN / 8; ++t) {
         const double2 b = *reinterpret_cast<const double2*>(bs + (t * 8 + g) * kBld + 8 * s + 2 * q);
-        dmma(acc[t], xa.x, b.x);
-        dmma(acc[t], xa.y, b.y);
+#pragma unroll
+        for (int r = 0; r < RG; ++r) {
+          dmma(acc[r][t], xa[r].x, b.x);
+          dmma(acc[r][t], xa[r].y, b.y);
+        }
       }
     }
     if (it % nchunk == nchunk - 1) {   // tile done: write, reset
       int64_t r0, n0;
       tile_of(it / nchunk, r0, n0);
-      const int64_t row = r0 + w * 8 + g;
-      if (row < M) {
-        double* crow = C + row * ldc + col0;
 #pragma unroll
-        for (int t = 0; t < BN / 8; ++t) {
-          const int64_t j = n0 + t * 8 + 2 * q;
-          if (j < Nn) crow[j] = acc[t].x;
-          if (j + 1 < Nn) crow[j + 1] = acc[t].y;
+      for (int r = 0; r < RG; ++r) {
+        const int64_t row = r0 + (w * RG + r) * 8 + g;
+        if (row < M) {
+          double* crow = C + row * ldc + col0;
+#pragma unroll
+          for (int t = 0; t < BN / 8; ++t) {
+            const int64_t j = n0 + t * 8 + 2 * q;
+            if (j < Nn) crow[j] = acc[r][t].x;
+            if (j + 1 < Nn) crow[j + 1] = acc[r][t].y;
+          }
         }
-      }
 #pragma unroll
-      for (int t = 0; t < BN / 8; ++t) acc[t] = make_double2(0.0, 0.0);
+        for (int t = 0; t < BN / 8; ++t) acc[r][t] = make_double2(0.0, 0.0);
+      }
     }
     __syncthreads();
   }
@@ -173,8 +193,9 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 1) k_update_mma(double* __rest
                                                                   const double* __restrict__ L,
                                                                   int64_t ldl, int64_t n, int64_t d,
                                                                   double* __restrict__ dvec,
-                                                                  const DevState* st) {
+                                                                  DevState* st) {
   using Cf = UpdCfg<BP>;
+  constexpr int RG = Cf::RG;
   extern __shared__ __align__(16) double sm[];
   if (st->stop) return;
   const int bp = st->b_prime;
@@ -182,36 +203,41 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 1) k_update_mma(double* __rest
   const int64_t k0 = st->k;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int g = lane >> 2, q = lane & 3;
-  const int64_t ntiles = (n + kMmaRows - 1) / kMmaRows;
+  const int64_t ntiles = (n + Cf::ROWS - 1) / Cf::ROWS;
   const int nchunk = (int)((d + kKC - 1) / kKC);
   const int64_t nmine = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int64_t total = nmine * nchunk;
-  auto r0_of = [&](int64_t j) { return (blockIdx.x + j * gridDim.x) * (int64_t)kMmaRows; };
+  auto r0_of = [&](int64_t j) { return (blockIdx.x + j * gridDim.x) * (int64_t)Cf::ROWS; };
   auto issue = [&](int64_t it) {
     if (it < total) {
       double* base = sm + (size_t)(it % Cf::NS) * Cf::STAGE;
       const int64_t c0 = (it % nchunk) * kKC;
-      stage_x(base, X, ldx, r0_of(it / nchunk), n, c0, d, tid);
-      stage_b<BP, kQld>(base + kMmaRows * kXld, Qt, d, 0, bp, c0, d, tid);
+      stage_x<Cf::ROWS>(base, X, ldx, r0_of(it / nchunk), n, c0, d, tid);
+      stage_b<BP, kQld>(base + Cf::ROWS * kXld, Qt, d, 0, bp, c0, d, tid);
     }
     cp_async_commit();
   };
-  // A fragments: -P[row][4 jc + q]
-  double a[BP / 4], an[BP / 4];
-  auto load_a = [&](double (&dst)[BP / 4], int64_t j) {
-    const int64_t row = r0_of(j) + w * 8 + g;
-    const bool rok = row < n;
-    const double* lrow = L + (rok ? row : 0) * ldl + k0;
+  // A fragments: -P[row][4 jc + q] for the warp's RG row groups
+  double a[RG][BP / 4], an[RG][BP / 4];
+  auto load_a = [&](double (&dst)[RG][BP / 4], int64_t j) {
 #pragma unroll
-    for (int jc = 0; jc < BP / 4; ++jc) {
-      const int jj = jc * 4 + q;
-      dst[jc] = (rok && jj < bp) ? -lrow[jj] : 0.0;
+    for (int r = 0; r < RG; ++r) {
+      const int64_t row = r0_of(j) + (w * RG + r) * 8 + g;
+      const bool rok = row < n;
+      const double* lrow = L + (rok ? row : 0) * ldl + k0;
+#pragma unroll
+      for (int jc = 0; jc < BP / 4; ++jc) {
+        const int jj = jc * 4 + q;
+        dst[r][jc] = (rok && jj < bp) ? -lrow[jj] : 0.0;
+      }
     }
   };
 #pragma unroll
   for (int i = 0; i < Cf::NS - 1; ++i) issue(i);
   if (total > 0) load_a(a, 0);
-  double nrm = 0.0;
+  double nrm[RG];
+#pragma unroll
+  for (int r = 0; r < RG; ++r) nrm[r] = 0.0;
   for (int64_t it = 0; it < total; ++it) {
     const int64_t j = it / nchunk;
     const int ch = (int)(it % nchunk);
@@ -220,38 +246,53 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 1) k_update_mma(double* __rest
     cp_async_wait<Cf::NS - 1>();
     __syncthreads();
     const double* xs = sm + (size_t)(it % Cf::NS) * Cf::STAGE;
-    const double* qb = xs + kMmaRows * kXld;
-    const int64_t row = r0_of(j) + w * 8 + g;
-    const bool rok = row < n;
-    double* xrow = X + (rok ? row : 0) * ldx;
+    const double* qb = xs + Cf::ROWS * kXld;
     const int64_t c0 = (int64_t)ch * kKC;
-    double2 xd[kKC / 8];
+    double2 xd[RG][kKC / 8];
 #pragma unroll
-    for (int s = 0; s < kKC / 8; ++s)
-      xd[s] = *reinterpret_cast<const double2*>(xs + (w * 8 + g) * kXld + 8 * s + 2 * q);
+    for (int r = 0; r < RG; ++r)
+#pragma unroll
+      for (int s = 0; s < kKC / 8; ++s)
+        xd[r][s] = *reinterpret_cast<const double2*>(xs + ((w * RG + r) * 8 + g) * kXld + 8 * s + 2 * q);
 #pragma unroll
     for (int jc = 0; jc < BP / 4; ++jc) {
 #pragma unroll
-      for (int s = 0; s < kKC / 8; ++s) dmma(xd[s], a[jc], qb[(jc * 4 + q) * kQld + 8 * s + g]);
+      for (int s = 0; s < kKC / 8; ++s) {
+        const double bq = qb[(jc * 4 + q) * kQld + 8 * s + g];
+#pragma unroll
+        for (int r = 0; r < RG; ++r) dmma(xd[r][s], a[r][jc], bq);
+      }
     }
 #pragma unroll
-    for (int s = 0; s < kKC / 8; ++s) {
-      const int64_t c = c0 + 8 * s + 2 * q;
-      if (rok && c < d) {
-        __stcs(reinterpret_cast<double2*>(xrow + c), xd[s]);
-        nrm += xd[s].x * xd[s].x + xd[s].y * xd[s].y;
+    for (int r = 0; r < RG; ++r) {
+      const int64_t row = r0_of(j) + (w * RG + r) * 8 + g;
+      const bool rok = row < n;
+      double* xrow = X + (rok ? row : 0) * ldx;
+#pragma unroll
+      for (int s = 0; s < kKC / 8; ++s) {
+        const int64_t c = c0 + 8 * s + 2 * q;
+        if (rok && c < d) {
+          __stcs(reinterpret_cast<double2*>(xrow + c), xd[r][s]);
+          nrm[r] += xd[r][s].x * xd[r][s].x + xd[r][s].y * xd[r][s].y;
+        }
+      }
+      if (ch == nchunk - 1) {
+        double v = nrm[r];
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        v += __shfl_xor_sync(0xffffffffu, v, 2);
+        if (rok && q == 0) dvec[row] = v;
+        nrm[r] = 0.0;
       }
     }
     if (ch == nchunk - 1) {
-      nrm += __shfl_xor_sync(0xffffffffu, nrm, 1);
-      nrm += __shfl_xor_sync(0xffffffffu, nrm, 2);
-      if (rok && q == 0) dvec[row] = nrm;
-      nrm = 0.0;
 #pragma unroll
-      for (int jc = 0; jc < BP / 4; ++jc) a[jc] = an[jc];
+      for (int r = 0; r < RG; ++r)
+#pragma unroll
+        for (int jc = 0; jc < BP / 4; ++jc) a[r][jc] = an[r][jc];
     }
     __syncthreads();
   }
+  proj_end_stamp(st);
 }
 
 static int g_num_sms = 0;
@@ -274,9 +315,9 @@ bool projection_mma_supported(const void* X, int64_t ldx, const void* Qt, int64_
 }
 
 cudaError_t launch_lhat_mma(const double* Xres, int64_t ldx, const double* Qt, int64_t n, int64_t d,
-                            double* L, int64_t ldl, const DevState* st, int bucket, cudaStream_t s) {
+                            double* L, int64_t ldl, DevState* st, int bucket, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  dim3 grid((unsigned)std::min<int64_t>(num_sms(), ceil_div(n, kMmaRows)), 1);
+  dim3 grid((unsigned)num_sms(), 1);
   auto go = [&](auto kern, size_t smem) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<grid, 32 * kMmaWarps, smem, s>>>(Xres, ldx, Qt, d, L, ldl, n, 0, d, st, 1);
@@ -291,10 +332,10 @@ cudaError_t launch_lhat_mma(const double* Xres, int64_t ldx, const double* Qt, i
 }
 
 cudaError_t launch_update_mma(double* Xres, int64_t ldx, const double* Qt, const double* L,
-                              int64_t ldl, int64_t n, int64_t d, double* dvec, const DevState* st,
+                              int64_t ldl, int64_t n, int64_t d, double* dvec, DevState* st,
                               int bucket, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  const int g = (int)std::min<int64_t>(num_sms(), ceil_div(n, kMmaRows));
+  const int g = num_sms();
   auto go = [&](auto kern, size_t smem) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<g, 32 * kMmaWarps, smem, s>>>(Xres, ldx, Qt, L, ldl, n, d, dvec, st);
@@ -312,7 +353,7 @@ cudaError_t launch_update_mma(double* Xres, int64_t ldx, const double* Qt, const
 bool gemm_nt_mma(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
                  int64_t M, int64_t N, int64_t K, cudaStream_t s, cudaError_t* err) {
   if (!mma_ok(A, lda, K) || !mma_ok(B, ldb, K)) return false;
-  dim3 grid((unsigned)std::min<int64_t>(num_sms(), (int64_t)ceil_div(M, kMmaRows) * ceil_div(N, 128)), 1);
+  dim3 grid((unsigned)num_sms(), 1);
   const size_t smem = NtCfg<128>::SMEM;
   cudaFuncSetAttribute(k_nt_mma<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_nt_mma<128><<<grid, 32 * kMmaWarps, smem, s>>>(A, lda, B, ldb, C, ldc, M, N, K, nullptr, 0);

@@ -45,6 +45,30 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample(SampleArgs A) {
   __shared__ int64_t chosen[kMaxB];
   __shared__ int64_t cand[kSampleThreads];
   __shared__ int wcount[kSampleThreads / 32];
+  __shared__ int s_tprev, s_log, s_btprev, s_bpprev;
+
+  // log the block that just finished (device-side, read by the host at the end)
+  if (tid == 0) {
+    s_tprev = st->t;
+    s_btprev = st->b_t;
+    s_bpprev = st->b_prime;
+    s_log = (!A.first && s_tprev >= 1 && s_tprev > st->nlogged && s_tprev <= A.log.maxlog &&
+             A.log.bt != nullptr);
+  }
+  __syncthreads();
+  if (s_log) {
+    const int slot = s_tprev - 1;
+    for (int i = tid; i < A.log.b; i += kSampleThreads) {
+      A.log.St[(int64_t)slot * A.log.b + i] = i < s_btprev ? A.S_t[i] : -1;
+      A.log.piv[(int64_t)slot * A.log.b + i] = i < s_bpprev ? A.piv[i] : -1;
+    }
+    if (tid == 0) {
+      A.log.bt[slot] = s_btprev;
+      A.log.bp[slot] = s_bpprev;
+      A.log.ts[2 * slot] = st->ts0;
+      A.log.ts[2 * slot + 1] = st->ts1;
+    }
+  }
 
   // the previous block's kept skeletons become part of S (Alg. 2 l.14)
   // (1) chunk prefix, fixed order: lane l sums a contiguous range of chunks
@@ -80,6 +104,10 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample(SampleArgs A) {
     st->total = total;
     st->npos = s_np;
     if (A.first) st->D0 = total;
+    if (s_log) {
+      A.log.rho[s_tprev - 1] = total / st->D0;
+      st->nlogged = s_tprev;
+    }
     const bool fixed = !(st->tau > 0.0);
     bool stop = st->stop != 0;
     if (!stop && st->k >= st->k_cap) {
@@ -102,10 +130,12 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample(SampleArgs A) {
     s_stop = stop;
     s_bt = bt;
     s_c = 0;
+    if (A.cond) cudaGraphSetConditional((cudaGraphConditionalHandle)A.cond, stop ? 0u : 1u);
   }
   __syncthreads();
   if (s_stop) return;
   if (A.replay_len >= 0) {
+    for (int i = tid; i < A.replay_len; i += kSampleThreads) A.S_t[i] = A.S_rep[i];
     if (tid == 0) { st->b_t = A.replay_len; st->draws = 0; }
     return;
   }

@@ -22,9 +22,13 @@ struct SampleArgs {
   const double* dvec;
   int64_t n_local, row_offset;
   int64_t* S_t;           // out: candidates (global ids)
-  int replay_len;         // >= 0: replay (S_t already filled); -1: sample
+  const int64_t* S_rep;   // replay: staged candidate ids, copied to S_t
+  int replay_len;         // >= 0: replay (ids in S_rep); -1: sample; -2: replay exhausted
   uint64_t seed;
   int first;              // 1 on the call right after init (sets D0)
+  const int32_t* piv;     // pivots of the block that just finished (logged)
+  BlockLog log;
+  unsigned long long cond;   // cudaGraphConditionalHandle of the WHILE node (0: none)
 };
 cudaError_t launch_sample(const SampleArgs& a, cudaStream_t s);
 
@@ -62,10 +66,10 @@ int filter_coop_nsplit(int64_t d);
 // k_project.cu — Alg. 2 l.13, l.16 in residual form
 template <typename T>
 cudaError_t launch_lhat(const T* Xres, int64_t ldx, const T* Qt, int64_t n, int64_t d, T* L,
-                        int64_t ldl, const DevState* st, int bucket, cudaStream_t s);
+                        int64_t ldl, DevState* st, int bucket, cudaStream_t s);
 template <typename T>
 cudaError_t launch_update(T* Xres, int64_t ldx, const T* Qt, const T* L, int64_t ldl, int64_t n,
-                          int64_t d, double* dvec, const DevState* st, int bucket, cudaStream_t s);
+                          int64_t d, double* dvec, DevState* st, int bucket, cudaStream_t s);
 template <typename T>
 cudaError_t launch_fixup(T* Xres, int64_t ldx, double* dvec, T* L, int64_t ldl, const double* Rtot,
                          const int64_t* S, int64_t n_local, int64_t row_offset, int64_t d,
@@ -74,9 +78,9 @@ cudaError_t launch_fixup(T* Xres, int64_t ldx, double* dvec, T* L, int64_t ldl, 
 // k_project_mma.cu — DMMA (FP64 tensor) projection
 bool projection_mma_supported(const void* X, int64_t ldx, const void* Qt, int64_t d);
 cudaError_t launch_lhat_mma(const double* Xres, int64_t ldx, const double* Qt, int64_t n, int64_t d,
-                            double* L, int64_t ldl, const DevState* st, int bucket, cudaStream_t s);
+                            double* L, int64_t ldl, DevState* st, int bucket, cudaStream_t s);
 cudaError_t launch_update_mma(double* Xres, int64_t ldx, const double* Qt, const double* L,
-                              int64_t ldl, int64_t n, int64_t d, double* dvec, const DevState* st,
+                              int64_t ldl, int64_t n, int64_t d, double* dvec, DevState* st,
                               int bucket, cudaStream_t s);
 bool gemm_nt_mma(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
                  int64_t M, int64_t N, int64_t K, cudaStream_t s, cudaError_t* err);

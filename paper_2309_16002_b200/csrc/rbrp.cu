@@ -1,16 +1,21 @@
 // rbrp.cu — C ABI of librbrp.so (include/rbrp.h) and the host orchestration of
 // Alg. 2 + Alg. 3.
 //
-// The host only sequences kernels on the caller's stream; every decision of the loop
-// (stop test l.3, b_t l.4, sampling l.5, b' l.8, |S| l.14) is taken on the device in
-// DevState.  One device->host read of DevState per block (the data-dependent stop).
+// Every decision of the loop (stop test l.3, b_t l.4, sampling l.5, b' l.8, |S| l.14)
+// is taken on the device in DevState, so the block loop needs no host round trip: the
+// kernels of one block are captured once into the body of a CUDA-graph conditional WHILE
+// node whose condition the sampler kernel sets (cudaGraphSetConditional).  The whole
+// selection runs as one graph launch; the instantiated graph is cached per (problem,
+// buffers).  Replay / profiling / graph-less runs use the same kernels launched eagerly,
+// with one host read of DevState per block.  Per-block results go to a device log that
+// the host reads once at the end.
 #include <cuda_runtime.h>
-#include <dlfcn.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
+#include <mutex>
 #include <vector>
 
 #include "comm.cuh"
@@ -30,8 +35,9 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
   size_t Xres = SIZE_MAX, dvec, cpre, ctot, cpos, cprefix, L, Qt, Vg, Gpart, G, Tg, Ag, R11, Rtot,
-         piv, mass, St, S, forced, cand, st, L1 = SIZE_MAX, LinvT = SIZE_MAX, total;
-  int nsplit, cw;
+         piv, mass, St, Srep, S, forced, dbg, st, L1 = SIZE_MAX, LinvT = SIZE_MAX;
+  size_t lbt, lbp, lrho, lSt, lpiv, lts, total;
+  int nsplit, maxlog;
   int64_t nchunks, k_cap;
 };
 
@@ -62,8 +68,8 @@ Layout make_layout(const rbrp_problem* p) {
   const int64_t n = p->n_local, d = p->d;
   L.k_cap = k_cap_of(p);
   L.nchunks = (p->n_global + RBRP_CHUNK - 1) / RBRP_CHUNK;
-  L.cw = 32;
-  L.nsplit = (int)((d + L.cw - 1) / L.cw);
+  L.nsplit = filter_coop_nsplit(d);
+  L.maxlog = (int)std::min<int64_t>(L.k_cap + 1, 8192);
   size_t off = 0;
   auto take = [&](size_t bytes) {
     size_t o = off;
@@ -89,10 +95,17 @@ Layout make_layout(const rbrp_problem* p) {
   L.piv = take(B * 4);
   L.mass = take(B * 8);
   L.St = take(B * 8);
+  L.Srep = take(B * 8);
   L.S = take((size_t)L.k_cap * 8);
   L.forced = take(B * 4);
-  L.cand = take(4096 * 8);
+  L.dbg = take(64 * 8);
   L.st = take(sizeof(DevState));
+  L.lbt = take((size_t)L.maxlog * 4);
+  L.lbp = take((size_t)L.maxlog * 4);
+  L.lrho = take((size_t)L.maxlog * 8);
+  L.lSt = take((size_t)L.maxlog * p->b * 8);
+  L.lpiv = take((size_t)L.maxlog * p->b * 4);
+  L.lts = take((size_t)L.maxlog * 16);
   if (!(p->flags & RBRP_NO_W)) {
     L.L1 = take((size_t)L.k_cap * L.k_cap * 8);
     L.LinvT = take((size_t)L.k_cap * L.k_cap * w);
@@ -121,23 +134,20 @@ struct Pinned {
 };
 thread_local Pinned g_pinned;
 
-// RBRP_FORCE_SIMT=1 selects the CUDA-core (DFMA/FFMA) projection kernels instead of DMMA
-bool dbg_stamps() {
-  const char* e = getenv("RBRP_DEBUG_STAMPS");
+bool env_on(const char* name) {
+  const char* e = getenv(name);
   return e && e[0] == '1';
 }
-bool force_simt() {
-  const char* e = getenv("RBRP_FORCE_SIMT");
-  return e && e[0] == '1';
-}
+// RBRP_FORCE_SIMT=1: CUDA-core projection kernels instead of DMMA.  RBRP_NO_GRAPH=1: eager
+// block loop.  RBRP_DEBUG_STAMPS=1: print the filter phase stamps of every block (eager).
+bool force_simt() { return env_on("RBRP_FORCE_SIMT"); }
 
-// per-phase CUDA events on the caller's stream (report.profile)
+// per-phase CUDA events on the caller's stream (report.profile, eager loop only)
 struct Prof {
   bool on = false;
   cudaStream_t s = nullptr;
   std::vector<int> phase;
   std::vector<cudaEvent_t> ev;   // pairs (start, end)
-  int open_phase = -1;
   void begin(int ph) {
     if (!on) return;
     cudaEvent_t a, b;
@@ -163,257 +173,434 @@ struct Prof {
   }
 };
 
+// device pointers of one call
+template <typename T>
+struct Ctx {
+  const rbrp_problem* p;
+  const Layout* Ly;
+  rbrp_comm* comm;
+  int64_t n, d, k_cap, chunk0, ldr;
+  T* X;
+  T* Xres;
+  double *dvec, *cpre, *ctot, *cprefix, *Vg, *Gpart, *G, *Tg, *Ag, *R11, *Rtot, *mass;
+  int32_t *cpos, *piv, *forced;
+  T *Lm, *Qt;
+  int64_t *St, *Srep, *S;
+  DevState* st;
+  long long* dbg;
+  BlockLog log;
+  bool use_mma, use_forced;
+  int bucketB;
+};
+
+// The kernels of one block (Alg. 2 l.6-16), optionally followed by the next block's
+// stop test and sample (l.3-5).  Every kernel reads its sizes from DevState and is a
+// no-op once stop is set, so the sequence can be replayed blindly (graph body).
+template <typename T>
+int enqueue_block(Ctx<T>& c, SampleArgs& sa, cudaStream_t s, Prof* prof, int* nl, int* nproj,
+                  bool with_sample) {
+#define LK(x)                                  \
+  do {                                         \
+    ++*nl;                                     \
+    if ((x) != cudaSuccess) return RBRP_ECUDA; \
+  } while (0)
+  const rbrp_problem* p = c.p;
+  if (prof) prof->begin(2);
+  FilterArgs fa;
+  fa.st = c.st;
+  fa.X = c.Xres;
+  fa.ldx = c.ldr;
+  fa.Vg = nullptr;
+  if (c.comm) {
+    LK(launch_gather_rows<T>(c.Xres, c.ldr, c.St, c.n, p->row_offset, c.st, c.d, c.Vg, s));
+    int rc = comm_allreduce_f64(c.comm, c.Vg, (int64_t)RBRP_MAX_B * c.d, s);
+    if (rc) return rc;
+    fa.Vg = c.Vg;
+  }
+  fa.S_t = c.St;
+  fa.row_offset = p->row_offset;
+  fa.d = c.d;
+  fa.Gpart = c.Gpart;
+  fa.G = c.G;
+  fa.forced = c.use_forced ? c.forced : nullptr;
+  fa.piv = c.piv;
+  fa.mass = c.mass;
+  fa.R11 = c.R11;
+  fa.Tg = c.Tg;
+  fa.Ag = c.Ag;
+  fa.Rtot = c.Rtot;
+  fa.S = c.S;
+  fa.Qt = c.Qt;
+  fa.bp_pad = c.bucketB;
+  fa.dbg = c.dbg;
+  LK(launch_filter_coop<T>(fa, s));
+  if (prof) prof->end();
+  // a4: projection + fused norms (l.13, l.16)
+  if (prof) prof->begin(3);
+  for (int bk = 16; bk <= c.bucketB; bk *= 2) {
+    if (c.use_mma)
+      LK(launch_lhat_mma((const double*)c.Xres, c.ldr, (const double*)c.Qt, c.n, c.d, (double*)c.Lm,
+                         c.k_cap, c.st, bk, s));
+    else
+      LK(launch_lhat<T>(c.Xres, c.ldr, c.Qt, c.n, c.d, c.Lm, c.k_cap, c.st, bk, s));
+  }
+  if (prof) prof->end();
+  if (prof) prof->begin(4);
+  for (int bk = 16; bk <= c.bucketB; bk *= 2) {
+    if (c.use_mma)
+      LK(launch_update_mma((double*)c.Xres, c.ldr, (const double*)c.Qt, (const double*)c.Lm, c.k_cap,
+                           c.n, c.d, c.dvec, c.st, bk, s));
+    else
+      LK(launch_update<T>(c.Xres, c.ldr, c.Qt, c.Lm, c.k_cap, c.n, c.d, c.dvec, c.st, bk, s));
+  }
+  if (prof) prof->end();
+  ++*nproj;
+  if (prof) prof->begin(5);
+  LK(launch_fixup<T>(c.Xres, c.ldr, c.dvec, c.Lm, c.k_cap, c.Rtot, c.S, c.n, p->row_offset, c.d, c.st, s));
+  LK(launch_chunk_scan(c.dvec, c.n, c.chunk0, c.cpre, c.ctot, c.cpos, s));
+  if (prof) prof->end();
+  if (c.comm) {
+    int rc = comm_allgather_chunks(c.comm, c.ctot, c.cpos, c.chunk0, (c.n + RBRP_CHUNK - 1) / RBRP_CHUNK,
+                                   c.Ly->nchunks, s);
+    if (rc) return rc;
+  }
+  if (with_sample) {
+    if (prof) prof->begin(1);
+    LK(launch_sample(sa, s));
+    if (prof) prof->end();
+  }
+#undef LK
+  return RBRP_OK;
+}
+
+// ---------------------------------------------------------------------------------
+// graph cache: one instantiated WHILE-loop graph per (problem, buffers, device)
+// ---------------------------------------------------------------------------------
+struct GraphKey {
+  rbrp_problem p;
+  const void* X;
+  const void* ws;
+  int device, use_mma;
+  bool operator==(const GraphKey& o) const { return memcmp(this, &o, sizeof(GraphKey)) == 0; }
+};
+struct GraphEntry {
+  GraphKey key;
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int launches_per_block = 0;
+  unsigned long long stamp = 0;
+};
+std::mutex g_graph_mu;
+std::vector<GraphEntry> g_graphs;
+unsigned long long g_graph_clock = 0;
+cudaStream_t g_capture_stream = nullptr;
+
+GraphKey make_key(const rbrp_problem* p, const void* X, const void* ws, bool use_mma) {
+  GraphKey k;
+  memset(&k, 0, sizeof(k));
+  k.p = *p;
+  k.p.replay_blocks = nullptr;
+  k.p.replay_lens = nullptr;
+  k.p.replay_pivots = nullptr;
+  k.X = X;
+  k.ws = ws;
+  cudaGetDevice(&k.device);
+  k.use_mma = use_mma;
+  return k;
+}
+
+// Returns the cached graph for key, building it if needed; nullptr if graphs are not
+// usable (the caller then runs the eager loop — same kernels, host-driven).
+template <typename T>
+GraphEntry* get_graph(Ctx<T>& c, SampleArgs sa, const GraphKey& key) {
+  std::lock_guard<std::mutex> lk(g_graph_mu);
+  for (auto& e : g_graphs)
+    if (e.key == key) {
+      e.stamp = ++g_graph_clock;
+      return &e;
+    }
+  if (!g_capture_stream && cudaStreamCreateWithFlags(&g_capture_stream, cudaStreamNonBlocking) != cudaSuccess)
+    return nullptr;
+  GraphEntry e;
+  e.key = key;
+  cudaGraphConditionalHandle h;
+  cudaGraphNode_t node;
+  cudaGraph_t body = nullptr;
+  if (cudaGraphCreate(&e.g, 0) != cudaSuccess) return nullptr;
+  bool ok = cudaGraphConditionalHandleCreate(&h, e.g, 1, cudaGraphCondAssignDefault) == cudaSuccess;
+  if (ok) {
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = h;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    ok = cudaGraphAddNode(&node, e.g, nullptr, 0, &np) == cudaSuccess;
+    if (ok) body = np.conditional.phGraph_out[0];
+    ok = ok && body;
+  }
+  if (ok) {
+    ok = cudaStreamBeginCaptureToGraph(g_capture_stream, body, nullptr, nullptr, 0,
+                                       cudaStreamCaptureModeRelaxed) == cudaSuccess;
+    if (ok) {
+      sa.cond = (unsigned long long)h;
+      sa.first = 0;
+      sa.replay_len = -1;
+      int nl = 0, nproj = 0;
+      const int rc = enqueue_block<T>(c, sa, g_capture_stream, nullptr, &nl, &nproj, true);
+      cudaGraph_t cap = nullptr;
+      const bool endok = cudaStreamEndCapture(g_capture_stream, &cap) == cudaSuccess;
+      ok = (rc == RBRP_OK) && endok;
+      e.launches_per_block = nl;
+    }
+  }
+  if (ok) ok = cudaGraphInstantiate(&e.exec, e.g, 0) == cudaSuccess;
+  if (!ok) {
+    cudaGetLastError();
+    if (e.exec) cudaGraphExecDestroy(e.exec);
+    if (e.g) cudaGraphDestroy(e.g);
+    return nullptr;
+  }
+  if (g_graphs.size() >= 8) {   // evict the least recently used
+    auto it = std::min_element(g_graphs.begin(), g_graphs.end(),
+                               [](const GraphEntry& a, const GraphEntry& b) { return a.stamp < b.stamp; });
+    cudaGraphExecDestroy(it->exec);
+    cudaGraphDestroy(it->g);
+    g_graphs.erase(it);
+  }
+  e.stamp = ++g_graph_clock;
+  g_graphs.push_back(e);
+  return &g_graphs.back();
+}
+
 template <typename T>
 int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* comm,
         cudaStream_t s, int64_t* S_out, void* W_out, rbrp_report* rep) {
-  const int64_t n = p->n_local, d = p->d, k_cap = Ly.k_cap;
+  Ctx<T> c;
+  c.p = p;
+  c.Ly = &Ly;
+  c.comm = comm;
+  c.n = p->n_local;
+  c.d = p->d;
+  c.k_cap = Ly.k_cap;
+  c.chunk0 = p->row_offset / RBRP_CHUNK;
   const bool inplace = (p->flags & RBRP_INPLACE) != 0;
-  T* X = (T*)Xv;
-  T* Xres = inplace ? X : (T*)(ws + Ly.Xres);
-  const int64_t ldr = inplace ? p->ld : d;
-  double* dvec = (double*)(ws + Ly.dvec);
-  double* cpre = (double*)(ws + Ly.cpre);
-  double* ctot = (double*)(ws + Ly.ctot);
-  int32_t* cpos = (int32_t*)(ws + Ly.cpos);
-  double* cprefix = (double*)(ws + Ly.cprefix);
-  T* Lm = (T*)(ws + Ly.L);
-  T* Qt = (T*)(ws + Ly.Qt);
-  double* Vg = (double*)(ws + Ly.Vg);
-  double* Gpart = (double*)(ws + Ly.Gpart);
-  double* G = (double*)(ws + Ly.G);
-  double* Tg = (double*)(ws + Ly.Tg);
-  double* Ag = (double*)(ws + Ly.Ag);
-  double* R11 = (double*)(ws + Ly.R11);
-  double* Rtot = (double*)(ws + Ly.Rtot);
-  int32_t* piv = (int32_t*)(ws + Ly.piv);
-  double* mass = (double*)(ws + Ly.mass);
-  int64_t* St = (int64_t*)(ws + Ly.St);
-  int64_t* S = (int64_t*)(ws + Ly.S);
-  int32_t* forced = (int32_t*)(ws + Ly.forced);
-  DevState* st = (DevState*)(ws + Ly.st);
+  c.X = (T*)Xv;
+  c.Xres = inplace ? c.X : (T*)(ws + Ly.Xres);
+  c.ldr = inplace ? p->ld : c.d;
+  c.dvec = (double*)(ws + Ly.dvec);
+  c.cpre = (double*)(ws + Ly.cpre);
+  c.ctot = (double*)(ws + Ly.ctot);
+  c.cpos = (int32_t*)(ws + Ly.cpos);
+  c.cprefix = (double*)(ws + Ly.cprefix);
+  c.Lm = (T*)(ws + Ly.L);
+  c.Qt = (T*)(ws + Ly.Qt);
+  c.Vg = (double*)(ws + Ly.Vg);
+  c.Gpart = (double*)(ws + Ly.Gpart);
+  c.G = (double*)(ws + Ly.G);
+  c.Tg = (double*)(ws + Ly.Tg);
+  c.Ag = (double*)(ws + Ly.Ag);
+  c.R11 = (double*)(ws + Ly.R11);
+  c.Rtot = (double*)(ws + Ly.Rtot);
+  c.piv = (int32_t*)(ws + Ly.piv);
+  c.mass = (double*)(ws + Ly.mass);
+  c.St = (int64_t*)(ws + Ly.St);
+  c.Srep = (int64_t*)(ws + Ly.Srep);
+  c.S = (int64_t*)(ws + Ly.S);
+  c.forced = (int32_t*)(ws + Ly.forced);
+  c.st = (DevState*)(ws + Ly.st);
+  const bool stamps = env_on("RBRP_DEBUG_STAMPS");
+  c.dbg = stamps ? (long long*)(ws + Ly.dbg) : nullptr;
+  c.log.bt = (int32_t*)(ws + Ly.lbt);
+  c.log.bp = (int32_t*)(ws + Ly.lbp);
+  c.log.rho = (double*)(ws + Ly.lrho);
+  c.log.St = (int64_t*)(ws + Ly.lSt);
+  c.log.piv = (int32_t*)(ws + Ly.lpiv);
+  c.log.ts = (long long*)(ws + Ly.lts);
+  c.log.maxlog = Ly.maxlog;
+  c.log.b = p->b;
+  c.use_forced = p->replay_pivots != nullptr;
+  c.use_mma = sizeof(T) == 8 && !force_simt() && projection_mma_supported(c.Xres, c.ldr, c.Qt, c.d);
+  c.bucketB = bucket_of((int)std::min<int64_t>(p->b, c.k_cap));
+  const int64_t k_cap = c.k_cap;
 
-  // pinned staging: [state A][state B][S_t][piv][S]
-  const size_t off_B = 256, off_St = 512, off_piv = off_St + RBRP_MAX_B * 8,
-               off_S = off_piv + RBRP_MAX_B * 4;
-  char* hp = (char*)g_pinned.get(off_S + (size_t)k_cap * 8 + 64);
+  // pinned staging: [state][S_t][piv][log ...][S]
+  const int mb = Ly.maxlog, b = p->b;
+  size_t o = 0;
+  auto carve = [&](size_t bytes) { size_t r = o; o = align256(o + bytes); return r; };
+  const size_t o_st = carve(sizeof(DevState)), o_St = carve(RBRP_MAX_B * 8),
+               o_piv = carve(RBRP_MAX_B * 4), o_bt = carve(mb * 4), o_bp = carve(mb * 4),
+               o_rho = carve(mb * 8), o_lSt = carve((size_t)mb * b * 8), o_lpiv = carve((size_t)mb * b * 4),
+               o_ts = carve((size_t)mb * 16), o_S = carve((size_t)k_cap * 8 + 8);
+  char* hp = (char*)g_pinned.get(o);
   if (!hp) return RBRP_ECUDA;
-  DevState* hA = (DevState*)hp;
-  DevState* hB = (DevState*)(hp + off_B);
-  int64_t* hSt = (int64_t*)(hp + off_St);
-  int32_t* hpiv = (int32_t*)(hp + off_piv);
-  int64_t* hS = (int64_t*)(hp + off_S);
+  DevState* hst = (DevState*)(hp + o_st);
+  int64_t* hSt = (int64_t*)(hp + o_St);
+  int32_t* hpiv = (int32_t*)(hp + o_piv);
 
-  DevState h0;
-  memset(&h0, 0, sizeof(h0));
-  h0.tau = p->tol > 0.0 ? p->tol : -1.0;
-  h0.tau_b = p->tau_b;
-  h0.k_cap = k_cap;
-  h0.b = p->b;
-  *hA = h0;
-  CK(cudaMemcpyAsync(st, hA, sizeof(DevState), cudaMemcpyHostToDevice, s));
+  memset(hst, 0, sizeof(DevState));
+  hst->tau = p->tol > 0.0 ? p->tol : -1.0;
+  hst->tau_b = p->tau_b;
+  hst->k_cap = k_cap;
+  hst->b = p->b;
+  CK(cudaMemcpyAsync(c.st, hst, sizeof(DevState), cudaMemcpyHostToDevice, s));
 
   Prof prof;
   prof.on = rep && rep->profile;
   prof.s = s;
   int nl = 0, nproj = 0;
-#define LK(x) \
-  do {        \
-    ++nl;     \
-    CK(x);    \
-  } while (0)
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
   CK(cudaEventRecord(e0, s));
 
-  const int64_t chunk0 = p->row_offset / RBRP_CHUNK;
   // a0: d^(0), X_res <- X (Alg. 2 l.1-2)
   prof.begin(0);
-  LK(launch_init_norms<T>(X, p->ld, Xres, n, d, dvec, st, !inplace, s));
-  LK(launch_chunk_scan(dvec, n, chunk0, cpre, ctot, cpos, s));
+  ++nl;
+  CK(launch_init_norms<T>(c.X, p->ld, c.Xres, c.n, c.d, c.dvec, c.st, !inplace, s));
+  ++nl;
+  CK(launch_chunk_scan(c.dvec, c.n, c.chunk0, c.cpre, c.ctot, c.cpos, s));
   prof.end();
   if (comm) {
-    int rc = comm_allgather_chunks(comm, ctot, cpos, chunk0, (n + RBRP_CHUNK - 1) / RBRP_CHUNK, Ly.nchunks, s);
+    int rc = comm_allgather_chunks(comm, c.ctot, c.cpos, c.chunk0, (c.n + RBRP_CHUNK - 1) / RBRP_CHUNK,
+                                   Ly.nchunks, s);
     if (rc) return rc;
   }
 
+  // replay: the ids of block blk are staged into Srep; the sampler copies them to S_t
   int64_t replay_pos = 0;
   auto stage_replay = [&](int blk) -> int {
     if (!p->replay_nblocks) return -1;
     if (blk >= p->replay_nblocks) return -2;
     const int len = p->replay_lens[blk];
     if (len < 1 || len > p->b) return RBRP_EREPLAY - 1000;
+    if (cudaStreamSynchronize(s) != cudaSuccess) return RBRP_ECUDA - 1000;   // staging reuse
     for (int i = 0; i < len; ++i) {
       const int64_t id = p->replay_blocks[replay_pos + i];
       if (id < 0 || id >= p->n_global) return RBRP_EREPLAY - 1000;
       hSt[i] = id;
     }
-    if (cudaMemcpyAsync(St, hSt, len * 8, cudaMemcpyHostToDevice, s) != cudaSuccess)
+    if (cudaMemcpyAsync(c.Srep, hSt, len * 8, cudaMemcpyHostToDevice, s) != cudaSuccess)
       return RBRP_ECUDA - 1000;
     if (p->replay_pivots) {
       for (int i = 0; i < len; ++i) hpiv[i] = p->replay_pivots[replay_pos + i];
-      if (cudaMemcpyAsync(forced, hpiv, len * 4, cudaMemcpyHostToDevice, s) != cudaSuccess)
+      if (cudaMemcpyAsync(c.forced, hpiv, len * 4, cudaMemcpyHostToDevice, s) != cudaSuccess)
         return RBRP_ECUDA - 1000;
     }
     replay_pos += len;
-    // the staging buffers are reused below: wait for the copies
-    if (cudaStreamSynchronize(s) != cudaSuccess) return RBRP_ECUDA - 1000;
     return len;
   };
 
   SampleArgs sa;
-  sa.st = st;
-  sa.ctot = ctot;
-  sa.cpos = cpos;
-  sa.cprefix = cprefix;
+  memset(&sa, 0, sizeof(sa));
+  sa.st = c.st;
+  sa.ctot = c.ctot;
+  sa.cpos = c.cpos;
+  sa.cprefix = c.cprefix;
   sa.nchunks = (int)Ly.nchunks;
-  sa.cpre = cpre;
-  sa.dvec = dvec;
-  sa.n_local = n;
+  sa.cpre = c.cpre;
+  sa.dvec = c.dvec;
+  sa.n_local = c.n;
   sa.row_offset = p->row_offset;
-  sa.S_t = St;
+  sa.S_t = c.St;
+  sa.S_rep = c.Srep;
   sa.seed = p->seed;
   sa.first = 1;
+  sa.piv = c.piv;
+  sa.log = c.log;
+  sa.cond = 0;
   int rl = stage_replay(0);
   if (rl < -100) return rl + 1000;
   sa.replay_len = rl;
   prof.begin(1);
-  LK(launch_sample(sa, s));
+  ++nl;
+  CK(launch_sample(sa, s));
   prof.end();
-  CK(cudaMemcpyAsync(hB, st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(hst, c.st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  if (hB->nonfinite) return RBRP_ENONFINITE;
-  if (!(hB->D0 > 0.0)) return RBRP_EDEGENERATE;
+  if (hst->nonfinite) return RBRP_ENONFINITE;
+  if (!(hst->D0 > 0.0)) return RBRP_EDEGENERATE;
 
-  const int bucketB = bucket_of((int)std::min<int64_t>(p->b, k_cap));
-  const bool use_forced = p->replay_pivots != nullptr;
-  const bool use_mma = sizeof(T) == 8 && !force_simt() && projection_mma_supported(Xres, ldr, Qt, d);
-  int nblocks = 0;
-  while (!hB->stop) {
-    // a3: gather V = X_res(S_t,:)^T, Gram, pivoted Cholesky + filter (l.6-9)
-    prof.begin(2);
-    FilterArgs fa;
-    fa.st = st;
-    fa.X = Xres;
-    fa.ldx = ldr;
-    fa.Vg = nullptr;
-    if (comm) {
-      LK(launch_gather_rows<T>(Xres, ldr, St, n, p->row_offset, st, d, Vg, s));
-      int rc = comm_allreduce_f64(comm, Vg, (int64_t)RBRP_MAX_B * d, s);
+  sa.first = 0;
+  const bool eager = p->replay_nblocks > 0 || prof.on || stamps || comm || env_on("RBRP_NO_GRAPH");
+  GraphEntry* ge = nullptr;
+  if (!eager && !hst->stop) ge = get_graph<T>(c, sa, make_key(p, Xv, ws, c.use_mma));
+  if (ge) {
+    // the whole block loop as one graph launch (conditional WHILE node)
+    CK(cudaGraphLaunch(ge->exec, s));
+  } else {
+    int blk = 0;
+    while (!hst->stop) {
+      int rc = enqueue_block<T>(c, sa, s, prof.on ? &prof : nullptr, &nl, &nproj, false);
       if (rc) return rc;
-      fa.Vg = Vg;
-    }
-    fa.S_t = St;
-    fa.row_offset = p->row_offset;
-    fa.d = d;
-    fa.Gpart = Gpart;
-    fa.G = G;
-    fa.forced = use_forced ? forced : nullptr;
-    fa.piv = piv;
-    fa.mass = mass;
-    fa.R11 = R11;
-    fa.Tg = Tg;
-    fa.Ag = Ag;
-    fa.Rtot = Rtot;
-    fa.S = S;
-    fa.Qt = Qt;
-    fa.bp_pad = bucketB;
-    fa.dbg = dbg_stamps() ? (long long*)(ws + Ly.cand) : nullptr;
-    LK(launch_filter_coop<T>(fa, s));
-    prof.end();
-    // a4: projection + fused norms (l.13, l.16)
-    prof.begin(3);
-    for (int bk = 16; bk <= bucketB; bk *= 2) {
-      if (use_mma)
-        LK(launch_lhat_mma((const double*)Xres, ldr, (const double*)Qt, n, d, (double*)Lm, k_cap,
-                           st, bk, s));
-      else
-        LK(launch_lhat<T>(Xres, ldr, Qt, n, d, Lm, k_cap, st, bk, s));
-    }
-    prof.end();
-    prof.begin(4);
-    for (int bk = 16; bk <= bucketB; bk *= 2) {
-      if (use_mma)
-        LK(launch_update_mma((double*)Xres, ldr, (const double*)Qt, (const double*)Lm, k_cap, n, d,
-                             dvec, st, bk, s));
-      else
-        LK(launch_update<T>(Xres, ldr, Qt, Lm, k_cap, n, d, dvec, st, bk, s));
-    }
-    prof.end();
-    ++nproj;
-    prof.begin(5);
-    LK(launch_fixup<T>(Xres, ldr, dvec, Lm, k_cap, Rtot, S, n, p->row_offset, d, st, s));
-    LK(launch_chunk_scan(dvec, n, chunk0, cpre, ctot, cpos, s));
-    prof.end();
-    if (comm) {
-      int rc = comm_allgather_chunks(comm, ctot, cpos, chunk0, (n + RBRP_CHUNK - 1) / RBRP_CHUNK, Ly.nchunks, s);
-      if (rc) return rc;
-    }
-    // log this block before the next sample overwrites S_t
-    const bool logit = rep && nblocks < rep->max_blocks;
-    CK(cudaMemcpyAsync(hA, st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
-    if (logit && (rep->block_idx || rep->block_piv)) {
-      CK(cudaMemcpyAsync(hSt, St, RBRP_MAX_B * 8, cudaMemcpyDeviceToHost, s));
-      CK(cudaMemcpyAsync(hpiv, piv, RBRP_MAX_B * 4, cudaMemcpyDeviceToHost, s));
+      ++blk;
+      rl = stage_replay(blk);
+      if (rl < -100) return rl + 1000;
+      sa.replay_len = rl;
+      prof.begin(1);
+      ++nl;
+      CK(launch_sample(sa, s));
+      prof.end();
+      CK(cudaMemcpyAsync(hst, c.st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
-      const int bt = hA->b_t;
-      for (int i = 0; i < p->b; ++i) {
-        if (rep->block_idx) rep->block_idx[(int64_t)nblocks * p->b + i] = i < bt ? hSt[i] : -1;
-        if (rep->block_piv) rep->block_piv[(int64_t)nblocks * p->b + i] = i < bt ? hpiv[i] : -1;
+      if (stamps) {
+        long long t[10];
+        if (cudaMemcpy(t, c.dbg, sizeof(t), cudaMemcpyDeviceToHost) == cudaSuccess) {
+          fprintf(stderr, "rbrp filter phases (us):");
+          for (int i = 1; i < 10; ++i) fprintf(stderr, " %.2f", (t[i] - t[0]) * 1e-3);
+          fprintf(stderr, "\n");
+        }
       }
     }
-    // next block: stop test + sample (l.3-5)
-    rl = stage_replay(nblocks + 1);
-    if (rl < -100) return rl + 1000;
-    sa.replay_len = rl;
-    sa.first = 0;
-    prof.begin(1);
-    LK(launch_sample(sa, s));
-    prof.end();
-    CK(cudaMemcpyAsync(hB, st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    if (dbg_stamps()) {   // diagnostics: phase stamps of this block's filter call (ns)
-      long long t[11];
-      if (cudaMemcpy(t, ws + Ly.cand, sizeof(t), cudaMemcpyDeviceToHost) == cudaSuccess) {
-        fprintf(stderr, "rbrp filter b_t=%d b'=%d phases (us):", hA->b_t, hA->b_prime);
-        for (int i = 1; i < 11; ++i) fprintf(stderr, " %.2f", (t[i] - t[0]) * 1e-3);
-        fprintf(stderr, "\n");
-      }
-    }
-    if (logit) {
-      if (rep->b_t) rep->b_t[nblocks] = hA->b_t;
-      if (rep->b_prime) rep->b_prime[nblocks] = hA->b_prime;
-      if (rep->rho) rep->rho[nblocks] = hB->total / hB->D0;
-    }
-    ++nblocks;
   }
 
-  const int64_t k = hB->k;
+  // read the state (k, flags) before W
+  CK(cudaMemcpyAsync(hst, c.st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const int64_t k = hst->k;
+  const int nblocks = std::min(hst->t, Ly.maxlog);
+  if (ge) {
+    nl += ge->launches_per_block * hst->t;
+    nproj += hst->t;
+  }
   // a6: W (Alg. 3)
   if (!(p->flags & RBRP_NO_W) && W_out && k > 0) {
     double* L1 = (double*)(ws + Ly.L1);
     T* LinvT = (T*)(ws + Ly.LinvT);
     prof.begin(6);
-    LK(launch_gather_L1<T>(Lm, k_cap, S, k, n, p->row_offset, L1, s));
+    ++nl;
+    CK(launch_gather_L1<T>(c.Lm, k_cap, c.S, k, c.n, p->row_offset, L1, s));
     if (comm) {
       int rc = comm_allreduce_f64(comm, L1, k * k, s);
       if (rc) return rc;
     }
-    LK(launch_trinv<T>(L1, k, LinvT, st, s));
+    ++nl;
+    CK(launch_trinv<T>(L1, k, LinvT, c.st, s));
     cudaError_t merr = cudaSuccess;
+    ++nl;
     if (sizeof(T) == 8 && !force_simt() &&
-        gemm_nt_mma((const double*)Lm, k_cap, (const double*)LinvT, k, (double*)W_out, k_cap, n, k,
+        gemm_nt_mma((const double*)c.Lm, k_cap, (const double*)LinvT, k, (double*)W_out, k_cap, c.n, k,
                     k, s, &merr)) {
-      ++nl;
       CK(merr);
     } else {
-      LK(launch_gemm_nt<T>(Lm, k_cap, LinvT, k, (T*)W_out, k_cap, n, k, k, s));
+      CK(launch_gemm_nt<T>(c.Lm, k_cap, LinvT, k, (T*)W_out, k_cap, c.n, k, k, s));
     }
-    LK(launch_w_identity<T>((T*)W_out, k_cap, S, k, n, p->row_offset, s));
+    ++nl;
+    CK(launch_w_identity<T>((T*)W_out, k_cap, c.S, k, c.n, p->row_offset, s));
     prof.end();
   }
-  CK(cudaMemcpyAsync(hS, S, (size_t)std::max<int64_t>(k, 1) * 8, cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(hB, st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+  int64_t* hS = (int64_t*)(hp + o_S);
+  CK(cudaMemcpyAsync(hS, c.S, (size_t)std::max<int64_t>(k, 1) * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(hst, c.st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+  const int nlog = std::max(nblocks, 1);
+  CK(cudaMemcpyAsync(hp + o_bt, c.log.bt, nlog * 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(hp + o_bp, c.log.bp, nlog * 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(hp + o_rho, c.log.rho, nlog * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(hp + o_ts, c.log.ts, nlog * 16, cudaMemcpyDeviceToHost, s));
+  const bool want_blocks = rep && (rep->block_idx || rep->block_piv);
+  if (want_blocks) {
+    CK(cudaMemcpyAsync(hp + o_lSt, c.log.St, (size_t)nlog * b * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hp + o_lpiv, c.log.piv, (size_t)nlog * b * 4, cudaMemcpyDeviceToHost, s));
+  }
   CK(cudaEventRecord(e1, s));
   CK(cudaStreamSynchronize(s));
   float ms = 0.f;
@@ -423,17 +610,37 @@ int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* 
   memcpy(S_out, hS, (size_t)k * 8);
   if (rep) {
     rep->k = k;
-    rep->fro2 = hB->D0;
-    rep->resid_rel = hB->total / hB->D0;
-    rep->nblocks = nblocks;
-    rep->flags = hB->flags;
+    rep->fro2 = hst->D0;
+    rep->resid_rel = hst->total / hst->D0;
+    rep->nblocks = hst->t;
+    rep->flags = hst->flags;
     rep->ms_total = ms;
     for (int i = 0; i < 8; ++i) rep->ms_phase[i] = 0.f;
     prof.collect(rep->ms_phase);
     rep->launches = nl;
     rep->proj_calls = nproj;
+    const int32_t* lbt = (const int32_t*)(hp + o_bt);
+    const int32_t* lbp = (const int32_t*)(hp + o_bp);
+    const double* lrho = (const double*)(hp + o_rho);
+    const long long* lts = (const long long*)(hp + o_ts);
+    const int64_t* lSt = (const int64_t*)(hp + o_lSt);
+    const int32_t* lpiv = (const int32_t*)(hp + o_lpiv);
+    double proj = 0.0;
+    for (int t = 0; t < nblocks; ++t) {
+      if (lbp[t] > 0 && lts[2 * t + 1] > lts[2 * t]) proj += (lts[2 * t + 1] - lts[2 * t]) * 1e-6;
+      if (t < rep->max_blocks) {
+        if (rep->b_t) rep->b_t[t] = lbt[t];
+        if (rep->b_prime) rep->b_prime[t] = lbp[t];
+        if (rep->rho) rep->rho[t] = lrho[t];
+        for (int i = 0; want_blocks && i < b; ++i) {
+          if (rep->block_idx) rep->block_idx[(int64_t)t * b + i] = lSt[(int64_t)t * b + i];
+          if (rep->block_piv) rep->block_piv[(int64_t)t * b + i] = lpiv[(int64_t)t * b + i];
+        }
+      }
+    }
+    rep->proj_ms = (float)proj;
+    rep->graph = ge ? 1 : 0;
   }
-#undef LK
   return RBRP_OK;
 }
 

@@ -50,7 +50,8 @@ class Report(ctypes.Structure):
                 ("block_idx", ctypes.POINTER(ctypes.c_int64)),
                 ("block_piv", ctypes.POINTER(ctypes.c_int32)), ("ms_total", ctypes.c_float),
                 ("profile", ctypes.c_int32), ("ms_phase", ctypes.c_float * 8),
-                ("launches", ctypes.c_int32), ("proj_calls", ctypes.c_int32)]
+                ("launches", ctypes.c_int32), ("proj_calls", ctypes.c_int32),
+                ("proj_ms", ctypes.c_float), ("graph", ctypes.c_int32)]
 
 PHASES = ["init", "sample", "filter", "lhat", "update", "fixup_scan", "W", "comm"]
 
@@ -106,6 +107,8 @@ class Result:
     ms_phase: dict                  # per-phase device ms (profile=True)
     launches: int                   # kernels launched by the call
     proj_calls: int
+    proj_ms: float                  # device time of the projection passes (in-kernel stamps)
+    graph: bool                     # block loop ran as one CUDA graph launch
 
 
 def _problem(X: torch.Tensor, tol, k, b, seed, k_max, tau_b, flags, n_global, row_offset, greedy):
@@ -153,13 +156,14 @@ def id(X: torch.Tensor, tol: Optional[float] = None, k: Optional[int] = None, b:
        replay_pivots: Optional[Sequence[Sequence[int]]] = None,
        max_blocks: int = 1024, log_blocks: bool = True, workspace: Optional[torch.Tensor] = None,
        comm=None, n_global: Optional[int] = None, row_offset: int = 0,
-       profile: bool = False) -> Result:
+       profile: bool = False, W_out: Optional[torch.Tensor] = None) -> Result:
     """RBRP interpolative decomposition X ~ W X_S of a CUDA tensor X (n x d).
 
     tol: tau, relative to ||X||_F^2 (for an (r, eps)-ID pass tol = (1+eps) eta_r,
     PAPER.md l.86); or k: fixed rank.  b: block size; seed: Philox key;
     tau_b < 0 -> 1/b_t.  Returns S (CPU int64, selection order), W (device,
-    n x k, W[S] = I) and the per-block log."""
+    n x k, W[S] = I) and the per-block log.  workspace / W_out: optional
+    preallocated buffers (W_out: n x k_cap, k_cap = k or k_max or min(n, d))."""
     if not X.is_cuda:
         raise ValueError("X must be a CUDA tensor (use id_host for host buffers)")
     if tol is None and k is None:
@@ -189,7 +193,15 @@ def id(X: torch.Tensor, tol: Optional[float] = None, k: Optional[int] = None, b:
     if workspace is None or workspace.numel() < sz.value:
         workspace = torch.empty(sz.value, dtype=torch.uint8, device=X.device)
     k_cap = p.k_max if p.k_max > 0 else min(p.n_global, p.d)
-    W = torch.empty((X.shape[0], k_cap), dtype=X.dtype, device=X.device) if with_W else None
+    W = None
+    if with_W:
+        if W_out is not None:
+            if (W_out.shape != (X.shape[0], k_cap) or W_out.dtype != X.dtype or not W_out.is_contiguous()
+                    or W_out.device != X.device):
+                raise ValueError(f"W_out must be a contiguous {(X.shape[0], k_cap)} {X.dtype} tensor on {X.device}")
+            W = W_out
+        else:
+            W = torch.empty((X.shape[0], k_cap), dtype=X.dtype, device=X.device)
     S = torch.empty(k_cap, dtype=torch.int64)
     rep = Report()
     mb = max_blocks
@@ -227,17 +239,27 @@ def id(X: torch.Tensor, tol: Optional[float] = None, k: Optional[int] = None, b:
                   b_t=list(b_t[:nb]), b_prime=list(b_pr[:nb]), rho=list(rho[:nb]),
                   blocks=blocks, pivots=pivots, ms=rep.ms_total,
                   ms_phase={nm: rep.ms_phase[i] for i, nm in enumerate(PHASES)},
-                  launches=rep.launches, proj_calls=rep.proj_calls)
+                  launches=rep.launches, proj_calls=rep.proj_calls, proj_ms=rep.proj_ms,
+                  graph=bool(rep.graph))
 
 
-def id_host(X_host: torch.Tensor, device="cuda", **kw):
-    """End-to-end entry with a HOST input: copies X (pinned host -> HBM), runs
-    id(), and copies W back to pinned host memory.  Returns (Result, W_host)."""
-    Xd = X_host.to(device, non_blocking=True)
-    res = id(Xd, **kw)
-    W_host = None
+def id_host(X_host: torch.Tensor, device="cuda", X_dev: Optional[torch.Tensor] = None,
+            W_host: Optional[torch.Tensor] = None, **kw):
+    """End-to-end entry with a HOST input: copies X (pinned host -> HBM) on the
+    current stream, runs id(), and copies W (n x k) back to host memory.
+    X_dev / W_host: optional preallocated device copy of X and pinned host
+    output (n x k_cap).  Returns (Result, W_host view n x k)."""
+    if X_dev is None:
+        X_dev = torch.empty(X_host.shape, dtype=X_host.dtype, device=device)
+    X_dev.copy_(X_host, non_blocking=True)
+    res = id(X_dev, **kw)
+    Wh = None
     if res.W is not None:
-        W_host = torch.empty(res.W.shape, dtype=res.W.dtype, pin_memory=True)
-        W_host.copy_(res.W, non_blocking=True)
-    torch.cuda.current_stream(Xd.device).synchronize()
-    return res, W_host
+        if W_host is None:
+            W_host = torch.empty(res.W.shape, dtype=res.W.dtype, pin_memory=True)
+            Wh = W_host
+        else:
+            Wh = W_host[:, :res.k]
+        Wh.copy_(res.W, non_blocking=True)
+    torch.cuda.current_stream(X_dev.device).synchronize()
+    return res, Wh

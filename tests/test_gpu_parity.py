@@ -244,3 +244,23 @@ def test_simt_and_mma_projection_paths_agree(monkeypatch):
     monkeypatch.setenv("RBRP_FORCE_SIMT", "0")
     b = _replay(Xnp, ores, np.float64, 16)
     assert a.S.tolist() == b.S.tolist()
+
+
+@cuda
+def test_graph_loop_equals_eager_loop(monkeypatch):
+    """The block loop as one CUDA graph (conditional WHILE node) and the eager,
+    host-driven loop launch the same kernels: identical S, b', rho and W."""
+    rb = _rb()
+    cfg = small_config("c2", n=20000, d=512, rank=70, b=32)
+    X = make(cfg, device="cuda")
+    g1 = rb.id(X, tol=1e-12, b=32, seed=3)
+    g2 = rb.id(X, tol=1e-12, b=32, seed=3)          # cached graph
+    monkeypatch.setenv("RBRP_NO_GRAPH", "1")
+    e = rb.id(X, tol=1e-12, b=32, seed=3)
+    assert g1.graph and g2.graph and not e.graph
+    for g in (g1, g2):
+        assert g.S.tolist() == e.S.tolist() and g.k == 70
+        assert g.b_prime == e.b_prime and g.rho == e.rho
+        assert torch.equal(g.W, e.W)
+        assert g.blocks == e.blocks
+    assert g1.proj_ms > 0
