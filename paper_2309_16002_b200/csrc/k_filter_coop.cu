@@ -118,6 +118,164 @@ __device__ int cta_pivchol(double* A, int lda, int nb, int mode, const int32_t* 
   return kept;
 }
 
+// Fast path for nb <= 64: pivoted (mode 1) or plain (mode 2) Cholesky AND T = R11^{-1},
+// right-looking, logical pivoting, each thread owning EPT fixed elements (r, c) of
+//   A(r, c)    the Schur complement (in registers), and
+//   acc(j, l)  sum_{q < i} T(j, q) R(q, l)  (in registers),
+// so that at step i with pivot p:  R(i, l) = A(p, l) / sqrt(A(p,p)) by the owners of row
+// p, T(j, i) = -acc(j, p) / R(i, p) (j < i) by the owners of column p, then the rank-1
+// update A -= R(i,.)^T R(i,.) and acc(j, .) += T(j, i) R(i, .).  Every warp finds the
+// pivot itself from the shared Schur diagonal (identical, deterministic), so a step costs
+// two barriers.  Pivot / mass / cut rules as cta_pivchol.  R: [step][orig] (ld), T:
+// [step][step] (ldt).
+template <int EPT>
+__device__ int cta_chol_inv(const double* __restrict__ Gg, int nb, int mode, const int32_t* forced,
+                            double tau_b, double* R, int ld, double* Tm, int ldt, int* perm,
+                            double* mass, double* dg, int* chosen_unused, int* rank_def) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  int er[EPT], ec[EPT];
+  double a[EPT], ta[EPT];
+#pragma unroll
+  for (int k = 0; k < EPT; ++k) {
+    const int e = tid + k * blockDim.x;
+    if (e < nb * nb) {
+      er[k] = e / nb;
+      ec[k] = e - er[k] * nb;
+      a[k] = Gg[er[k] * kMaxB + ec[k]];
+      if (er[k] == ec[k]) dg[er[k]] = a[k];
+    } else {
+      er[k] = -1;
+      ec[k] = -1;
+      a[k] = 0.0;
+    }
+    ta[k] = 0.0;
+  }
+  for (int e = tid; e < nb * ldt; e += blockDim.x) Tm[e] = 0.0;
+  if (tid == 0) *rank_def = 0;
+  __syncthreads();
+  unsigned long long chosen = 0ull;   // identical in every thread
+  double thr = 0.0;
+  int kept = nb;
+  for (int i = 0; i < nb; ++i) {
+    // every warp: residual mass (fixed order) and pivot (max, ties -> lowest index)
+    double ms = 0.0, best = -DBL_MAX;
+    int bl = 1 << 30;
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      const int l = lane + 32 * m;
+      if (l < nb && !((chosen >> l) & 1ull)) {
+        const double x = dg[l];
+        ms += fmax(x, 0.0);
+        if (x > best) { best = x; bl = l; }
+      }
+    }
+    ms = warp_sum(ms);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+      if (ob > best || (ob == best && ol < bl)) { best = ob; bl = ol; }
+    }
+    if (i == 0) thr = tau_b * ms;
+    int cut = 0;
+    if (mode == 1 && (!(ms > 0.0) || ms < thr)) cut = 1;            // l.8 cut
+    int p = bl;
+    if (mode == 2) p = i;
+    if (mode == 1 && forced) p = forced[i];
+    const double dp = dg[p];
+    if (!cut && !(dp > 0.0)) cut = 2;                               // non-positive pivot
+    if (tid == 0 && mode == 1) mass[i] = ms;
+    if (cut) {
+      if (tid == 0 && cut == 2) *rank_def = 1;
+      kept = i;
+      break;
+    }
+    const double rii = sqrt(dp);
+    const double inv = 1.0 / rii;
+    if (tid == 0) {
+      perm[i] = p;
+      Tm[i * ldt + i] = inv;
+    }
+#pragma unroll
+    for (int k = 0; k < EPT; ++k) {
+      const int c = ec[k];
+      const double rv = a[k] * inv, tv = -ta[k] * inv;   // computed by every lane
+      if (er[k] == p) R[i * ld + c] = (c == p) ? rii : (((chosen >> c) & 1ull) ? 0.0 : rv);
+      if (c == p && er[k] < i) Tm[er[k] * ldt + i] = tv;
+    }
+    chosen |= 1ull << p;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < EPT; ++k) {
+      const int r = er[k], c = ec[k];
+      if (r < 0) continue;
+      const double ric = R[i * ld + c];
+      a[k] = fma(-R[i * ld + r], ric, a[k]);
+      if (r == c) dg[r] = a[k];
+      if (r <= i) ta[k] = fma(Tm[r * ldt + i], ric, ta[k]);
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  return kept;
+}
+
+// small dense helpers on n x n shared-memory matrices (stride ld), all threads
+__device__ void sm_upper_phi(const double* M, double* U, int n, int ld) {   // U = Phi(M)
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int i = e / n, j = e - (e / n) * n;
+    U[i * ld + j] = i < j ? M[i * ld + j] : (i == j ? 0.5 * M[i * ld + j] : 0.0);
+  }
+}
+// C = E - U^T U  (U upper)
+__device__ void sm_e_minus_utu(const double* E, const double* U, double* C, int n, int ld) {
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int i = e / n, j = e - (e / n) * n;
+    const int m = i < j ? i : j;
+    double s = 0.0;
+    for (int k = 0; k <= m; ++k) s = fma(U[k * ld + i], U[k * ld + j], s);
+    C[i * ld + j] = E[i * ld + j] - s;
+  }
+}
+// C = A B (A, B upper)
+__device__ void sm_upper_mul(const double* A, const double* B, double* C, int n, int ld) {
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int i = e / n, j = e - (e / n) * n;
+    double s = 0.0;
+    for (int k = i; k <= j; ++k) s = fma(A[i * ld + k], B[k * ld + j], s);
+    C[i * ld + j] = i <= j ? s : 0.0;
+  }
+}
+
+// CholQR2 second pass for G2 = I + E with small E: R2 = I + U, U the fixed point of
+// U = Phi(E - U^T U) (two steps from Phi(E): error O(|E|^4)), T2 = R2^{-1} =
+// I - U + U^2 - U^3 (error O(|U|^4)).  Parallel; used when max|E| < 1e-5, otherwise
+// the caller runs the exact Cholesky.  E (destroyed), R, Tm, W: n x n, stride ld; R
+// doubles as scratch.  Writes R2 (upper) into R and T2 into Tm.
+__device__ void cholqr2_perturb(double* E, double* R, double* Tm, double* W, int n, int ld) {
+  sm_upper_phi(E, W, n, ld);                  // U0
+  __syncthreads();
+  sm_e_minus_utu(E, W, R, n, ld);
+  __syncthreads();
+  sm_upper_phi(R, W, n, ld);                  // U1
+  __syncthreads();
+  sm_e_minus_utu(E, W, R, n, ld);
+  __syncthreads();
+  sm_upper_phi(R, W, n, ld);                  // U2 = U
+  __syncthreads();
+  sm_upper_mul(W, W, R, n, ld);               // U^2 (in R)
+  __syncthreads();
+  sm_upper_mul(R, W, E, n, ld);               // U^3 (in E)
+  __syncthreads();
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int i = e / n, j = e - (e / n) * n;
+    const double u = W[i * ld + j], u2 = R[i * ld + j], u3 = E[i * ld + j], id = (i == j ? 1.0 : 0.0);
+    Tm[i * ld + j] = id - u + u2 - u3;
+    R[i * ld + j] = id + u;
+  }
+  __syncthreads();
+}
+
 // T = R11^{-1} for the upper-triangular R11(j, c) = R(j, perm[c]) (step order), one
 // thread per column c: T(c,c) = 1/R11(c,c); T(j,c) = -(sum_{j<q<=c} R11(j,q) T(q,c)) / R11(j,j).
 __device__ void cta_trinv(const double* R, int ldr, const int* perm, int bp, double* Tm, int ldt) {
@@ -197,7 +355,7 @@ __device__ __forceinline__ void stamp(long long* dbg, int k) {
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kFiltThreads) k_filter_coop(FilterArgs F) {
+__global__ void __launch_bounds__(kFiltThreads, 1) k_filter_coop(FilterArgs F) {
   cg::grid_group grid = cg::this_grid();
   stamp(F.dbg, 0);
   extern __shared__ double smd[];
@@ -255,22 +413,30 @@ __global__ void __launch_bounds__(kFiltThreads) k_filter_coop(FilterArgs F) {
   reduce_slices(F.Gpart, nsplit, nb, F.G);
   grid.sync();
   stamp(F.dbg, 3);
-  // C: pivoted Cholesky + filter (redundant in every CTA; the large case works on G in
-  // L2 and keeps T in a per-CTA global scratch)
+  // C: pivoted Cholesky + filter + T11 = R11^{-1} (redundant in every CTA).  b_t <= 64:
+  // register-resident fast path; larger blocks: shared/L2 path + column-parallel inverse.
   if (!small) {
     Ts = F.Tg + (int64_t)blockIdx.x * kMaxB * kMaxB;
     Gs = F.Ag + (int64_t)blockIdx.x * kMaxB * kMaxB;
   }
-  for (int e = tid; e < nb * nb; e += kFiltThreads) Gs[(e / nb) * ldg + e % nb] = F.G[(e / nb) * kMaxB + e % nb];
-  __syncthreads();
   {
     const double tb = st->tau_b < 0.0 ? 1.0 / nb : st->tau_b;
-    const int kept = cta_pivchol(Gs, ldg, nb, 1, F.forced, tb, Rs, ldr, perm, s_mass, s_dg, s_ch, &s_rd);
+    int kept;
+    if (nb <= 32) {
+      kept = cta_chol_inv<4>(F.G, nb, 1, F.forced, tb, Rs, ldr, Ts, ldt, perm, s_mass, s_dg, s_ch, &s_rd);
+    } else if (small) {
+      kept = cta_chol_inv<16>(F.G, nb, 1, F.forced, tb, Rs, ldr, Ts, ldt, perm, s_mass, s_dg, s_ch, &s_rd);
+    } else {
+      for (int e = tid; e < nb * nb; e += kFiltThreads) Gs[(e / nb) * ldg + e % nb] = F.G[(e / nb) * kMaxB + e % nb];
+      __syncthreads();
+      kept = cta_pivchol(Gs, ldg, nb, 1, F.forced, tb, Rs, ldr, perm, s_mass, s_dg, s_ch, &s_rd);
+      __syncthreads();
+      cta_trinv(Rs, ldr, perm, kept, Ts, ldt);
+    }
     if (tid == 0) s_kept = kept;
   }
   __syncthreads();
   const int bp = s_kept;
-  cta_trinv(Rs, ldr, perm, bp, Ts, ldt);
   stamp(F.dbg, 4);
   // R11 (step order) and the bookkeeping of l.8-9
   for (int e = tid; e < bp * bp; e += kFiltThreads) {
@@ -307,16 +473,42 @@ __global__ void __launch_bounds__(kFiltThreads) k_filter_coop(FilterArgs F) {
   reduce_slices(F.Gpart, nsplit, bp, F.G);
   grid.sync();
   stamp(F.dbg, 7);
-  // F: CholQR2 pass (R2 into Rs, T2 into Ts)
-  for (int e = tid; e < bp * bp; e += kFiltThreads) Gs[(e / bp) * ldg + e % bp] = F.G[(e / bp) * kMaxB + e % bp];
-  __syncthreads();
-  {
-    int rd2;
-    const int kept = cta_pivchol(Gs, ldg, bp, 2, nullptr, 0.0, Rs, ldr, perm2, nullptr, s_dg, s_ch, &rd2);
+  // F: CholQR2 pass (R2 into Rs, T2 = R2^{-1} into Ts).  G2 = I + E: if max|E| is small
+  // (the usual case) a parallel perturbation expansion, else the exact Cholesky.
+  __shared__ double s_emax;
+  if (small) {
+    double em = 0.0;
+    for (int e = tid; e < bp * bp; e += kFiltThreads) {
+      const int i = e / bp, j = e - (e / bp) * bp;
+      const double x = F.G[i * kMaxB + j] - (i == j ? 1.0 : 0.0);
+      Gs[i * ldg + j] = x;
+      em = fmax(em, fabs(x));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) em = fmax(em, __shfl_xor_sync(0xffffffffu, em, o));
+    if (tid == 0) s_emax = 0.0;
+    __syncthreads();
+    if ((tid & 31) == 0) atomicMax((unsigned long long*)&s_emax, (unsigned long long)__double_as_longlong(em));
+    __syncthreads();
+  }
+  if (small && s_emax < 1e-5) {
+    cholqr2_perturb(Gs, Rs, Ts, Vs, bp, ldr);
+    if (tid == 0) s_kept = bp;
+  } else {
+    int rd2, kept;
+    if (bp <= 32) {
+      kept = cta_chol_inv<4>(F.G, bp, 2, nullptr, 0.0, Rs, ldr, Ts, ldt, perm2, nullptr, s_dg, s_ch, &rd2);
+    } else if (small) {
+      kept = cta_chol_inv<16>(F.G, bp, 2, nullptr, 0.0, Rs, ldr, Ts, ldt, perm2, nullptr, s_dg, s_ch, &rd2);
+    } else {
+      for (int e = tid; e < bp * bp; e += kFiltThreads) Gs[(e / bp) * ldg + e % bp] = F.G[(e / bp) * kMaxB + e % bp];
+      __syncthreads();
+      kept = cta_pivchol(Gs, ldg, bp, 2, nullptr, 0.0, Rs, ldr, perm2, nullptr, s_dg, s_ch, &rd2);
+      __syncthreads();
+      cta_trinv(Rs, ldr, perm2, kept, Ts, ldt);
+    }
     if (tid == 0) s_kept = kept;
   }
-  __syncthreads();
-  cta_trinv(Rs, ldr, perm2, s_kept, Ts, ldt);
   const int bq = s_kept;   // normally bp; smaller only if G2 lost definiteness
   stamp(F.dbg, 8);
   if (blockIdx.x == 0) {

@@ -13,6 +13,8 @@
 // In k_nt_mma an A-row segment x[2q, 2q+1] (one 16-byte load) feeds two MMAs whose K
 // index is permuted as k = 2q + h; the B fragments are read with the same permutation
 // (one 16-byte shared load gives both), so no shuffles are needed.
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "launch.cuh"
@@ -35,46 +37,43 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 constexpr int kMmaWarps = 8;
-constexpr int kKC = 64;                   // K (columns) per staged chunk
-constexpr int kXld = kKC + 8;             // X tile stride (doubles), = 8 mod 16: LDS.128 conflict-free
-constexpr int kBld = kKC + 8;             // B tile stride for 16-byte B loads (k_nt_mma)
-constexpr int kQld = kKC + 4;             // Q tile stride for 8-byte B loads (k_update_mma), = 4 mod 16
 
-// RG row groups of 8 rows per warp: every B (Q) fragment read from shared memory feeds
-// RG MMAs, which halves the shared-memory traffic per MMA at RG = 2.
-template <int BN> struct NtCfg {
-  static constexpr int RG = BN == 128 ? 1 : 2;
-  static constexpr int ROWS = 8 * RG * kMmaWarps;                        // rows per tile
-  static constexpr int NS = 2;                                           // pipeline stages
-  static constexpr int STAGE = ROWS * kXld + BN * kBld;                  // doubles per stage
-  static constexpr size_t SMEM = sizeof(double) * NS * STAGE;
-};
-template <int BP> struct UpdCfg {
-  static constexpr int RG = BP == 128 ? 1 : 2;
+// Tile configuration: RG row groups of 8 rows per warp (each B fragment read from shared
+// memory feeds RG MMAs), KC-column K chunks through an NS-stage cp.async pipeline
+// (NS = as many stages as fit in ~200 KB, at most 4).  Strides: X / B tiles = KC + 8
+// doubles (= 8 mod 16: conflict-free 16-byte fragment loads), Q tiles for 8-byte loads =
+// KC + 4 (= 4 mod 16: conflict-free per half-warp).
+template <int BN, int RG_, int KC_, bool UPD>
+struct PCfg {
+  static constexpr int RG = RG_;
+  // fall back to 32-column chunks when two stages of the requested tile do not fit
+  static constexpr int KC = (8 * RG_ * kMmaWarps * (KC_ + 8) + BN * (KC_ + 8)) * 8 * 2 > 200 * 1024 ? 32 : KC_;
+  static constexpr int XLD = KC + 8;
+  static constexpr int BLD = UPD ? KC + 4 : KC + 8;
   static constexpr int ROWS = 8 * RG * kMmaWarps;
-  static constexpr int NS = 2;
-  static constexpr int STAGE = ROWS * kXld + BP * kQld;
+  static constexpr int STAGE = ROWS * XLD + BN * BLD;
+  static constexpr int NSF = (200 * 1024) / (STAGE * 8);
+  static constexpr int NS = NSF < 4 ? NSF : 4;
   static constexpr size_t SMEM = sizeof(double) * NS * STAGE;
+  static_assert(NS >= 2, "tile too large");
 };
 
-// X tile rows [r0, r0+ROWS) x columns [c0, c0+64) -> xs (zero-filled outside [0,M) x [0,K))
-template <int ROWS>
+template <int ROWS, int KC, int XLD>
 __device__ __forceinline__ void stage_x(double* xs, const double* __restrict__ A, int64_t lda,
                                         int64_t r0, int64_t M, int64_t c0, int64_t K, int tid) {
 #pragma unroll
-  for (int i = 0; i < (ROWS * kKC / 2) / (32 * kMmaWarps); ++i) {
+  for (int i = 0; i < (ROWS * KC / 2) / (32 * kMmaWarps); ++i) {
     const int e = tid + i * 32 * kMmaWarps;
-    const int r = e / (kKC / 2), c = (e % (kKC / 2)) * 2;
+    const int r = e / (KC / 2), c = (e % (KC / 2)) * 2;
     const bool ok = (r0 + r < M) && (c0 + c < K);
-    cp_async16(xs + r * kXld + c, ok ? A + (r0 + r) * lda + c0 + c : A, ok);
+    cp_async16(xs + r * XLD + c, ok ? A + (r0 + r) * lda + c0 + c : A, ok);
   }
 }
-// rows [0, BN) of B (rows >= nrows zero) x columns [c0, c0+64)
-template <int BN, int LD>
+template <int BN, int KC, int LD>
 __device__ __forceinline__ void stage_b(double* bs, const double* __restrict__ B, int64_t ldb,
                                         int64_t n0, int64_t nrows, int64_t c0, int64_t K, int tid) {
-  for (int e = tid; e < BN * (kKC / 2); e += 32 * kMmaWarps) {
-    const int j = e / (kKC / 2), c = (e % (kKC / 2)) * 2;
+  for (int e = tid; e < BN * (KC / 2); e += 32 * kMmaWarps) {
+    const int j = e / (KC / 2), c = (e % (KC / 2)) * 2;
     const bool ok = (n0 + j < nrows) && (c0 + c < K);
     cp_async16(bs + j * LD + c, ok ? B + (n0 + j) * ldb + c0 + c : B, ok);
   }
@@ -82,19 +81,19 @@ __device__ __forceinline__ void stage_b(double* bs, const double* __restrict__ B
 
 // ---------------------------------------------------------------------------------
 // C = A B^T: ROWS-row tiles x BN columns; persistent CTAs (one per SM) walk their tiles
-// and the 64-column K chunks of each tile as ONE flattened sequence, so the cp.async
+// and the 32-column K chunks of each tile as ONE flattened sequence, so the cp.async
 // pipeline never drains between tiles.  Warp w owns rows [w*8*RG, (w+1)*8*RG) of a tile.
 // Requirements (checked by the launcher): K % 8 == 0, lda % 2 == 0, ldb % 2 == 0,
 // 16-byte aligned A and B.
 // ---------------------------------------------------------------------------------
-template <int BN>
+template <int BN, int RG_, int KC_>
 __global__ void __launch_bounds__(32 * kMmaWarps, 1) k_nt_mma(const double* __restrict__ A, int64_t lda,
                                                               const double* __restrict__ B, int64_t ldb,
                                                               double* __restrict__ C, int64_t ldc,
                                                               int64_t M, int64_t N, int64_t K,
                                                               DevState* st, int mode) {
-  using Cf = NtCfg<BN>;
-  constexpr int RG = Cf::RG;
+  using Cf = PCfg<BN, RG_, KC_, false>;
+  constexpr int RG = Cf::RG, kKC = Cf::KC, kXld = Cf::XLD, kBld = Cf::BLD;
   extern __shared__ __align__(16) double sm[];
   int64_t col0 = 0, Nn = N;
   if (mode == 1) {   // L-hat: N = b', columns written at L[:, k + j]
@@ -124,8 +123,8 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 1) k_nt_mma(const double* __re
       tile_of(it / nchunk, r0, n0);
       const int64_t k0 = (it % nchunk) * kKC;
       double* base = sm + (size_t)(it % Cf::NS) * Cf::STAGE;
-      stage_x<Cf::ROWS>(base, A, lda, r0, M, k0, K, tid);
-      stage_b<BN, kBld>(base + Cf::ROWS * kXld, B, ldb, n0, Nn, k0, K, tid);
+      stage_x<Cf::ROWS, kKC, kXld>(base, A, lda, r0, M, k0, K, tid);
+      stage_b<BN, kKC, kBld>(base + Cf::ROWS * kXld, B, ldb, n0, Nn, k0, K, tid);
     }
     cp_async_commit();
   };
@@ -144,19 +143,22 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 1) k_nt_mma(const double* __re
     const double* bs = xs + Cf::ROWS * kXld;
 #pragma unroll
     for (int s = 0; s < kKC / 8; ++s) {
-      double2 xa[RG];
+      double2 xa[RG], b[BN / 8];
 #pragma unroll
       for (int r = 0; r < RG; ++r)
         xa[r] = *reinterpret_cast<const double2*>(xs + ((w * RG + r) * 8 + g) * kXld + 8 * s + 2 * q);
 #pragma unroll
-      for (int t = 0; t < BN / 8; ++t) {
-        const double2 b = *reinterpret_cast<const double2*>(bs + (t * 8 + g) * kBld + 8 * s + 2 * q);
+      for (int t = 0; t < BN / 8; ++t)
+        b[t] = *reinterpret_cast<const double2*>(bs + (t * 8 + g) * kBld + 8 * s + 2 * q);
+      // the two K halves of an accumulator are separated by all other accumulators' MMAs
 #pragma unroll
-        for (int r = 0; r < RG; ++r) {
-          dmma(acc[r][t], xa[r].x, b.x);
-          dmma(acc[r][t], xa[r].y, b.y);
-        }
-      }
+      for (int t = 0; t < BN / 8; ++t)
+#pragma unroll
+        for (int r = 0; r < RG; ++r) dmma(acc[r][t], xa[r].x, b[t].x);
+#pragma unroll
+      for (int t = 0; t < BN / 8; ++t)
+#pragma unroll
+        for (int r = 0; r < RG; ++r) dmma(acc[r][t], xa[r].y, b[t].y);
     }
     if (it % nchunk == nchunk - 1) {   // tile done: write, reset
       int64_t r0, n0;
@@ -187,15 +189,15 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 1) k_nt_mma(const double* __re
 // (the A fragments) are fetched into registers one chunk before the tile switch.
 // Requirements: d % 8 == 0, ldx % 2 == 0, 16-byte aligned X and Qt.
 // ---------------------------------------------------------------------------------
-template <int BP>
+template <int BP, int RG_, int KC_>
 __global__ void __launch_bounds__(32 * kMmaWarps, 1) k_update_mma(double* __restrict__ X, int64_t ldx,
                                                                   const double* __restrict__ Qt,
                                                                   const double* __restrict__ L,
                                                                   int64_t ldl, int64_t n, int64_t d,
                                                                   double* __restrict__ dvec,
                                                                   DevState* st) {
-  using Cf = UpdCfg<BP>;
-  constexpr int RG = Cf::RG;
+  using Cf = PCfg<BP, RG_, KC_, true>;
+  constexpr int RG = Cf::RG, kKC = Cf::KC, kXld = Cf::XLD, kQld = Cf::BLD;
   extern __shared__ __align__(16) double sm[];
   if (st->stop) return;
   const int bp = st->b_prime;
@@ -212,8 +214,8 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 1) k_update_mma(double* __rest
     if (it < total) {
       double* base = sm + (size_t)(it % Cf::NS) * Cf::STAGE;
       const int64_t c0 = (it % nchunk) * kKC;
-      stage_x<Cf::ROWS>(base, X, ldx, r0_of(it / nchunk), n, c0, d, tid);
-      stage_b<BP, kQld>(base + Cf::ROWS * kXld, Qt, d, 0, bp, c0, d, tid);
+      stage_x<Cf::ROWS, kKC, kXld>(base, X, ldx, r0_of(it / nchunk), n, c0, d, tid);
+      stage_b<BP, kKC, kQld>(base + Cf::ROWS * kXld, Qt, d, 0, bp, c0, d, tid);
     }
     cp_async_commit();
   };
@@ -314,19 +316,51 @@ bool projection_mma_supported(const void* X, int64_t ldx, const void* Qt, int64_
   return mma_ok(X, ldx, d) && ((uintptr_t)Qt % 16 == 0);
 }
 
+// projection tile variant: RBRP_PROJ_VARIANT = 0: (RG 1, KC 64)  1: (RG 2, KC 32)
+// 2: (RG 2, KC 64)  3: (RG 1, KC 32); default 0.  (RG 1 for b' > 64 in every variant.)
+static int proj_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RBRP_PROJ_VARIANT");
+    v = e ? atoi(e) : 0;
+    if (v < 0 || v > 3) v = 0;
+  }
+  return v;
+}
+
+template <int BN, int RG, int KC>
+static void go_lhat(const double* Xres, int64_t ldx, const double* Qt, int64_t n, int64_t d, double* L,
+                    int64_t ldl, DevState* st, cudaStream_t s) {
+  using Cf = PCfg<BN, RG, KC, false>;
+  auto kern = k_nt_mma<BN, RG, KC>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
+  kern<<<num_sms(), 32 * kMmaWarps, Cf::SMEM, s>>>(Xres, ldx, Qt, d, L, ldl, n, 0, d, st, 1);
+}
+template <int BP, int RG, int KC>
+static void go_upd(double* Xres, int64_t ldx, const double* Qt, const double* L, int64_t ldl, int64_t n,
+                   int64_t d, double* dvec, DevState* st, cudaStream_t s) {
+  using Cf = PCfg<BP, RG, KC, true>;
+  auto kern = k_update_mma<BP, RG, KC>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
+  kern<<<num_sms(), 32 * kMmaWarps, Cf::SMEM, s>>>(Xres, ldx, Qt, L, ldl, n, d, dvec, st);
+}
+
+#define RBRP_VARIANTS(GO, B, ...)                         \
+  switch (proj_variant()) {                              \
+    case 1: GO<B, 2, 32>(__VA_ARGS__); break;            \
+    case 2: GO<B, 2, 64>(__VA_ARGS__); break;            \
+    case 3: GO<B, 1, 32>(__VA_ARGS__); break;            \
+    default: GO<B, 1, 64>(__VA_ARGS__); break;           \
+  }
+
 cudaError_t launch_lhat_mma(const double* Xres, int64_t ldx, const double* Qt, int64_t n, int64_t d,
                             double* L, int64_t ldl, DevState* st, int bucket, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  dim3 grid((unsigned)num_sms(), 1);
-  auto go = [&](auto kern, size_t smem) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<grid, 32 * kMmaWarps, smem, s>>>(Xres, ldx, Qt, d, L, ldl, n, 0, d, st, 1);
-  };
   switch (bucket) {
-    case 16: go(k_nt_mma<16>, NtCfg<16>::SMEM); break;
-    case 32: go(k_nt_mma<32>, NtCfg<32>::SMEM); break;
-    case 64: go(k_nt_mma<64>, NtCfg<64>::SMEM); break;
-    default: go(k_nt_mma<128>, NtCfg<128>::SMEM); break;
+    case 16: RBRP_VARIANTS(go_lhat, 16, Xres, ldx, Qt, n, d, L, ldl, st, s); break;
+    case 32: RBRP_VARIANTS(go_lhat, 32, Xres, ldx, Qt, n, d, L, ldl, st, s); break;
+    case 64: RBRP_VARIANTS(go_lhat, 64, Xres, ldx, Qt, n, d, L, ldl, st, s); break;
+    default: go_lhat<128, 1, 32>(Xres, ldx, Qt, n, d, L, ldl, st, s); break;
   }
   return cudaGetLastError();
 }
@@ -335,16 +369,11 @@ cudaError_t launch_update_mma(double* Xres, int64_t ldx, const double* Qt, const
                               int64_t ldl, int64_t n, int64_t d, double* dvec, DevState* st,
                               int bucket, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  const int g = num_sms();
-  auto go = [&](auto kern, size_t smem) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<g, 32 * kMmaWarps, smem, s>>>(Xres, ldx, Qt, L, ldl, n, d, dvec, st);
-  };
   switch (bucket) {
-    case 16: go(k_update_mma<16>, UpdCfg<16>::SMEM); break;
-    case 32: go(k_update_mma<32>, UpdCfg<32>::SMEM); break;
-    case 64: go(k_update_mma<64>, UpdCfg<64>::SMEM); break;
-    default: go(k_update_mma<128>, UpdCfg<128>::SMEM); break;
+    case 16: RBRP_VARIANTS(go_upd, 16, Xres, ldx, Qt, L, ldl, n, d, dvec, st, s); break;
+    case 32: RBRP_VARIANTS(go_upd, 32, Xres, ldx, Qt, L, ldl, n, d, dvec, st, s); break;
+    case 64: RBRP_VARIANTS(go_upd, 64, Xres, ldx, Qt, L, ldl, n, d, dvec, st, s); break;
+    default: go_upd<128, 1, 32>(Xres, ldx, Qt, L, ldl, n, d, dvec, st, s); break;
   }
   return cudaGetLastError();
 }
@@ -354,9 +383,9 @@ bool gemm_nt_mma(const double* A, int64_t lda, const double* B, int64_t ldb, dou
                  int64_t M, int64_t N, int64_t K, cudaStream_t s, cudaError_t* err) {
   if (!mma_ok(A, lda, K) || !mma_ok(B, ldb, K)) return false;
   dim3 grid((unsigned)num_sms(), 1);
-  const size_t smem = NtCfg<128>::SMEM;
-  cudaFuncSetAttribute(k_nt_mma<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_nt_mma<128><<<grid, 32 * kMmaWarps, smem, s>>>(A, lda, B, ldb, C, ldc, M, N, K, nullptr, 0);
+  using Cf = PCfg<128, 1, 32, false>;
+  cudaFuncSetAttribute(k_nt_mma<128, 1, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
+  k_nt_mma<128, 1, 32><<<grid, 32 * kMmaWarps, Cf::SMEM, s>>>(A, lda, B, ldb, C, ldc, M, N, K, nullptr, 0);
   *err = cudaGetLastError();
   return true;
 }
