@@ -191,7 +191,10 @@ int rbrp_workspace_size(const rbrp_problem* p, size_t* bytes);
  *              unless RBRP_INPLACE.
  *   workspace  device, >= rbrp_workspace_size() bytes, 256-byte aligned, caller-owned;
  *              contents are scratch on entry and exit.
- *   comm       NULL (single GPU) or a communicator from rbrp_comm_init.
+ *   comm       NULL (single GPU) or a communicator from rbrp_comm_init: this rank's rows are
+ *              p->row_offset .. +n_local (row_offset a multiple of RBRP_CHUNK); per block the
+ *              chunk totals, the candidate rows of every draw round and the V rows are
+ *              combined with NCCL allreduces, and L_1 once for W.
  *   stream     cudaStream_t (as void*); all device work is ordered on it.  The call
  *              blocks the host once per block (the data-dependent stop test, l.3).
  *   S_out      host, int64[k_cap]: skeletons S in selection order (= pi(1:k)), global
@@ -208,6 +211,28 @@ int rbrp_workspace_size(const rbrp_problem* p, size_t* bytes);
  */
 int rbrp_id(const rbrp_problem* p, void* X, void* workspace, size_t ws_bytes,
             rbrp_comm* comm, void* stream, int64_t* S_out, void* W_out, rbrp_report* rep);
+
+/*
+ * rbrp_id_sharded — the row-sharded algorithm of a multi-GPU run for
+ * `nshards` contiguous row shards held on the CURRENT device by one process: the same
+ * kernels and exchange points as `nshards` ranks of rbrp_id with a communicator, with the
+ * collectives realised as shared device buffers written by the row owners.  Used to check
+ * shard invariance (S, b', rho, W rows identical for any sharding) on one GPU, and to run
+ * problems larger than one allocation.
+ *   p           problem; n_local / row_offset are ignored (taken from shard_rows).
+ *   shard_rows  host int64[nshards]: rows per shard, in order; every shard but the last a
+ *               multiple of RBRP_CHUNK; sum = n_global.
+ *   X           host array of nshards device pointers (shard h: shard_rows[h] x d, ld).
+ *   workspace   host array of nshards device pointers, each >= ws_bytes, where ws_bytes >=
+ *               rbrp_workspace_size() of every shard's problem (n_local = shard_rows[h]).
+ *   W_out       host array of nshards device pointers (shard_rows[h] x k_cap, ld k_cap), or
+ *               NULL; entries may be NULL.
+ *   S_out, rep  as rbrp_id (report of shard 0; S is the same for every shard).
+ * Errors as rbrp_id, plus RBRP_EINVAL for inconsistent shard sizes.
+ */
+int rbrp_id_sharded(const rbrp_problem* p, int nshards, const int64_t* shard_rows, void* const* X,
+                    void* const* workspace, size_t ws_bytes, void* stream, int64_t* S_out,
+                    void* const* W_out, rbrp_report* rep);
 
 /* Human-readable name of a status code (static string; never NULL). */
 const char* rbrp_strerror(int status);

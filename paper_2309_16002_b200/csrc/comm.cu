@@ -121,4 +121,12 @@ int comm_allreduce_max_i64(rbrp_comm* c, int64_t* buf, int64_t count, cudaStream
   return RBRP_OK;
 }
 
+int comm_allreduce_sum_i32(rbrp_comm* c, int32_t* buf, int64_t count, cudaStream_t s) {
+  NcclApi& a = api();
+  if (!a.ok) return RBRP_ENCCL;
+  if (a.AllReduce(buf, buf, count, ncclInt32, ncclSum, (ncclComm_t)c->nccl_comm, s) != ncclSuccess)
+    return RBRP_ENCCL;
+  return RBRP_OK;
+}
+
 }  // namespace rbrp

@@ -32,8 +32,11 @@ struct DevState {
   int32_t rank_def;   // pivoted Cholesky hit a non-positive pivot
   int32_t nlogged;    // blocks written to the device log
   uint32_t done_ctas; // CTA completion counter of the projection update kernel
-  int32_t pad;
+  int32_t exhausted;  // distributed sampling: support <= b_t (take all positive rows)
   long long ts0, ts1; // %globaltimer at projection start / end (current block)
+  int64_t jb;         // distributed sampling: next Philox draw index of the block
+  int32_t sample_c;   // distributed sampling: candidates accepted so far
+  int32_t sample_done;
 };
 
 __device__ __forceinline__ long long gtimer() {

@@ -6,8 +6,9 @@
 
 namespace rbrp {
 
-// V rows: Vg(i,:) = X_res(S_t[i],:) in fp64 when this rank owns the row, else 0
-// (multi-GPU: an allreduce(sum) then gives every rank the full V).
+// V rows: Vg(i,:) = X_res(S_t[i],:) in fp64, written by the owner of row S_t[i] only
+// (multi-GPU: Vg is zeroed first and an allreduce(sum) then gives every rank the full V,
+// SURVEY §8(e) C3; in-process shards share one Vg).
 template <typename T>
 __global__ void __launch_bounds__(256) k_gather_rows(const T* __restrict__ X, int64_t ldx,
                                                      const int64_t* __restrict__ rows,
@@ -18,9 +19,8 @@ __global__ void __launch_bounds__(256) k_gather_rows(const T* __restrict__ X, in
   const int i = blockIdx.x;
   if (i >= st->b_t) return;
   const int64_t r = rows[i] - row_offset;
-  const bool own = r >= 0 && r < n_local;
-  for (int64_t c = threadIdx.x; c < d; c += blockDim.x)
-    Vg[(int64_t)i * d + c] = own ? (double)X[r * ldx + c] : 0.0;
+  if (r < 0 || r >= n_local) return;   // another rank's row: left as is (zeroed before)
+  for (int64_t c = threadIdx.x; c < d; c += blockDim.x) Vg[(int64_t)i * d + c] = (double)X[r * ldx + c];
 }
 
 template <typename T>

@@ -17,8 +17,8 @@ __global__ void k_gather_L1(const T* __restrict__ L, int64_t ldl, const int64_t*
                             int64_t k, int64_t n_local, int64_t row_offset, double* __restrict__ L1) {
   const int64_t i = blockIdx.x;
   const int64_t r = S[i] - row_offset;
-  for (int64_t j = threadIdx.x; j < k; j += blockDim.x)
-    L1[i * k + j] = (r >= 0 && r < n_local) ? (double)L[r * ldl + j] : 0.0;
+  if (r < 0 || r >= n_local) return;   // another rank's skeleton (zeroed / shared buffer)
+  for (int64_t j = threadIdx.x; j < k; j += blockDim.x) L1[i * k + j] = (double)L[r * ldl + j];
 }
 
 template <typename T>
@@ -55,13 +55,15 @@ __global__ void __launch_bounds__(32 * kTrinvWarps) k_trinv(const double* __rest
   }
   if (j >= k) return;
   double* x = xs + (int64_t)w * k;
-  if (lane == 0) x[j] = 1.0 / L1[j * k + j];
+  const double xj = 1.0 / L1[j * k + j];   // fp64 math warp-uniform (single-lane fp64 is slow)
+  if (lane == 0) x[j] = xj;
   __syncwarp();
   for (int64_t i = j + 1; i < k; ++i) {
     double s = 0.0;
     for (int64_t m = j + lane; m < i; m += 32) s += L1[i * k + m] * x[m];
     s = warp_sum(s);
-    if (lane == 0) x[i] = -s / L1[i * k + i];
+    const double xi = -s / L1[i * k + i];
+    if (lane == 0) x[i] = xi;
     __syncwarp();
   }
   for (int64_t m = lane; m < k; m += 32) LinvT[j * k + m] = (m < j) ? T(0) : (T)x[m];

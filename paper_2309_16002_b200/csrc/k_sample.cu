@@ -134,6 +134,17 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample(SampleArgs A) {
   }
   __syncthreads();
   if (s_stop) return;
+  if (A.dist && A.replay_len < 0) {   // drawing happens in the resolve / accept rounds
+    if (tid == 0) {
+      st->jb = 0;
+      st->sample_c = 0;
+      st->sample_done = 0;
+      st->exhausted = s_np <= s_bt ? 1 : 0;
+      st->b_t = s_bt;
+      st->draws = 0;
+    }
+    return;
+  }
   if (A.replay_len >= 0) {
     for (int i = tid; i < A.replay_len; i += kSampleThreads) A.S_t[i] = A.S_rep[i];
     if (tid == 0) { st->b_t = A.replay_len; st->draws = 0; }
@@ -227,6 +238,125 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample(SampleArgs A) {
 
 cudaError_t launch_sample(const SampleArgs& a, cudaStream_t s) {
   k_sample<<<1, kSampleThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+// Round of kSampleRound draws: cand[j] = the global row of draw jb + j if it lands in one
+// of this rank's chunks (else left at -1).  Small support (reading R7): this rank's
+// positive rows, in row order, at slots [sum of positive counts of the earlier chunks, ...).
+__global__ void __launch_bounds__(kSampleRound) k_draw_resolve(SampleArgs A) {
+  const DevState* st = A.st;
+  if (st->stop || st->sample_done) return;
+  const int tid = threadIdx.x;
+  if (st->exhausted) {
+    __shared__ long long base;
+    __shared__ int wc[kSampleRound / 32];
+    const int lane = tid & 31, w = tid >> 5;
+    if (tid == 0) {
+      long long b = 0;
+      const int c0 = (int)(A.row_offset / kChunk);
+      for (int c = 0; c < c0; ++c) b += A.cpos[c];
+      base = b;
+    }
+    __syncthreads();
+    for (int64_t r0 = 0; r0 < A.n_local; r0 += kSampleRound) {
+      const int64_t r = r0 + tid;
+      const int f = (r < A.n_local && A.dvec[r] > 0.0) ? 1 : 0;
+      const unsigned m = __ballot_sync(0xffffffffu, f);
+      if (lane == 0) wc[w] = __popc(m);
+      __syncthreads();
+      long long off = base;
+      for (int q = 0; q < w; ++q) off += wc[q];
+      off += __popc(m & ((1u << lane) - 1u));
+      if (f && off < kSampleRound) A.cand[off] = r + A.row_offset;
+      __syncthreads();
+      if (tid == 0) {
+        long long t = 0;
+        for (int q = 0; q < kSampleRound / 32; ++q) t += wc[q];
+        base += t;
+      }
+      __syncthreads();
+    }
+    return;
+  }
+  const double total = st->total;
+  const uint2 key = make_uint2((uint32_t)(A.seed & 0xffffffffu), (uint32_t)(A.seed >> 32));
+  const uint32_t t = (uint32_t)st->t;
+  const uint32_t j = (uint32_t)(st->jb + tid);
+  const double u = u53(philox4x32_10(make_uint4(j, t, 0u, 0u), key));
+  const double target = u * total;
+  int a = 0, b = A.nchunks;
+  while (a < b) {
+    const int m = (a + b) >> 1;
+    if (A.cprefix[m] > target) b = m; else a = m + 1;
+  }
+  int64_t row;
+  if (a >= A.nchunks) {
+    int q = A.nchunks - 1;
+    while (q > 0 && A.cpos[q] == 0) --q;
+    row = resolve_in_chunk(q, 1e308, A.cpre, A.dvec, A.n_local, A.row_offset);
+  } else {
+    const double tq = target - (a > 0 ? A.cprefix[a - 1] : 0.0);
+    row = resolve_in_chunk(a, tq, A.cpre, A.dvec, A.n_local, A.row_offset);
+  }
+  if (row >= 0) A.cand[tid] = row;
+}
+
+// Accept the combined candidates of a round in draw order, rejecting repeats (reading
+// R6) — the same rule as k_sample's single-GPU loop, so S_t is identical for any sharding.
+__global__ void __launch_bounds__(kSampleRound) k_draw_accept(SampleArgs A) {
+  DevState* st = A.st;
+  if (st->stop || st->sample_done) return;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  __shared__ int64_t chosen[kMaxB];
+  __shared__ int64_t cand[kSampleRound];
+  __shared__ int wcount[kSampleRound / 32];
+  const int bt = st->b_t;
+  const int c = st->sample_c;
+  for (int i = tid; i < c; i += kSampleRound) chosen[i] = A.S_t[i];
+  const int64_t row = A.cand[tid];
+  cand[tid] = row;
+  __syncthreads();
+  if (st->exhausted) {
+    const int n = (int)min((int64_t)kMaxB, st->npos);
+    if (tid < n) A.S_t[tid] = cand[tid];
+    if (tid == 0) {
+      st->b_t = n;
+      st->sample_c = n;
+      st->sample_done = 1;
+      st->flags |= RBRP_F_SUPPORT_EXHAUSTED;
+    }
+    return;
+  }
+  int isnew = row >= 0;
+  for (int m = 0; m < c && isnew; ++m) isnew = chosen[m] != row;
+  for (int m = 0; m < tid && isnew; ++m) isnew = cand[m] != row;
+  const unsigned msk = __ballot_sync(0xffffffffu, isnew);
+  if (lane == 0) wcount[w] = __popc(msk);
+  __syncthreads();
+  int off = 0;
+  for (int q = 0; q < w; ++q) off += wcount[q];
+  off += __popc(msk & ((1u << lane) - 1u));
+  if (isnew && c + off < bt) A.S_t[c + off] = row;
+  if (tid == 0) {
+    int tot = 0;
+    for (int q = 0; q < kSampleRound / 32; ++q) tot += wcount[q];
+    const int nc = min(bt, c + tot);
+    st->sample_c = nc;
+    st->jb += kSampleRound;
+    if (nc >= bt || st->jb >= kJMax) {
+      st->sample_done = 1;
+      st->b_t = nc;
+    }
+  }
+}
+
+cudaError_t launch_draw_resolve(const SampleArgs& a, cudaStream_t s) {
+  k_draw_resolve<<<1, kSampleRound, 0, s>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_draw_accept(const SampleArgs& a, cudaStream_t s) {
+  k_draw_accept<<<1, kSampleRound, 0, s>>>(a);
   return cudaGetLastError();
 }
 

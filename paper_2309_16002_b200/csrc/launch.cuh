@@ -29,8 +29,16 @@ struct SampleArgs {
   const int32_t* piv;     // pivots of the block that just finished (logged)
   BlockLog log;
   unsigned long long cond;   // cudaGraphConditionalHandle of the WHILE node (0: none)
+  int dist;               // 1: row-sharded run; this kernel only does the stop test / b_t
+  int64_t* cand;          // distributed rounds: candidate rows of kSampleRound draws (-1 = not mine)
 };
 cudaError_t launch_sample(const SampleArgs& a, cudaStream_t s);
+// distributed sampling: every rank resolves the draws that land in its
+// own chunks; the candidate vectors are combined (max over ranks); every rank then
+// accepts in draw order (identical everywhere).  One round = kSampleRound draws.
+constexpr int kSampleRound = 256;
+cudaError_t launch_draw_resolve(const SampleArgs& a, cudaStream_t s);
+cudaError_t launch_draw_accept(const SampleArgs& a, cudaStream_t s);
 
 // k_filter.cu — Alg. 2 l.6-9
 template <typename T>

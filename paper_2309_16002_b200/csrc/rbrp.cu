@@ -35,7 +35,7 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
   size_t Xres = SIZE_MAX, dvec, cpre, ctot, cpos, cprefix, L, Qt, Vg, Gpart, G, Tg, Ag, R11, Rtot,
-         piv, mass, St, Srep, S, forced, dbg, st, L1 = SIZE_MAX, LinvT = SIZE_MAX;
+         piv, mass, St, Srep, S, forced, dbg, cand, st, L1 = SIZE_MAX, LinvT = SIZE_MAX;
   size_t lbt, lbp, lrho, lSt, lpiv, lts, total;
   int nsplit, maxlog;
   int64_t nchunks, k_cap;
@@ -99,6 +99,7 @@ Layout make_layout(const rbrp_problem* p) {
   L.S = take((size_t)L.k_cap * 8);
   L.forced = take(B * 4);
   L.dbg = take(64 * 8);
+  L.cand = take((size_t)kSampleRound * 8);
   L.st = take(sizeof(DevState));
   L.lbt = take((size_t)L.maxlog * 4);
   L.lbp = take((size_t)L.maxlog * 4);
@@ -185,13 +186,90 @@ struct Ctx {
   double *dvec, *cpre, *ctot, *cprefix, *Vg, *Gpart, *G, *Tg, *Ag, *R11, *Rtot, *mass;
   int32_t *cpos, *piv, *forced;
   T *Lm, *Qt;
-  int64_t *St, *Srep, *S;
+  int64_t *St, *Srep, *S, *cand;
+  double* L1;
+  T* LinvT;
   DevState* st;
   long long* dbg;
   BlockLog log;
   bool use_mma, use_forced;
   int bucketB;
 };
+
+// pointers of one shard's workspace
+template <typename T>
+void make_ctx(Ctx<T>& c, const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* comm) {
+  c.p = p;
+  c.Ly = &Ly;
+  c.comm = comm;
+  c.n = p->n_local;
+  c.d = p->d;
+  c.k_cap = Ly.k_cap;
+  c.chunk0 = p->row_offset / RBRP_CHUNK;
+  const bool inplace = (p->flags & RBRP_INPLACE) != 0;
+  c.X = (T*)Xv;
+  c.Xres = inplace ? c.X : (T*)(ws + Ly.Xres);
+  c.ldr = inplace ? p->ld : c.d;
+  c.dvec = (double*)(ws + Ly.dvec);
+  c.cpre = (double*)(ws + Ly.cpre);
+  c.ctot = (double*)(ws + Ly.ctot);
+  c.cpos = (int32_t*)(ws + Ly.cpos);
+  c.cprefix = (double*)(ws + Ly.cprefix);
+  c.Lm = (T*)(ws + Ly.L);
+  c.Qt = (T*)(ws + Ly.Qt);
+  c.Vg = (double*)(ws + Ly.Vg);
+  c.Gpart = (double*)(ws + Ly.Gpart);
+  c.G = (double*)(ws + Ly.G);
+  c.Tg = (double*)(ws + Ly.Tg);
+  c.Ag = (double*)(ws + Ly.Ag);
+  c.R11 = (double*)(ws + Ly.R11);
+  c.Rtot = (double*)(ws + Ly.Rtot);
+  c.piv = (int32_t*)(ws + Ly.piv);
+  c.mass = (double*)(ws + Ly.mass);
+  c.St = (int64_t*)(ws + Ly.St);
+  c.Srep = (int64_t*)(ws + Ly.Srep);
+  c.S = (int64_t*)(ws + Ly.S);
+  c.cand = (int64_t*)(ws + Ly.cand);
+  c.forced = (int32_t*)(ws + Ly.forced);
+  c.st = (DevState*)(ws + Ly.st);
+  c.L1 = Ly.L1 != SIZE_MAX ? (double*)(ws + Ly.L1) : nullptr;
+  c.LinvT = Ly.LinvT != SIZE_MAX ? (T*)(ws + Ly.LinvT) : nullptr;
+  c.dbg = env_on("RBRP_DEBUG_STAMPS") ? (long long*)(ws + Ly.dbg) : nullptr;
+  c.log.bt = (int32_t*)(ws + Ly.lbt);
+  c.log.bp = (int32_t*)(ws + Ly.lbp);
+  c.log.rho = (double*)(ws + Ly.lrho);
+  c.log.St = (int64_t*)(ws + Ly.lSt);
+  c.log.piv = (int32_t*)(ws + Ly.lpiv);
+  c.log.ts = (long long*)(ws + Ly.lts);
+  c.log.maxlog = Ly.maxlog;
+  c.log.b = p->b;
+  c.use_forced = p->replay_pivots != nullptr;
+  c.use_mma = sizeof(T) == 8 && !force_simt() && projection_mma_supported(c.Xres, c.ldr, c.Qt, c.d);
+  c.bucketB = bucket_of((int)std::min<int64_t>(p->b, c.k_cap));
+}
+
+template <typename T>
+void make_sample_args(SampleArgs& sa, const Ctx<T>& c, int dist) {
+  memset(&sa, 0, sizeof(sa));
+  sa.st = c.st;
+  sa.ctot = c.ctot;
+  sa.cpos = c.cpos;
+  sa.cprefix = c.cprefix;
+  sa.nchunks = (int)c.Ly->nchunks;
+  sa.cpre = c.cpre;
+  sa.dvec = c.dvec;
+  sa.n_local = c.n;
+  sa.row_offset = c.p->row_offset;
+  sa.S_t = c.St;
+  sa.S_rep = c.Srep;
+  sa.seed = c.p->seed;
+  sa.first = 1;
+  sa.piv = c.piv;
+  sa.log = c.log;
+  sa.cond = 0;
+  sa.dist = dist;
+  sa.cand = c.cand;
+}
 
 // The kernels of one block (Alg. 2 l.6-16), optionally followed by the next block's
 // stop test and sample (l.3-5).  Every kernel reads its sizes from DevState and is a
@@ -376,51 +454,9 @@ template <typename T>
 int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* comm,
         cudaStream_t s, int64_t* S_out, void* W_out, rbrp_report* rep) {
   Ctx<T> c;
-  c.p = p;
-  c.Ly = &Ly;
-  c.comm = comm;
-  c.n = p->n_local;
-  c.d = p->d;
-  c.k_cap = Ly.k_cap;
-  c.chunk0 = p->row_offset / RBRP_CHUNK;
+  make_ctx<T>(c, p, Xv, ws, Ly, comm);
   const bool inplace = (p->flags & RBRP_INPLACE) != 0;
-  c.X = (T*)Xv;
-  c.Xres = inplace ? c.X : (T*)(ws + Ly.Xres);
-  c.ldr = inplace ? p->ld : c.d;
-  c.dvec = (double*)(ws + Ly.dvec);
-  c.cpre = (double*)(ws + Ly.cpre);
-  c.ctot = (double*)(ws + Ly.ctot);
-  c.cpos = (int32_t*)(ws + Ly.cpos);
-  c.cprefix = (double*)(ws + Ly.cprefix);
-  c.Lm = (T*)(ws + Ly.L);
-  c.Qt = (T*)(ws + Ly.Qt);
-  c.Vg = (double*)(ws + Ly.Vg);
-  c.Gpart = (double*)(ws + Ly.Gpart);
-  c.G = (double*)(ws + Ly.G);
-  c.Tg = (double*)(ws + Ly.Tg);
-  c.Ag = (double*)(ws + Ly.Ag);
-  c.R11 = (double*)(ws + Ly.R11);
-  c.Rtot = (double*)(ws + Ly.Rtot);
-  c.piv = (int32_t*)(ws + Ly.piv);
-  c.mass = (double*)(ws + Ly.mass);
-  c.St = (int64_t*)(ws + Ly.St);
-  c.Srep = (int64_t*)(ws + Ly.Srep);
-  c.S = (int64_t*)(ws + Ly.S);
-  c.forced = (int32_t*)(ws + Ly.forced);
-  c.st = (DevState*)(ws + Ly.st);
   const bool stamps = env_on("RBRP_DEBUG_STAMPS");
-  c.dbg = stamps ? (long long*)(ws + Ly.dbg) : nullptr;
-  c.log.bt = (int32_t*)(ws + Ly.lbt);
-  c.log.bp = (int32_t*)(ws + Ly.lbp);
-  c.log.rho = (double*)(ws + Ly.lrho);
-  c.log.St = (int64_t*)(ws + Ly.lSt);
-  c.log.piv = (int32_t*)(ws + Ly.lpiv);
-  c.log.ts = (long long*)(ws + Ly.lts);
-  c.log.maxlog = Ly.maxlog;
-  c.log.b = p->b;
-  c.use_forced = p->replay_pivots != nullptr;
-  c.use_mma = sizeof(T) == 8 && !force_simt() && projection_mma_supported(c.Xres, c.ldr, c.Qt, c.d);
-  c.bucketB = bucket_of((int)std::min<int64_t>(p->b, c.k_cap));
   const int64_t k_cap = c.k_cap;
 
   // pinned staging: [state][S_t][piv][log ...][S]
@@ -491,23 +527,7 @@ int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* 
   };
 
   SampleArgs sa;
-  memset(&sa, 0, sizeof(sa));
-  sa.st = c.st;
-  sa.ctot = c.ctot;
-  sa.cpos = c.cpos;
-  sa.cprefix = c.cprefix;
-  sa.nchunks = (int)Ly.nchunks;
-  sa.cpre = c.cpre;
-  sa.dvec = c.dvec;
-  sa.n_local = c.n;
-  sa.row_offset = p->row_offset;
-  sa.S_t = c.St;
-  sa.S_rep = c.Srep;
-  sa.seed = p->seed;
-  sa.first = 1;
-  sa.piv = c.piv;
-  sa.log = c.log;
-  sa.cond = 0;
+  make_sample_args<T>(sa, c, 0);
   int rl = stage_replay(0);
   if (rl < -100) return rl + 1000;
   sa.replay_len = rl;
@@ -564,8 +584,8 @@ int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* 
   }
   // a6: W (Alg. 3)
   if (!(p->flags & RBRP_NO_W) && W_out && k > 0) {
-    double* L1 = (double*)(ws + Ly.L1);
-    T* LinvT = (T*)(ws + Ly.LinvT);
+    double* L1 = c.L1;
+    T* LinvT = c.LinvT;
     prof.begin(6);
     ++nl;
     CK(launch_gather_L1<T>(c.Lm, k_cap, c.S, k, c.n, p->row_offset, L1, s));
@@ -644,6 +664,279 @@ int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* 
   return RBRP_OK;
 }
 
+// ---------------------------------------------------------------------------------
+// Row-sharded run: nsh shards handled by this process.  With an NCCL
+// communicator (one process per GPU) nsh == 1 and the exchange points are NCCL
+// collectives; without one, nsh > 1 shards live on the current device (in-process
+// emulation of nsh ranks: the exchange buffers are shared and written by the owners only,
+// which is exactly what the collectives produce).  Per block: C1 chunk totals, C2
+// candidate rows of every draw round (max), C3 V rows (sum), once for W: C5 L_1 (sum).
+// Q_b is not broadcast: every shard runs the (deterministic) filter on identical data.
+// ---------------------------------------------------------------------------------
+template <typename T>
+int run_dist(int nsh, const rbrp_problem* ps, void* const* Xs, char* const* wss, const Layout* Lys,
+             rbrp_comm* comm, cudaStream_t s, int64_t* S_out, void* const* W_outs, rbrp_report* rep) {
+  std::vector<Ctx<T>> C(nsh);
+  std::vector<SampleArgs> SA(nsh);
+  for (int h = 0; h < nsh; ++h) make_ctx<T>(C[h], &ps[h], Xs[h], wss[h], Lys[h], comm);
+  const bool emul = comm == nullptr;
+  if (emul)
+    for (int h = 1; h < nsh; ++h) {   // exchange buffers shared with shard 0
+      C[h].ctot = C[0].ctot;
+      C[h].cpos = C[0].cpos;
+      C[h].cprefix = C[0].cprefix;
+      C[h].Vg = C[0].Vg;
+      C[h].cand = C[0].cand;
+      C[h].Srep = C[0].Srep;
+      C[h].L1 = C[0].L1;
+    }
+  for (int h = 0; h < nsh; ++h) make_sample_args<T>(SA[h], C[h], 1);
+  const rbrp_problem* p = &ps[0];
+  const int64_t k_cap = C[0].k_cap;
+  const int b = p->b, mb = Lys[0].maxlog;
+  size_t o = 0;
+  auto carve = [&](size_t bytes) { size_t r = o; o = align256(o + bytes); return r; };
+  const size_t o_st = carve(sizeof(DevState) * nsh), o_St = carve(RBRP_MAX_B * 8),
+               o_piv = carve(RBRP_MAX_B * 4), o_bt = carve(mb * 4), o_bp = carve(mb * 4),
+               o_rho = carve(mb * 8), o_lSt = carve((size_t)mb * b * 8), o_lpiv = carve((size_t)mb * b * 4),
+               o_ts = carve((size_t)mb * 16), o_S = carve((size_t)k_cap * 8 + 8);
+  char* hp = (char*)g_pinned.get(o);
+  if (!hp) return RBRP_ECUDA;
+  DevState* hst = (DevState*)(hp + o_st);
+  int64_t* hSt = (int64_t*)(hp + o_St);
+  int32_t* hpiv = (int32_t*)(hp + o_piv);
+  int nl = 0, nproj = 0;
+#define LKD(x)                                 \
+  do {                                         \
+    ++nl;                                      \
+    if ((x) != cudaSuccess) return RBRP_ECUDA; \
+  } while (0)
+#define RCD(x)              \
+  do {                      \
+    const int rc_ = (x);    \
+    if (rc_) return rc_;    \
+  } while (0)
+  for (int h = 0; h < nsh; ++h) {
+    DevState* hs = hst + h;
+    memset(hs, 0, sizeof(DevState));
+    hs->tau = p->tol > 0.0 ? p->tol : -1.0;
+    hs->tau_b = p->tau_b;
+    hs->k_cap = k_cap;
+    hs->b = p->b;
+    CK(cudaMemcpyAsync(C[h].st, hs, sizeof(DevState), cudaMemcpyHostToDevice, s));
+  }
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, s));
+  auto coll_chunks = [&]() -> int {
+    if (!comm) return RBRP_OK;
+    return comm_allgather_chunks(comm, C[0].ctot, C[0].cpos, C[0].chunk0,
+                                 (C[0].n + RBRP_CHUNK - 1) / RBRP_CHUNK, Lys[0].nchunks, s);
+  };
+  // a0
+  for (int h = 0; h < nsh; ++h) {
+    const bool inplace = (ps[h].flags & RBRP_INPLACE) != 0;
+    LKD(launch_init_norms<T>(C[h].X, ps[h].ld, C[h].Xres, C[h].n, C[h].d, C[h].dvec, C[h].st, !inplace, s));
+    LKD(launch_chunk_scan(C[h].dvec, C[h].n, C[h].chunk0, C[h].cpre, C[h].ctot, C[h].cpos, s));
+  }
+  RCD(coll_chunks());
+  // replay ids: one staging buffer (shard 0's Srep; shared in emulation, per rank with NCCL)
+  int64_t replay_pos = 0;
+  auto stage_replay = [&](int blk) -> int {
+    if (!p->replay_nblocks) return -1;
+    if (blk >= p->replay_nblocks) return -2;
+    const int len = p->replay_lens[blk];
+    if (len < 1 || len > p->b) return RBRP_EREPLAY - 1000;
+    if (cudaStreamSynchronize(s) != cudaSuccess) return RBRP_ECUDA - 1000;
+    for (int i = 0; i < len; ++i) {
+      const int64_t id = p->replay_blocks[replay_pos + i];
+      if (id < 0 || id >= p->n_global) return RBRP_EREPLAY - 1000;
+      hSt[i] = id;
+    }
+    if (cudaMemcpyAsync(C[0].Srep, hSt, len * 8, cudaMemcpyHostToDevice, s) != cudaSuccess)
+      return RBRP_ECUDA - 1000;
+    if (p->replay_pivots) {
+      for (int i = 0; i < len; ++i) hpiv[i] = p->replay_pivots[replay_pos + i];
+      for (int h = 0; h < nsh; ++h)
+        if (cudaMemcpyAsync(C[h].forced, hpiv, len * 4, cudaMemcpyHostToDevice, s) != cudaSuccess)
+          return RBRP_ECUDA - 1000;
+    }
+    replay_pos += len;
+    return len;
+  };
+  // stop test + next block (l.3-5); draws resolved by their owners, combined, accepted
+  auto sample = [&](int rl) -> int {
+    for (int h = 0; h < nsh; ++h) {
+      SA[h].replay_len = rl;
+      if (emul) SA[h].S_rep = C[0].Srep;
+      LKD(launch_sample(SA[h], s));
+      SA[h].first = 0;
+    }
+    if (rl >= 0 || rl == -2) return RBRP_OK;
+    for (int round = 0;; ++round) {
+      const int ncand = emul ? 1 : nsh;
+      for (int h = 0; h < ncand; ++h) CK(cudaMemsetAsync(C[h].cand, 0xff, kSampleRound * 8, s));
+      for (int h = 0; h < nsh; ++h) LKD(launch_draw_resolve(SA[h], s));
+      if (comm) RCD(comm_allreduce_max_i64(comm, C[0].cand, kSampleRound, s));
+      for (int h = 0; h < nsh; ++h) LKD(launch_draw_accept(SA[h], s));
+      CK(cudaMemcpyAsync(hst, C[0].st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      if (hst->stop || hst->sample_done) break;
+    }
+    return RBRP_OK;
+  };
+  int rl = stage_replay(0);
+  if (rl < -100) return rl + 1000;
+  RCD(sample(rl));
+  // errors: any shard saw NaN/Inf
+  if (comm) RCD(comm_allreduce_sum_i32(comm, &C[0].st->nonfinite, 1, s));
+  for (int h = 0; h < nsh; ++h) CK(cudaMemcpyAsync(hst + h, C[h].st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  for (int h = 0; h < nsh; ++h)
+    if (hst[h].nonfinite) return RBRP_ENONFINITE;
+  if (!(hst->D0 > 0.0)) return RBRP_EDEGENERATE;
+
+  int blk = 0;
+  while (!hst->stop) {
+    // a3: V rows from their owners (C3), then the filter on every shard
+    if (comm) CK(cudaMemsetAsync(C[0].Vg, 0, (size_t)RBRP_MAX_B * C[0].d * 8, s));
+    for (int h = 0; h < nsh; ++h)
+      LKD(launch_gather_rows<T>(C[h].Xres, C[h].ldr, C[h].St, C[h].n, ps[h].row_offset, C[h].st, C[h].d,
+                                C[h].Vg, s));
+    if (comm) RCD(comm_allreduce_f64(comm, C[0].Vg, (int64_t)RBRP_MAX_B * C[0].d, s));
+    for (int h = 0; h < nsh; ++h) {
+      Ctx<T>& c = C[h];
+      FilterArgs fa;
+      fa.st = c.st;
+      fa.X = c.Xres;
+      fa.ldx = c.ldr;
+      fa.Vg = c.Vg;
+      fa.S_t = c.St;
+      fa.row_offset = ps[h].row_offset;
+      fa.d = c.d;
+      fa.Gpart = c.Gpart;
+      fa.G = c.G;
+      fa.forced = c.use_forced ? c.forced : nullptr;
+      fa.piv = c.piv;
+      fa.mass = c.mass;
+      fa.R11 = c.R11;
+      fa.Tg = c.Tg;
+      fa.Ag = c.Ag;
+      fa.Rtot = c.Rtot;
+      fa.S = c.S;
+      fa.Qt = c.Qt;
+      fa.bp_pad = c.bucketB;
+      fa.dbg = nullptr;
+      LKD(launch_filter_coop<T>(fa, s));
+    }
+    // a4: projection, rank-local
+    for (int h = 0; h < nsh; ++h) {
+      Ctx<T>& c = C[h];
+      for (int bk = 16; bk <= c.bucketB; bk *= 2) {
+        if (c.use_mma) {
+          LKD(launch_lhat_mma((const double*)c.Xres, c.ldr, (const double*)c.Qt, c.n, c.d, (double*)c.Lm,
+                              c.k_cap, c.st, bk, s));
+          LKD(launch_update_mma((double*)c.Xres, c.ldr, (const double*)c.Qt, (const double*)c.Lm, c.k_cap,
+                                c.n, c.d, c.dvec, c.st, bk, s));
+        } else {
+          LKD(launch_lhat<T>(c.Xres, c.ldr, c.Qt, c.n, c.d, c.Lm, c.k_cap, c.st, bk, s));
+          LKD(launch_update<T>(c.Xres, c.ldr, c.Qt, c.Lm, c.k_cap, c.n, c.d, c.dvec, c.st, bk, s));
+        }
+      }
+      LKD(launch_fixup<T>(c.Xres, c.ldr, c.dvec, c.Lm, c.k_cap, c.Rtot, c.S, c.n, ps[h].row_offset, c.d, c.st, s));
+      LKD(launch_chunk_scan(c.dvec, c.n, c.chunk0, c.cpre, c.ctot, c.cpos, s));
+    }
+    ++nproj;
+    RCD(coll_chunks());
+    ++blk;
+    rl = stage_replay(blk);
+    if (rl < -100) return rl + 1000;
+    RCD(sample(rl));
+    CK(cudaMemcpyAsync(hst, C[0].st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  }
+  const int64_t k = hst->k;
+  const int nblocks = std::min(hst->t, mb);
+  // a6: W — L_1 rows from their owners (C5), then W rank-local
+  const bool want_W = !(p->flags & RBRP_NO_W) && W_outs && k > 0;
+  if (want_W) {
+    if (comm || nsh > 0) CK(cudaMemsetAsync(C[0].L1, 0, (size_t)k * k * 8, s));
+    for (int h = 0; h < nsh; ++h)
+      LKD(launch_gather_L1<T>(C[h].Lm, k_cap, C[h].S, k, C[h].n, ps[h].row_offset, C[h].L1, s));
+    if (comm) RCD(comm_allreduce_f64(comm, C[0].L1, k * k, s));
+    for (int h = 0; h < nsh; ++h) {
+      Ctx<T>& c = C[h];
+      if (!W_outs[h]) continue;
+      LKD(launch_trinv<T>(c.L1, k, c.LinvT, c.st, s));
+      cudaError_t merr = cudaSuccess;
+      ++nl;
+      if (sizeof(T) == 8 && !force_simt() &&
+          gemm_nt_mma((const double*)c.Lm, k_cap, (const double*)c.LinvT, k, (double*)W_outs[h], k_cap, c.n,
+                      k, k, s, &merr)) {
+        CK(merr);
+      } else {
+        CK(launch_gemm_nt<T>(c.Lm, k_cap, c.LinvT, k, (T*)W_outs[h], k_cap, c.n, k, k, s));
+      }
+      LKD(launch_w_identity<T>((T*)W_outs[h], k_cap, c.S, k, c.n, ps[h].row_offset, s));
+    }
+  }
+  int64_t* hS = (int64_t*)(hp + o_S);
+  CK(cudaMemcpyAsync(hS, C[0].S, (size_t)std::max<int64_t>(k, 1) * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(hst, C[0].st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+  const int nlog = std::max(nblocks, 1);
+  const BlockLog& lg = C[0].log;
+  CK(cudaMemcpyAsync(hp + o_bt, lg.bt, nlog * 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(hp + o_bp, lg.bp, nlog * 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(hp + o_rho, lg.rho, nlog * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(hp + o_ts, lg.ts, nlog * 16, cudaMemcpyDeviceToHost, s));
+  const bool want_blocks = rep && (rep->block_idx || rep->block_piv);
+  if (want_blocks) {
+    CK(cudaMemcpyAsync(hp + o_lSt, lg.St, (size_t)nlog * b * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hp + o_lpiv, lg.piv, (size_t)nlog * b * 4, cudaMemcpyDeviceToHost, s));
+  }
+  CK(cudaEventRecord(e1, s));
+  CK(cudaStreamSynchronize(s));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  memcpy(S_out, hS, (size_t)k * 8);
+  if (rep) {
+    rep->k = k;
+    rep->fro2 = hst->D0;
+    rep->resid_rel = hst->total / hst->D0;
+    rep->nblocks = hst->t;
+    rep->flags = hst->flags;
+    rep->ms_total = ms;
+    for (int i = 0; i < 8; ++i) rep->ms_phase[i] = 0.f;
+    rep->launches = nl;
+    rep->proj_calls = nproj;
+    const int32_t* lbt = (const int32_t*)(hp + o_bt);
+    const int32_t* lbp = (const int32_t*)(hp + o_bp);
+    const double* lrho = (const double*)(hp + o_rho);
+    const long long* lts = (const long long*)(hp + o_ts);
+    double proj = 0.0;
+    for (int t = 0; t < nblocks; ++t) {
+      if (lbp[t] > 0 && lts[2 * t + 1] > lts[2 * t]) proj += (lts[2 * t + 1] - lts[2 * t]) * 1e-6;
+      if (t < rep->max_blocks) {
+        if (rep->b_t) rep->b_t[t] = lbt[t];
+        if (rep->b_prime) rep->b_prime[t] = lbp[t];
+        if (rep->rho) rep->rho[t] = lrho[t];
+        for (int i = 0; want_blocks && i < b; ++i) {
+          if (rep->block_idx) rep->block_idx[(int64_t)t * b + i] = ((const int64_t*)(hp + o_lSt))[(int64_t)t * b + i];
+          if (rep->block_piv) rep->block_piv[(int64_t)t * b + i] = ((const int32_t*)(hp + o_lpiv))[(int64_t)t * b + i];
+        }
+      }
+    }
+    rep->proj_ms = (float)proj;
+    rep->graph = 0;
+  }
+#undef LKD
+#undef RCD
+  return RBRP_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -681,15 +974,53 @@ int rbrp_id(const rbrp_problem* p, void* X, void* workspace, size_t ws_bytes, rb
   if (p->flags & RBRP_FORM_PAPER) return RBRP_ENOTSUP;
   if (p->greedy) return RBRP_ENOTSUP;
   if (comm && (p->row_offset % RBRP_CHUNK) != 0) return RBRP_EINVAL;
-  if (comm) return RBRP_ENOTSUP;   // distributed sampler: not yet built
   if (filter_coop_nsplit(p->d) > 148) return RBRP_ENOTSUP;   // d > 4736: one CTA per 32 columns
   Layout Ly = make_layout(p);
   if (ws_bytes < Ly.total) return RBRP_ENOMEM;
   if ((uintptr_t)workspace % 256) return RBRP_EINVAL;
   cudaStream_t s = (cudaStream_t)stream;
+  if (comm) {
+    if (p->greedy) return RBRP_ENOTSUP;
+    char* ws = (char*)workspace;
+    void* Xs[1] = {X};
+    void* Ws[1] = {W_out};
+    if (p->dtype == RBRP_F64) return run_dist<double>(1, p, Xs, &ws, &Ly, comm, s, S_out, Ws, rep);
+    return run_dist<float>(1, p, Xs, &ws, &Ly, comm, s, S_out, Ws, rep);
+  }
   if (p->dtype == RBRP_F64)
     return run<double>(p, X, (char*)workspace, Ly, comm, s, S_out, W_out, rep);
   return run<float>(p, X, (char*)workspace, Ly, comm, s, S_out, W_out, rep);
+}
+
+int rbrp_id_sharded(const rbrp_problem* p, int nshards, const int64_t* shard_rows, void* const* X,
+                    void* const* workspace, size_t ws_bytes, void* stream, int64_t* S_out,
+                    void* const* W_out, rbrp_report* rep) {
+  if (!p || nshards < 1 || nshards > 64 || !shard_rows || !X || !workspace || !S_out) return RBRP_EINVAL;
+  if (p->flags & RBRP_FORM_PAPER) return RBRP_ENOTSUP;
+  if (p->greedy) return RBRP_ENOTSUP;
+  if (filter_coop_nsplit(p->d) > 148) return RBRP_ENOTSUP;
+  std::vector<rbrp_problem> ps(nshards, *p);
+  std::vector<Layout> Ly(nshards);
+  std::vector<char*> ws(nshards);
+  int64_t off = 0;
+  for (int h = 0; h < nshards; ++h) {
+    ps[h].n_local = shard_rows[h];
+    ps[h].row_offset = off;
+    if (shard_rows[h] < 0 || (h + 1 < nshards && shard_rows[h] % RBRP_CHUNK)) return RBRP_EINVAL;
+    off += shard_rows[h];
+    int rc = validate(&ps[h]);
+    if (rc) return rc;
+    if (shard_rows[h] > 0 && !X[h]) return RBRP_EINVAL;
+    Ly[h] = make_layout(&ps[h]);
+    if (ws_bytes < Ly[h].total) return RBRP_ENOMEM;
+    ws[h] = (char*)workspace[h];
+    if (!ws[h] || (uintptr_t)ws[h] % 256) return RBRP_EINVAL;
+  }
+  if (off != p->n_global) return RBRP_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (p->dtype == RBRP_F64)
+    return run_dist<double>(nshards, ps.data(), X, ws.data(), Ly.data(), nullptr, s, S_out, W_out, rep);
+  return run_dist<float>(nshards, ps.data(), X, ws.data(), Ly.data(), nullptr, s, S_out, W_out, rep);
 }
 
 }  // extern "C"

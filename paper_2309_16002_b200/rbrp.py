@@ -27,7 +27,7 @@ STATUS = {0: "RBRP_OK", -1: "RBRP_EINVAL", -2: "RBRP_ENONFINITE", -3: "RBRP_EDEG
           -4: "RBRP_ENOMEM", -5: "RBRP_ECUDA", -6: "RBRP_ENCCL", -7: "RBRP_EREPLAY",
           -8: "RBRP_ENOTSUP"}
 
-EXPORTED = ["rbrp_version", "rbrp_strerror", "rbrp_workspace_size", "rbrp_id",
+EXPORTED = ["rbrp_version", "rbrp_strerror", "rbrp_workspace_size", "rbrp_id", "rbrp_id_sharded",
             "rbrp_comm_unique_id", "rbrp_comm_init", "rbrp_comm_destroy"]
 
 
@@ -81,6 +81,12 @@ def lib() -> ctypes.CDLL:
                               ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p,
                               ctypes.POINTER(ctypes.c_int64), ctypes.c_void_p, ctypes.POINTER(Report)]
         L.rbrp_id.restype = ctypes.c_int
+        L.rbrp_id_sharded.argtypes = [ctypes.POINTER(Problem), ctypes.c_int,
+                                      ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_void_p),
+                                      ctypes.POINTER(ctypes.c_void_p), ctypes.c_size_t, ctypes.c_void_p,
+                                      ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_void_p),
+                                      ctypes.POINTER(Report)]
+        L.rbrp_id_sharded.restype = ctypes.c_int
         L.rbrp_comm_unique_id.argtypes = [ctypes.c_void_p]
         L.rbrp_comm_init.argtypes = [ctypes.POINTER(ctypes.c_void_p), ctypes.c_void_p, ctypes.c_int,
                                      ctypes.c_int, ctypes.c_int]
@@ -226,6 +232,11 @@ def id(X: torch.Tensor, tol: Optional[float] = None, k: Optional[int] = None, b:
                    ctypes.c_void_p(W.data_ptr()) if W is not None else None, ctypes.byref(rep))
     if rc:
         raise RBRPError(rc, L.rbrp_strerror(rc).decode())
+    return _result(rep, S, W, b_t, b_pr, rho, bidx if log_blocks else None, bpiv if log_blocks else None,
+                   mb, b, log_blocks)
+
+
+def _result(rep, S, W, b_t, b_pr, rho, bidx, bpiv, mb, b, log_blocks):
     kk = rep.k
     nb = min(rep.nblocks, mb)
     blocks, pivots = [], []
@@ -241,6 +252,77 @@ def id(X: torch.Tensor, tol: Optional[float] = None, k: Optional[int] = None, b:
                   ms_phase={nm: rep.ms_phase[i] for i, nm in enumerate(PHASES)},
                   launches=rep.launches, proj_calls=rep.proj_calls, proj_ms=rep.proj_ms,
                   graph=bool(rep.graph))
+
+
+def _report(mb, b, log_blocks):
+    rep = Report()
+    b_t = (ctypes.c_int32 * mb)()
+    b_pr = (ctypes.c_int32 * mb)()
+    rho = (ctypes.c_double * mb)()
+    rep.max_blocks = mb
+    rep.b_t = ctypes.cast(b_t, ctypes.POINTER(ctypes.c_int32))
+    rep.b_prime = ctypes.cast(b_pr, ctypes.POINTER(ctypes.c_int32))
+    rep.rho = ctypes.cast(rho, ctypes.POINTER(ctypes.c_double))
+    bidx = bpiv = None
+    if log_blocks:
+        bidx = (ctypes.c_int64 * (mb * b))()
+        bpiv = (ctypes.c_int32 * (mb * b))()
+        rep.block_idx = ctypes.cast(bidx, ctypes.POINTER(ctypes.c_int64))
+        rep.block_piv = ctypes.cast(bpiv, ctypes.POINTER(ctypes.c_int32))
+    return rep, b_t, b_pr, rho, bidx, bpiv
+
+
+def id_sharded(shards: Sequence[torch.Tensor], tol: Optional[float] = None, k: Optional[int] = None,
+               b: int = 16, seed: int = 0, k_max: int = 0, tau_b: float = -1.0, with_W: bool = True,
+               replay_blocks=None, replay_pivots=None, max_blocks: int = 1024):
+    """The row-sharded (multi-GPU) algorithm over in-process shards on one device:
+    `shards` are consecutive row blocks of X (every one but the last a multiple of
+    4096 rows).  Returns (Result of shard 0 with W = None, [W_h per shard])."""
+    L = lib()
+    X0 = shards[0]
+    n_global = sum(int(x.shape[0]) for x in shards)
+    flags = 0 if with_W else RBRP_NO_W
+    p = _problem(X0, tol, k, b, seed, k_max, tau_b, flags, n_global, 0, False)
+    keep = []
+    if replay_blocks is not None:
+        flat = [int(i) for blk in replay_blocks for i in blk]
+        lens = [len(blk) for blk in replay_blocks]
+        arr = (ctypes.c_int64 * max(1, len(flat)))(*flat)
+        la = (ctypes.c_int32 * max(1, len(lens)))(*lens)
+        p.replay_blocks = ctypes.cast(arr, ctypes.POINTER(ctypes.c_int64))
+        p.replay_lens = ctypes.cast(la, ctypes.POINTER(ctypes.c_int32))
+        p.replay_nblocks = len(lens)
+        keep += [arr, la]
+        if replay_pivots is not None:
+            fp = [int(i) for blk in replay_pivots for i in blk]
+            pa = (ctypes.c_int32 * max(1, len(fp)))(*fp)
+            p.replay_pivots = ctypes.cast(pa, ctypes.POINTER(ctypes.c_int32))
+            keep.append(pa)
+    ws_bytes = 0
+    for x in shards:
+        q = _problem(x, tol, k, b, seed, k_max, tau_b, flags, n_global, 0, False)
+        sz = ctypes.c_size_t()
+        rc = L.rbrp_workspace_size(ctypes.byref(q), ctypes.byref(sz))
+        if rc:
+            raise RBRPError(rc, "workspace_size")
+        ws_bytes = max(ws_bytes, sz.value)
+    wss = [torch.empty(ws_bytes, dtype=torch.uint8, device=x.device) for x in shards]
+    k_cap = p.k_max if p.k_max > 0 else min(p.n_global, p.d)
+    Ws = [torch.empty((x.shape[0], k_cap), dtype=x.dtype, device=x.device) for x in shards] if with_W else None
+    S = torch.empty(k_cap, dtype=torch.int64)
+    rows = (ctypes.c_int64 * len(shards))(*[int(x.shape[0]) for x in shards])
+    Xp = (ctypes.c_void_p * len(shards))(*[x.data_ptr() for x in shards])
+    Wp = (ctypes.c_void_p * len(shards))(*[w.data_ptr() for w in Ws]) if Ws else None
+    Sp = (ctypes.c_void_p * len(shards))(*[w.data_ptr() for w in wss])
+    rep, b_t, b_pr, rho, bidx, bpiv = _report(max_blocks, b, True)
+    stream = torch.cuda.current_stream(X0.device).cuda_stream
+    rc = L.rbrp_id_sharded(ctypes.byref(p), len(shards), rows, Xp, Sp, ws_bytes, ctypes.c_void_p(stream),
+                           ctypes.cast(S.data_ptr(), ctypes.POINTER(ctypes.c_int64)), Wp, ctypes.byref(rep))
+    if rc:
+        raise RBRPError(rc, L.rbrp_strerror(rc).decode())
+    res = _result(rep, S, None, b_t, b_pr, rho, bidx, bpiv, max_blocks, b, True)
+    Wk = [w[:, :res.k] for w in Ws] if Ws else None
+    return res, Wk
 
 
 def id_host(X_host: torch.Tensor, device="cuda", X_dev: Optional[torch.Tensor] = None,

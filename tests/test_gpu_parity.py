@@ -264,3 +264,59 @@ def test_graph_loop_equals_eager_loop(monkeypatch):
         assert torch.equal(g.W, e.W)
         assert g.blocks == e.blocks
     assert g1.proj_ms > 0
+
+
+@cuda
+@pytest.mark.parametrize("split", [[4096, 8192, None], [4096, 4096, 4096, None], [None]])
+def test_shard_invariance(split):
+    """Row-sharded run (the multi-GPU algorithm, shards in-process): S, b', rho and
+    W rows BIT-identical to the single-GPU run for any sharding."""
+    rb = _rb()
+    cfg = small_config("c2", n=3 * 4096 + 1234, d=256, rank=40, b=16)
+    X = make(cfg, device="cuda")
+    ref = rb.id(X, tol=1e-12, b=16, seed=2)
+    rows, off = [], 0
+    for sz in split:
+        sz = cfg.n - off if sz is None else sz
+        rows.append(X[off:off + sz])
+        off += sz
+    res, Ws = rb.rbrp.id_sharded(rows, tol=1e-12, b=16, seed=2)
+    assert res.S.tolist() == ref.S.tolist() and res.k == 40
+    assert res.b_prime == ref.b_prime and res.rho == ref.rho and res.b_t == ref.b_t
+    assert res.blocks == ref.blocks
+    assert torch.equal(torch.cat(Ws, 0), ref.W)
+
+
+@cuda
+def test_sharded_replay_and_c3_duplicates():
+    """Sharded run in forced-pivot replay against the oracle on the duplicate
+    adversary (c3 construction), 3 shards."""
+    cfg = small_config("c3", n=3 * 4096 + 999, d=64, n_heavy_dirs=20, n_heavy_rows=6000, b=16)
+    Xnp = make(cfg).numpy()
+    tau = 1.2 * R.eta(Xnp, 40)
+    ores = O.rbrp(Xnp, tau=tau, b=16, seed=0)
+    X = torch.from_numpy(Xnp).cuda()
+    shards = [X[:4096], X[4096:8192], X[8192:]]
+    res, Ws = _rb().rbrp.id_sharded(shards, k=ores.k, b=16, replay_blocks=[b.S_t for b in ores.blocks],
+                                    replay_pivots=[b.piv for b in ores.blocks])
+    assert res.S.tolist() == ores.S
+    for a, blk in zip(res.rho, ores.blocks):
+        assert abs(a - blk.rho) <= 1e-10
+    W = torch.cat(Ws, 0).cpu().numpy()
+    Wo, kappa, _ = O.form_W(ores.L, ores.S, method="trsm")
+    assert np.linalg.norm(W - Wo) <= max(1e-10, 10 * kappa * 1.1e-16) * np.linalg.norm(Wo)
+
+
+@cuda
+def test_sharded_sampling_with_small_support_and_nan():
+    rb = _rb()
+    dev = torch.device("cuda")
+    Z = torch.zeros(2 * 4096 + 10, 12, dtype=torch.float64, device=dev)
+    Z[[5, 4100, 8195]] = torch.randn(3, 12, dtype=torch.float64, device=dev)
+    res, _ = rb.rbrp.id_sharded([Z[:4096], Z[4096:8192], Z[8192:]], tol=1e-14, b=8)
+    assert sorted(res.S.tolist()) == [5, 4100, 8195]
+    Y = torch.randn(4096 + 5, 8, dtype=torch.float64, device=dev)
+    Y[4099, 2] = float("inf")
+    with pytest.raises(rb.RBRPError) as e:
+        rb.rbrp.id_sharded([Y[:4096], Y[4096:]], tol=0.1, b=4)
+    assert e.value.status == -2
