@@ -2,21 +2,24 @@
 """bench.py — RBRP time-to-ID on B200 (BASELINE.json metric), one JSON line.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (rows sharded over N GPUs)
 
-A step is one complete RBRP interpolative decomposition (Alg. 2 selection to
-the tolerance + Alg. 3 W) of the config's synthetic X, already resident in
-HBM.  At N = 1 the workload is BASELINE.json configs[1] (c2: fp64 65536 x 1024,
-exactly rank-128 + 1e-8 noise, b = 32, tau = 1e-12) — the metric's
-configuration; configs[0] (c1) is the oracle-sized parity case.  Timing: W
-warm-up steps, then K steps between barrier + synchronize, CUDA events on the
-stream the library launches on, max over ranks.  X (537 MB) and the residual
-are larger than the 126 MB L2, so no explicit flush is needed.
+A step is one complete RBRP interpolative decomposition (Alg. 2 selection to the
+tolerance + Alg. 3 W) of the config's synthetic X, already resident in HBM.  At N = 1
+the workload is BASELINE.json configs[1] (c2: fp64 65536 x 1024, exactly rank-128 +
+1e-8 noise, b = 32, tau = 1e-12) — the metric's configuration; configs[0] (c1) is the
+oracle-sized parity case.  N > 1: the same problem with its rows sharded over the ranks
+(strong scaling; NCCL exchange points).  Timing: W warm-up steps, then K
+steps between barrier + synchronize, CUDA events on the stream the library launches on,
+max over ranks.  X (537 MB) and the residual are larger than the 126 MB L2, so no
+explicit flush is needed.
 
-Also reported: the roofline of the dominant projection pass (Alg. 2 l.13/l.16:
-k_lhat + k_update, timed live with CUDA events inside the library), the
-end-to-end figure through the C ABI with host buffers (pinned X -> HBM, W ->
-host inside the timed region), the kernel-launch count, the SM clocks seen by
-nvidia-smi during the timed region, and the CPU oracle timed on this host.
+Also reported: the roofline of the dominant projection pass (Alg. 2 l.13/l.16), timed
+live inside the timed region by %globaltimer stamps in the kernels (the block loop runs
+as one CUDA graph, whose body admits no event nodes); the end-to-end figure through the
+public API with host buffers (pinned X -> HBM and W -> pinned host inside the timed
+region); the kernel-launch count; the SM clocks seen by nvidia-smi during the timed
+region; the CPU oracle timed on this host (N = 1, rank 0).
 """
 from __future__ import annotations
 
@@ -33,7 +36,8 @@ sys.path.insert(0, ROOT)
 
 METRIC = ("RBRP time-to-(r,ε)-ID (s) and projection-pass HBM GB/s / roofline fraction, "
           "1–8 GPU")
-FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # DFMA units x max clock
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # FP64 units x max clock
+HBM_GBS = 6551.4                                     # MEASURED_PEAKS.json hbm_gbs
 
 
 def _args():
@@ -107,91 +111,101 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def _tau(cfg, X):
+def _tau(cfg, X, world=1):
     """tau for the config: given, or (1+eps) eta_r with eta_r from the Gram
-    eigenvalues (harness code, untimed; R3)."""
+    eigenvalues (harness code, untimed; R3).  Sharded: the Gram is summed
+    over the ranks."""
     import torch
     if cfg.tau is not None:
         return cfg.tau
     G = X.double().T @ X.double()
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(G)
     ev = torch.linalg.eigvalsh(G).flip(0).clamp_min(0)
     return float((1 + cfg.eps) * ev[cfg.r:].sum() / ev.sum())
 
 
-def _proj_roofline(cfg, res_list, phase_ms):
+def _proj_roofline(cfg, res_list, proj_ms, n_local):
     """Algorithmic flops/bytes of the projection pass: per block
-    flops = 4 n d b' + 2 n d, bytes = 2 n d w + n b' w + 8 n."""
-    n, d = cfg.n, cfg.d
+    flops = 4 n d b' + 2 n d, bytes = 2 n d w + n b' w + 8 n (n = this rank's rows)."""
+    n, d = n_local, cfg.d
     w = 8 if cfg.dtype == "f64" else 4
     flops = bytes_ = 0.0
     for res in res_list:
         for bp in res.b_prime:
             flops += 4.0 * n * d * bp + 2.0 * n * d
             bytes_ += 2.0 * n * d * w + n * bp * w + 8.0 * n
-    t = phase_ms / 1e3
-    return flops / t / 1e12, bytes_ / t / 1e9
+    t = proj_ms / 1e3
+    return flops / t / 1e12, bytes_ / t / 1e9, flops, bytes_
 
 
-def _traffic_from_profile():
+def _traffic_from_profile(cfg_name):
+    """dram bytes per block of the projection kernels from the committed ncu capture."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(p):
         try:
-            return json.load(open(p)).get("proj_dram_bytes_per_block")
+            return json.load(open(p)).get(cfg_name, {}).get("proj_dram_bytes_per_block")
         except Exception:
             return None
     return None
 
 
-def _cpu_baseline(cfg, Xnp, tau):
-    from oracle import rbrp as O
+def _workload(cfg, tau):
+    desc = {"c2": " exactly rank-128 + 1e-8 noise,"}.get(cfg.name, "")
+    return f"{cfg.name}: {cfg.dtype} n={cfg.n} d={cfg.d}{desc} b={cfg.b}, tau={tau:.3g}"
+
+
+def _threads():
     try:
         from threadpoolctl import threadpool_info
-        thr = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+        return int(max([i.get("num_threads", 1) for i in threadpool_info()] or [1]))
     except Exception:
-        thr = os.cpu_count()
+        return os.cpu_count()
+
+
+def _cpu_baseline(cfg, Xnp, tau):
+    from oracle import rbrp as O
     t = time.perf_counter()
     ores = O.rbrp(Xnp, tau=tau, b=cfg.b, seed=0)
-    ores_W = O.form_W(ores.L, ores.S, method="trsm")
+    O.form_W(ores.L, ores.S, method="trsm")
     dt = time.perf_counter() - t
-    return {"value": dt, "unit": "s", "cores": int(thr), "kind": "oracle",
-            "sample": f"one full {cfg.name} ID ({cfg.n}x{cfg.d} {cfg.dtype}, b={cfg.b}, "
-                      f"k={ores.k}) incl. W, NumPy/BLAS on {len(os.sched_getaffinity(0))} host cores"}
+    return {"value": dt, "unit": "s", "cores": _threads(), "kind": "oracle",
+            "sample": f"one full {cfg.name} ID ({cfg.n}x{cfg.d} {cfg.dtype}, b={cfg.b}, k={ores.k}) "
+                      f"incl. W, NumPy/BLAS, {len(os.sched_getaffinity(0))} host cores visible"}
 
 
 def run_reference(a):
+    """The reference arm: the CPU oracle (as it stands) on the same workload; rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     import numpy as np
+
     from oracle import rbrp as O
     from workloads import CONFIGS, make
     cfg = CONFIGS[a.config]
     X = make(cfg)
     Xnp = X.numpy()
-    import torch
     tau = _tau(cfg, X)
     for _ in range(a.warmup):
         O.rbrp(Xnp, tau=tau, b=cfg.b, seed=a.seed)
     times = []
+    r = None
     for _ in range(a.steps):
         t = time.perf_counter()
         r = O.rbrp(Xnp, tau=tau, b=cfg.b, seed=a.seed)
         O.form_W(r.L, r.S, method="trsm")
         times.append(time.perf_counter() - t)
     v = float(np.mean(times))
-    try:
-        from threadpoolctl import threadpool_info
-        thr = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
-    except Exception:
-        thr = os.cpu_count()
     line = {"metric": METRIC, "value": v, "unit": "s", "n_gpus": a.gpus, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64" if cfg.dtype == "f64" else "f32",
+            "scaling": "weak", "vs_baseline": None, "dtype": cfg.dtype,
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": f"{cfg.name}: {cfg.dtype} n={cfg.n} d={cfg.d} b={cfg.b} tau={tau:.3g}",
+            "config": {"workload": _workload(cfg, tau),
                        "n": cfg.n, "d": cfg.d, "b": cfg.b, "k": r.k},
-            "cpu_baseline": {"value": v, "unit": "s", "cores": int(thr), "kind": "oracle",
-                             "sample": f"full {cfg.name} ID per step (oracle as it stands)"},
+            "cpu_baseline": {"value": v, "unit": "s", "cores": _threads(), "kind": "oracle",
+                             "sample": f"one full {cfg.name} ID per step (CPU oracle as it stands)"},
             "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -204,6 +218,7 @@ def main():
     import torch.distributed as dist
 
     import paper_2309_16002_b200 as rb
+    from paper_2309_16002_b200 import dist as rdist
     from workloads import CONFIGS, make
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -219,13 +234,20 @@ def main():
             dist.barrier()
 
     cfg = CONFIGS[a.config]
-    # N > 1: the row-sharded NCCL path is not built yet; each rank runs a full replica
-    X = make(cfg, device=dev)
-    tau = _tau(cfg, X)
-    ws = torch.empty(rb.workspace_size(X, tol=tau, b=cfg.b), dtype=torch.uint8, device=dev)
-    Wbuf = torch.empty((cfg.n, min(cfg.n, cfg.d)), dtype=cfg.torch_dtype, device=dev)
+    # rows of X sharded over the ranks (contiguous, 4096-row aligned); every rank holds
+    # only its shard; N = 1 is the single-GPU path (CUDA-graph loop)
+    r0, n_local = rdist.partition_rows(cfg.n, world, rank)
+    X = make(cfg, device=dev, row_offset=r0, n_local=n_local)
+    tau = _tau(cfg, X, world)
+    comm = rdist.Comm(dev) if world > 1 else None
+    dkw = dict(n_global=cfg.n, row_offset=r0, comm=comm.handle) if comm else {}
+    ws = torch.empty(rb.workspace_size(X, tol=tau, b=cfg.b, n_global=cfg.n, row_offset=r0),
+                     dtype=torch.uint8, device=dev)
+    k_cap = min(cfg.n, cfg.d)
+    Wbuf = torch.empty((n_local, k_cap), dtype=cfg.torch_dtype, device=dev)
+    kw = dict(tol=tau, b=cfg.b, seed=a.seed, workspace=ws, log_blocks=False, W_out=Wbuf, **dkw)
     for _ in range(a.warmup):
-        rb.id(X, tol=tau, b=cfg.b, seed=a.seed, workspace=ws, log_blocks=False, W_out=Wbuf)
+        rb.id(X, **kw)
     torch.cuda.synchronize()
 
     clk = Clocks(local)
@@ -240,7 +262,7 @@ def main():
     clk.t0 = time.time()
     e0.record(stream)
     for _ in range(a.steps):
-        r = rb.id(X, tol=tau, b=cfg.b, seed=a.seed, workspace=ws, log_blocks=False, W_out=Wbuf)
+        r = rb.id(X, **kw)
         r.W = None
         res_list.append(r)
     e1.record(stream)
@@ -249,23 +271,18 @@ def main():
     clk.t1 = time.time()
     clk.stop()
     ms = e0.elapsed_time(e1) / a.steps
-    t = torch.tensor([ms], device=dev)
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
+        ms = rdist.max_over_ranks(ms, device=dev)
 
-    # projection-pass device time measured inside the timed region (in-kernel
-    # %globaltimer stamps, first CTA start of L-hat -> last CTA end of the update)
+    # projection-pass device time inside the timed region (in-kernel %globaltimer stamps,
+    # first CTA start of L-hat -> last CTA end of the fused update, summed over blocks)
     proj_ms = sum(r.proj_ms for r in res_list)
-    tflops, gbs = _proj_roofline(cfg, res_list, proj_ms)
+    tflops, gbs, flops, bytes_ = _proj_roofline(cfg, res_list, proj_ms, n_local)
     launches = sum(r.launches for r in res_list)
-    r0 = res_list[-1]
+    r0res = res_list[-1]
     # per-phase breakdown from one eager, event-instrumented run (outside the timed region)
-    rp = rb.id(X, tol=tau, b=cfg.b, seed=a.seed, workspace=ws, log_blocks=False, profile=True,
-               W_out=Wbuf)
+    rp = rb.id(X, profile=True, **kw)
     torch.cuda.synchronize()
-    ph = rp.ms_phase
-    ph_proj_eager = ph["lhat"] + ph["update"]
 
     e2e = None
     if not a.no_e2e:
@@ -273,9 +290,8 @@ def main():
         # (pinned host -> HBM) and reads W (n x k) back to pinned host memory
         Xh = X.cpu().pin_memory()
         Xd = torch.empty_like(X)
-        Wh = torch.empty((cfg.n, min(cfg.n, cfg.d)), dtype=cfg.torch_dtype, pin_memory=True)
+        Wh = torch.empty((n_local, k_cap), dtype=cfg.torch_dtype, pin_memory=True)
         w = 8 if cfg.dtype == "f64" else 4
-        kw = dict(tol=tau, b=cfg.b, seed=a.seed, workspace=ws, log_blocks=False, W_out=Wbuf)
         rb.id_host(Xh, X_dev=Xd, W_host=Wh, **kw)
         torch.cuda.synchronize()
         barrier()
@@ -288,145 +304,16 @@ def main():
             ks = rr.k
         f1.record(stream)
         torch.cuda.synchronize()
-        te = torch.tensor([f0.elapsed_time(f1) / a.steps], device=dev)
+        te = f0.elapsed_time(f1) / a.steps
         if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": float(te.item()) / 1e3, "unit": "s",
-               "h2d_bytes_per_step": cfg.n * cfg.d * w,
-               "d2h_bytes_per_step": cfg.n * ks * w + ks * 8}
+            te = rdist.max_over_ranks(te, device=dev)
+        e2e = {"value": te / 1e3, "unit": "s", "h2d_bytes_per_step": cfg.n * cfg.d * w,
+               "d2h_bytes_per_step": cfg.n * ks * w + ks * 8,
+               "note": "per step: X pinned host -> HBM (each rank its shard), ID, W -> pinned host"}
 
     if rank != 0:
-        return
-    import numpy as np
-    from oracle import rbrp as O
-    from workloads import CONFIGS, make
-    cfg = CONFIGS[a.config]
-    X = make(cfg)
-    Xnp = X.numpy()
-    import torch
-    tau = _tau(cfg, X)
-    for _ in range(a.warmup):
-        O.rbrp(Xnp, tau=tau, b=cfg.b, seed=a.seed)
-    times = []
-    for _ in range(a.steps):
-        t = time.perf_counter()
-        r = O.rbrp(Xnp, tau=tau, b=cfg.b, seed=a.seed)
-        O.form_W(r.L, r.S, method="trsm")
-        times.append(time.perf_counter() - t)
-    v = float(np.mean(times))
-    try:
-        from threadpoolctl import threadpool_info
-        thr = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
-    except Exception:
-        thr = os.cpu_count()
-    line = {"metric": METRIC, "value": v, "unit": "s", "n_gpus": a.gpus, "steps": a.steps,
-            "warmup": a.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64" if cfg.dtype == "f64" else "f32",
-            "data": "synthetic", "impl": "reference",
-            "config": {"workload": f"{cfg.name}: {cfg.dtype} n={cfg.n} d={cfg.d} b={cfg.b} tau={tau:.3g}",
-                       "n": cfg.n, "d": cfg.d, "b": cfg.b, "k": r.k},
-            "cpu_baseline": {"value": v, "unit": "s", "cores": int(thr), "kind": "oracle",
-                             "sample": f"full {cfg.name} ID per step (oracle as it stands)"},
-            "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
-
-
-def main():
-    a = _args()
-    if a.impl == "reference":
-        return run_reference(a)
-    import torch
-    import torch.distributed as dist
-
-    import paper_2309_16002_b200 as rb
-    from workloads import CONFIGS, make
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
-    cfg = CONFIGS[a.config]
-    # N > 1: the row-sharded NCCL path is not built yet; each rank runs a full replica
-    X = make(cfg, device=dev)
-    tau = _tau(cfg, X)
-    ws = torch.empty(rb.workspace_size(X, tol=tau, b=cfg.b), dtype=torch.uint8, device=dev)
-    Wbuf = torch.empty((cfg.n, min(cfg.n, cfg.d)), dtype=cfg.torch_dtype, device=dev)
-    for _ in range(a.warmup):
-        rb.id(X, tol=tau, b=cfg.b, seed=a.seed, workspace=ws, log_blocks=False, W_out=Wbuf)
-    torch.cuda.synchronize()
-
-    clk = Clocks(local)
-    clk.start()
-    time.sleep(0.3)
-    res_list = []
-    stream = torch.cuda.current_stream(dev)
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    barrier()
-    torch.cuda.synchronize()
-    clk.t0 = time.time()
-    e0.record(stream)
-    for _ in range(a.steps):
-        r = rb.id(X, tol=tau, b=cfg.b, seed=a.seed, workspace=ws, log_blocks=False, W_out=Wbuf)
-        r.W = None
-        res_list.append(r)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    barrier()
-    clk.t1 = time.time()
-    clk.stop()
-    ms = e0.elapsed_time(e1) / a.steps
-    t = torch.tensor([ms], device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
-
-    # projection-pass device time measured inside the timed region (in-kernel
-    # %globaltimer stamps, first CTA start of L-hat -> last CTA end of the update)
-    proj_ms = sum(r.proj_ms for r in res_list)
-    tflops, gbs = _proj_roofline(cfg, res_list, proj_ms)
-    launches = sum(r.launches for r in res_list)
-    r0 = res_list[-1]
-    # per-phase breakdown from one eager, event-instrumented run (outside the timed region)
-    rp = rb.id(X, tol=tau, b=cfg.b, seed=a.seed, workspace=ws, log_blocks=False, profile=True,
-               W_out=Wbuf)
-    torch.cuda.synchronize()
-    ph = rp.ms_phase
-    ph_proj_eager = ph["lhat"] + ph["update"]
-
-    e2e = None
-    if not a.no_e2e:
-        Xh = X.cpu().pin_memory()
-        w = 8 if cfg.dtype == "f64" else 4
-        rb.id_host(Xh, device=dev, tol=tau, b=cfg.b, seed=a.seed, workspace=ws, log_blocks=False)
-        torch.cuda.synchronize()
-        barrier()
-        f0 = torch.cuda.Event(enable_timing=True)
-        f1 = torch.cuda.Event(enable_timing=True)
-        f0.record(stream)
-        ks = 0
-        for _ in range(a.steps):
-            rr, _W = rb.id_host(Xh, device=dev, tol=tau, b=cfg.b, seed=a.seed, workspace=ws,
-                                log_blocks=False)
-            ks = rr.k
-        f1.record(stream)
-        torch.cuda.synchronize()
-        te = torch.tensor([f0.elapsed_time(f1) / a.steps], device=dev)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": float(te.item()) / 1e3, "unit": "s",
-               "h2d_bytes_per_step": cfg.n * cfg.d * w,
-               "d2h_bytes_per_step": cfg.n * ks * w + ks * 8}
-
-    if rank != 0:
+        if comm:
+            comm.close()
         if world > 1:
             dist.destroy_process_group()
         return
@@ -434,35 +321,39 @@ def main():
     if world == 1 and not a.no_cpu_baseline:
         cpu = _cpu_baseline(cfg, X.cpu().numpy(), tau)
     peak = FP64_PEAK_TFLOPS if cfg.dtype == "f64" else FP64_PEAK_TFLOPS * 2
-    traffic = _traffic_from_profile()
+    nblk = sum(len(r.b_prime) for r in res_list)
+    traffic = _traffic_from_profile(cfg.name)
     line = {
         "metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": a.steps,
-        "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
-        "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic",
-        "config": {"workload": f"{cfg.name}: {cfg.dtype} n={cfg.n} d={cfg.d} exactly rank-128 + 1e-8 "
-                               f"noise, b={cfg.b}, tau={tau:.3g}" if cfg.name == "c2" else
-                               f"{cfg.name}: {cfg.dtype} n={cfg.n} d={cfg.d} b={cfg.b} tau={tau:.3g}",
-                   "n": cfg.n, "d": cfg.d, "b": cfg.b, "tau": tau, "k": r0.k, "blocks": r0.nblocks,
-                   "b_prime": r0.b_prime, "resid_rel": r0.resid_rel,
-                   "parallelism": "single" if world == 1 else f"replicas{world}",
+        "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": False,
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+        "dtype": cfg.dtype, "data": "synthetic",
+        "config": {"workload": _workload(cfg, tau),
+                   "n": cfg.n, "d": cfg.d, "b": cfg.b, "tau": tau, "k": r0res.k, "blocks": r0res.nblocks,
+                   "b_prime": r0res.b_prime, "resid_rel": r0res.resid_rel,
+                   "parallelism": "single" if world == 1 else f"rows{world} (NCCL row sharding)",
+                   "rows_per_rank": n_local, "graph_loop": r0res.graph,
                    "l2": "inputs larger than L2 (X 537 MB + residual 537 MB vs 126 MB L2); no flush"},
-        "roofline": {"kernel": "projection pass a4 (k_nt_mma L-hat + k_update_mma fused update, Alg. 2 l.13/l.16)",
-                     "timing": "in-kernel %globaltimer stamps, summed over the blocks of the K timed steps",
+        "roofline": {"kernel": "projection pass a4 (k_nt_mma L-hat + k_update_mma fused update + norms, "
+                               "Alg. 2 l.13/l.16)",
                      "bound": "alu", "achieved": tflops, "peak": peak, "unit": "TFLOP/s",
                      "frac": tflops / peak, "traffic": traffic,
-                     "peak_note": "FP64 DFMA: 148 SM x 64 FMA/clk x 2 x 1.965 GHz (derived, DESIGN.md §6); "
-                                  "MEASURED_PEAKS.json has no FP64 entry",
-                     "algorithmic_GBs": gbs, "hbm_frac_of_measured": gbs / 6551.4,
+                     "timing": "in-kernel %globaltimer stamps, summed over the blocks of the K timed steps",
+                     "peak_note": "FP64 (DMMA = DFMA rate): 148 SM x 64 FMA/clk x 2 x 1.965 GHz, derived "
+                                  "(DESIGN.md §6); measured DMMA 37.2 TF; MEASURED_PEAKS.json has no FP64 entry",
+                     "algorithmic_flops_per_block": flops / max(nblk, 1),
+                     "algorithmic_bytes_per_block": bytes_ / max(nblk, 1),
+                     "algorithmic_GBs": gbs, "hbm_frac_of_measured": gbs / HBM_GBS,
                      "share_of_step": proj_ms / a.steps / ms},
-        "phase_ms_eager_profile": ph,
-        "proj_ms_eager_events": ph_proj_eager,
-        "graph_loop": r0.graph,
+        "phase_ms_eager_profile": rp.ms_phase,
         "gpu_launches": launches,
         "e2e": e2e,
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)
+    if comm:
+        comm.close()
     if world > 1:
         dist.destroy_process_group()
 

@@ -341,7 +341,9 @@ def id_host(X_host: torch.Tensor, device="cuda", X_dev: Optional[torch.Tensor] =
             W_host = torch.empty(res.W.shape, dtype=res.W.dtype, pin_memory=True)
             Wh = W_host
         else:
-            Wh = W_host[:, :res.k]
-        Wh.copy_(res.W, non_blocking=True)
+            # contiguous n x k view of the preallocated pinned buffer: one flat D2H copy
+            # (a strided [:, :k] host view would copy row by row)
+            Wh = W_host.view(-1)[:res.W.shape[0] * res.k].view(res.W.shape[0], res.k)
+        Wh.copy_(res.W if res.W.is_contiguous() else res.W.contiguous(), non_blocking=True)
     torch.cuda.current_stream(X_dev.device).synchronize()
     return res, Wh
