@@ -90,6 +90,13 @@ cudaError_t launch_lhat_mma(const double* Xres, int64_t ldx, const double* Qt, i
 cudaError_t launch_update_mma(double* Xres, int64_t ldx, const double* Qt, const double* L,
                               int64_t ldl, int64_t n, int64_t d, double* dvec, DevState* st,
                               int bucket, cudaStream_t s);
+// k_project_fused.cu — single-pass fused projection (L-hat, update, norms), b' <= 64
+size_t fused_pack_bytes(int64_t d);
+int fused_max_bucket(const void* X, int64_t ldx, int64_t d);
+cudaError_t launch_pack_q(const double* Qt, int64_t d, double* Qp, DevState* st, cudaStream_t s);
+cudaError_t launch_proj_fused(double* Xres, int64_t ldx, const double* Qp, double* L, int64_t ldl,
+                              int64_t n, int64_t d, double* dvec, DevState* st, int bucket,
+                              cudaStream_t s);
 bool gemm_nt_mma(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
                  int64_t M, int64_t N, int64_t K, cudaStream_t s, cudaError_t* err);
 

@@ -34,7 +34,7 @@ namespace {
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
-  size_t Xres = SIZE_MAX, dvec, cpre, ctot, cpos, cprefix, L, Qt, Vg, Gpart, G, Tg, Ag, R11, Rtot,
+  size_t Xres = SIZE_MAX, dvec, cpre, ctot, cpos, cprefix, L, Qt, Qp, Vg, Gpart, G, Tg, Ag, R11, Rtot,
          piv, mass, St, Srep, S, forced, dbg, cand, st, L1 = SIZE_MAX, LinvT = SIZE_MAX;
   size_t lbt, lbp, lrho, lSt, lpiv, lts, total;
   int nsplit, maxlog;
@@ -85,6 +85,7 @@ Layout make_layout(const rbrp_problem* p) {
   L.cprefix = take((size_t)L.nchunks * 8);
   L.L = take((size_t)n * L.k_cap * w);
   L.Qt = take(B * d * w);
+  L.Qp = take(fused_pack_bytes(d));
   L.Vg = take(B * d * 8);
   L.Gpart = take((size_t)L.nsplit * B * B * 8);
   L.G = take(B * B * 8);
@@ -186,6 +187,7 @@ struct Ctx {
   double *dvec, *cpre, *ctot, *cprefix, *Vg, *Gpart, *G, *Tg, *Ag, *R11, *Rtot, *mass;
   int32_t *cpos, *piv, *forced;
   T *Lm, *Qt;
+  double* Qp;   // packed Q_b chunks of the fused projection
   int64_t *St, *Srep, *S, *cand;
   double* L1;
   T* LinvT;
@@ -194,6 +196,7 @@ struct Ctx {
   BlockLog log;
   bool use_mma, use_forced;
   int bucketB;
+  int fused_max;   // largest bucket run by the fused single-pass projection (0: none)
 };
 
 // pointers of one shard's workspace
@@ -217,6 +220,7 @@ void make_ctx(Ctx<T>& c, const rbrp_problem* p, void* Xv, char* ws, const Layout
   c.cprefix = (double*)(ws + Ly.cprefix);
   c.Lm = (T*)(ws + Ly.L);
   c.Qt = (T*)(ws + Ly.Qt);
+  c.Qp = (double*)(ws + Ly.Qp);
   c.Vg = (double*)(ws + Ly.Vg);
   c.Gpart = (double*)(ws + Ly.Gpart);
   c.G = (double*)(ws + Ly.G);
@@ -246,6 +250,7 @@ void make_ctx(Ctx<T>& c, const rbrp_problem* p, void* Xv, char* ws, const Layout
   c.use_forced = p->replay_pivots != nullptr;
   c.use_mma = sizeof(T) == 8 && !force_simt() && projection_mma_supported(c.Xres, c.ldr, c.Qt, c.d);
   c.bucketB = bucket_of((int)std::min<int64_t>(p->b, c.k_cap));
+  c.fused_max = (c.use_mma && !env_on("RBRP_NO_FUSED")) ? fused_max_bucket(c.Xres, c.ldr, c.d) : 0;
 }
 
 template <typename T>
@@ -269,6 +274,36 @@ void make_sample_args(SampleArgs& sa, const Ctx<T>& c, int dist) {
   sa.cond = 0;
   sa.dist = dist;
   sa.cand = c.cand;
+}
+
+// a4 (Alg. 2 l.13 + l.16): one fused single-pass kernel (k_proj_fused) for the buckets
+// it supports, else the two-kernel DMMA / CUDA-core path.  Each launch is a no-op unless
+// the block's b' falls in its bucket, so the sequence is graph-capturable.
+template <typename T>
+int enqueue_projection(Ctx<T>& c, cudaStream_t s, int* nl) {
+  auto lk = [&](cudaError_t e) {
+    ++*nl;
+    return e == cudaSuccess ? (int)RBRP_OK : (int)RBRP_ECUDA;
+  };
+  int rc = RBRP_OK;
+  if (c.fused_max > 0 && (rc = lk(launch_pack_q((const double*)c.Qt, c.d, c.Qp, c.st, s)))) return rc;
+  for (int bk = 16; bk <= c.bucketB; bk *= 2) {
+    if (bk <= c.fused_max) {
+      rc = lk(launch_proj_fused((double*)c.Xres, c.ldr, c.Qp, (double*)c.Lm, c.k_cap, c.n, c.d, c.dvec,
+                                c.st, bk, s));
+    } else if (c.use_mma) {
+      rc = lk(launch_lhat_mma((const double*)c.Xres, c.ldr, (const double*)c.Qt, c.n, c.d, (double*)c.Lm,
+                              c.k_cap, c.st, bk, s));
+      if (!rc)
+        rc = lk(launch_update_mma((double*)c.Xres, c.ldr, (const double*)c.Qt, (const double*)c.Lm,
+                                  c.k_cap, c.n, c.d, c.dvec, c.st, bk, s));
+    } else {
+      rc = lk(launch_lhat<T>(c.Xres, c.ldr, c.Qt, c.n, c.d, c.Lm, c.k_cap, c.st, bk, s));
+      if (!rc) rc = lk(launch_update<T>(c.Xres, c.ldr, c.Qt, c.Lm, c.k_cap, c.n, c.d, c.dvec, c.st, bk, s));
+    }
+    if (rc) return rc;
+  }
+  return RBRP_OK;
 }
 
 // The kernels of one block (Alg. 2 l.6-16), optionally followed by the next block's
@@ -315,21 +350,9 @@ int enqueue_block(Ctx<T>& c, SampleArgs& sa, cudaStream_t s, Prof* prof, int* nl
   if (prof) prof->end();
   // a4: projection + fused norms (l.13, l.16)
   if (prof) prof->begin(3);
-  for (int bk = 16; bk <= c.bucketB; bk *= 2) {
-    if (c.use_mma)
-      LK(launch_lhat_mma((const double*)c.Xres, c.ldr, (const double*)c.Qt, c.n, c.d, (double*)c.Lm,
-                         c.k_cap, c.st, bk, s));
-    else
-      LK(launch_lhat<T>(c.Xres, c.ldr, c.Qt, c.n, c.d, c.Lm, c.k_cap, c.st, bk, s));
-  }
-  if (prof) prof->end();
-  if (prof) prof->begin(4);
-  for (int bk = 16; bk <= c.bucketB; bk *= 2) {
-    if (c.use_mma)
-      LK(launch_update_mma((double*)c.Xres, c.ldr, (const double*)c.Qt, (const double*)c.Lm, c.k_cap,
-                           c.n, c.d, c.dvec, c.st, bk, s));
-    else
-      LK(launch_update<T>(c.Xres, c.ldr, c.Qt, c.Lm, c.k_cap, c.n, c.d, c.dvec, c.st, bk, s));
+  {
+    int rc = enqueue_projection(c, s, nl);
+    if (rc) return rc;
   }
   if (prof) prof->end();
   ++*nproj;
@@ -833,16 +856,9 @@ int run_dist(int nsh, const rbrp_problem* ps, void* const* Xs, char* const* wss,
     // a4: projection, rank-local
     for (int h = 0; h < nsh; ++h) {
       Ctx<T>& c = C[h];
-      for (int bk = 16; bk <= c.bucketB; bk *= 2) {
-        if (c.use_mma) {
-          LKD(launch_lhat_mma((const double*)c.Xres, c.ldr, (const double*)c.Qt, c.n, c.d, (double*)c.Lm,
-                              c.k_cap, c.st, bk, s));
-          LKD(launch_update_mma((double*)c.Xres, c.ldr, (const double*)c.Qt, (const double*)c.Lm, c.k_cap,
-                                c.n, c.d, c.dvec, c.st, bk, s));
-        } else {
-          LKD(launch_lhat<T>(c.Xres, c.ldr, c.Qt, c.n, c.d, c.Lm, c.k_cap, c.st, bk, s));
-          LKD(launch_update<T>(c.Xres, c.ldr, c.Qt, c.Lm, c.k_cap, c.n, c.d, c.dvec, c.st, bk, s));
-        }
+      {
+        int rc = enqueue_projection(c, s, &nl);
+        if (rc) return rc;
       }
       LKD(launch_fixup<T>(c.Xres, c.ldr, c.dvec, c.Lm, c.k_cap, c.Rtot, c.S, c.n, ps[h].row_offset, c.d, c.st, s));
       LKD(launch_chunk_scan(c.dvec, c.n, c.chunk0, c.cpre, c.ctot, c.cpos, s));

@@ -320,3 +320,32 @@ def test_sharded_sampling_with_small_support_and_nan():
     with pytest.raises(rb.RBRPError) as e:
         rb.rbrp.id_sharded([Y[:4096], Y[4096:]], tol=0.1, b=4)
     assert e.value.status == -2
+
+
+@cuda
+@pytest.mark.parametrize("n,d,rank,b", [
+    (148 * 16 * 3 + 5, 1024, 40, 32),    # several tiles per CTA, ragged tail, nc = 16
+    (9000, 330, 30, 16),                 # partial last chunk (330 = 5*64 + 10)
+    (7001, 512, 100, 64),                # bucket 64 (c3-like width)
+    (40, 200, 12, 16),                   # fewer tiles than SMs
+])
+def test_fused_projection_matches_two_kernel_path(monkeypatch, n, d, rank, b):
+    """The single-pass fused projection (k_proj_fused) and the two-kernel DMMA
+    path (RBRP_NO_FUSED=1) both match the oracle in replay mode: identical S and
+    b', rho_t within 1e-10 of the oracle and of each other, W within tolerance."""
+    cfg = small_config("c2", n=n, d=d, rank=rank, b=b)
+    Xnp = make(cfg).numpy()
+    ores = O.rbrp(Xnp, tau=1e-12, b=b, seed=0)
+    monkeypatch.setenv("RBRP_NO_FUSED", "1")
+    a = _replay(Xnp, ores, np.float64, b)
+    monkeypatch.setenv("RBRP_NO_FUSED", "0")
+    f = _replay(Xnp, ores, np.float64, b)
+    assert a.S.tolist() == f.S.tolist() and a.b_prime == f.b_prime
+    assert max(abs(x - y) for x, y in zip(a.rho, f.rho)) <= 1e-10
+    # same seed, sampling path: the fused run is reproducible bit for bit
+    X = torch.from_numpy(Xnp).cuda()
+    rb = _rb()
+    s1 = rb.id(X, tol=1e-12, b=b, seed=5)
+    s2 = rb.id(X, tol=1e-12, b=b, seed=5)
+    assert s1.S.tolist() == s2.S.tolist() and s1.rho == s2.rho and torch.equal(s1.W, s2.W)
+    assert s1.k == rank
