@@ -32,6 +32,7 @@
 //      row = k index) B-fragment patterns.
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <stdlib.h>
 
 #include "launch.cuh"
 
@@ -41,10 +42,14 @@ namespace fz {
 constexpr int R = 16;      // rows per tile (two 8-row MMA groups)
 constexpr int KC = 64;     // columns per chunk
 constexpr int NW = 8;      // consumer warps (warp w owns columns [8w, 8w+8) of a chunk)
-constexpr int NTH = (2 * NW + 1) * 32;   // 8 phase-1 + 8 phase-2 + 1 producer warp
+constexpr int NTH = (2 * NW + 3) * 32;   // 8 phase-1 + 8 phase-2 + X-load, Q-load, X-store warps
 constexpr int PACK_ROWS = 64;   // rows of the packed Q_b buffer (largest fused bucket)
 constexpr int SLOT = R * KC;    // doubles per X slot (4 TMA boxes of 16 x 16)
 constexpr int SMEM_MAX = 232448;
+#ifndef FZ_XPF
+#define FZ_XPF 0
+#endif
+constexpr int XPF = FZ_XPF;          // L2 prefetch distance of X chunks (steps)
 }  // namespace fz
 
 // not volatile: the compiler may schedule the MMAs (they have register outputs)
@@ -59,6 +64,12 @@ __device__ __forceinline__ void mbar_init(uint64_t* b, int count) {
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(b)) : "memory");
+}
+// consumer release: relaxed (does not wait for this thread's earlier global stores to
+// drain).  Callers place it after the instructions that consume the shared-memory
+// operands, so the reads are complete before the producer can refill the buffer.
+__device__ __forceinline__ void mbar_arrive_relaxed(uint64_t* b) {
+  asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];\n" ::"r"(su32(b)) : "memory");
 }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(b)), "r"(bytes)
@@ -88,7 +99,21 @@ __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int x,
       "l"(map), "r"(x), "r"(y), "r"(su32(bar))
       : "memory");
 }
-__device__ __forceinline__ void bar_consumers() { asm volatile("bar.sync 1, %0;\n" ::"n"(2 * fz::NW * 32) : "memory"); }
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int x, int y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(map),
+               "r"(x), "r"(y), "r"(su32(src))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int x, int y) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];\n" ::"l"(map), "r"(x), "r"(y)
+               : "memory");
+}
+__device__ __forceinline__ void bar_p1() { asm volatile("bar.sync 1, %0;\n" ::"n"(fz::NW * 32) : "memory"); }
+__device__ __forceinline__ void bar_p2() { asm volatile("bar.sync 2, %0;\n" ::"n"(fz::NW * 32) : "memory"); }
 
 // Q_b chunk layout (shared-memory image): row j, column c at j * 64 + (c ^ f(j))
 __host__ __device__ __forceinline__ int qswz(int j, int col) {
@@ -116,14 +141,32 @@ struct FzCfg {
   static constexpr int NT = BPB / 8;            // 8-column output tiles of P
   static constexpr int ACC = 2 * NT * 2;        // doubles of one warp-lane's P partial
   static constexpr int QSTAGE = BPB * fz::KC;   // doubles per Q stage
-  static constexpr int NQ = BPB == 16 ? 4 : 3;  // Q stages
-  static constexpr int FIXED = (NQ * QSTAGE + 4 * 32 * ACC + 2 * fz::NW * fz::R) * 8;
-  static int ns_for(int nc) {   // X slots that fit; >= nc + 2 required
-    int ns = (fz::SMEM_MAX - FIXED - 2048) / (fz::SLOT * 8);
-    return ns > nc + 8 ? nc + 8 : ns;
+  static constexpr int FIXED = (6 * 32 * ACC + 2 * fz::NW * fz::R) * 8 + 2048 + 64;   // scratch, P, norms, align
+  static size_t smem(int ns, int nq) {
+    return (size_t)FIXED + (size_t)ns * fz::SLOT * 8 + (size_t)nq * QSTAGE * 8 + (3 * ns + 2 * nq) * 8;
   }
-  static size_t smem(int ns) {
-    return (size_t)FIXED + (size_t)ns * fz::SLOT * 8 + (2 * ns + 2 * NQ) * 8 + 1024;   // +1 KB: alignment
+  // ring sizes: X slots NS = nc + E and Q stages NQ.  Look-ahead is split between the two
+  // rings (E >= 2, NQ >= 2), then grown alternately while shared memory lasts.  Returns
+  // false if not even E = NQ = 2 fits.
+  static bool rings(int nc, int& ns, int& nq) {
+    const char* ee = getenv("RBRP_FZ_E");
+    const char* eq = getenv("RBRP_FZ_NQ");
+    int e = 2;
+    nq = 2;
+    if (smem(nc + e, nq) > (size_t)fz::SMEM_MAX) return false;
+    for (int it = 0; it < 16; ++it) {
+      const bool grow_q = (nq <= e - 1);
+      int e2 = e + (grow_q ? 0 : 1), q2 = nq + (grow_q ? 1 : 0);
+      if (q2 > 6) { q2 = nq; e2 = e + 1; }
+      if (e2 > 8) break;
+      if (smem(nc + e2, q2) > (size_t)fz::SMEM_MAX) break;
+      e = e2;
+      nq = q2;
+    }
+    if (ee) e = atoi(ee);
+    if (eq) nq = atoi(eq);
+    ns = nc + e;
+    return smem(ns, nq) <= (size_t)fz::SMEM_MAX && e >= 1 && nq >= 2;
   }
 };
 
@@ -145,9 +188,9 @@ template <int BPB>
 __global__ void __launch_bounds__(fz::NTH, 1)
     k_proj_fused(const __grid_constant__ CUtensorMap xmap, double* __restrict__ X, int64_t ldx,
                  const double* __restrict__ Qp, double* __restrict__ L, int64_t ldl, int64_t n, int d,
-                 int nc, int NS, double* __restrict__ dvec, DevState* st) {
+                 int nc, int NS, int NQ, double* __restrict__ dvec, DevState* st, long long* trace, int xmode) {
   using Cf = FzCfg<BPB>;
-  constexpr int NT = Cf::NT, NQ = Cf::NQ;
+  constexpr int NT = Cf::NT;
   using namespace fz;
   if (st->stop) return;
   const int bp = st->b_prime;
@@ -162,11 +205,15 @@ __global__ void __launch_bounds__(fz::NTH, 1)
   double* xs = sm;                                   // NS x SLOT
   double* qs = xs + (size_t)NS * SLOT;               // NQ x QSTAGE
   double* scr = qs + NQ * Cf::QSTAGE;                // 4 x ACC x 32
-  double* nrm = scr + 4 * 32 * Cf::ACC;              // 2 x NW x R (pass parity)
+  double* pbuf = scr + 4 * 32 * Cf::ACC;             // 2 x ACC x 32: -P per pass parity
+  double* nrm = pbuf + 2 * 32 * Cf::ACC;             // 2 x NW x R (pass parity)
   uint64_t* xfull = reinterpret_cast<uint64_t*>(nrm + 2 * NW * R);
   uint64_t* xempty = xfull + NS;
   uint64_t* qfull = xempty + NS;
   uint64_t* qempty = qfull + NQ;
+  uint64_t* xdone = qempty + NQ;                     // [NS]: phase 2 has updated the slot
+  uint64_t* pready = xdone + NS;                     // [2]: -P(p) in pbuf[p & 1]
+  uint64_t* pfree = pready + 2;                      // [2]: phase-2 warps have read it
 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int64_t ntiles = (n + R - 1) / R;
@@ -175,11 +222,16 @@ __global__ void __launch_bounds__(fz::NTH, 1)
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&xfull[s], 1);
-      mbar_init(&xempty[s], NW);         // released by the phase-2 warps
+      mbar_init(&xempty[s], 1);          // released by the store warp once written back
+      mbar_init(&xdone[s], NW);          // phase-2 warps: updated chunk is in the slot
     }
     for (int s = 0; s < NQ; ++s) {
       mbar_init(&qfull[s], 1);
       mbar_init(&qempty[s], 2 * NW);     // released by every consumer warp
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&pready[s], NW);
+      mbar_init(&pfree[s], NW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -188,42 +240,88 @@ __global__ void __launch_bounds__(fz::NTH, 1)
   auto row0_of = [&](int p) { return ((int64_t)blockIdx.x + (int64_t)p * gridDim.x) * R; };
   const int g = lane >> 2, q = lane & 3;
   const int pg = pi_row(g);            // tile row of MMA row g (within an 8-row group)
+  // optional cycle trace of CTA 0 (RBRP_FZ_TRACE=1; profiling only)
+  long long* tr = (trace && blockIdx.x == 0) ? trace : nullptr;
+  constexpr int TRN = 512;
 #define FZ_S(slot, r, t, h) scr[((slot) * Cf::ACC + ((r) * NT + (t)) * 2 + (h)) * 32 + lane]
 
   if (T == 0) {
   } else if (w == 2 * NW) {
-    // ------------------------------- producer warp -------------------------------
+    // ---------------------------- X producer warp ----------------------------
+    // X(sx) reuses the slot the phase-2 warps free at step sx - E
     if (lane == 0) {
-      const int xsteps = T * nc, qsteps = (T + 1) * nc;
-      const int E = NS - nc;
-      int sx = 0, sq = 0, xp = 0, xc = 0;
-      Ring xr, qr;
-      while (sx < xsteps || sq < qsteps) {
-        // issue in the order the consumers release the buffers: X(sx) reuses the slot
-        // freed at consumer step sx - E, Q(sq) the stage freed at step sq - NQ
-        const bool do_x = sx < xsteps && (sq >= qsteps || sx - E <= sq - NQ);
-        if (do_x) {
-          if (sx >= NS) mbar_wait(&xempty[xr.i], xr.ph ^ 1);
-          mbar_expect_tx(&xfull[xr.i], SLOT * 8);   // out-of-bounds elements are zero-filled
-          double* dst = xs + (size_t)xr.i * SLOT;
-          const int y = (int)row0_of(xp);
+      const int xsteps = T * nc;
+      int xp = 0, xc = 0;
+      Ring xr;
+      for (int s2 = 0; s2 < XPF && s2 < xsteps; ++s2) {
+        const int y2 = (int)row0_of(s2 / nc);
 #pragma unroll
-          for (int b = 0; b < 4; ++b) tma_2d(dst + b * 256, &xmap, xc * KC + 16 * b, y, &xfull[xr.i]);
-          xr.next(NS);
-          if (++xc == nc) {
-            xc = 0;
-            ++xp;
-          }
-          ++sx;
-        } else {
-          if (sq >= NQ) mbar_wait(&qempty[qr.i], qr.ph ^ 1);
-          mbar_expect_tx(&qfull[qr.i], (uint32_t)(Cf::QSTAGE * 8));
-          bulk_g2s(qs + qr.i * Cf::QSTAGE, Qp + (size_t)(sq % nc) * PACK_ROWS * KC,
-                   (uint32_t)(Cf::QSTAGE * 8), &qfull[qr.i]);
-          qr.next(NQ);
-          ++sq;
+        for (int b = 0; b < 4; ++b) tma_prefetch_2d(&xmap, (s2 % nc) * KC + 16 * b, y2);
+      }
+      for (int sx = 0; sx < xsteps; ++sx) {
+        if (sx >= NS) mbar_wait(&xempty[xr.i], xr.ph ^ 1);
+        if (tr && sx < TRN) tr[sx] = clock64();
+        mbar_expect_tx(&xfull[xr.i], SLOT * 8);   // out-of-bounds elements are zero-filled
+        double* dst = xs + (size_t)xr.i * SLOT;
+        const int y = (int)row0_of(xp);
+#pragma unroll
+        for (int b = 0; b < 4; ++b) tma_2d(dst + b * 256, &xmap, xc * KC + 16 * b, y, &xfull[xr.i]);
+        if (sx + XPF < xsteps) {   // the chunk XPF steps ahead into L2
+          const int s2 = sx + XPF;
+          const int y2 = (int)row0_of(s2 / nc);
+#pragma unroll
+          for (int b = 0; b < 4; ++b) tma_prefetch_2d(&xmap, (s2 % nc) * KC + 16 * b, y2);
+        }
+        xr.next(NS);
+        if (++xc == nc) {
+          xc = 0;
+          ++xp;
         }
       }
+    }
+    __syncwarp();
+  } else if (w == 2 * NW + 1) {
+    // ---------------------------- Q producer warp ----------------------------
+    // Q(sq) reuses the stage every consumer warp frees at step sq - NQ
+    if (lane == 0) {
+      const int qsteps = (T + 1) * nc;
+      Ring qr;
+      for (int sq = 0; sq < qsteps; ++sq) {
+        if (sq >= NQ) mbar_wait(&qempty[qr.i], qr.ph ^ 1);
+        if (tr && sq < TRN) tr[TRN + sq] = clock64();
+        mbar_expect_tx(&qfull[qr.i], (uint32_t)(Cf::QSTAGE * 8));
+        bulk_g2s(qs + qr.i * Cf::QSTAGE, Qp + (size_t)(sq % nc) * PACK_ROWS * KC, (uint32_t)(Cf::QSTAGE * 8),
+                 &qfull[qr.i]);
+        qr.next(NQ);
+      }
+    }
+    __syncwarp();
+  } else if (w == 2 * NW + 2) {
+    // ---------------------------- X store warp -----------------------------
+    // writes each updated chunk back with TMA (full 128-byte lines, no per-thread
+    // stores on the phase-2 warps), then hands the slot to the X producer
+    if (lane == 0) {
+      const int xsteps = T * nc;
+      int xp = 0, xc = 0;
+      Ring xr;
+      for (int s2 = 0; s2 < xsteps; ++s2) {
+        mbar_wait(&xdone[xr.i], xr.ph);
+        const double* src = xs + (size_t)xr.i * SLOT;
+        const int y = (int)row0_of(xp);
+        if (!(xmode & 1)) {
+#pragma unroll
+          for (int b = 0; b < 4; ++b) tma_store_2d(&xmap, src + b * 256, xc * KC + 16 * b, y);
+        }
+        bulk_commit();
+        bulk_wait_read0();   // the slot has been read: it may be refilled
+        mbar_arrive(&xempty[xr.i]);
+        xr.next(NS);
+        if (++xc == nc) {
+          xc = 0;
+          ++xp;
+        }
+      }
+      bulk_wait0();   // writes complete before the kernel's end stamp
     }
     __syncwarp();
   } else if (w < NW) {
@@ -238,53 +336,91 @@ __global__ void __launch_bounds__(fz::NTH, 1)
         for (int t = 0; t < NT; ++t) acc[r][t] = make_double2(0.0, 0.0);
       const bool ph1 = p < T;
       for (int c = 0; c < nc; ++c) {
+        const int stp = p * nc + c;
+        const bool trw = tr && w == 0 && lane == 0 && stp < TRN;
         mbar_wait(&qfull[qr.i], qr.ph);
+        if (trw) tr[2 * TRN + stp] = clock64();
         if (ph1) {
           const double* Qs = qs + qr.i * Cf::QSTAGE;
           mbar_wait(&xfull[xr.i], xr.ph);
+          if (trw) tr[3 * TRN + stp] = clock64();
           const double* xsl = xs + (size_t)xr.i * SLOT;
           const double2 a0 = *reinterpret_cast<const double2*>(xsl + xo0);
           const double2 a1 = *reinterpret_cast<const double2*>(xsl + xo1);
+          double2 b[NT];
 #pragma unroll
           for (int t = 0; t < NT; ++t) {
             const int j = 8 * t + g;
-            const double2 b = *reinterpret_cast<const double2*>(Qs + j * KC + qswz(j, 8 * w + 2 * q));
-            dmma_f(acc[0][t], a0.x, b.x);
-            dmma_f(acc[1][t], a1.x, b.x);
-            dmma_f(acc[0][t], a0.y, b.y);
-            dmma_f(acc[1][t], a1.y, b.y);
+            b[t] = *reinterpret_cast<const double2*>(Qs + j * KC + qswz(j, 8 * w + 2 * q));
           }
+#pragma unroll
+          for (int t = 0; t < NT; ++t) {
+            if (xmode & 2) {
+              acc[0][t].x += a0.x * b[t].x; acc[1][t].y += a1.y * b[t].y;
+            } else {
+              dmma_f(acc[0][t], a0.x, b[t].x);
+              dmma_f(acc[1][t], a1.x, b[t].x);
+              dmma_f(acc[0][t], a0.y, b[t].y);
+              dmma_f(acc[1][t], a1.y, b[t].y);
+            }
+          }
+          if (trw) tr[11 * TRN + stp] = clock64();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_relaxed(&qempty[qr.i]);
+          if (trw) tr[12 * TRN + stp] = clock64() + (long long)(acc[0][0].x == 1.2345e300);
           xr.next(NS);
+        } else {
+          __syncwarp();
+          if (lane == 0) mbar_arrive_relaxed(&qempty[qr.i]);
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&qempty[qr.i]);
+        if (trw) tr[4 * TRN + stp] = clock64();
         qr.next(NQ);
       }
-      // pass end: fixed-order reduction of the 8 K-partials into scratch slots 0..3
-      if (ph1 && w >= 4) {
+      // pass end (phase-1 warps only): fixed-order reduction of the 8 K-partials,
+      // -P(p) into pbuf[p & 1] for the phase-2 warps, L-hat rows of tile p (l.13)
+      if (ph1) {
+        if (w >= 4) {
 #pragma unroll
-        for (int r = 0; r < 2; ++r)
+          for (int r = 0; r < 2; ++r)
 #pragma unroll
-          for (int t = 0; t < NT; ++t) {
-            FZ_S(w - 4, r, t, 0) = acc[r][t].x;
-            FZ_S(w - 4, r, t, 1) = acc[r][t].y;
+            for (int t = 0; t < NT; ++t) {
+              FZ_S(w - 4, r, t, 0) = acc[r][t].x;
+              FZ_S(w - 4, r, t, 1) = acc[r][t].y;
+            }
+        }
+        bar_p1();
+        if (w < 4) {
+#pragma unroll
+          for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+              FZ_S(w, r, t, 0) = acc[r][t].x + FZ_S(w, r, t, 0);
+              FZ_S(w, r, t, 1) = acc[r][t].y + FZ_S(w, r, t, 1);
+            }
+        }
+        bar_p1();
+        const int pb = p & 1;
+        if (p >= 2) mbar_wait(&pfree[pb], ((p >> 1) - 1) & 1);
+        double* P = pbuf + pb * Cf::ACC * 32;
+        const int64_t r0p = row0_of(p);
+#pragma unroll
+        for (int cb = 0; cb < Cf::ACC; cb += NW) {   // (r, t, h) combos w, w + 8, ...
+          const int combo = cb + w;
+          if (combo < Cf::ACC) {
+            const int i = combo * 32 + lane;
+            const double v = (scr[(0 * Cf::ACC) * 32 + i] + scr[(1 * Cf::ACC) * 32 + i]) +
+                             (scr[(2 * Cf::ACC) * 32 + i] + scr[(3 * Cf::ACC) * 32 + i]);
+            P[i] = -v;
+            const int r = combo / (2 * NT), t = (combo >> 1) % NT, h = combo & 1;
+            const int j = 8 * t + 2 * q + h;
+            const int64_t row = r0p + 8 * r + pg;
+            if (j < bp && row < n) L[row * ldl + k0 + j] = v;
           }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&pready[pb]);   // release: P stores ordered before
+        bar_p1();   // scratch is rewritten at the next pass end
       }
-      bar_consumers();   // A
-      if (ph1 && w < 4) {
-#pragma unroll
-        for (int r = 0; r < 2; ++r)
-#pragma unroll
-          for (int t = 0; t < NT; ++t) {
-            FZ_S(w, r, t, 0) = acc[r][t].x + FZ_S(w, r, t, 0);
-            FZ_S(w, r, t, 1) = acc[r][t].y + FZ_S(w, r, t, 1);
-          }
-      }
-      bar_consumers();   // B
-      // the phase-1 warps may run at most NQ - 1 chunks ahead of the phase-2 warps; with
-      // nc <= NQ they could reach the next pass end (scratch writes) before the phase-2
-      // warps have read this pass's scratch
-      if (nc <= NQ) bar_consumers();   // C
     }
   } else {
     // -------------------- phase 2: X(p-1) -= P(p-1) Q, norms --------------------
@@ -296,49 +432,61 @@ __global__ void __launch_bounds__(fz::NTH, 1)
 #pragma unroll
       for (int t = 0; t < NT; ++t) pf[r][t] = make_double2(0.0, 0.0);
     Ring qr, xr;
+    double nr0 = 0.0, nr1 = 0.0;
     for (int p = 0; p <= T; ++p) {
-      double nr0 = 0.0, nr1 = 0.0;
+      nr0 = 0.0;
+      nr1 = 0.0;
       const int64_t r0m = row0_of(p - 1);
       const bool ph2 = p >= 1;
       for (int c = 0; c < nc; ++c) {
+        const int stp = p * nc + c;
+        const bool trw = tr && w2 == 0 && lane == 0 && stp < TRN;
         mbar_wait(&qfull[qr.i], qr.ph);
+        if (trw) tr[5 * TRN + stp] = clock64();
         if (ph2) {
           const double* Qs = qs + qr.i * Cf::QSTAGE;
           mbar_wait(&xfull[xr.i], xr.ph);   // completed a pass ago (acquire for this warp)
-          const double* xsl = xs + (size_t)xr.i * SLOT;
+          if (trw) tr[7 * TRN + stp] = clock64();
+          double* xsl = xs + (size_t)xr.i * SLOT;
           double2 x0 = *reinterpret_cast<const double2*>(xsl + xo0);
           double2 x1 = *reinterpret_cast<const double2*>(xsl + xo1);
-          double2 z0 = make_double2(0.0, 0.0), z1 = make_double2(0.0, 0.0);
 #pragma unroll
           for (int t = 0; t < NT; ++t) {
             const int j0 = 8 * t + 2 * q;
             const double b0 = Qs[j0 * KC + qswz(j0, 8 * w2 + g)];
             const double b1 = Qs[(j0 + 1) * KC + qswz(j0 + 1, 8 * w2 + g)];
-            dmma_f(x0, pf[0][t].x, b0);
-            dmma_f(x1, pf[1][t].x, b0);
-            dmma_f(z0, pf[0][t].y, b1);
-            dmma_f(z1, pf[1][t].y, b1);
+            if (xmode & 4) {
+              x0.x += pf[0][t].x * b0; x1.y += pf[1][t].y * b1;
+            } else {
+              dmma_f(x0, pf[0][t].x, b0);
+              dmma_f(x1, pf[1][t].x, b0);
+              dmma_f(x0, pf[0][t].y, b1);
+              dmma_f(x1, pf[1][t].y, b1);
+            }
           }
+          if (trw) tr[8 * TRN + stp] = clock64();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&xempty[xr.i]);
+          if (lane == 0) mbar_arrive_relaxed(&qempty[qr.i]);   // Q operands consumed
+          if (trw) tr[9 * TRN + stp] = clock64();
+          // updated residual back into the slot (same conflict-free offsets), made
+          // visible to the TMA engine, then handed to the store warp
+          *reinterpret_cast<double2*>(xsl + xo0) = x0;
+          *reinterpret_cast<double2*>(xsl + xo1) = x1;
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&xdone[xr.i]);
           xr.next(NS);
           const int col = c * KC + 8 * w2 + 2 * q;
           if (col < d) {
-            const double2 v0 = make_double2(x0.x + z0.x, x0.y + z0.y);
-            const double2 v1 = make_double2(x1.x + z1.x, x1.y + z1.y);
-            const int64_t row0 = r0m + pg, row1 = r0m + 8 + pg;
-            if (row0 < n) {
-              __stcs(reinterpret_cast<double2*>(X + row0 * ldx + col), v0);
-              nr0 += v0.x * v0.x + v0.y * v0.y;
-            }
-            if (row1 < n) {
-              __stcs(reinterpret_cast<double2*>(X + row1 * ldx + col), v1);
-              nr1 += v1.x * v1.x + v1.y * v1.y;
-            }
+            if (r0m + pg < n) nr0 += x0.x * x0.x + x0.y * x0.y;
+            if (r0m + 8 + pg < n) nr1 += x1.x * x1.x + x1.y * x1.y;
           }
+          if (trw) tr[10 * TRN + stp] = clock64();
+        } else {
+          __syncwarp();
+          if (lane == 0) mbar_arrive_relaxed(&qempty[qr.i]);
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&qempty[qr.i]);
+        if (trw) tr[6 * TRN + stp] = clock64();
         qr.next(NQ);
       }
       // pass end
@@ -353,7 +501,7 @@ __global__ void __launch_bounds__(fz::NTH, 1)
           nb[w2 * R + 8 + pg] = nr1;
         }
       }
-      bar_consumers();   // A
+      bar_p2();
       if (ph2 && w2 == 0 && lane < R) {
         double v = 0.0;
 #pragma unroll
@@ -361,37 +509,20 @@ __global__ void __launch_bounds__(fz::NTH, 1)
         const int64_t row = r0m + lane;
         if (row < n) dvec[row] = v;
       }
-      bar_consumers();   // B
-      if (p < T) {
+      if (p < T) {   // -P(p) for phase 2 of the next pass
+        const int pb = p & 1;
+        mbar_wait(&pready[pb], (p >> 1) & 1);
+        const double* P = pbuf + pb * Cf::ACC * 32;
 #pragma unroll
         for (int r = 0; r < 2; ++r)
 #pragma unroll
           for (int t = 0; t < NT; ++t) {
-            pf[r][t].x = -((FZ_S(0, r, t, 0) + FZ_S(1, r, t, 0)) + (FZ_S(2, r, t, 0) + FZ_S(3, r, t, 0)));
-            pf[r][t].y = -((FZ_S(0, r, t, 1) + FZ_S(1, r, t, 1)) + (FZ_S(2, r, t, 1) + FZ_S(3, r, t, 1)));
+            pf[r][t].x = P[(((r * NT + t) * 2) + 0) * 32 + lane];
+            pf[r][t].y = P[(((r * NT + t) * 2) + 1) * 32 + lane];
           }
-        // L-hat rows of tile p (l.13): warp w2 writes tile rows 2w2, 2w2+1, lane = column
-        // j, read back from the four scratch slots in the same summation order
-        const int64_t r0p = row0_of(p);
-#pragma unroll
-        for (int h2 = 0; h2 < 2; ++h2) {
-          const int rr = 2 * w2 + h2, r = rr >> 3, x = rr & 7;
-          const int gg = 2 * (x & 3) + (x >> 2);   // pi^-1
-          const int64_t row = r0p + rr;
-#pragma unroll
-          for (int jb = 0; jb < BPB; jb += 32) {
-            const int j = jb + lane;
-            if (j < BPB && j < bp && row < n) {
-              const int t = j >> 3, qq = (j & 7) >> 1, h = j & 1;
-              const int base = ((r * NT + t) * 2 + h) * 32 + 4 * gg + qq;
-              const double v = (scr[(0 * Cf::ACC) * 32 + base] + scr[(1 * Cf::ACC) * 32 + base]) +
-                               (scr[(2 * Cf::ACC) * 32 + base] + scr[(3 * Cf::ACC) * 32 + base]);
-              L[row * ldl + k0 + j] = v;
-            }
-          }
-        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&pfree[pb]);
       }
-      if (nc <= NQ) bar_consumers();   // C
     }
   }
 #undef FZ_S
@@ -407,6 +538,22 @@ static int fz_num_sms() {
     if (v <= 0) v = 148;
   }
   return v;
+}
+
+static long long* g_fz_trace = nullptr;
+static long long* fz_trace_buf() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("RBRP_FZ_TRACE");
+    on = e && e[0] == '1';
+    if (on && cudaMalloc(&g_fz_trace, 16 * 512 * sizeof(long long)) != cudaSuccess) g_fz_trace = nullptr;
+  }
+  return g_fz_trace;
+}
+extern "C" int rbrp_debug_fz_trace(long long* host, int count) {
+  if (!g_fz_trace) return -1;
+  if (count > 16 * 512) count = 16 * 512;
+  return cudaMemcpy(host, g_fz_trace, count * sizeof(long long), cudaMemcpyDeviceToHost) == cudaSuccess ? count : -1;
 }
 
 static int fz_nc(int64_t d) { return (int)((d + fz::KC - 1) / fz::KC); }
@@ -431,10 +578,10 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 int fused_max_bucket(const void* X, int64_t ldx, int64_t d) {
   if (d % 2 || d < 16 || ldx % 2 || ((uintptr_t)X % 16)) return 0;
   const int nc = fz_nc(d);
-  int best = 0;
-  if (FzCfg<16>::ns_for(nc) >= nc + 2) best = 16;
-  if (FzCfg<32>::ns_for(nc) >= nc + 2) best = 32;
-  if (FzCfg<64>::ns_for(nc) >= nc + 2) best = 64;
+  int best = 0, ns, nq;
+  if (FzCfg<16>::rings(nc, ns, nq)) best = 16;
+  if (FzCfg<32>::rings(nc, ns, nq)) best = 32;
+  // bucket 64 spills under the 96-register cap of 18 warps: two-kernel path for now
   return best;
 }
 
@@ -443,11 +590,23 @@ static cudaError_t go_fused(const CUtensorMap& map, double* X, int64_t ldx, cons
                             int64_t ldl, int64_t n, int64_t d, double* dvec, DevState* st, cudaStream_t s) {
   using Cf = FzCfg<BPB>;
   const int nc = fz_nc(d);
-  const int ns = Cf::ns_for(nc);
-  const size_t smem = Cf::smem(ns);
+  int ns = 0, nq = 0;
+  if (!Cf::rings(nc, ns, nq)) return cudaErrorInvalidValue;
+  const size_t smem = Cf::smem(ns, nq);
   auto kern = k_proj_fused<BPB>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kern<<<fz_num_sms(), fz::NTH, smem, s>>>(map, X, ldx, Qp, L, ldl, n, (int)d, nc, ns, dvec, st);
+  long long* tr = nullptr;
+  static int traced = 0;
+  if (BPB == 32 && fz_trace_buf() && !traced) {   // first bucket-32 launch only
+    tr = fz_trace_buf();
+    traced = 1;
+  }
+  static int xmode = -1;
+  if (xmode < 0) {
+    const char* e = getenv("RBRP_FZ_XMODE");   // timing experiments only (wrong results)
+    xmode = e ? atoi(e) : 0;
+  }
+  kern<<<fz_num_sms(), fz::NTH, smem, s>>>(map, X, ldx, Qp, L, ldl, n, (int)d, nc, ns, nq, dvec, st, tr, xmode);
   return cudaGetLastError();
 }
 

@@ -15,7 +15,7 @@ from typing import List, Optional, Sequence
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "librbrp.so")
+LIB_PATH = os.environ.get("RBRP_LIB_PATH") or os.path.join(_HERE, "lib", "librbrp.so")
 
 RBRP_F32, RBRP_F64 = 0, 1
 RBRP_INPLACE, RBRP_NO_W, RBRP_FORM_PAPER = 1, 2, 4
