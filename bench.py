@@ -334,8 +334,8 @@ def main():
                    "parallelism": "single" if world == 1 else f"rows{world} (NCCL row sharding)",
                    "rows_per_rank": n_local, "graph_loop": r0res.graph,
                    "l2": "inputs larger than L2 (X 537 MB + residual 537 MB vs 126 MB L2); no flush"},
-        "roofline": {"kernel": "projection pass a4 (k_nt_mma L-hat + k_update_mma fused update + norms, "
-                               "Alg. 2 l.13/l.16)",
+        "roofline": {"kernel": "projection pass a4 (k_proj_fused: L-hat, residual update and row norms in "
+                               "one read + one write of X_res, Alg. 2 l.13/l.16)",
                      "bound": "alu", "achieved": tflops, "peak": peak, "unit": "TFLOP/s",
                      "frac": tflops / peak, "traffic": traffic,
                      "timing": "in-kernel %globaltimer stamps, summed over the blocks of the K timed steps",
@@ -345,7 +345,7 @@ def main():
                      "algorithmic_bytes_per_block": bytes_ / max(nblk, 1),
                      "algorithmic_GBs": gbs, "hbm_frac_of_measured": gbs / HBM_GBS,
                      "share_of_step": proj_ms / a.steps / ms},
-        "phase_ms_eager_profile": rp.ms_phase,
+        "phase_ms_eager_profile": {k: v for k, v in rp.ms_phase.items() if k != "unused"},
         "gpu_launches": launches,
         "e2e": e2e,
         "cpu_baseline": cpu,

@@ -112,6 +112,15 @@ __device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int x, i
   asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];\n" ::"l"(map), "r"(x), "r"(y)
                : "memory");
 }
+// explicit 16-byte shared-memory accesses (the compiler may otherwise split them)
+__device__ __forceinline__ double2 lds2(const double* p) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(su32(p)));
+  return v;
+}
+__device__ __forceinline__ void sts2(double* p, double2 v) {
+  asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(su32(p)), "d"(v.x), "d"(v.y) : "memory");
+}
 __device__ __forceinline__ void bar_p1() { asm volatile("bar.sync 1, %0;\n" ::"n"(fz::NW * 32) : "memory"); }
 __device__ __forceinline__ void bar_p2() { asm volatile("bar.sync 2, %0;\n" ::"n"(fz::NW * 32) : "memory"); }
 
@@ -345,13 +354,13 @@ __global__ void __launch_bounds__(fz::NTH, 1)
           mbar_wait(&xfull[xr.i], xr.ph);
           if (trw) tr[3 * TRN + stp] = clock64();
           const double* xsl = xs + (size_t)xr.i * SLOT;
-          const double2 a0 = *reinterpret_cast<const double2*>(xsl + xo0);
-          const double2 a1 = *reinterpret_cast<const double2*>(xsl + xo1);
+          const double2 a0 = lds2(xsl + xo0);
+          const double2 a1 = lds2(xsl + xo1);
           double2 b[NT];
 #pragma unroll
           for (int t = 0; t < NT; ++t) {
             const int j = 8 * t + g;
-            b[t] = *reinterpret_cast<const double2*>(Qs + j * KC + qswz(j, 8 * w + 2 * q));
+            b[t] = lds2(Qs + j * KC + qswz(j, 8 * w + 2 * q));
           }
 #pragma unroll
           for (int t = 0; t < NT; ++t) {
@@ -448,8 +457,8 @@ __global__ void __launch_bounds__(fz::NTH, 1)
           mbar_wait(&xfull[xr.i], xr.ph);   // completed a pass ago (acquire for this warp)
           if (trw) tr[7 * TRN + stp] = clock64();
           double* xsl = xs + (size_t)xr.i * SLOT;
-          double2 x0 = *reinterpret_cast<const double2*>(xsl + xo0);
-          double2 x1 = *reinterpret_cast<const double2*>(xsl + xo1);
+          double2 x0 = lds2(xsl + xo0);
+          double2 x1 = lds2(xsl + xo1);
 #pragma unroll
           for (int t = 0; t < NT; ++t) {
             const int j0 = 8 * t + 2 * q;
@@ -470,8 +479,8 @@ __global__ void __launch_bounds__(fz::NTH, 1)
           if (trw) tr[9 * TRN + stp] = clock64();
           // updated residual back into the slot (same conflict-free offsets), made
           // visible to the TMA engine, then handed to the store warp
-          *reinterpret_cast<double2*>(xsl + xo0) = x0;
-          *reinterpret_cast<double2*>(xsl + xo1) = x1;
+          sts2(xsl + xo0, x0);
+          sts2(xsl + xo1, x1);
           fence_proxy_async();
           __syncwarp();
           if (lane == 0) mbar_arrive(&xdone[xr.i]);

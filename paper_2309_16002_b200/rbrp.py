@@ -53,7 +53,7 @@ class Report(ctypes.Structure):
                 ("launches", ctypes.c_int32), ("proj_calls", ctypes.c_int32),
                 ("proj_ms", ctypes.c_float), ("graph", ctypes.c_int32)]
 
-PHASES = ["init", "sample", "filter", "lhat", "update", "fixup_scan", "W", "comm"]
+PHASES = ["init", "sample", "filter", "projection", "unused", "fixup_scan", "W", "comm"]
 
 
 class RBRPError(RuntimeError):
