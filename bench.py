@@ -50,6 +50,9 @@ def _args():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--form", default="residual", choices=["residual", "paper"],
+                    help="residual: north_star hot path (default); paper: Alg. 2 literally (NEXT-1)")
+    ap.add_argument("--no-alt-form", action="store_true", help="skip the side measurement of the other form")
     return ap.parse_args()
 
 
@@ -126,16 +129,22 @@ def _tau(cfg, X, world=1):
     return float((1 + cfg.eps) * ev[cfg.r:].sum() / ev.sum())
 
 
-def _proj_roofline(cfg, res_list, proj_ms, n_local):
-    """Algorithmic flops/bytes of the projection pass: per block
-    flops = 4 n d b' + 2 n d, bytes = 2 n d w + n b' w + 8 n (n = this rank's rows)."""
+def _proj_roofline(cfg, res_list, proj_ms, n_local, form="residual"):
+    """Algorithmic flops/bytes of the projection pass, per block:
+    residual form: flops = 4 n d b' + 2 n d, bytes = 2 n d w + n b' w + 8 n;
+    paper form (NEXT-1, read-only pass): flops = 2 n d b' + 2 n b',
+    bytes = n d w + n b' w + 16 n (n = this rank's rows)."""
     n, d = n_local, cfg.d
     w = 8 if cfg.dtype == "f64" else 4
     flops = bytes_ = 0.0
     for res in res_list:
         for bp in res.b_prime:
-            flops += 4.0 * n * d * bp + 2.0 * n * d
-            bytes_ += 2.0 * n * d * w + n * bp * w + 8.0 * n
+            if form == "paper":
+                flops += 2.0 * n * d * bp + 2.0 * n * bp
+                bytes_ += n * d * w + n * bp * w + 16.0 * n
+            else:
+                flops += 4.0 * n * d * bp + 2.0 * n * d
+                bytes_ += 2.0 * n * d * w + n * bp * w + 8.0 * n
     t = proj_ms / 1e3
     return flops / t / 1e12, bytes_ / t / 1e9, flops, bytes_
 
@@ -245,7 +254,7 @@ def main():
                      dtype=torch.uint8, device=dev)
     k_cap = min(cfg.n, cfg.d)
     Wbuf = torch.empty((n_local, k_cap), dtype=cfg.torch_dtype, device=dev)
-    kw = dict(tol=tau, b=cfg.b, seed=a.seed, workspace=ws, log_blocks=False, W_out=Wbuf, **dkw)
+    kw = dict(tol=tau, b=cfg.b, seed=a.seed, workspace=ws, log_blocks=False, W_out=Wbuf, form=a.form, **dkw)
     for _ in range(a.warmup):
         rb.id(X, **kw)
     torch.cuda.synchronize()
@@ -277,7 +286,7 @@ def main():
     # projection-pass device time inside the timed region (in-kernel %globaltimer stamps,
     # first CTA start of L-hat -> last CTA end of the fused update, summed over blocks)
     proj_ms = sum(r.proj_ms for r in res_list)
-    tflops, gbs, flops, bytes_ = _proj_roofline(cfg, res_list, proj_ms, n_local)
+    tflops, gbs, flops, bytes_ = _proj_roofline(cfg, res_list, proj_ms, n_local, a.form)
     launches = sum(r.launches for r in res_list)
     r0res = res_list[-1]
     # per-phase breakdown from one eager, event-instrumented run (outside the timed region)
@@ -310,6 +319,38 @@ def main():
         e2e = {"value": te / 1e3, "unit": "s", "h2d_bytes_per_step": cfg.n * cfg.d * w,
                "d2h_bytes_per_step": cfg.n * ks * w + ks * 8,
                "note": "per step: X pinned host -> HBM (each rank its shard), ID, W -> pinned host"}
+
+    alt = None
+    if not a.no_alt_form:
+        # side measurement of the other form of Alg. 2 on the same input (not the headline)
+        other = "paper" if a.form == "residual" else "residual"
+        kw2 = dict(kw, form=other)
+        for _ in range(2):
+            rb.id(X, **kw2)
+        torch.cuda.synchronize()
+        barrier()
+        g0 = torch.cuda.Event(enable_timing=True)
+        g1 = torch.cuda.Event(enable_timing=True)
+        ns = max(1, min(a.steps, 10))
+        rl2 = []
+        g0.record(stream)
+        for _ in range(ns):
+            r2 = rb.id(X, **kw2)
+            r2.W = None
+            rl2.append(r2)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        t2 = g0.elapsed_time(g1) / ns
+        if world > 1:
+            t2 = rdist.max_over_ranks(t2, device=dev)
+        pm2 = sum(r.proj_ms for r in rl2)
+        tf2, gb2, _, _ = _proj_roofline(cfg, rl2, pm2, n_local, other)
+        alt = {"form": other, "value": t2 / 1e3, "unit": "s", "steps": ns, "k": rl2[-1].k,
+               "b_prime": rl2[-1].b_prime, "resid_rel": rl2[-1].resid_rel,
+               "proj_tflops": tf2, "proj_frac_fp64": tf2 / FP64_PEAK_TFLOPS,
+               "proj_hbm_GBs": gb2, "proj_share": pm2 / ns / t2,
+               "note": ("paper: Alg. 2 literally (X read only, CGS2 l.6, downdated norms l.16; "
+                        "SURVEY NEXT-1)" if other == "paper" else "residual: north_star form")}
 
     if rank != 0:
         if comm:
@@ -347,6 +388,7 @@ def main():
                      "share_of_step": proj_ms / a.steps / ms},
         "phase_ms_eager_profile": {k: v for k, v in rp.ms_phase.items() if k != "unused"},
         "gpu_launches": launches,
+        "alt_form": alt,
         "e2e": e2e,
         "cpu_baseline": cpu,
         "clocks": clk.summary(),

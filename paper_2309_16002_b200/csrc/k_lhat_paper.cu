@@ -1,0 +1,358 @@
+// k_lhat_paper.cu — l.13 + l.16 of Alg. 2 in the paper-literal form (RBRP_FORM_PAPER,
+// SURVEY §8(f) NEXT-1): one read-only pass over X per block,
+//
+//     L-hat = X Q_b^T  (n x b', written to L[:, k : k+b'])            (l.13)
+//     d(i) <- max(0, d(i) - ||L-hat(i,:)||^2)                          (l.16, R14)
+//
+// on the FP64 tensor path (DMMA).  No tile has to stay resident (nothing is written back),
+// so tiles are 64 rows tall: every Q_b chunk fetched from L2 serves 64 rows (4x the reuse
+// of the residual-form kernel, whose 16-row tiles are bounded by shared memory).
+//
+// Persistent CTAs, one per SM; 16 consumer warps = 4 row pairs (16 rows each) x 4 column
+// groups (16 columns of every 64-column chunk: a K split); an X-producer warp (four TMA
+// boxes of 16 columns x 64 rows, 128-byte swizzle) and a Q-producer warp (one bulk copy of
+// the pre-packed chunk, layout of k_pack_q) on mbarrier full/empty rings.  At the end of
+// a tile the four K-partials of each row pair are folded in a fixed order
+// ((c0 + c2) + (c1 + c3)): bitwise reproducible.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "launch.cuh"
+
+namespace rbrp {
+
+namespace lp {
+constexpr int R = 64;            // rows per tile
+constexpr int KC = 64;           // columns per chunk
+constexpr int NCW = 4;           // column groups (16 columns each)
+constexpr int NRP = 4;           // row pairs (16 rows each)
+constexpr int NCONS = NCW * NRP; // consumer warps
+constexpr int NTH = (NCONS + 2) * 32;
+constexpr int SLOT = R * KC;     // doubles per X slot (4 boxes of 64 rows x 16 columns)
+constexpr int BOX = R * 16;      // doubles per box
+constexpr int PACK_ROWS = 64;    // rows of the packed Q_b buffer (k_pack_q)
+constexpr int SMEM_MAX = 232448;
+}  // namespace lp
+
+__device__ __forceinline__ void lp_dmma(double2& d, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d.x), "+d"(d.y)
+      : "d"(a), "d"(b));
+}
+__device__ __forceinline__ uint32_t lp_su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void lp_init(uint64_t* b, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(lp_su32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void lp_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(lp_su32(b)) : "memory");
+}
+__device__ __forceinline__ void lp_expect(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(lp_su32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void lp_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "W_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra W_%=;\n"
+      "}\n" ::"r"(lp_su32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ double2 lp_lds2(const double* p) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(lp_su32(p)));
+  return v;
+}
+__device__ __forceinline__ void lp_bar() { asm volatile("bar.sync 1, %0;\n" ::"n"(lp::NCONS * 32) : "memory"); }
+// Q chunk layout of k_pack_q: row j, column c at j * 64 + (c ^ f(j))
+__device__ __forceinline__ int lp_qswz(int j, int col) { return col ^ (8 * (j & 1)) ^ (4 * ((j >> 1) & 3)); }
+// X slot: box (col >> 4) of 64 rows x 16 doubles, 128-byte swizzle of 16-byte chunks by row
+__device__ __forceinline__ int lp_xoff(int row, int col) {
+  return (col >> 4) * lp::BOX + row * 16 + ((((col & 15) >> 1) ^ (row & 7)) << 1);
+}
+
+struct LpRing {
+  int i = 0, ph = 0;
+  __device__ __forceinline__ void next(int n) {
+    if (++i == n) {
+      i = 0;
+      ph ^= 1;
+    }
+  }
+};
+
+template <int BPB>
+struct LpCfg {
+  static constexpr int NT = BPB / 8;
+  static constexpr int ACC = 2 * NT * 2;          // doubles per lane of a row pair's partial
+  static constexpr int QSTAGE = BPB * lp::KC;
+  static constexpr int SCR = lp::NRP * 2 * ACC * 32;   // two partial slots per row pair
+  static size_t smem(int ns, int nq) {
+    return (size_t)ns * lp::SLOT * 8 + (size_t)nq * QSTAGE * 8 + (size_t)SCR * 8 + (2 * ns + 2 * nq) * 8 + 1024;
+  }
+  static bool rings(int& ns, int& nq) {
+    ns = 4;
+    nq = 4;
+    while (smem(ns, nq) > (size_t)lp::SMEM_MAX && nq > 2) --nq;
+    while (smem(ns, nq) > (size_t)lp::SMEM_MAX && ns > 2) --ns;
+    return smem(ns, nq) <= (size_t)lp::SMEM_MAX;
+  }
+};
+
+template <int BPB>
+__global__ void __launch_bounds__(lp::NTH, 1)
+    k_lhat_paper(const __grid_constant__ CUtensorMap xmap, const double* __restrict__ Qp,
+                 double* __restrict__ L, int64_t ldl, int64_t n, int d, int nc, int NS, int NQ,
+                 double* __restrict__ dvec, DevState* st) {
+  using Cf = LpCfg<BPB>;
+  constexpr int NT = Cf::NT;
+  using namespace lp;
+  if (st->stop) return;
+  const int bp = st->b_prime;
+  if (bp <= 0 || bucket_of(bp) != BPB) return;
+  const int64_t k0 = st->k;
+  if (blockIdx.x == 0 && threadIdx.x == 0) st->ts0 = gtimer();
+
+  extern __shared__ __align__(1024) double sm_raw[];
+  double* sm = sm_raw + ((1024u - (lp_su32(sm_raw) & 1023u)) & 1023u) / 8;
+  double* xs = sm;                                   // NS x SLOT
+  double* qs = xs + (size_t)NS * SLOT;               // NQ x QSTAGE
+  double* scr = qs + (size_t)NQ * Cf::QSTAGE;        // [rp][slot 0..1][ACC][32]
+  uint64_t* xfull = reinterpret_cast<uint64_t*>(scr + Cf::SCR);
+  uint64_t* xempty = xfull + NS;
+  uint64_t* qfull = xempty + NS;
+  uint64_t* qempty = qfull + NQ;
+
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int64_t ntiles = (n + R - 1) / R;
+  const int T = ntiles > blockIdx.x ? (int)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) {
+      lp_init(&xfull[s], 1);
+      lp_init(&xempty[s], NCONS);
+    }
+    for (int s = 0; s < NQ; ++s) {
+      lp_init(&qfull[s], 1);
+      lp_init(&qempty[s], NCONS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  auto row0_of = [&](int p) { return ((int64_t)blockIdx.x + (int64_t)p * gridDim.x) * R; };
+  const int steps = T * nc;
+
+  if (T == 0) {
+  } else if (w == NCONS) {
+    // X producer
+    if (lane == 0) {
+      LpRing xr;
+      for (int s = 0; s < steps; ++s) {
+        if (s >= NS) lp_wait(&xempty[xr.i], xr.ph ^ 1);
+        lp_expect(&xfull[xr.i], SLOT * 8);   // out-of-bounds rows / columns are zero-filled
+        double* dst = xs + (size_t)xr.i * SLOT;
+        const int y = (int)row0_of(s / nc), c = s % nc;
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, "
+              "{%2, %3}], [%4];\n" ::"r"(lp_su32(dst + b * BOX)),
+              "l"(&xmap), "r"(c * KC + 16 * b), "r"(y), "r"(lp_su32(&xfull[xr.i]))
+              : "memory");
+        xr.next(NS);
+      }
+    }
+    __syncwarp();
+  } else if (w == NCONS + 1) {
+    // Q producer (the packed Q_b chunk c is the same for every tile)
+    if (lane == 0) {
+      LpRing qr;
+      for (int s = 0; s < steps; ++s) {
+        if (s >= NQ) lp_wait(&qempty[qr.i], qr.ph ^ 1);
+        lp_expect(&qfull[qr.i], (uint32_t)(Cf::QSTAGE * 8));
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                lp_su32(qs + (size_t)qr.i * Cf::QSTAGE)),
+            "l"(Qp + (size_t)(s % nc) * PACK_ROWS * KC), "r"((uint32_t)(Cf::QSTAGE * 8)),
+            "r"(lp_su32(&qfull[qr.i]))
+            : "memory");
+        qr.next(NQ);
+      }
+    }
+    __syncwarp();
+  } else {
+    // consumers: warp = (row pair rp, column group cw)
+    const int rp = w >> 2, cw = w & 3;
+    const int g = lane >> 2, q = lane & 3;
+    const int pg = (g >> 1) + 4 * (g & 1);   // tile row of MMA row g (bank-conflict-free)
+    int xo[2][2];                            // [row group][8-column half]
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) xo[r][h] = lp_xoff(16 * rp + 8 * r + pg, 16 * cw + 8 * h + 2 * q);
+    double2 acc[2][NT];
+    LpRing qr, xr;
+    for (int p = 0; p < T; ++p) {
+#pragma unroll
+      for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int t = 0; t < NT; ++t) acc[r][t] = make_double2(0.0, 0.0);
+      for (int c = 0; c < nc; ++c) {
+        lp_wait(&qfull[qr.i], qr.ph);
+        lp_wait(&xfull[xr.i], xr.ph);
+        const double* xsl = xs + (size_t)xr.i * SLOT;
+        const double* Qs = qs + (size_t)qr.i * Cf::QSTAGE;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const double2 a0 = lp_lds2(xsl + xo[0][h]);
+          const double2 a1 = lp_lds2(xsl + xo[1][h]);
+#pragma unroll
+          for (int t = 0; t < NT; ++t) {
+            const int j = 8 * t + g;
+            const double2 b = lp_lds2(Qs + j * KC + lp_qswz(j, 16 * cw + 8 * h + 2 * q));
+            lp_dmma(acc[0][t], a0.x, b.x);
+            lp_dmma(acc[1][t], a1.x, b.x);
+            lp_dmma(acc[0][t], a0.y, b.y);
+            lp_dmma(acc[1][t], a1.y, b.y);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) {   // operands consumed (they fed the MMAs): release both buffers
+          lp_arrive(&xempty[xr.i]);
+          lp_arrive(&qempty[qr.i]);
+        }
+        xr.next(NS);
+        qr.next(NQ);
+      }
+      // tile end: P = (c0 + c2) + (c1 + c3) per row pair, in registers of the cw = 0 warp
+      double* sl = scr + (size_t)rp * 2 * Cf::ACC * 32;
+#define LP_S(slot, r, t, hh) sl[((slot) * Cf::ACC + ((r) * NT + (t)) * 2 + (hh)) * 32 + lane]
+      if (cw >= 2) {
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+          for (int t = 0; t < NT; ++t) {
+            LP_S(cw - 2, r, t, 0) = acc[r][t].x;
+            LP_S(cw - 2, r, t, 1) = acc[r][t].y;
+          }
+      }
+      lp_bar();
+      if (cw < 2) {
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+          for (int t = 0; t < NT; ++t) {
+            acc[r][t].x += LP_S(cw, r, t, 0);
+            acc[r][t].y += LP_S(cw, r, t, 1);
+          }
+      }
+      lp_bar();
+      if (cw == 1) {
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+          for (int t = 0; t < NT; ++t) {
+            LP_S(0, r, t, 0) = acc[r][t].x;
+            LP_S(0, r, t, 1) = acc[r][t].y;
+          }
+      }
+      lp_bar();
+      if (cw == 0) {
+        const int64_t r0 = row0_of(p) + 16 * rp;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          double ss = 0.0;
+          const int64_t row = r0 + 8 * r + pg;
+#pragma unroll
+          for (int t = 0; t < NT; ++t) {
+            const double vx = acc[r][t].x + LP_S(0, r, t, 0);
+            const double vy = acc[r][t].y + LP_S(0, r, t, 1);
+            const int j = 8 * t + 2 * q;
+            if (row < n) {
+              if (j < bp) L[row * ldl + k0 + j] = vx;
+              if (j + 1 < bp) L[row * ldl + k0 + j + 1] = vy;
+            }
+            ss += vx * vx + vy * vy;
+          }
+          // l.16 downdate: sum over the row's columns (q lanes), j ascending per lane
+          ss += __shfl_xor_sync(0xffffffffu, ss, 1);
+          ss += __shfl_xor_sync(0xffffffffu, ss, 2);
+          if (q == 0 && row < n) dvec[row] = fmax(dvec[row] - ss, 0.0);
+        }
+      }
+#undef LP_S
+      lp_bar();   // scratch is rewritten at the next tile end
+    }
+  }
+  proj_end_stamp(st);
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 lp_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    cudaDriverEntryPointQueryResult qr;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) == cudaSuccess &&
+        qr == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+  }
+  return fn;
+}
+
+static int lp_sms() {
+  static int v = 0;
+  if (!v) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    if (v <= 0) v = 148;
+  }
+  return v;
+}
+
+int lhat_paper_max_bucket(const void* X, int64_t ldx, int64_t d) {
+  if (d % 2 || d < 16 || ldx % 2 || ((uintptr_t)X % 16)) return 0;
+  int ns, nq, best = 0;
+  if (LpCfg<16>::rings(ns, nq)) best = 16;
+  if (LpCfg<32>::rings(ns, nq)) best = 32;
+  return best;
+}
+
+template <int BPB>
+static cudaError_t go_lp(const CUtensorMap& map, const double* Qp, double* L, int64_t ldl, int64_t n,
+                         int64_t d, double* dvec, DevState* st, cudaStream_t s) {
+  using Cf = LpCfg<BPB>;
+  int ns, nq;
+  if (!Cf::rings(ns, nq)) return cudaErrorInvalidValue;
+  const size_t smem = Cf::smem(ns, nq);
+  cudaFuncSetAttribute(k_lhat_paper<BPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int nc = (int)((d + lp::KC - 1) / lp::KC);
+  k_lhat_paper<BPB><<<lp_sms(), lp::NTH, smem, s>>>(map, Qp, L, ldl, n, (int)d, nc, ns, nq, dvec, st);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_lhat_paper(const double* X, int64_t ldx, const double* Qp, double* L, int64_t ldl,
+                              int64_t n, int64_t d, double* dvec, DevState* st, int bucket, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  auto enc = lp_encode();
+  if (!enc) return cudaErrorNotSupported;
+  CUtensorMap map;
+  const cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)n};
+  const cuuint64_t strides[1] = {(cuuint64_t)ldx * 8};
+  const cuuint32_t box[2] = {16, (cuuint32_t)lp::R};
+  const cuuint32_t estr[2] = {1, 1};
+  if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)X, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+      CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  switch (bucket) {
+    case 16: return go_lp<16>(map, Qp, L, ldl, n, d, dvec, st, s);
+    case 32: return go_lp<32>(map, Qp, L, ldl, n, d, dvec, st, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace rbrp

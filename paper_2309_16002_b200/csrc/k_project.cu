@@ -270,7 +270,8 @@ __global__ void __launch_bounds__(256) k_fixup(T* __restrict__ X, int64_t ldx,
   const int64_t k0 = st->k;
   const int64_t r = S[k0 + i] - row_offset;
   if (r < 0 || r >= n_local) return;
-  for (int64_t c = threadIdx.x; c < d; c += blockDim.x) X[r * ldx + c] = T(0);
+  if (X)   // residual form: the skeleton's residual row is 0 (paper form: X is read only)
+    for (int64_t c = threadIdx.x; c < d; c += blockDim.x) X[r * ldx + c] = T(0);
   for (int j = threadIdx.x; j < bp; j += blockDim.x)
     L[r * ldl + k0 + j] = (j <= i) ? (T)Rtot[j * kMaxB + i] : T(0);
   if (threadIdx.x == 0) dvec[r] = 0.0;

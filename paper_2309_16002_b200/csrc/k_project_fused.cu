@@ -122,6 +122,7 @@ __device__ __forceinline__ void sts2(double* p, double2 v) {
   asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(su32(p)), "d"(v.x), "d"(v.y) : "memory");
 }
 __device__ __forceinline__ void bar_p1() { asm volatile("bar.sync 1, %0;\n" ::"n"(fz::NW * 32) : "memory"); }
+__device__ __forceinline__ void bar_p1x() { asm volatile("bar.sync 3, %0;\n" ::"n"(2 * fz::NW * 32) : "memory"); }
 __device__ __forceinline__ void bar_p2() { asm volatile("bar.sync 2, %0;\n" ::"n"(fz::NW * 32) : "memory"); }
 
 // Q_b chunk layout (shared-memory image): row j, column c at j * 64 + (c ^ f(j))
@@ -157,7 +158,13 @@ struct FzCfg {
   // ring sizes: X slots NS = nc + E and Q stages NQ.  Look-ahead is split between the two
   // rings (E >= 2, NQ >= 2), then grown alternately while shared memory lasts.  Returns
   // false if not even E = NQ = 2 fits.
-  static bool rings(int nc, int& ns, int& nq) {
+  static bool rings(int nc, int& ns, int& nq, bool paper = false) {
+    if (paper) {   // streaming X ring (no tile residency): fixed look-ahead
+      ns = 12;
+      nq = 5;
+      while (smem(ns, nq) > (size_t)fz::SMEM_MAX && ns > 4) --ns;
+      return smem(ns, nq) <= (size_t)fz::SMEM_MAX;
+    }
     const char* ee = getenv("RBRP_FZ_E");
     const char* eq = getenv("RBRP_FZ_NQ");
     int e = 2;
@@ -197,7 +204,8 @@ template <int BPB>
 __global__ void __launch_bounds__(fz::NTH, 1)
     k_proj_fused(const __grid_constant__ CUtensorMap xmap, double* __restrict__ X, int64_t ldx,
                  const double* __restrict__ Qp, double* __restrict__ L, int64_t ldl, int64_t n, int d,
-                 int nc, int NS, int NQ, double* __restrict__ dvec, DevState* st, long long* trace, int xmode) {
+                 int nc, int NS, int NQ, double* __restrict__ dvec, DevState* st, long long* trace, int xmode,
+                 int paper) {
   using Cf = FzCfg<BPB>;
   constexpr int NT = Cf::NT;
   using namespace fz;
@@ -231,12 +239,12 @@ __global__ void __launch_bounds__(fz::NTH, 1)
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&xfull[s], 1);
-      mbar_init(&xempty[s], 1);          // released by the store warp once written back
+      mbar_init(&xempty[s], paper ? NW : 1);   // store warp once written back (paper: phase 1)
       mbar_init(&xdone[s], NW);          // phase-2 warps: updated chunk is in the slot
     }
     for (int s = 0; s < NQ; ++s) {
       mbar_init(&qfull[s], 1);
-      mbar_init(&qempty[s], 2 * NW);     // released by every consumer warp
+      mbar_init(&qempty[s], paper ? NW : 2 * NW);   // released by every consumer warp
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&pready[s], NW);
@@ -293,7 +301,7 @@ __global__ void __launch_bounds__(fz::NTH, 1)
     // ---------------------------- Q producer warp ----------------------------
     // Q(sq) reuses the stage every consumer warp frees at step sq - NQ
     if (lane == 0) {
-      const int qsteps = (T + 1) * nc;
+      const int qsteps = (T + (paper ? 0 : 1)) * nc;
       Ring qr;
       for (int sq = 0; sq < qsteps; ++sq) {
         if (sq >= NQ) mbar_wait(&qempty[qr.i], qr.ph ^ 1);
@@ -309,7 +317,7 @@ __global__ void __launch_bounds__(fz::NTH, 1)
     // ---------------------------- X store warp -----------------------------
     // writes each updated chunk back with TMA (full 128-byte lines, no per-thread
     // stores on the phase-2 warps), then hands the slot to the X producer
-    if (lane == 0) {
+    if (lane == 0 && !paper) {
       const int xsteps = T * nc;
       int xp = 0, xc = 0;
       Ring xr;
@@ -333,12 +341,16 @@ __global__ void __launch_bounds__(fz::NTH, 1)
       bulk_wait0();   // writes complete before the kernel's end stamp
     }
     __syncwarp();
-  } else if (w < NW) {
+  } else if (w < NW || (paper && w < 2 * NW)) {
     // ------------------------- phase 1: P(p) += X(p) Q^T -------------------------
-    const int xo0 = xoff(pg, 8 * w + 2 * q), xo1 = xoff(8 + pg, 8 * w + 2 * q);
+    // paper form: the phase-2 warps are free, so 16 warps run phase 1 as two sets that
+    // take alternate chunks (set = w >> 3); the 16 K-partials are folded in fixed order
+    const int set = w >> 3, cw = w & 7, nset = paper ? 2 : 1;
+    const int xo0 = xoff(pg, 8 * cw + 2 * q), xo1 = xoff(8 + pg, 8 * cw + 2 * q);
     double2 acc[2][NT];   // acc[r][t] = P[8r+pi(g)][8t+2q+{0,1}] (K-partial of this warp)
     Ring qr, xr;
-    for (int p = 0; p <= T; ++p) {
+    const int passes = paper ? T : T + 1;
+    for (int p = 0; p < passes; ++p) {
 #pragma unroll
       for (int r = 0; r < 2; ++r)
 #pragma unroll
@@ -347,6 +359,11 @@ __global__ void __launch_bounds__(fz::NTH, 1)
       for (int c = 0; c < nc; ++c) {
         const int stp = p * nc + c;
         const bool trw = tr && w == 0 && lane == 0 && stp < TRN;
+        if (nset == 2 && (c & 1) != set) {   // the other set's chunk
+          qr.next(NQ);
+          xr.next(NS);
+          continue;
+        }
         mbar_wait(&qfull[qr.i], qr.ph);
         if (trw) tr[2 * TRN + stp] = clock64();
         if (ph1) {
@@ -360,7 +377,7 @@ __global__ void __launch_bounds__(fz::NTH, 1)
 #pragma unroll
           for (int t = 0; t < NT; ++t) {
             const int j = 8 * t + g;
-            b[t] = lds2(Qs + j * KC + qswz(j, 8 * w + 2 * q));
+            b[t] = lds2(Qs + j * KC + qswz(j, 8 * cw + 2 * q));
           }
 #pragma unroll
           for (int t = 0; t < NT; ++t) {
@@ -375,7 +392,10 @@ __global__ void __launch_bounds__(fz::NTH, 1)
           }
           if (trw) tr[11 * TRN + stp] = clock64();
           __syncwarp();
-          if (lane == 0) mbar_arrive_relaxed(&qempty[qr.i]);
+          if (lane == 0) {
+            mbar_arrive_relaxed(&qempty[qr.i]);
+            if (paper) mbar_arrive_relaxed(&xempty[xr.i]);   // no phase 2: slot done
+          }
           if (trw) tr[12 * TRN + stp] = clock64() + (long long)(acc[0][0].x == 1.2345e300);
           xr.next(NS);
         } else {
@@ -388,16 +408,26 @@ __global__ void __launch_bounds__(fz::NTH, 1)
       // pass end (phase-1 warps only): fixed-order reduction of the 8 K-partials,
       // -P(p) into pbuf[p & 1] for the phase-2 warps, L-hat rows of tile p (l.13)
       if (ph1) {
-        if (w >= 4) {
+        // fold the K-partials into slots 0..3: slot s = acc(s) + acc(s+4) [+ acc(s+8) +
+        // acc(s+12)], added from the highest warp down (fixed order)
+        const int nw1 = NW * nset;
+        for (int top = nw1 - 4; top >= 4; top -= 4) {
+          if (w >= top && w < top + 4) {
 #pragma unroll
-          for (int r = 0; r < 2; ++r)
+            for (int r = 0; r < 2; ++r)
 #pragma unroll
-            for (int t = 0; t < NT; ++t) {
-              FZ_S(w - 4, r, t, 0) = acc[r][t].x;
-              FZ_S(w - 4, r, t, 1) = acc[r][t].y;
-            }
+              for (int t = 0; t < NT; ++t) {
+                if (top == nw1 - 4) {
+                  FZ_S(w - top, r, t, 0) = acc[r][t].x;
+                  FZ_S(w - top, r, t, 1) = acc[r][t].y;
+                } else {
+                  FZ_S(w - top, r, t, 0) = acc[r][t].x + FZ_S(w - top, r, t, 0);
+                  FZ_S(w - top, r, t, 1) = acc[r][t].y + FZ_S(w - top, r, t, 1);
+                }
+              }
+          }
+          if (nset == 2) bar_p1x(); else bar_p1();
         }
-        bar_p1();
         if (w < 4) {
 #pragma unroll
           for (int r = 0; r < 2; ++r)
@@ -407,32 +437,55 @@ __global__ void __launch_bounds__(fz::NTH, 1)
               FZ_S(w, r, t, 1) = acc[r][t].y + FZ_S(w, r, t, 1);
             }
         }
-        bar_p1();
+        if (nset == 2) bar_p1x(); else bar_p1();
         const int pb = p & 1;
-        if (p >= 2) mbar_wait(&pfree[pb], ((p >> 1) - 1) & 1);
+        if (p >= 2 && !paper) mbar_wait(&pfree[pb], ((p >> 1) - 1) & 1);
         double* P = pbuf + pb * Cf::ACC * 32;
         const int64_t r0p = row0_of(p);
 #pragma unroll
         for (int cb = 0; cb < Cf::ACC; cb += NW) {   // (r, t, h) combos w, w + 8, ...
           const int combo = cb + w;
-          if (combo < Cf::ACC) {
+          if (w < NW && combo < Cf::ACC) {
             const int i = combo * 32 + lane;
             const double v = (scr[(0 * Cf::ACC) * 32 + i] + scr[(1 * Cf::ACC) * 32 + i]) +
                              (scr[(2 * Cf::ACC) * 32 + i] + scr[(3 * Cf::ACC) * 32 + i]);
-            P[i] = -v;
+            P[i] = paper ? v : -v;
             const int r = combo / (2 * NT), t = (combo >> 1) % NT, h = combo & 1;
             const int j = 8 * t + 2 * q + h;
             const int64_t row = r0p + 8 * r + pg;
             if (j < bp && row < n) L[row * ldl + k0 + j] = v;
           }
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&pready[pb]);   // release: P stores ordered before
-        bar_p1();   // scratch is rewritten at the next pass end
+        if (paper) {
+          // l.16 (paper form): d(i) <- max(0, d(i) - ||L-hat(i,:)||^2), fixed order (t, h, q)
+          bar_p1x();
+          if (w == 0 && lane < R) {
+            const int rr = lane, r = rr >> 3, x = rr & 7;
+            const int gg = 2 * (x & 3) + (x >> 2);   // pi^-1
+            double ss = 0.0;
+#pragma unroll
+            for (int t = 0; t < NT; ++t)
+#pragma unroll
+              for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int qq = 0; qq < 4; ++qq) {
+                  const double v = P[((r * NT + t) * 2 + h) * 32 + 4 * gg + qq];
+                  ss += v * v;
+                }
+            const int64_t row = r0p + rr;
+            if (row < n) dvec[row] = fmax(dvec[row] - ss, 0.0);
+          }
+        } else {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&pready[pb]);   // release: P stores ordered before
+        }
+        if (nset == 2) bar_p1x(); else bar_p1();   // scratch is rewritten at the next pass end
       }
     }
   } else {
     // -------------------- phase 2: X(p-1) -= P(p-1) Q, norms --------------------
+    if (paper) goto done;   // left-looking form: X is read only
+    {
     const int w2 = w - NW;
     const int xo0 = xoff(pg, 8 * w2 + 2 * q), xo1 = xoff(8 + pg, 8 * w2 + 2 * q);
     double2 pf[2][NT];    // -P(p-1) in the accumulator layout (A fragments)
@@ -533,7 +586,9 @@ __global__ void __launch_bounds__(fz::NTH, 1)
         if (lane == 0) mbar_arrive(&pfree[pb]);
       }
     }
+    }
   }
+done:
 #undef FZ_S
   proj_end_stamp(st);
 }
@@ -596,11 +651,12 @@ int fused_max_bucket(const void* X, int64_t ldx, int64_t d) {
 
 template <int BPB>
 static cudaError_t go_fused(const CUtensorMap& map, double* X, int64_t ldx, const double* Qp, double* L,
-                            int64_t ldl, int64_t n, int64_t d, double* dvec, DevState* st, cudaStream_t s) {
+                            int64_t ldl, int64_t n, int64_t d, double* dvec, DevState* st, bool paper,
+                            cudaStream_t s) {
   using Cf = FzCfg<BPB>;
   const int nc = fz_nc(d);
   int ns = 0, nq = 0;
-  if (!Cf::rings(nc, ns, nq)) return cudaErrorInvalidValue;
+  if (!Cf::rings(nc, ns, nq, paper)) return cudaErrorInvalidValue;
   const size_t smem = Cf::smem(ns, nq);
   auto kern = k_proj_fused<BPB>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -615,7 +671,8 @@ static cudaError_t go_fused(const CUtensorMap& map, double* X, int64_t ldx, cons
     const char* e = getenv("RBRP_FZ_XMODE");   // timing experiments only (wrong results)
     xmode = e ? atoi(e) : 0;
   }
-  kern<<<fz_num_sms(), fz::NTH, smem, s>>>(map, X, ldx, Qp, L, ldl, n, (int)d, nc, ns, nq, dvec, st, tr, xmode);
+  kern<<<fz_num_sms(), fz::NTH, smem, s>>>(map, X, ldx, Qp, L, ldl, n, (int)d, nc, ns, nq, dvec, st, tr, xmode,
+                                           paper ? 1 : 0);
   return cudaGetLastError();
 }
 
@@ -626,7 +683,7 @@ cudaError_t launch_pack_q(const double* Qt, int64_t d, double* Qp, DevState* st,
 }
 
 cudaError_t launch_proj_fused(double* Xres, int64_t ldx, const double* Qp, double* L, int64_t ldl,
-                              int64_t n, int64_t d, double* dvec, DevState* st, int bucket,
+                              int64_t n, int64_t d, double* dvec, DevState* st, int bucket, bool paper,
                               cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   auto enc = encode_fn();
@@ -641,9 +698,9 @@ cudaError_t launch_proj_fused(double* Xres, int64_t ldx, const double* Qp, doubl
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
   switch (bucket) {
-    case 16: return go_fused<16>(map, Xres, ldx, Qp, L, ldl, n, d, dvec, st, s);
-    case 32: return go_fused<32>(map, Xres, ldx, Qp, L, ldl, n, d, dvec, st, s);
-    case 64: return go_fused<64>(map, Xres, ldx, Qp, L, ldl, n, d, dvec, st, s);
+    case 16: return go_fused<16>(map, Xres, ldx, Qp, L, ldl, n, d, dvec, st, paper, s);
+    case 32: return go_fused<32>(map, Xres, ldx, Qp, L, ldl, n, d, dvec, st, paper, s);
+    case 64: return go_fused<64>(map, Xres, ldx, Qp, L, ldl, n, d, dvec, st, paper, s);
     default: return cudaErrorInvalidValue;
   }
 }

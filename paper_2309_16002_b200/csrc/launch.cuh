@@ -81,7 +81,7 @@ cudaError_t launch_update(T* Xres, int64_t ldx, const T* Qt, const T* L, int64_t
 template <typename T>
 cudaError_t launch_fixup(T* Xres, int64_t ldx, double* dvec, T* L, int64_t ldl, const double* Rtot,
                          const int64_t* S, int64_t n_local, int64_t row_offset, int64_t d,
-                         DevState* st, cudaStream_t s);
+                         DevState* st, cudaStream_t s);   // Xres == nullptr: leave X (paper form)
 
 // k_project_mma.cu — DMMA (FP64 tensor) projection
 bool projection_mma_supported(const void* X, int64_t ldx, const void* Qt, int64_t d);
@@ -95,8 +95,27 @@ size_t fused_pack_bytes(int64_t d);
 int fused_max_bucket(const void* X, int64_t ldx, int64_t d);
 cudaError_t launch_pack_q(const double* Qt, int64_t d, double* Qp, DevState* st, cudaStream_t s);
 cudaError_t launch_proj_fused(double* Xres, int64_t ldx, const double* Qp, double* L, int64_t ldl,
-                              int64_t n, int64_t d, double* dvec, DevState* st, int bucket,
+                              int64_t n, int64_t d, double* dvec, DevState* st, int bucket, bool paper,
                               cudaStream_t s);
+
+// k_lhat_paper.cu — paper form, l.13 + l.16: read-only DMMA pass with 64-row tiles
+int lhat_paper_max_bucket(const void* X, int64_t ldx, int64_t d);
+cudaError_t launch_lhat_paper(const double* X, int64_t ldx, const double* Qp, double* L, int64_t ldl,
+                              int64_t n, int64_t d, double* dvec, DevState* st, int bucket, cudaStream_t s);
+
+// k_paper.cu — left-looking (paper) form of Alg. 2: CGS2 of the candidate rows (l.6),
+// Q append (l.10), exact zeros of earlier skeletons' L-hat (R13), d downdate (l.16)
+template <typename T>
+cudaError_t launch_cgs2_rows(double* Vg, int64_t d, const T* Qall, int64_t k_cap, double* C,
+                             const DevState* st, cudaStream_t s);   // C: kMaxB x k_cap scratch
+template <typename T>
+cudaError_t launch_append_q(const T* Qt, int64_t d, T* Qall, const DevState* st, cudaStream_t s);
+template <typename T>
+cudaError_t launch_zero_prev(T* L, int64_t ldl, const int64_t* S, int64_t n_local, int64_t row_offset,
+                             const DevState* st, cudaStream_t s);
+template <typename T>
+cudaError_t launch_downdate(const T* L, int64_t ldl, int64_t n, double* dvec, const DevState* st,
+                            int fused_max, cudaStream_t s);
 bool gemm_nt_mma(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
                  int64_t M, int64_t N, int64_t K, cudaStream_t s, cudaError_t* err);
 

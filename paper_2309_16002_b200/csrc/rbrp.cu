@@ -34,7 +34,7 @@ namespace {
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
-  size_t Xres = SIZE_MAX, dvec, cpre, ctot, cpos, cprefix, L, Qt, Qp, Vg, Gpart, G, Tg, Ag, R11, Rtot,
+  size_t Xres = SIZE_MAX, Qall = SIZE_MAX, Ccgs = SIZE_MAX, dvec, cpre, ctot, cpos, cprefix, L, Qt, Qp, Vg, Gpart, G, Tg, Ag, R11, Rtot,
          piv, mass, St, Srep, S, forced, dbg, cand, st, L1 = SIZE_MAX, LinvT = SIZE_MAX;
   size_t lbt, lbp, lrho, lSt, lpiv, lts, total;
   int nsplit, maxlog;
@@ -77,7 +77,12 @@ Layout make_layout(const rbrp_problem* p) {
     return o;
   };
   const size_t B = RBRP_MAX_B;
-  if (!(p->flags & RBRP_INPLACE)) L.Xres = take((size_t)n * d * w);
+  const bool paper = (p->flags & RBRP_FORM_PAPER) != 0;
+  if (!(p->flags & RBRP_INPLACE) && !paper) L.Xres = take((size_t)n * d * w);
+  if (paper) {
+    L.Qall = take((size_t)L.k_cap * d * w);   // Q = [Q_1 ... Q_t] rows (l.10)
+    L.Ccgs = take((size_t)RBRP_MAX_B * L.k_cap * 8);   // CGS coefficients (l.6)
+  }
   L.dvec = take((size_t)n * 8);
   L.cpre = take((size_t)n * 8);
   L.ctot = take((size_t)L.nchunks * 8);
@@ -188,6 +193,9 @@ struct Ctx {
   int32_t *cpos, *piv, *forced;
   T *Lm, *Qt;
   double* Qp;   // packed Q_b chunks of the fused projection
+  T* Qall;      // paper form: accumulated Q rows (k_cap x d)
+  double* Ccgs; // paper form: CGS coefficients
+  bool paper;   // RBRP_FORM_PAPER: left-looking, X read only
   int64_t *St, *Srep, *S, *cand;
   double* L1;
   T* LinvT;
@@ -197,6 +205,7 @@ struct Ctx {
   bool use_mma, use_forced;
   int bucketB;
   int fused_max;   // largest bucket run by the fused single-pass projection (0: none)
+  int lp_max;      // paper form: largest bucket run by k_lhat_paper (0: none)
 };
 
 // pointers of one shard's workspace
@@ -211,8 +220,11 @@ void make_ctx(Ctx<T>& c, const rbrp_problem* p, void* Xv, char* ws, const Layout
   c.chunk0 = p->row_offset / RBRP_CHUNK;
   const bool inplace = (p->flags & RBRP_INPLACE) != 0;
   c.X = (T*)Xv;
-  c.Xres = inplace ? c.X : (T*)(ws + Ly.Xres);
-  c.ldr = inplace ? p->ld : c.d;
+  c.paper = (p->flags & RBRP_FORM_PAPER) != 0;
+  c.Xres = (inplace || c.paper) ? c.X : (T*)(ws + Ly.Xres);   // paper form: X itself, read only
+  c.ldr = (inplace || c.paper) ? p->ld : c.d;
+  c.Qall = c.paper ? (T*)(ws + Ly.Qall) : nullptr;
+  c.Ccgs = c.paper ? (double*)(ws + Ly.Ccgs) : nullptr;
   c.dvec = (double*)(ws + Ly.dvec);
   c.cpre = (double*)(ws + Ly.cpre);
   c.ctot = (double*)(ws + Ly.ctot);
@@ -251,6 +263,7 @@ void make_ctx(Ctx<T>& c, const rbrp_problem* p, void* Xv, char* ws, const Layout
   c.use_mma = sizeof(T) == 8 && !force_simt() && projection_mma_supported(c.Xres, c.ldr, c.Qt, c.d);
   c.bucketB = bucket_of((int)std::min<int64_t>(p->b, c.k_cap));
   c.fused_max = (c.use_mma && !env_on("RBRP_NO_FUSED")) ? fused_max_bucket(c.Xres, c.ldr, c.d) : 0;
+  c.lp_max = (c.paper && c.use_mma && !env_on("RBRP_NO_FUSED")) ? lhat_paper_max_bucket(c.Xres, c.ldr, c.d) : 0;
 }
 
 template <typename T>
@@ -286,24 +299,37 @@ int enqueue_projection(Ctx<T>& c, cudaStream_t s, int* nl) {
     return e == cudaSuccess ? (int)RBRP_OK : (int)RBRP_ECUDA;
   };
   int rc = RBRP_OK;
-  if (c.fused_max > 0 && (rc = lk(launch_pack_q((const double*)c.Qt, c.d, c.Qp, c.st, s)))) return rc;
+  // the single-pass kernel: k_proj_fused (residual form) or k_lhat_paper (paper form)
+  const int fmax = c.paper ? c.lp_max : c.fused_max;
+  if (fmax > 0 && (rc = lk(launch_pack_q((const double*)c.Qt, c.d, c.Qp, c.st, s)))) return rc;
+  bool need_downdate = false;
   for (int bk = 16; bk <= c.bucketB; bk *= 2) {
-    if (bk <= c.fused_max) {
-      rc = lk(launch_proj_fused((double*)c.Xres, c.ldr, c.Qp, (double*)c.Lm, c.k_cap, c.n, c.d, c.dvec,
-                                c.st, bk, s));
+    if (bk <= fmax) {
+      if (c.paper)
+        rc = lk(launch_lhat_paper((const double*)c.Xres, c.ldr, c.Qp, (double*)c.Lm, c.k_cap, c.n, c.d,
+                                  c.dvec, c.st, bk, s));
+      else
+        rc = lk(launch_proj_fused((double*)c.Xres, c.ldr, c.Qp, (double*)c.Lm, c.k_cap, c.n, c.d, c.dvec,
+                                  c.st, bk, false, s));
     } else if (c.use_mma) {
       rc = lk(launch_lhat_mma((const double*)c.Xres, c.ldr, (const double*)c.Qt, c.n, c.d, (double*)c.Lm,
                               c.k_cap, c.st, bk, s));
-      if (!rc)
+      if (!rc && !c.paper)
         rc = lk(launch_update_mma((double*)c.Xres, c.ldr, (const double*)c.Qt, (const double*)c.Lm,
                                   c.k_cap, c.n, c.d, c.dvec, c.st, bk, s));
+      need_downdate = c.paper;
     } else {
       rc = lk(launch_lhat<T>(c.Xres, c.ldr, c.Qt, c.n, c.d, c.Lm, c.k_cap, c.st, bk, s));
-      if (!rc) rc = lk(launch_update<T>(c.Xres, c.ldr, c.Qt, c.Lm, c.k_cap, c.n, c.d, c.dvec, c.st, bk, s));
+      if (!rc && !c.paper)
+        rc = lk(launch_update<T>(c.Xres, c.ldr, c.Qt, c.Lm, c.k_cap, c.n, c.d, c.dvec, c.st, bk, s));
+      need_downdate = c.paper;
     }
     if (rc) return rc;
   }
-  return RBRP_OK;
+  // paper form on the two-kernel path: l.16 downdate from the L-hat columns (the kernel
+  // skips blocks whose bucket the fused kernel handled, which downdates in its epilogue)
+  if (need_downdate) rc = lk(launch_downdate<T>(c.Lm, c.k_cap, c.n, c.dvec, c.st, fmax, s));
+  return rc;
 }
 
 // The kernels of one block (Alg. 2 l.6-16), optionally followed by the next block's
@@ -324,10 +350,15 @@ int enqueue_block(Ctx<T>& c, SampleArgs& sa, cudaStream_t s, Prof* prof, int* nl
   fa.X = c.Xres;
   fa.ldx = c.ldr;
   fa.Vg = nullptr;
-  if (c.comm) {
+  if (c.comm || c.paper) {
+    if (c.comm) CK(cudaMemsetAsync(c.Vg, 0, (size_t)RBRP_MAX_B * c.d * 8, s));
     LK(launch_gather_rows<T>(c.Xres, c.ldr, c.St, c.n, p->row_offset, c.st, c.d, c.Vg, s));
-    int rc = comm_allreduce_f64(c.comm, c.Vg, (int64_t)RBRP_MAX_B * c.d, s);
-    if (rc) return rc;
+    if (c.comm) {
+      int rc = comm_allreduce_f64(c.comm, c.Vg, (int64_t)RBRP_MAX_B * c.d, s);
+      if (rc) return rc;
+    }
+    // paper form, l.6: V = X(S_t,:)^T - Q Q^T X(S_t,:)^T (CGS2)
+    if (c.paper) LK(launch_cgs2_rows<T>(c.Vg, c.d, c.Qall, c.k_cap, c.Ccgs, c.st, s));
     fa.Vg = c.Vg;
   }
   fa.S_t = c.St;
@@ -357,7 +388,12 @@ int enqueue_block(Ctx<T>& c, SampleArgs& sa, cudaStream_t s, Prof* prof, int* nl
   if (prof) prof->end();
   ++*nproj;
   if (prof) prof->begin(5);
-  LK(launch_fixup<T>(c.Xres, c.ldr, c.dvec, c.Lm, c.k_cap, c.Rtot, c.S, c.n, p->row_offset, c.d, c.st, s));
+  LK(launch_fixup<T>(c.paper ? nullptr : c.Xres, c.ldr, c.dvec, c.Lm, c.k_cap, c.Rtot, c.S, c.n, p->row_offset,
+                     c.d, c.st, s));
+  if (c.paper) {
+    LK(launch_zero_prev<T>(c.Lm, c.k_cap, c.S, c.n, p->row_offset, c.st, s));
+    LK(launch_append_q<T>(c.Qt, c.d, c.Qall, c.st, s));
+  }
   LK(launch_chunk_scan(c.dvec, c.n, c.chunk0, c.cpre, c.ctot, c.cpos, s));
   if (prof) prof->end();
   if (c.comm) {
@@ -515,7 +551,7 @@ int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* 
   // a0: d^(0), X_res <- X (Alg. 2 l.1-2)
   prof.begin(0);
   ++nl;
-  CK(launch_init_norms<T>(c.X, p->ld, c.Xres, c.n, c.d, c.dvec, c.st, !inplace, s));
+  CK(launch_init_norms<T>(c.X, p->ld, c.Xres, c.n, c.d, c.dvec, c.st, !inplace && !c.paper, s));
   ++nl;
   CK(launch_chunk_scan(c.dvec, c.n, c.chunk0, c.cpre, c.ctot, c.cpos, s));
   prof.end();
@@ -760,7 +796,8 @@ int run_dist(int nsh, const rbrp_problem* ps, void* const* Xs, char* const* wss,
   // a0
   for (int h = 0; h < nsh; ++h) {
     const bool inplace = (ps[h].flags & RBRP_INPLACE) != 0;
-    LKD(launch_init_norms<T>(C[h].X, ps[h].ld, C[h].Xres, C[h].n, C[h].d, C[h].dvec, C[h].st, !inplace, s));
+    LKD(launch_init_norms<T>(C[h].X, ps[h].ld, C[h].Xres, C[h].n, C[h].d, C[h].dvec, C[h].st,
+                               !inplace && !C[h].paper, s));
     LKD(launch_chunk_scan(C[h].dvec, C[h].n, C[h].chunk0, C[h].cpre, C[h].ctot, C[h].cpos, s));
   }
   RCD(coll_chunks());
@@ -828,6 +865,14 @@ int run_dist(int nsh, const rbrp_problem* ps, void* const* Xs, char* const* wss,
       LKD(launch_gather_rows<T>(C[h].Xres, C[h].ldr, C[h].St, C[h].n, ps[h].row_offset, C[h].st, C[h].d,
                                 C[h].Vg, s));
     if (comm) RCD(comm_allreduce_f64(comm, C[0].Vg, (int64_t)RBRP_MAX_B * C[0].d, s));
+    // paper form, l.6 (CGS2): once per distinct V buffer (in-process shards share one)
+    if (C[0].paper) {
+      for (int h = 0; h < nsh; ++h) {
+        bool seen = false;
+        for (int h2 = 0; h2 < h; ++h2) seen = seen || (C[h2].Vg == C[h].Vg);
+        if (!seen) LKD(launch_cgs2_rows<T>(C[h].Vg, C[h].d, C[h].Qall, C[h].k_cap, C[h].Ccgs, C[h].st, s));
+      }
+    }
     for (int h = 0; h < nsh; ++h) {
       Ctx<T>& c = C[h];
       FilterArgs fa;
@@ -860,7 +905,12 @@ int run_dist(int nsh, const rbrp_problem* ps, void* const* Xs, char* const* wss,
         int rc = enqueue_projection(c, s, &nl);
         if (rc) return rc;
       }
-      LKD(launch_fixup<T>(c.Xres, c.ldr, c.dvec, c.Lm, c.k_cap, c.Rtot, c.S, c.n, ps[h].row_offset, c.d, c.st, s));
+      LKD(launch_fixup<T>(c.paper ? nullptr : c.Xres, c.ldr, c.dvec, c.Lm, c.k_cap, c.Rtot, c.S, c.n,
+                          ps[h].row_offset, c.d, c.st, s));
+      if (c.paper) {
+        LKD(launch_zero_prev<T>(c.Lm, c.k_cap, c.S, c.n, ps[h].row_offset, c.st, s));
+        LKD(launch_append_q<T>(c.Qt, c.d, c.Qall, c.st, s));
+      }
       LKD(launch_chunk_scan(c.dvec, c.n, c.chunk0, c.cpre, c.ctot, c.cpos, s));
     }
     ++nproj;
@@ -987,7 +1037,6 @@ int rbrp_id(const rbrp_problem* p, void* X, void* workspace, size_t ws_bytes, rb
   int rc = validate(p);
   if (rc) return rc;
   if (!S_out || (p->n_local > 0 && !X) || !workspace) return RBRP_EINVAL;
-  if (p->flags & RBRP_FORM_PAPER) return RBRP_ENOTSUP;
   if (p->greedy) return RBRP_ENOTSUP;
   if (comm && (p->row_offset % RBRP_CHUNK) != 0) return RBRP_EINVAL;
   if (filter_coop_nsplit(p->d) > 148) return RBRP_ENOTSUP;   // d > 4736: one CTA per 32 columns
@@ -1012,7 +1061,6 @@ int rbrp_id_sharded(const rbrp_problem* p, int nshards, const int64_t* shard_row
                     void* const* workspace, size_t ws_bytes, void* stream, int64_t* S_out,
                     void* const* W_out, rbrp_report* rep) {
   if (!p || nshards < 1 || nshards > 64 || !shard_rows || !X || !workspace || !S_out) return RBRP_EINVAL;
-  if (p->flags & RBRP_FORM_PAPER) return RBRP_ENOTSUP;
   if (p->greedy) return RBRP_ENOTSUP;
   if (filter_coop_nsplit(p->d) > 148) return RBRP_ENOTSUP;
   std::vector<rbrp_problem> ps(nshards, *p);

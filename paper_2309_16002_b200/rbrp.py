@@ -162,20 +162,25 @@ def id(X: torch.Tensor, tol: Optional[float] = None, k: Optional[int] = None, b:
        replay_pivots: Optional[Sequence[Sequence[int]]] = None,
        max_blocks: int = 1024, log_blocks: bool = True, workspace: Optional[torch.Tensor] = None,
        comm=None, n_global: Optional[int] = None, row_offset: int = 0,
-       profile: bool = False, W_out: Optional[torch.Tensor] = None) -> Result:
+       profile: bool = False, W_out: Optional[torch.Tensor] = None, form: str = "residual") -> Result:
     """RBRP interpolative decomposition X ~ W X_S of a CUDA tensor X (n x d).
 
     tol: tau, relative to ||X||_F^2 (for an (r, eps)-ID pass tol = (1+eps) eta_r,
     PAPER.md l.86); or k: fixed rank.  b: block size; seed: Philox key;
     tau_b < 0 -> 1/b_t.  Returns S (CPU int64, selection order), W (device,
     n x k, W[S] = I) and the per-block log.  workspace / W_out: optional
-    preallocated buffers (W_out: n x k_cap, k_cap = k or k_max or min(n, d))."""
+    preallocated buffers (W_out: n x k_cap, k_cap = k or k_max or min(n, d)).
+    form: "residual" (north_star: X_res updated per block, exact residual norms) or
+    "paper" (Alg. 2 literally: X read only, CGS2 for l.6, downdated norms l.16)."""
     if not X.is_cuda:
         raise ValueError("X must be a CUDA tensor (use id_host for host buffers)")
     if tol is None and k is None:
         raise ValueError("need tol or k")
     L = lib()
-    flags = (0 if with_W else RBRP_NO_W) | (RBRP_INPLACE if inplace else 0)
+    if form not in ("residual", "paper"):
+        raise ValueError("form must be 'residual' or 'paper'")
+    flags = ((0 if with_W else RBRP_NO_W) | (RBRP_INPLACE if inplace else 0)
+             | (RBRP_FORM_PAPER if form == "paper" else 0))
     p = _problem(X, tol, k, b, seed, k_max, tau_b, flags, n_global, row_offset, greedy)
     keep = []
     if replay_blocks is not None:
@@ -274,14 +279,14 @@ def _report(mb, b, log_blocks):
 
 def id_sharded(shards: Sequence[torch.Tensor], tol: Optional[float] = None, k: Optional[int] = None,
                b: int = 16, seed: int = 0, k_max: int = 0, tau_b: float = -1.0, with_W: bool = True,
-               replay_blocks=None, replay_pivots=None, max_blocks: int = 1024):
+               replay_blocks=None, replay_pivots=None, max_blocks: int = 1024, form: str = "residual"):
     """The row-sharded (multi-GPU) algorithm over in-process shards on one device:
     `shards` are consecutive row blocks of X (every one but the last a multiple of
     4096 rows).  Returns (Result of shard 0 with W = None, [W_h per shard])."""
     L = lib()
     X0 = shards[0]
     n_global = sum(int(x.shape[0]) for x in shards)
-    flags = 0 if with_W else RBRP_NO_W
+    flags = (0 if with_W else RBRP_NO_W) | (RBRP_FORM_PAPER if form == "paper" else 0)
     p = _problem(X0, tol, k, b, seed, k_max, tau_b, flags, n_global, 0, False)
     keep = []
     if replay_blocks is not None:

@@ -349,3 +349,59 @@ def test_fused_projection_matches_two_kernel_path(monkeypatch, n, d, rank, b):
     s2 = rb.id(X, tol=1e-12, b=b, seed=5)
     assert s1.S.tolist() == s2.S.tolist() and s1.rho == s2.rho and torch.equal(s1.W, s2.W)
     assert s1.k == rank
+
+
+def _replay_form(Xnp, ores, dtype, b, form):
+    rb = _rb()
+    blocks = [blk.S_t for blk in ores.blocks]
+    piv = [blk.piv for blk in ores.blocks]
+    X = torch.from_numpy(Xnp).cuda()
+    X0 = X.clone()
+    res = rb.id(X, k=ores.k, b=b, replay_blocks=blocks, replay_pivots=piv, form=form)
+    assert torch.equal(X, X0)                      # paper form: X is read only
+    assert res.S.tolist() == ores.S
+    assert res.b_prime == [blk.b_prime for blk in ores.blocks]
+    for a, blk in zip(res.rho, ores.blocks):
+        assert abs(a - blk.rho) <= _tol(dtype)
+    _check_W(Xnp, res, ores, dtype)
+    return res
+
+
+@cuda
+@pytest.mark.parametrize("name,kw", [
+    ("c1", {}),
+    ("c2", dict(n=9000 + 77, d=1024, rank=70, b=32)),     # fused paper pass, nc = 16
+    ("c2", dict(n=6000, d=260, rank=24, b=8)),            # partial chunk, bucket 16
+    ("c3", dict(n=12000, d=64, n_heavy_dirs=20, n_heavy_rows=6000, b=16)),
+    ("c5", dict(n=12000, d=160, n_centres=120, b=64)),    # bucket 64: two-kernel + downdate
+])
+def test_paper_form_replay_parity(name, kw):
+    """NEXT-1 (RBRP_FORM_PAPER): Alg. 2 literally (CGS2 for l.6, read-only L-hat pass
+    for l.13, downdated norms for l.16) against the oracle's paper form in replay mode:
+    S and b' exact, rho_t within 1e-10 (the oracle downdates the same way), W within
+    tolerance, X untouched."""
+    cfg = CONFIGS[name] if not kw else small_config(name, **kw)
+    Xnp = make(cfg).numpy()
+    if cfg.tau is not None:
+        tau = cfg.tau
+    else:
+        tau = (1 + cfg.eps) * R.eta(Xnp, min(cfg.r, Xnp.shape[1] // 2))
+    ores = O.rbrp(Xnp, tau=tau, b=cfg.b, seed=0, form="paper")
+    _replay_form(Xnp, ores, np.float64, cfg.b, "paper")
+
+
+@cuda
+def test_paper_form_same_seed_matches_residual_form():
+    """The two forms are equal in exact arithmetic (Q_b orthogonal to Q): on an
+    exactly rank-70 input both stop at |S| = 70, rho within 1e-10 block by block, and the
+    same seed gives the same skeletons."""
+    rb = _rb()
+    cfg = small_config("c2", n=20000, d=512, rank=70, b=32)
+    X = make(cfg, device="cuda")
+    r = rb.id(X, tol=1e-12, b=32, seed=3)
+    p = rb.id(X, tol=1e-12, b=32, seed=3, form="paper")
+    assert r.k == p.k == 70
+    assert r.S.tolist() == p.S.tolist()
+    assert max(abs(a - b) for a, b in zip(r.rho, p.rho)) <= 1e-10
+    Wr, Wp = r.W.cpu(), p.W.cpu()
+    assert torch.linalg.norm(Wr - Wp) <= 1e-9 * torch.linalg.norm(Wr)
