@@ -52,8 +52,13 @@ enum {
   RBRP_INPLACE = 1,    /* X is overwritten by the residual X - L Q^T (saves n*d*w bytes of
                           workspace); X must then be writable */
   RBRP_NO_W = 2,       /* skeleton selection only; W_out is ignored */
-  RBRP_FORM_PAPER = 4  /* reserved: left-looking form of Alg. 2 l.6/l.13 (not yet built:
-                          returns RBRP_ENOTSUP) */
+  RBRP_FORM_PAPER = 4  /* left-looking form, Alg. 2 exactly as written: X is
+                          read only (never copied, never written; INPLACE is ignored);
+                          l.6 V = X(S_t,:)^T - Q Q^T X(S_t,:)^T by CGS2; l.13
+                          L-hat = X Q_b; l.16 d <- max(0, d - ||L-hat(i,:)||^2)
+                          (P:418).  Workspace adds k_cap x d x w for Q.  Without the flag:
+                          the residual form of north_star step 4 (X_res updated per block,
+                          exact residual norms) */
 };
 
 /* rbrp_report.flags (non-fatal) */
