@@ -69,9 +69,89 @@ __global__ void __launch_bounds__(32 * kTrinvWarps) k_trinv(const double* __rest
   for (int64_t m = lane; m < k; m += 32) LinvT[j * k + m] = (m < j) ? T(0) : (T)x[m];
 }
 
+// Small k (L_1 fits in shared memory): L_1 staged once per CTA (rows only from the CTA's
+// first column on), one warp per column j of L_1^{-1} as in k_trinv, but every operand of
+// the substitution step now comes from shared memory and 1/L(i,i) is precomputed, so a
+// step costs one shared-memory dot product + butterfly instead of an L2 round trip.
+constexpr int kTrinvSmallK = 160;   // k^2 + (k + 8 k) doubles of shared memory
+constexpr int kTrinvSmallWarps = 8;
+template <typename T>
+__global__ void __launch_bounds__(32 * kTrinvSmallWarps) k_trinv_small(const double* __restrict__ L1, int64_t k,
+                                                                       T* __restrict__ LinvT, DevState* st) {
+  extern __shared__ double ts_[];
+  const int kk = (int)k;
+  double* Ls = ts_;                    // [k][k]
+  double* dinv = Ls + (size_t)kk * kk; // [k]
+  double* xw = dinv + kk;              // [warps][k]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int j0 = blockIdx.x * kTrinvSmallWarps;
+  {   // rows [j0, k) of L_1 in one bulk copy (16-byte aligned: j0 * k * 8 and the size)
+    __shared__ __align__(8) uint64_t bar;
+    const int64_t first = (int64_t)j0 * kk, cnt = (int64_t)kk * kk - first;
+    const bool bulk = ((first * 8) % 16 == 0) && ((cnt * 8) % 16 == 0) && ((uintptr_t)L1 % 16 == 0);
+    if (bulk) {
+      const uint32_t sb = (uint32_t)__cvta_generic_to_shared(&bar);
+      if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sb) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sb), "r"((uint32_t)(cnt * 8))
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                (uint32_t)__cvta_generic_to_shared(Ls + first)),
+            "l"(L1 + first), "r"((uint32_t)(cnt * 8)), "r"(sb)
+            : "memory");
+      }
+      __syncthreads();
+      asm volatile(
+          "{\n .reg .pred p;\nW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra W_%=;\n}\n" ::"r"(sb)
+          : "memory");
+    } else {
+      for (int64_t e = first + threadIdx.x; e < (int64_t)kk * kk; e += blockDim.x) Ls[e] = L1[e];
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kk; i += blockDim.x) dinv[i] = 1.0 / Ls[(int64_t)i * kk + i];
+  if (blockIdx.x == 0 && w == 0) {   // W_CLIPPED check (Remark 5.2, reading R17)
+    double mx = 0.0, mn = DBL_MAX;
+    for (int i = lane; i < kk; i += 32) {
+      const double a = fabs(L1[(int64_t)i * kk + i]);
+      mx = fmax(mx, a);
+      mn = fmin(mn, a);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    }
+    if (lane == 0 && mn < 1e-12 * mx) atomicOr(&st->flags, (uint32_t)RBRP_F_W_CLIPPED);
+  }
+  __syncthreads();
+  const int j = j0 + w;
+  if (j >= kk) return;
+  double* x = xw + (size_t)w * kk;
+  if (lane == 0) x[j] = dinv[j];
+  __syncwarp();
+  for (int i = j + 1; i < kk; ++i) {
+    const double* li = Ls + (int64_t)i * kk;
+    double s = 0.0;
+    for (int m = j + lane; m < i; m += 32) s = fma(li[m], x[m], s);
+    s = warp_sum(s);
+    if (lane == 0) x[i] = -s * dinv[i];
+    __syncwarp();
+  }
+  for (int m = lane; m < kk; m += 32) LinvT[(int64_t)j * kk + m] = (m < j) ? T(0) : (T)x[m];
+}
+
 template <typename T>
 cudaError_t launch_trinv(const double* L1, int64_t k, T* LinvT, DevState* st, cudaStream_t s) {
   if (k <= 0) return cudaSuccess;
+  if (k <= kTrinvSmallK) {
+    const size_t smem = (size_t)(k * k + k + kTrinvSmallWarps * k) * sizeof(double);
+    cudaFuncSetAttribute(k_trinv_small<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_trinv_small<T><<<ceil_div(k, kTrinvSmallWarps), 32 * kTrinvSmallWarps, smem, s>>>(L1, k, LinvT, st);
+    return cudaGetLastError();
+  }
   size_t smem = (size_t)kTrinvWarps * k * sizeof(double);
   cudaFuncSetAttribute(k_trinv<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_trinv<T><<<ceil_div(k, kTrinvWarps), 32 * kTrinvWarps, smem, s>>>(L1, k, LinvT, st);
