@@ -35,7 +35,7 @@ constexpr int kTrinvWarps = 4;
 // Written transposed: LinvT(j, m) = x_m (zeros for m < j).
 template <typename T>
 __global__ void __launch_bounds__(32 * kTrinvWarps) k_trinv(const double* __restrict__ L1, int64_t k,
-                                                            T* __restrict__ LinvT, DevState* st) {
+                                                            T* __restrict__ LinvT, int64_t ldo, DevState* st) {
   extern __shared__ double xs[];   // [kTrinvWarps][k]
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t j = (int64_t)blockIdx.x * kTrinvWarps + w;
@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(32 * kTrinvWarps) k_trinv(const double* __rest
     if (lane == 0) x[i] = xi;
     __syncwarp();
   }
-  for (int64_t m = lane; m < k; m += 32) LinvT[j * k + m] = (m < j) ? T(0) : (T)x[m];
+  for (int64_t m = lane; m < ldo; m += 32) LinvT[j * ldo + m] = (m < j || m >= k) ? T(0) : (T)x[m];
 }
 
 // Small k (L_1 fits in shared memory): L_1 staged once per CTA (rows only from the CTA's
@@ -77,7 +77,8 @@ constexpr int kTrinvSmallK = 160;   // k^2 + (k + 8 k) doubles of shared memory
 constexpr int kTrinvSmallWarps = 8;
 template <typename T>
 __global__ void __launch_bounds__(32 * kTrinvSmallWarps) k_trinv_small(const double* __restrict__ L1, int64_t k,
-                                                                       T* __restrict__ LinvT, DevState* st) {
+                                                                       T* __restrict__ LinvT, int64_t ldo,
+                                                                       DevState* st) {
   extern __shared__ double ts_[];
   const int kk = (int)k;
   double* Ls = ts_;                    // [k][k]
@@ -140,21 +141,21 @@ __global__ void __launch_bounds__(32 * kTrinvSmallWarps) k_trinv_small(const dou
     if (lane == 0) x[i] = -s * dinv[i];
     __syncwarp();
   }
-  for (int m = lane; m < kk; m += 32) LinvT[(int64_t)j * kk + m] = (m < j) ? T(0) : (T)x[m];
+  for (int64_t m = lane; m < ldo; m += 32) LinvT[(int64_t)j * ldo + m] = (m < j || m >= kk) ? T(0) : (T)x[m];
 }
 
 template <typename T>
-cudaError_t launch_trinv(const double* L1, int64_t k, T* LinvT, DevState* st, cudaStream_t s) {
+cudaError_t launch_trinv(const double* L1, int64_t k, T* LinvT, int64_t ldo, DevState* st, cudaStream_t s) {
   if (k <= 0) return cudaSuccess;
   if (k <= kTrinvSmallK) {
     const size_t smem = (size_t)(k * k + k + kTrinvSmallWarps * k) * sizeof(double);
     cudaFuncSetAttribute(k_trinv_small<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_trinv_small<T><<<ceil_div(k, kTrinvSmallWarps), 32 * kTrinvSmallWarps, smem, s>>>(L1, k, LinvT, st);
+    k_trinv_small<T><<<ceil_div(k, kTrinvSmallWarps), 32 * kTrinvSmallWarps, smem, s>>>(L1, k, LinvT, ldo, st);
     return cudaGetLastError();
   }
   size_t smem = (size_t)kTrinvWarps * k * sizeof(double);
   cudaFuncSetAttribute(k_trinv<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_trinv<T><<<ceil_div(k, kTrinvWarps), 32 * kTrinvWarps, smem, s>>>(L1, k, LinvT, st);
+  k_trinv<T><<<ceil_div(k, kTrinvWarps), 32 * kTrinvWarps, smem, s>>>(L1, k, LinvT, ldo, st);
   return cudaGetLastError();
 }
 
@@ -178,7 +179,7 @@ cudaError_t launch_w_identity(T* W, int64_t ldw, const int64_t* S, int64_t k, in
 #define INSTW(T)                                                                                  \
   template cudaError_t launch_gather_L1<T>(const T*, int64_t, const int64_t*, int64_t, int64_t,  \
                                            int64_t, double*, cudaStream_t);                      \
-  template cudaError_t launch_trinv<T>(const double*, int64_t, T*, DevState*, cudaStream_t);     \
+  template cudaError_t launch_trinv<T>(const double*, int64_t, T*, int64_t, DevState*, cudaStream_t); \
   template cudaError_t launch_w_identity<T>(T*, int64_t, const int64_t*, int64_t, int64_t,       \
                                             int64_t, cudaStream_t);
 INSTW(double)

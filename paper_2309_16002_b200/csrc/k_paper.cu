@@ -186,24 +186,26 @@ cudaError_t launch_zero_prev(T* L, int64_t ldl, const int64_t* S, int64_t n_loca
 // j ascending)
 template <typename T>
 __global__ void k_downdate(const T* __restrict__ L, int64_t ldl, int64_t n, double* __restrict__ dvec,
-                           const DevState* st, int fused_max) {
+                           DevState* st, int fused_max) {
   if (st->stop) return;
   const int bp = st->b_prime;
   if (bp <= 0 || bucket_of(bp) <= fused_max) return;   // the fused kernel downdated already
   const int64_t k0 = st->k;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const T* l = L + i * ldl + k0;
-  double s = 0.0;
-  for (int j = 0; j < bp; ++j) {
-    const double v = (double)l[j];
-    s += v * v;
+  if (i < n) {
+    const T* l = L + i * ldl + k0;
+    double s = 0.0;
+    for (int j = 0; j < bp; ++j) {
+      const double v = (double)l[j];
+      s += v * v;
+    }
+    dvec[i] = fmax(dvec[i] - s, 0.0);
   }
-  dvec[i] = fmax(dvec[i] - s, 0.0);
+  proj_end_stamp(st);   // end of the projection pass on this path (L-hat + downdate)
 }
 
 template <typename T>
-cudaError_t launch_downdate(const T* L, int64_t ldl, int64_t n, double* dvec, const DevState* st,
+cudaError_t launch_downdate(const T* L, int64_t ldl, int64_t n, double* dvec, DevState* st,
                             int fused_max, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   k_downdate<T><<<ceil_div(n, 256), 256, 0, s>>>(L, ldl, n, dvec, st, fused_max);
@@ -216,7 +218,7 @@ cudaError_t launch_downdate(const T* L, int64_t ldl, int64_t n, double* dvec, co
   template cudaError_t launch_append_q<T>(const T*, int64_t, T*, const DevState*, cudaStream_t);      \
   template cudaError_t launch_zero_prev<T>(T*, int64_t, const int64_t*, int64_t, int64_t,             \
                                            const DevState*, cudaStream_t);                            \
-  template cudaError_t launch_downdate<T>(const T*, int64_t, int64_t, double*, const DevState*, int,  \
+  template cudaError_t launch_downdate<T>(const T*, int64_t, int64_t, double*, DevState*, int,        \
                                           cudaStream_t);
 INSTP(double)
 INSTP(float)

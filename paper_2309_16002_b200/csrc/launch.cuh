@@ -114,7 +114,7 @@ template <typename T>
 cudaError_t launch_zero_prev(T* L, int64_t ldl, const int64_t* S, int64_t n_local, int64_t row_offset,
                              const DevState* st, cudaStream_t s);
 template <typename T>
-cudaError_t launch_downdate(const T* L, int64_t ldl, int64_t n, double* dvec, const DevState* st,
+cudaError_t launch_downdate(const T* L, int64_t ldl, int64_t n, double* dvec, DevState* st,
                             int fused_max, cudaStream_t s);
 bool gemm_nt_mma(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
                  int64_t M, int64_t N, int64_t K, cudaStream_t s, cudaError_t* err);
@@ -124,7 +124,8 @@ template <typename T>
 cudaError_t launch_gather_L1(const T* L, int64_t ldl, const int64_t* S, int64_t k, int64_t n_local,
                              int64_t row_offset, double* L1, cudaStream_t s);
 template <typename T>
-cudaError_t launch_trinv(const double* L1, int64_t k, T* LinvT, DevState* st, cudaStream_t s);
+cudaError_t launch_trinv(const double* L1, int64_t k, T* LinvT, int64_t ldo, DevState* st,
+                         cudaStream_t s);   // LinvT: k x ldo, columns [k, ldo) zero
 template <typename T>
 cudaError_t launch_gemm_nt(const T* A, int64_t lda, const T* B, int64_t ldb, T* C, int64_t ldc,
                            int64_t M, int64_t N, int64_t K, cudaStream_t s);

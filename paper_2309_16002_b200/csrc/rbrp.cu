@@ -115,7 +115,7 @@ Layout make_layout(const rbrp_problem* p) {
   L.lts = take((size_t)L.maxlog * 16);
   if (!(p->flags & RBRP_NO_W)) {
     L.L1 = take((size_t)L.k_cap * L.k_cap * 8);
-    L.LinvT = take((size_t)L.k_cap * L.k_cap * w);
+    L.LinvT = take((size_t)L.k_cap * ((L.k_cap + 7) / 8 * 8) * w);   // k x round8(k) (K padded for DMMA)
   }
   L.total = off;
   return L;
@@ -652,16 +652,21 @@ int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* 
       int rc = comm_allreduce_f64(comm, L1, k * k, s);
       if (rc) return rc;
     }
+    // K padded to a multiple of 8 for the FP64 tensor path: L_1^{-T} gets zero columns
+    // [k, kp) and L's columns [k, kp) are zeroed (never written by the loop)
+    const int64_t kp = (k + 7) / 8 * 8;
     ++nl;
-    CK(launch_trinv<T>(L1, k, LinvT, c.st, s));
+    CK(launch_trinv<T>(L1, k, LinvT, kp, c.st, s));
+    if (kp > k && kp <= k_cap && c.n > 0)
+      CK(cudaMemset2DAsync(c.Lm + k, (size_t)k_cap * sizeof(T), 0, (size_t)(kp - k) * sizeof(T), (size_t)c.n, s));
     cudaError_t merr = cudaSuccess;
     ++nl;
-    if (sizeof(T) == 8 && !force_simt() &&
-        gemm_nt_mma((const double*)c.Lm, k_cap, (const double*)LinvT, k, (double*)W_out, k_cap, c.n, k,
-                    k, s, &merr)) {
+    if (sizeof(T) == 8 && !force_simt() && kp <= k_cap &&
+        gemm_nt_mma((const double*)c.Lm, k_cap, (const double*)LinvT, kp, (double*)W_out, k_cap, c.n, k,
+                    kp, s, &merr)) {
       CK(merr);
     } else {
-      CK(launch_gemm_nt<T>(c.Lm, k_cap, LinvT, k, (T*)W_out, k_cap, c.n, k, k, s));
+      CK(launch_gemm_nt<T>(c.Lm, k_cap, LinvT, kp, (T*)W_out, k_cap, c.n, k, k, s));
     }
     ++nl;
     CK(launch_w_identity<T>((T*)W_out, k_cap, c.S, k, c.n, p->row_offset, s));
@@ -934,15 +939,18 @@ int run_dist(int nsh, const rbrp_problem* ps, void* const* Xs, char* const* wss,
     for (int h = 0; h < nsh; ++h) {
       Ctx<T>& c = C[h];
       if (!W_outs[h]) continue;
-      LKD(launch_trinv<T>(c.L1, k, c.LinvT, c.st, s));
+      const int64_t kp = (k + 7) / 8 * 8;
+      LKD(launch_trinv<T>(c.L1, k, c.LinvT, kp, c.st, s));
+      if (kp > k && kp <= k_cap && c.n > 0)
+        CK(cudaMemset2DAsync(c.Lm + k, (size_t)k_cap * sizeof(T), 0, (size_t)(kp - k) * sizeof(T), (size_t)c.n, s));
       cudaError_t merr = cudaSuccess;
       ++nl;
-      if (sizeof(T) == 8 && !force_simt() &&
-          gemm_nt_mma((const double*)c.Lm, k_cap, (const double*)c.LinvT, k, (double*)W_outs[h], k_cap, c.n,
-                      k, k, s, &merr)) {
+      if (sizeof(T) == 8 && !force_simt() && kp <= k_cap &&
+          gemm_nt_mma((const double*)c.Lm, k_cap, (const double*)c.LinvT, kp, (double*)W_outs[h], k_cap, c.n,
+                      k, kp, s, &merr)) {
         CK(merr);
       } else {
-        CK(launch_gemm_nt<T>(c.Lm, k_cap, c.LinvT, k, (T*)W_outs[h], k_cap, c.n, k, k, s));
+        CK(launch_gemm_nt<T>(c.Lm, k_cap, c.LinvT, kp, (T*)W_outs[h], k_cap, c.n, k, k, s));
       }
       LKD(launch_w_identity<T>((T*)W_outs[h], k_cap, c.S, k, c.n, ps[h].row_offset, s));
     }
