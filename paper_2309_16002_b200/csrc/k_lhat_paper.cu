@@ -90,7 +90,8 @@ struct LpCfg {
   static constexpr int QSTAGE = BPB * lp::KC;
   static constexpr int SCR = lp::NRP * 2 * ACC * 32;   // two partial slots per row pair
   static size_t smem(int ns, int nq) {
-    return (size_t)ns * lp::SLOT * 8 + (size_t)nq * QSTAGE * 8 + (size_t)SCR * 8 + (2 * ns + 2 * nq) * 8 + 1024;
+    return (size_t)ns * lp::SLOT * 8 + (size_t)nq * QSTAGE * 8 + (size_t)(SCR + lp::NRP * lp::NCW * 16) * 8 +
+           (2 * ns + 2 * nq) * 8 + 1024;
   }
   static bool rings(int& ns, int& nq) {
     ns = 4;
@@ -105,7 +106,7 @@ template <int BPB>
 __global__ void __launch_bounds__(lp::NTH, 1)
     k_lhat_paper(const __grid_constant__ CUtensorMap xmap, const double* __restrict__ Qp,
                  double* __restrict__ L, int64_t ldl, int64_t n, int d, int nc, int NS, int NQ,
-                 double* __restrict__ dvec, DevState* st) {
+                 double* __restrict__ dvec, DevState* st, double* __restrict__ Xr, int64_t ldx, int resid) {
   using Cf = LpCfg<BPB>;
   constexpr int NT = Cf::NT;
   using namespace lp;
@@ -120,7 +121,8 @@ __global__ void __launch_bounds__(lp::NTH, 1)
   double* xs = sm;                                   // NS x SLOT
   double* qs = xs + (size_t)NS * SLOT;               // NQ x QSTAGE
   double* scr = qs + (size_t)NQ * Cf::QSTAGE;        // [rp][slot 0..1][ACC][32]
-  uint64_t* xfull = reinterpret_cast<uint64_t*>(scr + Cf::SCR);
+  double* nrm = scr + Cf::SCR;                       // [rp][cw][16] row-norm partials (residual form)
+  uint64_t* xfull = reinterpret_cast<uint64_t*>(nrm + NRP * NCW * 16);
   uint64_t* xempty = xfull + NS;
   uint64_t* qfull = xempty + NS;
   uint64_t* qempty = qfull + NQ;
@@ -141,24 +143,32 @@ __global__ void __launch_bounds__(lp::NTH, 1)
   }
   __syncthreads();
   auto row0_of = [&](int p) { return ((int64_t)blockIdx.x + (int64_t)p * gridDim.x) * R; };
-  const int steps = T * nc;
+  const int npass = resid ? 2 : 1;   // residual form: L-hat pass, then update pass per tile
+  const int steps = T * nc * npass;
 
   if (T == 0) {
   } else if (w == NCONS) {
-    // X producer
+    // X producer.  Residual form: the L-hat pass loads a tile with an L2 evict_last
+    // policy, the update pass (same addresses, shortly after) with evict_first, so the
+    // second read is served by L2 and HBM sees one read of X_res.
     if (lane == 0) {
+      uint64_t pol_keep, pol_drop;
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol_keep));
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol_drop));
       LpRing xr;
       for (int s = 0; s < steps; ++s) {
         if (s >= NS) lp_wait(&xempty[xr.i], xr.ph ^ 1);
         lp_expect(&xfull[xr.i], SLOT * 8);   // out-of-bounds rows / columns are zero-filled
         double* dst = xs + (size_t)xr.i * SLOT;
-        const int y = (int)row0_of(s / nc), c = s % nc;
+        const int y = (int)row0_of(s / (nc * npass)), c = s % nc;
+        const bool second = resid && ((s / nc) & 1);
+        const uint64_t pol = resid ? (second ? pol_drop : pol_keep) : pol_drop;
 #pragma unroll
         for (int b = 0; b < 4; ++b)
           asm volatile(
-              "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, "
-              "{%2, %3}], [%4];\n" ::"r"(lp_su32(dst + b * BOX)),
-              "l"(&xmap), "r"(c * KC + 16 * b), "r"(y), "r"(lp_su32(&xfull[xr.i]))
+              "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint "
+              "[%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(lp_su32(dst + b * BOX)),
+              "l"(&xmap), "r"(c * KC + 16 * b), "r"(y), "r"(lp_su32(&xfull[xr.i])), "l"(pol)
               : "memory");
         xr.next(NS);
       }
@@ -274,11 +284,88 @@ __global__ void __launch_bounds__(lp::NTH, 1)
               if (j + 1 < bp) L[row * ldl + k0 + j + 1] = vy;
             }
             ss += vx * vx + vy * vy;
+            if (resid) {   // -P for the update pass, in the free scratch slot 1
+              LP_S(1, r, t, 0) = -vx;
+              LP_S(1, r, t, 1) = -vy;
+            }
           }
-          // l.16 downdate: sum over the row's columns (q lanes), j ascending per lane
-          ss += __shfl_xor_sync(0xffffffffu, ss, 1);
-          ss += __shfl_xor_sync(0xffffffffu, ss, 2);
-          if (q == 0 && row < n) dvec[row] = fmax(dvec[row] - ss, 0.0);
+          if (!resid) {
+            // l.16 downdate (paper form): sum over the row's columns (q lanes)
+            ss += __shfl_xor_sync(0xffffffffu, ss, 1);
+            ss += __shfl_xor_sync(0xffffffffu, ss, 2);
+            if (q == 0 && row < n) dvec[row] = fmax(dvec[row] - ss, 0.0);
+          }
+        }
+      }
+      if (resid) {
+        // ----- update pass (residual form, l.16): X(tile) -= L-hat Q_b, chunk by chunk;
+        // the chunks come back through L2 (read from HBM by the L-hat pass just before)
+        lp_bar();
+        double2 pf[2][NT];   // -P rows of this row pair, accumulator layout (A fragments)
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+          for (int t = 0; t < NT; ++t) pf[r][t] = make_double2(LP_S(1, r, t, 0), LP_S(1, r, t, 1));
+        const int64_t r0 = row0_of(p) + 16 * rp;
+        double nr[2] = {0.0, 0.0};
+        for (int c = 0; c < nc; ++c) {
+          lp_wait(&qfull[qr.i], qr.ph);
+          lp_wait(&xfull[xr.i], xr.ph);
+          const double* xsl = xs + (size_t)xr.i * SLOT;
+          const double* Qs = qs + (size_t)qr.i * Cf::QSTAGE;
+          double2 xv[2][2];
+#pragma unroll
+          for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) xv[r][h] = lp_lds2(xsl + xo[r][h]);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+              const int j0 = 8 * t + 2 * q, col = 16 * cw + 8 * h + g;
+              const double b0 = Qs[j0 * KC + lp_qswz(j0, col)];
+              const double b1 = Qs[(j0 + 1) * KC + lp_qswz(j0 + 1, col)];
+              lp_dmma(xv[0][h], pf[0][t].x, b0);
+              lp_dmma(xv[1][h], pf[1][t].x, b0);
+              lp_dmma(xv[0][h], pf[0][t].y, b1);
+              lp_dmma(xv[1][h], pf[1][t].y, b1);
+            }
+          }
+          __syncwarp();
+          if (lane == 0) {
+            lp_arrive(&xempty[xr.i]);
+            lp_arrive(&qempty[qr.i]);
+          }
+          xr.next(NS);
+          qr.next(NQ);
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            const int64_t row = r0 + 8 * r + pg;
+            if (row >= n) continue;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int col = c * KC + 16 * cw + 8 * h + 2 * q;
+              if (col < d) {
+                __stcs(reinterpret_cast<double2*>(Xr + row * ldx + col), xv[r][h]);
+                nr[r] += xv[r][h].x * xv[r][h].x + xv[r][h].y * xv[r][h].y;
+              }
+            }
+          }
+        }
+        // d(i) = ||x_res,i||^2: q lanes, then the 4 column groups in order
+        double* nb = nrm + (size_t)rp * NCW * 16;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          double v = nr[r];
+          v += __shfl_xor_sync(0xffffffffu, v, 1);
+          v += __shfl_xor_sync(0xffffffffu, v, 2);
+          if (q == 0) nb[cw * 16 + 8 * r + pg] = v;
+        }
+        lp_bar();
+        if (cw == 0 && lane < 16) {
+          const double v = (nb[lane] + nb[16 + lane]) + (nb[32 + lane] + nb[48 + lane]);
+          const int64_t row = r0 + lane;
+          if (row < n) dvec[row] = v;
         }
       }
 #undef LP_S
@@ -323,19 +410,22 @@ int lhat_paper_max_bucket(const void* X, int64_t ldx, int64_t d) {
 
 template <int BPB>
 static cudaError_t go_lp(const CUtensorMap& map, const double* Qp, double* L, int64_t ldl, int64_t n,
-                         int64_t d, double* dvec, DevState* st, cudaStream_t s) {
+                         int64_t d, double* dvec, DevState* st, double* Xr, int64_t ldx, int resid,
+                         cudaStream_t s) {
   using Cf = LpCfg<BPB>;
   int ns, nq;
   if (!Cf::rings(ns, nq)) return cudaErrorInvalidValue;
   const size_t smem = Cf::smem(ns, nq);
   cudaFuncSetAttribute(k_lhat_paper<BPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int nc = (int)((d + lp::KC - 1) / lp::KC);
-  k_lhat_paper<BPB><<<lp_sms(), lp::NTH, smem, s>>>(map, Qp, L, ldl, n, (int)d, nc, ns, nq, dvec, st);
+  k_lhat_paper<BPB><<<lp_sms(), lp::NTH, smem, s>>>(map, Qp, L, ldl, n, (int)d, nc, ns, nq, dvec, st, Xr, ldx,
+                                                     resid);
   return cudaGetLastError();
 }
 
 cudaError_t launch_lhat_paper(const double* X, int64_t ldx, const double* Qp, double* L, int64_t ldl,
-                              int64_t n, int64_t d, double* dvec, DevState* st, int bucket, cudaStream_t s) {
+                              int64_t n, int64_t d, double* dvec, DevState* st, int bucket, bool resid,
+                              cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   auto enc = lp_encode();
   if (!enc) return cudaErrorNotSupported;
@@ -349,8 +439,8 @@ cudaError_t launch_lhat_paper(const double* X, int64_t ldx, const double* Qp, do
       CUDA_SUCCESS)
     return cudaErrorInvalidValue;
   switch (bucket) {
-    case 16: return go_lp<16>(map, Qp, L, ldl, n, d, dvec, st, s);
-    case 32: return go_lp<32>(map, Qp, L, ldl, n, d, dvec, st, s);
+    case 16: return go_lp<16>(map, Qp, L, ldl, n, d, dvec, st, (double*)X, ldx, resid ? 1 : 0, s);
+    case 32: return go_lp<32>(map, Qp, L, ldl, n, d, dvec, st, (double*)X, ldx, resid ? 1 : 0, s);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -101,7 +101,8 @@ cudaError_t launch_proj_fused(double* Xres, int64_t ldx, const double* Qp, doubl
 // k_lhat_paper.cu — paper form, l.13 + l.16: read-only DMMA pass with 64-row tiles
 int lhat_paper_max_bucket(const void* X, int64_t ldx, int64_t d);
 cudaError_t launch_lhat_paper(const double* X, int64_t ldx, const double* Qp, double* L, int64_t ldl,
-                              int64_t n, int64_t d, double* dvec, DevState* st, int bucket, cudaStream_t s);
+                              int64_t n, int64_t d, double* dvec, DevState* st, int bucket, bool resid,
+                              cudaStream_t s);   // resid: + the update pass (residual form, L2 re-read)
 
 // k_paper.cu — left-looking (paper) form of Alg. 2: CGS2 of the candidate rows (l.6),
 // Q append (l.10), exact zeros of earlier skeletons' L-hat (R13), d downdate (l.16)

@@ -205,7 +205,8 @@ struct Ctx {
   bool use_mma, use_forced;
   int bucketB;
   int fused_max;   // largest bucket run by the fused single-pass projection (0: none)
-  int lp_max;      // paper form: largest bucket run by k_lhat_paper (0: none)
+  int lp_max;      // largest bucket run by the 64-row tiled kernel k_lhat_paper (0: none)
+  bool tiled;      // residual form on the 64-row tiled kernel (L-hat pass + update pass via L2)
 };
 
 // pointers of one shard's workspace
@@ -263,7 +264,11 @@ void make_ctx(Ctx<T>& c, const rbrp_problem* p, void* Xv, char* ws, const Layout
   c.use_mma = sizeof(T) == 8 && !force_simt() && projection_mma_supported(c.Xres, c.ldr, c.Qt, c.d);
   c.bucketB = bucket_of((int)std::min<int64_t>(p->b, c.k_cap));
   c.fused_max = (c.use_mma && !env_on("RBRP_NO_FUSED")) ? fused_max_bucket(c.Xres, c.ldr, c.d) : 0;
-  c.lp_max = (c.paper && c.use_mma && !env_on("RBRP_NO_FUSED")) ? lhat_paper_max_bucket(c.Xres, c.ldr, c.d) : 0;
+  // residual form: the 64-row tiled kernel (L-hat pass + update pass re-reading the tile
+  // through L2) by default; RBRP_FUSED16=1 selects the 16-row smem-resident k_proj_fused
+  c.tiled = !c.paper && c.use_mma && !env_on("RBRP_FUSED16");
+  c.lp_max = ((c.paper || c.tiled) && c.use_mma && !env_on("RBRP_NO_FUSED")) ? lhat_paper_max_bucket(c.Xres, c.ldr, c.d)
+                                                                            : 0;
 }
 
 template <typename T>
@@ -300,14 +305,14 @@ int enqueue_projection(Ctx<T>& c, cudaStream_t s, int* nl) {
   };
   int rc = RBRP_OK;
   // the single-pass kernel: k_proj_fused (residual form) or k_lhat_paper (paper form)
-  const int fmax = c.paper ? c.lp_max : c.fused_max;
+  const int fmax = (c.paper || c.tiled) ? c.lp_max : c.fused_max;
   if (fmax > 0 && (rc = lk(launch_pack_q((const double*)c.Qt, c.d, c.Qp, c.st, s)))) return rc;
   bool need_downdate = false;
   for (int bk = 16; bk <= c.bucketB; bk *= 2) {
     if (bk <= fmax) {
-      if (c.paper)
+      if (c.paper || c.tiled)
         rc = lk(launch_lhat_paper((const double*)c.Xres, c.ldr, c.Qp, (double*)c.Lm, c.k_cap, c.n, c.d,
-                                  c.dvec, c.st, bk, s));
+                                  c.dvec, c.st, bk, !c.paper, s));
       else
         rc = lk(launch_proj_fused((double*)c.Xres, c.ldr, c.Qp, (double*)c.Lm, c.k_cap, c.n, c.d, c.dvec,
                                   c.st, bk, false, s));
