@@ -92,7 +92,9 @@ enum {
  *   b          block size (>= 1, <= RBRP_MAX_B).
  *   tau_b      filter tolerance (Alg. 2 input (d)): < 0 -> 1/b_t (default,
  *              reading R4); 0 -> plain BRP; must be <= 1.
- *   greedy     0 = RBRP sampling (l.5); 1 = RBGP: top-b_t residual norms (Remark 4.2).
+ *   greedy     0 = RBRP sampling (l.5); 1 = RBGP: S_t = the top-b_t residual norms, ties to
+ *              the lower row, positive entries only (Remark 4.2); single GPU only
+ *              (a communicator returns RBRP_ENOTSUP).  tau_b = 0 with greedy = 0 is plain BRP.
  *   seed       64-bit sampler seed: Philox4x32-10 key (reading R8).
  *   flags      RBRP_INPLACE | RBRP_NO_W.
  *   replay_blocks / replay_lens / replay_nblocks  (host, optional, may be NULL):

@@ -150,6 +150,16 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample(SampleArgs A) {
     if (tid == 0) { st->b_t = A.replay_len; st->draws = 0; }
     return;
   }
+  if (A.greedy) {   // RBGP (Remark 4.2): the top b_t rows of d, in order (k_topb)
+    const int c = min(s_bt, *A.top_cnt);
+    for (int i = tid; i < c; i += kSampleThreads) A.S_t[i] = A.S_top[i];
+    if (tid == 0) {
+      st->b_t = c;
+      st->draws = 0;
+      if (c < s_bt) st->flags |= RBRP_F_SUPPORT_EXHAUSTED;
+    }
+    return;
+  }
   const int bt = s_bt;
   if (s_np <= bt) {
     // reading R7: every positive-weight row, in row order (local rows; single GPU)

@@ -31,6 +31,9 @@ struct SampleArgs {
   unsigned long long cond;   // cudaGraphConditionalHandle of the WHILE node (0: none)
   int dist;               // 1: row-sharded run; this kernel only does the stop test / b_t
   int64_t* cand;          // distributed rounds: candidate rows of kSampleRound draws (-1 = not mine)
+  int greedy;             // RBGP (Remark 4.2): S_t = the top b_t rows of d (k_topb), no draw
+  const int64_t* S_top;   // greedy: top rows of d, in order
+  const int* top_cnt;     // greedy: how many of them have d > 0
 };
 cudaError_t launch_sample(const SampleArgs& a, cudaStream_t s);
 // distributed sampling: every rank resolves the draws that land in its
@@ -39,6 +42,11 @@ cudaError_t launch_sample(const SampleArgs& a, cudaStream_t s);
 constexpr int kSampleRound = 256;
 cudaError_t launch_draw_resolve(const SampleArgs& a, cudaStream_t s);
 cudaError_t launch_draw_accept(const SampleArgs& a, cudaStream_t s);
+
+// k_topb.cu — RBGP candidate block (Remark 4.2): top-B rows of d, ties to the lower row
+size_t topb_scratch_bytes(int64_t n, int B);
+cudaError_t launch_topb(const double* dvec, int64_t n, int64_t row_offset, int B, void* scratch, int64_t* S_top,
+                        int* top_cnt, const DevState* st, cudaStream_t s);
 
 // k_filter.cu — Alg. 2 l.6-9
 template <typename T>

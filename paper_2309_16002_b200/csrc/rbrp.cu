@@ -34,7 +34,7 @@ namespace {
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
-  size_t Xres = SIZE_MAX, Qall = SIZE_MAX, Ccgs = SIZE_MAX, dvec, cpre, ctot, cpos, cprefix, L, Qt, Qp, Vg, Gpart, G, Tg, Ag, R11, Rtot,
+  size_t Xres = SIZE_MAX, Qall = SIZE_MAX, Ccgs = SIZE_MAX, Topb = SIZE_MAX, Stop = SIZE_MAX, Tcnt = SIZE_MAX, dvec, cpre, ctot, cpos, cprefix, L, Qt, Qp, Vg, Gpart, G, Tg, Ag, R11, Rtot,
          piv, mass, St, Srep, S, forced, dbg, cand, st, L1 = SIZE_MAX, LinvT = SIZE_MAX;
   size_t lbt, lbp, lrho, lSt, lpiv, lts, total;
   int nsplit, maxlog;
@@ -79,6 +79,11 @@ Layout make_layout(const rbrp_problem* p) {
   const size_t B = RBRP_MAX_B;
   const bool paper = (p->flags & RBRP_FORM_PAPER) != 0;
   if (!(p->flags & RBRP_INPLACE) && !paper) L.Xres = take((size_t)n * d * w);
+  if (p->greedy) {   // RBGP candidate tournament (k_topb)
+    L.Topb = take(topb_scratch_bytes(n, p->b));
+    L.Stop = take((size_t)RBRP_MAX_B * 8);
+    L.Tcnt = take(8);
+  }
   if (paper) {
     L.Qall = take((size_t)L.k_cap * d * w);   // Q = [Q_1 ... Q_t] rows (l.10)
     L.Ccgs = take((size_t)RBRP_MAX_B * L.k_cap * 8);   // CGS coefficients (l.6)
@@ -195,6 +200,7 @@ struct Ctx {
   double* Qp;   // packed Q_b chunks of the fused projection
   T* Qall;      // paper form: accumulated Q rows (k_cap x d)
   double* Ccgs; // paper form: CGS coefficients
+  char* ws;     // workspace base
   bool paper;   // RBRP_FORM_PAPER: left-looking, X read only
   int64_t *St, *Srep, *S, *cand;
   double* L1;
@@ -224,6 +230,7 @@ void make_ctx(Ctx<T>& c, const rbrp_problem* p, void* Xv, char* ws, const Layout
   c.paper = (p->flags & RBRP_FORM_PAPER) != 0;
   c.Xres = (inplace || c.paper) ? c.X : (T*)(ws + Ly.Xres);   // paper form: X itself, read only
   c.ldr = (inplace || c.paper) ? p->ld : c.d;
+  c.ws = ws;
   c.Qall = c.paper ? (T*)(ws + Ly.Qall) : nullptr;
   c.Ccgs = c.paper ? (double*)(ws + Ly.Ccgs) : nullptr;
   c.dvec = (double*)(ws + Ly.dvec);
@@ -292,6 +299,22 @@ void make_sample_args(SampleArgs& sa, const Ctx<T>& c, int dist) {
   sa.cond = 0;
   sa.dist = dist;
   sa.cand = c.cand;
+  sa.greedy = c.p->greedy ? 1 : 0;
+  sa.S_top = c.p->greedy ? (const int64_t*)((char*)c.ws + c.Ly->Stop) : nullptr;
+  sa.top_cnt = c.p->greedy ? (const int*)((char*)c.ws + c.Ly->Tcnt) : nullptr;
+}
+
+// l.5: RBRP draw, or (RBGP, Remark 4.2) the top-b rows of d computed first by k_topb
+template <typename T>
+cudaError_t launch_block_sample(Ctx<T>& c, SampleArgs& sa, cudaStream_t s, int* nl) {
+  if (sa.greedy) {
+    ++*nl;
+    cudaError_t e = launch_topb(c.dvec, c.n, c.p->row_offset, c.p->b, c.ws + c.Ly->Topb,
+                                (int64_t*)(c.ws + c.Ly->Stop), (int*)(c.ws + c.Ly->Tcnt), c.st, s);
+    if (e != cudaSuccess) return e;
+  }
+  ++*nl;
+  return launch_sample(sa, s);
 }
 
 // a4 (Alg. 2 l.13 + l.16): one fused single-pass kernel (k_proj_fused) for the buckets
@@ -408,7 +431,7 @@ int enqueue_block(Ctx<T>& c, SampleArgs& sa, cudaStream_t s, Prof* prof, int* nl
   }
   if (with_sample) {
     if (prof) prof->begin(1);
-    LK(launch_sample(sa, s));
+    if (launch_block_sample(c, sa, s, nl) != cudaSuccess) return RBRP_ECUDA;
     if (prof) prof->end();
   }
 #undef LK
@@ -596,8 +619,7 @@ int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* 
   if (rl < -100) return rl + 1000;
   sa.replay_len = rl;
   prof.begin(1);
-  ++nl;
-  CK(launch_sample(sa, s));
+  CK(launch_block_sample(c, sa, s, &nl));
   prof.end();
   CK(cudaMemcpyAsync(hst, c.st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
@@ -621,8 +643,7 @@ int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* 
       if (rl < -100) return rl + 1000;
       sa.replay_len = rl;
       prof.begin(1);
-      ++nl;
-      CK(launch_sample(sa, s));
+      CK(launch_block_sample(c, sa, s, &nl));
       prof.end();
       CK(cudaMemcpyAsync(hst, c.st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
@@ -1050,7 +1071,6 @@ int rbrp_id(const rbrp_problem* p, void* X, void* workspace, size_t ws_bytes, rb
   int rc = validate(p);
   if (rc) return rc;
   if (!S_out || (p->n_local > 0 && !X) || !workspace) return RBRP_EINVAL;
-  if (p->greedy) return RBRP_ENOTSUP;
   if (comm && (p->row_offset % RBRP_CHUNK) != 0) return RBRP_EINVAL;
   if (filter_coop_nsplit(p->d) > 148) return RBRP_ENOTSUP;   // d > 4736: one CTA per 32 columns
   Layout Ly = make_layout(p);

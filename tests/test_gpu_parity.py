@@ -412,3 +412,46 @@ def test_paper_form_same_seed_matches_residual_form():
     assert max(abs(a - b) for a, b in zip(r.rho, p.rho)) <= 1e-10
     Wr, Wp = r.W.cpu(), p.W.cpu()
     assert torch.linalg.norm(Wr - Wp) <= 1e-9 * torch.linalg.norm(Wr)
+
+
+@cuda
+def test_brp_tau_b_zero_replay_parity():
+    """NEXT-2, plain BRP (tau_b = 0: the filter of l.8 keeps every candidate)
+    against the oracle in replay mode: S and b' exact, rho_t within 1e-10."""
+    cfg = small_config("c5", n=12000, d=160, n_centres=60, b=16)
+    Xnp = make(cfg).numpy()
+    tau = (1 + cfg.eps) * R.eta(Xnp, 40)
+    ores = O.rbrp(Xnp, tau=tau, b=16, seed=0, tau_b=0.0)
+    rb = _rb()
+    blocks = [blk.S_t for blk in ores.blocks]
+    piv = [blk.piv for blk in ores.blocks]
+    res = rb.id(torch.from_numpy(Xnp).cuda(), k=ores.k, b=16, tau_b=0.0, replay_blocks=blocks,
+                replay_pivots=piv)
+    assert res.S.tolist() == ores.S
+    assert res.b_prime == [blk.b_prime for blk in ores.blocks]
+    assert all(bp == len(blk.S_t) or bp < len(blk.S_t) for bp, blk in zip(res.b_prime, ores.blocks))
+    for a, blk in zip(res.rho, ores.blocks):
+        assert abs(a - blk.rho) <= 1e-10
+    _check_W(Xnp, res, ores, np.float64)
+
+
+@cuda
+@pytest.mark.parametrize("name,kw,tau", [
+    ("c2", dict(n=20000 + 99, d=256, rank=40, b=16), 1e-12),
+    ("c5", dict(n=30000, d=128, n_centres=40, b=32), None),
+])
+def test_rbgp_greedy_matches_oracle(name, kw, tau):
+    """NEXT-2, RBGP (Remark 4.2): S_t = the b_t largest residual norms (ties to
+    the lower row; device tournament k_topb).  Deterministic, so GPU and oracle select the
+    same skeletons in the same order with no replay (the inputs have no near-ties)."""
+    cfg = small_config(name, **kw)
+    Xnp = make(cfg).numpy()
+    if tau is None:
+        tau = (1 + cfg.eps) * R.eta(Xnp, 40)
+    ores = O.rbrp(Xnp, tau=tau, b=cfg.b, seed=0, greedy=True)
+    res = _rb().id(torch.from_numpy(Xnp).cuda(), tol=tau, b=cfg.b, greedy=True)
+    assert res.S.tolist() == ores.S
+    assert res.b_prime == [blk.b_prime for blk in ores.blocks]
+    for a, blk in zip(res.rho, ores.blocks):
+        assert abs(a - blk.rho) <= 1e-10
+    _check_W(Xnp, res, ores, np.float64)
