@@ -455,3 +455,24 @@ def test_rbgp_greedy_matches_oracle(name, kw, tau):
     for a, blk in zip(res.rho, ores.blocks):
         assert abs(a - blk.rho) <= 1e-10
     _check_W(Xnp, res, ores, np.float64)
+
+
+@cuda
+def test_table3_gmm_robust_filter_and_replay_parity():
+    """NEXT-3 workload (Example 4.1, the paper's Table 3 matrix at full size):
+    fixed-rank RBRP at k = 52 matches the oracle in replay mode, and at k = 100 the robust
+    filter yields (nearly) one skeleton per cluster while plain BRP (tau_b = 0) repeats
+    clusters -- the pitfall the example describes (Fig. 1)."""
+    from workloads import CONFIGS as C
+    cfg = C["t3"]
+    X = make(cfg, device="cuda")
+    Xnp = X.cpu().numpy()
+    ores = O.rbrp(Xnp, k=52, b=cfg.b, seed=0)
+    _replay(Xnp, ores, np.float64, cfg.b)
+    rb = _rb()
+    m = cfg.n // cfg.n_centres
+    r = rb.id(X, k=100, b=cfg.b, seed=0, with_W=False)
+    p = rb.id(X, k=100, b=cfg.b, seed=0, tau_b=0.0, with_W=False)
+    cr = len({int(i) // m for i in r.S.tolist()})
+    cp = len({int(i) // m for i in p.S.tolist()})
+    assert cr >= 90 and cr > cp, (cr, cp)

@@ -7,4 +7,4 @@ BASELINE.json's configs (and scaled-down versions of them) from a seeded
 generator.  Both the CPU oracle (`oracle/`) and the CUDA path consume its
 output; neither imports the other.
 """
-from .generators import CONFIGS, Config, make, small_config  # noqa: F401
+from .generators import CONFIGS, T3_RANKS, Config, make, small_config  # noqa: F401

@@ -16,6 +16,8 @@ The constructions follow BASELINE.json `configs` with the readings of SURVEY
       Example 2.3 / 4.1 spirit)
   c4  X = U diag(i^-1.5) V^T rounded to fp32, U CholQR2-orthonormalised
       Gaussian, V Haar
+  t3  Example 4.1's adversarial GMM (the paper's Table 3 workload, NEXT-3): row
+      m (j-1) + i = 10 j e_j + xi_i, j = 1..100 clusters of m = 1000 rows, xi ~ N(0, I)
   c5  row i = mu_(c(i)) + 0.05 xi_i, 256 centres mu ~ N(0, I)  (GMM, Example
       4.1 spirit)
 No item of any public dataset is reproduced: all inputs are synthetic.
@@ -59,7 +61,14 @@ CONFIGS = {
     "c3": Config("c3", "c3", "f64", 131072, 512, 64, r=200, eps=0.2),
     "c4": Config("c4", "c4", "f32", 1048576, 2048, 64, tau=1e-3),
     "c5": Config("c5", "c5", "f64", 4194304, 1024, 128, r=256, eps=0.1),
+    # the paper's own GPU workload (Table 3): the adversarial GMM
+    # of Example 4.1, n = 10^5, d = 10^3, k = 100 clusters of m = 1000 rows,
+    # row m(j-1)+i = 10 j e_j + xi_i, run in fixed-rank mode with b = 40
+    "t3": Config("t3", "t3", "f64", 100000, 1000, 40, n_centres=100),
 }
+
+# Table 3 fixed ranks
+T3_RANKS = (32, 52, 73, 100, 157, 220, 283, 346, 409, 472)
 
 
 def small_config(name: str, **kw) -> Config:
@@ -139,6 +148,13 @@ def make(cfg: Config, device="cpu", row_offset: int = 0, n_local: Optional[int] 
         return X.to(dt).contiguous()
     if cfg.kind == "c4":
         return _make_c4(cfg, device, r0, r1)
+    if cfg.kind == "t3":
+        # Example 4.1: clusters are contiguous row ranges of m = n / k rows
+        m = n // cfg.n_centres
+        j = torch.arange(r0, r1, device=device) // m                     # 0-based cluster
+        X = _randn_rows(s, 1, r0, r1, d, device)
+        X[torch.arange(r1 - r0, device=device), j] += 10.0 * (j + 1).to(torch.float64)
+        return X.to(dt).contiguous()
     if cfg.kind == "c5":
         C = _randn_rows(s, 1, 0, cfg.n_centres, d, device)
         # label c(i): uniform over centres, drawn per panel
