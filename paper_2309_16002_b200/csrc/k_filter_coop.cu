@@ -365,10 +365,12 @@ __global__ void __launch_bounds__(kFiltThreads, 1) k_filter_coop(FilterArgs F) {
   __shared__ long long s_k;
   DevState* st = F.st;
   const int tid = threadIdx.x, w = tid >> 5;
+  __shared__ int s_first;
   if (tid == 0) {
     s_stop = st->stop;
     s_nb = st->b_t;
     s_k = st->k;
+    s_first = (F.X0 != nullptr && st->t == 1) ? 1 : 0;   // lazy X_res: block 1 reads X
   }
   __syncthreads();
   if (s_stop || s_nb <= 0) return;   // uniform over the grid
@@ -399,7 +401,7 @@ __global__ void __launch_bounds__(kFiltThreads, 1) k_filter_coop(FilterArgs F) {
         v = F.Vg[(int64_t)i * d + c0 + c];
       } else {
         const int64_t r = F.S_t[i] - F.row_offset;
-        v = (double)((const T*)F.X)[r * F.ldx + c0 + c];
+        v = s_first ? (double)((const T*)F.X0)[r * F.ldx0 + c0 + c] : (double)((const T*)F.X)[r * F.ldx + c0 + c];
       }
     }
     Vs[i * kFiltLd + c] = v;

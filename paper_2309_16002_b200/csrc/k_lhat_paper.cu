@@ -104,7 +104,8 @@ struct LpCfg {
 
 template <int BPB>
 __global__ void __launch_bounds__(lp::NTH, 1)
-    k_lhat_paper(const __grid_constant__ CUtensorMap xmap, const double* __restrict__ Qp,
+    k_lhat_paper(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap xmap0,
+                 int lazy, const double* __restrict__ Qp,
                  double* __restrict__ L, int64_t ldl, int64_t n, int d, int nc, int NS, int NQ,
                  double* __restrict__ dvec, DevState* st, double* __restrict__ Xr, int64_t ldx, int resid) {
   using Cf = LpCfg<BPB>;
@@ -151,6 +152,8 @@ __global__ void __launch_bounds__(lp::NTH, 1)
     // X producer.  Residual form: the L-hat pass loads a tile with an L2 evict_last
     // policy, the update pass (same addresses, shortly after) with evict_first, so the
     // second read is served by L2 and HBM sees one read of X_res.
+    // lazy X_res copy: block 1 reads the input X (xmap0); the update pass writes X_res
+    const CUtensorMap* mp = (lazy && st->t == 1) ? &xmap0 : &xmap;
     if (lane == 0) {
       uint64_t pol_keep, pol_drop;
       asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol_keep));
@@ -168,7 +171,7 @@ __global__ void __launch_bounds__(lp::NTH, 1)
           asm volatile(
               "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint "
               "[%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(lp_su32(dst + b * BOX)),
-              "l"(&xmap), "r"(c * KC + 16 * b), "r"(y), "r"(lp_su32(&xfull[xr.i])), "l"(pol)
+              "l"(mp), "r"(c * KC + 16 * b), "r"(y), "r"(lp_su32(&xfull[xr.i])), "l"(pol)
               : "memory");
         xr.next(NS);
       }
@@ -409,38 +412,42 @@ int lhat_paper_max_bucket(const void* X, int64_t ldx, int64_t d) {
 }
 
 template <int BPB>
-static cudaError_t go_lp(const CUtensorMap& map, const double* Qp, double* L, int64_t ldl, int64_t n,
-                         int64_t d, double* dvec, DevState* st, double* Xr, int64_t ldx, int resid,
-                         cudaStream_t s) {
+static cudaError_t go_lp(const CUtensorMap& map, const CUtensorMap& map0, int lazy, const double* Qp, double* L,
+                         int64_t ldl, int64_t n, int64_t d, double* dvec, DevState* st, double* Xr, int64_t ldx,
+                         int resid, cudaStream_t s) {
   using Cf = LpCfg<BPB>;
   int ns, nq;
   if (!Cf::rings(ns, nq)) return cudaErrorInvalidValue;
   const size_t smem = Cf::smem(ns, nq);
   cudaFuncSetAttribute(k_lhat_paper<BPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int nc = (int)((d + lp::KC - 1) / lp::KC);
-  k_lhat_paper<BPB><<<lp_sms(), lp::NTH, smem, s>>>(map, Qp, L, ldl, n, (int)d, nc, ns, nq, dvec, st, Xr, ldx,
-                                                     resid);
+  k_lhat_paper<BPB><<<lp_sms(), lp::NTH, smem, s>>>(map, map0, lazy, Qp, L, ldl, n, (int)d, nc, ns, nq, dvec, st,
+                                                     Xr, ldx, resid);
   return cudaGetLastError();
 }
 
 cudaError_t launch_lhat_paper(const double* X, int64_t ldx, const double* Qp, double* L, int64_t ldl,
                               int64_t n, int64_t d, double* dvec, DevState* st, int bucket, bool resid,
-                              cudaStream_t s) {
+                              cudaStream_t s, const double* X0, int64_t ldx0) {
   if (n <= 0) return cudaSuccess;
   auto enc = lp_encode();
   if (!enc) return cudaErrorNotSupported;
-  CUtensorMap map;
-  const cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)n};
-  const cuuint64_t strides[1] = {(cuuint64_t)ldx * 8};
-  const cuuint32_t box[2] = {16, (cuuint32_t)lp::R};
-  const cuuint32_t estr[2] = {1, 1};
-  if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)X, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
-      CUDA_SUCCESS)
-    return cudaErrorInvalidValue;
+  auto make_map = [&](const double* P, int64_t ld, CUtensorMap* map) {
+    const cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)n};
+    const cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
+    const cuuint32_t box[2] = {16, (cuuint32_t)lp::R};
+    const cuuint32_t estr[2] = {1, 1};
+    return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)P, dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  };
+  CUtensorMap map, map0;
+  if (!make_map(X, ldx, &map)) return cudaErrorInvalidValue;
+  const int lazy = X0 != nullptr ? 1 : 0;
+  if (!make_map(lazy ? X0 : X, lazy ? ldx0 : ldx, &map0)) return cudaErrorInvalidValue;
   switch (bucket) {
-    case 16: return go_lp<16>(map, Qp, L, ldl, n, d, dvec, st, (double*)X, ldx, resid ? 1 : 0, s);
-    case 32: return go_lp<32>(map, Qp, L, ldl, n, d, dvec, st, (double*)X, ldx, resid ? 1 : 0, s);
+    case 16: return go_lp<16>(map, map0, lazy, Qp, L, ldl, n, d, dvec, st, (double*)X, ldx, resid ? 1 : 0, s);
+    case 32: return go_lp<32>(map, map0, lazy, Qp, L, ldl, n, d, dvec, st, (double*)X, ldx, resid ? 1 : 0, s);
     default: return cudaErrorInvalidValue;
   }
 }

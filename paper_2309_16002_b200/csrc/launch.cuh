@@ -58,6 +58,8 @@ struct FilterArgs {
   DevState* st;
   const void* X;            // X_res (dtype T), used when Vg == nullptr
   int64_t ldx;
+  const void* X0;           // lazy X_res copy: block 1 reads V from X itself (or null)
+  int64_t ldx0;
   const double* Vg;         // pre-gathered V rows (multi-GPU, after allreduce) or null
   const int64_t* S_t;       // candidates (global ids)
   int64_t row_offset, d;
@@ -110,7 +112,9 @@ cudaError_t launch_proj_fused(double* Xres, int64_t ldx, const double* Qp, doubl
 int lhat_paper_max_bucket(const void* X, int64_t ldx, int64_t d);
 cudaError_t launch_lhat_paper(const double* X, int64_t ldx, const double* Qp, double* L, int64_t ldl,
                               int64_t n, int64_t d, double* dvec, DevState* st, int bucket, bool resid,
-                              cudaStream_t s);   // resid: + the update pass (residual form, L2 re-read)
+                              cudaStream_t s, const double* X0 = nullptr, int64_t ldx0 = 0);
+// resid: + the update pass (residual form, L2 re-read).  X0 (lazy X_res): in block 1 the
+// tile is read from X0 (the input) and the update is written to X (X_res)
 
 // k_paper.cu — left-looking (paper) form of Alg. 2: CGS2 of the candidate rows (l.6),
 // Q append (l.10), exact zeros of earlier skeletons' L-hat (R13), d downdate (l.16)

@@ -213,6 +213,7 @@ struct Ctx {
   int fused_max;   // largest bucket run by the fused single-pass projection (0: none)
   int lp_max;      // largest bucket run by the 64-row tiled kernel k_lhat_paper (0: none)
   bool tiled;      // residual form on the 64-row tiled kernel (L-hat pass + update pass via L2)
+  bool lazy;       // X_res not copied at init: block 1's projection reads X and writes X_res
 };
 
 // pointers of one shard's workspace
@@ -276,6 +277,11 @@ void make_ctx(Ctx<T>& c, const rbrp_problem* p, void* Xv, char* ws, const Layout
   c.tiled = !c.paper && c.use_mma && !env_on("RBRP_FUSED16");
   c.lp_max = ((c.paper || c.tiled) && c.use_mma && !env_on("RBRP_NO_FUSED")) ? lhat_paper_max_bucket(c.Xres, c.ldr, c.d)
                                                                             : 0;
+  // the tiled kernel handles every bucket of this problem, so it can take block 1 straight
+  // from X (X_res is then never copied: one HBM read + write less per ID).  Single-GPU
+  // path only (run_dist keeps the copy).
+  c.lazy = c.tiled && !inplace && c.Xres != c.X && c.lp_max >= c.bucketB && c.lp_max > 0 &&
+           lhat_paper_max_bucket(c.X, p->ld, c.d) >= c.bucketB && !comm && !env_on("RBRP_EAGER_COPY");
 }
 
 template <typename T>
@@ -335,7 +341,8 @@ int enqueue_projection(Ctx<T>& c, cudaStream_t s, int* nl) {
     if (bk <= fmax) {
       if (c.paper || c.tiled)
         rc = lk(launch_lhat_paper((const double*)c.Xres, c.ldr, c.Qp, (double*)c.Lm, c.k_cap, c.n, c.d,
-                                  c.dvec, c.st, bk, !c.paper, s));
+                                  c.dvec, c.st, bk, !c.paper, s, c.lazy ? (const double*)c.X : nullptr,
+                                  c.p->ld));
       else
         rc = lk(launch_proj_fused((double*)c.Xres, c.ldr, c.Qp, (double*)c.Lm, c.k_cap, c.n, c.d, c.dvec,
                                   c.st, bk, false, s));
@@ -377,6 +384,8 @@ int enqueue_block(Ctx<T>& c, SampleArgs& sa, cudaStream_t s, Prof* prof, int* nl
   fa.st = c.st;
   fa.X = c.Xres;
   fa.ldx = c.ldr;
+  fa.X0 = c.lazy ? c.X : nullptr;
+  fa.ldx0 = p->ld;
   fa.Vg = nullptr;
   if (c.comm || c.paper) {
     if (c.comm) CK(cudaMemsetAsync(c.Vg, 0, (size_t)RBRP_MAX_B * c.d * 8, s));
@@ -579,7 +588,7 @@ int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* 
   // a0: d^(0), X_res <- X (Alg. 2 l.1-2)
   prof.begin(0);
   ++nl;
-  CK(launch_init_norms<T>(c.X, p->ld, c.Xres, c.n, c.d, c.dvec, c.st, !inplace && !c.paper, s));
+  CK(launch_init_norms<T>(c.X, p->ld, c.Xres, c.n, c.d, c.dvec, c.st, !inplace && !c.paper && !c.lazy, s));
   ++nl;
   CK(launch_chunk_scan(c.dvec, c.n, c.chunk0, c.cpre, c.ctot, c.cpos, s));
   prof.end();
@@ -910,6 +919,8 @@ int run_dist(int nsh, const rbrp_problem* ps, void* const* Xs, char* const* wss,
       fa.st = c.st;
       fa.X = c.Xres;
       fa.ldx = c.ldr;
+      fa.X0 = nullptr;
+      fa.ldx0 = 0;
       fa.Vg = c.Vg;
       fa.S_t = c.St;
       fa.row_offset = ps[h].row_offset;
