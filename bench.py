@@ -149,6 +149,43 @@ def _proj_roofline(cfg, res_list, proj_ms, n_local, form="residual"):
     return flops / t / 1e12, bytes_ / t / 1e9, flops, bytes_
 
 
+def _dominant_kernel(cfg, res_list, n_local, form="residual"):
+    """Roofline of the DOMINANT projection kernel: the bucket instantiation (b' <= 16, 32,
+    64, 128 -> one kernel template each) with the most device time.  Per launch: the
+    algorithmic flops/bytes of _proj_roofline, divided by that launch's in-kernel stamp
+    time.  Also the mixed-bound fraction over all blocks: sum of per-block roofline floors
+    max(flops/F64 peak, bytes/HBM peak) over the summed block times."""
+    n, d = n_local, cfg.d
+    w = 8 if cfg.dtype == "f64" else 4
+    peak = FP64_PEAK_TFLOPS if cfg.dtype == "f64" else FP64_PEAK_TFLOPS * 2
+    per = {}
+    floor_s = time_s = 0.0
+    for res in res_list:
+        for bp, ms in zip(res.b_prime, res.proj_ms_blk):
+            if bp <= 0 or ms <= 0:
+                continue
+            bk = 16 if bp <= 16 else 32 if bp <= 32 else 64 if bp <= 64 else 128
+            if form == "paper":
+                fl, by = 2.0 * n * d * bp + 2.0 * n * bp, n * d * w + n * bp * w + 16.0 * n
+            else:
+                fl, by = 4.0 * n * d * bp + 2.0 * n * d, 2.0 * n * d * w + n * bp * w + 8.0 * n
+            e = per.setdefault(bk, [0.0, 0.0, 0.0, 0])
+            e[0] += fl
+            e[1] += by
+            e[2] += ms / 1e3
+            e[3] += 1
+            floor_s += max(fl / (peak * 1e12), by / (HBM_GBS * 1e9))
+            time_s += ms / 1e3
+    if not per:
+        return None
+    bk, (fl, by, t, cnt) = max(per.items(), key=lambda kv: kv[1][2])
+    return {"bucket": bk, "launches": cnt, "avg_launch_ms": t / cnt * 1e3,
+            "achieved_tflops": fl / t / 1e12, "frac_fp64": fl / t / 1e12 / peak,
+            "achieved_GBs": by / t / 1e9, "frac_hbm": by / t / 1e9 / HBM_GBS,
+            "algorithmic_flops_per_launch": fl / cnt, "algorithmic_bytes_per_launch": by / cnt,
+            "mixed_bound_frac_all_blocks": floor_s / time_s if time_s > 0 else None}
+
+
 def _traffic_from_profile(cfg_name):
     """dram bytes per block of the projection kernels from the committed ncu capture."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
@@ -287,6 +324,7 @@ def main():
     # first CTA start of L-hat -> last CTA end of the fused update, summed over blocks)
     proj_ms = sum(r.proj_ms for r in res_list)
     tflops, gbs, flops, bytes_ = _proj_roofline(cfg, res_list, proj_ms, n_local, a.form)
+    dom = _dominant_kernel(cfg, res_list, n_local, a.form)
     launches = sum(r.launches for r in res_list)
     r0res = res_list[-1]
     # per-phase breakdown from one eager, event-instrumented run (outside the timed region)
@@ -375,16 +413,23 @@ def main():
                    "parallelism": "single" if world == 1 else f"rows{world} (NCCL row sharding)",
                    "rows_per_rank": n_local, "graph_loop": r0res.graph,
                    "l2": "inputs larger than L2 (X 537 MB + residual 537 MB vs 126 MB L2); no flush"},
-        "roofline": {"kernel": "projection pass a4 (k_proj_fused: L-hat, residual update and row norms in "
-                               "one read + one write of X_res, Alg. 2 l.13/l.16)",
-                     "bound": "alu", "achieved": tflops, "peak": peak, "unit": "TFLOP/s",
-                     "frac": tflops / peak, "traffic": traffic,
-                     "timing": "in-kernel %globaltimer stamps, summed over the blocks of the K timed steps",
+        "roofline": {"kernel": ("projection pass a4, dominant kernel: the b' <= %d instantiation "
+                                "(%d launches; residual form: L-hat pass + update pass per 64-row tile, "
+                                "Alg. 2 l.13/l.16)" % (dom["bucket"], dom["launches"])) if dom else "projection pass a4",
+                     "bound": "alu", "achieved": dom["achieved_tflops"] if dom else tflops, "peak": peak,
+                     "unit": "TFLOP/s", "frac": (dom["frac_fp64"] if dom else tflops / peak), "traffic": traffic,
+                     "timing": "in-kernel %globaltimer stamps per launch (first CTA start -> last CTA end), "
+                               "K timed steps",
                      "peak_note": "FP64 (DMMA = DFMA rate): 148 SM x 64 FMA/clk x 2 x 1.965 GHz, derived "
                                   "(DESIGN.md §6); measured DMMA 37.2 TF; MEASURED_PEAKS.json has no FP64 entry",
+                     "dominant": dom,
+                     "all_blocks": {"achieved_tflops": tflops, "frac_fp64": tflops / peak,
+                                    "algorithmic_GBs": gbs, "hbm_frac_of_measured": gbs / HBM_GBS,
+                                    "mixed_bound_frac": dom["mixed_bound_frac_all_blocks"] if dom else None,
+                                    "note": "every block incl. the HBM-bound small-b' tail block; mixed_bound_frac "
+                                            "= sum of per-block max(flops/F64 peak, bytes/HBM peak) / sum of times"},
                      "algorithmic_flops_per_block": flops / max(nblk, 1),
                      "algorithmic_bytes_per_block": bytes_ / max(nblk, 1),
-                     "algorithmic_GBs": gbs, "hbm_frac_of_measured": gbs / HBM_GBS,
                      "share_of_step": proj_ms / a.steps / ms},
         "phase_ms_eager_profile": {k: v for k, v in rp.ms_phase.items() if k != "unused"},
         "gpu_launches": launches,

@@ -149,6 +149,8 @@ typedef struct {
  *              (first CTA start of L-hat to last CTA end of the update).
  *   graph      (out) 1 if the block loop ran as one CUDA-graph launch (conditional WHILE
  *              node), 0 if it was launched eagerly (replay, profile, or graphs unusable).
+ *   proj_ms_blk (optional, caller array of max_blocks floats, NULL to skip) the projection
+ *              device time of each logged block (same stamps as proj_ms).
  */
 typedef struct {
   int64_t k;
@@ -169,6 +171,7 @@ typedef struct {
   int32_t proj_calls;
   float proj_ms;
   int32_t graph;
+  float* proj_ms_blk;
 } rbrp_report;
 
 /* Opaque NCCL communicator wrapper; NULL means a single-GPU call. */

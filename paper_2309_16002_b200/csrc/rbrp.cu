@@ -746,7 +746,9 @@ int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* 
     const int32_t* lpiv = (const int32_t*)(hp + o_lpiv);
     double proj = 0.0;
     for (int t = 0; t < nblocks; ++t) {
-      if (lbp[t] > 0 && lts[2 * t + 1] > lts[2 * t]) proj += (lts[2 * t + 1] - lts[2 * t]) * 1e-6;
+      const double pms = (lbp[t] > 0 && lts[2 * t + 1] > lts[2 * t]) ? (lts[2 * t + 1] - lts[2 * t]) * 1e-6 : 0.0;
+      proj += pms;
+      if (rep->proj_ms_blk && t < rep->max_blocks) rep->proj_ms_blk[t] = (float)pms;
       if (t < rep->max_blocks) {
         if (rep->b_t) rep->b_t[t] = lbt[t];
         if (rep->b_prime) rep->b_prime[t] = lbp[t];
@@ -1029,7 +1031,9 @@ int run_dist(int nsh, const rbrp_problem* ps, void* const* Xs, char* const* wss,
     const long long* lts = (const long long*)(hp + o_ts);
     double proj = 0.0;
     for (int t = 0; t < nblocks; ++t) {
-      if (lbp[t] > 0 && lts[2 * t + 1] > lts[2 * t]) proj += (lts[2 * t + 1] - lts[2 * t]) * 1e-6;
+      const double pms = (lbp[t] > 0 && lts[2 * t + 1] > lts[2 * t]) ? (lts[2 * t + 1] - lts[2 * t]) * 1e-6 : 0.0;
+      proj += pms;
+      if (rep->proj_ms_blk && t < rep->max_blocks) rep->proj_ms_blk[t] = (float)pms;
       if (t < rep->max_blocks) {
         if (rep->b_t) rep->b_t[t] = lbt[t];
         if (rep->b_prime) rep->b_prime[t] = lbp[t];

@@ -51,7 +51,8 @@ class Report(ctypes.Structure):
                 ("block_piv", ctypes.POINTER(ctypes.c_int32)), ("ms_total", ctypes.c_float),
                 ("profile", ctypes.c_int32), ("ms_phase", ctypes.c_float * 8),
                 ("launches", ctypes.c_int32), ("proj_calls", ctypes.c_int32),
-                ("proj_ms", ctypes.c_float), ("graph", ctypes.c_int32)]
+                ("proj_ms", ctypes.c_float), ("graph", ctypes.c_int32),
+                ("proj_ms_blk", ctypes.POINTER(ctypes.c_float))]
 
 PHASES = ["init", "sample", "filter", "projection", "unused", "fixup_scan", "W", "comm"]
 
@@ -115,6 +116,7 @@ class Result:
     proj_calls: int
     proj_ms: float                  # device time of the projection passes (in-kernel stamps)
     graph: bool                     # block loop ran as one CUDA graph launch
+    proj_ms_blk: List[float] = dataclasses.field(default_factory=list)   # per block
 
 
 def _problem(X: torch.Tensor, tol, k, b, seed, k_max, tau_b, flags, n_global, row_offset, greedy):
@@ -214,8 +216,8 @@ def id(X: torch.Tensor, tol: Optional[float] = None, k: Optional[int] = None, b:
         else:
             W = torch.empty((X.shape[0], k_cap), dtype=X.dtype, device=X.device)
     S = torch.empty(k_cap, dtype=torch.int64)
-    rep = Report()
     mb = max_blocks
+    rep = _with_proj_blk(Report(), mb)
     b_t = (ctypes.c_int32 * mb)()
     b_pr = (ctypes.c_int32 * mb)()
     rho = (ctypes.c_double * mb)()
@@ -256,11 +258,18 @@ def _result(rep, S, W, b_t, b_pr, rho, bidx, bpiv, mb, b, log_blocks):
                   blocks=blocks, pivots=pivots, ms=rep.ms_total,
                   ms_phase={nm: rep.ms_phase[i] for i, nm in enumerate(PHASES)},
                   launches=rep.launches, proj_calls=rep.proj_calls, proj_ms=rep.proj_ms,
-                  graph=bool(rep.graph))
+                  graph=bool(rep.graph), proj_ms_blk=list(rep._pms[:nb]) if hasattr(rep, "_pms") else [])
+
+
+def _with_proj_blk(rep, mb):
+    """attach the optional per-block projection-time array (kept alive on the report)"""
+    rep._pms = (ctypes.c_float * mb)()
+    rep.proj_ms_blk = ctypes.cast(rep._pms, ctypes.POINTER(ctypes.c_float))
+    return rep
 
 
 def _report(mb, b, log_blocks):
-    rep = Report()
+    rep = _with_proj_blk(Report(), mb)
     b_t = (ctypes.c_int32 * mb)()
     b_pr = (ctypes.c_int32 * mb)()
     rho = (ctypes.c_double * mb)()
