@@ -16,6 +16,7 @@
 // ((c0 + c2) + (c1 + c3)): bitwise reproducible.
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <stdlib.h>
 
 #include "launch.cuh"
 
@@ -90,12 +91,14 @@ struct LpCfg {
   static constexpr int QSTAGE = BPB * lp::KC;
   static constexpr int SCR = lp::NRP * 2 * ACC * 32;   // two partial slots per row pair
   static size_t smem(int ns, int nq) {
-    return (size_t)ns * lp::SLOT * 8 + (size_t)nq * QSTAGE * 8 + (size_t)(SCR + lp::NRP * lp::NCW * 16) * 8 +
+    return (size_t)ns * lp::SLOT * 8 + (size_t)nq * QSTAGE * 8 + (size_t)(SCR + 2 * lp::NRP * lp::NCW * 16) * 8 +
            (2 * ns + 2 * nq) * 8 + 1024;
   }
   static bool rings(int& ns, int& nq) {
     ns = 4;
     nq = 4;
+    if (const char* e = getenv("RBRP_LP_NS")) ns = atoi(e);   // experiments only
+    if (const char* e = getenv("RBRP_LP_NQ")) nq = atoi(e);
     while (smem(ns, nq) > (size_t)lp::SMEM_MAX && nq > 2) --nq;
     while (smem(ns, nq) > (size_t)lp::SMEM_MAX && ns > 2) --ns;
     return smem(ns, nq) <= (size_t)lp::SMEM_MAX;
@@ -122,8 +125,8 @@ __global__ void __launch_bounds__(lp::NTH, 1)
   double* xs = sm;                                   // NS x SLOT
   double* qs = xs + (size_t)NS * SLOT;               // NQ x QSTAGE
   double* scr = qs + (size_t)NQ * Cf::QSTAGE;        // [rp][slot 0..1][ACC][32]
-  double* nrm = scr + Cf::SCR;                       // [rp][cw][16] row-norm partials (residual form)
-  uint64_t* xfull = reinterpret_cast<uint64_t*>(nrm + NRP * NCW * 16);
+  double* nrm = scr + Cf::SCR;                       // [tile parity][rp][cw][16] row-norm partials
+  uint64_t* xfull = reinterpret_cast<uint64_t*>(nrm + 2 * NRP * NCW * 16);
   uint64_t* xempty = xfull + NS;
   uint64_t* qfull = xempty + NS;
   uint64_t* qempty = qfull + NQ;
@@ -260,14 +263,13 @@ __global__ void __launch_bounds__(lp::NTH, 1)
             acc[r][t].y += LP_S(cw, r, t, 1);
           }
       }
-      lp_bar();
-      if (cw == 1) {
+      if (cw == 1) {   // c1 + c3 back into slot 1 (read above by this warp only)
 #pragma unroll
         for (int r = 0; r < 2; ++r)
 #pragma unroll
           for (int t = 0; t < NT; ++t) {
-            LP_S(0, r, t, 0) = acc[r][t].x;
-            LP_S(0, r, t, 1) = acc[r][t].y;
+            LP_S(1, r, t, 0) = acc[r][t].x;
+            LP_S(1, r, t, 1) = acc[r][t].y;
           }
       }
       lp_bar();
@@ -279,17 +281,17 @@ __global__ void __launch_bounds__(lp::NTH, 1)
           const int64_t row = r0 + 8 * r + pg;
 #pragma unroll
           for (int t = 0; t < NT; ++t) {
-            const double vx = acc[r][t].x + LP_S(0, r, t, 0);
-            const double vy = acc[r][t].y + LP_S(0, r, t, 1);
+            const double vx = acc[r][t].x + LP_S(1, r, t, 0);
+            const double vy = acc[r][t].y + LP_S(1, r, t, 1);
             const int j = 8 * t + 2 * q;
             if (row < n) {
               if (j < bp) L[row * ldl + k0 + j] = vx;
               if (j + 1 < bp) L[row * ldl + k0 + j + 1] = vy;
             }
             ss += vx * vx + vy * vy;
-            if (resid) {   // -P for the update pass, in the free scratch slot 1
-              LP_S(1, r, t, 0) = -vx;
-              LP_S(1, r, t, 1) = -vy;
+            if (resid) {   // -P for the update pass, in scratch slot 0 (read only by this warp)
+              LP_S(0, r, t, 0) = -vx;
+              LP_S(0, r, t, 1) = -vy;
             }
           }
           if (!resid) {
@@ -308,7 +310,7 @@ __global__ void __launch_bounds__(lp::NTH, 1)
 #pragma unroll
         for (int r = 0; r < 2; ++r)
 #pragma unroll
-          for (int t = 0; t < NT; ++t) pf[r][t] = make_double2(LP_S(1, r, t, 0), LP_S(1, r, t, 1));
+          for (int t = 0; t < NT; ++t) pf[r][t] = make_double2(LP_S(0, r, t, 0), LP_S(0, r, t, 1));
         const int64_t r0 = row0_of(p) + 16 * rp;
         double nr[2] = {0.0, 0.0};
         for (int c = 0; c < nc; ++c) {
@@ -356,7 +358,7 @@ __global__ void __launch_bounds__(lp::NTH, 1)
           }
         }
         // d(i) = ||x_res,i||^2: q lanes, then the 4 column groups in order
-        double* nb = nrm + (size_t)rp * NCW * 16;
+        double* nb = nrm + (size_t)((p & 1) * NRP + rp) * NCW * 16;
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
           double v = nr[r];
@@ -372,7 +374,10 @@ __global__ void __launch_bounds__(lp::NTH, 1)
         }
       }
 #undef LP_S
-      lp_bar();   // scratch is rewritten at the next tile end
+      // scratch is rewritten at the next tile's fold, nc chunk steps later; the NQ-stage Q
+      // ring keeps every warp within NQ steps of the others, so this barrier is only
+      // needed when a tile has no more than NQ chunks
+      if (nc <= NQ + 1) lp_bar();
     }
   }
   proj_end_stamp(st);
