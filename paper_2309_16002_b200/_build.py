@@ -69,7 +69,9 @@ def build(verbose: bool = False, force: bool = False) -> str:
         obj = os.path.join(OBJDIR, os.path.basename(src).replace(".cu", ".o"))
         objs.append(obj)
         if force or _stale(obj, [src] + headers):
-            jobs.append([nvcc, *ARCH, *FLAGS, *inc, "-c", src, "-o", obj])
+            # RBRP_EXTRA_NVCC: profiling builds only (e.g. "-DLP_TRACE=1"); force a rebuild
+            extra = os.environ.get("RBRP_EXTRA_NVCC", "").split()
+            jobs.append([nvcc, *ARCH, *FLAGS, *extra, *inc, "-c", src, "-o", obj])
     logs = []
 
     def run(cmd):

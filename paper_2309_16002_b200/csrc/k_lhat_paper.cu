@@ -20,6 +20,13 @@
 
 #include "launch.cuh"
 
+#ifndef LP_ABL_NOX2
+#define LP_ABL_NOX2 0
+#endif
+#ifndef LP_TRACE
+#define LP_TRACE 0   // cycle trace of CTA 0 (build with -DLP_TRACE=1; scripts/lp_trace.py)
+#endif
+
 namespace rbrp {
 
 namespace lp {
@@ -28,7 +35,7 @@ constexpr int KC = 64;           // columns per chunk
 constexpr int NCW = 4;           // column groups (16 columns each)
 constexpr int NRP = 4;           // row pairs (16 rows each)
 constexpr int NCONS = NCW * NRP; // consumer warps
-constexpr int NTH = (NCONS + 2) * 32;
+constexpr int NTH = (NCONS + 2) * 32;   // consumers + X and Q producer warps
 constexpr int SLOT = R * KC;     // doubles per X slot (4 boxes of 64 rows x 16 columns)
 constexpr int BOX = R * 16;      // doubles per box
 constexpr int PACK_ROWS = 64;    // rows of the packed Q_b buffer (k_pack_q)
@@ -39,6 +46,11 @@ __device__ __forceinline__ void lp_dmma(double2& d, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
       : "+d"(d.x), "+d"(d.y)
       : "d"(a), "d"(b));
+}
+__device__ __forceinline__ void lp_dmma_v(double2& d, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d.x), "+d"(d.y)
+               : "d"(a), "d"(b));
 }
 __device__ __forceinline__ uint32_t lp_su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void lp_init(uint64_t* b, int count) {
@@ -60,6 +72,24 @@ __device__ __forceinline__ void lp_wait(uint64_t* b, uint32_t parity) {
       "}\n" ::"r"(lp_su32(b)),
       "r"(parity)
       : "memory");
+}
+__device__ __forceinline__ double2 lp_lds2s(uint32_t a) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void lp_waits(uint32_t b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "W_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra W_%=;\n"
+      "}\n" ::"r"(b),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void lp_arrives(uint32_t b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(b) : "memory");
 }
 __device__ __forceinline__ double2 lp_lds2(const double* p) {
   double2 v;
@@ -110,7 +140,8 @@ __global__ void __launch_bounds__(lp::NTH, 1)
     k_lhat_paper(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap xmap0,
                  int lazy, const double* __restrict__ Qp,
                  double* __restrict__ L, int64_t ldl, int64_t n, int d, int nc, int NS, int NQ,
-                 double* __restrict__ dvec, DevState* st, double* __restrict__ Xr, int64_t ldx, int resid) {
+                 double* __restrict__ dvec, DevState* st, double* __restrict__ Xr, int64_t ldx, int resid,
+                 long long* __restrict__ tr) {
   using Cf = LpCfg<BPB>;
   constexpr int NT = Cf::NT;
   using namespace lp;
@@ -134,6 +165,10 @@ __global__ void __launch_bounds__(lp::NTH, 1)
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int64_t ntiles = (n + R - 1) / R;
   const int T = ntiles > blockIdx.x ? (int)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+  if (T == 0) {
+    proj_end_stamp(st);
+    return;
+  }
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
       lp_init(&xfull[s], 1);
@@ -150,24 +185,30 @@ __global__ void __launch_bounds__(lp::NTH, 1)
   const int npass = resid ? 2 : 1;   // residual form: L-hat pass, then update pass per tile
   const int steps = T * nc * npass;
 
-  if (T == 0) {
-  } else if (w == NCONS) {
-    // X producer.  Residual form: the L-hat pass loads a tile with an L2 evict_last
-    // policy, the update pass (same addresses, shortly after) with evict_first, so the
-    // second read is served by L2 and HBM sees one read of X_res.
-    // lazy X_res copy: block 1 reads the input X (xmap0); the update pass writes X_res
-    const CUtensorMap* mp = (lazy && st->t == 1) ? &xmap0 : &xmap;
-    if (lane == 0) {
+  if (w >= NCONS) {
+    if (w == NCONS && lane == 0) {
+      // X producer.  Residual form: the L-hat pass loads a tile with an L2 evict_last
+      // policy, the update pass (same addresses, shortly after) with evict_first, so the
+      // second read is served by L2 and HBM sees one read of X_res.
+      // Lazy X_res copy: block 1 reads the input X (xmap0); the update pass writes X_res.
+      const CUtensorMap* mp = (lazy && st->t == 1) ? &xmap0 : &xmap;
       uint64_t pol_keep, pol_drop;
       asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol_keep));
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol_drop));
       LpRing xr;
       for (int s = 0; s < steps; ++s) {
         if (s >= NS) lp_wait(&xempty[xr.i], xr.ph ^ 1);
-        lp_expect(&xfull[xr.i], SLOT * 8);   // out-of-bounds rows / columns are zero-filled
-        double* dst = xs + (size_t)xr.i * SLOT;
         const int y = (int)row0_of(s / (nc * npass)), c = s % nc;
         const bool second = resid && ((s / nc) & 1);
+#if LP_ABL_NOX2   // timing ablation only (wrong results): the update pass reuses stale slots
+        if (second) {
+          lp_arrive(&xfull[xr.i]);
+          xr.next(NS);
+          continue;
+        }
+#endif
+        lp_expect(&xfull[xr.i], SLOT * 8);   // out-of-bounds rows / columns are zero-filled
+        double* dst = xs + (size_t)xr.i * SLOT;
         const uint64_t pol = resid ? (second ? pol_drop : pol_keep) : pol_drop;
 #pragma unroll
         for (int b = 0; b < 4; ++b)
@@ -178,29 +219,56 @@ __global__ void __launch_bounds__(lp::NTH, 1)
               : "memory");
         xr.next(NS);
       }
-    }
-    __syncwarp();
-  } else if (w == NCONS + 1) {
-    // Q producer (the packed Q_b chunk c is the same for every tile)
-    if (lane == 0) {
+    } else if (w == NCONS + 1 && lane == 0) {
+      // Q producer: packed Q_b chunk c (image 2, row pairs, for the update pass)
       LpRing qr;
       for (int s = 0; s < steps; ++s) {
         if (s >= NQ) lp_wait(&qempty[qr.i], qr.ph ^ 1);
         lp_expect(&qfull[qr.i], (uint32_t)(Cf::QSTAGE * 8));
+        const int in = s % (nc * npass);
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
                 lp_su32(qs + (size_t)qr.i * Cf::QSTAGE)),
-            "l"(Qp + (size_t)(s % nc) * PACK_ROWS * KC), "r"((uint32_t)(Cf::QSTAGE * 8)),
-            "r"(lp_su32(&qfull[qr.i]))
+            "l"(Qp + (in >= nc ? (size_t)nc * PACK_ROWS * KC : 0) + (size_t)(in % nc) * PACK_ROWS * KC),
+            "r"((uint32_t)(Cf::QSTAGE * 8)), "r"(lp_su32(&qfull[qr.i]))
             : "memory");
         qr.next(NQ);
       }
     }
     __syncwarp();
   } else {
+    // operands of the step consumed (they fed issued MMAs): release both buffers
+    // 32-bit shared addresses, computed once
+    const uint32_t xs_s = lp_su32(xs), qs_s = lp_su32(qs);
+    const uint32_t xf_s = lp_su32(xfull), xe_s = lp_su32(xempty), qf_s = lp_su32(qfull), qe_s = lp_su32(qempty);
+    auto release = [&](int xi, int qi) {
+      __syncwarp();
+      if (lane == 0) {
+        lp_arrives(xe_s + 8 * xi);
+        lp_arrives(qe_s + 8 * qi);
+      }
+    };
     // consumers: warp = (row pair rp, column group cw)
     const int rp = w >> 2, cw = w & 3;
     const int g = lane >> 2, q = lane & 3;
+    // optional cycle trace of CTA 0 (RBRP_LP_TRACE=1; profiling only): per warp and tile
+    // 8 events, then per warp and chunk step the time its operands were ready
+#if LP_TRACE
+    int sidx = 0;
+    long long* trw = (tr && blockIdx.x == 0 && lane == 0) ? tr + w * 64 : nullptr;
+    long long* trs = (tr && blockIdx.x == 0 && lane == 0) ? tr + 1024 + w * 256 : nullptr;
+#define LP_T(e)                                                   \
+  do {                                                            \
+    if (trw && p < 8) trw[p * 8 + (e)] = clock64();               \
+  } while (0)
+#define LP_TS()                                                   \
+  do {                                                            \
+    if (trs && sidx < 256) trs[sidx++] = clock64();               \
+  } while (0)
+#else
+#define LP_T(e)
+#define LP_TS()
+#endif
     const int pg = (g >> 1) + 4 * (g & 1);   // tile row of MMA row g (bank-conflict-free)
     int xo[2][2];                            // [row group][8-column half]
 #pragma unroll
@@ -210,38 +278,37 @@ __global__ void __launch_bounds__(lp::NTH, 1)
     double2 acc[2][NT];
     LpRing qr, xr;
     for (int p = 0; p < T; ++p) {
+      LP_T(0);
 #pragma unroll
       for (int r = 0; r < 2; ++r)
 #pragma unroll
         for (int t = 0; t < NT; ++t) acc[r][t] = make_double2(0.0, 0.0);
       for (int c = 0; c < nc; ++c) {
-        lp_wait(&qfull[qr.i], qr.ph);
-        lp_wait(&xfull[xr.i], xr.ph);
-        const double* xsl = xs + (size_t)xr.i * SLOT;
-        const double* Qs = qs + (size_t)qr.i * Cf::QSTAGE;
+        lp_waits(qf_s + 8 * qr.i, qr.ph);
+        lp_waits(xf_s + 8 * xr.i, xr.ph);
+        LP_TS();
+        const uint32_t xsl = xs_s + xr.i * (SLOT * 8);
+        const uint32_t Qs = qs_s + qr.i * (Cf::QSTAGE * 8);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const double2 a0 = lp_lds2(xsl + xo[0][h]);
-          const double2 a1 = lp_lds2(xsl + xo[1][h]);
+          const double2 a0 = lp_lds2s(xsl + 8 * xo[0][h]);
+          const double2 a1 = lp_lds2s(xsl + 8 * xo[1][h]);
 #pragma unroll
           for (int t = 0; t < NT; ++t) {
             const int j = 8 * t + g;
-            const double2 b = lp_lds2(Qs + j * KC + lp_qswz(j, 16 * cw + 8 * h + 2 * q));
+            const double2 b = lp_lds2s(Qs + 8 * (j * KC + lp_qswz(j, 16 * cw + 8 * h + 2 * q)));
             lp_dmma(acc[0][t], a0.x, b.x);
             lp_dmma(acc[1][t], a1.x, b.x);
             lp_dmma(acc[0][t], a0.y, b.y);
             lp_dmma(acc[1][t], a1.y, b.y);
           }
         }
-        __syncwarp();
-        if (lane == 0) {   // operands consumed (they fed the MMAs): release both buffers
-          lp_arrive(&xempty[xr.i]);
-          lp_arrive(&qempty[qr.i]);
-        }
+        release(xr.i, qr.i);
         xr.next(NS);
         qr.next(NQ);
       }
       // tile end: P = (c0 + c2) + (c1 + c3) per row pair, in registers of the cw = 0 warp
+      LP_T(1);
       double* sl = scr + (size_t)rp * 2 * Cf::ACC * 32;
 #define LP_S(slot, r, t, hh) sl[((slot) * Cf::ACC + ((r) * NT + (t)) * 2 + (hh)) * 32 + lane]
       if (cw >= 2) {
@@ -254,6 +321,7 @@ __global__ void __launch_bounds__(lp::NTH, 1)
           }
       }
       lp_bar();
+      LP_T(2);
       if (cw < 2) {
 #pragma unroll
         for (int r = 0; r < 2; ++r)
@@ -273,6 +341,7 @@ __global__ void __launch_bounds__(lp::NTH, 1)
           }
       }
       lp_bar();
+      LP_T(3);
       if (cw == 0) {
         const int64_t r0 = row0_of(p) + 16 * rp;
 #pragma unroll
@@ -306,6 +375,7 @@ __global__ void __launch_bounds__(lp::NTH, 1)
         // ----- update pass (residual form, l.16): X(tile) -= L-hat Q_b, chunk by chunk;
         // the chunks come back through L2 (read from HBM by the L-hat pass just before)
         lp_bar();
+        LP_T(4);
         double2 pf[2][NT];   // -P rows of this row pair, accumulator layout (A fragments)
 #pragma unroll
         for (int r = 0; r < 2; ++r)
@@ -313,50 +383,75 @@ __global__ void __launch_bounds__(lp::NTH, 1)
           for (int t = 0; t < NT; ++t) pf[r][t] = make_double2(LP_S(0, r, t, 0), LP_S(0, r, t, 1));
         const int64_t r0 = row0_of(p) + 16 * rp;
         double nr[2] = {0.0, 0.0};
+        // this lane's two rows (MMA rows g of the two 8-row groups) and columns 2q, 2q+1 of
+        // its two 8-column halves; padding rows / columns were zero-filled by TMA, so they
+        // add nothing to the norms
+        const bool v0 = r0 + pg < n, v1 = r0 + 8 + pg < n;
+        double* xp = Xr + (r0 + pg) * ldx + 16 * cw + 2 * q;
+        const int64_t l8 = 8 * ldx;
         for (int c = 0; c < nc; ++c) {
-          lp_wait(&qfull[qr.i], qr.ph);
-          lp_wait(&xfull[xr.i], xr.ph);
-          const double* xsl = xs + (size_t)xr.i * SLOT;
-          const double* Qs = qs + (size_t)qr.i * Cf::QSTAGE;
+          lp_waits(qf_s + 8 * qr.i, qr.ph);
+          lp_waits(xf_s + 8 * xr.i, xr.ph);
+          LP_TS();
+          const uint32_t xsl = xs_s + xr.i * (SLOT * 8);
+          const uint32_t Qs = qs_s + qr.i * (Cf::QSTAGE * 8);
           double2 xv[2][2];
 #pragma unroll
           for (int r = 0; r < 2; ++r)
 #pragma unroll
-            for (int h = 0; h < 2; ++h) xv[r][h] = lp_lds2(xsl + xo[r][h]);
+            for (int h = 0; h < 2; ++h) xv[r][h] = lp_lds2s(xsl + 8 * xo[r][h]);
+          // B fragments from the pair image: (Q(j0, col), Q(j0 + 1, col)), j0 = 8t + 2q, in
+          // one 16-byte load, one t ahead; the four accumulator chains interleaved in issue
+          // order (volatile: ptxas would otherwise run them two at a time)
+          const uint32_t qb = Qs + 16 * (q * KC + ((16 * cw + g) ^ (2 * q)));
+          double2 bb[2], bn[2];
+          bb[0] = lp_lds2s(qb);
+          bb[1] = lp_lds2s(qb + 128);
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-#pragma unroll
-            for (int t = 0; t < NT; ++t) {
-              const int j0 = 8 * t + 2 * q, col = 16 * cw + 8 * h + g;
-              const double b0 = Qs[j0 * KC + lp_qswz(j0, col)];
-              const double b1 = Qs[(j0 + 1) * KC + lp_qswz(j0 + 1, col)];
-              lp_dmma(xv[0][h], pf[0][t].x, b0);
-              lp_dmma(xv[1][h], pf[1][t].x, b0);
-              lp_dmma(xv[0][h], pf[0][t].y, b1);
-              lp_dmma(xv[1][h], pf[1][t].y, b1);
+          for (int t = 0; t < NT; ++t) {
+            if (t + 1 < NT) {
+              bn[0] = lp_lds2s(qb + 16 * 4 * KC * (t + 1));
+              bn[1] = lp_lds2s(qb + 16 * 4 * KC * (t + 1) + 128);
+            }
+            lp_dmma_v(xv[0][0], pf[0][t].x, bb[0].x);
+            lp_dmma_v(xv[1][0], pf[1][t].x, bb[0].x);
+            lp_dmma_v(xv[0][1], pf[0][t].x, bb[1].x);
+            lp_dmma_v(xv[1][1], pf[1][t].x, bb[1].x);
+            lp_dmma_v(xv[0][0], pf[0][t].y, bb[0].y);
+            lp_dmma_v(xv[1][0], pf[1][t].y, bb[0].y);
+            lp_dmma_v(xv[0][1], pf[0][t].y, bb[1].y);
+            lp_dmma_v(xv[1][1], pf[1][t].y, bb[1].y);
+            if (t + 1 < NT) {
+              bb[0] = bn[0];
+              bb[1] = bn[1];
             }
           }
-          __syncwarp();
-          if (lane == 0) {
-            lp_arrive(&xempty[xr.i]);
-            lp_arrive(&qempty[qr.i]);
-          }
+          release(xr.i, qr.i);
           xr.next(NS);
           qr.next(NQ);
-#pragma unroll
-          for (int r = 0; r < 2; ++r) {
-            const int64_t row = r0 + 8 * r + pg;
-            if (row >= n) continue;
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int col = c * KC + 16 * cw + 8 * h + 2 * q;
-              if (col < d) {
-                __stcs(reinterpret_cast<double2*>(Xr + row * ldx + col), xv[r][h]);
-                nr[r] += xv[r][h].x * xv[r][h].x + xv[r][h].y * xv[r][h].y;
-              }
+          double* xc = xp + c * KC;
+          if (c * KC + KC <= d) {
+            if (v0) {
+              __stcs(reinterpret_cast<double2*>(xc), xv[0][0]);
+              __stcs(reinterpret_cast<double2*>(xc + 8), xv[0][1]);
             }
+            if (v1) {
+              __stcs(reinterpret_cast<double2*>(xc + l8), xv[1][0]);
+              __stcs(reinterpret_cast<double2*>(xc + l8 + 8), xv[1][1]);
+            }
+          } else {   // ragged last chunk (d even: a column pair is in or out as a whole)
+            const int col = c * KC + 16 * cw + 2 * q;
+            if (v0 && col < d) __stcs(reinterpret_cast<double2*>(xc), xv[0][0]);
+            if (v0 && col + 8 < d) __stcs(reinterpret_cast<double2*>(xc + 8), xv[0][1]);
+            if (v1 && col < d) __stcs(reinterpret_cast<double2*>(xc + l8), xv[1][0]);
+            if (v1 && col + 8 < d) __stcs(reinterpret_cast<double2*>(xc + l8 + 8), xv[1][1]);
           }
+#pragma unroll
+          for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) nr[r] += xv[r][h].x * xv[r][h].x + xv[r][h].y * xv[r][h].y;
         }
+        LP_T(5);
         // d(i) = ||x_res,i||^2: q lanes, then the 4 column groups in order
         double* nb = nrm + (size_t)((p & 1) * NRP + rp) * NCW * 16;
 #pragma unroll
@@ -367,6 +462,7 @@ __global__ void __launch_bounds__(lp::NTH, 1)
           if (q == 0) nb[cw * 16 + 8 * r + pg] = v;
         }
         lp_bar();
+        LP_T(6);
         if (cw == 0 && lane < 16) {
           const double v = (nb[lane] + nb[16 + lane]) + (nb[32 + lane] + nb[48 + lane]);
           const int64_t row = r0 + lane;
@@ -378,7 +474,10 @@ __global__ void __launch_bounds__(lp::NTH, 1)
       // ring keeps every warp within NQ steps of the others, so this barrier is only
       // needed when a tile has no more than NQ chunks
       if (nc <= NQ + 1) lp_bar();
+      LP_T(7);
     }
+#undef LP_T
+#undef LP_TS
   }
   proj_end_stamp(st);
 }
@@ -395,6 +494,23 @@ static PFN_cuTensorMapEncodeTiled_v12000 lp_encode() {
       fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
   }
   return fn;
+}
+
+static long long* g_lp_trace = nullptr;
+static long long* lp_trace_buf() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("RBRP_LP_TRACE");
+    on = e && e[0] == '1';
+    if (on && cudaMalloc(&g_lp_trace, 5120 * sizeof(long long)) != cudaSuccess) g_lp_trace = nullptr;
+    if (g_lp_trace) cudaMemset(g_lp_trace, 0, 5120 * sizeof(long long));
+  }
+  return g_lp_trace;
+}
+extern "C" int rbrp_debug_lp_trace(long long* host, int count) {
+  if (!g_lp_trace) return -1;
+  if (count > 5120) count = 5120;
+  return cudaMemcpy(host, g_lp_trace, count * sizeof(long long), cudaMemcpyDeviceToHost) == cudaSuccess ? count : -1;
 }
 
 static int lp_sms() {
@@ -426,8 +542,14 @@ static cudaError_t go_lp(const CUtensorMap& map, const CUtensorMap& map0, int la
   const size_t smem = Cf::smem(ns, nq);
   cudaFuncSetAttribute(k_lhat_paper<BPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int nc = (int)((d + lp::KC - 1) / lp::KC);
+  long long* tr = nullptr;
+  static int traced = 0;
+  if (BPB == 32 && lp_trace_buf() && !traced) {   // first bucket-32 launch only
+    tr = lp_trace_buf();
+    traced = 1;
+  }
   k_lhat_paper<BPB><<<lp_sms(), lp::NTH, smem, s>>>(map, map0, lazy, Qp, L, ldl, n, (int)d, nc, ns, nq, dvec, st,
-                                                     Xr, ldx, resid);
+                                                     Xr, ldx, resid, tr);
   return cudaGetLastError();
 }
 

@@ -144,6 +144,11 @@ __global__ void k_pack_q(const double* __restrict__ Qt, int64_t d, double* __res
   const int64_t gc = (int64_t)c * fz::KC + col;
   const double v = (j < bp && gc < d) ? Qt[(int64_t)j * d + gc] : 0.0;
   Qp[((int64_t)c * fz::PACK_ROWS + j) * fz::KC + qswz(j, col)] = v;
+  // second image (update pass of k_lhat_paper): rows in pairs, (Q(2p, col), Q(2p+1, col))
+  // adjacent, 16-byte unit of pair p and column col at p * KC + (col ^ 2 (p & 3))
+  const int pr = j >> 1;
+  double* Q2 = Qp + (int64_t)gridDim.x * fz::PACK_ROWS * fz::KC + (int64_t)c * fz::PACK_ROWS * fz::KC;
+  Q2[(pr * fz::KC + (col ^ (2 * (pr & 3)))) * 2 + (j & 1)] = v;
 }
 
 template <int BPB>
@@ -622,7 +627,7 @@ extern "C" int rbrp_debug_fz_trace(long long* host, int count) {
 
 static int fz_nc(int64_t d) { return (int)((d + fz::KC - 1) / fz::KC); }
 
-size_t fused_pack_bytes(int64_t d) { return (size_t)fz_nc(d) * fz::PACK_ROWS * fz::KC * 8; }
+size_t fused_pack_bytes(int64_t d) { return 2 * (size_t)fz_nc(d) * fz::PACK_ROWS * fz::KC * 8; }   // two images
 
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
