@@ -125,8 +125,8 @@ __device__ int cta_pivchol(double* A, int lda, int nb, int mode, const int32_t* 
 // so that at step i with pivot p:  R(i, l) = A(p, l) / sqrt(A(p,p)) by the owners of row
 // p, T(j, i) = -acc(j, p) / R(i, p) (j < i) by the owners of column p, then the rank-1
 // update A -= R(i,.)^T R(i,.) and acc(j, .) += T(j, i) R(i, .).  Every warp finds the
-// pivot itself from the shared Schur diagonal (identical, deterministic), so a step costs
-// two barriers.  Pivot / mass / cut rules as cta_pivchol.  R: [step][orig] (ld), T:
+// pivot itself from its register copy of the Schur diagonal (identical, deterministic),
+// so a step costs one barrier.  Pivot / mass / cut rules as cta_pivchol.  R: [step][orig] (ld), T:
 // [step][step] (ldt).
 template <int EPT>
 __device__ int cta_chol_inv(const double* __restrict__ Gg, int nb, int mode, const int32_t* forced,
@@ -153,6 +153,10 @@ __device__ int cta_chol_inv(const double* __restrict__ Gg, int nb, int mode, con
   for (int e = tid; e < nb * ldt; e += blockDim.x) Tm[e] = 0.0;
   if (tid == 0) *rank_def = 0;
   __syncthreads();
+  // the Schur-complement diagonal, in registers of every warp (entries lane, lane + 32):
+  // updated redundantly with the same fma as the matrix entry it mirrors, so the pivot
+  // search needs no barrier after the update -- one __syncthreads per step
+  double dg0 = lane < nb ? dg[lane] : 0.0, dg1 = lane + 32 < nb ? dg[lane + 32] : 0.0;
   unsigned long long chosen = 0ull;   // identical in every thread
   double thr = 0.0;
   int kept = nb;
@@ -164,7 +168,7 @@ __device__ int cta_chol_inv(const double* __restrict__ Gg, int nb, int mode, con
     for (int m = 0; m < 2; ++m) {
       const int l = lane + 32 * m;
       if (l < nb && !((chosen >> l) & 1ull)) {
-        const double x = dg[l];
+        const double x = m ? dg1 : dg0;
         ms += fmax(x, 0.0);
         if (x > best) { best = x; bl = l; }
       }
@@ -182,7 +186,8 @@ __device__ int cta_chol_inv(const double* __restrict__ Gg, int nb, int mode, con
     int p = bl;
     if (mode == 2) p = i;
     if (mode == 1 && forced) p = forced[i];
-    const double dp = dg[p];
+    const double dq0 = __shfl_sync(0xffffffffu, dg0, p & 31), dq1 = __shfl_sync(0xffffffffu, dg1, p & 31);
+    const double dp = p < 32 ? dq0 : dq1;
     if (!cut && !(dp > 0.0)) cut = 2;                               // non-positive pivot
     if (tid == 0 && mode == 1) mass[i] = ms;
     if (cut) {
@@ -204,17 +209,23 @@ __device__ int cta_chol_inv(const double* __restrict__ Gg, int nb, int mode, con
       if (c == p && er[k] < i) Tm[er[k] * ldt + i] = tv;
     }
     chosen |= 1ull << p;
-    __syncthreads();
+    __syncthreads();   // row i of R and column i of T complete; step i+1 writes row / column i+1
 #pragma unroll
     for (int k = 0; k < EPT; ++k) {
       const int r = er[k], c = ec[k];
       if (r < 0) continue;
       const double ric = R[i * ld + c];
       a[k] = fma(-R[i * ld + r], ric, a[k]);
-      if (r == c) dg[r] = a[k];
       if (r <= i) ta[k] = fma(Tm[r * ldt + i], ric, ta[k]);
     }
-    __syncthreads();
+    if (lane < nb) {
+      const double rl = R[i * ld + lane];
+      dg0 = fma(-rl, rl, dg0);
+    }
+    if (lane + 32 < nb) {
+      const double rl = R[i * ld + lane + 32];
+      dg1 = fma(-rl, rl, dg1);
+    }
   }
   __syncthreads();
   return kept;
@@ -248,30 +259,42 @@ __device__ void sm_upper_mul(const double* A, const double* B, double* C, int n,
 }
 
 // CholQR2 second pass for G2 = I + E with small E: R2 = I + U, U the fixed point of
-// U = Phi(E - U^T U) (two steps from Phi(E): error O(|E|^4)), T2 = R2^{-1} =
-// I - U + U^2 - U^3 (error O(|U|^4)).  Parallel; used when max|E| < 1e-5, otherwise
-// the caller runs the exact Cholesky.  E (destroyed), R, Tm, W: n x n, stride ld; R
+// U = Phi(E - U^T U) (iterated from Phi(E)), T2 = R2^{-1} = I - U + U^2 - ...; the number
+// of fixed-point steps and series terms is the smallest that leaves an error below the
+// rounding of R2 and T2 (usually none and one: |E| ~ 1e-14 after the first pass).
+// Parallel; used when n max|E| < 1e-4, otherwise the caller runs the exact Cholesky.  E (destroyed), R, Tm, W: n x n, stride ld; R
 // doubles as scratch.  Writes R2 (upper) into R and T2 into Tm.
-__device__ void cholqr2_perturb(double* E, double* R, double* Tm, double* W, int n, int ld) {
+__device__ void cholqr2_perturb(double* E, double* R, double* Tm, double* W, int n, int ld, double eta) {
+  // eta = n max|E| >= ||E||_2.  Fixed-point error after s steps ~ 2^s eta^(s+2); series
+  // truncation after U^m ~ eta^(m+1): both taken below 1e-17 (rounding level of R2, T2)
+  const double e2 = eta * eta, e3 = e2 * eta, e4 = e3 * eta;
+  const int steps = e2 < 1e-17 ? 0 : (2 * e3 < 1e-17 ? 1 : (4 * e4 < 1e-17 ? 2 : 3));
+  const int terms = e2 < 1e-17 ? 1 : (e3 < 1e-17 ? 2 : (e4 < 1e-17 ? 3 : 4));
   sm_upper_phi(E, W, n, ld);                  // U0
   __syncthreads();
-  sm_e_minus_utu(E, W, R, n, ld);
-  __syncthreads();
-  sm_upper_phi(R, W, n, ld);                  // U1
-  __syncthreads();
-  sm_e_minus_utu(E, W, R, n, ld);
-  __syncthreads();
-  sm_upper_phi(R, W, n, ld);                  // U2 = U
-  __syncthreads();
-  sm_upper_mul(W, W, R, n, ld);               // U^2 (in R)
-  __syncthreads();
-  sm_upper_mul(R, W, E, n, ld);               // U^3 (in E)
-  __syncthreads();
+  for (int it = 0; it < steps; ++it) {
+    sm_e_minus_utu(E, W, R, n, ld);
+    __syncthreads();
+    sm_upper_phi(R, W, n, ld);                // U_{it+1}
+    __syncthreads();
+  }
+  // T2 = I - U + U^2 - ... (-U)^terms, Horner: P <- I - U P
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
     const int i = e / n, j = e - (e / n) * n;
-    const double u = W[i * ld + j], u2 = R[i * ld + j], u3 = E[i * ld + j], id = (i == j ? 1.0 : 0.0);
-    Tm[i * ld + j] = id - u + u2 - u3;
-    R[i * ld + j] = id + u;
+    Tm[i * ld + j] = (i == j ? 1.0 : 0.0) - W[i * ld + j];
+  }
+  for (int t = 2; t <= terms; ++t) {
+    __syncthreads();
+    sm_upper_mul(W, Tm, E, n, ld);            // U P (E is free now)
+    __syncthreads();
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+      const int i = e / n, j = e - (e / n) * n;
+      Tm[i * ld + j] = (i == j ? 1.0 : 0.0) - E[i * ld + j];
+    }
+  }
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int i = e / n, j = e - (e / n) * n;
+    R[i * ld + j] = (i == j ? 1.0 : 0.0) + W[i * ld + j];
   }
   __syncthreads();
 }
@@ -493,8 +516,8 @@ __global__ void __launch_bounds__(kFiltThreads, 1) k_filter_coop(FilterArgs F) {
     if ((tid & 31) == 0) atomicMax((unsigned long long*)&s_emax, (unsigned long long)__double_as_longlong(em));
     __syncthreads();
   }
-  if (small && s_emax < 1e-5) {
-    cholqr2_perturb(Gs, Rs, Ts, Vs, bp, ldr);
+  if (small && bp * s_emax < 1e-4) {
+    cholqr2_perturb(Gs, Rs, Ts, Vs, bp, ldr, bp * s_emax);
     if (tid == 0) s_kept = bp;
   } else {
     int rd2, kept;
