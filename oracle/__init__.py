@@ -21,11 +21,15 @@ Modules
   rbrp     Alg. 2 (RBRP; residual and paper forms, BRP / RBGP variants),
            Alg. 1 (SRP), Householder CPQR, the robust filter, Alg. 3 (W).
   referee  errskel (Eq. 1.2), errid, eta_r (Eq. 1.3), brute-force best subset.
+  sketch   SkLUPP-OSID: Gaussian embedding (reading R24), Y = X Omega,
+           LUPP on Y (reading R25), OSID W = Y Y_S^+ (Alg. 4 / Eq. 5.3).
 
 Pins (tests/test_oracle_*.py) tie every function to something other than
 itself: published Philox known-answer vectors, closed forms of Example 2.3
 and of the Gaussian-exp spectrum, LAPACK geqp3 pivot order, brute-force best
-subsets, exact rank recovery, lstsq for W, the b=1 reduction to SRP.
+subsets, exact rank recovery, lstsq for W, the b=1 reduction to SRP; for the sketch
+module LAPACK getrf pivots, LU reconstruction, least-squares W under an orthogonal
+embedding, Eq. 5.2 at l = k and normal-sample statistics.
 Parity unpinned: the RBRP skeleton-complexity conjecture (Conj. 4.3)
 and time-to-ID (Table 3) -- neither is a checkable value.
 """
