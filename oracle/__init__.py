@@ -21,8 +21,8 @@ Modules
   rbrp     Alg. 2 (RBRP; residual and paper forms, BRP / RBGP variants),
            Alg. 1 (SRP), Householder CPQR, the robust filter, Alg. 3 (W).
   referee  errskel (Eq. 1.2), errid, eta_r (Eq. 1.3), brute-force best subset.
-  sketch   SkLUPP-OSID: Gaussian embedding (reading R24), Y = X Omega,
-           LUPP on Y (reading R25), OSID W = Y Y_S^+ (Alg. 4 / Eq. 5.3).
+  sketch   SkLUPP-OSID: Gaussian embedding (reading R25), Y = X Omega,
+           LUPP on Y (reading R26), OSID W = Y Y_S^+ (Alg. 4 / Eq. 5.3).
 
 Pins (tests/test_oracle_*.py) tie every function to something other than
 itself: published Philox known-answer vectors, closed forms of Example 2.3

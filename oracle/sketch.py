@@ -6,23 +6,23 @@ TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).  Plain NumPy, fp64, no blocki
 
   gaussian_embedding(d, l, seed)  Omega (d x l), iid N(0, 1/l) (Prop. 5.3, P:643;
                                   Remark 3.2), drawn with Philox4x32-10 and the
-                                  Box-Muller transform (reading R24).
+                                  Box-Muller transform (reading R25).
   sketch(X, Omega)                Y = X Omega (P:356, "the sketched sample matrix";
                                   Alg. 4 l.1).
   lupp(Y, k)                      the first k pivot rows of LU with partial pivoting on Y
-                                  ("LUPP [GVL 3.4] ... on Y"); reading R25.
+                                  ("LUPP [GVL 3.4] ... on Y"); reading R26.
   osid_w(Y, S)                    W(S,:) = I_k, W(rest,:) = (Y(rest,:) Q) R^{-T} with
                                   Y_S^T = Q R (Alg. 4 l.2-4; Eq. 5.3).
   sketchy_id(X, k, Omega)         S = lupp(X Omega, k), W = osid_w(X Omega, S).
 
-Reading R24 (the paper names no generator): entry (j, i) of Omega^T (row j < l, column
+Reading R25 (the paper names no generator): entry (j, i) of Omega^T (row j < l, column
 i < d; e = j d + i) is normal number e % 2 of Philox block q = e // 2 with counter
 (q_lo, q_hi, 0, 0x4F4D4547) and key (seed_lo, seed_hi); with u1 = U53(w0, w1),
 u2 = U53(w2, w3): r = sqrt(-2 ln(1 - u1)), z0 = r cos(2 pi u2), z1 = r sin(2 pi u2),
 entry = z / sqrt(l).  The fourth counter word keeps these blocks apart from the
 sampler's (j, t, 0, 0).
 
-Reading R25 (LUPP conventions the paper leaves to [GVL 3.4]): rows are not swapped;
+Reading R26 (LUPP conventions the paper leaves to [GVL 3.4]): rows are not swapped;
 step m takes the active column c (starting at 0) and pivots on the active row of
 largest |A(i, c)|, ties to the lowest row index; an exactly zero active column is
 skipped (c advances, no pivot); the Schur update of every other active row is
@@ -40,11 +40,11 @@ import scipy.linalg
 
 from . import philox
 
-OMEGA_TAG = 0x4F4D4547   # counter word 3 of the embedding's Philox blocks (reading R24)
+OMEGA_TAG = 0x4F4D4547   # counter word 3 of the embedding's Philox blocks (reading R25)
 
 
 def gaussian_embedding(d: int, l: int, seed: int) -> np.ndarray:
-    """Omega (d x l) with iid N(0, 1/l) entries, by reading R24.  Pure Python
+    """Omega (d x l) with iid N(0, 1/l) entries, by reading R25.  Pure Python
     per Philox block: for small d * l only."""
     key = philox.seed_key(seed)
     total = d * l
@@ -75,7 +75,7 @@ class LUPP:
 
 
 def lupp(Y, k: int) -> LUPP:
-    """Partial-pivoting LU on Y (n x l), first k steps, reading R25."""
+    """Partial-pivoting LU on Y (n x l), first k steps, reading R26."""
     A = np.array(Y, dtype=np.float64, copy=True)
     n, l = A.shape
     active = np.ones(n, dtype=bool)

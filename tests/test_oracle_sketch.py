@@ -1,5 +1,5 @@
 """Pins for the sketchy-pivoting oracle: LUPP on the sketch,
-OSID (Alg. 4 / Eq. 5.3) and the Gaussian embedding (reading R24).
+OSID (Alg. 4 / Eq. 5.3) and the Gaussian embedding (reading R25).
 
 Each check ties oracle/sketch.py to something other than itself: LAPACK getrf's pivot
 sequence, permutation and diagonally dominant inputs, LU reconstruction, least-squares
