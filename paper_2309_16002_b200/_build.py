@@ -62,7 +62,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
     os.makedirs(OBJDIR, exist_ok=True)
     nvcc = _nvcc()
     inc = ["-I", _nccl_include(), "-I", os.path.join(ROOT, "include")]
-    headers = glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(ROOT, "include", "rbrp.h")]
+    headers = glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(ROOT, "include", "*.h"))
     jobs = []
     objs = []
     for src in sources():

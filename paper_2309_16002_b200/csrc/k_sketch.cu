@@ -1,0 +1,665 @@
+// k_sketch.cu — sketchy pivoting with LUPP and the oversampled sketchy interpolation
+// matrix, SkLUPP-OSID (section 3.2; Alg. 4, P:611-622;
+// Eq. 5.3).  fp64.
+//
+//   k_embedding  Omega^T (l x d), iid N(0, 1/l) by Philox4x32-10 + Box-Muller
+//                (reading R25).
+//   Y = X Omega  the FP64 tensor-path GEMM of k_project_mma.cu (gemm_nt_mma).
+//   k_lupp       partial-pivoting LU on Y, first k pivots (reading R26): one
+//                cooperative kernel, rows split over the CTAs (one per SM), columns in
+//                panels of PW held in shared memory.  Per step: every CTA proposes its
+//                best active row (|A(i, c)|, ties to the lower row) with its panel values,
+//                one grid barrier, every CTA picks the same winner and updates its rows.
+//                At a panel start the earlier pivots' U rows for the panel columns are
+//                rebuilt by forward substitution from Y and the stored multipliers, and
+//                each active row applies them in pivot order -- every entry sees exactly
+//                the updates a - l*u (product rounded, then the difference, as the
+//                unblocked loop) in the same order, so pivots and multipliers equal the
+//                textbook loop's bit for bit.
+//   OSID         Z = Y(S,:) (k x l); CholQR2 of Z^T: G1 = Z Z^T = C1 C1^T, P1 = C1^{-1} Z,
+//                G2 = P1 P1^T = C2 C2^T, Q^T = C2^{-1} P1; M^T = (R2 R1)^{-1} Q^T with
+//                R = C2^T C1^T, so W = Y M = (Y Q) R^{-T} (Alg. 4 l.4) = Y Y_S^+; then
+//                W(S,:) = I_k (l.3).  Small k x k / k x l steps are CUDA-core kernels;
+//                W = Y M is the FP64 tensor-path GEMM again.
+#include <cooperative_groups.h>
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+
+#include "../../include/rbrp_sketch.h"
+#include "launch.cuh"
+#include "philox.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace rbrp {
+namespace sk {
+constexpr int kThreads = 256;
+constexpr int kSmemMax = 227 * 1024;
+constexpr uint32_t kOmegaTag = 0x4F4D4547u;   // reading R25
+}  // namespace sk
+
+// ------------------------------------------------------------------------------------
+// Gaussian embedding (reading R25)
+// ------------------------------------------------------------------------------------
+__global__ void k_embedding(int64_t d, int64_t l, uint2 key, double* __restrict__ OmT, int64_t ldo) {
+  const int64_t total = d * l, nq = (total + 1) / 2;
+  const double sl = sqrt((double)l);
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 w = philox4x32_10(make_uint4((uint32_t)q, (uint32_t)(q >> 32), 0u, sk::kOmegaTag), key);
+    const double u1 = u53(w);
+    const double u2 = u53(make_uint4(w.z, w.w, 0u, 0u));
+    const double r = sqrt(-2.0 * log(1.0 - u1));
+    const double a = (2.0 * M_PI) * u2;
+    const double z0 = r * cos(a), z1 = r * sin(a);
+    const int64_t e0 = 2 * q;
+    {
+      const int64_t j = e0 / d, i = e0 - j * d;
+      OmT[j * ldo + i] = z0 / sl;
+    }
+    if (e0 + 1 < total) {
+      const int64_t j = (e0 + 1) / d, i = (e0 + 1) - j * d;
+      OmT[j * ldo + i] = z1 / sl;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// LUPP (reading R26)
+// ------------------------------------------------------------------------------------
+struct LuArgs {
+  const double* Y;
+  int64_t n, l, ldy;
+  int k, R;
+  double* Lm;       // n x k multipliers
+  double* cand;     // [2][G][PW + 2]: |v|, row (bits), panel values of each CTA's candidate
+  int64_t* piv;     // k
+  int64_t* pcol;    // k
+  int* out;         // [0] pivots found
+};
+
+__device__ __forceinline__ bool lu_better(double v, long long r, double bv, long long br) {
+  return v > bv || (v == bv && r < br);
+}
+
+template <int PW>
+__global__ void __launch_bounds__(sk::kThreads, 1) k_lupp(LuArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  constexpr int LD = PW + 1, CS = PW + 2, NW = sk::kThreads / 32;
+  extern __shared__ __align__(16) double smd[];
+  const int R = a.R, k = a.k, G = gridDim.x;
+  double* A = smd;                                       // R x LD: own rows, panel columns
+  double* Us = A + (size_t)R * LD;                       // k x PW: U rows of earlier pivots
+  double* Up = Us + (size_t)k * PW;                      // PW: the current pivot row
+  long long* spiv = reinterpret_cast<long long*>(Up + PW);   // k: pivot rows so far
+  unsigned char* act = reinterpret_cast<unsigned char*>(spiv + k);   // R: row still active
+  __shared__ double s_wv[NW];
+  __shared__ long long s_wr[NW];
+  __shared__ int s_wg[NW];
+  __shared__ double s_bv;
+  __shared__ int s_bl, s_win;
+  __shared__ long long s_br;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int64_t r0 = (int64_t)blockIdx.x * R;
+  const int nr = (int)max((int64_t)0, min((int64_t)R, a.n - r0));
+  for (int i = tid; i < R; i += sk::kThreads) act[i] = i < nr ? 1 : 0;
+  __syncthreads();
+  int npiv = 0, par = 0;
+  int64_t c = 0;
+  while (npiv < k && c < a.l) {
+    const int64_t c0 = c;
+    const int pw = (int)min((int64_t)PW, a.l - c0);
+    const int np0 = npiv;
+    // (1) U(m, c0 + j), m < np0: Y(p_m, .) minus the earlier pivots' updates, in order
+    for (int e = tid; e < np0 * pw; e += sk::kThreads) {
+      const int m = e / pw, j = e - m * pw;
+      Us[m * PW + j] = a.Y[spiv[m] * a.ldy + c0 + j];
+    }
+    __syncthreads();
+    for (int mm = 0; mm + 1 < np0; ++mm) {
+      const int cnt = (np0 - 1 - mm) * pw;
+      for (int e = tid; e < cnt; e += sk::kThreads) {
+        const int m = mm + 1 + e / pw, j = e % pw;
+        const double lm = a.Lm[spiv[m] * k + mm];
+        Us[m * PW + j] = __dsub_rn(Us[m * PW + j], __dmul_rn(lm, Us[mm * PW + j]));
+      }
+      __syncthreads();
+    }
+    // (2) own active rows: panel columns of Y, then the earlier pivots' updates in order
+    for (int i = tid; i < nr; i += sk::kThreads) {
+      if (!act[i]) continue;
+      const double* yr = a.Y + (r0 + i) * a.ldy + c0;
+      double* ar = A + (size_t)i * LD;
+      for (int j = 0; j < pw; ++j) ar[j] = yr[j];
+      const double* lr = a.Lm + (r0 + i) * k;
+      for (int m = 0; m < np0; ++m) {
+        const double lm = lr[m];
+        const double* u = Us + m * PW;
+        for (int j = 0; j < pw; ++j) ar[j] = __dsub_rn(ar[j], __dmul_rn(lm, u[j]));
+      }
+    }
+    __syncthreads();
+    // (3) the panel's steps
+    int s = 0;
+    for (; s < pw && npiv < k; ++s) {
+      double bv = -1.0;
+      long long br = LLONG_MAX;
+      int bl = -1;
+      for (int i = tid; i < nr; i += sk::kThreads)
+        if (act[i]) {
+          const double v = fabs(A[(size_t)i * LD + s]);
+          if (v > bv) {   // rows visited in increasing order: ties keep the lower row
+            bv = v;
+            bl = i;
+            br = r0 + i;
+          }
+        }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const long long orr = __shfl_xor_sync(0xffffffffu, br, o);
+        const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+        if (lu_better(ov, orr, bv, br)) {
+          bv = ov;
+          br = orr;
+          bl = ol;
+        }
+      }
+      if (lane == 0) {
+        s_wv[w] = bv;
+        s_wr[w] = br;
+        s_wg[w] = bl;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        double v = s_wv[0];
+        long long r = s_wr[0];
+        int li = s_wg[0];
+        for (int q = 1; q < NW; ++q)
+          if (lu_better(s_wv[q], s_wr[q], v, r)) {
+            v = s_wv[q];
+            r = s_wr[q];
+            li = s_wg[q];
+          }
+        s_bv = v;
+        s_bl = li;
+      }
+      __syncthreads();
+      double* cr = a.cand + ((size_t)par * G + blockIdx.x) * CS;
+      if (tid == 0) {
+        cr[0] = s_bv;
+        cr[1] = __longlong_as_double(s_bl >= 0 ? (long long)(r0 + s_bl) : -1ll);
+      }
+      if (s_bl >= 0)
+        for (int j = tid; j < pw; j += sk::kThreads) cr[2 + j] = A[(size_t)s_bl * LD + j];
+      grid.sync();
+      // the winner, identical in every CTA
+      if (w == 0) {
+        double v = -1.0;
+        long long r = LLONG_MAX;
+        int who = -1;
+        for (int g = lane; g < G; g += 32) {
+          const double* q = a.cand + ((size_t)par * G + g) * CS;
+          const long long qr = __double_as_longlong(q[1]);
+          if (qr >= 0 && lu_better(q[0], qr, v, r)) {
+            v = q[0];
+            r = qr;
+            who = g;
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+          const long long orr = __shfl_xor_sync(0xffffffffu, r, o);
+          const int og = __shfl_xor_sync(0xffffffffu, who, o);
+          if (og >= 0 && (who < 0 || lu_better(ov, orr, v, r))) {
+            v = ov;
+            r = orr;
+            who = og;
+          }
+        }
+        if (lane == 0) {
+          s_bv = v;
+          s_br = r;
+          s_win = who;
+        }
+      }
+      __syncthreads();
+      const int pb = par;
+      par ^= 1;
+      if (s_win < 0) {   // no active row left anywhere
+        c = a.l;
+        break;
+      }
+      if (!(s_bv > 0.0)) continue;   // exactly zero active column: skipped (no pivot)
+      const long long prow = s_br;
+      const int m = npiv++;
+      const double* q = a.cand + ((size_t)pb * G + s_win) * CS;
+      for (int j = tid; j < pw; j += sk::kThreads) Up[j] = q[2 + j];
+      if (tid == 0) {
+        spiv[m] = prow;
+        if (prow >= r0 && prow < r0 + nr) act[prow - r0] = 0;
+        if (blockIdx.x == 0) {
+          a.piv[m] = prow;
+          a.pcol[m] = c0 + s;
+        }
+      }
+      __syncthreads();
+      const double pv = Up[s];
+      for (int i = tid; i < nr; i += sk::kThreads) {
+        if (!act[i]) continue;
+        double* ar = A + (size_t)i * LD;
+        const double lv = ar[s] / pv;
+        a.Lm[(r0 + i) * k + m] = lv;
+        for (int j = s + 1; j < pw; ++j) ar[j] = __dsub_rn(ar[j], __dmul_rn(lv, Up[j]));
+      }
+      __syncthreads();
+    }
+    if (c < a.l) c = c0 + s;
+    grid.sync();   // this panel's multipliers are read by every CTA in (1) of the next
+  }
+  if (blockIdx.x == 0 && tid == 0) a.out[0] = npiv;
+}
+
+static int sk_num_sms() {
+  static int v = 0;
+  if (!v) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    if (v <= 0) v = 148;
+  }
+  return v;
+}
+
+static size_t lupp_smem(int PW, int R, int k) {
+  return (size_t)R * (PW + 1) * 8 + (size_t)k * PW * 8 + PW * 8 + (size_t)k * 8 + R + 64;
+}
+
+// grid and panel width for n rows: one CTA per SM, the widest panel that fits
+static bool lupp_plan(int64_t n, int k, int* G, int* R, int* PW) {
+  const int sms = sk_num_sms();
+  *G = (int)std::min<int64_t>(sms, n);
+  *R = (int)((n + *G - 1) / *G);
+  for (int pw : {32, 16, 8})
+    if (lupp_smem(pw, *R, k) <= (size_t)sk::kSmemMax) {
+      *PW = pw;
+      return true;
+    }
+  return false;
+}
+
+template <int PW>
+static cudaError_t go_lupp(LuArgs a, int G, cudaStream_t s) {
+  const size_t smem = lupp_smem(PW, a.R, a.k);
+  cudaError_t e = cudaFuncSetAttribute(k_lupp<PW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(G);
+  cfg.blockDim = dim3(sk::kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute la[1];
+  la[0].id = cudaLaunchAttributeCooperative;
+  la[0].val.cooperative = 1;
+  cfg.attrs = la;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_lupp<PW>, a);
+}
+
+static cudaError_t launch_lupp(LuArgs a, int G, int PW, cudaStream_t s) {
+  switch (PW) {
+    case 32: return go_lupp<32>(a, G, s);
+    case 16: return go_lupp<16>(a, G, s);
+    default: return go_lupp<8>(a, G, s);
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// OSID helpers (small k x k and k x l steps)
+// ------------------------------------------------------------------------------------
+__global__ void k_gather_rows(const double* __restrict__ Y, int64_t ldy, const int64_t* __restrict__ S, int k,
+                              int64_t lp, double* __restrict__ Z) {
+  const int i = blockIdx.x;
+  if (i >= k) return;
+  const double* y = Y + S[i] * ldy;
+  for (int64_t c = threadIdx.x; c < lp; c += blockDim.x) Z[(int64_t)i * lp + c] = y[c];
+}
+
+// G = Z Z^T (k x k), one output per thread, sequential dot over the l columns
+__global__ void k_gram_rows(const double* __restrict__ Z, int k, int64_t lp, double* __restrict__ G) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= k * k) return;
+  const int i = e / k, j = e - i * k;
+  const double* zi = Z + (int64_t)i * lp;
+  const double* zj = Z + (int64_t)j * lp;
+  double s = 0.0;
+  for (int64_t c = 0; c < lp; ++c) s = fma(zi[c], zj[c], s);
+  G[e] = s;
+}
+
+// G = C C^T (Cholesky, C lower, k <= RBRP_SK_MAX_K) in one CTA; info = 1 if not positive
+// definite
+__global__ void __launch_bounds__(1024) k_chol_small(const double* __restrict__ G, int k, double* __restrict__ C,
+                                                     int* __restrict__ info) {
+  extern __shared__ double cs[];   // k x (k + 1)
+  const int ld = k + 1, tid = threadIdx.x, nt = blockDim.x;
+  for (int e = tid; e < k * k; e += nt) cs[(e / k) * ld + e % k] = G[e];
+  __shared__ int bad;
+  if (tid == 0) bad = 0;
+  __syncthreads();
+  for (int j = 0; j < k; ++j) {
+    if (tid == 0) {
+      const double dj = cs[j * ld + j];
+      if (!(dj > 0.0)) bad = 1;
+      cs[j * ld + j] = sqrt(dj > 0.0 ? dj : 1.0);
+    }
+    __syncthreads();
+    const double djj = cs[j * ld + j];
+    for (int i = j + 1 + tid; i < k; i += nt) cs[i * ld + j] /= djj;
+    __syncthreads();
+    const int m = k - j - 1;
+    for (int e = tid; e < m * m; e += nt) {
+      const int i = j + 1 + e / m, q = j + 1 + e % m;
+      if (q <= i) cs[i * ld + q] = fma(-cs[i * ld + j], cs[q * ld + j], cs[i * ld + q]);
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < k * k; e += nt) {
+    const int i = e / k, j = e % k;
+    C[e] = j <= i ? cs[i * ld + j] : 0.0;
+  }
+  if (tid == 0 && bad) *info = 1;
+}
+
+// B (k x lp, row-major) <- C^{-1} B (trans = 0, forward) or C^{-T} B (trans = 1,
+// backward), C lower (k x k); one thread per column of B
+__global__ void k_trsm_cols(const double* __restrict__ C, int k, double* __restrict__ B, int64_t lp, int trans) {
+  extern __shared__ double ts[];   // k x k
+  for (int e = threadIdx.x; e < k * k; e += blockDim.x) ts[e] = C[e];
+  __syncthreads();
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= lp) return;
+  if (!trans) {
+    for (int i = 0; i < k; ++i) {
+      double s = B[(int64_t)i * lp + c];
+      for (int j = 0; j < i; ++j) s = fma(-ts[i * k + j], B[(int64_t)j * lp + c], s);
+      B[(int64_t)i * lp + c] = s / ts[i * k + i];
+    }
+  } else {
+    for (int i = k - 1; i >= 0; --i) {
+      double s = B[(int64_t)i * lp + c];
+      for (int j = i + 1; j < k; ++j) s = fma(-ts[j * k + i], B[(int64_t)j * lp + c], s);
+      B[(int64_t)i * lp + c] = s / ts[i * k + i];
+    }
+  }
+}
+
+}  // namespace rbrp
+
+using namespace rbrp;
+
+namespace {
+
+size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+int64_t round8(int64_t x) { return (x + 7) & ~int64_t(7); }
+
+struct LuLayout {
+  size_t Lm, cand, piv, pcol, out, total;
+};
+LuLayout lu_layout(int64_t n, int64_t k, int G, bool own_L) {
+  LuLayout L{};
+  size_t o = 0;
+  L.Lm = own_L ? o : SIZE_MAX;
+  if (own_L) o += al256((size_t)n * k * 8);
+  L.cand = o;
+  o += al256((size_t)2 * G * (32 + 2) * 8);
+  L.piv = o;
+  o += al256((size_t)k * 8);
+  L.pcol = o;
+  o += al256((size_t)k * 8);
+  L.out = o;
+  o += 256;
+  L.total = o;
+  return L;
+}
+
+int lupp_check(int64_t n, int64_t l, int64_t ldy, int64_t k) {
+  if (n < 1 || l < 1 || ldy < l || k < 1 || k > n || k > l || k > RBRP_SK_MAX_K) return RBRP_EINVAL;
+  return RBRP_OK;
+}
+
+// run the LUPP kernel; pivots copied to the host (synchronises the stream)
+int run_lupp(const double* Y, int64_t n, int64_t l, int64_t ldy, int64_t k, char* ws, double* Lm,
+             cudaStream_t s, int64_t* piv_h, int64_t* pcol_h, int64_t* npiv_h, int64_t** piv_dev) {
+  int G, R, PW;
+  if (!lupp_plan(n, (int)k, &G, &R, &PW)) return RBRP_ENOTSUP;
+  LuLayout Ly = lu_layout(n, k, G, Lm == nullptr);
+  if (!Lm) Lm = (double*)(ws + Ly.Lm);
+  if (cudaMemsetAsync(Lm, 0, (size_t)n * k * 8, s) != cudaSuccess) return RBRP_ECUDA;
+  LuArgs a;
+  a.Y = Y;
+  a.n = n;
+  a.l = l;
+  a.ldy = ldy;
+  a.k = (int)k;
+  a.R = R;
+  a.Lm = Lm;
+  a.cand = (double*)(ws + Ly.cand);
+  a.piv = (int64_t*)(ws + Ly.piv);
+  a.pcol = (int64_t*)(ws + Ly.pcol);
+  a.out = (int*)(ws + Ly.out);
+  if (launch_lupp(a, G, PW, s) != cudaSuccess) return RBRP_ECUDA;
+  int np = 0;
+  if (cudaMemcpyAsync(&np, a.out, sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess) return RBRP_ECUDA;
+  if (cudaStreamSynchronize(s) != cudaSuccess) return RBRP_ECUDA;
+  *npiv_h = np;
+  if (np > 0 && piv_h && cudaMemcpy(piv_h, a.piv, np * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return RBRP_ECUDA;
+  if (np > 0 && pcol_h && cudaMemcpy(pcol_h, a.pcol, np * 8, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return RBRP_ECUDA;
+  if (piv_dev) *piv_dev = a.piv;
+  return RBRP_OK;
+}
+
+struct SkLayout {
+  size_t OmT, Y, lu, Z, G, C1, C2, info, total;
+  int64_t lp;
+};
+SkLayout sk_layout(int64_t n, int64_t d, int64_t k, int64_t l) {
+  SkLayout L{};
+  L.lp = round8(l);
+  int G = (int)std::min<int64_t>(sk_num_sms(), n);
+  size_t o = 0;
+  L.OmT = o;
+  o += al256((size_t)L.lp * d * 8);
+  L.Y = o;
+  o += al256((size_t)n * L.lp * 8);
+  L.lu = o;
+  o += lu_layout(n, k, G, true).total;
+  L.Z = o;
+  o += al256((size_t)k * L.lp * 8);
+  L.G = o;
+  o += al256((size_t)k * k * 8);
+  L.C1 = o;
+  o += al256((size_t)k * k * 8);
+  L.C2 = o;
+  o += al256((size_t)k * k * 8);
+  L.info = o;
+  o += 256;
+  L.total = o;
+  return L;
+}
+
+int sk_check(int64_t n, int64_t d, int64_t ldx, int64_t k, int64_t l) {
+  if (n < 1 || d < 1 || ldx < d || k < 1 || k > n || k > RBRP_SK_MAX_K || l < k || l > 4 * k || l > d)
+    return RBRP_EINVAL;
+  return RBRP_OK;
+}
+
+struct Ev {
+  cudaEvent_t e[2] = {nullptr, nullptr};
+  bool on = false;
+  void begin(bool p, cudaStream_t s) {
+    on = p;
+    if (!on) return;
+    cudaEventCreate(&e[0]);
+    cudaEventCreate(&e[1]);
+    cudaEventRecord(e[0], s);
+  }
+  float end(cudaStream_t s) {
+    if (!on) return 0.f;
+    float ms = 0.f;
+    cudaEventRecord(e[1], s);
+    cudaEventSynchronize(e[1]);
+    cudaEventElapsedTime(&ms, e[0], e[1]);
+    cudaEventDestroy(e[0]);
+    cudaEventDestroy(e[1]);
+    return ms;
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+int rbrp_gaussian_embedding(int64_t d, int64_t l, uint64_t seed, double* OmegaT, int64_t ldo, void* stream) {
+  if (d < 1 || l < 1 || ldo < d || !OmegaT) return RBRP_EINVAL;
+  const int64_t nq = (d * l + 1) / 2;
+  const int blocks = (int)std::min<int64_t>((nq + 255) / 256, 148 * 16);
+  k_embedding<<<blocks, 256, 0, (cudaStream_t)stream>>>(d, l, make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)),
+                                                         OmegaT, ldo);
+  return cudaGetLastError() == cudaSuccess ? RBRP_OK : RBRP_ECUDA;
+}
+
+int rbrp_lupp_workspace_size(int64_t n, int64_t l, int64_t k, size_t* bytes) {
+  int rc = lupp_check(n, l, l, k);
+  if (rc) return rc;
+  if (!bytes) return RBRP_EINVAL;
+  *bytes = lu_layout(n, k, (int)std::min<int64_t>(sk_num_sms(), n), true).total;
+  return RBRP_OK;
+}
+
+int rbrp_lupp(const double* Y, int64_t n, int64_t l, int64_t ldy, int64_t k, void* workspace, size_t ws_bytes,
+              void* stream, int64_t* piv_out, int64_t* pcol_out, int64_t* npiv_out, double* L_out) {
+  int rc = lupp_check(n, l, ldy, k);
+  if (rc) return rc;
+  if (!Y || !workspace || !piv_out || !npiv_out || ((uintptr_t)workspace % 256)) return RBRP_EINVAL;
+  size_t need = 0;
+  rbrp_lupp_workspace_size(n, l, k, &need);
+  if (ws_bytes < need) return RBRP_ENOMEM;
+  return run_lupp(Y, n, l, ldy, k, (char*)workspace, L_out, (cudaStream_t)stream, piv_out, pcol_out, npiv_out,
+                  nullptr);
+}
+
+int rbrp_sketch_workspace_size(int64_t n, int64_t d, int64_t k, int64_t l, size_t* bytes) {
+  int rc = sk_check(n, d, d, k, l);
+  if (rc) return rc;
+  if (!bytes) return RBRP_EINVAL;
+  *bytes = sk_layout(n, d, k, l).total;
+  return RBRP_OK;
+}
+
+int rbrp_sketch_id(const double* X, int64_t n, int64_t d, int64_t ldx, int64_t k, int64_t l, uint64_t seed,
+                   const double* OmegaT, void* workspace, size_t ws_bytes, void* stream, int64_t* S_out,
+                   double* W_out, rbrp_sketch_report* rep) {
+  int rc = sk_check(n, d, ldx, k, l);
+  if (rc) return rc;
+  if (!X || !workspace || !S_out || ((uintptr_t)workspace % 256)) return RBRP_EINVAL;
+  if (d % 8 || ldx % 2 || ((uintptr_t)X % 16)) return RBRP_ENOTSUP;
+  SkLayout Ly = sk_layout(n, d, k, l);
+  if (ws_bytes < Ly.total) return RBRP_ENOMEM;
+  cudaStream_t s = (cudaStream_t)stream;
+  char* ws = (char*)workspace;
+  const int64_t lp = Ly.lp;
+  double* OmT = (double*)(ws + Ly.OmT);
+  double* Y = (double*)(ws + Ly.Y);
+  double* Z = (double*)(ws + Ly.Z);
+  double* Gm = (double*)(ws + Ly.G);
+  double* C1 = (double*)(ws + Ly.C1);
+  double* C2 = (double*)(ws + Ly.C2);
+  int* info = (int*)(ws + Ly.info);
+  const bool prof = rep && rep->profile;
+  int launches = 0;
+  cudaEvent_t t0, t1;
+  cudaEventCreate(&t0);
+  cudaEventCreate(&t1);
+  cudaEventRecord(t0, s);
+  float ph[4] = {0, 0, 0, 0};
+  Ev ev;
+#define SK(x)                                   \
+  do {                                          \
+    if ((x) != cudaSuccess) return RBRP_ECUDA;  \
+  } while (0)
+  // Alg. 4 l.1: Omega (rows l .. lp of Omega^T are zero, so Y's padding columns are 0)
+  ev.begin(prof, s);
+  SK(cudaMemsetAsync(OmT + l * d, 0, (size_t)(lp - l) * d * 8, s));
+  if (OmegaT) {
+    SK(cudaMemcpyAsync(OmT, OmegaT, (size_t)l * d * 8, cudaMemcpyDeviceToDevice, s));
+  } else {
+    if ((rc = rbrp_gaussian_embedding(d, l, seed, OmT, d, stream))) return rc;
+    ++launches;
+  }
+  ph[0] = ev.end(s);
+  // Y = X Omega
+  ev.begin(prof, s);
+  cudaError_t ge = cudaSuccess;
+  if (!gemm_nt_mma(X, ldx, OmT, d, Y, lp, n, lp, d, s, &ge)) return RBRP_ENOTSUP;
+  SK(ge);
+  ++launches;
+  ph[1] = ev.end(s);
+  // S = the first k LUPP pivots of Y
+  ev.begin(prof, s);
+  int64_t np = 0;
+  int64_t* Sdev = nullptr;
+  rc = run_lupp(Y, n, l, lp, k, ws + Ly.lu, nullptr, s, S_out, nullptr, &np, &Sdev);
+  if (rc) return rc;
+  launches += 1;
+  ph[2] = ev.end(s);
+  uint32_t flags = np < k ? RBRP_SK_SHORT : 0;
+  // OSID (Alg. 4 l.2-4): W = Y Y_S^+ = Y M, M^T = G1^{-1} Z via CholQR2 of Z^T
+  ev.begin(prof, s);
+  if (np > 0 && W_out) {
+    const int kk = (int)np;
+    const size_t csm = (size_t)kk * (kk + 1) * 8, tsm = (size_t)kk * kk * 8;
+    SK(cudaFuncSetAttribute(k_chol_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
+    SK(cudaFuncSetAttribute(k_trsm_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
+    SK(cudaMemsetAsync(info, 0, sizeof(int), s));
+    const unsigned gt = (unsigned)((lp + 127) / 128), gg = (unsigned)((kk * kk + 255) / 256);
+    k_gather_rows<<<kk, 256, 0, s>>>(Y, lp, Sdev, kk, lp, Z);
+    k_gram_rows<<<gg, 256, 0, s>>>(Z, kk, lp, Gm);                    // G1 = Z Z^T
+    k_chol_small<<<1, 1024, csm, s>>>(Gm, kk, C1, info);             // G1 = C1 C1^T, R1 = C1^T
+    k_trsm_cols<<<gt, 128, tsm, s>>>(C1, kk, Z, lp, 0);             // P1 = C1^{-1} Z = Q1^T
+    k_gram_rows<<<gg, 256, 0, s>>>(Z, kk, lp, Gm);                    // G2 = P1 P1^T
+    k_chol_small<<<1, 1024, csm, s>>>(Gm, kk, C2, info);             // R2 = C2^T
+    k_trsm_cols<<<gt, 128, tsm, s>>>(C2, kk, Z, lp, 0);             // Q^T = C2^{-1} P1
+    k_trsm_cols<<<gt, 128, tsm, s>>>(C2, kk, Z, lp, 1);             // R2^{-1} Q^T
+    k_trsm_cols<<<gt, 128, tsm, s>>>(C1, kk, Z, lp, 1);             // M^T = R1^{-1} R2^{-1} Q^T
+    SK(cudaGetLastError());
+    launches += 9;
+    if (!gemm_nt_mma(Y, lp, Z, lp, W_out, k, n, kk, lp, s, &ge)) return RBRP_ENOTSUP;   // W = Y M
+    SK(ge);
+    SK(launch_w_identity<double>(W_out, k, Sdev, kk, n, 0, s));                         // W(S,:) = I
+    launches += 2;
+  }
+  ph[3] = ev.end(s);
+  int hinfo = 0;
+  SK(cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, s));
+  cudaEventRecord(t1, s);
+  SK(cudaEventSynchronize(t1));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, t0, t1);
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+#undef SK
+  if (rep) {
+    rep->k = np;
+    rep->flags = flags;
+    rep->ms_total = ms;
+    for (int i = 0; i < 4; ++i) rep->ms_phase[i] = ph[i];
+    rep->launches = launches;
+  }
+  return (np > 0 && W_out && hinfo) ? RBRP_EDEGENERATE : RBRP_OK;
+}
+
+}  // extern "C"

@@ -12,8 +12,8 @@ from tests.conftest import ROOT
 rb = pytest.importorskip("paper_2309_16002_b200.rbrp")
 
 
-def _declared():
-    txt = open(os.path.join(ROOT, "include", "rbrp.h")).read()
+def _declared(header="rbrp.h"):
+    txt = open(os.path.join(ROOT, "include", header)).read()
     return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(rbrp_\w+)\s*\(", txt, re.M)))
 
 
@@ -24,6 +24,32 @@ def test_library_exports_header_symbols():
     for name in decl:
         assert hasattr(L, name), name
     assert set(decl) == set(rb.EXPORTED)
+
+
+def test_library_exports_sketch_header_symbols():
+    from paper_2309_16002_b200 import sketch as sk
+    L = sk.lib()
+    decl = _declared("rbrp_sketch.h")
+    assert "rbrp_sketch_id" in decl and "rbrp_lupp" in decl
+    for name in decl:
+        assert hasattr(L, name), name
+    assert set(decl) == set(sk.EXPORTED)
+    headers = sorted(f for f in os.listdir(os.path.join(ROOT, "include")) if f.endswith(".h"))
+    assert headers == ["rbrp.h", "rbrp_sketch.h"]
+
+
+def test_sketch_validation_before_cuda():
+    from paper_2309_16002_b200 import sketch as sk
+    L = sk.lib()
+    sz = ctypes.c_size_t()
+    assert L.rbrp_sketch_workspace_size(1000, 64, 10, 30, ctypes.byref(sz)) == 0
+    assert sz.value > 1000 * 32 * 8
+    for bad in [(1000, 64, 0, 30), (1000, 64, 10, 9), (1000, 64, 10, 41), (1000, 64, 161, 480),
+                (1000, 16, 10, 30), (5, 64, 10, 30)]:
+        assert L.rbrp_sketch_workspace_size(*bad, ctypes.byref(sz)) == -1, bad
+    assert L.rbrp_lupp_workspace_size(1000, 30, 10, ctypes.byref(sz)) == 0
+    assert L.rbrp_lupp_workspace_size(1000, 30, 31, ctypes.byref(sz)) == -1
+    assert L.rbrp_gaussian_embedding(0, 10, 0, None, 0, None) == -1
 
 
 def test_version_and_strerror():
