@@ -126,18 +126,25 @@ __global__ void __launch_bounds__(sk::kThreads, 1) k_lupp(LuArgs a) {
       }
       __syncthreads();
     }
-    // (2) own active rows: panel columns of Y, then the earlier pivots' updates in order
+    // (2) own active rows: panel columns of Y, then the earlier pivots' updates in order,
+    // the row held in registers (columns >= pw carry unused values)
     for (int i = tid; i < nr; i += sk::kThreads) {
       if (!act[i]) continue;
       const double* yr = a.Y + (r0 + i) * a.ldy + c0;
-      double* ar = A + (size_t)i * LD;
-      for (int j = 0; j < pw; ++j) ar[j] = yr[j];
+      double rv[PW];
+#pragma unroll
+      for (int j = 0; j < PW; ++j) rv[j] = j < pw ? yr[j] : 0.0;
       const double* lr = a.Lm + (r0 + i) * k;
+#pragma unroll 2
       for (int m = 0; m < np0; ++m) {
         const double lm = lr[m];
         const double* u = Us + m * PW;
-        for (int j = 0; j < pw; ++j) ar[j] = __dsub_rn(ar[j], __dmul_rn(lm, u[j]));
+#pragma unroll
+        for (int j = 0; j < PW; ++j) rv[j] = __dsub_rn(rv[j], __dmul_rn(lm, u[j]));
       }
+      double* ar = A + (size_t)i * LD;
+#pragma unroll
+      for (int j = 0; j < PW; ++j) ar[j] = rv[j];
     }
     __syncthreads();
     // (3) the panel's steps
@@ -373,27 +380,23 @@ __global__ void __launch_bounds__(1024) k_chol_small(const double* __restrict__ 
   if (tid == 0 && bad) *info = 1;
 }
 
-// B (k x lp, row-major) <- C^{-1} B (trans = 0, forward) or C^{-T} B (trans = 1,
-// backward), C lower (k x k); one thread per column of B
-__global__ void k_trsm_cols(const double* __restrict__ C, int k, double* __restrict__ B, int64_t lp, int trans) {
-  extern __shared__ double ts[];   // k x k
-  for (int e = threadIdx.x; e < k * k; e += blockDim.x) ts[e] = C[e];
-  __syncthreads();
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= lp) return;
-  if (!trans) {
-    for (int i = 0; i < k; ++i) {
-      double s = B[(int64_t)i * lp + c];
-      for (int j = 0; j < i; ++j) s = fma(-ts[i * k + j], B[(int64_t)j * lp + c], s);
-      B[(int64_t)i * lp + c] = s / ts[i * k + i];
-    }
-  } else {
-    for (int i = k - 1; i >= 0; --i) {
-      double s = B[(int64_t)i * lp + c];
-      for (int j = i + 1; j < k; ++j) s = fma(-ts[j * k + i], B[(int64_t)j * lp + c], s);
-      B[(int64_t)i * lp + c] = s / ts[i * k + i];
-    }
+// out (k x lp) = op(A) B, A (k x k) triangular, op(A) = A (transA = 0) or A^T; one output
+// per thread, sequential dot over the nonzero range.  lowerA: A lower (else upper).
+__global__ void k_small_tri_mm(const double* __restrict__ A, int k, int transA, int lowerA,
+                               const double* __restrict__ B, int64_t lp, double* __restrict__ out) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)k * lp) return;
+  const int i = (int)(e / lp);
+  const int64_t c = e - (int64_t)i * lp;
+  // op(A)(i, j) nonzero for j <= i if op(A) is lower, j >= i if upper
+  const bool opLower = (lowerA != 0) != (transA != 0);
+  const int j0 = opLower ? 0 : i, j1 = opLower ? i : k - 1;
+  double s = 0.0;
+  for (int j = j0; j <= j1; ++j) {
+    const double a = transA ? A[(int64_t)j * k + i] : A[(int64_t)i * k + j];
+    s = fma(a, B[(int64_t)j * lp + c], s);
   }
+  out[e] = s;
 }
 
 }  // namespace rbrp
@@ -463,7 +466,7 @@ int run_lupp(const double* Y, int64_t n, int64_t l, int64_t ldy, int64_t k, char
 }
 
 struct SkLayout {
-  size_t OmT, Y, lu, Z, G, C1, C2, info, total;
+  size_t OmT, Y, lu, Z, P, G, C1, C2, A1T, A2T, st, info, total;
   int64_t lp;
 };
 SkLayout sk_layout(int64_t n, int64_t d, int64_t k, int64_t l) {
@@ -479,6 +482,14 @@ SkLayout sk_layout(int64_t n, int64_t d, int64_t k, int64_t l) {
   o += lu_layout(n, k, G, true).total;
   L.Z = o;
   o += al256((size_t)k * L.lp * 8);
+  L.P = o;
+  o += al256((size_t)k * L.lp * 8);
+  L.A1T = o;
+  o += al256((size_t)k * k * 8);
+  L.A2T = o;
+  o += al256((size_t)k * k * 8);
+  L.st = o;
+  o += al256(sizeof(DevState));
   L.G = o;
   o += al256((size_t)k * k * 8);
   L.C1 = o;
@@ -621,22 +632,28 @@ int rbrp_sketch_id(const double* X, int64_t n, int64_t d, int64_t ldx, int64_t k
   ev.begin(prof, s);
   if (np > 0 && W_out) {
     const int kk = (int)np;
-    const size_t csm = (size_t)kk * (kk + 1) * 8, tsm = (size_t)kk * kk * 8;
+    double* P = (double*)(ws + Ly.P);
+    double* A1T = (double*)(ws + Ly.A1T);
+    double* A2T = (double*)(ws + Ly.A2T);
+    DevState* dst = (DevState*)(ws + Ly.st);
+    const size_t csm = (size_t)kk * (kk + 1) * 8;
     SK(cudaFuncSetAttribute(k_chol_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
-    SK(cudaFuncSetAttribute(k_trsm_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
     SK(cudaMemsetAsync(info, 0, sizeof(int), s));
-    const unsigned gt = (unsigned)((lp + 127) / 128), gg = (unsigned)((kk * kk + 255) / 256);
-    k_gather_rows<<<kk, 256, 0, s>>>(Y, lp, Sdev, kk, lp, Z);
-    k_gram_rows<<<gg, 256, 0, s>>>(Z, kk, lp, Gm);                    // G1 = Z Z^T
-    k_chol_small<<<1, 1024, csm, s>>>(Gm, kk, C1, info);             // G1 = C1 C1^T, R1 = C1^T
-    k_trsm_cols<<<gt, 128, tsm, s>>>(C1, kk, Z, lp, 0);             // P1 = C1^{-1} Z = Q1^T
-    k_gram_rows<<<gg, 256, 0, s>>>(Z, kk, lp, Gm);                    // G2 = P1 P1^T
-    k_chol_small<<<1, 1024, csm, s>>>(Gm, kk, C2, info);             // R2 = C2^T
-    k_trsm_cols<<<gt, 128, tsm, s>>>(C2, kk, Z, lp, 0);             // Q^T = C2^{-1} P1
-    k_trsm_cols<<<gt, 128, tsm, s>>>(C2, kk, Z, lp, 1);             // R2^{-1} Q^T
-    k_trsm_cols<<<gt, 128, tsm, s>>>(C1, kk, Z, lp, 1);             // M^T = R1^{-1} R2^{-1} Q^T
+    SK(cudaMemsetAsync(dst, 0, sizeof(DevState), s));
+    const unsigned gm = (unsigned)(((int64_t)kk * lp + 255) / 256), gg = (unsigned)((kk * kk + 255) / 256);
+    k_gather_rows<<<kk, 256, 0, s>>>(Y, lp, Sdev, kk, lp, Z);          // Z = Y(S,:)
+    k_gram_rows<<<gg, 256, 0, s>>>(Z, kk, lp, Gm);                      // G1 = Z Z^T
+    k_chol_small<<<1, 1024, csm, s>>>(Gm, kk, C1, info);               // G1 = C1 C1^T (R1 = C1^T)
+    SK(launch_trinv<double>(C1, kk, A1T, kk, dst, s));                 // A1T = C1^{-T}
+    k_small_tri_mm<<<gm, 256, 0, s>>>(A1T, kk, 1, 0, Z, lp, P);        // P1 = C1^{-1} Z = Q1^T
+    k_gram_rows<<<gg, 256, 0, s>>>(P, kk, lp, Gm);                      // G2 = P1 P1^T
+    k_chol_small<<<1, 1024, csm, s>>>(Gm, kk, C2, info);               // G2 = C2 C2^T (R2 = C2^T)
+    SK(launch_trinv<double>(C2, kk, A2T, kk, dst, s));                 // A2T = C2^{-T}
+    k_small_tri_mm<<<gm, 256, 0, s>>>(A2T, kk, 1, 0, P, lp, Z);        // Q^T = C2^{-1} P1
+    k_small_tri_mm<<<gm, 256, 0, s>>>(A2T, kk, 0, 0, Z, lp, P);        // R2^{-1} Q^T
+    k_small_tri_mm<<<gm, 256, 0, s>>>(A1T, kk, 0, 0, P, lp, Z);        // M^T = R1^{-1} R2^{-1} Q^T
     SK(cudaGetLastError());
-    launches += 9;
+    launches += 11;
     if (!gemm_nt_mma(Y, lp, Z, lp, W_out, k, n, kk, lp, s, &ge)) return RBRP_ENOTSUP;   // W = Y M
     SK(ge);
     SK(launch_w_identity<double>(W_out, k, Sdev, kk, n, 0, s));                         // W(S,:) = I
