@@ -53,6 +53,7 @@ def _args():
     ap.add_argument("--form", default="residual", choices=["residual", "paper"],
                     help="residual: north_star hot path (default); paper: Alg. 2 literally (NEXT-1)")
     ap.add_argument("--no-alt-form", action="store_true", help="skip the side measurement of the other form")
+    ap.add_argument("--no-sketch", action="store_true", help="skip the SkLUPP-OSID side measurement (NEXT-4)")
     return ap.parse_args()
 
 
@@ -390,6 +391,31 @@ def main():
                "note": ("paper: Alg. 2 literally (X read only, CGS2 l.6, downdated norms l.16; "
                         "SURVEY NEXT-1)" if other == "paper" else "residual: north_star form")}
 
+    sk = None
+    if not a.no_sketch and world == 1 and cfg.dtype == "f64" and cfg.d % 8 == 0:
+        # side measurement of SkLUPP-OSID at the ID's rank, l = 3k
+        from paper_2309_16002_b200 import sketch as rbs
+        ksk = min(res_list[-1].k, rbs.SK_MAX_K)
+        kws = dict(k=ksk, l=3 * ksk, seed=a.seed)
+        for _ in range(2):
+            rbs.sketch_id(X, **kws)
+        torch.cuda.synchronize()
+        g0 = torch.cuda.Event(enable_timing=True)
+        g1 = torch.cuda.Event(enable_timing=True)
+        ns = max(1, min(a.steps, 10))
+        g0.record(stream)
+        for _ in range(ns):
+            rs = rbs.sketch_id(X, **kws)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        ts = g0.elapsed_time(g1) / ns
+        ph = rbs.sketch_id(X, profile=True, **kws).ms_phase
+        lp = (3 * ksk + 7) // 8 * 8
+        sk = {"method": "SkLUPP-OSID (Alg. 4, l = 3k)", "value": ts / 1e3, "unit": "s", "steps": ns, "k": rs.k,
+              "l": 3 * ksk, "ms_phase": ph, "launches": rs.launches,
+              "sketch_gemm_tflops": 2 * cfg.n * cfg.d * lp / (ph["sketch"] * 1e9),
+              "note": "SURVEY NEXT-4 (the paper's GPU competitor, Table 3 P:783); not the headline"}
+
     if rank != 0:
         if comm:
             comm.close()
@@ -434,6 +460,7 @@ def main():
         "phase_ms_eager_profile": {k: v for k, v in rp.ms_phase.items() if k != "unused"},
         "gpu_launches": launches,
         "alt_form": alt,
+        "next4_sklupp_osid": sk,
         "e2e": e2e,
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
