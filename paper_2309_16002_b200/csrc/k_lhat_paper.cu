@@ -17,6 +17,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include "launch.cuh"
 
@@ -367,7 +368,7 @@ __global__ void __launch_bounds__(lp::NTH, 1)
             // l.16 downdate (paper form): sum over the row's columns (q lanes)
             ss += __shfl_xor_sync(0xffffffffu, ss, 1);
             ss += __shfl_xor_sync(0xffffffffu, ss, 2);
-            if (q == 0 && row < n) dvec[row] = fmax(dvec[row] - ss, 0.0);
+            if (q == 0 && row < n && dvec) dvec[row] = fmax(dvec[row] - ss, 0.0);   // none: plain GEMM
           }
         }
       }
@@ -577,6 +578,53 @@ cudaError_t launch_lhat_paper(const double* X, int64_t ldx, const double* Qp, do
     case 32: return go_lp<32>(map, map0, lazy, Qp, L, ldl, n, d, dvec, st, (double*)X, ldx, resid ? 1 : 0, s);
     default: return cudaErrorInvalidValue;
   }
+}
+
+// ------------------------------------------------------------------------------------
+// C = A B^T as a sequence of read-only L-hat passes (the paper-form kernel without a
+// downdate), 32 columns of C per launch: every launch streams A once through TMA and
+// runs the 64-row-tile DMMA loop that reaches 97% of the DMMA rate (profiles/README).
+// Used for W = L L_1^{-1} (Alg. 3) and the SkLUPP-OSID GEMMs.  Each column group gets
+// its own DevState (b_prime = group width, k = first column) in the scratch.
+// ------------------------------------------------------------------------------------
+__global__ void k_gemm_groups(DevState* st, int64_t N, int gw) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g * gw >= N) return;
+  DevState z;
+  memset(&z, 0, sizeof(z));
+  z.k = g * gw;
+  z.k_cap = N;
+  z.b_prime = (int)(N - g * gw < gw ? N - g * gw : gw);
+  z.t = 2;
+  st[g] = z;
+}
+
+size_t gemm_lp_scratch_bytes(int64_t N, int64_t K) {
+  const int64_t G = (N + 31) / 32;
+  return ((fused_pack_bytes(K) + 255) & ~(size_t)255) + (size_t)G * sizeof(DevState);
+}
+
+// K >= 512: the per-tile fold of the 4-way K split is amortised over >= 8 chunk steps
+// (measured: W = L L_1^{-1} at K = 128 and the OSID W at K = 384 ran slower than k_nt_mma)
+bool gemm_lp_supported(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t K) {
+  return K >= 512 && lhat_paper_max_bucket(A, lda, K) >= 32 && ldb == K && ((uintptr_t)B % 16) == 0;
+}
+
+cudaError_t gemm_nt_lp(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
+                       int64_t M, int64_t N, int64_t K, void* scratch, cudaStream_t s) {
+  if (M <= 0 || N <= 0) return cudaSuccess;
+  if (!gemm_lp_supported(A, lda, B, ldb, K)) return cudaErrorNotSupported;
+  double* Qp = (double*)scratch;
+  DevState* st = (DevState*)((char*)scratch + ((fused_pack_bytes(K) + 255) & ~(size_t)255));
+  const int64_t G = (N + 31) / 32;
+  k_gemm_groups<<<(unsigned)((G + 127) / 128), 128, 0, s>>>(st, N, 32);
+  cudaError_t e = cudaGetLastError();
+  for (int64_t g = 0; g < G && e == cudaSuccess; ++g) {
+    const int bg = (int)(N - 32 * g < 32 ? N - 32 * g : 32);
+    e = launch_pack_q(B + 32 * g * ldb, K, Qp, st + g, s);
+    if (e == cudaSuccess) e = launch_lhat_paper(A, lda, Qp, C, ldc, M, K, nullptr, st + g, bucket_of(bg), false, s);
+  }
+  return e;
 }
 
 }  // namespace rbrp

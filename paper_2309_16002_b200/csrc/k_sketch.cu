@@ -466,7 +466,7 @@ int run_lupp(const double* Y, int64_t n, int64_t l, int64_t ldy, int64_t k, char
 }
 
 struct SkLayout {
-  size_t OmT, Y, lu, Z, P, G, C1, C2, A1T, A2T, st, info, total;
+  size_t OmT, Y, lu, Z, P, G, C1, C2, A1T, A2T, st, gsc, info, total;
   int64_t lp;
 };
 SkLayout sk_layout(int64_t n, int64_t d, int64_t k, int64_t l) {
@@ -490,6 +490,8 @@ SkLayout sk_layout(int64_t n, int64_t d, int64_t k, int64_t l) {
   o += al256((size_t)k * k * 8);
   L.st = o;
   o += al256(sizeof(DevState));
+  L.gsc = o;
+  o += al256(std::max(gemm_lp_scratch_bytes(L.lp, d), gemm_lp_scratch_bytes(k, L.lp)));
   L.G = o;
   o += al256((size_t)k * k * 8);
   L.C1 = o;
@@ -615,9 +617,15 @@ int rbrp_sketch_id(const double* X, int64_t n, int64_t d, int64_t ldx, int64_t k
   // Y = X Omega
   ev.begin(prof, s);
   cudaError_t ge = cudaSuccess;
-  if (!gemm_nt_mma(X, ldx, OmT, d, Y, lp, n, lp, d, s, &ge)) return RBRP_ENOTSUP;
-  SK(ge);
-  ++launches;
+  void* gsc = ws + Ly.gsc;
+  if (gemm_lp_supported(X, ldx, OmT, d, d)) {   // 32-column read-only DMMA passes
+    SK(gemm_nt_lp(X, ldx, OmT, d, Y, lp, n, lp, d, gsc, s));
+    launches += 1 + 2 * (int)((lp + 31) / 32);
+  } else {
+    if (!gemm_nt_mma(X, ldx, OmT, d, Y, lp, n, lp, d, s, &ge)) return RBRP_ENOTSUP;
+    SK(ge);
+    ++launches;
+  }
   ph[1] = ev.end(s);
   // S = the first k LUPP pivots of Y
   ev.begin(prof, s);
@@ -654,8 +662,13 @@ int rbrp_sketch_id(const double* X, int64_t n, int64_t d, int64_t ldx, int64_t k
     k_small_tri_mm<<<gm, 256, 0, s>>>(A1T, kk, 0, 0, P, lp, Z);        // M^T = R1^{-1} R2^{-1} Q^T
     SK(cudaGetLastError());
     launches += 11;
-    if (!gemm_nt_mma(Y, lp, Z, lp, W_out, k, n, kk, lp, s, &ge)) return RBRP_ENOTSUP;   // W = Y M
-    SK(ge);
+    if (gemm_lp_supported(Y, lp, Z, lp, lp)) {                                         // W = Y M
+      SK(gemm_nt_lp(Y, lp, Z, lp, W_out, k, n, kk, lp, gsc, s));
+      launches += 2 * (kk + 31) / 32;
+    } else {
+      if (!gemm_nt_mma(Y, lp, Z, lp, W_out, k, n, kk, lp, s, &ge)) return RBRP_ENOTSUP;
+      SK(ge);
+    }
     SK(launch_w_identity<double>(W_out, k, Sdev, kk, n, 0, s));                         // W(S,:) = I
     launches += 2;
   }

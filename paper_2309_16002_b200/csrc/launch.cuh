@@ -131,6 +131,12 @@ cudaError_t launch_downdate(const T* L, int64_t ldl, int64_t n, double* dvec, De
                             int fused_max, cudaStream_t s);
 bool gemm_nt_mma(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
                  int64_t M, int64_t N, int64_t K, cudaStream_t s, cudaError_t* err);
+// k_lhat_paper.cu: C = A B^T by read-only L-hat passes of 32 columns (B: N x K, ldb == K);
+// scratch >= gemm_lp_scratch_bytes(N, K), 256-byte aligned
+size_t gemm_lp_scratch_bytes(int64_t N, int64_t K);
+bool gemm_lp_supported(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t K);
+cudaError_t gemm_nt_lp(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
+                       int64_t M, int64_t N, int64_t K, void* scratch, cudaStream_t s);
 
 // k_formw.cu — Alg. 3 by triangular solve
 template <typename T>

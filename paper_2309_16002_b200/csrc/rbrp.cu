@@ -35,7 +35,7 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
   size_t Xres = SIZE_MAX, Qall = SIZE_MAX, Ccgs = SIZE_MAX, Topb = SIZE_MAX, Stop = SIZE_MAX, Tcnt = SIZE_MAX, dvec, cpre, ctot, cpos, cprefix, L, Qt, Qp, Vg, Gpart, G, Tg, Ag, R11, Rtot,
-         piv, mass, St, Srep, S, forced, dbg, cand, st, L1 = SIZE_MAX, LinvT = SIZE_MAX;
+         piv, mass, St, Srep, S, forced, dbg, cand, st, L1 = SIZE_MAX, LinvT = SIZE_MAX, Wsc = SIZE_MAX;
   size_t lbt, lbp, lrho, lSt, lpiv, lts, total;
   int nsplit, maxlog;
   int64_t nchunks, k_cap;
@@ -121,6 +121,7 @@ Layout make_layout(const rbrp_problem* p) {
   if (!(p->flags & RBRP_NO_W)) {
     L.L1 = take((size_t)L.k_cap * L.k_cap * 8);
     L.LinvT = take((size_t)L.k_cap * ((L.k_cap + 7) / 8 * 8) * w);   // k x round8(k) (K padded for DMMA)
+    L.Wsc = take(gemm_lp_scratch_bytes(L.k_cap, (L.k_cap + 7) / 8 * 8));   // packed L_1^{-T} groups
   }
   L.total = off;
   return L;
@@ -205,6 +206,7 @@ struct Ctx {
   int64_t *St, *Srep, *S, *cand;
   double* L1;
   T* LinvT;
+  void* Wsc;   // scratch of the W GEMM (gemm_nt_lp)
   DevState* st;
   long long* dbg;
   BlockLog log;
@@ -259,6 +261,7 @@ void make_ctx(Ctx<T>& c, const rbrp_problem* p, void* Xv, char* ws, const Layout
   c.st = (DevState*)(ws + Ly.st);
   c.L1 = Ly.L1 != SIZE_MAX ? (double*)(ws + Ly.L1) : nullptr;
   c.LinvT = Ly.LinvT != SIZE_MAX ? (T*)(ws + Ly.LinvT) : nullptr;
+  c.Wsc = Ly.Wsc != SIZE_MAX ? (void*)(ws + Ly.Wsc) : nullptr;
   c.dbg = env_on("RBRP_DEBUG_STAMPS") ? (long long*)(ws + Ly.dbg) : nullptr;
   c.log.bt = (int32_t*)(ws + Ly.lbt);
   c.log.bp = (int32_t*)(ws + Ly.lbp);
@@ -696,9 +699,14 @@ int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* 
       CK(cudaMemset2DAsync(c.Lm + k, (size_t)k_cap * sizeof(T), 0, (size_t)(kp - k) * sizeof(T), (size_t)c.n, s));
     cudaError_t merr = cudaSuccess;
     ++nl;
-    if (sizeof(T) == 8 && !force_simt() && kp <= k_cap &&
-        gemm_nt_mma((const double*)c.Lm, k_cap, (const double*)LinvT, kp, (double*)W_out, k_cap, c.n, k,
-                    kp, s, &merr)) {
+    if (sizeof(T) == 8 && !force_simt() && kp <= k_cap && c.Wsc && !env_on("RBRP_W_NTMMA") &&
+        gemm_lp_supported((const double*)c.Lm, k_cap, (const double*)LinvT, kp, kp)) {
+      CK(gemm_nt_lp((const double*)c.Lm, k_cap, (const double*)LinvT, kp, (double*)W_out, k_cap, c.n, k, kp,
+                    c.Wsc, s));
+      nl += 2 * (int)((k + 31) / 32);
+    } else if (sizeof(T) == 8 && !force_simt() && kp <= k_cap &&
+               gemm_nt_mma((const double*)c.Lm, k_cap, (const double*)LinvT, kp, (double*)W_out, k_cap, c.n, k,
+                           kp, s, &merr)) {
       CK(merr);
     } else {
       CK(launch_gemm_nt<T>(c.Lm, k_cap, LinvT, kp, (T*)W_out, k_cap, c.n, k, k, s));
@@ -984,9 +992,14 @@ int run_dist(int nsh, const rbrp_problem* ps, void* const* Xs, char* const* wss,
         CK(cudaMemset2DAsync(c.Lm + k, (size_t)k_cap * sizeof(T), 0, (size_t)(kp - k) * sizeof(T), (size_t)c.n, s));
       cudaError_t merr = cudaSuccess;
       ++nl;
-      if (sizeof(T) == 8 && !force_simt() && kp <= k_cap &&
-          gemm_nt_mma((const double*)c.Lm, k_cap, (const double*)c.LinvT, kp, (double*)W_outs[h], k_cap, c.n,
-                      k, kp, s, &merr)) {
+      if (sizeof(T) == 8 && !force_simt() && kp <= k_cap && c.Wsc && !env_on("RBRP_W_NTMMA") &&
+          gemm_lp_supported((const double*)c.Lm, k_cap, (const double*)c.LinvT, kp, kp)) {
+        CK(gemm_nt_lp((const double*)c.Lm, k_cap, (const double*)c.LinvT, kp, (double*)W_outs[h], k_cap, c.n, k,
+                      kp, c.Wsc, s));
+        nl += 2 * (int)((k + 31) / 32);
+      } else if (sizeof(T) == 8 && !force_simt() && kp <= k_cap &&
+                 gemm_nt_mma((const double*)c.Lm, k_cap, (const double*)c.LinvT, kp, (double*)W_outs[h], k_cap,
+                             c.n, k, kp, s, &merr)) {
         CK(merr);
       } else {
         CK(launch_gemm_nt<T>(c.Lm, k_cap, c.LinvT, kp, (T*)W_outs[h], k_cap, c.n, k, k, s));
