@@ -142,15 +142,28 @@ __global__ void __launch_bounds__(lp::NTH, 1)
                  int lazy, const double* __restrict__ Qp,
                  double* __restrict__ L, int64_t ldl, int64_t n, int d, int nc, int NS, int NQ,
                  double* __restrict__ dvec, DevState* st, double* __restrict__ Xr, int64_t ldx, int resid,
-                 long long* __restrict__ tr) {
+                 long long* __restrict__ tr, int part) {
   using Cf = LpCfg<BPB>;
   constexpr int NT = Cf::NT;
   using namespace lp;
   if (st->stop) return;
-  const int bp = st->b_prime;
-  if (bp <= 0 || bucket_of(bp) != BPB) return;
-  const int64_t k0 = st->k;
-  if (blockIdx.x == 0 && threadIdx.x == 0) st->ts0 = gtimer();
+  // part < 0: the block's b' columns if b' falls in this bucket.  part >= 0 (b' > 32): the
+  // 32-column part [32 part, min(b', 32 part + 32)) of Q_b; the parts run in order, each
+  // on the residual the previous one left (Q_b's rows are orthonormal, so the sequence
+  // equals one projection up to rounding; the paper form downdates per part).
+  int bp;
+  int64_t k0;
+  if (part < 0) {
+    bp = st->b_prime;
+    if (bp <= 0 || bucket_of(bp) != BPB) return;
+    k0 = st->k;
+  } else {
+    const int bpa = st->b_prime;
+    bp = bpa - 32 * part < 32 ? bpa - 32 * part : 32;
+    if (bpa <= 32 || bp <= 0) return;
+    k0 = st->k + 32 * part;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && part <= 0) st->ts0 = gtimer();
 
   extern __shared__ __align__(1024) double sm_raw[];
   double* sm = sm_raw + ((1024u - (lp_su32(sm_raw) & 1023u)) & 1023u) / 8;
@@ -192,7 +205,7 @@ __global__ void __launch_bounds__(lp::NTH, 1)
       // policy, the update pass (same addresses, shortly after) with evict_first, so the
       // second read is served by L2 and HBM sees one read of X_res.
       // Lazy X_res copy: block 1 reads the input X (xmap0); the update pass writes X_res.
-      const CUtensorMap* mp = (lazy && st->t == 1) ? &xmap0 : &xmap;
+      const CUtensorMap* mp = (lazy && st->t == 1 && part <= 0) ? &xmap0 : &xmap;
       uint64_t pol_keep, pol_drop;
       asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol_keep));
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol_drop));
@@ -536,7 +549,7 @@ int lhat_paper_max_bucket(const void* X, int64_t ldx, int64_t d) {
 template <int BPB>
 static cudaError_t go_lp(const CUtensorMap& map, const CUtensorMap& map0, int lazy, const double* Qp, double* L,
                          int64_t ldl, int64_t n, int64_t d, double* dvec, DevState* st, double* Xr, int64_t ldx,
-                         int resid, cudaStream_t s) {
+                         int resid, cudaStream_t s, int part) {
   using Cf = LpCfg<BPB>;
   int ns, nq;
   if (!Cf::rings(ns, nq)) return cudaErrorInvalidValue;
@@ -550,13 +563,13 @@ static cudaError_t go_lp(const CUtensorMap& map, const CUtensorMap& map0, int la
     traced = 1;
   }
   k_lhat_paper<BPB><<<lp_sms(), lp::NTH, smem, s>>>(map, map0, lazy, Qp, L, ldl, n, (int)d, nc, ns, nq, dvec, st,
-                                                     Xr, ldx, resid, tr);
+                                                     Xr, ldx, resid, tr, part);
   return cudaGetLastError();
 }
 
 cudaError_t launch_lhat_paper(const double* X, int64_t ldx, const double* Qp, double* L, int64_t ldl,
                               int64_t n, int64_t d, double* dvec, DevState* st, int bucket, bool resid,
-                              cudaStream_t s, const double* X0, int64_t ldx0) {
+                              cudaStream_t s, const double* X0, int64_t ldx0, int part) {
   if (n <= 0) return cudaSuccess;
   auto enc = lp_encode();
   if (!enc) return cudaErrorNotSupported;
@@ -574,8 +587,8 @@ cudaError_t launch_lhat_paper(const double* X, int64_t ldx, const double* Qp, do
   const int lazy = X0 != nullptr ? 1 : 0;
   if (!make_map(lazy ? X0 : X, lazy ? ldx0 : ldx, &map0)) return cudaErrorInvalidValue;
   switch (bucket) {
-    case 16: return go_lp<16>(map, map0, lazy, Qp, L, ldl, n, d, dvec, st, (double*)X, ldx, resid ? 1 : 0, s);
-    case 32: return go_lp<32>(map, map0, lazy, Qp, L, ldl, n, d, dvec, st, (double*)X, ldx, resid ? 1 : 0, s);
+    case 16: return go_lp<16>(map, map0, lazy, Qp, L, ldl, n, d, dvec, st, (double*)X, ldx, resid ? 1 : 0, s, -1);
+    case 32: return go_lp<32>(map, map0, lazy, Qp, L, ldl, n, d, dvec, st, (double*)X, ldx, resid ? 1 : 0, s, part);
     default: return cudaErrorInvalidValue;
   }
 }

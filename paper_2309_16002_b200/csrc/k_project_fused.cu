@@ -135,14 +135,24 @@ __device__ __forceinline__ int xoff(int row, int col) {
 }
 __device__ __forceinline__ int pi_row(int g) { return (g >> 1) + 4 * (g & 1); }
 
+// part < 0: rows [0, b'), b' <= 64.  part >= 0 (b' > 32 split into 32-row parts, see
+// launch_lhat_paper): rows [32 part, min(b', 32 part + 32)).
 __global__ void k_pack_q(const double* __restrict__ Qt, int64_t d, double* __restrict__ Qp,
-                         const DevState* st) {
+                         const DevState* st, int part) {
   if (st->stop) return;
-  const int bp = st->b_prime;
-  if (bp <= 0 || bp > fz::PACK_ROWS) return;
+  const int bpa = st->b_prime;
+  int bp, r0 = 0;
+  if (part < 0) {
+    bp = bpa;
+    if (bp <= 0 || bp > fz::PACK_ROWS) return;
+  } else {
+    r0 = 32 * part;
+    bp = bpa - r0 < 32 ? bpa - r0 : 32;
+    if (bpa <= 32 || bp <= 0) return;
+  }
   const int c = blockIdx.x, j = blockIdx.y, col = threadIdx.x;   // blockDim = KC
   const int64_t gc = (int64_t)c * fz::KC + col;
-  const double v = (j < bp && gc < d) ? Qt[(int64_t)j * d + gc] : 0.0;
+  const double v = (j < bp && gc < d) ? Qt[(int64_t)(r0 + j) * d + gc] : 0.0;
   Qp[((int64_t)c * fz::PACK_ROWS + j) * fz::KC + qswz(j, col)] = v;
   // second image (update pass of k_lhat_paper): rows in pairs, (Q(2p, col), Q(2p+1, col))
   // adjacent, 16-byte unit of pair p and column col at p * KC + (col ^ 2 (p & 3))
@@ -681,9 +691,9 @@ static cudaError_t go_fused(const CUtensorMap& map, double* X, int64_t ldx, cons
   return cudaGetLastError();
 }
 
-cudaError_t launch_pack_q(const double* Qt, int64_t d, double* Qp, DevState* st, cudaStream_t s) {
+cudaError_t launch_pack_q(const double* Qt, int64_t d, double* Qp, DevState* st, cudaStream_t s, int part) {
   dim3 grid((unsigned)fz_nc(d), fz::PACK_ROWS);
-  k_pack_q<<<grid, fz::KC, 0, s>>>(Qt, d, Qp, st);
+  k_pack_q<<<grid, fz::KC, 0, s>>>(Qt, d, Qp, st, part);
   return cudaGetLastError();
 }
 

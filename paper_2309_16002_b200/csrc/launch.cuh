@@ -103,7 +103,7 @@ cudaError_t launch_update_mma(double* Xres, int64_t ldx, const double* Qt, const
 // k_project_fused.cu — single-pass fused projection (L-hat, update, norms), b' <= 64
 size_t fused_pack_bytes(int64_t d);
 int fused_max_bucket(const void* X, int64_t ldx, int64_t d);
-cudaError_t launch_pack_q(const double* Qt, int64_t d, double* Qp, DevState* st, cudaStream_t s);
+cudaError_t launch_pack_q(const double* Qt, int64_t d, double* Qp, DevState* st, cudaStream_t s, int part = -1);
 cudaError_t launch_proj_fused(double* Xres, int64_t ldx, const double* Qp, double* L, int64_t ldl,
                               int64_t n, int64_t d, double* dvec, DevState* st, int bucket, bool paper,
                               cudaStream_t s);
@@ -112,7 +112,7 @@ cudaError_t launch_proj_fused(double* Xres, int64_t ldx, const double* Qp, doubl
 int lhat_paper_max_bucket(const void* X, int64_t ldx, int64_t d);
 cudaError_t launch_lhat_paper(const double* X, int64_t ldx, const double* Qp, double* L, int64_t ldl,
                               int64_t n, int64_t d, double* dvec, DevState* st, int bucket, bool resid,
-                              cudaStream_t s, const double* X0 = nullptr, int64_t ldx0 = 0);
+                              cudaStream_t s, const double* X0 = nullptr, int64_t ldx0 = 0, int part = -1);
 // resid: + the update pass (residual form, L2 re-read).  X0 (lazy X_res): in block 1 the
 // tile is read from X0 (the input) and the update is written to X (X_res)
 

@@ -283,8 +283,10 @@ void make_ctx(Ctx<T>& c, const rbrp_problem* p, void* Xv, char* ws, const Layout
   // the tiled kernel handles every bucket of this problem, so it can take block 1 straight
   // from X (X_res is then never copied: one HBM read + write less per ID).  Single-GPU
   // path only (run_dist keeps the copy).
-  c.lazy = c.tiled && !inplace && c.Xres != c.X && c.lp_max >= c.bucketB && c.lp_max > 0 &&
-           lhat_paper_max_bucket(c.X, p->ld, c.d) >= c.bucketB && !comm && !env_on("RBRP_EAGER_COPY");
+  // (b' > 32 runs as 32-column parts on the same kernel, enqueue_projection)
+  const int lp_need = c.bucketB > 32 && !env_on("RBRP_NO_PARTS") ? 32 : c.bucketB;
+  c.lazy = c.tiled && !inplace && c.Xres != c.X && c.lp_max >= lp_need && c.lp_max > 0 &&
+           lhat_paper_max_bucket(c.X, p->ld, c.d) >= lp_need && !comm && !env_on("RBRP_EAGER_COPY");
 }
 
 template <typename T>
@@ -340,7 +342,11 @@ int enqueue_projection(Ctx<T>& c, cudaStream_t s, int* nl) {
   const int fmax = (c.paper || c.tiled) ? c.lp_max : c.fused_max;
   if (fmax > 0 && (rc = lk(launch_pack_q((const double*)c.Qt, c.d, c.Qp, c.st, s)))) return rc;
   bool need_downdate = false;
+  // b' > 32 on the 64-row-tile kernel: 32-column parts in sequence (RBRP_NO_PARTS=1: the
+  // two-kernel path instead)
+  const bool parts = (c.paper || c.tiled) && c.lp_max >= 32 && c.bucketB > 32 && !env_on("RBRP_NO_PARTS");
   for (int bk = 16; bk <= c.bucketB; bk *= 2) {
+    if (bk > 32 && parts) continue;
     if (bk <= fmax) {
       if (c.paper || c.tiled)
         rc = lk(launch_lhat_paper((const double*)c.Xres, c.ldr, c.Qp, (double*)c.Lm, c.k_cap, c.n, c.d,
@@ -363,6 +369,12 @@ int enqueue_projection(Ctx<T>& c, cudaStream_t s, int* nl) {
       need_downdate = c.paper;
     }
     if (rc) return rc;
+  }
+  for (int part = 0; parts && part < c.bucketB / 32; ++part) {
+    if ((rc = lk(launch_pack_q((const double*)c.Qt, c.d, c.Qp, c.st, s, part)))) return rc;
+    if ((rc = lk(launch_lhat_paper((const double*)c.Xres, c.ldr, c.Qp, (double*)c.Lm, c.k_cap, c.n, c.d, c.dvec,
+                                   c.st, 32, !c.paper, s, c.lazy ? (const double*)c.X : nullptr, c.p->ld, part))))
+      return rc;
   }
   // paper form on the two-kernel path: l.16 downdate from the L-hat columns (the kernel
   // skips blocks whose bucket the fused kernel handled, which downdates in its epilogue)
