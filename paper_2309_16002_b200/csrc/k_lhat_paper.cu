@@ -37,8 +37,7 @@ constexpr int NCW = 4;           // column groups (16 columns each)
 constexpr int NRP = 4;           // row pairs (16 rows each)
 constexpr int NCONS = NCW * NRP; // consumer warps
 constexpr int NTH = (NCONS + 2) * 32;   // consumers + X and Q producer warps
-constexpr int SLOT = R * KC;     // doubles per X slot (4 boxes of 64 rows x 16 columns)
-constexpr int BOX = R * 16;      // doubles per box
+constexpr int SLOT = R * KC;     // elements per X slot
 constexpr int PACK_ROWS = 64;    // rows of the packed Q_b buffer (k_pack_q)
 constexpr int SMEM_MAX = 232448;
 }  // namespace lp
@@ -100,9 +99,41 @@ __device__ __forceinline__ double2 lp_lds2(const double* p) {
 __device__ __forceinline__ void lp_bar() { asm volatile("bar.sync 1, %0;\n" ::"n"(lp::NCONS * 32) : "memory"); }
 // Q chunk layout of k_pack_q: row j, column c at j * 64 + (c ^ f(j))
 __device__ __forceinline__ int lp_qswz(int j, int col) { return col ^ (8 * (j & 1)) ^ (4 * ((j >> 1) & 3)); }
-// X slot: box (col >> 4) of 64 rows x 16 doubles, 128-byte swizzle of 16-byte chunks by row
-__device__ __forceinline__ int lp_xoff(int row, int col) {
-  return (col >> 4) * lp::BOX + row * 16 + ((((col & 15) >> 1) ^ (row & 7)) << 1);
+
+// element type of X / X_res / L (storage); the arithmetic is fp64 DMMA either way.  A
+// 128-byte TMA box row holds CPB elements; MMA row g of an 8-row group is tile row pg(g),
+// chosen so that the 8-byte fragment loads of a half-warp hit 32 distinct banks under the
+// 128-byte swizzle (fp64: rows {0,4,1,5}/{2,6,3,7}; fp32: rows {0,2,4,6}/{1,3,5,7}).
+template <typename E>
+struct LpE;
+template <>
+struct LpE<double> {
+  static constexpr int CPB = 16;
+  __device__ static int pg(int g) { return (g >> 1) + 4 * (g & 1); }
+  __device__ static double2 ld2(uint32_t a) { return lp_lds2s(a); }
+  __device__ static double2 rnd(double2 v) { return v; }   // the value as stored
+  __device__ static void st2(double* p, double2 v) { __stcs(reinterpret_cast<double2*>(p), v); }
+};
+template <>
+struct LpE<float> {
+  static constexpr int CPB = 32;
+  __device__ static int pg(int g) { return 2 * (g & 3) + (g >> 2); }
+  __device__ static double2 ld2(uint32_t a) {
+    float x, y;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];\n" : "=f"(x), "=f"(y) : "r"(a));
+    return make_double2(x, y);
+  }
+  __device__ static double2 rnd(double2 v) { return make_double2((double)(float)v.x, (double)(float)v.y); }
+  __device__ static void st2(float* p, double2 v) {
+    __stcs(reinterpret_cast<float2*>(p), make_float2((float)v.x, (float)v.y));
+  }
+};
+// X slot: KC / CPB boxes of 64 rows x CPB elements, 128-byte swizzle of 16-byte chunks by row
+template <typename E>
+__device__ __forceinline__ int lp_xoff_e(int row, int col) {
+  constexpr int CPB = LpE<E>::CPB, EPC = 16 / (int)sizeof(E);   // elements per 16-byte chunk
+  const int c = col % CPB;
+  return (col / CPB) * (lp::R * CPB) + row * CPB + (((c / EPC) ^ (row & 7)) * EPC) + (c % EPC);
 }
 
 struct LpRing {
@@ -115,14 +146,15 @@ struct LpRing {
   }
 };
 
-template <int BPB>
+template <int BPB, typename E = double>
 struct LpCfg {
   static constexpr int NT = BPB / 8;
   static constexpr int ACC = 2 * NT * 2;          // doubles per lane of a row pair's partial
   static constexpr int QSTAGE = BPB * lp::KC;
   static constexpr int SCR = lp::NRP * 2 * ACC * 32;   // two partial slots per row pair
+  static constexpr int SLOTB = lp::SLOT * (int)sizeof(E);   // bytes per X slot
   static size_t smem(int ns, int nq) {
-    return (size_t)ns * lp::SLOT * 8 + (size_t)nq * QSTAGE * 8 + (size_t)(SCR + 2 * lp::NRP * lp::NCW * 16) * 8 +
+    return (size_t)ns * SLOTB + (size_t)nq * QSTAGE * 8 + (size_t)(SCR + 2 * lp::NRP * lp::NCW * 16) * 8 +
            (2 * ns + 2 * nq) * 8 + 1024;
   }
   static bool rings(int& ns, int& nq) {
@@ -136,14 +168,16 @@ struct LpCfg {
   }
 };
 
-template <int BPB>
+template <int BPB, typename E>
 __global__ void __launch_bounds__(lp::NTH, 1)
     k_lhat_paper(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap xmap0,
                  int lazy, const double* __restrict__ Qp,
-                 double* __restrict__ L, int64_t ldl, int64_t n, int d, int nc, int NS, int NQ,
-                 double* __restrict__ dvec, DevState* st, double* __restrict__ Xr, int64_t ldx, int resid,
+                 E* __restrict__ L, int64_t ldl, int64_t n, int d, int nc, int NS, int NQ,
+                 double* __restrict__ dvec, DevState* st, E* __restrict__ Xr, int64_t ldx, int resid,
                  long long* __restrict__ tr, int part) {
-  using Cf = LpCfg<BPB>;
+  using Cf = LpCfg<BPB, E>;
+  using LE = LpE<E>;
+  constexpr int CPB = LE::CPB, NBOX = lp::KC / CPB, BOXE = lp::R * CPB;
   constexpr int NT = Cf::NT;
   using namespace lp;
   if (st->stop) return;
@@ -167,8 +201,8 @@ __global__ void __launch_bounds__(lp::NTH, 1)
 
   extern __shared__ __align__(1024) double sm_raw[];
   double* sm = sm_raw + ((1024u - (lp_su32(sm_raw) & 1023u)) & 1023u) / 8;
-  double* xs = sm;                                   // NS x SLOT
-  double* qs = xs + (size_t)NS * SLOT;               // NQ x QSTAGE
+  E* xs = reinterpret_cast<E*>(sm);                  // NS x SLOT elements of E
+  double* qs = reinterpret_cast<double*>(xs + (size_t)NS * SLOT);   // NQ x QSTAGE
   double* scr = qs + (size_t)NQ * Cf::QSTAGE;        // [rp][slot 0..1][ACC][32]
   double* nrm = scr + Cf::SCR;                       // [tile parity][rp][cw][16] row-norm partials
   uint64_t* xfull = reinterpret_cast<uint64_t*>(nrm + 2 * NRP * NCW * 16);
@@ -221,15 +255,15 @@ __global__ void __launch_bounds__(lp::NTH, 1)
           continue;
         }
 #endif
-        lp_expect(&xfull[xr.i], SLOT * 8);   // out-of-bounds rows / columns are zero-filled
-        double* dst = xs + (size_t)xr.i * SLOT;
+        lp_expect(&xfull[xr.i], Cf::SLOTB);   // out-of-bounds rows / columns are zero-filled
+        E* dst = xs + (size_t)xr.i * SLOT;
         const uint64_t pol = resid ? (second ? pol_drop : pol_keep) : pol_drop;
 #pragma unroll
-        for (int b = 0; b < 4; ++b)
+        for (int b = 0; b < NBOX; ++b)
           asm volatile(
               "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint "
-              "[%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(lp_su32(dst + b * BOX)),
-              "l"(mp), "r"(c * KC + 16 * b), "r"(y), "r"(lp_su32(&xfull[xr.i])), "l"(pol)
+              "[%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(lp_su32(dst + b * BOXE)),
+              "l"(mp), "r"(c * KC + CPB * b), "r"(y), "r"(lp_su32(&xfull[xr.i])), "l"(pol)
               : "memory");
         xr.next(NS);
       }
@@ -283,12 +317,12 @@ __global__ void __launch_bounds__(lp::NTH, 1)
 #define LP_T(e)
 #define LP_TS()
 #endif
-    const int pg = (g >> 1) + 4 * (g & 1);   // tile row of MMA row g (bank-conflict-free)
+    const int pg = LE::pg(g);                // tile row of MMA row g (bank-conflict-free)
     int xo[2][2];                            // [row group][8-column half]
 #pragma unroll
     for (int r = 0; r < 2; ++r)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) xo[r][h] = lp_xoff(16 * rp + 8 * r + pg, 16 * cw + 8 * h + 2 * q);
+      for (int h = 0; h < 2; ++h) xo[r][h] = lp_xoff_e<E>(16 * rp + 8 * r + pg, 16 * cw + 8 * h + 2 * q);
     double2 acc[2][NT];
     LpRing qr, xr;
     for (int p = 0; p < T; ++p) {
@@ -301,12 +335,12 @@ __global__ void __launch_bounds__(lp::NTH, 1)
         lp_waits(qf_s + 8 * qr.i, qr.ph);
         lp_waits(xf_s + 8 * xr.i, xr.ph);
         LP_TS();
-        const uint32_t xsl = xs_s + xr.i * (SLOT * 8);
+        const uint32_t xsl = xs_s + xr.i * Cf::SLOTB;
         const uint32_t Qs = qs_s + qr.i * (Cf::QSTAGE * 8);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const double2 a0 = lp_lds2s(xsl + 8 * xo[0][h]);
-          const double2 a1 = lp_lds2s(xsl + 8 * xo[1][h]);
+          const double2 a0 = LE::ld2(xsl + (int)sizeof(E) * xo[0][h]);
+          const double2 a1 = LE::ld2(xsl + (int)sizeof(E) * xo[1][h]);
 #pragma unroll
           for (int t = 0; t < NT; ++t) {
             const int j = 8 * t + g;
@@ -368,8 +402,8 @@ __global__ void __launch_bounds__(lp::NTH, 1)
             const double vy = acc[r][t].y + LP_S(1, r, t, 1);
             const int j = 8 * t + 2 * q;
             if (row < n) {
-              if (j < bp) L[row * ldl + k0 + j] = vx;
-              if (j + 1 < bp) L[row * ldl + k0 + j + 1] = vy;
+              if (j < bp) L[row * ldl + k0 + j] = (E)vx;
+              if (j + 1 < bp) L[row * ldl + k0 + j + 1] = (E)vy;
             }
             ss += vx * vx + vy * vy;
             if (resid) {   // -P for the update pass, in scratch slot 0 (read only by this warp)
@@ -401,19 +435,19 @@ __global__ void __launch_bounds__(lp::NTH, 1)
         // its two 8-column halves; padding rows / columns were zero-filled by TMA, so they
         // add nothing to the norms
         const bool v0 = r0 + pg < n, v1 = r0 + 8 + pg < n;
-        double* xp = Xr + (r0 + pg) * ldx + 16 * cw + 2 * q;
+        E* xp = Xr + (r0 + pg) * ldx + 16 * cw + 2 * q;
         const int64_t l8 = 8 * ldx;
         for (int c = 0; c < nc; ++c) {
           lp_waits(qf_s + 8 * qr.i, qr.ph);
           lp_waits(xf_s + 8 * xr.i, xr.ph);
           LP_TS();
-          const uint32_t xsl = xs_s + xr.i * (SLOT * 8);
+          const uint32_t xsl = xs_s + xr.i * Cf::SLOTB;
           const uint32_t Qs = qs_s + qr.i * (Cf::QSTAGE * 8);
           double2 xv[2][2];
 #pragma unroll
           for (int r = 0; r < 2; ++r)
 #pragma unroll
-            for (int h = 0; h < 2; ++h) xv[r][h] = lp_lds2s(xsl + 8 * xo[r][h]);
+            for (int h = 0; h < 2; ++h) xv[r][h] = LE::ld2(xsl + (int)sizeof(E) * xo[r][h]);
           // B fragments from the pair image: (Q(j0, col), Q(j0 + 1, col)), j0 = 8t + 2q, in
           // one 16-byte load, one t ahead; the four accumulator chains interleaved in issue
           // order (volatile: ptxas would otherwise run them two at a time)
@@ -443,27 +477,30 @@ __global__ void __launch_bounds__(lp::NTH, 1)
           release(xr.i, qr.i);
           xr.next(NS);
           qr.next(NQ);
-          double* xc = xp + c * KC;
+          E* xc = xp + c * KC;
           if (c * KC + KC <= d) {
             if (v0) {
-              __stcs(reinterpret_cast<double2*>(xc), xv[0][0]);
-              __stcs(reinterpret_cast<double2*>(xc + 8), xv[0][1]);
+              LE::st2(xc, xv[0][0]);
+              LE::st2(xc + 8, xv[0][1]);
             }
             if (v1) {
-              __stcs(reinterpret_cast<double2*>(xc + l8), xv[1][0]);
-              __stcs(reinterpret_cast<double2*>(xc + l8 + 8), xv[1][1]);
+              LE::st2(xc + l8, xv[1][0]);
+              LE::st2(xc + l8 + 8, xv[1][1]);
             }
           } else {   // ragged last chunk (d even: a column pair is in or out as a whole)
             const int col = c * KC + 16 * cw + 2 * q;
-            if (v0 && col < d) __stcs(reinterpret_cast<double2*>(xc), xv[0][0]);
-            if (v0 && col + 8 < d) __stcs(reinterpret_cast<double2*>(xc + 8), xv[0][1]);
-            if (v1 && col < d) __stcs(reinterpret_cast<double2*>(xc + l8), xv[1][0]);
-            if (v1 && col + 8 < d) __stcs(reinterpret_cast<double2*>(xc + l8 + 8), xv[1][1]);
+            if (v0 && col < d) LE::st2(xc, xv[0][0]);
+            if (v0 && col + 8 < d) LE::st2(xc + 8, xv[0][1]);
+            if (v1 && col < d) LE::st2(xc + l8, xv[1][0]);
+            if (v1 && col + 8 < d) LE::st2(xc + l8 + 8, xv[1][1]);
           }
 #pragma unroll
           for (int r = 0; r < 2; ++r)
 #pragma unroll
-            for (int h = 0; h < 2; ++h) nr[r] += xv[r][h].x * xv[r][h].x + xv[r][h].y * xv[r][h].y;
+            for (int h = 0; h < 2; ++h) {   // norms of the stored (rounded) residual
+              const double2 u = LE::rnd(xv[r][h]);
+              nr[r] += u.x * u.x + u.y * u.y;
+            }
         }
         LP_T(5);
         // d(i) = ||x_res,i||^2: q lanes, then the 4 column groups in order
@@ -538,59 +575,77 @@ static int lp_sms() {
   return v;
 }
 
-int lhat_paper_max_bucket(const void* X, int64_t ldx, int64_t d) {
-  if (d % 2 || d < 16 || ldx % 2 || ((uintptr_t)X % 16)) return 0;
+// TMA: 16-byte aligned base and row stride; fragments read column pairs (d even)
+template <typename E>
+int lhat_paper_max_bucket_t(const void* X, int64_t ldx, int64_t d) {
+  if (d % 2 || d < 16 || (ldx * (int64_t)sizeof(E)) % 16 || ((uintptr_t)X % 16)) return 0;
   int ns, nq, best = 0;
-  if (LpCfg<16>::rings(ns, nq)) best = 16;
-  if (LpCfg<32>::rings(ns, nq)) best = 32;
+  if (LpCfg<16, E>::rings(ns, nq)) best = 16;
+  if (LpCfg<32, E>::rings(ns, nq)) best = 32;
   return best;
 }
+int lhat_paper_max_bucket(const void* X, int64_t ldx, int64_t d) { return lhat_paper_max_bucket_t<double>(X, ldx, d); }
+int lhat_paper_max_bucket_f32(const void* X, int64_t ldx, int64_t d) {
+  return lhat_paper_max_bucket_t<float>(X, ldx, d);
+}
 
-template <int BPB>
-static cudaError_t go_lp(const CUtensorMap& map, const CUtensorMap& map0, int lazy, const double* Qp, double* L,
-                         int64_t ldl, int64_t n, int64_t d, double* dvec, DevState* st, double* Xr, int64_t ldx,
+template <int BPB, typename E>
+static cudaError_t go_lp(const CUtensorMap& map, const CUtensorMap& map0, int lazy, const double* Qp, E* L,
+                         int64_t ldl, int64_t n, int64_t d, double* dvec, DevState* st, E* Xr, int64_t ldx,
                          int resid, cudaStream_t s, int part) {
-  using Cf = LpCfg<BPB>;
+  using Cf = LpCfg<BPB, E>;
   int ns, nq;
   if (!Cf::rings(ns, nq)) return cudaErrorInvalidValue;
   const size_t smem = Cf::smem(ns, nq);
-  cudaFuncSetAttribute(k_lhat_paper<BPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_lhat_paper<BPB, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int nc = (int)((d + lp::KC - 1) / lp::KC);
   long long* tr = nullptr;
   static int traced = 0;
-  if (BPB == 32 && lp_trace_buf() && !traced) {   // first bucket-32 launch only
+  if (BPB == 32 && sizeof(E) == 8 && lp_trace_buf() && !traced) {   // first fp64 bucket-32 launch only
     tr = lp_trace_buf();
     traced = 1;
   }
-  k_lhat_paper<BPB><<<lp_sms(), lp::NTH, smem, s>>>(map, map0, lazy, Qp, L, ldl, n, (int)d, nc, ns, nq, dvec, st,
-                                                     Xr, ldx, resid, tr, part);
+  k_lhat_paper<BPB, E><<<lp_sms(), lp::NTH, smem, s>>>(map, map0, lazy, Qp, L, ldl, n, (int)d, nc, ns, nq, dvec,
+                                                        st, Xr, ldx, resid, tr, part);
   return cudaGetLastError();
 }
 
-cudaError_t launch_lhat_paper(const double* X, int64_t ldx, const double* Qp, double* L, int64_t ldl,
-                              int64_t n, int64_t d, double* dvec, DevState* st, int bucket, bool resid,
-                              cudaStream_t s, const double* X0, int64_t ldx0, int part) {
+template <typename E>
+static cudaError_t launch_lhat_paper_t(const E* X, int64_t ldx, const double* Qp, E* L, int64_t ldl, int64_t n,
+                                       int64_t d, double* dvec, DevState* st, int bucket, bool resid,
+                                       cudaStream_t s, const E* X0, int64_t ldx0, int part) {
   if (n <= 0) return cudaSuccess;
   auto enc = lp_encode();
   if (!enc) return cudaErrorNotSupported;
-  auto make_map = [&](const double* P, int64_t ld, CUtensorMap* map) {
+  auto make_map = [&](const E* P, int64_t ld, CUtensorMap* map) {
     const cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)n};
-    const cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
-    const cuuint32_t box[2] = {16, (cuuint32_t)lp::R};
+    const cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(E)};
+    const cuuint32_t box[2] = {(cuuint32_t)LpE<E>::CPB, (cuuint32_t)lp::R};
     const cuuint32_t estr[2] = {1, 1};
-    return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)P, dims, strides, box, estr,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    return enc(map, sizeof(E) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+               (void*)P, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
   };
   CUtensorMap map, map0;
   if (!make_map(X, ldx, &map)) return cudaErrorInvalidValue;
   const int lazy = X0 != nullptr ? 1 : 0;
   if (!make_map(lazy ? X0 : X, lazy ? ldx0 : ldx, &map0)) return cudaErrorInvalidValue;
   switch (bucket) {
-    case 16: return go_lp<16>(map, map0, lazy, Qp, L, ldl, n, d, dvec, st, (double*)X, ldx, resid ? 1 : 0, s, -1);
-    case 32: return go_lp<32>(map, map0, lazy, Qp, L, ldl, n, d, dvec, st, (double*)X, ldx, resid ? 1 : 0, s, part);
+    case 16: return go_lp<16, E>(map, map0, lazy, Qp, L, ldl, n, d, dvec, st, (E*)X, ldx, resid ? 1 : 0, s, -1);
+    case 32: return go_lp<32, E>(map, map0, lazy, Qp, L, ldl, n, d, dvec, st, (E*)X, ldx, resid ? 1 : 0, s, part);
     default: return cudaErrorInvalidValue;
   }
+}
+
+cudaError_t launch_lhat_paper(const double* X, int64_t ldx, const double* Qp, double* L, int64_t ldl,
+                              int64_t n, int64_t d, double* dvec, DevState* st, int bucket, bool resid,
+                              cudaStream_t s, const double* X0, int64_t ldx0, int part) {
+  return launch_lhat_paper_t<double>(X, ldx, Qp, L, ldl, n, d, dvec, st, bucket, resid, s, X0, ldx0, part);
+}
+cudaError_t launch_lhat_paper(const float* X, int64_t ldx, const double* Qp, float* L, int64_t ldl,
+                              int64_t n, int64_t d, double* dvec, DevState* st, int bucket, bool resid,
+                              cudaStream_t s, const float* X0, int64_t ldx0, int part) {
+  return launch_lhat_paper_t<float>(X, ldx, Qp, L, ldl, n, d, dvec, st, bucket, resid, s, X0, ldx0, part);
 }
 
 // ------------------------------------------------------------------------------------

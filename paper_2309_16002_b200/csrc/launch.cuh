@@ -104,6 +104,7 @@ cudaError_t launch_update_mma(double* Xres, int64_t ldx, const double* Qt, const
 size_t fused_pack_bytes(int64_t d);
 int fused_max_bucket(const void* X, int64_t ldx, int64_t d);
 cudaError_t launch_pack_q(const double* Qt, int64_t d, double* Qp, DevState* st, cudaStream_t s, int part = -1);
+cudaError_t launch_pack_q(const float* Qt, int64_t d, double* Qp, DevState* st, cudaStream_t s, int part = -1);
 cudaError_t launch_proj_fused(double* Xres, int64_t ldx, const double* Qp, double* L, int64_t ldl,
                               int64_t n, int64_t d, double* dvec, DevState* st, int bucket, bool paper,
                               cudaStream_t s);
@@ -113,6 +114,11 @@ int lhat_paper_max_bucket(const void* X, int64_t ldx, int64_t d);
 cudaError_t launch_lhat_paper(const double* X, int64_t ldx, const double* Qp, double* L, int64_t ldl,
                               int64_t n, int64_t d, double* dvec, DevState* st, int bucket, bool resid,
                               cudaStream_t s, const double* X0 = nullptr, int64_t ldx0 = 0, int part = -1);
+// fp32 storage (X, X_res, L), fp64 DMMA arithmetic, fp64 norms (R19)
+cudaError_t launch_lhat_paper(const float* X, int64_t ldx, const double* Qp, float* L, int64_t ldl,
+                              int64_t n, int64_t d, double* dvec, DevState* st, int bucket, bool resid,
+                              cudaStream_t s, const float* X0 = nullptr, int64_t ldx0 = 0, int part = -1);
+int lhat_paper_max_bucket_f32(const void* X, int64_t ldx, int64_t d);
 // resid: + the update pass (residual form, L2 re-read).  X0 (lazy X_res): in block 1 the
 // tile is read from X0 (the input) and the update is written to X (X_res)
 

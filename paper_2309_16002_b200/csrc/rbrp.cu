@@ -154,6 +154,10 @@ bool env_on(const char* name) {
 // RBRP_FORCE_SIMT=1: CUDA-core projection kernels instead of DMMA.  RBRP_NO_GRAPH=1: eager
 // block loop.  RBRP_DEBUG_STAMPS=1: print the filter phase stamps of every block (eager).
 bool force_simt() { return env_on("RBRP_FORCE_SIMT"); }
+template <typename T>
+int lp_max_bucket(const void* X, int64_t ldx, int64_t d) {
+  return sizeof(T) == 8 ? lhat_paper_max_bucket(X, ldx, d) : lhat_paper_max_bucket_f32(X, ldx, d);
+}
 
 // per-phase CUDA events on the caller's stream (report.profile, eager loop only)
 struct Prof {
@@ -277,16 +281,18 @@ void make_ctx(Ctx<T>& c, const rbrp_problem* p, void* Xv, char* ws, const Layout
   c.fused_max = (c.use_mma && !env_on("RBRP_NO_FUSED")) ? fused_max_bucket(c.Xres, c.ldr, c.d) : 0;
   // residual form: the 64-row tiled kernel (L-hat pass + update pass re-reading the tile
   // through L2) by default; RBRP_FUSED16=1 selects the 16-row smem-resident k_proj_fused
-  c.tiled = !c.paper && c.use_mma && !env_on("RBRP_FUSED16");
-  c.lp_max = ((c.paper || c.tiled) && c.use_mma && !env_on("RBRP_NO_FUSED")) ? lhat_paper_max_bucket(c.Xres, c.ldr, c.d)
-                                                                            : 0;
+  // fp32: the same kernel with fp32 storage and fp64 DMMA arithmetic (R19);
+  // RBRP_FP32_SIMT=1 keeps the CUDA-core fp32 kernels
+  const bool lp_ok = sizeof(T) == 8 ? c.use_mma : (!force_simt() && !env_on("RBRP_FP32_SIMT"));
+  c.tiled = !c.paper && lp_ok && (sizeof(T) == 4 || !env_on("RBRP_FUSED16"));
+  c.lp_max = ((c.paper || c.tiled) && lp_ok && !env_on("RBRP_NO_FUSED")) ? lp_max_bucket<T>(c.Xres, c.ldr, c.d) : 0;
   // the tiled kernel handles every bucket of this problem, so it can take block 1 straight
   // from X (X_res is then never copied: one HBM read + write less per ID).  Single-GPU
   // path only (run_dist keeps the copy).
   // (b' > 32 runs as 32-column parts on the same kernel, enqueue_projection)
   const int lp_need = c.bucketB > 32 && !env_on("RBRP_NO_PARTS") ? 32 : c.bucketB;
   c.lazy = c.tiled && !inplace && c.Xres != c.X && c.lp_max >= lp_need && c.lp_max > 0 &&
-           lhat_paper_max_bucket(c.X, p->ld, c.d) >= lp_need && !comm && !env_on("RBRP_EAGER_COPY");
+           lp_max_bucket<T>(c.X, p->ld, c.d) >= lp_need && !comm && !env_on("RBRP_EAGER_COPY");
 }
 
 template <typename T>
@@ -340,7 +346,7 @@ int enqueue_projection(Ctx<T>& c, cudaStream_t s, int* nl) {
   int rc = RBRP_OK;
   // the single-pass kernel: k_proj_fused (residual form) or k_lhat_paper (paper form)
   const int fmax = (c.paper || c.tiled) ? c.lp_max : c.fused_max;
-  if (fmax > 0 && (rc = lk(launch_pack_q((const double*)c.Qt, c.d, c.Qp, c.st, s)))) return rc;
+  if (fmax > 0 && (rc = lk(launch_pack_q(c.Qt, c.d, c.Qp, c.st, s)))) return rc;
   bool need_downdate = false;
   // b' > 32 on the 64-row-tile kernel: 32-column parts in sequence (RBRP_NO_PARTS=1: the
   // two-kernel path instead)
@@ -349,9 +355,8 @@ int enqueue_projection(Ctx<T>& c, cudaStream_t s, int* nl) {
     if (bk > 32 && parts) continue;
     if (bk <= fmax) {
       if (c.paper || c.tiled)
-        rc = lk(launch_lhat_paper((const double*)c.Xres, c.ldr, c.Qp, (double*)c.Lm, c.k_cap, c.n, c.d,
-                                  c.dvec, c.st, bk, !c.paper, s, c.lazy ? (const double*)c.X : nullptr,
-                                  c.p->ld));
+        rc = lk(launch_lhat_paper((const T*)c.Xres, c.ldr, c.Qp, c.Lm, c.k_cap, c.n, c.d, c.dvec, c.st, bk,
+                                  !c.paper, s, c.lazy ? (const T*)c.X : nullptr, c.p->ld));
       else
         rc = lk(launch_proj_fused((double*)c.Xres, c.ldr, c.Qp, (double*)c.Lm, c.k_cap, c.n, c.d, c.dvec,
                                   c.st, bk, false, s));
@@ -371,9 +376,9 @@ int enqueue_projection(Ctx<T>& c, cudaStream_t s, int* nl) {
     if (rc) return rc;
   }
   for (int part = 0; parts && part < c.bucketB / 32; ++part) {
-    if ((rc = lk(launch_pack_q((const double*)c.Qt, c.d, c.Qp, c.st, s, part)))) return rc;
-    if ((rc = lk(launch_lhat_paper((const double*)c.Xres, c.ldr, c.Qp, (double*)c.Lm, c.k_cap, c.n, c.d, c.dvec,
-                                   c.st, 32, !c.paper, s, c.lazy ? (const double*)c.X : nullptr, c.p->ld, part))))
+    if ((rc = lk(launch_pack_q(c.Qt, c.d, c.Qp, c.st, s, part)))) return rc;
+    if ((rc = lk(launch_lhat_paper((const T*)c.Xres, c.ldr, c.Qp, c.Lm, c.k_cap, c.n, c.d, c.dvec, c.st, 32,
+                                   !c.paper, s, c.lazy ? (const T*)c.X : nullptr, c.p->ld, part))))
       return rc;
   }
   // paper form on the two-kernel path: l.16 downdate from the L-hat columns (the kernel
