@@ -679,7 +679,7 @@ bool gemm_lp_supported(const double* A, int64_t lda, const double* B, int64_t ld
 }
 
 cudaError_t gemm_nt_lp(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
-                       int64_t M, int64_t N, int64_t K, void* scratch, cudaStream_t s) {
+                       int64_t M, int64_t N, int64_t K, void* scratch, cudaStream_t s, bool lower_b) {
   if (M <= 0 || N <= 0) return cudaSuccess;
   if (!gemm_lp_supported(A, lda, B, ldb, K)) return cudaErrorNotSupported;
   double* Qp = (double*)scratch;
@@ -689,8 +689,10 @@ cudaError_t gemm_nt_lp(const double* A, int64_t lda, const double* B, int64_t ld
   cudaError_t e = cudaGetLastError();
   for (int64_t g = 0; g < G && e == cudaSuccess; ++g) {
     const int bg = (int)(N - 32 * g < 32 ? N - 32 * g : 32);
-    e = launch_pack_q(B + 32 * g * ldb, K, Qp, st + g, s);
-    if (e == cudaSuccess) e = launch_lhat_paper(A, lda, Qp, C, ldc, M, K, nullptr, st + g, bucket_of(bg), false, s);
+    const int64_t k0 = lower_b ? (32 * g / lp::KC) * lp::KC : 0;   // B(rows of g, m < k0) = 0
+    e = launch_pack_q(B + 32 * g * ldb + k0, K - k0, Qp, st + g, s, -1, ldb);
+    if (e == cudaSuccess)
+      e = launch_lhat_paper(A + k0, lda, Qp, C, ldc, M, K - k0, nullptr, st + g, bucket_of(bg), false, s);
   }
   return e;
 }

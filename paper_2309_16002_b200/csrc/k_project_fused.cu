@@ -139,7 +139,7 @@ __device__ __forceinline__ int pi_row(int g) { return (g >> 1) + 4 * (g & 1); }
 // launch_lhat_paper): rows [32 part, min(b', 32 part + 32)).
 template <typename QT>
 __global__ void k_pack_q(const QT* __restrict__ Qt, int64_t d, double* __restrict__ Qp,
-                         const DevState* st, int part) {
+                         const DevState* st, int part, int64_t ldq) {
   if (st->stop) return;
   const int bpa = st->b_prime;
   int bp, r0 = 0;
@@ -153,7 +153,7 @@ __global__ void k_pack_q(const QT* __restrict__ Qt, int64_t d, double* __restric
   }
   const int c = blockIdx.x, j = blockIdx.y, col = threadIdx.x;   // blockDim = KC
   const int64_t gc = (int64_t)c * fz::KC + col;
-  const double v = (j < bp && gc < d) ? (double)Qt[(int64_t)(r0 + j) * d + gc] : 0.0;
+  const double v = (j < bp && gc < d) ? (double)Qt[(int64_t)(r0 + j) * ldq + gc] : 0.0;
   Qp[((int64_t)c * fz::PACK_ROWS + j) * fz::KC + qswz(j, col)] = v;
   // second image (update pass of k_lhat_paper): rows in pairs, (Q(2p, col), Q(2p+1, col))
   // adjacent, 16-byte unit of pair p and column col at p * KC + (col ^ 2 (p & 3))
@@ -692,15 +692,17 @@ static cudaError_t go_fused(const CUtensorMap& map, double* X, int64_t ldx, cons
   return cudaGetLastError();
 }
 
-cudaError_t launch_pack_q(const float* Qt, int64_t d, double* Qp, DevState* st, cudaStream_t s, int part) {
+cudaError_t launch_pack_q(const float* Qt, int64_t d, double* Qp, DevState* st, cudaStream_t s, int part,
+                          int64_t ldq) {
   dim3 grid((unsigned)fz_nc(d), fz::PACK_ROWS);
-  k_pack_q<float><<<grid, fz::KC, 0, s>>>(Qt, d, Qp, st, part);
+  k_pack_q<float><<<grid, fz::KC, 0, s>>>(Qt, d, Qp, st, part, ldq > 0 ? ldq : d);
   return cudaGetLastError();
 }
 
-cudaError_t launch_pack_q(const double* Qt, int64_t d, double* Qp, DevState* st, cudaStream_t s, int part) {
+cudaError_t launch_pack_q(const double* Qt, int64_t d, double* Qp, DevState* st, cudaStream_t s, int part,
+                          int64_t ldq) {
   dim3 grid((unsigned)fz_nc(d), fz::PACK_ROWS);
-  k_pack_q<double><<<grid, fz::KC, 0, s>>>(Qt, d, Qp, st, part);
+  k_pack_q<double><<<grid, fz::KC, 0, s>>>(Qt, d, Qp, st, part, ldq > 0 ? ldq : d);
   return cudaGetLastError();
 }
 

@@ -103,8 +103,11 @@ cudaError_t launch_update_mma(double* Xres, int64_t ldx, const double* Qt, const
 // k_project_fused.cu — single-pass fused projection (L-hat, update, norms), b' <= 64
 size_t fused_pack_bytes(int64_t d);
 int fused_max_bucket(const void* X, int64_t ldx, int64_t d);
-cudaError_t launch_pack_q(const double* Qt, int64_t d, double* Qp, DevState* st, cudaStream_t s, int part = -1);
-cudaError_t launch_pack_q(const float* Qt, int64_t d, double* Qp, DevState* st, cudaStream_t s, int part = -1);
+// Qt: rows of Q_b (leading dimension ldq, 0 -> d), d columns packed
+cudaError_t launch_pack_q(const double* Qt, int64_t d, double* Qp, DevState* st, cudaStream_t s, int part = -1,
+                          int64_t ldq = 0);
+cudaError_t launch_pack_q(const float* Qt, int64_t d, double* Qp, DevState* st, cudaStream_t s, int part = -1,
+                          int64_t ldq = 0);
 cudaError_t launch_proj_fused(double* Xres, int64_t ldx, const double* Qp, double* L, int64_t ldl,
                               int64_t n, int64_t d, double* dvec, DevState* st, int bucket, bool paper,
                               cudaStream_t s);
@@ -141,8 +144,10 @@ bool gemm_nt_mma(const double* A, int64_t lda, const double* B, int64_t ldb, dou
 // scratch >= gemm_lp_scratch_bytes(N, K), 256-byte aligned
 size_t gemm_lp_scratch_bytes(int64_t N, int64_t K);
 bool gemm_lp_supported(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t K);
+// lower_b: B(j, m) = 0 for m < j (B = L_1^{-T} of W): each 32-column group starts its K
+// range at the 64-column chunk holding its first nonzero (about half the work)
 cudaError_t gemm_nt_lp(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
-                       int64_t M, int64_t N, int64_t K, void* scratch, cudaStream_t s);
+                       int64_t M, int64_t N, int64_t K, void* scratch, cudaStream_t s, bool lower_b = false);
 
 // k_formw.cu — Alg. 3 by triangular solve
 template <typename T>

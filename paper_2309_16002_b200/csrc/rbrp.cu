@@ -719,7 +719,7 @@ int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* 
     if (sizeof(T) == 8 && !force_simt() && kp <= k_cap && c.Wsc && !env_on("RBRP_W_NTMMA") &&
         gemm_lp_supported((const double*)c.Lm, k_cap, (const double*)LinvT, kp, kp)) {
       CK(gemm_nt_lp((const double*)c.Lm, k_cap, (const double*)LinvT, kp, (double*)W_out, k_cap, c.n, k, kp,
-                    c.Wsc, s));
+                    c.Wsc, s, true));
       nl += 2 * (int)((k + 31) / 32);
     } else if (sizeof(T) == 8 && !force_simt() && kp <= k_cap &&
                gemm_nt_mma((const double*)c.Lm, k_cap, (const double*)LinvT, kp, (double*)W_out, k_cap, c.n, k,
@@ -1012,7 +1012,7 @@ int run_dist(int nsh, const rbrp_problem* ps, void* const* Xs, char* const* wss,
       if (sizeof(T) == 8 && !force_simt() && kp <= k_cap && c.Wsc && !env_on("RBRP_W_NTMMA") &&
           gemm_lp_supported((const double*)c.Lm, k_cap, (const double*)c.LinvT, kp, kp)) {
         CK(gemm_nt_lp((const double*)c.Lm, k_cap, (const double*)c.LinvT, kp, (double*)W_outs[h], k_cap, c.n, k,
-                      kp, c.Wsc, s));
+                      kp, c.Wsc, s, true));
         nl += 2 * (int)((k + 31) / 32);
       } else if (sizeof(T) == 8 && !force_simt() && kp <= k_cap &&
                  gemm_nt_mma((const double*)c.Lm, k_cap, (const double*)c.LinvT, kp, (double*)W_outs[h], k_cap,
