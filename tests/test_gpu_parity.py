@@ -124,11 +124,20 @@ def test_replay_parity_fp64(name, kw):
 
 
 @cuda
-def test_replay_parity_fp32_c4_small():
-    cfg = small_config("c4", n=20000, d=192, b=16)
+@pytest.mark.parametrize("b", [16, 64])
+def test_replay_parity_fp32_c4_small(monkeypatch, b):
+    """fp32 (c4-like): the default projection (fp32 storage, fp64 DMMA arithmetic, reading
+    R19; b' > 32 in parts) and the CUDA-core fp32 kernels (RBRP_FP32_SIMT=1) both match the
+    oracle's fp32 run in replay: S and b' exact, rho_t within the fp32 tolerance."""
+    cfg = small_config("c4", n=20000, d=192, b=b)
     Xnp = make(cfg).numpy()
-    ores = O.rbrp(Xnp, tau=1e-3, b=16, seed=0)
-    _replay(Xnp, ores, np.float32, 16)
+    ores = O.rbrp(Xnp, tau=1e-3, b=b, seed=0)
+    monkeypatch.setenv("RBRP_FP32_SIMT", "0")
+    a = _replay(Xnp, ores, np.float32, b)
+    monkeypatch.setenv("RBRP_FP32_SIMT", "1")
+    s = _replay(Xnp, ores, np.float32, b)
+    monkeypatch.setenv("RBRP_FP32_SIMT", "0")
+    assert a.S.tolist() == s.S.tolist() and a.b_prime == s.b_prime
 
 
 @cuda
@@ -339,14 +348,16 @@ def test_fused_projection_matches_two_kernel_path(monkeypatch, n, d, rank, b):
     Xnp = make(cfg).numpy()
     ores = O.rbrp(Xnp, tau=1e-12, b=b, seed=0)
     runs = {}
-    for name, env in (("two_kernel", {"RBRP_NO_FUSED": "1", "RBRP_FUSED16": "0"}),
-                      ("fused16", {"RBRP_NO_FUSED": "0", "RBRP_FUSED16": "1"}),
-                      ("tiled", {"RBRP_NO_FUSED": "0", "RBRP_FUSED16": "0"})):
+    for name, env in (("two_kernel", {"RBRP_NO_FUSED": "1", "RBRP_FUSED16": "0", "RBRP_NO_PARTS": "0"}),
+                      ("fused16", {"RBRP_NO_FUSED": "0", "RBRP_FUSED16": "1", "RBRP_NO_PARTS": "0"}),
+                      ("tiled", {"RBRP_NO_FUSED": "0", "RBRP_FUSED16": "0", "RBRP_NO_PARTS": "0"}),
+                      ("tiled_no_parts", {"RBRP_NO_FUSED": "0", "RBRP_FUSED16": "0", "RBRP_NO_PARTS": "1"})):
         for k_, v in env.items():
             monkeypatch.setenv(k_, v)
         runs[name] = _replay(Xnp, ores, np.float64, b)
+    monkeypatch.setenv("RBRP_NO_PARTS", "0")
     a = runs["two_kernel"]
-    for f in (runs["fused16"], runs["tiled"]):
+    for f in (runs["fused16"], runs["tiled"], runs["tiled_no_parts"]):
         assert a.S.tolist() == f.S.tolist() and a.b_prime == f.b_prime
         assert max(abs(x - y) for x, y in zip(a.rho, f.rho)) <= 1e-10
     # same seed, sampling path (default kernel): reproducible bit for bit
