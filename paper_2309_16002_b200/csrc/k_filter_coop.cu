@@ -231,6 +231,97 @@ __device__ int cta_chol_inv(const double* __restrict__ Gg, int nb, int mode, con
   return kept;
 }
 
+// 64 < nb <= kMaxB = 128, blockDim = 256: cta_pivchol with the Schur complement in
+// registers (thread t: column c = t & 127, rows 64 (t >> 7) .. +64) and its diagonal
+// mirrored in registers of every warp (entries lane + 32 m).  The update a -= R(i,r) R(i,c)
+// runs over every element: for a chosen row or column one factor is exactly zero (or the
+// element is never read again), so the kept entries equal cta_pivchol's bit for bit; the
+// row loads are warp-uniform broadcasts.  One barrier per step, no memory traffic.
+__device__ int cta_pivchol_reg(const double* __restrict__ Gg, int nb, int mode, const int32_t* forced,
+                               double tau_b, double* R, int ldr, int* perm, double* mass, int* rank_def) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int c = tid & 127, r0 = 64 * (tid >> 7);
+  double a[64];
+#pragma unroll
+  for (int k = 0; k < 64; ++k) a[k] = (r0 + k < nb && c < nb) ? Gg[(r0 + k) * kMaxB + c] : 0.0;
+  double dgv[4];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const int l = lane + 32 * m;
+    dgv[m] = l < nb ? Gg[l * kMaxB + l] : 0.0;
+  }
+  if (tid == 0) *rank_def = 0;
+  unsigned long long ch0 = 0ull, ch1 = 0ull;   // chosen columns (identical in every thread)
+  auto chosen = [&](int l) { return ((l < 64 ? ch0 >> l : ch1 >> (l - 64)) & 1ull) != 0ull; };
+  double thr = 0.0;
+  int kept = nb;
+  for (int i = 0; i < nb; ++i) {
+    double ms = 0.0, best = -DBL_MAX;
+    int bl = 1 << 30;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int l = lane + 32 * m;
+      if (l < nb && !chosen(l)) {
+        const double x = dgv[m];
+        ms += fmax(x, 0.0);
+        if (x > best) { best = x; bl = l; }
+      }
+    }
+    ms = warp_sum(ms);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+      if (ob > best || (ob == best && ol < bl)) { best = ob; bl = ol; }
+    }
+    int cut = 0;
+    if (mode == 1) {
+      if (tid == 0) mass[i] = ms;
+      if (i == 0) thr = tau_b * ms;
+      if (!(ms > 0.0) || ms < thr) cut = 1;                        // l.8 cut
+    }
+    int p = bl;
+    if (mode == 2) p = i;
+    if (mode == 1 && forced) p = forced[i];
+    const double q0 = __shfl_sync(0xffffffffu, dgv[0], p & 31), q1 = __shfl_sync(0xffffffffu, dgv[1], p & 31);
+    const double q2 = __shfl_sync(0xffffffffu, dgv[2], p & 31), q3 = __shfl_sync(0xffffffffu, dgv[3], p & 31);
+    const int pm = (p >> 5) & 3;
+    const double dp = pm == 0 ? q0 : (pm == 1 ? q1 : (pm == 2 ? q2 : q3));
+    if (!cut && !(dp > 0.0)) cut = 2;                               // non-positive pivot
+    if (cut) {
+      if (tid == 0 && cut == 2) *rank_def = 1;
+      kept = i;
+      break;
+    }
+    if (tid == 0) perm[i] = p;
+    const double rii = sqrt(dp);
+    if ((p >> 6) == (tid >> 7)) {   // this thread holds A(p, c)
+      double v = 0.0;
+#pragma unroll
+      for (int k = 0; k < 64; ++k)
+        if (r0 + k == p) v = a[k];
+      R[i * ldr + c] = c >= nb ? 0.0 : ((c == p) ? rii : (chosen(c) ? 0.0 : v / rii));
+    }
+    if (p < 64) ch0 |= 1ull << p;
+    else ch1 |= 1ull << (p - 64);
+    __syncthreads();   // row i of R complete; step i+1 writes row i+1
+    const double* Ri = R + i * ldr;
+    const double rc = Ri[c];
+#pragma unroll
+    for (int k = 0; k < 64; ++k) a[k] = fma(-Ri[r0 + k], rc, a[k]);
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int l = lane + 32 * m;
+      if (l < nb && l != p) {
+        const double rl = Ri[l];
+        if (rl != 0.0) dgv[m] = fma(-rl, rl, dgv[m]);
+      }
+    }
+  }
+  __syncthreads();
+  return kept;
+}
+
 // small dense helpers on n x n shared-memory matrices (stride ld), all threads
 __device__ void sm_upper_phi(const double* M, double* U, int n, int ld) {   // U = Phi(M)
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
@@ -299,23 +390,42 @@ __device__ void cholqr2_perturb(double* E, double* R, double* Tm, double* W, int
   __syncthreads();
 }
 
-// T = R11^{-1} for the upper-triangular R11(j, c) = R(j, perm[c]) (step order), one
-// thread per column c: T(c,c) = 1/R11(c,c); T(j,c) = -(sum_{j<q<=c} R11(j,q) T(q,c)) / R11(j,j).
-__device__ void cta_trinv(const double* R, int ldr, const int* perm, int bp, double* Tm, int ldt) {
-  for (int c = threadIdx.x; c < bp; c += blockDim.x) {
-    const int pc = perm[c];
-    Tm[c * ldt + c] = 1.0 / R[c * ldr + pc];
-    for (int j = c - 1; j >= 0; --j) {
-      double t0 = 0.0, t1 = 0.0;
-      int q = j + 1;
-      for (; q + 1 <= c; q += 2) {
-        t0 = fma(R[j * ldr + perm[q]], Tm[q * ldt + c], t0);
-        t1 = fma(R[j * ldr + perm[q + 1]], Tm[(q + 1) * ldt + c], t1);
+// T = R11^{-1} (bp <= 128), one warp per column c of T: back substitution in column form,
+// R11 x = e_c from q = c down to 0, x_q = (delta_qc - s_q) / R11(q,q) by its owner lane
+// (rows lane + 32 m in registers), broadcast by one shuffle, then s_j += R11(j,q) x_q for
+// j < q.  R11(j, q) = R(j, perm[q]) in shared memory; T written once per column.
+__device__ void cta_trinv_warp(const double* R, int ldr, const int* perm, int bp, double* Tm, int ldt) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __shared__ double rinv[kMaxB];   // 1 / R11(q, q), off the dependent chain
+  for (int q = threadIdx.x; q < bp; q += blockDim.x) rinv[q] = 1.0 / R[q * ldr + perm[q]];
+  __syncthreads();
+  for (int c = w; c < bp; c += nw) {
+    double sacc[4] = {0.0, 0.0, 0.0, 0.0}, xr[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int q = c; q >= 0; --q) {
+      const int pq = perm[q], mq = q >> 5;
+      double xq = 0.0;
+      if (lane == (q & 31)) {
+        double sq = sacc[0];
+#pragma unroll
+        for (int m = 1; m < 4; ++m)
+          if (m == mq) sq = sacc[m];
+        xq = ((q == c ? 1.0 : 0.0) - sq) * rinv[q];
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+          if (m == mq) xr[m] = xq;
       }
-      if (q <= c) t0 = fma(R[j * ldr + perm[q]], Tm[q * ldt + c], t0);
-      Tm[j * ldt + c] = -(t0 + t1) / R[j * ldr + perm[j]];
+      xq = __shfl_sync(0xffffffffu, xq, q & 31);
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const int j = lane + 32 * m;
+        if (j < q) sacc[m] = fma(R[j * ldr + pq], xq, sacc[m]);
+      }
     }
-    for (int j = c + 1; j < bp; ++j) Tm[j * ldt + c] = 0.0;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int j = lane + 32 * m;
+      if (j < bp) Tm[j * ldt + c] = j <= c ? xr[m] : 0.0;
+    }
   }
   __syncthreads();
 }
@@ -387,7 +497,7 @@ __global__ void __launch_bounds__(kFiltThreads, 1) k_filter_coop(FilterArgs F) {
   __shared__ int s_nb, s_stop, s_kept, s_rd;
   __shared__ long long s_k;
   DevState* st = F.st;
-  const int tid = threadIdx.x, w = tid >> 5;
+  const int tid = threadIdx.x;
   __shared__ int s_first;
   if (tid == 0) {
     s_stop = st->stop;
@@ -452,11 +562,10 @@ __global__ void __launch_bounds__(kFiltThreads, 1) k_filter_coop(FilterArgs F) {
     } else if (small) {
       kept = cta_chol_inv<16>(F.G, nb, 1, F.forced, tb, Rs, ldr, Ts, ldt, perm, s_mass, s_dg, s_ch, &s_rd);
     } else {
-      for (int e = tid; e < nb * nb; e += kFiltThreads) Gs[(e / nb) * ldg + e % nb] = F.G[(e / nb) * kMaxB + e % nb];
+      kept = cta_pivchol_reg(F.G, nb, 1, F.forced, tb, Rs, ldr, perm, s_mass, &s_rd);
       __syncthreads();
-      kept = cta_pivchol(Gs, ldg, nb, 1, F.forced, tb, Rs, ldr, perm, s_mass, s_dg, s_ch, &s_rd);
-      __syncthreads();
-      cta_trinv(Rs, ldr, perm, kept, Ts, ldt);
+      stamp(F.dbg, 10);
+      cta_trinv_warp(Rs, ldr, perm, kept, Ts, ldt);
     }
     if (tid == 0) s_kept = kept;
   }
@@ -501,7 +610,7 @@ __global__ void __launch_bounds__(kFiltThreads, 1) k_filter_coop(FilterArgs F) {
   // F: CholQR2 pass (R2 into Rs, T2 = R2^{-1} into Ts).  G2 = I + E: if max|E| is small
   // (the usual case) a parallel perturbation expansion, else the exact Cholesky.
   __shared__ double s_emax;
-  if (small) {
+  {
     double em = 0.0;
     for (int e = tid; e < bp * bp; e += kFiltThreads) {
       const int i = e / bp, j = e - (e / bp) * bp;
@@ -519,6 +628,18 @@ __global__ void __launch_bounds__(kFiltThreads, 1) k_filter_coop(FilterArgs F) {
   if (small && bp * s_emax < 1e-4) {
     cholqr2_perturb(Gs, Rs, Ts, Vs, bp, ldr, bp * s_emax);
     if (tid == 0) s_kept = bp;
+  } else if (!small && bp * s_emax < 3e-9) {
+    // large block, eta^2 < 1e-17: cholqr2_perturb with no fixed-point step and one series
+    // term, elementwise: U = Phi(E), R2 = I + U, T2 = I - U
+    for (int e = tid; e < bp * bp; e += kFiltThreads) {
+      const int i = e / bp, j = e - (e / bp) * bp;
+      const double x = Gs[i * ldg + j];
+      const double u = i < j ? x : (i == j ? 0.5 * x : 0.0), id = (i == j ? 1.0 : 0.0);
+      Ts[i * ldt + j] = id - u;
+      Rs[i * ldr + j] = id + u;
+    }
+    __syncthreads();
+    if (tid == 0) s_kept = bp;
   } else {
     int rd2, kept;
     if (bp <= 32) {
@@ -530,7 +651,7 @@ __global__ void __launch_bounds__(kFiltThreads, 1) k_filter_coop(FilterArgs F) {
       __syncthreads();
       kept = cta_pivchol(Gs, ldg, bp, 2, nullptr, 0.0, Rs, ldr, perm2, nullptr, s_dg, s_ch, &rd2);
       __syncthreads();
-      cta_trinv(Rs, ldr, perm2, kept, Ts, ldt);
+      cta_trinv_warp(Rs, ldr, perm2, kept, Ts, ldt);
     }
     if (tid == 0) s_kept = kept;
   }

@@ -677,10 +677,10 @@ int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* 
       CK(cudaMemcpyAsync(hst, c.st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
       if (stamps) {
-        long long t[10];
+        long long t[11];
         if (cudaMemcpy(t, c.dbg, sizeof(t), cudaMemcpyDeviceToHost) == cudaSuccess) {
           fprintf(stderr, "rbrp filter phases (us):");
-          for (int i = 1; i < 10; ++i) fprintf(stderr, " %.2f", (t[i] - t[0]) * 1e-3);
+          for (int i = 1; i < 11; ++i) fprintf(stderr, " %.2f", (t[i] - t[0]) * 1e-3);
           fprintf(stderr, "\n");
         }
       }
