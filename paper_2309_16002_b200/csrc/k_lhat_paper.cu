@@ -158,7 +158,7 @@ struct LpCfg {
            (2 * ns + 2 * nq) * 8 + 1024;
   }
   static bool rings(int& ns, int& nq) {
-    ns = 4;
+    ns = BPB <= 16 ? 5 : 4;   // the small-b' pass is HBM-bound: one X slot more in flight
     nq = 4;
     if (const char* e = getenv("RBRP_LP_NS")) ns = atoi(e);   // experiments only
     if (const char* e = getenv("RBRP_LP_NQ")) nq = atoi(e);
