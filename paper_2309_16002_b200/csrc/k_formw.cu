@@ -149,7 +149,12 @@ cudaError_t launch_trinv(const double* L1, int64_t k, T* LinvT, int64_t ldo, Dev
   if (k <= 0) return cudaSuccess;
   if (k <= kTrinvSmallK) {
     const size_t smem = (size_t)(k * k + k + kTrinvSmallWarps * k) * sizeof(double);
-    cudaFuncSetAttribute(k_trinv_small<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    static bool attr = false;   // once, for the largest k of this path
+    if (!attr) {
+      const size_t mx = (size_t)(kTrinvSmallK * kTrinvSmallK + kTrinvSmallK + kTrinvSmallWarps * kTrinvSmallK) * 8;
+      cudaFuncSetAttribute(k_trinv_small<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
+      attr = true;
+    }
     k_trinv_small<T><<<ceil_div(k, kTrinvSmallWarps), 32 * kTrinvSmallWarps, smem, s>>>(L1, k, LinvT, ldo, st);
     return cudaGetLastError();
   }

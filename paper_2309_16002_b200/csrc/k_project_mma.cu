@@ -384,7 +384,11 @@ bool gemm_nt_mma(const double* A, int64_t lda, const double* B, int64_t ldb, dou
   if (!mma_ok(A, lda, K) || !mma_ok(B, ldb, K)) return false;
   dim3 grid((unsigned)num_sms(), 1);
   using Cf = PCfg<128, 1, 32, false>;
-  cudaFuncSetAttribute(k_nt_mma<128, 1, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_nt_mma<128, 1, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
+    attr = true;
+  }
   k_nt_mma<128, 1, 32><<<grid, 32 * kMmaWarps, Cf::SMEM, s>>>(A, lda, B, ldb, C, ldc, M, N, K, nullptr, 0);
   *err = cudaGetLastError();
   return true;

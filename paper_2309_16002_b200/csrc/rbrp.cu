@@ -18,6 +18,8 @@
 #include <mutex>
 #include <vector>
 
+#include <chrono>
+
 #include "comm.cuh"
 #include "launch.cuh"
 
@@ -154,6 +156,21 @@ bool env_on(const char* name) {
 // RBRP_FORCE_SIMT=1: CUDA-core projection kernels instead of DMMA.  RBRP_NO_GRAPH=1: eager
 // block loop.  RBRP_DEBUG_STAMPS=1: print the filter phase stamps of every block (eager).
 bool force_simt() { return env_on("RBRP_FORCE_SIMT"); }
+// RBRP_HOST_TIMING=1: host microseconds between the marks of one rbrp_id (profiling only)
+struct HostMarks {
+  bool on = env_on("RBRP_HOST_TIMING");
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  char buf[512];
+  int len = 0;
+  void mark(const char* what) {
+    if (!on) return;
+    const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    len += snprintf(buf + len, sizeof(buf) - len, " %s %.1f", what, us);
+  }
+  ~HostMarks() {
+    if (on) fprintf(stderr, "rbrp host us:%s\n", buf);
+  }
+};
 template <typename T>
 int lp_max_bucket(const void* X, int64_t ldx, int64_t d) {
   return sizeof(T) == 8 ? lhat_paper_max_bucket(X, ldx, d) : lhat_paper_max_bucket_f32(X, ldx, d);
@@ -569,8 +586,10 @@ GraphEntry* get_graph(Ctx<T>& c, SampleArgs sa, const GraphKey& key) {
 template <typename T>
 int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* comm,
         cudaStream_t s, int64_t* S_out, void* W_out, rbrp_report* rep) {
+  HostMarks hm;
   Ctx<T> c;
   make_ctx<T>(c, p, Xv, ws, Ly, comm);
+  hm.mark("ctx");
   const bool inplace = (p->flags & RBRP_INPLACE) != 0;
   const bool stamps = env_on("RBRP_DEBUG_STAMPS");
   const int64_t k_cap = c.k_cap;
@@ -604,6 +623,7 @@ int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* 
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
   CK(cudaEventRecord(e0, s));
+  hm.mark("e0");
 
   // a0: d^(0), X_res <- X (Alg. 2 l.1-2)
   prof.begin(0);
@@ -650,19 +670,22 @@ int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* 
   prof.begin(1);
   CK(launch_block_sample(c, sa, s, &nl));
   prof.end();
-  CK(cudaMemcpyAsync(hst, c.st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  if (hst->nonfinite) return RBRP_ENONFINITE;
-  if (!(hst->D0 > 0.0)) return RBRP_EDEGENERATE;
 
   sa.first = 0;
   const bool eager = p->replay_nblocks > 0 || prof.on || stamps || comm || env_on("RBRP_NO_GRAPH");
   GraphEntry* ge = nullptr;
-  if (!eager && !hst->stop) ge = get_graph<T>(c, sa, make_key(p, Xv, ws, c.use_mma));
+  if (!eager) ge = get_graph<T>(c, sa, make_key(p, Xv, ws, c.use_mma));
   if (ge) {
-    // the whole block loop as one graph launch (conditional WHILE node)
+    // the whole block loop as one graph launch (conditional WHILE node), enqueued right
+    // behind a0 and the first sample: no host round trip in between (a non-finite or
+    // all-zero X stops the loop on the device -- the sampler's stop test fails on a NaN
+    // or zero total -- and is reported after it)
     CK(cudaGraphLaunch(ge->exec, s));
   } else {
+    CK(cudaMemcpyAsync(hst, c.st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (hst->nonfinite) return RBRP_ENONFINITE;
+    if (!(hst->D0 > 0.0)) return RBRP_EDEGENERATE;
     int blk = 0;
     while (!hst->stop) {
       int rc = enqueue_block<T>(c, sa, s, prof.on ? &prof : nullptr, &nl, &nproj, false);
@@ -688,8 +711,12 @@ int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* 
   }
 
   // read the state (k, flags) before W
+  hm.mark("loop_enqueued");
   CK(cudaMemcpyAsync(hst, c.st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  hm.mark("loop_done");
+  if (hst->nonfinite) return RBRP_ENONFINITE;
+  if (!(hst->D0 > 0.0)) return RBRP_EDEGENERATE;
   const int64_t k = hst->k;
   const int nblocks = std::min(hst->t, Ly.maxlog);
   if (ge) {
@@ -745,8 +772,10 @@ int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* 
     CK(cudaMemcpyAsync(hp + o_lSt, c.log.St, (size_t)nlog * b * 8, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(hp + o_lpiv, c.log.piv, (size_t)nlog * b * 4, cudaMemcpyDeviceToHost, s));
   }
+  hm.mark("w_enqueued");
   CK(cudaEventRecord(e1, s));
   CK(cudaStreamSynchronize(s));
+  hm.mark("done");
   float ms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);
   cudaEventDestroy(e0);

@@ -10,6 +10,7 @@ from __future__ import annotations
 import ctypes
 import dataclasses
 import os
+import threading
 from typing import List, Optional, Sequence
 
 import torch
@@ -64,6 +65,7 @@ class RBRPError(RuntimeError):
 
 
 _lib = None
+_tls = threading.local()
 
 
 def lib() -> ctypes.CDLL:
@@ -205,6 +207,7 @@ def id(X: torch.Tensor, tol: Optional[float] = None, k: Optional[int] = None, b:
         raise RBRPError(rc, "workspace_size")
     if workspace is None or workspace.numel() < sz.value:
         workspace = torch.empty(sz.value, dtype=torch.uint8, device=X.device)
+    ws_bytes = sz.value
     k_cap = p.k_max if p.k_max > 0 else min(p.n_global, p.d)
     W = None
     if with_W:
@@ -215,25 +218,34 @@ def id(X: torch.Tensor, tol: Optional[float] = None, k: Optional[int] = None, b:
             W = W_out
         else:
             W = torch.empty((X.shape[0], k_cap), dtype=X.dtype, device=X.device)
-    S = torch.empty(k_cap, dtype=torch.int64)
     mb = max_blocks
-    rep = _with_proj_blk(Report(), mb)
-    b_t = (ctypes.c_int32 * mb)()
-    b_pr = (ctypes.c_int32 * mb)()
-    rho = (ctypes.c_double * mb)()
-    rep.max_blocks = mb
+    # host buffers of the report, reused across calls of the same shape (per thread)
+    key = (mb, b if log_blocks else 0, k_cap)
+    cache = _tls.__dict__.setdefault("bufs", {})
+    if key not in cache:
+        if len(cache) > 16:
+            cache.clear()
+        rep = _with_proj_blk(Report(), mb)
+        b_t = (ctypes.c_int32 * mb)()
+        b_pr = (ctypes.c_int32 * mb)()
+        rho = (ctypes.c_double * mb)()
+        rep.max_blocks = mb
+        rep.b_t = ctypes.cast(b_t, ctypes.POINTER(ctypes.c_int32))
+        rep.b_prime = ctypes.cast(b_pr, ctypes.POINTER(ctypes.c_int32))
+        rep.rho = ctypes.cast(rho, ctypes.POINTER(ctypes.c_double))
+        bidx = bpiv = None
+        if log_blocks:
+            bidx = (ctypes.c_int64 * (mb * b))()
+            bpiv = (ctypes.c_int32 * (mb * b))()
+            rep.block_idx = ctypes.cast(bidx, ctypes.POINTER(ctypes.c_int64))
+            rep.block_piv = ctypes.cast(bpiv, ctypes.POINTER(ctypes.c_int32))
+        S = torch.empty(k_cap, dtype=torch.int64)
+        cache[key] = (rep, b_t, b_pr, rho, bidx, bpiv, S)
+    rep, b_t, b_pr, rho, bidx, bpiv, S = cache[key]
     rep.profile = 1 if profile else 0
-    rep.b_t = ctypes.cast(b_t, ctypes.POINTER(ctypes.c_int32))
-    rep.b_prime = ctypes.cast(b_pr, ctypes.POINTER(ctypes.c_int32))
-    rep.rho = ctypes.cast(rho, ctypes.POINTER(ctypes.c_double))
-    if log_blocks:
-        bidx = (ctypes.c_int64 * (mb * b))()
-        bpiv = (ctypes.c_int32 * (mb * b))()
-        rep.block_idx = ctypes.cast(bidx, ctypes.POINTER(ctypes.c_int64))
-        rep.block_piv = ctypes.cast(bpiv, ctypes.POINTER(ctypes.c_int32))
     stream = torch.cuda.current_stream(X.device).cuda_stream
     rc = L.rbrp_id(ctypes.byref(p), ctypes.c_void_p(X.data_ptr()),
-                   ctypes.c_void_p(workspace.data_ptr()), sz.value,
+                   ctypes.c_void_p(workspace.data_ptr()), ws_bytes,
                    ctypes.c_void_p(comm) if comm else None, ctypes.c_void_p(stream),
                    ctypes.cast(S.data_ptr(), ctypes.POINTER(ctypes.c_int64)),
                    ctypes.c_void_p(W.data_ptr()) if W is not None else None, ctypes.byref(rep))
