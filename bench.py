@@ -396,7 +396,10 @@ def main():
         # side measurement of SkLUPP-OSID at the ID's rank, l = 3k
         from paper_2309_16002_b200 import sketch as rbs
         ksk = min(res_list[-1].k, rbs.SK_MAX_K)
-        kws = dict(k=ksk, l=3 * ksk, seed=a.seed)
+        sk_ws = torch.empty(rbs.sketch_workspace_size(X.shape[0], X.shape[1], ksk, 3 * ksk), dtype=torch.uint8,
+                            device=dev)
+        sk_W = torch.empty((X.shape[0], ksk), dtype=torch.float64, device=dev)
+        kws = dict(k=ksk, l=3 * ksk, seed=a.seed, workspace=sk_ws, W_out=sk_W)
         for _ in range(2):
             rbs.sketch_id(X, **kws)
         torch.cuda.synchronize()
