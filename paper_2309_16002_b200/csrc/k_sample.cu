@@ -14,17 +14,35 @@
 namespace rbrp {
 
 constexpr int kSampleThreads = 256;
+constexpr int kSmemChunks = 2048;   // chunk prefixes searched in shared memory up to 8.4M rows
+
+constexpr int kSkipRows = 64;       // rows per entry of the shared skip table
+constexpr int kSkipMax = 2048;      // skip table in shared memory up to 131072 local rows
 
 // smallest local row r of global chunk q with cpre[r] > tq; falls back to the last
-// positive row of the chunk when tq is past the chunk's end (rounding).
+// positive row of the chunk when tq is past the chunk's end (rounding).  skip (optional):
+// cpre at the last row of every 64-row sub-block of the local rows, so the search runs
+// over the chunk's sub-blocks in shared memory first (cpre is non-decreasing inside a
+// chunk: the first row above tq lies in the first sub-block whose last value is above
+// tq), then over 64 rows -- the same row, 6 global loads on the dependent path, not 12.
 __device__ int64_t resolve_in_chunk(int q, double tq, const double* __restrict__ cpre,
                                     const double* __restrict__ dvec, int64_t n_local,
-                                    int64_t row_offset) {
+                                    int64_t row_offset, const double* skip = nullptr) {
   int64_t lo = (int64_t)q * kChunk - row_offset;
   int64_t hi = lo + kChunk;
   if (hi > n_local) hi = n_local;
   if (lo < 0 || lo >= n_local) return -1;   // chunk owned by another rank
   int64_t a = lo, b = hi;                    // search in [a, b)
+  if (skip && lo % kSkipRows == 0) {
+    int64_t sa = lo / kSkipRows, sb = (hi + kSkipRows - 1) / kSkipRows;
+    while (sa < sb) {
+      const int64_t m = (sa + sb) >> 1;
+      if (skip[m] > tq) sb = m; else sa = m + 1;
+    }
+    a = sa * kSkipRows;
+    if (a > hi) a = hi;
+    b = a + kSkipRows < hi ? a + kSkipRows : hi;
+  }
   while (a < b) {
     int64_t m = (a + b) >> 1;
     if (cpre[m] > tq) b = m; else a = m + 1;
@@ -46,6 +64,8 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample(SampleArgs A) {
   __shared__ int64_t cand[kSampleThreads];
   __shared__ int wcount[kSampleThreads / 32];
   __shared__ int s_tprev, s_log, s_btprev, s_bpprev;
+  __shared__ double s_cpref[kSmemChunks];
+  __shared__ double s_skip[kSkipMax];
 
   // log the block that just finished (device-side, read by the host at the end)
   if (tid == 0) {
@@ -87,14 +107,15 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample(SampleArgs A) {
     }
     double p = __shfl_up_sync(0xffffffffu, incl, 1);
     if (lane == 0) p = 0.0;
-    for (int c = c0; c < c1; ++c) { p += A.ctot[c]; A.cprefix[c] = p; }
+    for (int c = c0; c < c1; ++c) {
+      p += A.ctot[c];
+      A.cprefix[c] = p;
+      if (nch <= kSmemChunks) s_cpref[c] = p;   // the draws search a shared copy
+    }
+    if (c0 < nch && c1 == nch) s_total = p;     // = cprefix[nch - 1], no read-back
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) np += __shfl_xor_sync(0xffffffffu, np, o);
-    __syncwarp();
-    if (lane == 0) {
-      s_total = A.cprefix[nch - 1];
-      s_np = np;
-    }
+    if (lane == 0) s_np = np;
   }
   __syncthreads();
   if (tid == 0) {
@@ -191,6 +212,15 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample(SampleArgs A) {
     return;
   }
   // (3) rejection rounds
+  const int64_t nskip = (A.n_local + kSkipRows - 1) / kSkipRows;
+  const bool use_skip = nskip <= kSkipMax;
+  if (use_skip) {
+    for (int64_t j = tid; j < nskip; j += kSampleThreads) {
+      const int64_t r = j * kSkipRows + kSkipRows - 1;
+      s_skip[j] = A.cpre[r < A.n_local ? r : A.n_local - 1];
+    }
+    __syncthreads();
+  }
   const double total = s_total;
   const uint2 key = make_uint2((uint32_t)(A.seed & 0xffffffffu), (uint32_t)(A.seed >> 32));
   const uint32_t t = (uint32_t)st->t;
@@ -202,10 +232,11 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample(SampleArgs A) {
     const double u = u53(philox4x32_10(make_uint4(j, t, 0u, 0u), key));
     const double target = u * total;
     // first chunk q with cprefix[q] > target
+    const double* cpf = A.nchunks <= kSmemChunks ? s_cpref : A.cprefix;
     int a = 0, b = A.nchunks;
     while (a < b) {
       int m = (a + b) >> 1;
-      if (A.cprefix[m] > target) b = m; else a = m + 1;
+      if (cpf[m] > target) b = m; else a = m + 1;
     }
     int64_t row;
     if (a >= A.nchunks) {
@@ -214,8 +245,8 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample(SampleArgs A) {
       while (q > 0 && A.cpos[q] == 0) --q;
       row = resolve_in_chunk(q, 1e308, A.cpre, A.dvec, A.n_local, A.row_offset);
     } else {
-      const double tq = target - (a > 0 ? A.cprefix[a - 1] : 0.0);
-      row = resolve_in_chunk(a, tq, A.cpre, A.dvec, A.n_local, A.row_offset);
+      const double tq = target - (a > 0 ? cpf[a - 1] : 0.0);
+      row = resolve_in_chunk(a, tq, A.cpre, A.dvec, A.n_local, A.row_offset, use_skip ? s_skip : nullptr);
     }
     cand[tid] = row;
     __syncthreads();
