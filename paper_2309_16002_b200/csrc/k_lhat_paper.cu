@@ -21,9 +21,6 @@
 
 #include "launch.cuh"
 
-#ifndef LP_ABL_NOX2
-#define LP_ABL_NOX2 0
-#endif
 #ifndef LP_TRACE
 #define LP_TRACE 0   // cycle trace of CTA 0 (build with -DLP_TRACE=1; scripts/lp_trace.py)
 #endif
@@ -248,13 +245,6 @@ __global__ void __launch_bounds__(lp::NTH, 1)
         if (s >= NS) lp_wait(&xempty[xr.i], xr.ph ^ 1);
         const int y = (int)row0_of(s / (nc * npass)), c = s % nc;
         const bool second = resid && ((s / nc) & 1);
-#if LP_ABL_NOX2   // timing ablation only (wrong results): the update pass reuses stale slots
-        if (second) {
-          lp_arrive(&xfull[xr.i]);
-          xr.next(NS);
-          continue;
-        }
-#endif
         lp_expect(&xfull[xr.i], Cf::SLOTB);   // out-of-bounds rows / columns are zero-filled
         E* dst = xs + (size_t)xr.i * SLOT;
         const uint64_t pol = resid ? (second ? pol_drop : pol_keep) : pol_drop;

@@ -682,11 +682,10 @@ static cudaError_t go_fused(const CUtensorMap& map, double* X, int64_t ldx, cons
     tr = fz_trace_buf();
     traced = 1;
   }
-  static int xmode = -1;
-  if (xmode < 0) {
-    const char* e = getenv("RBRP_FZ_XMODE");   // timing experiments only (wrong results)
-    xmode = e ? atoi(e) : 0;
-  }
+#ifndef FZ_XMODE
+#define FZ_XMODE 0   // timing ablations of profiles/r01b_fused_ablation.jsonl (wrong results);
+#endif               // a profiling build sets it with RBRP_EXTRA_NVCC=-DFZ_XMODE=n
+  const int xmode = FZ_XMODE;
   kern<<<fz_num_sms(), fz::NTH, smem, s>>>(map, X, ldx, Qp, L, ldl, n, (int)d, nc, ns, nq, dvec, st, tr, xmode,
                                            paper ? 1 : 0);
   return cudaGetLastError();
