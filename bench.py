@@ -445,12 +445,14 @@ def main():
         "roofline": {"kernel": ("projection pass a4, dominant kernel: the b' <= %d instantiation "
                                 "(%d launches; residual form: L-hat pass + update pass per 64-row tile, "
                                 "Alg. 2 l.13/l.16)" % (dom["bucket"], dom["launches"])) if dom else "projection pass a4",
-                     "bound": "alu", "achieved": dom["achieved_tflops"] if dom else tflops, "peak": peak,
+                     "bound": "tensor", "achieved": dom["achieved_tflops"] if dom else tflops, "peak": peak,
                      "unit": "TFLOP/s", "frac": (dom["frac_fp64"] if dom else tflops / peak), "traffic": traffic,
                      "timing": "in-kernel %globaltimer stamps per launch (first CTA start -> last CTA end), "
                                "K timed steps",
-                     "peak_note": "FP64 (DMMA = DFMA rate): 148 SM x 64 FMA/clk x 2 x 1.965 GHz, derived "
-                                  "(DESIGN.md §6); measured DMMA 37.2 TF; MEASURED_PEAKS.json has no FP64 entry",
+                     "peak_note": "FP64 tensor path (DMMA, mma.sync.m8n8k4.f64; tcgen05 has no f64 kind): "
+                                  "measured 37.15 TF (profiles/r01_peak_fp64.json) = 148 SM x 64 FMA/clk x 2 x "
+                                  "1.965 GHz (37.2, used); MEASURED_PEAKS.json has no FP64 entry and the guide no "
+                                  "FP64 nominal ratio to scale its bf16 peak (DESIGN.md §6)",
                      "dominant": dom,
                      "all_blocks": {"achieved_tflops": tflops, "frac_fp64": tflops / peak,
                                     "algorithmic_GBs": gbs, "hbm_frac_of_measured": gbs / HBM_GBS,
