@@ -583,6 +583,96 @@ GraphEntry* get_graph(Ctx<T>& c, SampleArgs sa, const GraphKey& key) {
   return &g_graphs.back();
 }
 
+// a6: W(S,:) = I, W(rest,:) = L_2 L_1^{-1} (Alg. 3; triangular inverse)
+template <typename T>
+int enqueue_W(Ctx<T>& c, const rbrp_problem* p, rbrp_comm* comm, void* W_out, int64_t k, cudaStream_t s,
+              int* nl) {
+  const int64_t k_cap = c.k_cap;
+  double* L1 = c.L1;
+  T* LinvT = c.LinvT;
+  ++*nl;
+  CK(launch_gather_L1<T>(c.Lm, k_cap, c.S, k, c.n, p->row_offset, L1, s));
+  if (comm) {
+    int rc = comm_allreduce_f64(comm, L1, k * k, s);
+    if (rc) return rc;
+  }
+  // K padded to a multiple of 8 for the FP64 tensor path: L_1^{-T} gets zero columns
+  // [k, kp) and L's columns [k, kp) are zeroed (never written by the loop)
+  const int64_t kp = (k + 7) / 8 * 8;
+  ++*nl;
+  CK(launch_trinv<T>(L1, k, LinvT, kp, c.st, s));
+  if (kp > k && kp <= k_cap && c.n > 0)
+    CK(cudaMemset2DAsync(c.Lm + k, (size_t)k_cap * sizeof(T), 0, (size_t)(kp - k) * sizeof(T), (size_t)c.n, s));
+  cudaError_t merr = cudaSuccess;
+  ++*nl;
+  if (sizeof(T) == 8 && !force_simt() && kp <= k_cap && c.Wsc && !env_on("RBRP_W_NTMMA") &&
+      gemm_lp_supported((const double*)c.Lm, k_cap, (const double*)LinvT, kp, kp)) {
+    CK(gemm_nt_lp((const double*)c.Lm, k_cap, (const double*)LinvT, kp, (double*)W_out, k_cap, c.n, k, kp, c.Wsc,
+                  s, true));
+    *nl += 2 * (int)((k + 31) / 32);
+  } else if (sizeof(T) == 8 && !force_simt() && kp <= k_cap &&
+             gemm_nt_mma((const double*)c.Lm, k_cap, (const double*)LinvT, kp, (double*)W_out, k_cap, c.n, k, kp, s,
+                         &merr)) {
+    CK(merr);
+  } else {
+    CK(launch_gemm_nt<T>(c.Lm, k_cap, LinvT, kp, (T*)W_out, k_cap, c.n, k, k, s));
+  }
+  ++*nl;
+  CK(launch_w_identity<T>((T*)W_out, k_cap, c.S, k, c.n, p->row_offset, s));
+  return RBRP_OK;
+}
+
+struct WGraph {
+  GraphKey key;
+  const void* W;
+  int64_t k;
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int launches = 0;
+  unsigned long long stamp = 0;
+};
+std::vector<WGraph> g_wgraphs;
+
+template <typename T>
+WGraph* get_w_graph(Ctx<T>& c, const rbrp_problem* p, const GraphKey& key, void* W_out, int64_t k) {
+  if (env_on("RBRP_NO_GRAPH")) return nullptr;
+  std::lock_guard<std::mutex> lk(g_graph_mu);
+  for (auto& e : g_wgraphs)
+    if (e.key == key && e.W == W_out && e.k == k) {
+      e.stamp = ++g_graph_clock;
+      return &e;
+    }
+  if (!g_capture_stream && cudaStreamCreateWithFlags(&g_capture_stream, cudaStreamNonBlocking) != cudaSuccess)
+    return nullptr;
+  WGraph e;
+  e.key = key;
+  e.W = W_out;
+  e.k = k;
+  bool ok = cudaStreamBeginCapture(g_capture_stream, cudaStreamCaptureModeRelaxed) == cudaSuccess;
+  if (ok) {
+    const int rc = enqueue_W<T>(c, p, nullptr, W_out, k, g_capture_stream, &e.launches);
+    const bool endok = cudaStreamEndCapture(g_capture_stream, &e.g) == cudaSuccess;
+    ok = rc == RBRP_OK && endok && e.g;
+  }
+  if (ok) ok = cudaGraphInstantiate(&e.exec, e.g, 0) == cudaSuccess;
+  if (!ok) {
+    cudaGetLastError();
+    if (e.exec) cudaGraphExecDestroy(e.exec);
+    if (e.g) cudaGraphDestroy(e.g);
+    return nullptr;
+  }
+  if (g_wgraphs.size() >= 8) {
+    auto it = std::min_element(g_wgraphs.begin(), g_wgraphs.end(),
+                               [](const WGraph& a, const WGraph& b) { return a.stamp < b.stamp; });
+    cudaGraphExecDestroy(it->exec);
+    cudaGraphDestroy(it->g);
+    g_wgraphs.erase(it);
+  }
+  e.stamp = ++g_graph_clock;
+  g_wgraphs.push_back(e);
+  return &g_wgraphs.back();
+}
+
 template <typename T>
 int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* comm,
         cudaStream_t s, int64_t* S_out, void* W_out, rbrp_report* rep) {
@@ -723,40 +813,19 @@ int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* 
     nl += ge->launches_per_block * hst->t;
     nproj += hst->t;
   }
-  // a6: W (Alg. 3)
+  // a6: W (Alg. 3); in graph mode the W kernels are replayed from a cached graph (keyed by
+  // the loop's graph, W_out and k), so the host does not launch them one by one while the
+  // GPU waits behind the stop-test read-back
   if (!(p->flags & RBRP_NO_W) && W_out && k > 0) {
-    double* L1 = c.L1;
-    T* LinvT = c.LinvT;
     prof.begin(6);
-    ++nl;
-    CK(launch_gather_L1<T>(c.Lm, k_cap, c.S, k, c.n, p->row_offset, L1, s));
-    if (comm) {
-      int rc = comm_allreduce_f64(comm, L1, k * k, s);
+    WGraph* wg = (ge && !comm && !prof.on) ? get_w_graph<T>(c, p, ge->key, W_out, k) : nullptr;
+    if (wg) {
+      CK(cudaGraphLaunch(wg->exec, s));
+      nl += wg->launches;
+    } else {
+      const int rc = enqueue_W<T>(c, p, comm, W_out, k, s, &nl);
       if (rc) return rc;
     }
-    // K padded to a multiple of 8 for the FP64 tensor path: L_1^{-T} gets zero columns
-    // [k, kp) and L's columns [k, kp) are zeroed (never written by the loop)
-    const int64_t kp = (k + 7) / 8 * 8;
-    ++nl;
-    CK(launch_trinv<T>(L1, k, LinvT, kp, c.st, s));
-    if (kp > k && kp <= k_cap && c.n > 0)
-      CK(cudaMemset2DAsync(c.Lm + k, (size_t)k_cap * sizeof(T), 0, (size_t)(kp - k) * sizeof(T), (size_t)c.n, s));
-    cudaError_t merr = cudaSuccess;
-    ++nl;
-    if (sizeof(T) == 8 && !force_simt() && kp <= k_cap && c.Wsc && !env_on("RBRP_W_NTMMA") &&
-        gemm_lp_supported((const double*)c.Lm, k_cap, (const double*)LinvT, kp, kp)) {
-      CK(gemm_nt_lp((const double*)c.Lm, k_cap, (const double*)LinvT, kp, (double*)W_out, k_cap, c.n, k, kp,
-                    c.Wsc, s, true));
-      nl += 2 * (int)((k + 31) / 32);
-    } else if (sizeof(T) == 8 && !force_simt() && kp <= k_cap &&
-               gemm_nt_mma((const double*)c.Lm, k_cap, (const double*)LinvT, kp, (double*)W_out, k_cap, c.n, k,
-                           kp, s, &merr)) {
-      CK(merr);
-    } else {
-      CK(launch_gemm_nt<T>(c.Lm, k_cap, LinvT, kp, (T*)W_out, k_cap, c.n, k, k, s));
-    }
-    ++nl;
-    CK(launch_w_identity<T>((T*)W_out, k_cap, c.S, k, c.n, p->row_offset, s));
     prof.end();
   }
   int64_t* hS = (int64_t*)(hp + o_S);
