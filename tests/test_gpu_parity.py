@@ -170,6 +170,13 @@ def test_ragged_shapes_and_odd_d():
         Xnp += 1e-3 * rng.standard_normal((n, d))
         ores = O.rbrp(Xnp, k=min(12, d), b=b, seed=2)
         _replay(Xnp, ores, np.float64, b)
+    # fp32: odd d and d = 2 mod 4 (row stride not 16-byte aligned: CUDA-core fallback), and a
+    # ragged d on the tiled DMMA path (d = 100: partial last chunk, two 32-column boxes)
+    for (n, d, b) in [(3001, 37, 8), (2500, 70, 16), (6000, 100, 40)]:
+        Xnp = (rng.standard_normal((n, 10)) @ rng.standard_normal((10, d))).astype(np.float32)
+        Xnp += np.float32(1e-2) * rng.standard_normal((n, d)).astype(np.float32)
+        ores = O.rbrp(Xnp, k=10, b=b, seed=2)
+        _replay(Xnp, ores, np.float32, b)
 
 
 @cuda
