@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define RBRP_SK_MAX_K 160   /* largest k of rbrp_sketch_id (one-CTA k x k Cholesky in smem) */
+#define RBRP_SK_MAX_K 512   /* largest k of rbrp_sketch_id and rbrp_lupp */
 
 /* rbrp_sketch_report.flags */
 enum {
@@ -91,7 +91,8 @@ int rbrp_lupp(const double* Y, int64_t n, int64_t l, int64_t ldy, int64_t k, voi
  *   X          device, n x d row-major, leading dimension ldx (even, >= d); d % 8 == 0;
  *              16-byte aligned.  Read only.
  *   k, l       skeletons and sketch size, 1 <= k <= min(RBRP_SK_MAX_K, n), k <= l <= 4k
- *              (the paper's oversampling is l = 3k).
+ *              (the paper's oversampling is l = 3k; l may exceed d, as at the
+ *              paper's Table 3 ranks k > d/3).
  *   seed       embedding seed (rbrp_gaussian_embedding) when OmegaT is NULL.
  *   OmegaT     device l x d (ld d) or NULL: a caller-supplied Omega^T.
  *   workspace  device, >= rbrp_sketch_workspace_size(), 256-byte aligned.

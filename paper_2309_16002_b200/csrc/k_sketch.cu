@@ -23,6 +23,7 @@
 //                W = Y M is the FP64 tensor-path GEMM again.
 #include <cooperative_groups.h>
 #include <math.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -201,16 +202,19 @@ __global__ void __launch_bounds__(sk::kThreads, 1) k_lupp(LuArgs a) {
       if (s_bl >= 0)
         for (int j = tid; j < pw; j += sk::kThreads) cr[2 + j] = A[(size_t)s_bl * LD + j];
       grid.sync();
-      // the winner, identical in every CTA
-      if (w == 0) {
+      // the winner, identical in every CTA: thread g reads candidate g (all loads in
+      // flight at once, L2 only: the buffer was written by other CTAs), then a warp
+      // argmax and one over the NW warp results
+      {
         double v = -1.0;
         long long r = LLONG_MAX;
         int who = -1;
-        for (int g = lane; g < G; g += 32) {
+        for (int g = tid; g < G; g += sk::kThreads) {
           const double* q = a.cand + ((size_t)par * G + g) * CS;
-          const long long qr = __double_as_longlong(q[1]);
-          if (qr >= 0 && lu_better(q[0], qr, v, r)) {
-            v = q[0];
+          const double qv = __ldcg(q);
+          const long long qr = __double_as_longlong(__ldcg(q + 1));
+          if (qr >= 0 && lu_better(qv, qr, v, r)) {
+            v = qv;
             r = qr;
             who = g;
           }
@@ -227,10 +231,25 @@ __global__ void __launch_bounds__(sk::kThreads, 1) k_lupp(LuArgs a) {
           }
         }
         if (lane == 0) {
-          s_bv = v;
-          s_br = r;
-          s_win = who;
+          s_wv[w] = v;
+          s_wr[w] = r;
+          s_wg[w] = who;
         }
+      }
+      __syncthreads();
+      if (tid == 0) {
+        double v = -1.0;
+        long long r = LLONG_MAX;
+        int who = -1;
+        for (int q = 0; q < NW; ++q)
+          if (s_wg[q] >= 0 && (who < 0 || lu_better(s_wv[q], s_wr[q], v, r))) {
+            v = s_wv[q];
+            r = s_wr[q];
+            who = s_wg[q];
+          }
+        s_bv = v;
+        s_br = r;
+        s_win = who;
       }
       __syncthreads();
       const int pb = par;
@@ -243,7 +262,7 @@ __global__ void __launch_bounds__(sk::kThreads, 1) k_lupp(LuArgs a) {
       const long long prow = s_br;
       const int m = npiv++;
       const double* q = a.cand + ((size_t)pb * G + s_win) * CS;
-      for (int j = tid; j < pw; j += sk::kThreads) Up[j] = q[2 + j];
+      for (int j = tid; j < pw; j += sk::kThreads) Up[j] = __ldcg(q + 2 + j);
       if (tid == 0) {
         spiv[m] = prow;
         if (prow >= r0 && prow < r0 + nr) act[prow - r0] = 0;
@@ -289,8 +308,10 @@ static bool lupp_plan(int64_t n, int k, int* G, int* R, int* PW) {
   const int sms = sk_num_sms();
   *G = (int)std::min<int64_t>(sms, n);
   *R = (int)((n + *G - 1) / *G);
+  const char* cap = getenv("RBRP_LUPP_PW");   // test knob: largest panel width tried
+  const int pw_max = cap ? atoi(cap) : 32;
   for (int pw : {32, 16, 8})
-    if (lupp_smem(pw, *R, k) <= (size_t)sk::kSmemMax) {
+    if (pw <= pw_max && lupp_smem(pw, *R, k) <= (size_t)sk::kSmemMax) {
       *PW = pw;
       return true;
     }
@@ -378,6 +399,110 @@ __global__ void __launch_bounds__(1024) k_chol_small(const double* __restrict__ 
     C[e] = j <= i ? cs[i * ld + j] : 0.0;
   }
   if (tid == 0 && bad) *info = 1;
+}
+
+// Blocked right-looking Cholesky for k > kCholSmallK (C = G's lower factor, in place in
+// C after a copy of G): per 32-column panel, one CTA factors the diagonal block (warp 0,
+// lane i owns row i) and solves the rows below against it (a thread per row), then a
+// tile per 32 x 32 lower block of the trailing matrix applies C_below C_below^T.
+constexpr int kCholNB = 32;
+constexpr int kCholSmallK = 160;
+
+__global__ void __launch_bounds__(512) k_chol_panel(double* __restrict__ C, int k, int j0, int* __restrict__ info) {
+  __shared__ double D[kCholNB][kCholNB + 1];
+  const int jb = min(kCholNB, k - j0), tid = threadIdx.x;
+  for (int e = tid; e < jb * jb; e += blockDim.x) {
+    const int i = e / jb, q = e - i * jb;
+    D[i][q] = C[(size_t)(j0 + i) * k + j0 + q];
+  }
+  __syncthreads();
+  if (tid < 32) {
+    bool bad = false;
+    for (int j = 0; j < jb; ++j) {
+      double dj = D[j][j];
+      if (!(dj > 0.0)) {
+        bad = true;
+        dj = 1.0;
+      }
+      dj = sqrt(dj);
+      __syncwarp();
+      if (tid == j) D[j][j] = dj;
+      if (tid > j && tid < jb) D[tid][j] /= dj;
+      __syncwarp();
+      if (tid > j && tid < jb)
+        for (int q = j + 1; q <= tid; ++q) D[tid][q] = fma(-D[tid][j], D[q][j], D[tid][q]);
+      __syncwarp();
+    }
+    if (tid == 0 && bad) *info = 1;
+  }
+  __syncthreads();
+  for (int e = tid; e < jb * jb; e += blockDim.x) {
+    const int i = e / jb, q = e - i * jb;
+    C[(size_t)(j0 + i) * k + j0 + q] = q <= i ? D[i][q] : 0.0;
+  }
+  for (int e = tid; e < jb * (k - j0 - jb); e += blockDim.x) {   // upper part of the panel rows
+    const int i = e / (k - j0 - jb), q = e - i * (k - j0 - jb);
+    C[(size_t)(j0 + i) * k + j0 + jb + q] = 0.0;
+  }
+  // rows below: x D^T = g  ->  x_q = (g_q - sum_{t<q} x_t D(q, t)) / D(q, q)
+  for (int i = j0 + jb + tid; i < k; i += blockDim.x) {
+    double* row = C + (size_t)i * k + j0;
+    double x[kCholNB];
+#pragma unroll
+    for (int q = 0; q < kCholNB; ++q) x[q] = q < jb ? row[q] : 0.0;
+#pragma unroll
+    for (int q = 0; q < kCholNB; ++q) {
+      if (q < jb) {
+        double v = x[q];
+#pragma unroll
+        for (int t = 0; t < q; ++t) v = fma(-x[t], D[q][t], v);
+        x[q] = v / D[q][q];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kCholNB; ++q)
+      if (q < jb) row[q] = x[q];
+  }
+}
+
+// trailing update C(i, q) -= sum_t C(i, j0 + t) C(q, j0 + t), j1 = j0 + 32 <= q <= i < k;
+// one 32 x 32 block of (i, q) per CTA (lower blocks only), panel rows staged in smem
+__global__ void __launch_bounds__(1024) k_chol_update(double* __restrict__ C, int k, int j0) {
+  __shared__ double Pi[kCholNB][kCholNB + 1], Pq[kCholNB][kCholNB + 1];
+  const int j1 = j0 + kCholNB;
+  const int bi = blockIdx.y, bq = blockIdx.x;
+  if (bq > bi) return;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int i0 = j1 + bi * kCholNB, q0 = j1 + bq * kCholNB;
+  {
+    const int ri = i0 + ty, rq = q0 + ty;
+    Pi[ty][tx] = ri < k ? C[(size_t)ri * k + j0 + tx] : 0.0;
+    Pq[ty][tx] = rq < k ? C[(size_t)rq * k + j0 + tx] : 0.0;
+  }
+  __syncthreads();
+  const int i = i0 + ty, q = q0 + tx;
+  if (i >= k || q > i) return;
+  double v = C[(size_t)i * k + q];
+#pragma unroll
+  for (int t = 0; t < kCholNB; ++t) v = fma(-Pi[ty][t], Pq[tx][t], v);
+  C[(size_t)i * k + q] = v;
+}
+
+// G (k x k) = C C^T, C lower with zeros above the diagonal; info = 1 if not positive definite
+static cudaError_t chol_blocked(const double* G, int k, double* C, int* info, cudaStream_t s, int* launches) {
+  cudaError_t e = cudaMemcpyAsync(C, G, (size_t)k * k * 8, cudaMemcpyDeviceToDevice, s);
+  if (e != cudaSuccess) return e;
+  for (int j0 = 0; j0 < k; j0 += kCholNB) {
+    k_chol_panel<<<1, 512, 0, s>>>(C, k, j0, info);
+    ++*launches;
+    const int m = k - j0 - kCholNB;
+    if (m > 0) {
+      const int nb = (m + kCholNB - 1) / kCholNB;
+      k_chol_update<<<dim3(nb, nb), dim3(kCholNB, kCholNB), 0, s>>>(C, k, j0);
+      ++*launches;
+    }
+  }
+  return cudaGetLastError();
 }
 
 // out (k x lp) = op(A) B, A (k x k) triangular, op(A) = A (transA = 0) or A^T; one output
@@ -505,7 +630,7 @@ SkLayout sk_layout(int64_t n, int64_t d, int64_t k, int64_t l) {
 }
 
 int sk_check(int64_t n, int64_t d, int64_t ldx, int64_t k, int64_t l) {
-  if (n < 1 || d < 1 || ldx < d || k < 1 || k > n || k > RBRP_SK_MAX_K || l < k || l > 4 * k || l > d)
+  if (n < 1 || d < 1 || ldx < d || k < 1 || k > n || k > RBRP_SK_MAX_K || l < k || l > 4 * k)
     return RBRP_EINVAL;
   return RBRP_OK;
 }
@@ -645,23 +770,30 @@ int rbrp_sketch_id(const double* X, int64_t n, int64_t d, int64_t ldx, int64_t k
     double* A2T = (double*)(ws + Ly.A2T);
     DevState* dst = (DevState*)(ws + Ly.st);
     const size_t csm = (size_t)kk * (kk + 1) * 8;
-    SK(cudaFuncSetAttribute(k_chol_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
+    const bool small = kk <= kCholSmallK;
+    if (small) SK(cudaFuncSetAttribute(k_chol_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
     SK(cudaMemsetAsync(info, 0, sizeof(int), s));
     SK(cudaMemsetAsync(dst, 0, sizeof(DevState), s));
     const unsigned gm = (unsigned)(((int64_t)kk * lp + 255) / 256), gg = (unsigned)((kk * kk + 255) / 256);
+    auto chol = [&](double* Cout) -> cudaError_t {   // Gm = Cout Cout^T
+      if (!small) return chol_blocked(Gm, kk, Cout, info, s, &launches);
+      k_chol_small<<<1, 1024, csm, s>>>(Gm, kk, Cout, info);
+      ++launches;
+      return cudaGetLastError();
+    };
     k_gather_rows<<<kk, 256, 0, s>>>(Y, lp, Sdev, kk, lp, Z);          // Z = Y(S,:)
     k_gram_rows<<<gg, 256, 0, s>>>(Z, kk, lp, Gm);                      // G1 = Z Z^T
-    k_chol_small<<<1, 1024, csm, s>>>(Gm, kk, C1, info);               // G1 = C1 C1^T (R1 = C1^T)
+    SK(chol(C1));                                                       // G1 = C1 C1^T (R1 = C1^T)
     SK(launch_trinv<double>(C1, kk, A1T, kk, dst, s));                 // A1T = C1^{-T}
     k_small_tri_mm<<<gm, 256, 0, s>>>(A1T, kk, 1, 0, Z, lp, P);        // P1 = C1^{-1} Z = Q1^T
     k_gram_rows<<<gg, 256, 0, s>>>(P, kk, lp, Gm);                      // G2 = P1 P1^T
-    k_chol_small<<<1, 1024, csm, s>>>(Gm, kk, C2, info);               // G2 = C2 C2^T (R2 = C2^T)
+    SK(chol(C2));                                                       // G2 = C2 C2^T (R2 = C2^T)
     SK(launch_trinv<double>(C2, kk, A2T, kk, dst, s));                 // A2T = C2^{-T}
     k_small_tri_mm<<<gm, 256, 0, s>>>(A2T, kk, 1, 0, P, lp, Z);        // Q^T = C2^{-1} P1
     k_small_tri_mm<<<gm, 256, 0, s>>>(A2T, kk, 0, 0, Z, lp, P);        // R2^{-1} Q^T
     k_small_tri_mm<<<gm, 256, 0, s>>>(A1T, kk, 0, 0, P, lp, Z);        // M^T = R1^{-1} R2^{-1} Q^T
     SK(cudaGetLastError());
-    launches += 11;
+    launches += 9;
     if (gemm_lp_supported(Y, lp, Z, lp, lp)) {                                         // W = Y M
       SK(gemm_nt_lp(Y, lp, Z, lp, W_out, k, n, kk, lp, gsc, s));
       launches += 2 * (kk + 31) / 32;

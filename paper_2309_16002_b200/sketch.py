@@ -14,7 +14,7 @@ import torch
 
 from .rbrp import RBRPError, lib as _base_lib
 
-SK_MAX_K = 160
+SK_MAX_K = 512
 SK_SHORT = 1
 PHASES = ["embedding", "sketch", "lupp", "osid"]
 EXPORTED = ["rbrp_gaussian_embedding", "rbrp_lupp_workspace_size", "rbrp_lupp",

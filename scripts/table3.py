@@ -28,6 +28,7 @@ PAPER_V100_S = dict(zip(T3_RANKS, (3.105e-2, 4.448e-2, 5.838e-2, 7.231e-2, 9.512
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--sketch-only", action="store_true", help="SkLUPP-OSID rows only")
 a = ap.parse_args()
 # Table 3, SkLUPP-OSID row, V100
 PAPER_V100_SK = dict(zip(T3_RANKS, (1.036e-2, 1.204e-2, 1.666e-2, 2.233e-2, 3.430e-2, 4.835e-2, 6.960e-2,
@@ -35,7 +36,7 @@ PAPER_V100_SK = dict(zip(T3_RANKS, (1.036e-2, 1.204e-2, 1.666e-2, 2.233e-2, 3.43
 cfg = CONFIGS["t3"]
 X = make(cfg, device="cuda")
 m = cfg.n // cfg.n_centres
-for form in ("residual", "paper"):
+for form in (() if a.sketch_only else ("residual", "paper")):
     for r in T3_RANKS:
         kw = dict(k=r, b=cfg.b, seed=0, form=form, log_blocks=False)
         rb.id(X, **kw)

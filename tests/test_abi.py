@@ -44,9 +44,10 @@ def test_sketch_validation_before_cuda():
     sz = ctypes.c_size_t()
     assert L.rbrp_sketch_workspace_size(1000, 64, 10, 30, ctypes.byref(sz)) == 0
     assert sz.value > 1000 * 32 * 8
-    for bad in [(1000, 64, 0, 30), (1000, 64, 10, 9), (1000, 64, 10, 41), (1000, 64, 161, 480),
-                (1000, 16, 10, 30), (5, 64, 10, 30)]:
+    for bad in [(1000, 64, 0, 30), (1000, 64, 10, 9), (1000, 64, 10, 41), (4000, 2048, 513, 1600),
+                (5, 64, 10, 30)]:
         assert L.rbrp_sketch_workspace_size(*bad, ctypes.byref(sz)) == -1, bad
+    assert L.rbrp_sketch_workspace_size(1000, 16, 10, 30, ctypes.byref(sz)) == 0   # l > d allowed
     assert L.rbrp_lupp_workspace_size(1000, 30, 10, ctypes.byref(sz)) == 0
     assert L.rbrp_lupp_workspace_size(1000, 30, 31, ctypes.byref(sz)) == -1
     assert L.rbrp_gaussian_embedding(0, 10, 0, None, 0, None) == -1

@@ -58,6 +58,25 @@ def test_lupp_bitwise(n, l, k):
 
 
 @cuda
+@pytest.mark.parametrize("pw", [16, 8])
+def test_lupp_bitwise_narrow_panels(pw, monkeypatch):
+    """the 16- and 8-column panel variants (chosen when the rows of a CTA and the U rows
+    of k pivots do not fit 32 columns in shared memory), forced by the test knob"""
+    monkeypatch.setenv("RBRP_LUPP_PW", str(pw))
+    rng = np.random.default_rng(pw)
+    Y = rng.standard_normal((3000, 96)) * np.exp(-np.arange(96) / 30.0)
+    _lupp_case(Y, 70)
+
+
+@cuda
+def test_lupp_bitwise_large_k():
+    """k = 300 pivots (about ten 32-column panels, 300 grid barriers)"""
+    rng = np.random.default_rng(300)
+    Y = rng.standard_normal((8000, 320)) * np.exp(-np.arange(320) / 100.0)
+    _lupp_case(Y, 300)
+
+
+@cuda
 def test_lupp_zero_column_duplicates_and_short():
     rng = np.random.default_rng(4)
     Y = rng.standard_normal((900, 40))
@@ -92,6 +111,24 @@ def test_sketch_id_matches_oracle(seeded):
     assert np.linalg.norm(Wg - W) <= 1e-9 * np.linalg.norm(W)
     e_g, e_o = R.errid(X, f.piv, Wg), R.errid(X, f.piv, W)
     assert abs(e_g - e_o) <= 1e-9 * e_o
+
+
+@cuda
+def test_sketch_id_large_k_blocked_cholesky():
+    """k = 200 > 160: the OSID Cholesky factorizations take the blocked multi-CTA path;
+    the sketch is wider than X (l > d)"""
+    rng = np.random.default_rng(23)
+    n, d, k = 6000, 512, 200              # l = 600 > d (as at Table 3 ranks k > d/3)
+    l = 3 * k
+    X = rng.standard_normal((n, d)) * np.exp(-np.arange(d) / 150.0)
+    Om = rng.standard_normal((d, l)) / np.sqrt(l)
+    res = _sk().sketch_id(torch.as_tensor(X, device="cuda"), k, l,
+                          omega_T=torch.as_tensor(Om.T.copy(), device="cuda"))
+    f, W, _ = K.sketchy_id(X, k, Om)
+    assert res.S.tolist() == f.piv
+    Wg = res.W.cpu().numpy()
+    assert np.array_equal(Wg[f.piv], np.eye(k))
+    assert np.linalg.norm(Wg - W) <= 1e-9 * np.linalg.norm(W)
 
 
 @cuda
