@@ -36,9 +36,10 @@ namespace cg = cooperative_groups;
 
 namespace rbrp {
 namespace sk {
-constexpr int kThreads = 256;
+constexpr int kThreads = 512;   // >= RBRP_SK_MAX_K: one U row per thread in (1)
 constexpr int kSmemMax = 227 * 1024;
 constexpr uint32_t kOmegaTag = 0x4F4D4547u;   // reading R25
+static_assert(kThreads >= RBRP_SK_MAX_K, "k_lupp step (1) holds one U row per thread");
 }  // namespace sk
 
 // ------------------------------------------------------------------------------------
@@ -84,10 +85,26 @@ __device__ __forceinline__ bool lu_better(double v, long long r, double bv, long
   return v > bv || (v == bv && r < br);
 }
 
+#ifdef LU_TRACE   // phase cycle counts of CTA 0 (debug builds: -DLU_TRACE)
+__device__ long long g_lu_trace[8];
+#define LU_T0() long long lu_t = clock64()
+#define LU_T(i)                                                  \
+  do {                                                           \
+    const long long lu_n = clock64();                            \
+    if (blockIdx.x == 0 && threadIdx.x == 0) g_lu_trace[i] += lu_n - lu_t; \
+    lu_t = lu_n;                                                 \
+  } while (0)
+#else
+#define LU_T0()
+#define LU_T(i)
+#endif
+
 template <int PW>
 __global__ void __launch_bounds__(sk::kThreads, 1) k_lupp(LuArgs a) {
   cg::grid_group grid = cg::this_grid();
   constexpr int LD = PW + 1, CS = PW + 2, NW = sk::kThreads / 32;
+  constexpr int LA1 = PW >= 32 ? 4 : 8, LA = 8;   // multipliers loaded per batch in (1), (2)
+  constexpr int HW = PW > 16 ? 16 : PW, NH = PW / HW;   // (2): columns per work item
   extern __shared__ __align__(16) double smd[];
   const int R = a.R, k = a.k, G = gridDim.x;
   double* A = smd;                                       // R x LD: own rows, panel columns
@@ -108,46 +125,83 @@ __global__ void __launch_bounds__(sk::kThreads, 1) k_lupp(LuArgs a) {
   __syncthreads();
   int npiv = 0, par = 0;
   int64_t c = 0;
+  LU_T0();
   while (npiv < k && c < a.l) {
     const int64_t c0 = c;
     const int pw = (int)min((int64_t)PW, a.l - c0);
     const int np0 = npiv;
-    // (1) U(m, c0 + j), m < np0: Y(p_m, .) minus the earlier pivots' updates, in order
-    for (int e = tid; e < np0 * pw; e += sk::kThreads) {
-      const int m = e / pw, j = e - m * pw;
-      Us[m * PW + j] = a.Y[spiv[m] * a.ldy + c0 + j];
-    }
-    __syncthreads();
-    for (int mm = 0; mm + 1 < np0; ++mm) {
-      const int cnt = (np0 - 1 - mm) * pw;
-      for (int e = tid; e < cnt; e += sk::kThreads) {
-        const int m = mm + 1 + e / pw, j = e % pw;
-        const double lm = a.Lm[spiv[m] * k + mm];
-        Us[m * PW + j] = __dsub_rn(Us[m * PW + j], __dmul_rn(lm, Us[mm * PW + j]));
+    // (1) U(m, c0 + j), m < np0: Y(p_m, .) minus the earlier pivots' updates, in order.
+    // Thread m holds U row m in registers; step mm publishes the (final) row mm in smem,
+    // then every row m > mm subtracts L(p_m, mm) U(mm, .).  The multipliers of row m are
+    // read LA1 steps ahead (one batch of loads in flight while the previous 8 steps run).
+    {
+      double u[PW];
+      const bool own = tid < np0;
+      const int64_t prow = own ? spiv[tid] : 0;
+      if (own) {
+        const double* yr = a.Y + prow * a.ldy + c0;
+#pragma unroll
+        for (int j = 0; j < PW; ++j) u[j] = j < pw ? yr[j] : 0.0;
+      }
+      const double* lr = a.Lm + prow * k;
+      double lcur[LA1], lnext[LA1];
+#pragma unroll
+      for (int t = 0; t < LA1; ++t) lcur[t] = (own && t < tid) ? lr[t] : 0.0;
+      for (int mg = 0; mg < np0; mg += LA1) {
+#pragma unroll
+        for (int t = 0; t < LA1; ++t) lnext[t] = (own && mg + LA1 + t < tid) ? lr[mg + LA1 + t] : 0.0;
+#pragma unroll
+        for (int t = 0; t < LA1; ++t) {
+          const int mm = mg + t;
+          if (mm >= np0) break;
+          if (tid == mm) {
+#pragma unroll
+            for (int j = 0; j < PW; ++j) Us[mm * PW + j] = u[j];
+          }
+          __syncthreads();
+          if (own && tid > mm) {
+            const double lm = lcur[t];
+            const double* ur = Us + mm * PW;
+#pragma unroll
+            for (int j = 0; j < PW; ++j) u[j] = __dsub_rn(u[j], __dmul_rn(lm, ur[j]));
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < LA1; ++t) lcur[t] = lnext[t];
       }
       __syncthreads();
     }
+    LU_T(0);
     // (2) own active rows: panel columns of Y, then the earlier pivots' updates in order,
-    // the row held in registers (columns >= pw carry unused values)
-    for (int i = tid; i < nr; i += sk::kThreads) {
+    // held in registers (columns >= pw carry unused values).  Work items are (row, group
+    // of HW columns): every entry's update sequence is its own, so the split is exact.
+    for (int e = tid; e < nr * NH; e += sk::kThreads) {
+      const int i = e / NH, h = e - i * NH;
       if (!act[i]) continue;
-      const double* yr = a.Y + (r0 + i) * a.ldy + c0;
-      double rv[PW];
+      const int j0 = h * HW;
+      const double* yr = a.Y + (r0 + i) * a.ldy + c0 + j0;
+      double rv[HW];
 #pragma unroll
-      for (int j = 0; j < PW; ++j) rv[j] = j < pw ? yr[j] : 0.0;
+      for (int j = 0; j < HW; ++j) rv[j] = j0 + j < pw ? yr[j] : 0.0;
       const double* lr = a.Lm + (r0 + i) * k;
-#pragma unroll 2
-      for (int m = 0; m < np0; ++m) {
-        const double lm = lr[m];
-        const double* u = Us + m * PW;
+      for (int mg = 0; mg < np0; mg += LA) {
+        double lb[LA];
 #pragma unroll
-        for (int j = 0; j < PW; ++j) rv[j] = __dsub_rn(rv[j], __dmul_rn(lm, u[j]));
+        for (int t = 0; t < LA; ++t) lb[t] = mg + t < np0 ? lr[mg + t] : 0.0;
+#pragma unroll
+        for (int t = 0; t < LA; ++t) {
+          if (mg + t >= np0) break;
+          const double* u = Us + (mg + t) * PW + j0;
+#pragma unroll
+          for (int j = 0; j < HW; ++j) rv[j] = __dsub_rn(rv[j], __dmul_rn(lb[t], u[j]));
+        }
       }
-      double* ar = A + (size_t)i * LD;
+      double* ar = A + (size_t)i * LD + j0;
 #pragma unroll
-      for (int j = 0; j < PW; ++j) ar[j] = rv[j];
+      for (int j = 0; j < HW; ++j) ar[j] = rv[j];
     }
     __syncthreads();
+    LU_T(1);
     // (3) the panel's steps
     int s = 0;
     for (; s < pw && npiv < k; ++s) {
@@ -201,7 +255,9 @@ __global__ void __launch_bounds__(sk::kThreads, 1) k_lupp(LuArgs a) {
       }
       if (s_bl >= 0)
         for (int j = tid; j < pw; j += sk::kThreads) cr[2 + j] = A[(size_t)s_bl * LD + j];
+      LU_T(2);
       grid.sync();
+      LU_T(3);
       // the winner, identical in every CTA: thread g reads candidate g (all loads in
       // flight at once, L2 only: the buffer was written by other CTAs), then a warp
       // argmax and one over the NW warp results
@@ -252,6 +308,7 @@ __global__ void __launch_bounds__(sk::kThreads, 1) k_lupp(LuArgs a) {
         s_win = who;
       }
       __syncthreads();
+      LU_T(4);
       const int pb = par;
       par ^= 1;
       if (s_win < 0) {   // no active row left anywhere
@@ -281,9 +338,11 @@ __global__ void __launch_bounds__(sk::kThreads, 1) k_lupp(LuArgs a) {
         for (int j = s + 1; j < pw; ++j) ar[j] = __dsub_rn(ar[j], __dmul_rn(lv, Up[j]));
       }
       __syncthreads();
+      LU_T(5);
     }
     if (c < a.l) c = c0 + s;
     grid.sync();   // this panel's multipliers are read by every CTA in (1) of the next
+    LU_T(6);
   }
   if (blockIdx.x == 0 && tid == 0) a.out[0] = npiv;
 }
@@ -660,6 +719,18 @@ struct Ev {
 }  // namespace
 
 extern "C" {
+
+#ifdef LU_TRACE
+int rbrp_debug_lu_trace(long long* out, int reset) {
+  cudaDeviceSynchronize();
+  if (cudaMemcpyFromSymbol(out, g_lu_trace, sizeof(long long) * 8) != cudaSuccess) return RBRP_ECUDA;
+  if (reset) {
+    long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_lu_trace, z, sizeof(z));
+  }
+  return RBRP_OK;
+}
+#endif
 
 int rbrp_gaussian_embedding(int64_t d, int64_t l, uint64_t seed, double* OmegaT, int64_t ldo, void* stream) {
   if (d < 1 || l < 1 || ldo < d || !OmegaT) return RBRP_EINVAL;
