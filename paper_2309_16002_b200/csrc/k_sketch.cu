@@ -74,7 +74,8 @@ struct LuArgs {
   const double* Y;
   int64_t n, l, ldy;
   int k, R;
-  double* Lm;       // n x k multipliers
+  double* Lm;       // k x n multipliers, column-major: L(i, m) at Lm[m * n + i]
+  double* Lp;       // k x k row-major: the pivot rows' multipliers, Lp[m * k + mm] = L(p_m, mm)
   double* cand;     // [2][G][PW + 2]: |v|, row (bits), panel values of each CTA's candidate
   int64_t* piv;     // k
   int64_t* pcol;    // k
@@ -137,13 +138,13 @@ __global__ void __launch_bounds__(sk::kThreads, 1) k_lupp(LuArgs a) {
     {
       double u[PW];
       const bool own = tid < np0;
-      const int64_t prow = own ? spiv[tid] : 0;
+      const int64_t prow = own ? spiv[tid] : 0;   // U row tid = Y(p_tid, .) - ...
       if (own) {
         const double* yr = a.Y + prow * a.ldy + c0;
 #pragma unroll
         for (int j = 0; j < PW; ++j) u[j] = j < pw ? yr[j] : 0.0;
       }
-      const double* lr = a.Lm + prow * k;
+      const double* lr = a.Lp + (own ? tid : 0) * k;
       double lcur[LA1], lnext[LA1];
 #pragma unroll
       for (int t = 0; t < LA1; ++t) lcur[t] = (own && t < tid) ? lr[t] : 0.0;
@@ -183,11 +184,11 @@ __global__ void __launch_bounds__(sk::kThreads, 1) k_lupp(LuArgs a) {
       double rv[HW];
 #pragma unroll
       for (int j = 0; j < HW; ++j) rv[j] = j0 + j < pw ? yr[j] : 0.0;
-      const double* lr = a.Lm + (r0 + i) * k;
+      const double* lr = a.Lm + r0 + i;   // column-major: coalesced over the CTA's rows
       for (int mg = 0; mg < np0; mg += LA) {
         double lb[LA];
 #pragma unroll
-        for (int t = 0; t < LA; ++t) lb[t] = mg + t < np0 ? lr[mg + t] : 0.0;
+        for (int t = 0; t < LA; ++t) lb[t] = mg + t < np0 ? lr[(size_t)(mg + t) * a.n] : 0.0;
 #pragma unroll
         for (int t = 0; t < LA; ++t) {
           if (mg + t >= np0) break;
@@ -328,13 +329,16 @@ __global__ void __launch_bounds__(sk::kThreads, 1) k_lupp(LuArgs a) {
           a.pcol[m] = c0 + s;
         }
       }
+      // the owner files the new pivot row's multipliers for (1) of later panels
+      if (prow >= r0 && prow < r0 + nr)
+        for (int mm = tid; mm < m; mm += sk::kThreads) a.Lp[(size_t)m * k + mm] = a.Lm[(size_t)mm * a.n + prow];
       __syncthreads();
       const double pv = Up[s];
       for (int i = tid; i < nr; i += sk::kThreads) {
         if (!act[i]) continue;
         double* ar = A + (size_t)i * LD;
         const double lv = ar[s] / pv;
-        a.Lm[(r0 + i) * k + m] = lv;
+        a.Lm[(size_t)m * a.n + r0 + i] = lv;
         for (int j = s + 1; j < pw; ++j) ar[j] = __dsub_rn(ar[j], __dmul_rn(lv, Up[j]));
       }
       __syncthreads();
@@ -400,6 +404,21 @@ static cudaError_t launch_lupp(LuArgs a, int G, int PW, cudaStream_t s) {
     case 32: return go_lupp<32>(a, G, s);
     case 16: return go_lupp<16>(a, G, s);
     default: return go_lupp<8>(a, G, s);
+  }
+}
+
+// B (cols x rows, row-major) = A^T, A rows x cols row-major; 32 x 32 tiles through smem
+__global__ void k_transpose(const double* __restrict__ A, int64_t rows, int64_t cols, double* __restrict__ B) {
+  __shared__ double t[32][33];
+  const int64_t c0 = (int64_t)blockIdx.x * 32, r0 = (int64_t)blockIdx.y * 32;
+  for (int y = threadIdx.y; y < 32; y += 8) {
+    const int64_t r = r0 + y, c = c0 + threadIdx.x;
+    t[y][threadIdx.x] = (r < rows && c < cols) ? A[r * cols + c] : 0.0;
+  }
+  __syncthreads();
+  for (int y = threadIdx.y; y < 32; y += 8) {
+    const int64_t c = c0 + y, r = r0 + threadIdx.x;
+    if (c < cols && r < rows) B[c * rows + r] = t[threadIdx.x][y];
   }
 }
 
@@ -593,13 +612,15 @@ size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 int64_t round8(int64_t x) { return (x + 7) & ~int64_t(7); }
 
 struct LuLayout {
-  size_t Lm, cand, piv, pcol, out, total;
+  size_t Lm, Lp, cand, piv, pcol, out, total;
 };
-LuLayout lu_layout(int64_t n, int64_t k, int G, bool own_L) {
+LuLayout lu_layout(int64_t n, int64_t k, int G) {
   LuLayout L{};
   size_t o = 0;
-  L.Lm = own_L ? o : SIZE_MAX;
-  if (own_L) o += al256((size_t)n * k * 8);
+  L.Lm = o;
+  o += al256((size_t)n * k * 8);
+  L.Lp = o;
+  o += al256((size_t)k * k * 8);
   L.cand = o;
   o += al256((size_t)2 * G * (32 + 2) * 8);
   L.piv = o;
@@ -618,13 +639,15 @@ int lupp_check(int64_t n, int64_t l, int64_t ldy, int64_t k) {
 }
 
 // run the LUPP kernel; pivots copied to the host (synchronises the stream)
-int run_lupp(const double* Y, int64_t n, int64_t l, int64_t ldy, int64_t k, char* ws, double* Lm,
+// L_out (n x k row-major, optional): the multipliers, zero where a row was not active
+int run_lupp(const double* Y, int64_t n, int64_t l, int64_t ldy, int64_t k, char* ws, double* L_out,
              cudaStream_t s, int64_t* piv_h, int64_t* pcol_h, int64_t* npiv_h, int64_t** piv_dev) {
   int G, R, PW;
   if (!lupp_plan(n, (int)k, &G, &R, &PW)) return RBRP_ENOTSUP;
-  LuLayout Ly = lu_layout(n, k, G, Lm == nullptr);
-  if (!Lm) Lm = (double*)(ws + Ly.Lm);
-  if (cudaMemsetAsync(Lm, 0, (size_t)n * k * 8, s) != cudaSuccess) return RBRP_ECUDA;
+  LuLayout Ly = lu_layout(n, k, G);
+  double* Lm = (double*)(ws + Ly.Lm);
+  // the kernel reads only multipliers it wrote; zeros matter for the exported L only
+  if (L_out && cudaMemsetAsync(Lm, 0, (size_t)n * k * 8, s) != cudaSuccess) return RBRP_ECUDA;
   LuArgs a;
   a.Y = Y;
   a.n = n;
@@ -633,11 +656,16 @@ int run_lupp(const double* Y, int64_t n, int64_t l, int64_t ldy, int64_t k, char
   a.k = (int)k;
   a.R = R;
   a.Lm = Lm;
+  a.Lp = (double*)(ws + Ly.Lp);
   a.cand = (double*)(ws + Ly.cand);
   a.piv = (int64_t*)(ws + Ly.piv);
   a.pcol = (int64_t*)(ws + Ly.pcol);
   a.out = (int*)(ws + Ly.out);
   if (launch_lupp(a, G, PW, s) != cudaSuccess) return RBRP_ECUDA;
+  if (L_out) {
+    k_transpose<<<dim3((unsigned)((n + 31) / 32), (unsigned)((k + 31) / 32)), dim3(32, 8), 0, s>>>(Lm, k, n, L_out);
+    if (cudaGetLastError() != cudaSuccess) return RBRP_ECUDA;
+  }
   int np = 0;
   if (cudaMemcpyAsync(&np, a.out, sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess) return RBRP_ECUDA;
   if (cudaStreamSynchronize(s) != cudaSuccess) return RBRP_ECUDA;
@@ -663,7 +691,7 @@ SkLayout sk_layout(int64_t n, int64_t d, int64_t k, int64_t l) {
   L.Y = o;
   o += al256((size_t)n * L.lp * 8);
   L.lu = o;
-  o += lu_layout(n, k, G, true).total;
+  o += lu_layout(n, k, G).total;
   L.Z = o;
   o += al256((size_t)k * L.lp * 8);
   L.P = o;
@@ -745,7 +773,7 @@ int rbrp_lupp_workspace_size(int64_t n, int64_t l, int64_t k, size_t* bytes) {
   int rc = lupp_check(n, l, l, k);
   if (rc) return rc;
   if (!bytes) return RBRP_EINVAL;
-  *bytes = lu_layout(n, k, (int)std::min<int64_t>(sk_num_sms(), n), true).total;
+  *bytes = lu_layout(n, k, (int)std::min<int64_t>(sk_num_sms(), n)).total;
   return RBRP_OK;
 }
 
