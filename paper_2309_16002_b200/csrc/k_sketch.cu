@@ -86,6 +86,21 @@ __device__ __forceinline__ bool lu_better(double v, long long r, double bv, long
   return v > bv || (v == bv && r < br);
 }
 
+// warp argmax of (v, r) with owner tag `who` (< 0: no candidate); result in every lane
+__device__ __forceinline__ void lu_warp_best(double& v, long long& r, int& who) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+    const long long orr = __shfl_xor_sync(0xffffffffu, r, o);
+    const int og = __shfl_xor_sync(0xffffffffu, who, o);
+    if (og >= 0 && (who < 0 || lu_better(ov, orr, v, r))) {
+      v = ov;
+      r = orr;
+      who = og;
+    }
+  }
+}
+
 #ifdef LU_TRACE   // phase cycle counts of CTA 0 (debug builds: -DLU_TRACE)
 __device__ long long g_lu_trace[8];
 #define LU_T0() long long lu_t = clock64()
@@ -218,35 +233,22 @@ __global__ void __launch_bounds__(sk::kThreads, 1) k_lupp(LuArgs a) {
             br = r0 + i;
           }
         }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        const long long orr = __shfl_xor_sync(0xffffffffu, br, o);
-        const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
-        if (lu_better(ov, orr, bv, br)) {
-          bv = ov;
-          br = orr;
-          bl = ol;
-        }
-      }
+      lu_warp_best(bv, br, bl);
       if (lane == 0) {
         s_wv[w] = bv;
         s_wr[w] = br;
         s_wg[w] = bl;
       }
       __syncthreads();
-      if (tid == 0) {
-        double v = s_wv[0];
-        long long r = s_wr[0];
-        int li = s_wg[0];
-        for (int q = 1; q < NW; ++q)
-          if (lu_better(s_wv[q], s_wr[q], v, r)) {
-            v = s_wv[q];
-            r = s_wr[q];
-            li = s_wg[q];
-          }
-        s_bv = v;
-        s_bl = li;
+      if (w == 0) {
+        double v = lane < NW ? s_wv[lane] : -1.0;
+        long long r = lane < NW ? s_wr[lane] : LLONG_MAX;
+        int li = lane < NW ? s_wg[lane] : -1;
+        lu_warp_best(v, r, li);
+        if (lane == 0) {
+          s_bv = v;
+          s_bl = li;
+        }
       }
       __syncthreads();
       double* cr = a.cand + ((size_t)par * G + blockIdx.x) * CS;
@@ -276,17 +278,7 @@ __global__ void __launch_bounds__(sk::kThreads, 1) k_lupp(LuArgs a) {
             who = g;
           }
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const double ov = __shfl_xor_sync(0xffffffffu, v, o);
-          const long long orr = __shfl_xor_sync(0xffffffffu, r, o);
-          const int og = __shfl_xor_sync(0xffffffffu, who, o);
-          if (og >= 0 && (who < 0 || lu_better(ov, orr, v, r))) {
-            v = ov;
-            r = orr;
-            who = og;
-          }
-        }
+        lu_warp_best(v, r, who);
         if (lane == 0) {
           s_wv[w] = v;
           s_wr[w] = r;
@@ -294,19 +286,16 @@ __global__ void __launch_bounds__(sk::kThreads, 1) k_lupp(LuArgs a) {
         }
       }
       __syncthreads();
-      if (tid == 0) {
-        double v = -1.0;
-        long long r = LLONG_MAX;
-        int who = -1;
-        for (int q = 0; q < NW; ++q)
-          if (s_wg[q] >= 0 && (who < 0 || lu_better(s_wv[q], s_wr[q], v, r))) {
-            v = s_wv[q];
-            r = s_wr[q];
-            who = s_wg[q];
-          }
-        s_bv = v;
-        s_br = r;
-        s_win = who;
+      if (w == 0) {
+        double v = lane < NW ? s_wv[lane] : -1.0;
+        long long r = lane < NW ? s_wr[lane] : LLONG_MAX;
+        int who = lane < NW ? s_wg[lane] : -1;
+        lu_warp_best(v, r, who);
+        if (lane == 0) {
+          s_bv = v;
+          s_br = r;
+          s_win = who;
+        }
       }
       __syncthreads();
       LU_T(4);
