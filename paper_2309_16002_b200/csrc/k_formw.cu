@@ -58,13 +58,41 @@ __global__ void __launch_bounds__(32 * kTrinvWarps) k_trinv(const double* __rest
   const double xj = 1.0 / L1[j * k + j];   // fp64 math warp-uniform (single-lane fp64 is slow)
   if (lane == 0) x[j] = xj;
   __syncwarp();
+  // row i's segment L(i, j..i-1) (the first 32 NB of it) is loaded one step ahead, so
+  // the L2 latency overlaps the previous step's dot product and butterfly
+  constexpr int NB = 16;
+  double cur[NB], nxt[NB];
+  auto load_row = [&](int64_t i, double* buf) {
+#pragma unroll
+    for (int u = 0; u < NB; ++u) {
+      const int64_t m = j + lane + 32 * u;
+      buf[u] = m < i ? L1[i * k + m] : 0.0;
+    }
+  };
+  double dnext = 1.0;
+  if (j + 1 < k) {
+    load_row(j + 1, cur);
+    dnext = L1[(j + 1) * k + j + 1];
+  }
   for (int64_t i = j + 1; i < k; ++i) {
+    const double dii = dnext;
+    if (i + 1 < k) {
+      load_row(i + 1, nxt);
+      dnext = L1[(i + 1) * k + i + 1];
+    }
     double s = 0.0;
-    for (int64_t m = j + lane; m < i; m += 32) s += L1[i * k + m] * x[m];
+#pragma unroll
+    for (int u = 0; u < NB; ++u) {
+      const int64_t m = j + lane + 32 * u;
+      if (m < i) s += cur[u] * x[m];
+    }
+    for (int64_t m = j + 32 * NB + lane; m < i; m += 32) s += L1[i * k + m] * x[m];
     s = warp_sum(s);
-    const double xi = -s / L1[i * k + i];
+    const double xi = -s / dii;
     if (lane == 0) x[i] = xi;
     __syncwarp();
+#pragma unroll
+    for (int u = 0; u < NB; ++u) cur[u] = nxt[u];
   }
   for (int64_t m = lane; m < ldo; m += 32) LinvT[j * ldo + m] = (m < j || m >= k) ? T(0) : (T)x[m];
 }

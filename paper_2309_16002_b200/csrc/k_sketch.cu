@@ -422,16 +422,60 @@ __global__ void k_gather_rows(const double* __restrict__ Y, int64_t ldy, const i
   for (int64_t c = threadIdx.x; c < lp; c += blockDim.x) Z[(int64_t)i * lp + c] = y[c];
 }
 
-// G = Z Z^T (k x k), one output per thread, sequential dot over the l columns
-__global__ void k_gram_rows(const double* __restrict__ Z, int k, int64_t lp, double* __restrict__ G) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= k * k) return;
-  const int i = e / k, j = e - i * k;
-  const double* zi = Z + (int64_t)i * lp;
-  const double* zj = Z + (int64_t)j * lp;
-  double s = 0.0;
-  for (int64_t c = 0; c < lp; ++c) s = fma(zi[c], zj[c], s);
-  G[e] = s;
+// C (M x N, ldc) = sum_t A(i, t) B(t, j) with A(i, t) = A[i sa0 + t sa1], B(t, j) =
+// B[t sb0 + j sb1] (any transposition); tri = 1: A(i, t) = 0 for t > i, tri = 2: for t < i
+// (the zero triangle is neither read nor trusted); lower_only: tiles above the diagonal
+// of C skipped (a Gram matrix whose lower part is used).  32 x 32 tiles, K in chunks of 32
+// through smem, 2 x 2 outputs per thread; for the k x k and k x l steps of OSID.
+__global__ void __launch_bounds__(256) k_dgemm_small(const double* __restrict__ A, int64_t sa0, int64_t sa1,
+                                                     const double* __restrict__ B, int64_t sb0, int64_t sb1,
+                                                     double* __restrict__ C, int64_t ldc, int M, int N, int K,
+                                                     int tri, int lower_only) {
+  __shared__ double As[32][33], Bs[32][33];   // As[r][q] = A(i0 + r, t0 + q), Bs[r][q] = B(t0 + r, j0 + q)
+  const int bi = blockIdx.y, bj = blockIdx.x;
+  if (lower_only && bj > bi) return;
+  const int i0 = bi * 32, j0 = bj * 32;
+  const int t_lo = tri == 2 ? i0 : 0, t_hi = tri == 1 ? min(K, i0 + 32) : K;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const bool a_row = sa1 == 1, b_row = sb1 == 1;   // the contiguous index runs over the lanes
+  double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
+  for (int t0 = t_lo; t0 < t_hi; t0 += 32) {
+    for (int e = threadIdx.x; e < 1024; e += 256) {
+      const int f = e >> 5, g = e & 31;
+      {
+        const int r = a_row ? f : g, q = a_row ? g : f;
+        const int i = i0 + r, t = t0 + q;
+        const bool z = i >= M || t >= t_hi || (tri == 1 && t > i) || (tri == 2 && t < i);
+        As[r][q] = z ? 0.0 : A[(int64_t)i * sa0 + (int64_t)t * sa1];
+      }
+      {
+        const int r = b_row ? f : g, q = b_row ? g : f;
+        const int t = t0 + r, j = j0 + q;
+        Bs[r][q] = (t >= t_hi || j >= N) ? 0.0 : B[(int64_t)t * sb0 + (int64_t)j * sb1];
+      }
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int q = 0; q < 32; ++q) {
+      const double a0 = As[ty][q], a1 = As[ty + 16][q], b0 = Bs[q][tx], b1 = Bs[q][tx + 16];
+      c00 = fma(a0, b0, c00);
+      c01 = fma(a0, b1, c01);
+      c10 = fma(a1, b0, c10);
+      c11 = fma(a1, b1, c11);
+    }
+    __syncthreads();
+  }
+  const int i = i0 + ty, j = j0 + tx;
+  if (i < M && j < N) C[(int64_t)i * ldc + j] = c00;
+  if (i < M && j + 16 < N) C[(int64_t)i * ldc + j + 16] = c01;
+  if (i + 16 < M && j < N) C[(int64_t)(i + 16) * ldc + j] = c10;
+  if (i + 16 < M && j + 16 < N) C[(int64_t)(i + 16) * ldc + j + 16] = c11;
+}
+
+static void dgemm_small(const double* A, int64_t sa0, int64_t sa1, const double* B, int64_t sb0, int64_t sb1,
+                        double* C, int64_t ldc, int M, int N, int K, int tri, int lower_only, cudaStream_t s) {
+  k_dgemm_small<<<dim3((unsigned)((N + 31) / 32), (unsigned)((M + 31) / 32)), 256, 0, s>>>(
+      A, sa0, sa1, B, sb0, sb1, C, ldc, M, N, K, tri, lower_only);
 }
 
 // G = C C^T (Cholesky, C lower, k <= RBRP_SK_MAX_K) in one CTA; info = 1 if not positive
@@ -473,62 +517,78 @@ __global__ void __launch_bounds__(1024) k_chol_small(const double* __restrict__ 
 // lane i owns row i) and solves the rows below against it (a thread per row), then a
 // tile per 32 x 32 lower block of the trailing matrix applies C_below C_below^T.
 constexpr int kCholNB = 32;
-constexpr int kCholSmallK = 160;
+constexpr int kCholSmallK = 0;   // one-CTA k_chol_small kept for reference; blocked for every k
 
-__global__ void __launch_bounds__(512) k_chol_panel(double* __restrict__ C, int k, int j0, int* __restrict__ info) {
+// Panel j0: warp 0 of every CTA factors the diagonal block (lane i holds row i in
+// registers, column j's multipliers broadcast by shuffles), then each warp solves one row
+// below it: x D^T = g, x_q = (g_q - sum_{t<q} x_t D(q, t)) / D(q, q), t ascending.  The
+// diagonal block is read by every CTA, so the factor goes to Dbuf (copied into C after
+// the last panel) and C's diagonal block stays untouched until then; CTA 0 zeroes the
+// panel rows right of the block.
+__global__ void __launch_bounds__(256) k_chol_panel(double* __restrict__ C, int k, int j0,
+                                                    double* __restrict__ Dbuf, int* __restrict__ info) {
   __shared__ double D[kCholNB][kCholNB + 1];
-  const int jb = min(kCholNB, k - j0), tid = threadIdx.x;
-  for (int e = tid; e < jb * jb; e += blockDim.x) {
-    const int i = e / jb, q = e - i * jb;
-    D[i][q] = C[(size_t)(j0 + i) * k + j0 + q];
-  }
-  __syncthreads();
-  if (tid < 32) {
+  __shared__ double Dinv[kCholNB];
+  const int jb = min(kCholNB, k - j0), lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (w == 0) {
+    double r[kCholNB];
+    const double* src = C + (size_t)(j0 + min(lane, jb - 1)) * k + j0;
+#pragma unroll
+    for (int q = 0; q < kCholNB; ++q) r[q] = (lane < jb && q <= lane) ? src[q] : 0.0;
     bool bad = false;
-    for (int j = 0; j < jb; ++j) {
-      double dj = D[j][j];
-      if (!(dj > 0.0)) {
-        bad = true;
-        dj = 1.0;
+#pragma unroll
+    for (int j = 0; j < kCholNB; ++j) {
+      if (j < jb) {
+        double djj = __shfl_sync(0xffffffffu, r[j], j);
+        if (!(djj > 0.0)) {
+          bad = true;
+          djj = 1.0;
+        }
+        const double rs = rsqrt(djj);   // one reciprocal square root per step: the
+        r[j] = lane > j ? r[j] * rs : (lane == j ? djj * rs : 0.0);   // chain is 32 steps long
+#pragma unroll
+        for (int q = j + 1; q < kCholNB; ++q) {
+          const double lqj = __shfl_sync(0xffffffffu, r[j], q);
+          if (lane >= q) r[q] = fma(-r[j], lqj, r[q]);
+        }
       }
-      dj = sqrt(dj);
-      __syncwarp();
-      if (tid == j) D[j][j] = dj;
-      if (tid > j && tid < jb) D[tid][j] /= dj;
-      __syncwarp();
-      if (tid > j && tid < jb)
-        for (int q = j + 1; q <= tid; ++q) D[tid][q] = fma(-D[tid][j], D[q][j], D[tid][q]);
-      __syncwarp();
     }
-    if (tid == 0 && bad) *info = 1;
+    if (blockIdx.x == 0 && lane == 0 && bad) *info = 1;
+#pragma unroll
+    for (int q = 0; q < kCholNB; ++q) D[lane][q] = (lane < jb && q <= lane) ? r[q] : 0.0;
+    __syncwarp();
+    Dinv[lane] = lane < jb ? 1.0 / D[lane][lane] : 0.0;
   }
   __syncthreads();
-  for (int e = tid; e < jb * jb; e += blockDim.x) {
-    const int i = e / jb, q = e - i * jb;
-    C[(size_t)(j0 + i) * k + j0 + q] = q <= i ? D[i][q] : 0.0;
-  }
-  for (int e = tid; e < jb * (k - j0 - jb); e += blockDim.x) {   // upper part of the panel rows
-    const int i = e / (k - j0 - jb), q = e - i * (k - j0 - jb);
-    C[(size_t)(j0 + i) * k + j0 + jb + q] = 0.0;
-  }
-  // rows below: x D^T = g  ->  x_q = (g_q - sum_{t<q} x_t D(q, t)) / D(q, q)
-  for (int i = j0 + jb + tid; i < k; i += blockDim.x) {
-    double* row = C + (size_t)i * k + j0;
-    double x[kCholNB];
-#pragma unroll
-    for (int q = 0; q < kCholNB; ++q) x[q] = q < jb ? row[q] : 0.0;
-#pragma unroll
-    for (int q = 0; q < kCholNB; ++q) {
-      if (q < jb) {
-        double v = x[q];
-#pragma unroll
-        for (int t = 0; t < q; ++t) v = fma(-x[t], D[q][t], v);
-        x[q] = v / D[q][q];
-      }
+  if (blockIdx.x == 0) {
+    double* db = Dbuf + (size_t)(j0 / kCholNB) * kCholNB * kCholNB;
+    for (int e = threadIdx.x; e < kCholNB * kCholNB; e += blockDim.x) db[e] = D[e >> 5][e & 31];
+    const int wr = k - j0 - jb;
+    for (int e = threadIdx.x; e < jb * wr; e += blockDim.x) {
+      const int i = e / wr, q = e - i * wr;
+      C[(size_t)(j0 + i) * k + j0 + jb + q] = 0.0;
     }
+  }
+  const int i = j0 + kCholNB + blockIdx.x * 8 + w;
+  if (i >= k) return;
+  double* row = C + (size_t)i * k + j0;
+  double acc = row[lane];
+  double x = 0.0;
 #pragma unroll
-    for (int q = 0; q < kCholNB; ++q)
-      if (q < jb) row[q] = x[q];
+  for (int t = 0; t < kCholNB; ++t) {
+    if (lane == t) x = acc * Dinv[t];
+    const double xt = __shfl_sync(0xffffffffu, x, t);
+    if (lane > t) acc = fma(-xt, D[lane][t], acc);
+  }
+  row[lane] = x;
+}
+
+// the factored diagonal blocks from Dbuf into C (block b per CTA)
+__global__ void k_chol_diag_store(double* __restrict__ C, int k, const double* __restrict__ Dbuf) {
+  const int b = blockIdx.x, j0 = b * kCholNB, jb = min(kCholNB, k - j0);
+  for (int e = threadIdx.x; e < kCholNB * kCholNB; e += blockDim.x) {
+    const int r = e >> 5, q = e & 31;
+    if (r < jb && q < jb) C[(size_t)(j0 + r) * k + j0 + q] = Dbuf[(size_t)b * kCholNB * kCholNB + e];
   }
 }
 
@@ -555,41 +615,27 @@ __global__ void __launch_bounds__(1024) k_chol_update(double* __restrict__ C, in
   C[(size_t)i * k + q] = v;
 }
 
-// G (k x k) = C C^T, C lower with zeros above the diagonal; info = 1 if not positive definite
-static cudaError_t chol_blocked(const double* G, int k, double* C, int* info, cudaStream_t s, int* launches) {
+// G (k x k) = C C^T, C lower with zeros above the diagonal; info = 1 if not positive
+// definite.  Dbuf: ceil(k / 32) blocks of 32 x 32 doubles.
+static cudaError_t chol_blocked(const double* G, int k, double* C, double* Dbuf, int* info, cudaStream_t s,
+                                int* launches) {
   cudaError_t e = cudaMemcpyAsync(C, G, (size_t)k * k * 8, cudaMemcpyDeviceToDevice, s);
   if (e != cudaSuccess) return e;
   for (int j0 = 0; j0 < k; j0 += kCholNB) {
-    k_chol_panel<<<1, 512, 0, s>>>(C, k, j0, info);
+    const int m = k - j0 - kCholNB;   // rows below the diagonal block
+    k_chol_panel<<<m > 0 ? (m + 7) / 8 : 1, 256, 0, s>>>(C, k, j0, Dbuf, info);
     ++*launches;
-    const int m = k - j0 - kCholNB;
     if (m > 0) {
       const int nb = (m + kCholNB - 1) / kCholNB;
       k_chol_update<<<dim3(nb, nb), dim3(kCholNB, kCholNB), 0, s>>>(C, k, j0);
       ++*launches;
     }
   }
+  k_chol_diag_store<<<(k + kCholNB - 1) / kCholNB, 256, 0, s>>>(C, k, Dbuf);
+  ++*launches;
   return cudaGetLastError();
 }
 
-// out (k x lp) = op(A) B, A (k x k) triangular, op(A) = A (transA = 0) or A^T; one output
-// per thread, sequential dot over the nonzero range.  lowerA: A lower (else upper).
-__global__ void k_small_tri_mm(const double* __restrict__ A, int k, int transA, int lowerA,
-                               const double* __restrict__ B, int64_t lp, double* __restrict__ out) {
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= (int64_t)k * lp) return;
-  const int i = (int)(e / lp);
-  const int64_t c = e - (int64_t)i * lp;
-  // op(A)(i, j) nonzero for j <= i if op(A) is lower, j >= i if upper
-  const bool opLower = (lowerA != 0) != (transA != 0);
-  const int j0 = opLower ? 0 : i, j1 = opLower ? i : k - 1;
-  double s = 0.0;
-  for (int j = j0; j <= j1; ++j) {
-    const double a = transA ? A[(int64_t)j * k + i] : A[(int64_t)i * k + j];
-    s = fma(a, B[(int64_t)j * lp + c], s);
-  }
-  out[e] = s;
-}
 
 }  // namespace rbrp
 
@@ -667,7 +713,7 @@ int run_lupp(const double* Y, int64_t n, int64_t l, int64_t ldy, int64_t k, char
 }
 
 struct SkLayout {
-  size_t OmT, Y, lu, Z, P, G, C1, C2, A1T, A2T, st, gsc, info, total;
+  size_t OmT, Y, lu, Z, P, G, C1, C2, A1T, A2T, st, gsc, Db, info, total;
   int64_t lp;
 };
 SkLayout sk_layout(int64_t n, int64_t d, int64_t k, int64_t l) {
@@ -699,6 +745,8 @@ SkLayout sk_layout(int64_t n, int64_t d, int64_t k, int64_t l) {
   o += al256((size_t)k * k * 8);
   L.C2 = o;
   o += al256((size_t)k * k * 8);
+  L.Db = o;
+  o += al256((size_t)((k + 31) / 32) * 32 * 32 * 8);
   L.info = o;
   o += 256;
   L.total = o;
@@ -805,6 +853,7 @@ int rbrp_sketch_id(const double* X, int64_t n, int64_t d, int64_t ldx, int64_t k
   double* C1 = (double*)(ws + Ly.C1);
   double* C2 = (double*)(ws + Ly.C2);
   int* info = (int*)(ws + Ly.info);
+  double* Dbuf = (double*)(ws + Ly.Db);
   const bool prof = rep && rep->profile;
   int launches = 0;
   cudaEvent_t t0, t1;
@@ -862,24 +911,23 @@ int rbrp_sketch_id(const double* X, int64_t n, int64_t d, int64_t ldx, int64_t k
     if (small) SK(cudaFuncSetAttribute(k_chol_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
     SK(cudaMemsetAsync(info, 0, sizeof(int), s));
     SK(cudaMemsetAsync(dst, 0, sizeof(DevState), s));
-    const unsigned gm = (unsigned)(((int64_t)kk * lp + 255) / 256), gg = (unsigned)((kk * kk + 255) / 256);
     auto chol = [&](double* Cout) -> cudaError_t {   // Gm = Cout Cout^T
-      if (!small) return chol_blocked(Gm, kk, Cout, info, s, &launches);
+      if (!small) return chol_blocked(Gm, kk, Cout, Dbuf, info, s, &launches);
       k_chol_small<<<1, 1024, csm, s>>>(Gm, kk, Cout, info);
       ++launches;
       return cudaGetLastError();
     };
     k_gather_rows<<<kk, 256, 0, s>>>(Y, lp, Sdev, kk, lp, Z);          // Z = Y(S,:)
-    k_gram_rows<<<gg, 256, 0, s>>>(Z, kk, lp, Gm);                      // G1 = Z Z^T
+    dgemm_small(Z, lp, 1, Z, 1, lp, Gm, kk, kk, kk, (int)lp, 0, 1, s);   // G1 = Z Z^T (lower part)
     SK(chol(C1));                                                       // G1 = C1 C1^T (R1 = C1^T)
     SK(launch_trinv<double>(C1, kk, A1T, kk, dst, s));                 // A1T = C1^{-T}
-    k_small_tri_mm<<<gm, 256, 0, s>>>(A1T, kk, 1, 0, Z, lp, P);        // P1 = C1^{-1} Z = Q1^T
-    k_gram_rows<<<gg, 256, 0, s>>>(P, kk, lp, Gm);                      // G2 = P1 P1^T
+    dgemm_small(A1T, 1, kk, Z, lp, 1, P, lp, kk, (int)lp, kk, 1, 0, s);  // P1 = C1^{-1} Z = A1T^T Z = Q1^T
+    dgemm_small(P, lp, 1, P, 1, lp, Gm, kk, kk, kk, (int)lp, 0, 1, s);   // G2 = P1 P1^T
     SK(chol(C2));                                                       // G2 = C2 C2^T (R2 = C2^T)
     SK(launch_trinv<double>(C2, kk, A2T, kk, dst, s));                 // A2T = C2^{-T}
-    k_small_tri_mm<<<gm, 256, 0, s>>>(A2T, kk, 1, 0, P, lp, Z);        // Q^T = C2^{-1} P1
-    k_small_tri_mm<<<gm, 256, 0, s>>>(A2T, kk, 0, 0, Z, lp, P);        // R2^{-1} Q^T
-    k_small_tri_mm<<<gm, 256, 0, s>>>(A1T, kk, 0, 0, P, lp, Z);        // M^T = R1^{-1} R2^{-1} Q^T
+    dgemm_small(A2T, 1, kk, P, lp, 1, Z, lp, kk, (int)lp, kk, 1, 0, s);  // Q^T = C2^{-1} P1
+    dgemm_small(A2T, kk, 1, Z, lp, 1, P, lp, kk, (int)lp, kk, 2, 0, s);  // R2^{-1} Q^T (A2T upper)
+    dgemm_small(A1T, kk, 1, P, lp, 1, Z, lp, kk, (int)lp, kk, 2, 0, s);  // M^T = R1^{-1} R2^{-1} Q^T
     SK(cudaGetLastError());
     launches += 9;
     if (gemm_lp_supported(Y, lp, Z, lp, lp)) {                                         // W = Y M
