@@ -664,14 +664,14 @@ size_t gemm_lp_scratch_bytes(int64_t N, int64_t K) {
 
 // K >= 512: the per-tile fold of the 4-way K split is amortised over >= 8 chunk steps
 // (measured: W = L L_1^{-1} at K = 128 and the OSID W at K = 384 ran slower than k_nt_mma)
-bool gemm_lp_supported(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t K) {
-  return K >= 512 && lhat_paper_max_bucket(A, lda, K) >= 32 && ldb == K && ((uintptr_t)B % 16) == 0;
+bool gemm_lp_supported(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t K, int64_t min_k) {
+  return K >= min_k && lhat_paper_max_bucket(A, lda, K) >= 32 && ldb == K && ((uintptr_t)B % 16) == 0;
 }
 
 cudaError_t gemm_nt_lp(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
-                       int64_t M, int64_t N, int64_t K, void* scratch, cudaStream_t s, bool lower_b) {
+                       int64_t M, int64_t N, int64_t K, void* scratch, cudaStream_t s, bool lower_b, int64_t min_k) {
   if (M <= 0 || N <= 0) return cudaSuccess;
-  if (!gemm_lp_supported(A, lda, B, ldb, K)) return cudaErrorNotSupported;
+  if (!gemm_lp_supported(A, lda, B, ldb, K, min_k)) return cudaErrorNotSupported;
   double* Qp = (double*)scratch;
   DevState* st = (DevState*)((char*)scratch + ((fused_pack_bytes(K) + 255) & ~(size_t)255));
   const int64_t G = (N + 31) / 32;

@@ -19,7 +19,8 @@
 //   OSID         Z = Y(S,:) (k x l); CholQR2 of Z^T: G1 = Z Z^T = C1 C1^T, P1 = C1^{-1} Z,
 //                G2 = P1 P1^T = C2 C2^T, Q^T = C2^{-1} P1; M^T = (R2 R1)^{-1} Q^T with
 //                R = C2^T C1^T, so W = Y M = (Y Q) R^{-T} (Alg. 4 l.4) = Y Y_S^+; then
-//                W(S,:) = I_k (l.3).  Small k x k / k x l steps are CUDA-core kernels;
+//                W(S,:) = I_k (l.3).  The k x k / k x l steps (Gram, blocked Cholesky,
+//                triangular products) are CUDA-core kernels;
 //                W = Y M is the FP64 tensor-path GEMM again.
 #include <cooperative_groups.h>
 #include <math.h>
@@ -478,46 +479,11 @@ static void dgemm_small(const double* A, int64_t sa0, int64_t sa1, const double*
       A, sa0, sa1, B, sb0, sb1, C, ldc, M, N, K, tri, lower_only);
 }
 
-// G = C C^T (Cholesky, C lower, k <= RBRP_SK_MAX_K) in one CTA; info = 1 if not positive
-// definite
-__global__ void __launch_bounds__(1024) k_chol_small(const double* __restrict__ G, int k, double* __restrict__ C,
-                                                     int* __restrict__ info) {
-  extern __shared__ double cs[];   // k x (k + 1)
-  const int ld = k + 1, tid = threadIdx.x, nt = blockDim.x;
-  for (int e = tid; e < k * k; e += nt) cs[(e / k) * ld + e % k] = G[e];
-  __shared__ int bad;
-  if (tid == 0) bad = 0;
-  __syncthreads();
-  for (int j = 0; j < k; ++j) {
-    if (tid == 0) {
-      const double dj = cs[j * ld + j];
-      if (!(dj > 0.0)) bad = 1;
-      cs[j * ld + j] = sqrt(dj > 0.0 ? dj : 1.0);
-    }
-    __syncthreads();
-    const double djj = cs[j * ld + j];
-    for (int i = j + 1 + tid; i < k; i += nt) cs[i * ld + j] /= djj;
-    __syncthreads();
-    const int m = k - j - 1;
-    for (int e = tid; e < m * m; e += nt) {
-      const int i = j + 1 + e / m, q = j + 1 + e % m;
-      if (q <= i) cs[i * ld + q] = fma(-cs[i * ld + j], cs[q * ld + j], cs[i * ld + q]);
-    }
-    __syncthreads();
-  }
-  for (int e = tid; e < k * k; e += nt) {
-    const int i = e / k, j = e % k;
-    C[e] = j <= i ? cs[i * ld + j] : 0.0;
-  }
-  if (tid == 0 && bad) *info = 1;
-}
-
-// Blocked right-looking Cholesky for k > kCholSmallK (C = G's lower factor, in place in
-// C after a copy of G): per 32-column panel, one CTA factors the diagonal block (warp 0,
-// lane i owns row i) and solves the rows below against it (a thread per row), then a
-// tile per 32 x 32 lower block of the trailing matrix applies C_below C_below^T.
+// Blocked right-looking Cholesky (C = G's lower factor, in place in C after a copy of G):
+// per 32-column panel, k_chol_panel factors the diagonal block and solves the rows below
+// it (a warp per row), then k_chol_update applies C_below C_below^T to the trailing
+// matrix, a CTA per 32 x 32 lower block.
 constexpr int kCholNB = 32;
-constexpr int kCholSmallK = 0;   // one-CTA k_chol_small kept for reference; blocked for every k
 
 // Panel j0: warp 0 of every CTA factors the diagonal block (lane i holds row i in
 // registers, column j's multipliers broadcast by shuffles), then each warp solves one row
@@ -906,16 +872,10 @@ int rbrp_sketch_id(const double* X, int64_t n, int64_t d, int64_t ldx, int64_t k
     double* A1T = (double*)(ws + Ly.A1T);
     double* A2T = (double*)(ws + Ly.A2T);
     DevState* dst = (DevState*)(ws + Ly.st);
-    const size_t csm = (size_t)kk * (kk + 1) * 8;
-    const bool small = kk <= kCholSmallK;
-    if (small) SK(cudaFuncSetAttribute(k_chol_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
     SK(cudaMemsetAsync(info, 0, sizeof(int), s));
     SK(cudaMemsetAsync(dst, 0, sizeof(DevState), s));
     auto chol = [&](double* Cout) -> cudaError_t {   // Gm = Cout Cout^T
-      if (!small) return chol_blocked(Gm, kk, Cout, Dbuf, info, s, &launches);
-      k_chol_small<<<1, 1024, csm, s>>>(Gm, kk, Cout, info);
-      ++launches;
-      return cudaGetLastError();
+      return chol_blocked(Gm, kk, Cout, Dbuf, info, s, &launches);
     };
     k_gather_rows<<<kk, 256, 0, s>>>(Y, lp, Sdev, kk, lp, Z);          // Z = Y(S,:)
     dgemm_small(Z, lp, 1, Z, 1, lp, Gm, kk, kk, kk, (int)lp, 0, 1, s);   // G1 = Z Z^T (lower part)
@@ -930,8 +890,8 @@ int rbrp_sketch_id(const double* X, int64_t n, int64_t d, int64_t ldx, int64_t k
     dgemm_small(A1T, kk, 1, P, lp, 1, Z, lp, kk, (int)lp, kk, 2, 0, s);  // M^T = R1^{-1} R2^{-1} Q^T
     SK(cudaGetLastError());
     launches += 9;
-    if (gemm_lp_supported(Y, lp, Z, lp, lp)) {                                         // W = Y M
-      SK(gemm_nt_lp(Y, lp, Z, lp, W_out, k, n, kk, lp, gsc, s));
+    if (gemm_lp_supported(Y, lp, Z, lp, lp, 256)) {                                   // W = Y M
+      SK(gemm_nt_lp(Y, lp, Z, lp, W_out, k, n, kk, lp, gsc, s, false, 256));
       launches += 2 * (kk + 31) / 32;
     } else {
       if (!gemm_nt_mma(Y, lp, Z, lp, W_out, k, n, kk, lp, s, &ge)) return RBRP_ENOTSUP;

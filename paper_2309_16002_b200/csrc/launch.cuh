@@ -143,11 +143,15 @@ bool gemm_nt_mma(const double* A, int64_t lda, const double* B, int64_t ldb, dou
 // k_lhat_paper.cu: C = A B^T by read-only L-hat passes of 32 columns (B: N x K, ldb == K);
 // scratch >= gemm_lp_scratch_bytes(N, K), 256-byte aligned
 size_t gemm_lp_scratch_bytes(int64_t N, int64_t K);
-bool gemm_lp_supported(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t K);
+// min_k: smallest K for which the pass structure beats k_nt_mma (512 for the W GEMMs of
+// the ID, 256 for OSID's W = Y M whose K = l is larger relative to N = k)
+bool gemm_lp_supported(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t K,
+                       int64_t min_k = 512);
 // lower_b: B(j, m) = 0 for m < j (B = L_1^{-T} of W): each 32-column group starts its K
 // range at the 64-column chunk holding its first nonzero (about half the work)
 cudaError_t gemm_nt_lp(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
-                       int64_t M, int64_t N, int64_t K, void* scratch, cudaStream_t s, bool lower_b = false);
+                       int64_t M, int64_t N, int64_t K, void* scratch, cudaStream_t s, bool lower_b = false,
+                       int64_t min_k = 512);
 
 // k_formw.cu — Alg. 3 by triangular solve
 template <typename T>
