@@ -38,6 +38,7 @@ namespace cg = cooperative_groups;
 namespace rbrp {
 namespace sk {
 constexpr int kThreads = 512;   // >= RBRP_SK_MAX_K: one U row per thread in (1)
+constexpr int kCandPerLane = 5;   // winner search: 160 candidates per pass of warp 0
 constexpr int kSmemMax = 227 * 1024;
 constexpr uint32_t kOmegaTag = 0x4F4D4547u;   // reading R25
 static_assert(kThreads >= RBRP_SK_MAX_K, "k_lupp step (1) holds one U row per thread");
@@ -133,7 +134,7 @@ __global__ void __launch_bounds__(sk::kThreads, 1) k_lupp(LuArgs a) {
   __shared__ long long s_wr[NW];
   __shared__ int s_wg[NW];
   __shared__ double s_bv;
-  __shared__ int s_bl, s_win;
+  __shared__ int s_win;
   __shared__ long long s_br;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int64_t r0 = (int64_t)blockIdx.x * R;
@@ -241,56 +242,48 @@ __global__ void __launch_bounds__(sk::kThreads, 1) k_lupp(LuArgs a) {
         s_wg[w] = bl;
       }
       __syncthreads();
+      // warp 0: the CTA's candidate (|v|, row, its pw <= 32 panel values); the grid barrier
+      // below starts with a CTA barrier
       if (w == 0) {
         double v = lane < NW ? s_wv[lane] : -1.0;
         long long r = lane < NW ? s_wr[lane] : LLONG_MAX;
         int li = lane < NW ? s_wg[lane] : -1;
         lu_warp_best(v, r, li);
+        double* cr = a.cand + ((size_t)par * G + blockIdx.x) * CS;
+        if (li >= 0 && lane < pw) cr[2 + lane] = A[(size_t)li * LD + lane];
         if (lane == 0) {
-          s_bv = v;
-          s_bl = li;
+          cr[0] = v;
+          cr[1] = __longlong_as_double(li >= 0 ? (long long)(r0 + li) : -1ll);
         }
       }
-      __syncthreads();
-      double* cr = a.cand + ((size_t)par * G + blockIdx.x) * CS;
-      if (tid == 0) {
-        cr[0] = s_bv;
-        cr[1] = __longlong_as_double(s_bl >= 0 ? (long long)(r0 + s_bl) : -1ll);
-      }
-      if (s_bl >= 0)
-        for (int j = tid; j < pw; j += sk::kThreads) cr[2 + j] = A[(size_t)s_bl * LD + j];
       LU_T(2);
       grid.sync();
       LU_T(3);
-      // the winner, identical in every CTA: thread g reads candidate g (all loads in
-      // flight at once, L2 only: the buffer was written by other CTAs), then a warp
-      // argmax and one over the NW warp results
-      {
+      // the winner, identical in every CTA: warp 0 reads every candidate through L2 (lane
+      // l takes candidates l, l + 32, ...; all loads issued before the compares), then a
+      // warp argmax
+      if (w == 0) {
         double v = -1.0;
         long long r = LLONG_MAX;
         int who = -1;
-        for (int g = tid; g < G; g += sk::kThreads) {
-          const double* q = a.cand + ((size_t)par * G + g) * CS;
-          const double qv = __ldcg(q);
-          const long long qr = __double_as_longlong(__ldcg(q + 1));
-          if (qr >= 0 && lu_better(qv, qr, v, r)) {
-            v = qv;
-            r = qr;
-            who = g;
+        for (int gb = 0; gb < G; gb += 32 * sk::kCandPerLane) {
+          double qv[sk::kCandPerLane];
+          long long qr[sk::kCandPerLane];
+#pragma unroll
+          for (int u = 0; u < sk::kCandPerLane; ++u) {
+            const int g = gb + lane + 32 * u;
+            const double* q = a.cand + ((size_t)par * G + g) * CS;
+            qv[u] = g < G ? __ldcg(q) : -1.0;
+            qr[u] = g < G ? __double_as_longlong(__ldcg(q + 1)) : -1ll;
           }
+#pragma unroll
+          for (int u = 0; u < sk::kCandPerLane; ++u)
+            if (qr[u] >= 0 && lu_better(qv[u], qr[u], v, r)) {
+              v = qv[u];
+              r = qr[u];
+              who = gb + lane + 32 * u;
+            }
         }
-        lu_warp_best(v, r, who);
-        if (lane == 0) {
-          s_wv[w] = v;
-          s_wr[w] = r;
-          s_wg[w] = who;
-        }
-      }
-      __syncthreads();
-      if (w == 0) {
-        double v = lane < NW ? s_wv[lane] : -1.0;
-        long long r = lane < NW ? s_wr[lane] : LLONG_MAX;
-        int who = lane < NW ? s_wg[lane] : -1;
         lu_warp_best(v, r, who);
         if (lane == 0) {
           s_bv = v;
