@@ -285,6 +285,19 @@ __global__ void __launch_bounds__(sk::kThreads, 1) k_lupp(LuArgs a) {
             }
         }
         lu_warp_best(v, r, who);
+        // the winner's panel values and the bookkeeping, before the CTA barrier
+        if (who >= 0 && v > 0.0) {
+          const double* q = a.cand + ((size_t)par * G + who) * CS;
+          if (lane < pw) Up[lane] = __ldcg(q + 2 + lane);
+          if (lane == 0) {
+            spiv[npiv] = r;
+            if (r >= r0 && r < r0 + nr) act[r - r0] = 0;
+            if (blockIdx.x == 0) {
+              a.piv[npiv] = r;
+              a.pcol[npiv] = c0 + s;
+            }
+          }
+        }
         if (lane == 0) {
           s_bv = v;
           s_br = r;
@@ -293,7 +306,6 @@ __global__ void __launch_bounds__(sk::kThreads, 1) k_lupp(LuArgs a) {
       }
       __syncthreads();
       LU_T(4);
-      const int pb = par;
       par ^= 1;
       if (s_win < 0) {   // no active row left anywhere
         c = a.l;
@@ -302,20 +314,9 @@ __global__ void __launch_bounds__(sk::kThreads, 1) k_lupp(LuArgs a) {
       if (!(s_bv > 0.0)) continue;   // exactly zero active column: skipped (no pivot)
       const long long prow = s_br;
       const int m = npiv++;
-      const double* q = a.cand + ((size_t)pb * G + s_win) * CS;
-      for (int j = tid; j < pw; j += sk::kThreads) Up[j] = __ldcg(q + 2 + j);
-      if (tid == 0) {
-        spiv[m] = prow;
-        if (prow >= r0 && prow < r0 + nr) act[prow - r0] = 0;
-        if (blockIdx.x == 0) {
-          a.piv[m] = prow;
-          a.pcol[m] = c0 + s;
-        }
-      }
       // the owner files the new pivot row's multipliers for (1) of later panels
       if (prow >= r0 && prow < r0 + nr)
         for (int mm = tid; mm < m; mm += sk::kThreads) a.Lp[(size_t)m * k + mm] = a.Lm[(size_t)mm * a.n + prow];
-      __syncthreads();
       const double pv = Up[s];
       for (int i = tid; i < nr; i += sk::kThreads) {
         if (!act[i]) continue;
