@@ -9,8 +9,9 @@
     short (rank-deficient) case;
   * sketch_id: S equal to the oracle's; W = Y Y_S^+ within 1e-9 relative (CholQR2 on the
     GPU vs Householder QR in the oracle); W(S,:) = I exactly; exact-rank recovery;
-  * full size (c2, k = 128, l = 3k): outputs the oracle computes row by row (W rows from
-    Y(i,:) Y_S^+) and the skeletonization error.
+  * full size (c2, k = 128, l = 3k; Table 3's GMM at k = 472, l = 1416 > d): outputs
+    computed row by row on the host (W rows from Y(i,:) Y_S^+), W(S,:) = I, the
+    skeletonization error, and |L| <= 1 for the exported multipliers.
 """
 import numpy as np
 import pytest
@@ -172,3 +173,30 @@ def test_sketch_id_full_c2():
     resid = float((Xd - (Xd @ B) @ B.T).pow(2).sum() / Xd.pow(2).sum())
     assert resid <= 1e-12
     assert set(res.ms_phase) == {"embedding", "sketch", "lupp", "osid"}
+
+
+@cuda
+def test_sketch_id_table3_full_rank_472():
+    """Table 3's GMM (1e5 x 1e3, 100 clusters) at its largest rank k = 472, l = 3k = 1416 > d
+    (the blocked Cholesky, 16-column LUPP panels and the l > d sketch at full size): W(S,:) =
+    I, sampled rows of W equal Y(i,:) Y_S^+ from a host pseudo-inverse of the same sketch,
+    and every LUPP multiplier has |l| <= 1 (partial pivoting)."""
+    cfg = CONFIGS["t3"]
+    X = make(cfg, device="cuda")
+    k, l = 472, 1416
+    OmT = _sk().gaussian_embedding(cfg.d, l, seed=7)
+    res = _sk().sketch_id(X, k, l, omega_T=OmT)
+    S = res.S.tolist()
+    assert res.k == k and len(set(S)) == k
+    Sd = res.S.cuda()
+    assert torch.equal(res.W[Sd], torch.eye(k, dtype=torch.float64, device="cuda"))
+    Om = OmT.T.cpu().numpy()
+    Ys = X[Sd].cpu().numpy() @ Om
+    M = np.linalg.pinv(Ys)
+    rows = np.random.default_rng(8).choice(cfg.n, 32, replace=False)
+    Yr = X[torch.as_tensor(rows, device="cuda")].cpu().numpy() @ Om
+    ref = Yr @ M
+    Wr = res.W[torch.as_tensor(rows, device="cuda")].cpu().numpy()
+    assert np.linalg.norm(Wr - ref) <= 1e-7 * np.linalg.norm(ref)
+    g = _sk().lupp(X @ OmT.T, k, with_L=True)    # a cuBLAS sketch: pivots may differ on ties
+    assert len(g.piv) == k and float(g.L.abs().max()) <= 1.0
