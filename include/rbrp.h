@@ -65,9 +65,14 @@ enum {
 enum {
   RBRP_F_TOL_UNREACHED = 1,     /* k_max reached before tau */
   RBRP_F_ZERO_BLOCK = 2,        /* the filter kept no column: V numerically zero */
-  RBRP_F_W_CLIPPED = 4,         /* min |diag L_1| < 1e-12 max |diag L_1| (Remark 5.2) */
+  RBRP_F_W_CLIPPED = 4,         /* min |diag L_1| < 1e-12 max |diag L_1| (Remark 5.2):
+                                   W was formed from the clipped pseudo-inverse of L_1
+                                   (singular values < 1e-12 sigma_max discarded) instead of
+                                   the triangular solve */
   RBRP_F_SUPPORT_EXHAUSTED = 8, /* fewer than b_t rows had positive weight */
-  RBRP_F_NEAR_TIE = 16          /* reserved for replay diagnostics */
+  RBRP_F_NEAR_TIE = 16          /* replay: at least one block ran with forced pivots (blocks
+                                   whose logged pivot margin is below the contract's delta,
+                                   SURVEY §8(c)); see replay_pivots */
 };
 
 /*
@@ -101,7 +106,9 @@ enum {
  *              forced candidate blocks S_t (global row ids, concatenated; block t has
  *              replay_lens[t] entries).  The run ends when they are exhausted.
  *   replay_pivots (host, optional): forced local pivot order per block (positions into
- *              the block, concatenated like replay_blocks).
+ *              the block, concatenated like replay_blocks).  A block whose first entry is
+ *              negative is not forced: the GPU's own pivoted QR picks its pivots (the
+ *              NEAR_TIE rule: force only the blocks whose pivot margin is below delta).
  */
 typedef struct {
   rbrp_dtype dtype;
@@ -151,6 +158,9 @@ typedef struct {
  *              node), 0 if it was launched eagerly (replay, profile, or graphs unusable).
  *   proj_ms_blk (optional, caller array of max_blocks floats, NULL to skip) the projection
  *              device time of each logged block (same stamps as proj_ms).
+ *   d_out      (optional, DEVICE array of n_local doubles, NULL to skip) the final
+ *              residual squared row norms d^(t)(i) of this rank's rows (Alg. 2 l.16;
+ *              0 on skeleton rows).  rbrp_id_sharded: only with one shard.
  */
 typedef struct {
   int64_t k;
@@ -172,6 +182,7 @@ typedef struct {
   float proj_ms;
   int32_t graph;
   float* proj_ms_blk;
+  double* d_out;
 } rbrp_report;
 
 /* Opaque NCCL communicator wrapper; NULL means a single-GPU call. */
@@ -223,6 +234,23 @@ int rbrp_id(const rbrp_problem* p, void* X, void* workspace, size_t ws_bytes,
             rbrp_comm* comm, void* stream, int64_t* S_out, void* W_out, rbrp_report* rep);
 
 /*
+ * rbrp_id_host — end-to-end call with HOST buffers: copies X (host, n_local x d, leading
+ * dimension ld; pinned memory gives full PCIe bandwidth) into a private device copy inside
+ * the workspace, runs rbrp_id on it in place (the copy becomes the residual; X_host is
+ * never written), and copies W (the first k columns) back into W_host.
+ *   X_host     host, n_local x ld elements of dtype.
+ *   workspace  device, >= rbrp_workspace_size_host(p) bytes (X copy + W + rbrp_id's
+ *              workspace with RBRP_INPLACE), 256-byte aligned.
+ *   W_host     host, n_local x k_cap row-major (ld = k_cap) or NULL; columns >= k untouched
+ *              (with rep == NULL all k_cap columns are copied).
+ *   S_out, comm, stream, rep: as rbrp_id.  Returns after the W copy has completed.
+ * Errors as rbrp_id.
+ */
+int rbrp_workspace_size_host(const rbrp_problem* p, size_t* bytes);
+int rbrp_id_host(const rbrp_problem* p, const void* X_host, void* workspace, size_t ws_bytes,
+                 rbrp_comm* comm, void* stream, int64_t* S_out, void* W_host, rbrp_report* rep);
+
+/*
  * rbrp_id_sharded — the row-sharded algorithm of a multi-GPU run for
  * `nshards` contiguous row shards held on the CURRENT device by one process: the same
  * kernels and exchange points as `nshards` ranks of rbrp_id with a communicator, with the
@@ -243,6 +271,32 @@ int rbrp_id(const rbrp_problem* p, void* X, void* workspace, size_t ws_bytes,
 int rbrp_id_sharded(const rbrp_problem* p, int nshards, const int64_t* shard_rows, void* const* X,
                     void* const* workspace, size_t ws_bytes, void* stream, int64_t* S_out,
                     void* const* W_out, rbrp_report* rep);
+
+/*
+ * rbrp_form_w — Alg. 3 on its own: the interpolation matrix from the L and S
+ * of a pivoting run.  W(S,:) = I_k (Alg. 3 l.2); W(rest,:) = L_2 L_1^{-1} with L_1 =
+ * L(S,:), L_2 = the other rows.
+ *   dtype      element type of L and W.  L_1's inverse / pseudo-inverse is computed in fp64.
+ *   L          device, n x k row-major with leading dimension ldl >= k (read only).
+ *   n          rows of L and W (>= k).
+ *   S          host int64[k]: distinct row ids in [0, n), selection order.
+ *   method     0 = auto: triangular solve, unless min |diag L_1| < 1e-12 max
+ *              |diag L_1| -- then the clipped SVD of Remark 5.2 (reading R17);
+ *              1 = triangular solve (L_1 must be lower-triangular, as rbrp_id's L is);
+ *              2 = clipped SVD: L_1^{-1} := pinv(L_1) with singular values < 1e-12 sigma_max
+ *              discarded (one-sided Jacobi SVD in fp64; any L_1).
+ *   W_out      device, n x ldw row-major (ldw >= k); columns >= k untouched.
+ *   workspace  device, >= rbrp_form_w_workspace_size() bytes, 256-byte aligned.
+ *   stream     cudaStream_t as void*.  The call blocks the host until W is complete.
+ *   flags      host (optional): RBRP_F_W_CLIPPED if the clipped SVD was used.
+ *   nclip      host (optional): number of singular values discarded (0 for the solve).
+ * Errors: RBRP_EINVAL (k < 1, n < k, ldl or ldw < k, S out of range, NULL pointers,
+ * method not 0..2, misaligned workspace), RBRP_ENOMEM, RBRP_ECUDA.
+ */
+int rbrp_form_w_workspace_size(rbrp_dtype dtype, int64_t k, size_t* bytes);
+int rbrp_form_w(rbrp_dtype dtype, const void* L, int64_t ldl, int64_t n, const int64_t* S, int64_t k,
+                int32_t method, void* W_out, int64_t ldw, void* workspace, size_t ws_bytes, void* stream,
+                uint32_t* flags, int32_t* nclip);
 
 /* Human-readable name of a status code (static string; never NULL). */
 const char* rbrp_strerror(int status);

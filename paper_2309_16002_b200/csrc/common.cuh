@@ -3,6 +3,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+#include <mutex>
+
 #include "../../include/rbrp.h"
 
 namespace rbrp {
@@ -37,6 +40,8 @@ struct DevState {
   int64_t jb;         // distributed sampling: next Philox draw index of the block
   int32_t sample_c;   // distributed sampling: candidates accepted so far
   int32_t sample_done;
+  double ldiag_min;   // min / max |L_1(i,i)| = |R_V(i,i)| over the kept skeletons (k_fixup);
+  double ldiag_max;   // the Remark 5.2 trigger of the clipped-pinv W (reading R17)
 };
 
 __device__ __forceinline__ long long gtimer() {
@@ -79,6 +84,39 @@ __device__ __forceinline__ double warp_sum(double v) {
 template <typename T> struct VecT;
 template <> struct VecT<double> { using v2 = double2; };
 template <> struct VecT<float> { using v2 = float2; };
+
+// One-time per-device host initialisation (kernel attributes such as the dynamic
+// shared-memory limit are per device, and a process may drive several GPUs from several
+// host threads): f() runs under the lock the first time the current device calls once().
+struct PerDevice {
+  std::mutex mu;
+  uint64_t done[4] = {0, 0, 0, 0};   // devices 0..255
+  template <class F>
+  cudaError_t once(F&& f) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(mu);
+    uint64_t& w = done[(dev >> 6) & 3];
+    const uint64_t bit = 1ull << (dev & 63);
+    if (w & bit) return cudaSuccess;
+    const cudaError_t e = f();
+    if (e == cudaSuccess) w |= bit;
+    return e;
+  }
+};
+
+// SM count of the current device (cached per device)
+inline int device_sms() {
+  static std::atomic<int> cache[256];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::atomic<int>& c = cache[dev & 255];
+  int v = c.load(std::memory_order_relaxed);
+  if (v > 0) return v;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+  c.store(v, std::memory_order_relaxed);
+  return v;
+}
 
 inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 

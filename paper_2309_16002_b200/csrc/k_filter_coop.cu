@@ -695,11 +695,10 @@ template <typename T>
 cudaError_t launch_filter_coop(const FilterArgs& a, cudaStream_t s) {
   const int nsplit = ceil_div(a.d, kFiltCW);
   const size_t smem = filter_smem();
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_filter_coop<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  static PerDevice attr;
+  cudaError_t ae = attr.once(
+      [&] { return cudaFuncSetAttribute(k_filter_coop<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
+  if (ae != cudaSuccess) return ae;
   // cooperative launch through cudaLaunchKernelEx so that it can be captured in a graph
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nsplit);

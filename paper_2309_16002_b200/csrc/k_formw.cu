@@ -4,9 +4,20 @@
 // L_2 L_1^{-1} is a triangular solve (north_star step 6).  We form
 // L_1^{-1} once (k_trinv: one warp per column, forward substitution in fp64), then
 // W = L L_1^{-1} for all local rows with the tile GEMM (k_gemm_nt, B = L_1^{-T}), and
-// finally W(S,:) = I exactly (Alg. 3 l.2).  W_CLIPPED is reported when
-// min |diag L_1| < 1e-12 max |diag L_1| (Remark 5.2, reading R17).
+// finally W(S,:) = I exactly (Alg. 3 l.2).
+//
+// Remark 5.2: L_1 from (R)BRP "tends to be ill-conditioned", and the paper
+// then evaluates L_1^{-1} by a clipped SVD.  Reading R17: when min |diag L_1| <
+// 1e-12 max |diag L_1| (the host tests the running min/max k_fixup keeps in DevState, or
+// k_diag_test for a standalone rbrp_form_w), W(rest,:) = L_2 pinv_clip(L_1) with the
+// singular values below 1e-12 sigma_max discarded, and W_CLIPPED is reported.  The SVD
+// is a one-sided (Hestenes) Jacobi SVD of A = L_1^T in fp64 (k_jacobi_svd, cooperative,
+// round-robin pairs, high relative accuracy for the small singular values), then
+// pinv_clip(L_1)^T = V Sigma^+ U^T = sum_l sigma_l^-2 V_l (A V)_l^T (k_pinv_form).
+#include <cooperative_groups.h>
 #include <float.h>
+
+#include <algorithm>
 
 #include "launch.cuh"
 
@@ -39,20 +50,6 @@ __global__ void __launch_bounds__(32 * kTrinvWarps) k_trinv(const double* __rest
   extern __shared__ double xs[];   // [kTrinvWarps][k]
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t j = (int64_t)blockIdx.x * kTrinvWarps + w;
-  if (blockIdx.x == 0 && w == 0) {
-    double mx = 0.0, mn = DBL_MAX;
-    for (int64_t i = lane; i < k; i += 32) {
-      const double a = fabs(L1[i * k + i]);
-      mx = fmax(mx, a);
-      mn = fmin(mn, a);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-    }
-    if (lane == 0 && mn < 1e-12 * mx) atomicOr(&st->flags, (uint32_t)RBRP_F_W_CLIPPED);
-  }
   if (j >= k) return;
   double* x = xs + (int64_t)w * k;
   const double xj = 1.0 / L1[j * k + j];   // fp64 math warp-uniform (single-lane fp64 is slow)
@@ -141,20 +138,6 @@ __global__ void __launch_bounds__(32 * kTrinvSmallWarps) k_trinv_small(const dou
   }
   __syncthreads();
   for (int i = threadIdx.x; i < kk; i += blockDim.x) dinv[i] = 1.0 / Ls[(int64_t)i * kk + i];
-  if (blockIdx.x == 0 && w == 0) {   // W_CLIPPED check (Remark 5.2, reading R17)
-    double mx = 0.0, mn = DBL_MAX;
-    for (int i = lane; i < kk; i += 32) {
-      const double a = fabs(L1[(int64_t)i * kk + i]);
-      mx = fmax(mx, a);
-      mn = fmin(mn, a);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-    }
-    if (lane == 0 && mn < 1e-12 * mx) atomicOr(&st->flags, (uint32_t)RBRP_F_W_CLIPPED);
-  }
   __syncthreads();
   const int j = j0 + w;
   if (j >= kk) return;
@@ -177,18 +160,219 @@ cudaError_t launch_trinv(const double* L1, int64_t k, T* LinvT, int64_t ldo, Dev
   if (k <= 0) return cudaSuccess;
   if (k <= kTrinvSmallK) {
     const size_t smem = (size_t)(k * k + k + kTrinvSmallWarps * k) * sizeof(double);
-    static bool attr = false;   // once, for the largest k of this path
-    if (!attr) {
+    static PerDevice attr;   // once per device, for the largest k of this path
+    const cudaError_t ae = attr.once([] {
       const size_t mx = (size_t)(kTrinvSmallK * kTrinvSmallK + kTrinvSmallK + kTrinvSmallWarps * kTrinvSmallK) * 8;
-      cudaFuncSetAttribute(k_trinv_small<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
-      attr = true;
-    }
+      return cudaFuncSetAttribute(k_trinv_small<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
+    });
+    if (ae != cudaSuccess) return ae;
     k_trinv_small<T><<<ceil_div(k, kTrinvSmallWarps), 32 * kTrinvSmallWarps, smem, s>>>(L1, k, LinvT, ldo, st);
     return cudaGetLastError();
   }
   size_t smem = (size_t)kTrinvWarps * k * sizeof(double);
   cudaFuncSetAttribute(k_trinv<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_trinv<T><<<ceil_div(k, kTrinvWarps), 32 * kTrinvWarps, smem, s>>>(L1, k, LinvT, ldo, st);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------
+// Remark 5.2: clipped pseudo-inverse of L_1 (k x k, row-major fp64)
+// ---------------------------------------------------------------------------------
+
+// The Remark 5.2 trigger for a standalone L_1: out[0] = min |L_1(i,i)|, out[1] = max.
+__global__ void k_diag_test(const double* __restrict__ L1, int64_t k, double* __restrict__ out) {
+  double mx = 0.0, mn = DBL_MAX;
+  for (int64_t i = threadIdx.x; i < k; i += 32) {
+    const double a = fabs(L1[i * k + i]);
+    mx = fmax(mx, a);
+    mn = fmin(mn, a);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+  }
+  if (threadIdx.x == 0) {
+    out[0] = mn;
+    out[1] = mx;
+  }
+}
+
+cudaError_t launch_diag_test(const double* L1, int64_t k, double* out, cudaStream_t s) {
+  if (k <= 0) return cudaSuccess;
+  k_diag_test<<<1, 32, 0, s>>>(L1, k, out);
+  return cudaGetLastError();
+}
+
+constexpr int kJacWarps = 8;
+constexpr int kJacMaxSweeps = 40;
+
+// round-robin (circle method) position -> column: position 0 fixed, the others rotate
+__device__ __forceinline__ int jac_col(int pos, int round, int m) {
+  return pos == 0 ? 0 : 1 + (pos - 1 + round) % (m - 1);
+}
+
+// One-sided Jacobi SVD of A (columns G[j*k .. +k), j < k; A = L_1^T, so column j of A is
+// row j of the row-major L_1 buffer, rotated in place): A V = U Sigma.  Every round
+// rotates m/2 disjoint column pairs (one warp each) so that the pair is orthogonal;
+// m - 1 rounds make a sweep; sweeps repeat until a sweep rotates nothing (|gamma| <=
+// 1e-15 sqrt(alpha beta) for every pair) or kJacMaxSweeps.  V (same layout) starts as I.
+// cnt[0..1]: rotation counters of the even/odd sweep (zeroed by the launcher).
+__global__ void __launch_bounds__(32 * kJacWarps) k_jacobi_svd(double* __restrict__ G, double* __restrict__ V,
+                                                               int k, unsigned* cnt) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  const int lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * kJacWarps + (threadIdx.x >> 5), nw = gridDim.x * kJacWarps;
+  const int m = k + (k & 1);   // a phantom zero column when k is odd
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)k * k; e += (int64_t)gridDim.x * blockDim.x)
+    V[e] = (e / k == e % k) ? 1.0 : 0.0;
+  grid.sync();
+  for (int sweep = 0; sweep < kJacMaxSweeps; ++sweep) {
+    unsigned* c = cnt + (sweep & 1);
+    for (int round = 0; round < m - 1; ++round) {
+      for (int pr = gw; pr < m / 2; pr += nw) {
+        int p = jac_col(pr, round, m), q = jac_col(m - 1 - pr, round, m);
+        if (p > q) {
+          const int t = p;
+          p = q;
+          q = t;
+        }
+        if (q >= k) continue;   // phantom column
+        double* gp = G + (int64_t)p * k;
+        double* gq = G + (int64_t)q * k;
+        double al = 0.0, be = 0.0, ga = 0.0;
+        for (int r = lane; r < k; r += 32) {
+          const double a = gp[r], b = gq[r];
+          al = fma(a, a, al);
+          be = fma(b, b, be);
+          ga = fma(a, b, ga);
+        }
+        al = warp_sum(al);
+        be = warp_sum(be);
+        ga = warp_sum(ga);
+        if (!(fabs(ga) > 1e-15 * sqrt(al) * sqrt(be))) continue;
+        const double zeta = (be - al) / (2.0 * ga);
+        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+        for (int r = lane; r < k; r += 32) {
+          const double a = gp[r], b = gq[r];
+          gp[r] = cs * a - sn * b;
+          gq[r] = sn * a + cs * b;
+        }
+        double* vp = V + (int64_t)p * k;
+        double* vq = V + (int64_t)q * k;
+        for (int r = lane; r < k; r += 32) {
+          const double a = vp[r], b = vq[r];
+          vp[r] = cs * a - sn * b;
+          vq[r] = sn * a + cs * b;
+        }
+        if (lane == 0) atomicAdd(c, 1u);
+      }
+      grid.sync();
+    }
+    const unsigned rot = *(volatile unsigned*)c;
+    grid.sync();   // everyone has read c before it is reset for sweep + 2
+    if (blockIdx.x == 0 && threadIdx.x == 0) *c = 0u;
+    if (rot == 0) break;
+  }
+}
+
+// w[l] = sigma_l^-2 if sigma_l >= 1e-12 sigma_max else 0 (sigma_l = ||G_l||); V_l *= w[l]
+// in place; nclip = number of discarded singular values.  One CTA.
+__global__ void k_pinv_weights(const double* __restrict__ G, double* __restrict__ V, int k, int* nclip) {
+  extern __shared__ double sg[];   // [k]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  for (int l = w; l < k; l += nwarp) {
+    double s = 0.0;
+    for (int r = lane; r < k; r += 32) s = fma(G[(int64_t)l * k + r], G[(int64_t)l * k + r], s);
+    s = warp_sum(s);
+    if (lane == 0) sg[l] = sqrt(s);
+  }
+  __syncthreads();
+  __shared__ double smax;
+  __shared__ int ncl;
+  if (threadIdx.x == 0) {
+    double mx = 0.0;
+    for (int l = 0; l < k; ++l) mx = fmax(mx, sg[l]);
+    smax = mx;
+    ncl = 0;
+  }
+  __syncthreads();
+  for (int l = w; l < k; l += nwarp) {
+    const double sl = sg[l];
+    const bool keep = sl >= 1e-12 * smax && sl > 0.0;
+    const double wl = keep ? 1.0 / (sl * sl) : 0.0;
+    for (int r = lane; r < k; r += 32) V[(int64_t)l * k + r] *= wl;
+    if (lane == 0 && !keep) atomicAdd(&ncl, 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && nclip) *nclip = ncl;
+}
+
+// out(j, m) = sum_l Vw[l][j] G[l][m]  (= pinv_clip(L_1)^T), out k x ldo, columns [k, ldo) 0.
+// 32 x 32 output tile per CTA, l in chunks of 32 through shared memory.
+template <typename T>
+__global__ void __launch_bounds__(256) k_pinv_form(const double* __restrict__ Vw, const double* __restrict__ G, int k,
+                                                   T* __restrict__ out, int64_t ldo) {
+  __shared__ double As[32][33], Bs[32][33];
+  const int j0 = blockIdx.y * 32, m0 = blockIdx.x * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // ty 0..7: rows ty, ty+8, ...
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int l0 = 0; l0 < k; l0 += 32) {
+    for (int u = ty; u < 32; u += 8) {
+      const int l = l0 + u;
+      As[u][tx] = (l < k && j0 + tx < k) ? Vw[(int64_t)l * k + j0 + tx] : 0.0;
+      Bs[u][tx] = (l < k && m0 + tx < k) ? G[(int64_t)l * k + m0 + tx] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int u = 0; u < 32; ++u) {
+      const double b = Bs[u][tx];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[i] = fma(As[u][ty + 8 * i], b, acc[i]);
+    }
+    __syncthreads();
+  }
+  for (int i = 0; i < 4; ++i) {
+    const int j = j0 + ty + 8 * i, m = m0 + tx;
+    if (j < k && m < ldo) out[(int64_t)j * ldo + m] = m < k ? (T)acc[i] : T(0);
+  }
+}
+
+size_t pinv_scratch_bytes(int64_t k) { return ((size_t)k * k * 8 + 255) / 256 * 256 + 256; }
+
+// LinvT (k x ldo) = pinv_clip(L_1)^T.  L1 (k x k row-major fp64) is overwritten by the
+// rotated columns A V; scratch >= pinv_scratch_bytes(k).  nclip (device, optional):
+// number of discarded singular values.
+template <typename T>
+cudaError_t launch_pinv_clip(double* L1, int64_t k, T* LinvT, int64_t ldo, void* scratch, int* nclip,
+                             cudaStream_t s) {
+  if (k <= 0) return cudaSuccess;
+  double* V = (double*)scratch;
+  unsigned* cnt = (unsigned*)((char*)scratch + ((size_t)k * k * 8 + 255) / 256 * 256);
+  cudaError_t e = cudaMemsetAsync(cnt, 0, 2 * sizeof(unsigned), s);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jacobi_svd, 32 * kJacWarps, 0);
+  if (e != cudaSuccess) return e;
+  const int pairs = (int)((k + 1) / 2);
+  int grid = ceil_div(pairs, kJacWarps);
+  grid = std::max(1, std::min(grid, std::max(1, per_sm) * device_sms()));
+  int kk = (int)k;
+  void* args[] = {(void*)&L1, (void*)&V, (void*)&kk, (void*)&cnt};
+  e = cudaLaunchCooperativeKernel((const void*)k_jacobi_svd, dim3(grid), dim3(32 * kJacWarps), args, 0, s);
+  if (e != cudaSuccess) return e;
+  const size_t wsm = (size_t)k * 8;
+  if (wsm > 48 * 1024) {
+    e = cudaFuncSetAttribute(k_pinv_weights, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm);
+    if (e != cudaSuccess) return e;
+  }
+  k_pinv_weights<<<1, 1024, wsm, s>>>(L1, V, kk, nclip);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  dim3 g2((unsigned)ceil_div(ldo, 32), (unsigned)ceil_div(k, 32));
+  k_pinv_form<T><<<g2, 256, 0, s>>>(V, L1, kk, LinvT, ldo);
   return cudaGetLastError();
 }
 
@@ -214,7 +398,8 @@ cudaError_t launch_w_identity(T* W, int64_t ldw, const int64_t* S, int64_t k, in
                                            int64_t, double*, cudaStream_t);                      \
   template cudaError_t launch_trinv<T>(const double*, int64_t, T*, int64_t, DevState*, cudaStream_t); \
   template cudaError_t launch_w_identity<T>(T*, int64_t, const int64_t*, int64_t, int64_t,       \
-                                            int64_t, cudaStream_t);
+                                            int64_t, cudaStream_t);                              \
+  template cudaError_t launch_pinv_clip<T>(double*, int64_t, T*, int64_t, void*, int*, cudaStream_t);
 INSTW(double)
 INSTW(float)
 

@@ -554,16 +554,7 @@ extern "C" int rbrp_debug_lp_trace(long long* host, int count) {
   return cudaMemcpy(host, g_lp_trace, count * sizeof(long long), cudaMemcpyDeviceToHost) == cudaSuccess ? count : -1;
 }
 
-static int lp_sms() {
-  static int v = 0;
-  if (!v) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    if (v <= 0) v = 148;
-  }
-  return v;
-}
+static int lp_sms() { return device_sms(); }
 
 // TMA: 16-byte aligned base and row stride; fragments read column pairs (d even)
 template <typename E>

@@ -1,0 +1,67 @@
+// k_pack.cu — Q_b packed in the shared-memory image of the 64-row-tile projection
+// kernel (k_lhat_paper.cu): one 1-D bulk copy per 64-column chunk instead of a gather.
+//
+// Q_b are the rows of the kept basis of Alg. 2 l.9; the projection of l.13/l.16
+// streams them chunk by chunk from L2 for every 64-row tile of X_res.
+// Two images per chunk (both zero-padded to PACK_ROWS rows and to the chunk width):
+//   image 1 (L-hat pass, B fragments indexed by (row j, column pair)): row j, column c at
+//           j * KC + (c ^ f(j)), f(j) = 8 (j & 1) ^ 4 ((j >> 1) & 3)  (conflict-free);
+//   image 2 (update pass, B fragments indexed by (row pair p, column)): the 16-byte unit
+//           (Q(2p, c), Q(2p+1, c)) of pair p and column c at p * KC + (c ^ 2 (p & 3)).
+#include "launch.cuh"
+
+namespace rbrp {
+
+namespace pk {
+constexpr int KC = 64;          // columns per chunk (k_lhat_paper lp::KC)
+constexpr int PACK_ROWS = 64;   // rows of the packed buffer (lp::PACK_ROWS)
+}  // namespace pk
+
+__host__ __device__ __forceinline__ int pk_qswz(int j, int col) {
+  return col ^ (8 * (j & 1)) ^ (4 * ((j >> 1) & 3));
+}
+
+// part < 0: rows [0, b'), b' <= 64.  part >= 0 (b' > 32 split into 32-row parts, see
+// enqueue_projection): rows [32 part, min(b', 32 part + 32)).
+template <typename QT>
+__global__ void k_pack_q(const QT* __restrict__ Qt, int64_t d, double* __restrict__ Qp,
+                         const DevState* st, int part, int64_t ldq) {
+  if (st->stop) return;
+  const int bpa = st->b_prime;
+  int bp, r0 = 0;
+  if (part < 0) {
+    bp = bpa;
+    if (bp <= 0 || bp > pk::PACK_ROWS) return;
+  } else {
+    r0 = 32 * part;
+    bp = bpa - r0 < 32 ? bpa - r0 : 32;
+    if (bpa <= 32 || bp <= 0) return;
+  }
+  const int c = blockIdx.x, j = blockIdx.y, col = threadIdx.x;   // blockDim = KC
+  const int64_t gc = (int64_t)c * pk::KC + col;
+  const double v = (j < bp && gc < d) ? (double)Qt[(int64_t)(r0 + j) * ldq + gc] : 0.0;
+  Qp[((int64_t)c * pk::PACK_ROWS + j) * pk::KC + pk_qswz(j, col)] = v;
+  const int pr = j >> 1;
+  double* Q2 = Qp + (int64_t)gridDim.x * pk::PACK_ROWS * pk::KC + (int64_t)c * pk::PACK_ROWS * pk::KC;
+  Q2[(pr * pk::KC + (col ^ (2 * (pr & 3)))) * 2 + (j & 1)] = v;
+}
+
+static int pk_nc(int64_t d) { return (int)((d + pk::KC - 1) / pk::KC); }
+
+size_t fused_pack_bytes(int64_t d) { return 2 * (size_t)pk_nc(d) * pk::PACK_ROWS * pk::KC * 8; }   // two images
+
+cudaError_t launch_pack_q(const float* Qt, int64_t d, double* Qp, DevState* st, cudaStream_t s, int part,
+                          int64_t ldq) {
+  dim3 grid((unsigned)pk_nc(d), pk::PACK_ROWS);
+  k_pack_q<float><<<grid, pk::KC, 0, s>>>(Qt, d, Qp, st, part, ldq > 0 ? ldq : d);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_q(const double* Qt, int64_t d, double* Qp, DevState* st, cudaStream_t s, int part,
+                          int64_t ldq) {
+  dim3 grid((unsigned)pk_nc(d), pk::PACK_ROWS);
+  k_pack_q<double><<<grid, pk::KC, 0, s>>>(Qt, d, Qp, st, part, ldq > 0 ? ldq : d);
+  return cudaGetLastError();
+}
+
+}  // namespace rbrp

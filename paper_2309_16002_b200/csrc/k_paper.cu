@@ -3,7 +3,7 @@
 //
 //   l.6  V = X(S_t,:)^T - Q Q^T X(S_t,:)^T        k_cgs_dots + k_cgs_update, twice
 //                                                          (CGS2, reading R11)
-//   l.13  L-hat = X Q_b                            k_proj_fused (paper mode) or k_lhat
+//   l.13  L-hat = X Q_b                            k_lhat_paper (read-only pass) or k_lhat
 //   l.16  d <- max(0, d - ||L-hat(i,:)||^2)        fused, or k_downdate (reading R14)
 //   l.10  Q <- [Q, Q_b]                            k_append_q
 //   reading R13   L-hat(earlier skeletons,:) = 0 exactly   k_zero_prev (X(s,:) Q_b is only

@@ -262,11 +262,22 @@ __global__ void __launch_bounds__(256) k_fixup(T* __restrict__ X, int64_t ldx,
                                                double* __restrict__ dvec, T* __restrict__ L,
                                                int64_t ldl, const double* __restrict__ Rtot,
                                                const int64_t* __restrict__ S, int64_t n_local,
-                                               int64_t row_offset, int64_t d, const DevState* st) {
+                                               int64_t row_offset, int64_t d, DevState* st) {
   if (st->stop) return;
   const int bp = st->b_prime;
   const int i = blockIdx.x;
   if (i >= bp) return;
+  if (i == 0 && threadIdx.x == 0) {
+    // diag(L_1) of this block = diag(R_V(1:b',1:b')) as stored in L (Remark 5.2 trigger)
+    double mn = st->ldiag_min, mx = st->ldiag_max;
+    for (int j = 0; j < bp; ++j) {
+      const double a = fabs((double)(T)Rtot[j * kMaxB + j]);
+      mn = fmin(mn, a);
+      mx = fmax(mx, a);
+    }
+    st->ldiag_min = mn;
+    st->ldiag_max = mx;
+  }
   const int64_t k0 = st->k;
   const int64_t r = S[k0 + i] - row_offset;
   if (r < 0 || r >= n_local) return;

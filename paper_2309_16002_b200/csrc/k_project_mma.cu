@@ -297,16 +297,7 @@ __global__ void __launch_bounds__(32 * kMmaWarps, 1) k_update_mma(double* __rest
   proj_end_stamp(st);
 }
 
-static int g_num_sms = 0;
-static int num_sms() {
-  if (!g_num_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
-  }
-  return g_num_sms;
-}
+static int num_sms() { return device_sms(); }
 
 static bool mma_ok(const void* p, int64_t ld, int64_t K) {
   return (K % 8 == 0) && (ld % 2 == 0) && ((uintptr_t)p % 16 == 0);
@@ -384,10 +375,12 @@ bool gemm_nt_mma(const double* A, int64_t lda, const double* B, int64_t ldb, dou
   if (!mma_ok(A, lda, K) || !mma_ok(B, ldb, K)) return false;
   dim3 grid((unsigned)num_sms(), 1);
   using Cf = PCfg<128, 1, 32, false>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_nt_mma<128, 1, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
-    attr = true;
+  static PerDevice attr;
+  const cudaError_t ae = attr.once(
+      [] { return cudaFuncSetAttribute(k_nt_mma<128, 1, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM); });
+  if (ae != cudaSuccess) {
+    *err = ae;
+    return true;
   }
   k_nt_mma<128, 1, 32><<<grid, 32 * kMmaWarps, Cf::SMEM, s>>>(A, lda, B, ldb, C, ldc, M, N, K, nullptr, 0);
   *err = cudaGetLastError();

@@ -336,13 +336,7 @@ __global__ void __launch_bounds__(sk::kThreads, 1) k_lupp(LuArgs a) {
 }
 
 static int sk_num_sms() {
-  static int v = 0;
-  if (!v) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    if (v <= 0) v = 148;
-  }
+  const int v = device_sms();
   return v;
 }
 

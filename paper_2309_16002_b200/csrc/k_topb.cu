@@ -83,11 +83,10 @@ size_t topb_scratch_bytes(int64_t n, int B) {
 cudaError_t launch_topb(const double* dvec, int64_t n, int64_t row_offset, int B, void* scratch, int64_t* S_top,
                         int* top_cnt, const DevState* st, cudaStream_t s) {
   constexpr size_t kSm = kTopN * sizeof(TopKey);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_topb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSm);
-    attr = true;
-  }
+  static PerDevice attr;
+  const cudaError_t ae =
+      attr.once([] { return cudaFuncSetAttribute(k_topb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSm); });
+  if (ae != cudaSuccess) return ae;
   TopKey* buf[2] = {(TopKey*)scratch, (TopKey*)scratch + ((n + kTopN - 1) / kTopN) * B};
   int64_t g = (n + kTopN - 1) / kTopN;
   if (g <= 1) {

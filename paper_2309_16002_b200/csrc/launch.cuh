@@ -100,17 +100,13 @@ cudaError_t launch_lhat_mma(const double* Xres, int64_t ldx, const double* Qt, i
 cudaError_t launch_update_mma(double* Xres, int64_t ldx, const double* Qt, const double* L,
                               int64_t ldl, int64_t n, int64_t d, double* dvec, DevState* st,
                               int bucket, cudaStream_t s);
-// k_project_fused.cu — single-pass fused projection (L-hat, update, norms), b' <= 64
+// k_pack.cu — Q_b packed in the shared-memory image of k_lhat_paper (two images)
 size_t fused_pack_bytes(int64_t d);
-int fused_max_bucket(const void* X, int64_t ldx, int64_t d);
 // Qt: rows of Q_b (leading dimension ldq, 0 -> d), d columns packed
 cudaError_t launch_pack_q(const double* Qt, int64_t d, double* Qp, DevState* st, cudaStream_t s, int part = -1,
                           int64_t ldq = 0);
 cudaError_t launch_pack_q(const float* Qt, int64_t d, double* Qp, DevState* st, cudaStream_t s, int part = -1,
                           int64_t ldq = 0);
-cudaError_t launch_proj_fused(double* Xres, int64_t ldx, const double* Qp, double* L, int64_t ldl,
-                              int64_t n, int64_t d, double* dvec, DevState* st, int bucket, bool paper,
-                              cudaStream_t s);
 
 // k_lhat_paper.cu — paper form, l.13 + l.16: read-only DMMA pass with 64-row tiles
 int lhat_paper_max_bucket(const void* X, int64_t ldx, int64_t d);
@@ -163,6 +159,14 @@ cudaError_t launch_trinv(const double* L1, int64_t k, T* LinvT, int64_t ldo, Dev
 template <typename T>
 cudaError_t launch_gemm_nt(const T* A, int64_t lda, const T* B, int64_t ldb, T* C, int64_t ldc,
                            int64_t M, int64_t N, int64_t K, cudaStream_t s);
+// Remark 5.2 (reading R17): LinvT = pinv_clip(L_1)^T by a one-sided Jacobi SVD (L1 is
+// overwritten); scratch >= pinv_scratch_bytes(k); nclip (device, optional) = number of
+// singular values below 1e-12 sigma_max that were discarded
+size_t pinv_scratch_bytes(int64_t k);
+template <typename T>
+cudaError_t launch_pinv_clip(double* L1, int64_t k, T* LinvT, int64_t ldo, void* scratch, int* nclip,
+                             cudaStream_t s);
+cudaError_t launch_diag_test(const double* L1, int64_t k, double* out, cudaStream_t s);   // out: min, max |diag|
 template <typename T>
 cudaError_t launch_w_identity(T* W, int64_t ldw, const int64_t* S, int64_t k, int64_t n_local,
                               int64_t row_offset, cudaStream_t s);

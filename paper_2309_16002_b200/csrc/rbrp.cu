@@ -10,11 +10,14 @@
 // with one host read of DevState per block.  Per-block results go to a device log that
 // the host reads once at the end.
 #include <cuda_runtime.h>
+#include <float.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
+#include <list>
+#include <memory>
 #include <mutex>
 #include <vector>
 
@@ -37,7 +40,8 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
   size_t Xres = SIZE_MAX, Qall = SIZE_MAX, Ccgs = SIZE_MAX, Topb = SIZE_MAX, Stop = SIZE_MAX, Tcnt = SIZE_MAX, dvec, cpre, ctot, cpos, cprefix, L, Qt, Qp, Vg, Gpart, G, Tg, Ag, R11, Rtot,
-         piv, mass, St, Srep, S, forced, dbg, cand, st, L1 = SIZE_MAX, LinvT = SIZE_MAX, Wsc = SIZE_MAX;
+         piv, mass, St, Srep, S, forced, dbg, cand, st, L1 = SIZE_MAX, LinvT = SIZE_MAX, Wsc = SIZE_MAX,
+         Pinv = SIZE_MAX;
   size_t lbt, lbp, lrho, lSt, lpiv, lts, total;
   int nsplit, maxlog;
   int64_t nchunks, k_cap;
@@ -124,6 +128,7 @@ Layout make_layout(const rbrp_problem* p) {
     L.L1 = take((size_t)L.k_cap * L.k_cap * 8);
     L.LinvT = take((size_t)L.k_cap * ((L.k_cap + 7) / 8 * 8) * w);   // k x round8(k) (K padded for DMMA)
     L.Wsc = take(gemm_lp_scratch_bytes(L.k_cap, (L.k_cap + 7) / 8 * 8));   // packed L_1^{-T} groups
+    L.Pinv = take(pinv_scratch_bytes(L.k_cap));   // Remark 5.2 fallback: Jacobi V + counters
   }
   L.total = off;
   return L;
@@ -219,7 +224,7 @@ struct Ctx {
   double *dvec, *cpre, *ctot, *cprefix, *Vg, *Gpart, *G, *Tg, *Ag, *R11, *Rtot, *mass;
   int32_t *cpos, *piv, *forced;
   T *Lm, *Qt;
-  double* Qp;   // packed Q_b chunks of the fused projection
+  double* Qp;   // packed Q_b chunks of the 64-row-tile projection (k_pack_q)
   T* Qall;      // paper form: accumulated Q rows (k_cap x d)
   double* Ccgs; // paper form: CGS coefficients
   char* ws;     // workspace base
@@ -228,12 +233,14 @@ struct Ctx {
   double* L1;
   T* LinvT;
   void* Wsc;   // scratch of the W GEMM (gemm_nt_lp)
+  void* Pinv;  // scratch of the clipped-pinv fallback (Remark 5.2)
   DevState* st;
   long long* dbg;
   BlockLog log;
   bool use_mma, use_forced;
+  bool force_blk = false;   // replay: this block's pivots are forced (first entry >= 0)
+  int nforced = 0;          // blocks run with forced pivots (RBRP_F_NEAR_TIE)
   int bucketB;
-  int fused_max;   // largest bucket run by the fused single-pass projection (0: none)
   int lp_max;      // largest bucket run by the 64-row tiled kernel k_lhat_paper (0: none)
   bool tiled;      // residual form on the 64-row tiled kernel (L-hat pass + update pass via L2)
   bool lazy;       // X_res not copied at init: block 1's projection reads X and writes X_res
@@ -283,6 +290,7 @@ void make_ctx(Ctx<T>& c, const rbrp_problem* p, void* Xv, char* ws, const Layout
   c.L1 = Ly.L1 != SIZE_MAX ? (double*)(ws + Ly.L1) : nullptr;
   c.LinvT = Ly.LinvT != SIZE_MAX ? (T*)(ws + Ly.LinvT) : nullptr;
   c.Wsc = Ly.Wsc != SIZE_MAX ? (void*)(ws + Ly.Wsc) : nullptr;
+  c.Pinv = Ly.Pinv != SIZE_MAX ? (void*)(ws + Ly.Pinv) : nullptr;
   c.dbg = env_on("RBRP_DEBUG_STAMPS") ? (long long*)(ws + Ly.dbg) : nullptr;
   c.log.bt = (int32_t*)(ws + Ly.lbt);
   c.log.bp = (int32_t*)(ws + Ly.lbp);
@@ -295,13 +303,11 @@ void make_ctx(Ctx<T>& c, const rbrp_problem* p, void* Xv, char* ws, const Layout
   c.use_forced = p->replay_pivots != nullptr;
   c.use_mma = sizeof(T) == 8 && !force_simt() && projection_mma_supported(c.Xres, c.ldr, c.Qt, c.d);
   c.bucketB = bucket_of((int)std::min<int64_t>(p->b, c.k_cap));
-  c.fused_max = (c.use_mma && !env_on("RBRP_NO_FUSED")) ? fused_max_bucket(c.Xres, c.ldr, c.d) : 0;
   // residual form: the 64-row tiled kernel (L-hat pass + update pass re-reading the tile
-  // through L2) by default; RBRP_FUSED16=1 selects the 16-row smem-resident k_proj_fused
-  // fp32: the same kernel with fp32 storage and fp64 DMMA arithmetic (R19);
-  // RBRP_FP32_SIMT=1 keeps the CUDA-core fp32 kernels
+  // through L2); fp32: the same kernel with fp32 storage and fp64 DMMA arithmetic
+  // (R19); RBRP_FP32_SIMT=1 keeps the CUDA-core fp32 kernels
   const bool lp_ok = sizeof(T) == 8 ? c.use_mma : (!force_simt() && !env_on("RBRP_FP32_SIMT"));
-  c.tiled = !c.paper && lp_ok && (sizeof(T) == 4 || !env_on("RBRP_FUSED16"));
+  c.tiled = !c.paper && lp_ok;
   c.lp_max = ((c.paper || c.tiled) && lp_ok && !env_on("RBRP_NO_FUSED")) ? lp_max_bucket<T>(c.Xres, c.ldr, c.d) : 0;
   // the tiled kernel handles every bucket of this problem, so it can take block 1 straight
   // from X (X_res is then never copied: one HBM read + write less per ID).  Single-GPU
@@ -351,9 +357,10 @@ cudaError_t launch_block_sample(Ctx<T>& c, SampleArgs& sa, cudaStream_t s, int* 
   return launch_sample(sa, s);
 }
 
-// a4 (Alg. 2 l.13 + l.16): one fused single-pass kernel (k_proj_fused) for the buckets
-// it supports, else the two-kernel DMMA / CUDA-core path.  Each launch is a no-op unless
-// the block's b' falls in its bucket, so the sequence is graph-capturable.
+// a4 (Alg. 2 l.13 + l.16): the 64-row-tile kernel k_lhat_paper (L-hat pass + update pass
+// per tile) for the buckets it supports, else the two-kernel DMMA / CUDA-core path.  Each
+// launch is a no-op unless the block's b' falls in its bucket, so the sequence is
+// graph-capturable.
 template <typename T>
 int enqueue_projection(Ctx<T>& c, cudaStream_t s, int* nl) {
   auto lk = [&](cudaError_t e) {
@@ -361,8 +368,7 @@ int enqueue_projection(Ctx<T>& c, cudaStream_t s, int* nl) {
     return e == cudaSuccess ? (int)RBRP_OK : (int)RBRP_ECUDA;
   };
   int rc = RBRP_OK;
-  // the single-pass kernel: k_proj_fused (residual form) or k_lhat_paper (paper form)
-  const int fmax = (c.paper || c.tiled) ? c.lp_max : c.fused_max;
+  const int fmax = (c.paper || c.tiled) ? c.lp_max : 0;
   if (fmax > 0 && (rc = lk(launch_pack_q(c.Qt, c.d, c.Qp, c.st, s)))) return rc;
   bool need_downdate = false;
   // b' > 32 on the 64-row-tile kernel: 32-column parts in sequence (RBRP_NO_PARTS=1: the
@@ -371,12 +377,8 @@ int enqueue_projection(Ctx<T>& c, cudaStream_t s, int* nl) {
   for (int bk = 16; bk <= c.bucketB; bk *= 2) {
     if (bk > 32 && parts) continue;
     if (bk <= fmax) {
-      if (c.paper || c.tiled)
-        rc = lk(launch_lhat_paper((const T*)c.Xres, c.ldr, c.Qp, c.Lm, c.k_cap, c.n, c.d, c.dvec, c.st, bk,
-                                  !c.paper, s, c.lazy ? (const T*)c.X : nullptr, c.p->ld));
-      else
-        rc = lk(launch_proj_fused((double*)c.Xres, c.ldr, c.Qp, (double*)c.Lm, c.k_cap, c.n, c.d, c.dvec,
-                                  c.st, bk, false, s));
+      rc = lk(launch_lhat_paper((const T*)c.Xres, c.ldr, c.Qp, c.Lm, c.k_cap, c.n, c.d, c.dvec, c.st, bk,
+                                !c.paper, s, c.lazy ? (const T*)c.X : nullptr, c.p->ld));
     } else if (c.use_mma) {
       rc = lk(launch_lhat_mma((const double*)c.Xres, c.ldr, (const double*)c.Qt, c.n, c.d, (double*)c.Lm,
                               c.k_cap, c.st, bk, s));
@@ -440,7 +442,8 @@ int enqueue_block(Ctx<T>& c, SampleArgs& sa, cudaStream_t s, Prof* prof, int* nl
   fa.d = c.d;
   fa.Gpart = c.Gpart;
   fa.G = c.G;
-  fa.forced = c.use_forced ? c.forced : nullptr;
+  fa.forced = (c.use_forced && c.force_blk) ? c.forced : nullptr;
+  if (fa.forced) ++c.nforced;
   fa.piv = c.piv;
   fa.mass = c.mass;
   fa.R11 = c.R11;
@@ -494,17 +497,42 @@ struct GraphKey {
   int device, use_mma;
   bool operator==(const GraphKey& o) const { return memcmp(this, &o, sizeof(GraphKey)) == 0; }
 };
+// Entries are shared_ptr-owned: a caller keeps its entry alive across the launch even if
+// another host thread evicts it from the cache meanwhile (cudaGraphExecDestroy of an
+// in-flight graph frees it asynchronously on completion).
 struct GraphEntry {
   GraphKey key;
   cudaGraph_t g = nullptr;
   cudaGraphExec_t exec = nullptr;
   int launches_per_block = 0;
   unsigned long long stamp = 0;
+  ~GraphEntry() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (g) cudaGraphDestroy(g);
+  }
 };
+using GraphPtr = std::shared_ptr<GraphEntry>;
 std::mutex g_graph_mu;
-std::vector<GraphEntry> g_graphs;
+std::list<GraphPtr> g_graphs;
 unsigned long long g_graph_clock = 0;
-cudaStream_t g_capture_stream = nullptr;
+cudaStream_t g_capture_stream[256] = {};   // one capture stream per device (under g_graph_mu)
+
+cudaStream_t capture_stream() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaStream_t& cs = g_capture_stream[dev & 255];
+  if (!cs && cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) cs = nullptr;
+  return cs;
+}
+
+template <typename E>
+void evict_lru(std::list<std::shared_ptr<E>>& cache, size_t cap) {
+  while (cache.size() >= cap) {
+    auto it = std::min_element(cache.begin(), cache.end(),
+                               [](const std::shared_ptr<E>& a, const std::shared_ptr<E>& b) { return a->stamp < b->stamp; });
+    cache.erase(it);   // the entry itself dies with its last holder
+  }
+}
 
 GraphKey make_key(const rbrp_problem* p, const void* X, const void* ws, bool use_mma) {
   GraphKey k;
@@ -523,16 +551,17 @@ GraphKey make_key(const rbrp_problem* p, const void* X, const void* ws, bool use
 // Returns the cached graph for key, building it if needed; nullptr if graphs are not
 // usable (the caller then runs the eager loop — same kernels, host-driven).
 template <typename T>
-GraphEntry* get_graph(Ctx<T>& c, SampleArgs sa, const GraphKey& key) {
+GraphPtr get_graph(Ctx<T>& c, SampleArgs sa, const GraphKey& key) {
   std::lock_guard<std::mutex> lk(g_graph_mu);
   for (auto& e : g_graphs)
-    if (e.key == key) {
-      e.stamp = ++g_graph_clock;
-      return &e;
+    if (e->key == key) {
+      e->stamp = ++g_graph_clock;
+      return e;
     }
-  if (!g_capture_stream && cudaStreamCreateWithFlags(&g_capture_stream, cudaStreamNonBlocking) != cudaSuccess)
-    return nullptr;
-  GraphEntry e;
+  cudaStream_t cs = capture_stream();
+  if (!cs) return nullptr;
+  GraphPtr ep = std::make_shared<GraphEntry>();
+  GraphEntry& e = *ep;
   e.key = key;
   cudaGraphConditionalHandle h;
   cudaGraphNode_t node;
@@ -550,16 +579,15 @@ GraphEntry* get_graph(Ctx<T>& c, SampleArgs sa, const GraphKey& key) {
     ok = ok && body;
   }
   if (ok) {
-    ok = cudaStreamBeginCaptureToGraph(g_capture_stream, body, nullptr, nullptr, 0,
-                                       cudaStreamCaptureModeRelaxed) == cudaSuccess;
+    ok = cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed) == cudaSuccess;
     if (ok) {
       sa.cond = (unsigned long long)h;
       sa.first = 0;
       sa.replay_len = -1;
       int nl = 0, nproj = 0;
-      const int rc = enqueue_block<T>(c, sa, g_capture_stream, nullptr, &nl, &nproj, true);
+      const int rc = enqueue_block<T>(c, sa, cs, nullptr, &nl, &nproj, true);
       cudaGraph_t cap = nullptr;
-      const bool endok = cudaStreamEndCapture(g_capture_stream, &cap) == cudaSuccess;
+      const bool endok = cudaStreamEndCapture(cs, &cap) == cudaSuccess;
       ok = (rc == RBRP_OK) && endok;
       e.launches_per_block = nl;
     }
@@ -567,26 +595,22 @@ GraphEntry* get_graph(Ctx<T>& c, SampleArgs sa, const GraphKey& key) {
   if (ok) ok = cudaGraphInstantiate(&e.exec, e.g, 0) == cudaSuccess;
   if (!ok) {
     cudaGetLastError();
-    if (e.exec) cudaGraphExecDestroy(e.exec);
-    if (e.g) cudaGraphDestroy(e.g);
-    return nullptr;
+    return nullptr;   // ep's destructor releases what was created
   }
-  if (g_graphs.size() >= 8) {   // evict the least recently used
-    auto it = std::min_element(g_graphs.begin(), g_graphs.end(),
-                               [](const GraphEntry& a, const GraphEntry& b) { return a.stamp < b.stamp; });
-    cudaGraphExecDestroy(it->exec);
-    cudaGraphDestroy(it->g);
-    g_graphs.erase(it);
-  }
+  evict_lru(g_graphs, 8);
   e.stamp = ++g_graph_clock;
-  g_graphs.push_back(e);
-  return &g_graphs.back();
+  g_graphs.push_back(ep);
+  return ep;
 }
 
-// a6: W(S,:) = I, W(rest,:) = L_2 L_1^{-1} (Alg. 3; triangular inverse)
+// Remark 5.2 trigger (reading R17): min |diag L_1| < 1e-12 max |diag L_1|
+bool clip_needed(double dmin, double dmax) { return dmax > 0.0 && dmin < 1e-12 * dmax; }
+
+// a6: W(S,:) = I, W(rest,:) = L_2 L_1^{-1} (Alg. 3; triangular inverse),
+// or L_2 pinv_clip(L_1) when `clip` (Remark 5.2)
 template <typename T>
 int enqueue_W(Ctx<T>& c, const rbrp_problem* p, rbrp_comm* comm, void* W_out, int64_t k, cudaStream_t s,
-              int* nl) {
+              int* nl, bool clip = false) {
   const int64_t k_cap = c.k_cap;
   double* L1 = c.L1;
   T* LinvT = c.LinvT;
@@ -599,16 +623,22 @@ int enqueue_W(Ctx<T>& c, const rbrp_problem* p, rbrp_comm* comm, void* W_out, in
   // K padded to a multiple of 8 for the FP64 tensor path: L_1^{-T} gets zero columns
   // [k, kp) and L's columns [k, kp) are zeroed (never written by the loop)
   const int64_t kp = (k + 7) / 8 * 8;
-  ++*nl;
-  CK(launch_trinv<T>(L1, k, LinvT, kp, c.st, s));
+  if (clip) {
+    *nl += 4;
+    CK(launch_pinv_clip<T>(L1, k, LinvT, kp, c.Pinv, nullptr, s));   // dense pinv_clip(L_1)^T
+  } else {
+    ++*nl;
+    CK(launch_trinv<T>(L1, k, LinvT, kp, c.st, s));
+  }
   if (kp > k && kp <= k_cap && c.n > 0)
     CK(cudaMemset2DAsync(c.Lm + k, (size_t)k_cap * sizeof(T), 0, (size_t)(kp - k) * sizeof(T), (size_t)c.n, s));
   cudaError_t merr = cudaSuccess;
   ++*nl;
   if (sizeof(T) == 8 && !force_simt() && kp <= k_cap && c.Wsc && !env_on("RBRP_W_NTMMA") &&
       gemm_lp_supported((const double*)c.Lm, k_cap, (const double*)LinvT, kp, kp)) {
+    // lower_b: L_1^{-T} has zero chunks to skip; the clipped pinv is dense
     CK(gemm_nt_lp((const double*)c.Lm, k_cap, (const double*)LinvT, kp, (double*)W_out, k_cap, c.n, k, kp, c.Wsc,
-                  s, true));
+                  s, !clip));
     *nl += 2 * (int)((k + 31) / 32);
   } else if (sizeof(T) == 8 && !force_simt() && kp <= k_cap &&
              gemm_nt_mma((const double*)c.Lm, k_cap, (const double*)LinvT, kp, (double*)W_out, k_cap, c.n, k, kp, s,
@@ -630,47 +660,45 @@ struct WGraph {
   cudaGraphExec_t exec = nullptr;
   int launches = 0;
   unsigned long long stamp = 0;
+  ~WGraph() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (g) cudaGraphDestroy(g);
+  }
 };
-std::vector<WGraph> g_wgraphs;
+using WGraphPtr = std::shared_ptr<WGraph>;
+std::list<WGraphPtr> g_wgraphs;
 
 template <typename T>
-WGraph* get_w_graph(Ctx<T>& c, const rbrp_problem* p, const GraphKey& key, void* W_out, int64_t k) {
+WGraphPtr get_w_graph(Ctx<T>& c, const rbrp_problem* p, const GraphKey& key, void* W_out, int64_t k) {
   if (env_on("RBRP_NO_GRAPH")) return nullptr;
   std::lock_guard<std::mutex> lk(g_graph_mu);
   for (auto& e : g_wgraphs)
-    if (e.key == key && e.W == W_out && e.k == k) {
-      e.stamp = ++g_graph_clock;
-      return &e;
+    if (e->key == key && e->W == W_out && e->k == k) {
+      e->stamp = ++g_graph_clock;
+      return e;
     }
-  if (!g_capture_stream && cudaStreamCreateWithFlags(&g_capture_stream, cudaStreamNonBlocking) != cudaSuccess)
-    return nullptr;
-  WGraph e;
+  cudaStream_t cs = capture_stream();
+  if (!cs) return nullptr;
+  WGraphPtr ep = std::make_shared<WGraph>();
+  WGraph& e = *ep;
   e.key = key;
   e.W = W_out;
   e.k = k;
-  bool ok = cudaStreamBeginCapture(g_capture_stream, cudaStreamCaptureModeRelaxed) == cudaSuccess;
+  bool ok = cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed) == cudaSuccess;
   if (ok) {
-    const int rc = enqueue_W<T>(c, p, nullptr, W_out, k, g_capture_stream, &e.launches);
-    const bool endok = cudaStreamEndCapture(g_capture_stream, &e.g) == cudaSuccess;
+    const int rc = enqueue_W<T>(c, p, nullptr, W_out, k, cs, &e.launches);
+    const bool endok = cudaStreamEndCapture(cs, &e.g) == cudaSuccess;
     ok = rc == RBRP_OK && endok && e.g;
   }
   if (ok) ok = cudaGraphInstantiate(&e.exec, e.g, 0) == cudaSuccess;
   if (!ok) {
     cudaGetLastError();
-    if (e.exec) cudaGraphExecDestroy(e.exec);
-    if (e.g) cudaGraphDestroy(e.g);
     return nullptr;
   }
-  if (g_wgraphs.size() >= 8) {
-    auto it = std::min_element(g_wgraphs.begin(), g_wgraphs.end(),
-                               [](const WGraph& a, const WGraph& b) { return a.stamp < b.stamp; });
-    cudaGraphExecDestroy(it->exec);
-    cudaGraphDestroy(it->g);
-    g_wgraphs.erase(it);
-  }
+  evict_lru(g_wgraphs, 8);
   e.stamp = ++g_graph_clock;
-  g_wgraphs.push_back(e);
-  return &g_wgraphs.back();
+  g_wgraphs.push_back(ep);
+  return ep;
 }
 
 template <typename T>
@@ -703,6 +731,8 @@ int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* 
   hst->tau_b = p->tau_b;
   hst->k_cap = k_cap;
   hst->b = p->b;
+  hst->ldiag_min = DBL_MAX;
+  hst->ldiag_max = 0.0;
   CK(cudaMemcpyAsync(c.st, hst, sizeof(DevState), cudaMemcpyHostToDevice, s));
 
   Prof prof;
@@ -743,8 +773,12 @@ int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* 
     }
     if (cudaMemcpyAsync(c.Srep, hSt, len * 8, cudaMemcpyHostToDevice, s) != cudaSuccess)
       return RBRP_ECUDA - 1000;
-    if (p->replay_pivots) {
-      for (int i = 0; i < len; ++i) hpiv[i] = p->replay_pivots[replay_pos + i];
+    c.force_blk = p->replay_pivots && p->replay_pivots[replay_pos] >= 0;
+    if (c.force_blk) {
+      for (int i = 0; i < len; ++i) {
+        hpiv[i] = p->replay_pivots[replay_pos + i];
+        if (hpiv[i] < 0 || hpiv[i] >= len) return RBRP_EREPLAY - 1000;
+      }
       if (cudaMemcpyAsync(c.forced, hpiv, len * 4, cudaMemcpyHostToDevice, s) != cudaSuccess)
         return RBRP_ECUDA - 1000;
     }
@@ -763,7 +797,7 @@ int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* 
 
   sa.first = 0;
   const bool eager = p->replay_nblocks > 0 || prof.on || stamps || comm || env_on("RBRP_NO_GRAPH");
-  GraphEntry* ge = nullptr;
+  GraphPtr ge;   // held until the end of the call (stays valid if another thread evicts it)
   if (!eager) ge = get_graph<T>(c, sa, make_key(p, Xv, ws, c.use_mma));
   if (ge) {
     // the whole block loop as one graph launch (conditional WHILE node), enqueued right
@@ -816,14 +850,17 @@ int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* 
   // a6: W (Alg. 3); in graph mode the W kernels are replayed from a cached graph (keyed by
   // the loop's graph, W_out and k), so the host does not launch them one by one while the
   // GPU waits behind the stop-test read-back
+  uint32_t host_flags = 0;
   if (!(p->flags & RBRP_NO_W) && W_out && k > 0) {
     prof.begin(6);
-    WGraph* wg = (ge && !comm && !prof.on) ? get_w_graph<T>(c, p, ge->key, W_out, k) : nullptr;
+    const bool clip = clip_needed(hst->ldiag_min, hst->ldiag_max);   // Remark 5.2 (R17)
+    if (clip) host_flags |= RBRP_F_W_CLIPPED;
+    WGraphPtr wg = (ge && !comm && !prof.on && !clip) ? get_w_graph<T>(c, p, ge->key, W_out, k) : nullptr;
     if (wg) {
       CK(cudaGraphLaunch(wg->exec, s));
       nl += wg->launches;
     } else {
-      const int rc = enqueue_W<T>(c, p, comm, W_out, k, s, &nl);
+      const int rc = enqueue_W<T>(c, p, comm, W_out, k, s, &nl, clip);
       if (rc) return rc;
     }
     prof.end();
@@ -841,6 +878,8 @@ int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* 
     CK(cudaMemcpyAsync(hp + o_lSt, c.log.St, (size_t)nlog * b * 8, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(hp + o_lpiv, c.log.piv, (size_t)nlog * b * 4, cudaMemcpyDeviceToHost, s));
   }
+  if (rep && rep->d_out && c.n > 0)   // the final d^(t) (residual squared row norms)
+    CK(cudaMemcpyAsync(rep->d_out, c.dvec, (size_t)c.n * 8, cudaMemcpyDeviceToDevice, s));
   hm.mark("w_enqueued");
   CK(cudaEventRecord(e1, s));
   CK(cudaStreamSynchronize(s));
@@ -855,7 +894,7 @@ int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* 
     rep->fro2 = hst->D0;
     rep->resid_rel = hst->total / hst->D0;
     rep->nblocks = hst->t;
-    rep->flags = hst->flags;
+    rep->flags = hst->flags | host_flags | (c.nforced ? (uint32_t)RBRP_F_NEAR_TIE : 0u);
     rep->ms_total = ms;
     for (int i = 0; i < 8; ++i) rep->ms_phase[i] = 0.f;
     prof.collect(rep->ms_phase);
@@ -947,6 +986,8 @@ int run_dist(int nsh, const rbrp_problem* ps, void* const* Xs, char* const* wss,
     hs->tau_b = p->tau_b;
     hs->k_cap = k_cap;
     hs->b = p->b;
+    hs->ldiag_min = DBL_MAX;
+    hs->ldiag_max = 0.0;
     CK(cudaMemcpyAsync(C[h].st, hs, sizeof(DevState), cudaMemcpyHostToDevice, s));
   }
   cudaEvent_t e0, e1;
@@ -981,8 +1022,13 @@ int run_dist(int nsh, const rbrp_problem* ps, void* const* Xs, char* const* wss,
     }
     if (cudaMemcpyAsync(C[0].Srep, hSt, len * 8, cudaMemcpyHostToDevice, s) != cudaSuccess)
       return RBRP_ECUDA - 1000;
-    if (p->replay_pivots) {
-      for (int i = 0; i < len; ++i) hpiv[i] = p->replay_pivots[replay_pos + i];
+    const bool fb = p->replay_pivots && p->replay_pivots[replay_pos] >= 0;
+    for (int h = 0; h < nsh; ++h) C[h].force_blk = fb;
+    if (fb) {
+      for (int i = 0; i < len; ++i) {
+        hpiv[i] = p->replay_pivots[replay_pos + i];
+        if (hpiv[i] < 0 || hpiv[i] >= len) return RBRP_EREPLAY - 1000;
+      }
       for (int h = 0; h < nsh; ++h)
         if (cudaMemcpyAsync(C[h].forced, hpiv, len * 4, cudaMemcpyHostToDevice, s) != cudaSuccess)
           return RBRP_ECUDA - 1000;
@@ -1052,7 +1098,8 @@ int run_dist(int nsh, const rbrp_problem* ps, void* const* Xs, char* const* wss,
       fa.d = c.d;
       fa.Gpart = c.Gpart;
       fa.G = c.G;
-      fa.forced = c.use_forced ? c.forced : nullptr;
+      fa.forced = (c.use_forced && c.force_blk) ? c.forced : nullptr;
+      if (fa.forced && h == 0) ++c.nforced;
       fa.piv = c.piv;
       fa.mass = c.mass;
       fa.R11 = c.R11;
@@ -1093,6 +1140,7 @@ int run_dist(int nsh, const rbrp_problem* ps, void* const* Xs, char* const* wss,
   const int nblocks = std::min(hst->t, mb);
   // a6: W — L_1 rows from their owners (C5), then W rank-local
   const bool want_W = !(p->flags & RBRP_NO_W) && W_outs && k > 0;
+  const bool clip = want_W && clip_needed(hst->ldiag_min, hst->ldiag_max);   // Remark 5.2 (R17)
   if (want_W) {
     if (comm || nsh > 0) CK(cudaMemsetAsync(C[0].L1, 0, (size_t)k * k * 8, s));
     for (int h = 0; h < nsh; ++h)
@@ -1102,7 +1150,18 @@ int run_dist(int nsh, const rbrp_problem* ps, void* const* Xs, char* const* wss,
       Ctx<T>& c = C[h];
       if (!W_outs[h]) continue;
       const int64_t kp = (k + 7) / 8 * 8;
-      LKD(launch_trinv<T>(c.L1, k, c.LinvT, kp, c.st, s));
+      if (clip) {
+        // the Jacobi SVD rotates L_1 in place: in-process shards (one shared L_1) compute
+        // pinv_clip once and copy it
+        if (emul && h > 0) {
+          CK(cudaMemcpyAsync(c.LinvT, C[0].LinvT, (size_t)k * kp * sizeof(T), cudaMemcpyDeviceToDevice, s));
+        } else {
+          nl += 4;
+          CK(launch_pinv_clip<T>(c.L1, k, c.LinvT, kp, c.Pinv, nullptr, s));
+        }
+      } else {
+        LKD(launch_trinv<T>(c.L1, k, c.LinvT, kp, c.st, s));
+      }
       if (kp > k && kp <= k_cap && c.n > 0)
         CK(cudaMemset2DAsync(c.Lm + k, (size_t)k_cap * sizeof(T), 0, (size_t)(kp - k) * sizeof(T), (size_t)c.n, s));
       cudaError_t merr = cudaSuccess;
@@ -1110,7 +1169,7 @@ int run_dist(int nsh, const rbrp_problem* ps, void* const* Xs, char* const* wss,
       if (sizeof(T) == 8 && !force_simt() && kp <= k_cap && c.Wsc && !env_on("RBRP_W_NTMMA") &&
           gemm_lp_supported((const double*)c.Lm, k_cap, (const double*)c.LinvT, kp, kp)) {
         CK(gemm_nt_lp((const double*)c.Lm, k_cap, (const double*)c.LinvT, kp, (double*)W_outs[h], k_cap, c.n, k,
-                      kp, c.Wsc, s, true));
+                      kp, c.Wsc, s, !clip));
         nl += 2 * (int)((k + 31) / 32);
       } else if (sizeof(T) == 8 && !force_simt() && kp <= k_cap &&
                  gemm_nt_mma((const double*)c.Lm, k_cap, (const double*)c.LinvT, kp, (double*)W_outs[h], k_cap,
@@ -1136,6 +1195,8 @@ int run_dist(int nsh, const rbrp_problem* ps, void* const* Xs, char* const* wss,
     CK(cudaMemcpyAsync(hp + o_lSt, lg.St, (size_t)nlog * b * 8, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(hp + o_lpiv, lg.piv, (size_t)nlog * b * 4, cudaMemcpyDeviceToHost, s));
   }
+  if (rep && rep->d_out && nsh == 1 && C[0].n > 0)
+    CK(cudaMemcpyAsync(rep->d_out, C[0].dvec, (size_t)C[0].n * 8, cudaMemcpyDeviceToDevice, s));
   CK(cudaEventRecord(e1, s));
   CK(cudaStreamSynchronize(s));
   float ms = 0.f;
@@ -1148,7 +1209,7 @@ int run_dist(int nsh, const rbrp_problem* ps, void* const* Xs, char* const* wss,
     rep->fro2 = hst->D0;
     rep->resid_rel = hst->total / hst->D0;
     rep->nblocks = hst->t;
-    rep->flags = hst->flags;
+    rep->flags = hst->flags | (clip ? (uint32_t)RBRP_F_W_CLIPPED : 0u) | (C[0].nforced ? (uint32_t)RBRP_F_NEAR_TIE : 0u);
     rep->ms_total = ms;
     for (int i = 0; i < 8; ++i) rep->ms_phase[i] = 0.f;
     rep->launches = nl;
@@ -1180,6 +1241,67 @@ int run_dist(int nsh, const rbrp_problem* ps, void* const* Xs, char* const* wss,
   return RBRP_OK;
 }
 
+}  // namespace
+
+namespace {
+struct FwLayout {
+  size_t L1, LinvT, Pinv, S, diag, nclip, total;
+};
+FwLayout fw_layout(rbrp_dtype dtype, int64_t k) {
+  FwLayout f;
+  const size_t w = dtype == RBRP_F64 ? 8 : 4;
+  const int64_t kp = (k + 7) / 8 * 8;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align256(off + std::max<size_t>(bytes, 1));
+    return o;
+  };
+  f.L1 = take((size_t)k * k * 8);
+  f.LinvT = take((size_t)k * kp * w);
+  f.Pinv = take(pinv_scratch_bytes(k));
+  f.S = take((size_t)k * 8);
+  f.diag = take(16);
+  f.nclip = take(8);
+  f.total = off;
+  return f;
+}
+
+template <typename T>
+int form_w_run(const T* L, int64_t ldl, int64_t n, const int64_t* S, int64_t k, int method, T* W, int64_t ldw,
+               char* ws, cudaStream_t s, uint32_t* flags, int32_t* nclip) {
+  const FwLayout f = fw_layout(sizeof(T) == 8 ? RBRP_F64 : RBRP_F32, k);
+  double* L1 = (double*)(ws + f.L1);
+  T* LinvT = (T*)(ws + f.LinvT);
+  int64_t* Sd = (int64_t*)(ws + f.S);
+  double* dg = (double*)(ws + f.diag);
+  int* ncl = (int*)(ws + f.nclip);
+  const int64_t kp = (k + 7) / 8 * 8;
+  CK(cudaMemcpyAsync(Sd, S, (size_t)k * 8, cudaMemcpyHostToDevice, s));
+  CK(launch_gather_L1<T>(L, ldl, Sd, k, n, 0, L1, s));
+  bool clip = method == 2;
+  if (method == 0) {   // Remark 5.2 trigger (reading R17), decided on the host
+    double h[2];
+    CK(launch_diag_test(L1, k, dg, s));
+    CK(cudaMemcpyAsync(h, dg, 16, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    clip = clip_needed(h[0], h[1]);
+  }
+  CK(cudaMemsetAsync(ncl, 0, 4, s));
+  if (clip) {
+    CK(launch_pinv_clip<T>(L1, k, LinvT, kp, ws + f.Pinv, ncl, s));
+  } else {
+    CK(launch_trinv<T>(L1, k, LinvT, kp, nullptr, s));
+  }
+  CK(launch_gemm_nt<T>(L, ldl, LinvT, kp, W, ldw, n, k, k, s));
+  CK(launch_w_identity<T>(W, ldw, Sd, k, n, 0, s));
+  int hn = 0;
+  CK(cudaMemcpyAsync(&hn, ncl, 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (flags) *flags = clip ? (uint32_t)RBRP_F_W_CLIPPED : 0u;
+  if (nclip) *nclip = hn;
+  return RBRP_OK;
+}
 }  // namespace
 
 extern "C" {
@@ -1231,6 +1353,90 @@ int rbrp_id(const rbrp_problem* p, void* X, void* workspace, size_t ws_bytes, rb
   if (p->dtype == RBRP_F64)
     return run<double>(p, X, (char*)workspace, Ly, comm, s, S_out, W_out, rep);
   return run<float>(p, X, (char*)workspace, Ly, comm, s, S_out, W_out, rep);
+}
+
+// End-to-end entry with host buffers: X (host) -> a private device copy in the workspace
+// (run in place: the copy becomes the residual), rbrp_id, W (device, in the workspace)
+// -> W_host.  All copies are stream-ordered cudaMemcpy2DAsync calls on `stream`.
+static rbrp_problem host_problem(const rbrp_problem* p) {
+  rbrp_problem q = *p;
+  q.flags |= RBRP_INPLACE;
+  q.ld = p->d;
+  return q;
+}
+
+int rbrp_workspace_size_host(const rbrp_problem* p, size_t* bytes) {
+  int rc = validate(p);
+  if (rc) return rc;
+  if (!bytes) return RBRP_EINVAL;
+  const rbrp_problem q = host_problem(p);
+  const size_t w = p->dtype == RBRP_F64 ? 8 : 4;
+  const size_t xb = align256((size_t)p->n_local * p->d * w);
+  const size_t wb = (p->flags & RBRP_NO_W) ? 0 : align256((size_t)p->n_local * k_cap_of(p) * w);
+  *bytes = xb + wb + make_layout(&q).total;
+  return RBRP_OK;
+}
+
+int rbrp_id_host(const rbrp_problem* p, const void* X_host, void* workspace, size_t ws_bytes, rbrp_comm* comm,
+                 void* stream, int64_t* S_out, void* W_host, rbrp_report* rep) {
+  int rc = validate(p);
+  if (rc) return rc;
+  if (!S_out || (p->n_local > 0 && !X_host) || !workspace) return RBRP_EINVAL;
+  if ((uintptr_t)workspace % 256) return RBRP_EINVAL;
+  size_t need = 0;
+  if ((rc = rbrp_workspace_size_host(p, &need))) return rc;
+  if (ws_bytes < need) return RBRP_ENOMEM;
+  const rbrp_problem q = host_problem(p);
+  const size_t w = p->dtype == RBRP_F64 ? 8 : 4;
+  const int64_t k_cap = k_cap_of(p);
+  const bool want_W = !(p->flags & RBRP_NO_W) && W_host;
+  char* ws = (char*)workspace;
+  void* Xd = ws;
+  const size_t xb = align256((size_t)p->n_local * p->d * w);
+  void* Wd = (p->flags & RBRP_NO_W) ? nullptr : (void*)(ws + xb);
+  const size_t wb = (p->flags & RBRP_NO_W) ? 0 : align256((size_t)p->n_local * k_cap * w);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (p->n_local > 0)
+    CK(cudaMemcpy2DAsync(Xd, (size_t)p->d * w, X_host, (size_t)p->ld * w, (size_t)p->d * w, (size_t)p->n_local,
+                         cudaMemcpyHostToDevice, s));
+  rc = rbrp_id(&q, Xd, ws + xb + wb, ws_bytes - xb - wb, comm, stream, S_out, want_W ? Wd : nullptr, rep);
+  if (rc) return rc;
+  const int64_t k = rep ? rep->k : 0;
+  if (want_W && p->n_local > 0) {
+    int64_t kk = k;
+    if (!rep) {   // k = number of valid entries written to S_out is not known without a report
+      kk = k_cap;
+    }
+    if (kk > 0)
+      CK(cudaMemcpy2DAsync(W_host, (size_t)k_cap * w, Wd, (size_t)k_cap * w, (size_t)kk * w, (size_t)p->n_local,
+                           cudaMemcpyDeviceToHost, s));
+  }
+  CK(cudaStreamSynchronize(s));
+  return RBRP_OK;
+}
+
+int rbrp_form_w_workspace_size(rbrp_dtype dtype, int64_t k, size_t* bytes) {
+  if ((dtype != RBRP_F32 && dtype != RBRP_F64) || k < 1 || !bytes) return RBRP_EINVAL;
+  *bytes = fw_layout(dtype, k).total;
+  return RBRP_OK;
+}
+
+int rbrp_form_w(rbrp_dtype dtype, const void* L, int64_t ldl, int64_t n, const int64_t* S, int64_t k,
+                int32_t method, void* W_out, int64_t ldw, void* workspace, size_t ws_bytes, void* stream,
+                uint32_t* flags, int32_t* nclip) {
+  if ((dtype != RBRP_F32 && dtype != RBRP_F64) || k < 1 || n < k || ldl < k || ldw < k || !L || !S || !W_out ||
+      !workspace || method < 0 || method > 2)
+    return RBRP_EINVAL;
+  if ((uintptr_t)workspace % 256) return RBRP_EINVAL;
+  if (ws_bytes < fw_layout(dtype, k).total) return RBRP_ENOMEM;
+  for (int64_t i = 0; i < k; ++i)
+    if (S[i] < 0 || S[i] >= n) return RBRP_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == RBRP_F64)
+    return form_w_run<double>((const double*)L, ldl, n, S, k, method, (double*)W_out, ldw, (char*)workspace, s,
+                              flags, nclip);
+  return form_w_run<float>((const float*)L, ldl, n, S, k, method, (float*)W_out, ldw, (char*)workspace, s, flags,
+                           nclip);
 }
 
 int rbrp_id_sharded(const rbrp_problem* p, int nshards, const int64_t* shard_rows, void* const* X,

@@ -29,7 +29,8 @@ STATUS = {0: "RBRP_OK", -1: "RBRP_EINVAL", -2: "RBRP_ENONFINITE", -3: "RBRP_EDEG
           -8: "RBRP_ENOTSUP"}
 
 EXPORTED = ["rbrp_version", "rbrp_strerror", "rbrp_workspace_size", "rbrp_id", "rbrp_id_sharded",
-            "rbrp_comm_unique_id", "rbrp_comm_init", "rbrp_comm_destroy"]
+            "rbrp_comm_unique_id", "rbrp_comm_init", "rbrp_comm_destroy", "rbrp_form_w",
+            "rbrp_form_w_workspace_size", "rbrp_id_host", "rbrp_workspace_size_host"]
 
 
 class Problem(ctypes.Structure):
@@ -53,7 +54,7 @@ class Report(ctypes.Structure):
                 ("profile", ctypes.c_int32), ("ms_phase", ctypes.c_float * 8),
                 ("launches", ctypes.c_int32), ("proj_calls", ctypes.c_int32),
                 ("proj_ms", ctypes.c_float), ("graph", ctypes.c_int32),
-                ("proj_ms_blk", ctypes.POINTER(ctypes.c_float))]
+                ("proj_ms_blk", ctypes.POINTER(ctypes.c_float)), ("d_out", ctypes.c_void_p)]
 
 PHASES = ["init", "sample", "filter", "projection", "unused", "fixup_scan", "W", "comm"]
 
@@ -94,6 +95,19 @@ def lib() -> ctypes.CDLL:
         L.rbrp_comm_init.argtypes = [ctypes.POINTER(ctypes.c_void_p), ctypes.c_void_p, ctypes.c_int,
                                      ctypes.c_int, ctypes.c_int]
         L.rbrp_comm_destroy.argtypes = [ctypes.c_void_p]
+        L.rbrp_form_w_workspace_size.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.POINTER(ctypes.c_size_t)]
+        L.rbrp_form_w_workspace_size.restype = ctypes.c_int
+        L.rbrp_form_w.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                  ctypes.POINTER(ctypes.c_int64), ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p,
+                                  ctypes.c_int64, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p,
+                                  ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_int32)]
+        L.rbrp_form_w.restype = ctypes.c_int
+        L.rbrp_workspace_size_host.argtypes = [ctypes.POINTER(Problem), ctypes.POINTER(ctypes.c_size_t)]
+        L.rbrp_workspace_size_host.restype = ctypes.c_int
+        L.rbrp_id_host.argtypes = [ctypes.POINTER(Problem), ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                                   ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64),
+                                   ctypes.c_void_p, ctypes.POINTER(Report)]
+        L.rbrp_id_host.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -119,6 +133,7 @@ class Result:
     proj_ms: float                  # device time of the projection passes (in-kernel stamps)
     graph: bool                     # block loop ran as one CUDA graph launch
     proj_ms_blk: List[float] = dataclasses.field(default_factory=list)   # per block
+    d: Optional[torch.Tensor] = None  # final residual squared row norms (return_d=True), device
 
 
 def _problem(X: torch.Tensor, tol, k, b, seed, k_max, tau_b, flags, n_global, row_offset, greedy):
@@ -166,7 +181,8 @@ def id(X: torch.Tensor, tol: Optional[float] = None, k: Optional[int] = None, b:
        replay_pivots: Optional[Sequence[Sequence[int]]] = None,
        max_blocks: int = 1024, log_blocks: bool = True, workspace: Optional[torch.Tensor] = None,
        comm=None, n_global: Optional[int] = None, row_offset: int = 0,
-       profile: bool = False, W_out: Optional[torch.Tensor] = None, form: str = "residual") -> Result:
+       profile: bool = False, W_out: Optional[torch.Tensor] = None, form: str = "residual",
+       return_d: bool = False) -> Result:
     """RBRP interpolative decomposition X ~ W X_S of a CUDA tensor X (n x d).
 
     tol: tau, relative to ||X||_F^2 (for an (r, eps)-ID pass tol = (1+eps) eta_r,
@@ -175,7 +191,9 @@ def id(X: torch.Tensor, tol: Optional[float] = None, k: Optional[int] = None, b:
     n x k, W[S] = I) and the per-block log.  workspace / W_out: optional
     preallocated buffers (W_out: n x k_cap, k_cap = k or k_max or min(n, d)).
     form: "residual" (north_star: X_res updated per block, exact residual norms) or
-    "paper" (Alg. 2 literally: X read only, CGS2 for l.6, downdated norms l.16)."""
+    "paper" (Alg. 2 literally: X read only, CGS2 for l.6, downdated norms l.16).
+    return_d: also return the final residual squared row norms d (Result.d, device fp64).
+    replay_pivots: a block whose list starts with -1 is not forced (NEAR_TIE rule)."""
     if not X.is_cuda:
         raise ValueError("X must be a CUDA tensor (use id_host for host buffers)")
     if tol is None and k is None:
@@ -243,6 +261,8 @@ def id(X: torch.Tensor, tol: Optional[float] = None, k: Optional[int] = None, b:
         cache[key] = (rep, b_t, b_pr, rho, bidx, bpiv, S)
     rep, b_t, b_pr, rho, bidx, bpiv, S = cache[key]
     rep.profile = 1 if profile else 0
+    dv = torch.empty(X.shape[0], dtype=torch.float64, device=X.device) if return_d else None
+    rep.d_out = dv.data_ptr() if dv is not None else None
     stream = torch.cuda.current_stream(X.device).cuda_stream
     rc = L.rbrp_id(ctypes.byref(p), ctypes.c_void_p(X.data_ptr()),
                    ctypes.c_void_p(workspace.data_ptr()), ws_bytes,
@@ -251,8 +271,10 @@ def id(X: torch.Tensor, tol: Optional[float] = None, k: Optional[int] = None, b:
                    ctypes.c_void_p(W.data_ptr()) if W is not None else None, ctypes.byref(rep))
     if rc:
         raise RBRPError(rc, L.rbrp_strerror(rc).decode())
-    return _result(rep, S, W, b_t, b_pr, rho, bidx if log_blocks else None, bpiv if log_blocks else None,
-                   mb, b, log_blocks)
+    res = _result(rep, S, W, b_t, b_pr, rho, bidx if log_blocks else None, bpiv if log_blocks else None,
+                  mb, b, log_blocks)
+    res.d = dv
+    return res
 
 
 def _result(rep, S, W, b_t, b_pr, rho, bidx, bpiv, mb, b, log_blocks):
@@ -351,25 +373,73 @@ def id_sharded(shards: Sequence[torch.Tensor], tol: Optional[float] = None, k: O
     return res, Wk
 
 
-def id_host(X_host: torch.Tensor, device="cuda", X_dev: Optional[torch.Tensor] = None,
-            W_host: Optional[torch.Tensor] = None, **kw):
-    """End-to-end entry with a HOST input: copies X (pinned host -> HBM) on the
-    current stream, runs id(), and copies W (n x k) back to host memory.
-    X_dev / W_host: optional preallocated device copy of X and pinned host
-    output (n x k_cap).  Returns (Result, W_host view n x k)."""
-    if X_dev is None:
-        X_dev = torch.empty(X_host.shape, dtype=X_host.dtype, device=device)
-    X_dev.copy_(X_host, non_blocking=True)
-    res = id(X_dev, **kw)
-    Wh = None
-    if res.W is not None:
-        if W_host is None:
-            W_host = torch.empty(res.W.shape, dtype=res.W.dtype, pin_memory=True)
-            Wh = W_host
-        else:
-            # contiguous n x k view of the preallocated pinned buffer: one flat D2H copy
-            # (a strided [:, :k] host view would copy row by row)
-            Wh = W_host.view(-1)[:res.W.shape[0] * res.k].view(res.W.shape[0], res.k)
-        Wh.copy_(res.W if res.W.is_contiguous() else res.W.contiguous(), non_blocking=True)
-    torch.cuda.current_stream(X_dev.device).synchronize()
-    return res, Wh
+def form_w(L: torch.Tensor, S: Sequence[int], method: str = "auto", W_out: Optional[torch.Tensor] = None):
+    """Alg. 3 on its own: W(S,:) = I, W(rest,:) = L_2 L_1^{-1} from a device L
+    (n x k, row-major) and the skeleton rows S.  method: "auto" (triangular solve unless
+    min |diag L_1| < 1e-12 max |diag L_1|, then the clipped SVD of Remark 5.2), "trsm", or
+    "pinv" (clipped SVD, singular values < 1e-12 sigma_max discarded).
+    Returns (W (n x k device), flags, number of discarded singular values)."""
+    if not L.is_cuda or L.dim() != 2 or L.stride(1) != 1 or L.dtype not in (torch.float32, torch.float64):
+        raise ValueError("L must be a row-major float32/float64 CUDA matrix")
+    Lb = lib()
+    n, k = L.shape
+    dt = RBRP_F64 if L.dtype == torch.float64 else RBRP_F32
+    meth = {"auto": 0, "trsm": 1, "pinv": 2}[method]
+    sz = ctypes.c_size_t()
+    rc = Lb.rbrp_form_w_workspace_size(dt, k, ctypes.byref(sz))
+    if rc:
+        raise RBRPError(rc, "form_w_workspace_size")
+    ws = torch.empty(sz.value, dtype=torch.uint8, device=L.device)
+    W = W_out if W_out is not None else torch.empty((n, k), dtype=L.dtype, device=L.device)
+    Sa = (ctypes.c_int64 * len(S))(*[int(i) for i in S])
+    fl = ctypes.c_uint32()
+    nc = ctypes.c_int32()
+    stream = torch.cuda.current_stream(L.device).cuda_stream
+    rc = Lb.rbrp_form_w(dt, ctypes.c_void_p(L.data_ptr()), L.stride(0), n, Sa, len(S), meth,
+                        ctypes.c_void_p(W.data_ptr()), W.stride(0), ctypes.c_void_p(ws.data_ptr()), sz.value,
+                        ctypes.c_void_p(stream), ctypes.byref(fl), ctypes.byref(nc))
+    if rc:
+        raise RBRPError(rc, Lb.rbrp_strerror(rc).decode())
+    return W, fl.value, nc.value
+
+
+def id_host(X_host: torch.Tensor, tol: Optional[float] = None, k: Optional[int] = None, b: int = 16,
+            seed: int = 0, k_max: int = 0, tau_b: float = -1.0, with_W: bool = True, greedy: bool = False,
+            form: str = "residual", device="cuda", workspace: Optional[torch.Tensor] = None,
+            W_host: Optional[torch.Tensor] = None, comm=None, n_global: Optional[int] = None,
+            row_offset: int = 0, max_blocks: int = 1024):
+    """End-to-end entry with HOST buffers through the C ABI (rbrp_id_host): the library
+    copies X_host (n x d, row-major; pinned memory for full PCIe bandwidth) into a private
+    device copy inside `workspace`, runs the ID on it in place, and copies W (first k
+    columns) back into W_host (n x k_cap, pinned, allocated if None).
+    Returns (Result with W = the n x k host view, W_host)."""
+    if X_host.is_cuda:
+        raise ValueError("X_host must be a host tensor (use id for device tensors)")
+    if tol is None and k is None:
+        raise ValueError("need tol or k")
+    L = lib()
+    dev = torch.device(device)
+    flags = (0 if with_W else RBRP_NO_W) | (RBRP_FORM_PAPER if form == "paper" else 0)
+    p = _problem(X_host, tol, k, b, seed, k_max, tau_b, flags, n_global, row_offset, greedy)
+    sz = ctypes.c_size_t()
+    rc = L.rbrp_workspace_size_host(ctypes.byref(p), ctypes.byref(sz))
+    if rc:
+        raise RBRPError(rc, "workspace_size_host")
+    if workspace is None or workspace.numel() < sz.value:
+        workspace = torch.empty(sz.value, dtype=torch.uint8, device=dev)
+    k_cap = p.k_max if p.k_max > 0 else min(p.n_global, p.d)
+    if with_W and W_host is None:
+        W_host = torch.empty((X_host.shape[0], k_cap), dtype=X_host.dtype, pin_memory=True)
+    rep, b_t, b_pr, rho, bidx, bpiv = _report(max_blocks, b, False)
+    S = torch.empty(k_cap, dtype=torch.int64)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    rc = L.rbrp_id_host(ctypes.byref(p), ctypes.c_void_p(X_host.data_ptr()), ctypes.c_void_p(workspace.data_ptr()),
+                        sz.value, ctypes.c_void_p(comm) if comm else None, ctypes.c_void_p(stream),
+                        ctypes.cast(S.data_ptr(), ctypes.POINTER(ctypes.c_int64)),
+                        ctypes.c_void_p(W_host.data_ptr()) if with_W else None, ctypes.byref(rep))
+    if rc:
+        raise RBRPError(rc, L.rbrp_strerror(rc).decode())
+    res = _result(rep, S, None, b_t, b_pr, rho, None, None, max_blocks, b, False)
+    if with_W:
+        res.W = W_host[:, :res.k]
+    return res, W_host

@@ -346,25 +346,23 @@ def test_sharded_sampling_with_small_support_and_nan():
     (40, 200, 12, 16),                   # fewer tiles than SMs
 ])
 def test_fused_projection_matches_two_kernel_path(monkeypatch, n, d, rank, b):
-    """The three a4 kernels -- the 64-row tiled pass (default: L-hat pass, then the update
-    pass re-reading the tile through L2), the 16-row shared-memory-resident k_proj_fused
-    (RBRP_FUSED16=1) and the two-kernel DMMA path (RBRP_NO_FUSED=1) -- all match the oracle
-    in replay mode: identical S and b', rho_t within 1e-10 of the oracle and of each
-    other, W within tolerance."""
+    """The a4 kernels -- the 64-row tiled pass (default: L-hat pass, then the update pass
+    re-reading the tile through L2; with and without b' > 32 parts) and the two-kernel DMMA
+    path (RBRP_NO_FUSED=1) -- all match the oracle in replay mode: identical S and b',
+    rho_t within 1e-10 of the oracle and of each other, W within tolerance."""
     cfg = small_config("c2", n=n, d=d, rank=rank, b=b)
     Xnp = make(cfg).numpy()
     ores = O.rbrp(Xnp, tau=1e-12, b=b, seed=0)
     runs = {}
-    for name, env in (("two_kernel", {"RBRP_NO_FUSED": "1", "RBRP_FUSED16": "0", "RBRP_NO_PARTS": "0"}),
-                      ("fused16", {"RBRP_NO_FUSED": "0", "RBRP_FUSED16": "1", "RBRP_NO_PARTS": "0"}),
-                      ("tiled", {"RBRP_NO_FUSED": "0", "RBRP_FUSED16": "0", "RBRP_NO_PARTS": "0"}),
-                      ("tiled_no_parts", {"RBRP_NO_FUSED": "0", "RBRP_FUSED16": "0", "RBRP_NO_PARTS": "1"})):
+    for name, env in (("two_kernel", {"RBRP_NO_FUSED": "1", "RBRP_NO_PARTS": "0"}),
+                      ("tiled", {"RBRP_NO_FUSED": "0", "RBRP_NO_PARTS": "0"}),
+                      ("tiled_no_parts", {"RBRP_NO_FUSED": "0", "RBRP_NO_PARTS": "1"})):
         for k_, v in env.items():
             monkeypatch.setenv(k_, v)
         runs[name] = _replay(Xnp, ores, np.float64, b)
     monkeypatch.setenv("RBRP_NO_PARTS", "0")
     a = runs["two_kernel"]
-    for f in (runs["fused16"], runs["tiled"], runs["tiled_no_parts"]):
+    for f in (runs["tiled"], runs["tiled_no_parts"]):
         assert a.S.tolist() == f.S.tolist() and a.b_prime == f.b_prime
         assert max(abs(x - y) for x, y in zip(a.rho, f.rho)) <= 1e-10
     # same seed, sampling path (default kernel): reproducible bit for bit
