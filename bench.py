@@ -415,21 +415,24 @@ def main():
     r0res = res_list[-1]
     # per-phase breakdown from one eager, event-instrumented run (outside the timed region)
     rp = rb.id(X, profile=True, **kw)
+    rp.W = None
     torch.cuda.synchronize()
+    kw = None              # release the headline's workspace and W before the next measurement
+    torch.cuda.empty_cache()
 
     alt = None
     if not a.no_alt_form:
         # side measurement of the other form of Alg. 2 on the same input (not the headline)
         other = "paper" if a.form == "residual" else "residual"
         ns = max(1, min(a.steps, 5))
-        t2, rl2, _ = _measure(rb, cfg, X, tau, k_max, n_local, ns, 1, other, a.seed, dev, dkw, barrier, world)
+        t2, rl2, kw2 = _measure(rb, cfg, X, tau, k_max, n_local, ns, 1, other, a.seed, dev, dkw, barrier, world)
+        kw2 = None
+        torch.cuda.empty_cache()
         e2 = _config_entry(cfg, tau, k_max, t2, rl2, n_local, other, ns)
         alt = {"form": other, "value": t2 / 1e3, "unit": "s", "steps": ns, "k": e2["k"],
                "b_prime": e2["b_prime"], "resid_rel": e2["resid_rel"], "roofline": e2["roofline"],
                "note": ("paper: Alg. 2 literally (X read only, CGS2 l.6, downdated norms l.16; "
                         "SURVEY NEXT-1)" if other == "paper" else "residual: north_star form")}
-    # free the headline's device buffers before the host-buffer run
-    kw = None
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
 
@@ -492,9 +495,11 @@ def main():
             ns = max(1, min(a.steps, 10))
             mc, rlc, kwc = _measure(rb, c2, Xc, tc, km, c2.n, ns, 2, a.form, a.seed, dev, {}, barrier, world)
             configs[name] = _config_entry(c2, tc, km, mc, rlc, c2.n, a.form, ns)
+            kwc = None
+            torch.cuda.empty_cache()
             if name == "c2" and not a.no_sketch:
                 sk = _sketch_side(rb, Xc, rlc[-1].k, a, dev, c2)
-            del Xc, kwc
+            del Xc
             torch.cuda.empty_cache()
 
     if rank != 0:
