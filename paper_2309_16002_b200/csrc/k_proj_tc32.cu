@@ -1,0 +1,537 @@
+// k_proj_tc32.cu — the a4 projection for fp32 data on the 5th-generation tensor cores
+// (north_star step 4; Alg. 2 l.13 + l.16, in the right-looking form of P:523):
+//
+//     L-hat = X_res Q_b^T                 (n x b', written to L[:, k : k+b'])
+//     X_res <- X_res - L-hat Q_b ,  d(i) = ||x_res,i||^2  (fp64)
+//
+// fp32 accuracy from TF32 tensor cores by the 3xTF32 split (reading R19): every operand
+// v = v_hi + v_lo with v_hi = v truncated to TF32 (low 13 mantissa bits cleared, exact in
+// TF32) and v_lo = v - v_hi (exact in fp32); a product is a_hi b_hi + a_hi b_lo + a_lo b_hi
+// (the dropped a_lo b_lo and the TF32 rounding of the lo parts are ~2^-21 relative), with
+// fp32 accumulation in TMEM.
+//
+// Tiles of M = 128 rows (one TMEM lane per row), persistent CTAs (one per SM), chunks of
+// KC = 32 columns (one 128-byte swizzle row of fp32).  Per tile:
+//   pass 1 (l.13): per chunk c the X chunk arrives by TMA (128-byte swizzle); 8 row warps
+//     split it into hi / lo and store both into TMEM (tcgen05.st, two A stages); one thread
+//     issues, per 8-column k-step,
+//         D1[0:2N1)  += X_hi . [Q_hi ; Q_lo]^T      (N = 2 N1: both products, one A read)
+//         D1[0:N1)   += X_lo . Q_hi^T
+//     (tcgen05.mma kind::tf32, A from TMEM, B = the packed Q_b chunk in shared memory,
+//     K-major, 128-byte swizzle).  L-hat = D1[0:N1) + D1[N1:2N1).
+//   epilogue 1: the row warps read L-hat (tcgen05.ld), write L, and store its hi / lo split
+//     back into TMEM as the A operand of pass 2.
+//   pass 2 (l.16): per chunk c the same X chunk comes back through L2 (pass 1 loaded it
+//     with an evict_last policy, pass 2 with evict_first); per 8-row k-step of Q_b
+//         D2 += L_hi . Q_hi  +  L_hi . Q_lo  +  L_lo . Q_hi   (N = 32, B = the same packed
+//     chunk read MN-major); the row warps form x - D2 in fp32, store it (the residual is
+//     read once from HBM and written once), and accumulate ||x_res,i||^2 in fp64.
+// N1 = b' rounded up to 16 (<= 64; b' > 64 runs as 64-column parts in sequence, as the
+// DMMA kernel does with 32-column parts: Q_b's rows are orthonormal).
+//
+// Warp roles (352 threads): warp 0 X producer (TMA), warp 1 MMA issuer (one thread; the
+// warp allocates TMEM), warp 2 Q producer (1-D bulk copies of the pre-packed chunk
+// images), warps 3..10 row warps: warp w serves TMEM lanes 32 (w % 4) .. +32 (the
+// tcgen05.ld/st lane-quarter rule) and columns 16 h .. +16 of a chunk, h = (w - 3) / 4.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <stdlib.h>
+
+#include "launch.cuh"
+
+namespace rbrp {
+
+namespace tc {
+constexpr int M = 128;                    // rows per tile (TMEM lanes)
+constexpr int KC = 32;                    // columns per chunk (128-byte swizzle row)
+constexpr int NMAX = 64;                  // Q_b rows per part
+constexpr int XSLOT = M * KC * 4;         // 16 KB X chunk
+constexpr int QSLOT = 2 * NMAX * KC * 4;  // 16 KB packed Q chunk (hi rows, then lo rows)
+constexpr int NSX = 6, NSQ = 4;           // ring depths
+constexpr int NROWW = 8;                  // row warps
+constexpr int W_XP = 0, W_MMA = 1, W_QP = 2, W_ROW0 = 3;
+constexpr int NTH = (W_ROW0 + NROWW) * 32;
+constexpr int NACC2 = 4;
+// TMEM columns (512 allocated)
+constexpr uint32_t T_ACC1 = 0;     // D1: 2 N1 <= 128 columns
+constexpr uint32_t T_XA = 128;     // pass-1 A: 2 stages x (hi 32 | lo 32)
+constexpr uint32_t T_LA = 256;     // pass-2 A: L-hat hi (64) | lo (64)
+constexpr uint32_t T_ACC2 = 384;   // D2: NACC2 stages x 32
+constexpr size_t SMEM = 1024 + (size_t)NSX * XSLOT + (size_t)NSQ * QSLOT + 2 * 2 * M * 8 + 512;
+}  // namespace tc
+
+__device__ __forceinline__ uint32_t tc_su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void tc_bar_init(uint32_t b, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(b), "r"(count) : "memory");
+}
+__device__ __forceinline__ void tc_arrive(uint32_t b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(b) : "memory");
+}
+__device__ __forceinline__ void tc_expect(uint32_t b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(b), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tc_wait(uint32_t b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "W_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra W_%=;\n"
+      "}\n" ::"r"(b),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+// tcgen05.mma kind::tf32, A from TMEM, B from a shared-memory descriptor, D in TMEM
+__device__ __forceinline__ void tc_mma(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      " setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(d),
+      "r"(a), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// arrive on the mbarrier once every tcgen05 operation issued so far by this thread is done
+__device__ __forceinline__ void tc_commit(uint32_t b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(b)
+               : "memory");
+}
+// shared-memory matrix descriptor: 128-byte swizzle, version 1 (sm_100)
+__device__ __forceinline__ uint64_t tc_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) | (2ull << 61);
+}
+// instruction descriptor: D f32, A/B tf32, A K-major, B K-major (b_mn = 0) or MN-major,
+// M = 128, N
+__device__ __forceinline__ uint32_t tc_idesc(int N, int b_mn) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)b_mn << 16) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(tc::M >> 4) << 24);
+}
+__device__ __forceinline__ void tc_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tc_ld8(uint32_t taddr, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tc_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16};\n" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+__device__ __forceinline__ void tc_st8(uint32_t taddr, const uint32_t (&r)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"r"(taddr),
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
+__device__ __forceinline__ void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ float4 tc_lds4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+// TF32 split: hi = v with the low 13 mantissa bits cleared, lo = v - hi (exact)
+__device__ __forceinline__ void tc_split(float v, uint32_t& hi, uint32_t& lo) {
+  hi = __float_as_uint(v) & 0xFFFFE000u;
+  lo = __float_as_uint(v - __uint_as_float(hi));
+}
+__device__ __forceinline__ void tc_rowbar() {
+  asm volatile("bar.sync 1, %0;\n" ::"n"(tc::NROWW * 32) : "memory");
+}
+
+struct TcRing {
+  int i = 0;
+  uint32_t ph = 0;
+  __device__ __forceinline__ void next(int n) {
+    if (++i == n) {
+      i = 0;
+      ph ^= 1u;
+    }
+  }
+};
+
+__global__ void __launch_bounds__(tc::NTH, 1)
+    k_proj_tc32(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap xmap0, int lazy,
+                const float* __restrict__ Qimg, float* __restrict__ L, int64_t ldl, int64_t n, int d, int nc,
+                DevState* st, float* __restrict__ Xr, int64_t ldx, double* __restrict__ dvec, int part) {
+  using namespace tc;
+  if (st->stop) return;
+  int bp;
+  int64_t k0;
+  if (part < 0) {
+    bp = st->b_prime;
+    if (bp <= 0 || bp > NMAX) return;
+    k0 = st->k;
+  } else {
+    const int bpa = st->b_prime;
+    bp = bpa - NMAX * part < NMAX ? bpa - NMAX * part : NMAX;
+    if (bpa <= NMAX || bp <= 0) return;
+    k0 = st->k + NMAX * part;
+  }
+  const int N1 = (bp + 15) & ~15;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && part <= 0) st->ts0 = gtimer();
+
+  extern __shared__ __align__(1024) uint8_t tc_smem[];
+  uint8_t* sm = tc_smem + ((1024u - (tc_su32(tc_smem) & 1023u)) & 1023u);
+  uint8_t* xs = sm;
+  uint8_t* qs = xs + (size_t)NSX * XSLOT;
+  double* nrm = reinterpret_cast<double*>(qs + (size_t)NSQ * QSLOT);   // [tile parity][h][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(nrm + 2 * 2 * M);
+  uint64_t* xfull = bars;
+  uint64_t* xempty = xfull + NSX;
+  uint64_t* qfull = xempty + NSX;
+  uint64_t* qempty = qfull + NSQ;
+  uint64_t* afull = qempty + NSQ;
+  uint64_t* aempty = afull + 2;
+  uint64_t* a2full = aempty + 2;
+  uint64_t* a2empty = a2full + NACC2;
+  uint64_t* a1full = a2empty + NACC2;
+  uint64_t* lafull = a1full + 1;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(lafull + 1);
+
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int64_t ntiles = (n + M - 1) / M;
+  const int T = ntiles > blockIdx.x ? (int)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+  if (T == 0) {
+    proj_end_stamp(st);
+    return;
+  }
+  if (tid == 0) {
+    for (int s = 0; s < NSX; ++s) {
+      tc_bar_init(tc_su32(&xfull[s]), 1);
+      tc_bar_init(tc_su32(&xempty[s]), NROWW);
+    }
+    for (int s = 0; s < NSQ; ++s) {
+      tc_bar_init(tc_su32(&qfull[s]), 1);
+      tc_bar_init(tc_su32(&qempty[s]), 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      tc_bar_init(tc_su32(&afull[s]), NROWW);
+      tc_bar_init(tc_su32(&aempty[s]), 1);
+    }
+    for (int s = 0; s < NACC2; ++s) {
+      tc_bar_init(tc_su32(&a2full[s]), 1);
+      tc_bar_init(tc_su32(&a2empty[s]), NROWW);
+    }
+    tc_bar_init(tc_su32(a1full), 1);
+    tc_bar_init(tc_su32(lafull), NROWW);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (w == W_MMA) {   // the whole warp allocates all 512 TMEM columns (one CTA per SM)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(tc_su32(tslot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+  auto row0_of = [&](int p) { return ((int64_t)blockIdx.x + (int64_t)p * gridDim.x) * M; };
+  const int steps = T * 2 * nc;
+
+  if (w == W_XP) {
+    if (lane == 0) {
+      // X chunks, pass 1 then pass 2 of every tile.  Lazy X_res copy: block 1 reads X itself
+      const CUtensorMap* mp = (lazy && st->t == 1 && part <= 0) ? &xmap0 : &xmap;
+      uint64_t pol_keep, pol_drop;
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol_keep));
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol_drop));
+      TcRing xr;
+      for (int s = 0; s < steps; ++s) {
+        tc_wait(tc_su32(&xempty[xr.i]), xr.ph ^ 1u);
+        const int y = (int)row0_of(s / (2 * nc)), c = s % nc;
+        const bool second = (s / nc) & 1;
+        const uint32_t fb = tc_su32(&xfull[xr.i]);
+        tc_expect(fb, XSLOT);   // out-of-bounds rows / columns are zero-filled
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint "
+            "[%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(tc_su32(xs + (size_t)xr.i * XSLOT)),
+            "l"(mp), "r"(c * KC), "r"(y), "r"(fb), "l"(second ? pol_drop : pol_keep)
+            : "memory");
+        xr.next(NSX);
+      }
+    }
+  } else if (w == W_QP) {
+    if (lane == 0) {
+      // packed Q_b chunk images (hi rows [0, N1), lo rows [N1, 2 N1)), for both passes
+      const uint32_t bytes = (uint32_t)(2 * N1 * KC * 4);
+      TcRing qr;
+      for (int s = 0; s < steps; ++s) {
+        tc_wait(tc_su32(&qempty[qr.i]), qr.ph ^ 1u);
+        const uint32_t fb = tc_su32(&qfull[qr.i]);
+        tc_expect(fb, bytes);
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                tc_su32(qs + (size_t)qr.i * QSLOT)),
+            "l"(Qimg + (size_t)(s % nc) * (QSLOT / 4)), "r"(bytes), "r"(fb)
+            : "memory");
+        qr.next(NSQ);
+      }
+    }
+  } else if (w == W_MMA) {
+    if (lane == 0) {
+      const uint32_t id1a = tc_idesc(2 * N1, 0), id1b = tc_idesc(N1, 0), id2 = tc_idesc(KC, 1);
+      const uint32_t qs0 = tc_su32(qs);
+      TcRing qr, ar, cr;
+      for (int p = 0; p < T; ++p) {
+        // pass 1: D1 = X_hi [Q_hi; Q_lo]^T + X_lo [Q_hi]^T
+        for (int c = 0; c < nc; ++c) {
+          tc_wait(tc_su32(&afull[ar.i]), ar.ph);
+          tc_wait(tc_su32(&qfull[qr.i]), qr.ph);
+          tc_fence_after();
+          const uint32_t qa = qs0 + qr.i * QSLOT;
+          const uint32_t xa = tbase + T_XA + 64u * ar.i;
+#pragma unroll
+          for (int ks = 0; ks < KC / 8; ++ks) {
+            const uint64_t bd = tc_desc(qa + 32 * ks, 16, 1024);   // K-major: advance 8 fp32 along K
+            tc_mma(tbase + T_ACC1, xa + 8 * ks, bd, id1a, (c | ks) != 0);
+            tc_mma(tbase + T_ACC1, xa + 32 + 8 * ks, bd, id1b, 1u);
+          }
+          tc_commit(tc_su32(&aempty[ar.i]));
+          tc_commit(tc_su32(&qempty[qr.i]));
+          ar.next(2);
+          qr.next(NSQ);
+        }
+        tc_commit(tc_su32(a1full));
+        // pass 2: D2(chunk) = L_hi Q_hi + L_hi Q_lo + L_lo Q_hi  (B read MN-major)
+        tc_wait(tc_su32(lafull), (uint32_t)(p & 1));
+        tc_fence_after();
+        for (int c = 0; c < nc; ++c) {
+          tc_wait(tc_su32(&qfull[qr.i]), qr.ph);
+          tc_wait(tc_su32(&a2empty[cr.i]), cr.ph ^ 1u);
+          tc_fence_after();
+          const uint32_t qa = qs0 + qr.i * QSLOT;
+          const uint32_t da = tbase + T_ACC2 + KC * cr.i;
+          for (int ks = 0; ks < N1 / 8; ++ks) {
+            const uint64_t bh = tc_desc(qa + 1024 * ks, 8192, 1024);
+            const uint64_t bl = tc_desc(qa + 128 * N1 + 1024 * ks, 8192, 1024);
+            tc_mma(da, tbase + T_LA + 8 * ks, bh, id2, ks != 0);
+            tc_mma(da, tbase + T_LA + 8 * ks, bl, id2, 1u);
+            tc_mma(da, tbase + T_LA + 64 + 8 * ks, bh, id2, 1u);
+          }
+          tc_commit(tc_su32(&qempty[qr.i]));
+          tc_commit(tc_su32(&a2full[cr.i]));
+          qr.next(NSQ);
+          cr.next(NACC2);
+        }
+      }
+    }
+  } else {
+    // row warps
+    const int e = w - W_ROW0;
+    const int qq = w & 3;                 // TMEM lane quarter of this warp
+    const int h = e >> 2;                 // column half of a chunk
+    const int r = 32 * qq + lane;         // tile row
+    const uint32_t tl = tbase + ((uint32_t)(32 * qq) << 16);
+    const uint32_t xs0 = tc_su32(xs);
+    const int half = N1 / 2;
+    TcRing xr, ar, cr;
+    for (int p = 0; p < T; ++p) {
+      const int64_t row = row0_of(p) + r;
+      const bool vr = row < n;
+      // ---- pass 1: split the X chunk into TMEM (A operand)
+      for (int c = 0; c < nc; ++c) {
+        tc_wait(tc_su32(&xfull[xr.i]), xr.ph);
+        const uint32_t xa = xs0 + xr.i * XSLOT + r * 128;
+        float v[16];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float4 f = tc_lds4(xa + ((((4 * h + i) ^ (r & 7))) << 4));
+          v[4 * i] = f.x;
+          v[4 * i + 1] = f.y;
+          v[4 * i + 2] = f.z;
+          v[4 * i + 3] = f.w;
+        }
+        __syncwarp();
+        if (lane == 0) tc_arrive(tc_su32(&xempty[xr.i]));
+        xr.next(NSX);
+        uint32_t hi[16], lo[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) tc_split(v[i], hi[i], lo[i]);
+        tc_wait(tc_su32(&aempty[ar.i]), ar.ph ^ 1u);
+        tc_fence_after();
+        tc_st16(tl + T_XA + 64u * ar.i + 16 * h, hi);
+        tc_st16(tl + T_XA + 64u * ar.i + 32 + 16 * h, lo);
+        tc_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc_arrive(tc_su32(&afull[ar.i]));
+        ar.next(2);
+      }
+      // ---- epilogue 1: L-hat = D1[0:N1) + D1[N1:2N1) -> L, and its split -> TMEM (pass-2 A)
+      tc_wait(tc_su32(a1full), (uint32_t)(p & 1));
+      tc_fence_after();
+      for (int j0 = h * half; j0 < (h + 1) * half; j0 += 8) {
+        float a[8], b[8];
+        tc_ld8(tl + T_ACC1 + j0, a);
+        tc_ld8(tl + T_ACC1 + N1 + j0, b);
+        uint32_t hi[8], lo[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float lv = a[j] + b[j];
+          if (vr && j0 + j < bp) L[row * ldl + k0 + j0 + j] = lv;
+          tc_split(lv, hi[j], lo[j]);
+        }
+        tc_st8(tl + T_LA + j0, hi);
+        tc_st8(tl + T_LA + 64 + j0, lo);
+      }
+      tc_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc_arrive(tc_su32(lafull));
+      // ---- pass 2: x_res = x - D2, stored once; fp64 norms of the stored values
+      double nr = 0.0;
+      float* xrow = Xr + row * ldx;
+      for (int c = 0; c < nc; ++c) {
+        tc_wait(tc_su32(&a2full[cr.i]), cr.ph);
+        tc_fence_after();
+        float a[16];
+        tc_ld16(tl + T_ACC2 + KC * cr.i + 16 * h, a);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc_arrive(tc_su32(&a2empty[cr.i]));
+        cr.next(NACC2);
+        tc_wait(tc_su32(&xfull[xr.i]), xr.ph);
+        const uint32_t xa = xs0 + xr.i * XSLOT + r * 128;
+        float4 xv[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) xv[i] = tc_lds4(xa + ((((4 * h + i) ^ (r & 7))) << 4));
+        __syncwarp();
+        if (lane == 0) tc_arrive(tc_su32(&xempty[xr.i]));
+        xr.next(NSX);
+        const int col0 = c * KC + 16 * h;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          float4 o;
+          o.x = xv[i].x - a[4 * i];
+          o.y = xv[i].y - a[4 * i + 1];
+          o.z = xv[i].z - a[4 * i + 2];
+          o.w = xv[i].w - a[4 * i + 3];
+          nr = fma((double)o.x, (double)o.x, nr);
+          nr = fma((double)o.y, (double)o.y, nr);
+          nr = fma((double)o.z, (double)o.z, nr);
+          nr = fma((double)o.w, (double)o.w, nr);
+          if (vr && col0 + 4 * i < d) __stcs(reinterpret_cast<float4*>(xrow + col0 + 4 * i), o);
+        }
+      }
+      // d(i) = ||x_res,i||^2: the two column halves summed in a fixed order
+      double* nb = nrm + (size_t)(p & 1) * 2 * M;
+      nb[h * M + r] = nr;
+      tc_rowbar();
+      if (h == 0 && vr) dvec[row] = nb[r] + nb[M + r];
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (w == W_MMA) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase) : "memory");
+  }
+  proj_end_stamp(st);
+}
+
+// Packed Q_b chunk images for k_proj_tc32: chunk c holds rows [0, N1) = hi and [N1, 2 N1) =
+// lo of Q_b(r0 + j, 32 c .. 32 c + 32), each row 128 bytes with the 16-byte unit u at
+// u ^ (row & 7) (the 128-byte swizzle of a 1024-byte-aligned shared-memory image; read as
+// K-major B in pass 1 and MN-major B in pass 2).  Rows j >= b' and columns >= d are zero.
+__global__ void k_pack_tc32(const float* __restrict__ Qt, int64_t d, float* __restrict__ Qimg, const DevState* st,
+                            int part, int64_t ldq) {
+  using namespace tc;
+  if (st->stop) return;
+  const int bpa = st->b_prime;
+  int bp, r0 = 0;
+  if (part < 0) {
+    bp = bpa;
+    if (bp <= 0 || bp > NMAX) return;
+  } else {
+    r0 = NMAX * part;
+    bp = bpa - r0 < NMAX ? bpa - r0 : NMAX;
+    if (bpa <= NMAX || bp <= 0) return;
+  }
+  const int N1 = (bp + 15) & ~15;
+  const int c = blockIdx.x, rr = blockIdx.y, col = threadIdx.x;   // blockDim = 32
+  if (rr >= 2 * N1) return;
+  const int j = rr < N1 ? rr : rr - N1;
+  const int64_t gc = (int64_t)c * KC + col;
+  const float v = (j < bp && gc < d) ? Qt[(int64_t)(r0 + j) * ldq + gc] : 0.0f;
+  const uint32_t hi = __float_as_uint(v) & 0xFFFFE000u;
+  const float out = rr < N1 ? __uint_as_float(hi) : v - __uint_as_float(hi);
+  Qimg[(size_t)c * (QSLOT / 4) + rr * KC + ((((col >> 2) ^ (rr & 7))) << 2) + (col & 3)] = out;
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 tc_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult qr;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) == cudaSuccess &&
+        qr == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+  });
+  return fn;
+}
+
+bool proj_tc32_supported(const void* X, int64_t ldx, int64_t d) {
+  return d >= 8 && d % 4 == 0 && ldx % 4 == 0 && ((uintptr_t)X % 16) == 0 && tc_encode() != nullptr;
+}
+
+size_t tc32_pack_bytes(int64_t d) { return (size_t)((d + tc::KC - 1) / tc::KC) * tc::QSLOT; }
+
+cudaError_t launch_pack_tc32(const float* Qt, int64_t d, float* Qimg, DevState* st, cudaStream_t s, int part) {
+  dim3 grid((unsigned)((d + tc::KC - 1) / tc::KC), 2 * tc::NMAX);
+  k_pack_tc32<<<grid, tc::KC, 0, s>>>(Qt, d, Qimg, st, part, d);
+  return cudaGetLastError();
+}
+
+static bool tc_map(CUtensorMap* map, const float* X, int64_t ldx, int64_t n, int64_t d) {
+  auto enc = tc_encode();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)(n > 0 ? n : 1)};
+  const cuuint64_t strides[1] = {(cuuint64_t)ldx * 4};
+  const cuuint32_t box[2] = {(cuuint32_t)tc::KC, (cuuint32_t)tc::M};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)X, dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+cudaError_t launch_proj_tc32(float* X, int64_t ldx, const float* Qimg, float* L, int64_t ldl, int64_t n, int64_t d,
+                             double* dvec, DevState* st, cudaStream_t s, const float* X0, int64_t ldx0, int part) {
+  if (n <= 0) return cudaSuccess;
+  CUtensorMap map, map0;
+  if (!tc_map(&map, X, ldx, n, d)) return cudaErrorInvalidValue;
+  if (X0) {
+    if (!tc_map(&map0, X0, ldx0, n, d)) return cudaErrorInvalidValue;
+  } else {
+    map0 = map;
+  }
+  static PerDevice attr;
+  cudaError_t e = attr.once(
+      [] { return cudaFuncSetAttribute(k_proj_tc32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::SMEM); });
+  if (e != cudaSuccess) return e;
+  const int nc = (int)((d + tc::KC - 1) / tc::KC);
+  k_proj_tc32<<<device_sms(), tc::NTH, tc::SMEM, s>>>(map, map0, X0 ? 1 : 0, Qimg, L, ldl, n, (int)d, nc, st, X, ldx,
+                                                       dvec, part);
+  return cudaGetLastError();
+}
+
+}  // namespace rbrp

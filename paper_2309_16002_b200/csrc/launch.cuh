@@ -121,6 +121,14 @@ int lhat_paper_max_bucket_f32(const void* X, int64_t ldx, int64_t d);
 // resid: + the update pass (residual form, L2 re-read).  X0 (lazy X_res): in block 1 the
 // tile is read from X0 (the input) and the update is written to X (X_res)
 
+// k_proj_tc32.cu — fp32 residual-form projection on tcgen05 (kind::tf32, 3xTF32 split),
+// TMEM accumulators; b' <= 64 per launch (part >= 0: 64-column parts of b' > 64)
+bool proj_tc32_supported(const void* X, int64_t ldx, int64_t d);
+size_t tc32_pack_bytes(int64_t d);
+cudaError_t launch_pack_tc32(const float* Qt, int64_t d, float* Qimg, DevState* st, cudaStream_t s, int part);
+cudaError_t launch_proj_tc32(float* X, int64_t ldx, const float* Qimg, float* L, int64_t ldl, int64_t n, int64_t d,
+                             double* dvec, DevState* st, cudaStream_t s, const float* X0, int64_t ldx0, int part);
+
 // k_paper.cu — left-looking (paper) form of Alg. 2: CGS2 of the candidate rows (l.6),
 // Q append (l.10), exact zeros of earlier skeletons' L-hat (R13), d downdate (l.16)
 template <typename T>

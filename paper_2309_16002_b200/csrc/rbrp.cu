@@ -41,7 +41,7 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 struct Layout {
   size_t Xres = SIZE_MAX, Qall = SIZE_MAX, Ccgs = SIZE_MAX, Topb = SIZE_MAX, Stop = SIZE_MAX, Tcnt = SIZE_MAX, dvec, cpre, ctot, cpos, cprefix, L, Qt, Qp, Vg, Gpart, G, Tg, Ag, R11, Rtot,
          piv, mass, St, Srep, S, forced, dbg, cand, st, L1 = SIZE_MAX, LinvT = SIZE_MAX, Wsc = SIZE_MAX,
-         Pinv = SIZE_MAX;
+         Pinv = SIZE_MAX, Qtc = SIZE_MAX;
   size_t lbt, lbp, lrho, lSt, lpiv, lts, total;
   int nsplit, maxlog;
   int64_t nchunks, k_cap;
@@ -102,6 +102,7 @@ Layout make_layout(const rbrp_problem* p) {
   L.L = take((size_t)n * L.k_cap * w);
   L.Qt = take(B * d * w);
   L.Qp = take(fused_pack_bytes(d));
+  if (p->dtype == RBRP_F32) L.Qtc = take(tc32_pack_bytes(d));   // packed Q_b images of k_proj_tc32
   L.Vg = take(B * d * 8);
   L.Gpart = take((size_t)L.nsplit * B * B * 8);
   L.G = take(B * B * 8);
@@ -234,6 +235,8 @@ struct Ctx {
   T* LinvT;
   void* Wsc;   // scratch of the W GEMM (gemm_nt_lp)
   void* Pinv;  // scratch of the clipped-pinv fallback (Remark 5.2)
+  float* Qtc;  // packed Q_b chunk images of the tcgen05 fp32 projection
+  bool tc32 = false;   // fp32 residual form on tcgen05 (k_proj_tc32)
   DevState* st;
   long long* dbg;
   BlockLog log;
@@ -291,6 +294,7 @@ void make_ctx(Ctx<T>& c, const rbrp_problem* p, void* Xv, char* ws, const Layout
   c.LinvT = Ly.LinvT != SIZE_MAX ? (T*)(ws + Ly.LinvT) : nullptr;
   c.Wsc = Ly.Wsc != SIZE_MAX ? (void*)(ws + Ly.Wsc) : nullptr;
   c.Pinv = Ly.Pinv != SIZE_MAX ? (void*)(ws + Ly.Pinv) : nullptr;
+  c.Qtc = Ly.Qtc != SIZE_MAX ? (float*)(ws + Ly.Qtc) : nullptr;
   c.dbg = env_on("RBRP_DEBUG_STAMPS") ? (long long*)(ws + Ly.dbg) : nullptr;
   c.log.bt = (int32_t*)(ws + Ly.lbt);
   c.log.bp = (int32_t*)(ws + Ly.lbp);
@@ -316,6 +320,13 @@ void make_ctx(Ctx<T>& c, const rbrp_problem* p, void* Xv, char* ws, const Layout
   const int lp_need = c.bucketB > 32 && !env_on("RBRP_NO_PARTS") ? 32 : c.bucketB;
   c.lazy = c.tiled && !inplace && c.Xres != c.X && c.lp_max >= lp_need && c.lp_max > 0 &&
            lp_max_bucket<T>(c.X, p->ld, c.d) >= lp_need && !comm && !env_on("RBRP_EAGER_COPY");
+  // fp32 residual form: the tcgen05 3xTF32 kernel (RBRP_FP32_DMMA=1 keeps the fp64-DMMA one)
+  if (sizeof(T) == 4 && !c.paper && c.Qtc && !force_simt() && !env_on("RBRP_FP32_DMMA") && !env_on("RBRP_FP32_SIMT") &&
+      proj_tc32_supported(c.Xres, c.ldr, c.d)) {
+    c.tc32 = true;
+    c.tiled = false;
+    c.lazy = !inplace && c.Xres != c.X && proj_tc32_supported(c.X, p->ld, c.d) && !comm && !env_on("RBRP_EAGER_COPY");
+  }
 }
 
 template <typename T>
@@ -368,6 +379,17 @@ int enqueue_projection(Ctx<T>& c, cudaStream_t s, int* nl) {
     return e == cudaSuccess ? (int)RBRP_OK : (int)RBRP_ECUDA;
   };
   int rc = RBRP_OK;
+  if (c.tc32) {   // fp32 residual form on tcgen05: one launch (b' <= 64) or 64-column parts
+    const int nparts = c.bucketB > 64 ? (c.bucketB + 63) / 64 : 0;
+    for (int part = nparts ? 0 : -1; part < std::max(nparts, 0); ++part) {
+      if ((rc = lk(launch_pack_tc32((const float*)c.Qt, c.d, c.Qtc, c.st, s, part)))) return rc;
+      if ((rc = lk(launch_proj_tc32((float*)c.Xres, c.ldr, c.Qtc, (float*)c.Lm, c.k_cap, c.n, c.d, c.dvec, c.st, s,
+                                    c.lazy ? (const float*)c.X : nullptr, c.p->ld, part))))
+        return rc;
+      if (part < 0) break;
+    }
+    return RBRP_OK;
+  }
   const int fmax = (c.paper || c.tiled) ? c.lp_max : 0;
   if (fmax > 0 && (rc = lk(launch_pack_q(c.Qt, c.d, c.Qp, c.st, s)))) return rc;
   bool need_downdate = false;
