@@ -36,6 +36,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include "launch.cuh"
 
@@ -46,7 +47,8 @@ constexpr int M = 128;                    // rows per tile (TMEM lanes)
 constexpr int KC = 32;                    // columns per chunk (128-byte swizzle row)
 constexpr int NMAX = 64;                  // Q_b rows per part
 constexpr int XSLOT = M * KC * 4;         // 16 KB X chunk
-constexpr int QSLOT = 2 * NMAX * KC * 4;  // 16 KB packed Q chunk (hi rows, then lo rows)
+constexpr int QSLOT = 2 * NMAX * KC * 4;  // 16 KB shared-memory Q stage (one image)
+constexpr int QIMG = 2 * QSLOT;           // global: image 1 (pass 1) + image 2 (pass 2) per chunk
 constexpr int NSX = 6, NSQ = 4;           // ring depths
 constexpr int NROWW = 8;                  // row warps
 constexpr int W_XP = 0, W_MMA = 1, W_QP = 2, W_ROW0 = 3;
@@ -271,24 +273,30 @@ __global__ void __launch_bounds__(tc::NTH, 1)
     }
   } else if (w == W_QP) {
     if (lane == 0) {
-      // packed Q_b chunk images (hi rows [0, N1), lo rows [N1, 2 N1)), for both passes
-      const uint32_t bytes = (uint32_t)(2 * N1 * KC * 4);
+      // packed Q_b chunk images: pass 1 image 1 (hi rows [0, N1), lo rows [N1, 2 N1), K-major
+      // B of N = 2 N1), pass 2 image 2 (Q_b^T blocks of 32 columns x 32 K: hi blocks, then
+      // lo blocks, K-major B of N = 32)
+      const int nkb = (N1 + 31) / 32;
+      const uint32_t bytes1 = (uint32_t)(2 * N1 * KC * 4), bytes2 = (uint32_t)(2 * nkb * KC * 128);
       TcRing qr;
       for (int s = 0; s < steps; ++s) {
         tc_wait(tc_su32(&qempty[qr.i]), qr.ph ^ 1u);
         const uint32_t fb = tc_su32(&qfull[qr.i]);
+        const bool second = (s / nc) & 1;
+        const uint32_t bytes = second ? bytes2 : bytes1;
         tc_expect(fb, bytes);
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
                 tc_su32(qs + (size_t)qr.i * QSLOT)),
-            "l"(Qimg + (size_t)(s % nc) * (QSLOT / 4)), "r"(bytes), "r"(fb)
+            "l"(Qimg + (size_t)(s % nc) * (QIMG / 4) + (second ? QSLOT / 4 : 0)), "r"(bytes), "r"(fb)
             : "memory");
         qr.next(NSQ);
       }
     }
   } else if (w == W_MMA) {
     if (lane == 0) {
-      const uint32_t id1a = tc_idesc(2 * N1, 0), id1b = tc_idesc(N1, 0), id2 = tc_idesc(KC, 1);
+      const uint32_t id1a = tc_idesc(2 * N1, 0), id1b = tc_idesc(N1, 0), id2 = tc_idesc(KC, 0);
+      const int nkb = (N1 + 31) / 32;
       const uint32_t qs0 = tc_su32(qs);
       TcRing qr, ar, cr;
       for (int p = 0; p < T; ++p) {
@@ -311,7 +319,7 @@ __global__ void __launch_bounds__(tc::NTH, 1)
           qr.next(NSQ);
         }
         tc_commit(tc_su32(a1full));
-        // pass 2: D2(chunk) = L_hi Q_hi + L_hi Q_lo + L_lo Q_hi  (B read MN-major)
+        // pass 2: D2(chunk) = L_hi Q_hi + L_hi Q_lo + L_lo Q_hi  (B = image 2, K-major)
         tc_wait(tc_su32(lafull), (uint32_t)(p & 1));
         tc_fence_after();
         for (int c = 0; c < nc; ++c) {
@@ -321,8 +329,9 @@ __global__ void __launch_bounds__(tc::NTH, 1)
           const uint32_t qa = qs0 + qr.i * QSLOT;
           const uint32_t da = tbase + T_ACC2 + KC * cr.i;
           for (int ks = 0; ks < N1 / 8; ++ks) {
-            const uint64_t bh = tc_desc(qa + 1024 * ks, 8192, 1024);
-            const uint64_t bl = tc_desc(qa + 128 * N1 + 1024 * ks, 8192, 1024);
+            const uint32_t kb = (uint32_t)(ks >> 2), koff = 32u * (ks & 3);   // 32-K block, 8-K step in it
+            const uint64_t bh = tc_desc(qa + 4096u * kb + koff, 16, 1024);
+            const uint64_t bl = tc_desc(qa + 4096u * (nkb + kb) + koff, 16, 1024);
             tc_mma(da, tbase + T_LA + 8 * ks, bh, id2, ks != 0);
             tc_mma(da, tbase + T_LA + 8 * ks, bl, id2, 1u);
             tc_mma(da, tbase + T_LA + 64 + 8 * ks, bh, id2, 1u);
@@ -448,10 +457,14 @@ __global__ void __launch_bounds__(tc::NTH, 1)
   proj_end_stamp(st);
 }
 
-// Packed Q_b chunk images for k_proj_tc32: chunk c holds rows [0, N1) = hi and [N1, 2 N1) =
-// lo of Q_b(r0 + j, 32 c .. 32 c + 32), each row 128 bytes with the 16-byte unit u at
-// u ^ (row & 7) (the 128-byte swizzle of a 1024-byte-aligned shared-memory image; read as
-// K-major B in pass 1 and MN-major B in pass 2).  Rows j >= b' and columns >= d are zero.
+// Packed Q_b chunk images for k_proj_tc32 (128-byte swizzle of a 1024-byte-aligned shared-
+// memory image: row r is 128 bytes, its 16-byte unit u stored at u ^ (r & 7)), per chunk c
+// of 32 columns, QIMG bytes apart:
+//   image 1 (pass 1, K-major B, N = 2 N1): rows [0, N1) = hi, [N1, 2 N1) = lo of
+//     Q_b(r0 + j, 32 c .. 32 c + 32);
+//   image 2 (pass 2, K-major B, N = 32, at +QSLOT): blocks of 32 rows (one per column of the
+//     chunk) x 32 K values (Q_b rows 32 kb .. +32): hi blocks kb = 0 .. nkb-1, then lo blocks.
+// Rows j >= b' and columns >= d are zero.
 __global__ void k_pack_tc32(const float* __restrict__ Qt, int64_t d, float* __restrict__ Qimg, const DevState* st,
                             int part, int64_t ldq) {
   using namespace tc;
@@ -467,14 +480,28 @@ __global__ void k_pack_tc32(const float* __restrict__ Qt, int64_t d, float* __re
     if (bpa <= NMAX || bp <= 0) return;
   }
   const int N1 = (bp + 15) & ~15;
-  const int c = blockIdx.x, rr = blockIdx.y, col = threadIdx.x;   // blockDim = 32
-  if (rr >= 2 * N1) return;
-  const int j = rr < N1 ? rr : rr - N1;
-  const int64_t gc = (int64_t)c * KC + col;
-  const float v = (j < bp && gc < d) ? Qt[(int64_t)(r0 + j) * ldq + gc] : 0.0f;
-  const uint32_t hi = __float_as_uint(v) & 0xFFFFE000u;
-  const float out = rr < N1 ? __uint_as_float(hi) : v - __uint_as_float(hi);
-  Qimg[(size_t)c * (QSLOT / 4) + rr * KC + ((((col >> 2) ^ (rr & 7))) << 2) + (col & 3)] = out;
+  const int c = blockIdx.x, y = blockIdx.y, lane = threadIdx.x;   // blockDim = 32
+  float* img = Qimg + (size_t)c * (QIMG / 4);
+  if (y < 2 * NMAX) {   // image 1: row rr = y, column lane
+    const int rr = y;
+    if (rr >= 2 * N1) return;
+    const int j = rr < N1 ? rr : rr - N1;
+    const int64_t gc = (int64_t)c * KC + lane;
+    const float v = (j < bp && gc < d) ? Qt[(int64_t)(r0 + j) * ldq + gc] : 0.0f;
+    const uint32_t hi = __float_as_uint(v) & 0xFFFFE000u;
+    const float out = rr < N1 ? __uint_as_float(hi) : v - __uint_as_float(hi);
+    img[rr * KC + ((((lane >> 2) ^ (rr & 7))) << 2) + (lane & 3)] = out;
+  } else {              // image 2: block (hl, kb), row n (column of the chunk), K index lane
+    const int yy = y - 2 * NMAX, nkb = (N1 + 31) / 32;
+    const int hl = yy / (2 * KC), kb = (yy / KC) & 1, nn = yy % KC;
+    if (kb >= nkb) return;
+    const int j = 32 * kb + lane;
+    const int64_t gc = (int64_t)c * KC + nn;
+    const float v = (j < bp && gc < d) ? Qt[(int64_t)(r0 + j) * ldq + gc] : 0.0f;
+    const uint32_t hi = __float_as_uint(v) & 0xFFFFE000u;
+    const float out = hl == 0 ? __uint_as_float(hi) : v - __uint_as_float(hi);
+    img[QSLOT / 4 + (hl * nkb + kb) * (KC * KC) + nn * KC + ((((lane >> 2) ^ (nn & 7))) << 2) + (lane & 3)] = out;
+  }
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 tc_encode() {
@@ -494,10 +521,10 @@ bool proj_tc32_supported(const void* X, int64_t ldx, int64_t d) {
   return d >= 8 && d % 4 == 0 && ldx % 4 == 0 && ((uintptr_t)X % 16) == 0 && tc_encode() != nullptr;
 }
 
-size_t tc32_pack_bytes(int64_t d) { return (size_t)((d + tc::KC - 1) / tc::KC) * tc::QSLOT; }
+size_t tc32_pack_bytes(int64_t d) { return (size_t)((d + tc::KC - 1) / tc::KC) * tc::QIMG; }
 
 cudaError_t launch_pack_tc32(const float* Qt, int64_t d, float* Qimg, DevState* st, cudaStream_t s, int part) {
-  dim3 grid((unsigned)((d + tc::KC - 1) / tc::KC), 2 * tc::NMAX);
+  dim3 grid((unsigned)((d + tc::KC - 1) / tc::KC), 2 * tc::NMAX + 4 * tc::KC);
   k_pack_tc32<<<grid, tc::KC, 0, s>>>(Qt, d, Qimg, st, part, d);
   return cudaGetLastError();
 }
@@ -535,3 +562,26 @@ cudaError_t launch_proj_tc32(float* X, int64_t ldx, const float* Qimg, float* L,
 }
 
 }  // namespace rbrp
+
+// Development probe (not in the ABI header): one projection of X (n x d, device, ld d) by
+// the b rows of Q (device, b x d): X <- X - (X Q^T) Q in place, L (n x b) and d(i) out.
+extern "C" int rbrp_debug_tc32(float* X, int64_t n, int64_t d, const float* Q, int b, float* L, double* dvec) {
+  using namespace rbrp;
+  DevState h;
+  memset(&h, 0, sizeof(h));
+  h.b_prime = b;
+  h.k = 0;
+  h.t = 2;
+  DevState* st = nullptr;
+  float* img = nullptr;
+  if (cudaMalloc(&st, sizeof(DevState)) != cudaSuccess) return -5;
+  if (cudaMalloc(&img, tc32_pack_bytes(d)) != cudaSuccess) return -5;
+  cudaMemcpy(st, &h, sizeof(h), cudaMemcpyHostToDevice);
+  cudaMemset(img, 0xff, tc32_pack_bytes(d));
+  cudaError_t e = launch_pack_tc32(Q, d, img, st, 0, -1);
+  if (e == cudaSuccess) e = launch_proj_tc32(X, d, img, L, b, n, d, dvec, st, 0, nullptr, 0, -1);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  cudaFree(st);
+  cudaFree(img);
+  return e == cudaSuccess ? 0 : -(int)e;
+}

@@ -556,7 +556,7 @@ void evict_lru(std::list<std::shared_ptr<E>>& cache, size_t cap) {
   }
 }
 
-GraphKey make_key(const rbrp_problem* p, const void* X, const void* ws, bool use_mma) {
+GraphKey make_key(const rbrp_problem* p, const void* X, const void* ws, int variant) {
   GraphKey k;
   memset(&k, 0, sizeof(k));
   k.p = *p;
@@ -566,7 +566,7 @@ GraphKey make_key(const rbrp_problem* p, const void* X, const void* ws, bool use
   k.X = X;
   k.ws = ws;
   cudaGetDevice(&k.device);
-  k.use_mma = use_mma;
+  k.use_mma = variant;
   return k;
 }
 
@@ -820,7 +820,9 @@ int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* 
   sa.first = 0;
   const bool eager = p->replay_nblocks > 0 || prof.on || stamps || comm || env_on("RBRP_NO_GRAPH");
   GraphPtr ge;   // held until the end of the call (stays valid if another thread evicts it)
-  if (!eager) ge = get_graph<T>(c, sa, make_key(p, Xv, ws, c.use_mma));
+  // the key records the kernel variant too (environment knobs select alternatives)
+  if (!eager) ge = get_graph<T>(c, sa, make_key(p, Xv, ws, (c.use_mma ? 1 : 0) | (c.tc32 ? 2 : 0) | (c.tiled ? 4 : 0) |
+                                                              (c.lazy ? 8 : 0) | (c.paper ? 16 : 0)));
   if (ge) {
     // the whole block loop as one graph launch (conditional WHILE node), enqueued right
     // behind a0 and the first sample: no host round trip in between (a non-finite or

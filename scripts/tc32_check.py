@@ -21,7 +21,7 @@ def run(X, env, **kw):
 
 
 def main():
-    for (n, d, b) in [(20000, 192, 64), (3000, 64, 16), (9001, 100, 40), (12345, 2048, 64)]:
+    for (n, d, b) in ([] if os.environ.get("TC_TIME_ONLY") else [(20000, 192, 64), (3000, 64, 16), (9001, 100, 40), (12345, 2048, 64)]):
         cfg = small_config("c4", n=n, d=d, b=b)
         Xnp = make(cfg).numpy()
         ores = O.rbrp(Xnp, tau=1e-3, b=b, seed=0)
@@ -31,6 +31,10 @@ def main():
         out = {}
         for env in ("1", "0"):
             r = run(X, env, k=ores.k, b=b, replay_blocks=blocks, replay_pivots=piv, return_d=True)
+            print(env, "k", r.k, ores.k, "bp", r.b_prime, [x.b_prime for x in ores.blocks], "flags", r.flags,
+                  "rho", r.rho, [x.rho for x in ores.blocks], flush=True)
+            if r.k != ores.k:
+                continue
             Wo, kap, _ = O.form_W(ores.L, ores.S, method="trsm")
             W = r.W.double().cpu().numpy()
             out[env] = dict(S=r.S.tolist() == ores.S, bp=r.b_prime == [x.b_prime for x in ores.blocks],
