@@ -259,8 +259,10 @@ __global__ void __launch_bounds__(tc::NTH, 1)
       TcRing xr;
       for (int s = 0; s < steps; ++s) {
         tc_wait(tc_su32(&xempty[xr.i]), xr.ph ^ 1u);
-        const int y = (int)row0_of(s / (2 * nc)), c = s % nc;
         const bool second = (s / nc) & 1;
+        // pass 2 walks the chunks in reverse: the most recently loaded ones are re-read first,
+        // while they are still in L2
+        const int y = (int)row0_of(s / (2 * nc)), c = second ? nc - 1 - s % nc : s % nc;
         const uint32_t fb = tc_su32(&xfull[xr.i]);
         tc_expect(fb, XSLOT);   // out-of-bounds rows / columns are zero-filled
         asm volatile(
@@ -288,7 +290,8 @@ __global__ void __launch_bounds__(tc::NTH, 1)
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
                 tc_su32(qs + (size_t)qr.i * QSLOT)),
-            "l"(Qimg + (size_t)(s % nc) * (QIMG / 4) + (second ? QSLOT / 4 : 0)), "r"(bytes), "r"(fb)
+            "l"(Qimg + (size_t)(second ? nc - 1 - s % nc : s % nc) * (QIMG / 4) + (second ? QSLOT / 4 : 0)), "r"(bytes),
+            "r"(fb)
             : "memory");
         qr.next(NSQ);
       }
@@ -426,7 +429,7 @@ __global__ void __launch_bounds__(tc::NTH, 1)
         __syncwarp();
         if (lane == 0) tc_arrive(tc_su32(&xempty[xr.i]));
         xr.next(NSX);
-        const int col0 = c * KC + 16 * h;
+        const int col0 = (nc - 1 - c) * KC + 16 * h;   // reverse chunk order (see the X producer)
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           float4 o;
