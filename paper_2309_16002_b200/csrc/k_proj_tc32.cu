@@ -59,7 +59,7 @@ constexpr uint32_t T_ACC1 = 0;     // D1: 2 N1 <= 128 columns
 constexpr uint32_t T_XA = 128;     // pass-1 A: 2 stages x (hi 32 | lo 32)
 constexpr uint32_t T_LA = 256;     // pass-2 A: L-hat hi (64) | lo (64)
 constexpr uint32_t T_ACC2 = 384;   // D2: NACC2 stages x 32
-constexpr size_t SMEM = 1024 + (size_t)NSX * XSLOT + (size_t)NSQ * QSLOT + (size_t)M * NMAX * 4 + 4 * M * 8 + 512;
+constexpr size_t SMEM = 1024 + (size_t)NSX * XSLOT + (size_t)NSQ * QSLOT + 2 * 2 * M * 8 + 512;
 }  // namespace tc
 
 __device__ __forceinline__ uint32_t tc_su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -155,13 +155,6 @@ __device__ __forceinline__ void tc_split(float v, uint32_t& hi, uint32_t& lo) {
   hi = __float_as_uint(v) & 0xFFFFE000u;
   lo = __float_as_uint(v - __uint_as_float(hi));
 }
-__device__ __forceinline__ void tc_arrive_n(uint32_t b, uint32_t n) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;\n" ::"r"(b), "r"(n) : "memory");
-}
-__device__ __forceinline__ void tc_sts4(uint32_t a, float4 v) {
-  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
-               : "memory");
-}
 __device__ __forceinline__ void tc_rowbar() {
   asm volatile("bar.sync 1, %0;\n" ::"n"(tc::NROWW * 32) : "memory");
 }
@@ -177,56 +170,12 @@ struct TcRing {
   }
 };
 
-// DSMEM helpers (cluster of two CTAs: the column halves of one row tile)
-__device__ __forceinline__ uint32_t tc_mapa(uint32_t a, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(a), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ void tc_st_remote4(uint32_t a, float x, float y, float z, float w) {
-  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(a), "f"(x), "f"(y), "f"(z), "f"(w)
-               : "memory");
-}
-__device__ __forceinline__ void tc_st_remote_f64(uint32_t a, double v) {
-  asm volatile("st.shared::cluster.f64 [%0], %1;\n" ::"r"(a), "d"(v) : "memory");
-}
-__device__ __forceinline__ void tc_arrive_remote(uint32_t a) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(a) : "memory");
-}
-__device__ __forceinline__ void tc_wait_cluster(uint32_t b, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n"
-      "W_%=:\n"
-      " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra W_%=;\n"
-      "}\n" ::"r"(b),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void tc_cluster_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-}
-
-// Clusters of two CTAs share each 128-row tile: CTA rank r owns the chunks [r nch, (r+1) nch)
-// of the columns (nch = ceil(nc / 2)), so a CTA keeps only 128 x d/2 of the tile alive
-// between its two passes (the L2 re-read working set of 148 SMs stays well inside the
-// 126 MB L2).  Pass 1 gives each CTA a partial L-hat over its columns; the partials are
-// exchanged through distributed shared memory (remote stores + a remote mbarrier arrive)
-// and summed (P_0 + P_1, identical in both CTAs); pass 2 updates each CTA's own columns;
-// rank 1 sends its partial row norms to rank 0, which writes d(i) = n_0(i) + n_1(i).
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::NTH, 1)
+__global__ void __launch_bounds__(tc::NTH, 1)
     k_proj_tc32(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap xmap0, int lazy,
                 const float* __restrict__ Qimg, float* __restrict__ L, int64_t ldl, int64_t n, int d, int nc,
-                DevState* st, double* __restrict__ dvec, int part, long long* __restrict__ tr) {
+                DevState* st, float* __restrict__ Xr, int64_t ldx, double* __restrict__ dvec, int part) {
   using namespace tc;
-  // optional cycle trace of CTA 0, tiles 0-1 (RBRP_TC_TRACE=1; profiling only):
-  // tr[(event * 2 + tile) * 128 + step]
-  if (blockIdx.x != 0) tr = nullptr;
-#define TC_T(ev, pp, ss)                                                             \
-  do {                                                                               \
-    if (tr && (pp) < 2 && (ss) < 128) tr[((ev) * 2 + (pp)) * 128 + (ss)] = clock64(); \
-  } while (0)
-  if (st->stop) return;   // uniform over the grid (both CTAs of a cluster return together)
+  if (st->stop) return;
   int bp;
   int64_t k0;
   if (part < 0) {
@@ -246,10 +195,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::NTH, 1)
   uint8_t* sm = tc_smem + ((1024u - (tc_su32(tc_smem) & 1023u)) & 1023u);
   uint8_t* xs = sm;
   uint8_t* qs = xs + (size_t)NSX * XSLOT;
-  float* lrecv = reinterpret_cast<float*>(qs + (size_t)NSQ * QSLOT);   // [128][64] peer partial L-hat
-  double* nrm = reinterpret_cast<double*>(lrecv + M * NMAX);           // [h][128]
-  double* nrecv = nrm + 2 * M;                                          // [2][128] peer norms (rank 0)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(nrecv + 2 * M);
+  double* nrm = reinterpret_cast<double*>(qs + (size_t)NSQ * QSLOT);   // [tile parity][h][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(nrm + 2 * 2 * M);
   uint64_t* xfull = bars;
   uint64_t* xempty = xfull + NSX;
   uint64_t* qfull = xempty + NSX;
@@ -260,20 +207,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::NTH, 1)
   uint64_t* a2empty = a2full + NACC2;
   uint64_t* a1full = a2empty + NACC2;
   uint64_t* lafull = a1full + 1;
-  uint64_t* lfull = lafull + 1;    // the peer's partial L-hat has arrived (8 remote arrivals)
-  uint64_t* lempty = lfull + 1;    // the peer has consumed my previous partial (8 remote arrivals)
-  uint64_t* nfull = lempty + 1;    // [2] rank 1's norms have arrived (rank 0; 4 remote arrivals)
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(nfull + 2);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(lafull + 1);
 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  uint32_t rank;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(rank));
-  const uint32_t peer = rank ^ 1u;
-  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
-  const int nch = (nc + 1) / 2, cbeg = (int)rank * nch;
-  const int mync = nc - cbeg < nch ? nc - cbeg : nch;   // >= 1 (nc >= 2, proj_tc32_supported)
   const int64_t ntiles = (n + M - 1) / M;
-  const int T = ntiles > cid ? (int)((ntiles - 1 - cid) / ncl + 1) : 0;   // same for both CTAs
+  const int T = ntiles > blockIdx.x ? (int)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
   if (T == 0) {
     proj_end_stamp(st);
     return;
@@ -290,7 +228,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::NTH, 1)
     for (int s = 0; s < 2; ++s) {
       tc_bar_init(tc_su32(&afull[s]), NROWW);
       tc_bar_init(tc_su32(&aempty[s]), 1);
-      tc_bar_init(tc_su32(&nfull[s]), NROWW / 2);
     }
     for (int s = 0; s < NACC2; ++s) {
       tc_bar_init(tc_su32(&a2full[s]), 1);
@@ -298,8 +235,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::NTH, 1)
     }
     tc_bar_init(tc_su32(a1full), 1);
     tc_bar_init(tc_su32(lafull), NROWW);
-    tc_bar_init(tc_su32(lfull), NROWW);
-    tc_bar_init(tc_su32(lempty), NROWW);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (w == W_MMA) {   // the whole warp allocates all 512 TMEM columns (one CTA per SM)
@@ -308,36 +243,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::NTH, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
   }
   tc_fence_before();
-  tc_cluster_sync();   // barriers of both CTAs initialised before any remote arrive
+  __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tslot;
-  auto row0_of = [&](int p) { return ((int64_t)cid + (int64_t)p * ncl) * M; };
-  // local chunk index (pass 1 forward, pass 2 in reverse: the most recently loaded chunks
-  // are re-read first, while they are still in L2) -> global chunk
-  auto gchunk = [&](int s) {
-    const int cl = s % mync;
-    return cbeg + (((s / mync) & 1) ? mync - 1 - cl : cl);
-  };
-  const int steps = T * 2 * mync;
+  auto row0_of = [&](int p) { return ((int64_t)blockIdx.x + (int64_t)p * gridDim.x) * M; };
+  const int steps = T * 2 * nc;
 
   if (w == W_XP) {
     if (lane == 0) {
-      const CUtensorMap* mp = (lazy && st->t == 1 && part <= 0) ? &xmap0 : &xmap;   // lazy X_res copy
+      // X chunks, pass 1 then pass 2 of every tile.  Lazy X_res copy: block 1 reads X itself
+      const CUtensorMap* mp = (lazy && st->t == 1 && part <= 0) ? &xmap0 : &xmap;
       uint64_t pol_keep, pol_drop;
       asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol_keep));
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol_drop));
       TcRing xr;
       for (int s = 0; s < steps; ++s) {
         tc_wait(tc_su32(&xempty[xr.i]), xr.ph ^ 1u);
-        TC_T(8, s / (2 * mync), s % (2 * mync));
-        const bool second = (s / mync) & 1;
-        const int y = (int)row0_of(s / (2 * mync));
+        const bool second = (s / nc) & 1;
+        // pass 2 walks the chunks in reverse: the most recently loaded ones are re-read first,
+        // while they are still in L2
+        const int y = (int)row0_of(s / (2 * nc)), c = second ? nc - 1 - s % nc : s % nc;
         const uint32_t fb = tc_su32(&xfull[xr.i]);
         tc_expect(fb, XSLOT);   // out-of-bounds rows / columns are zero-filled
         asm volatile(
             "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint "
             "[%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(tc_su32(xs + (size_t)xr.i * XSLOT)),
-            "l"(mp), "r"(gchunk(s) * KC), "r"(y), "r"(fb), "l"(second ? pol_drop : pol_keep)
+            "l"(mp), "r"(c * KC), "r"(y), "r"(fb), "l"(second ? pol_drop : pol_keep)
             : "memory");
         xr.next(NSX);
       }
@@ -353,13 +284,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::NTH, 1)
       for (int s = 0; s < steps; ++s) {
         tc_wait(tc_su32(&qempty[qr.i]), qr.ph ^ 1u);
         const uint32_t fb = tc_su32(&qfull[qr.i]);
-        const bool second = (s / mync) & 1;
+        const bool second = (s / nc) & 1;
         const uint32_t bytes = second ? bytes2 : bytes1;
         tc_expect(fb, bytes);
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
                 tc_su32(qs + (size_t)qr.i * QSLOT)),
-            "l"(Qimg + (size_t)gchunk(s) * (QIMG / 4) + (second ? QSLOT / 4 : 0)), "r"(bytes), "r"(fb)
+            "l"(Qimg + (size_t)(second ? nc - 1 - s % nc : s % nc) * (QIMG / 4) + (second ? QSLOT / 4 : 0)), "r"(bytes),
+            "r"(fb)
             : "memory");
         qr.next(NSQ);
       }
@@ -371,12 +303,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::NTH, 1)
       const uint32_t qs0 = tc_su32(qs);
       TcRing qr, ar, cr;
       for (int p = 0; p < T; ++p) {
-        // pass 1: D1 = X_hi [Q_hi; Q_lo]^T + X_lo [Q_hi]^T over this CTA's columns
-        for (int c = 0; c < mync; ++c) {
+        // pass 1: D1 = X_hi [Q_hi; Q_lo]^T + X_lo [Q_hi]^T
+        for (int c = 0; c < nc; ++c) {
           tc_wait(tc_su32(&afull[ar.i]), ar.ph);
           tc_wait(tc_su32(&qfull[qr.i]), qr.ph);
           tc_fence_after();
-          TC_T(0, p, c);
           const uint32_t qa = qs0 + qr.i * QSLOT;
           const uint32_t xa = tbase + T_XA + 64u * ar.i;
 #pragma unroll
@@ -387,7 +318,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::NTH, 1)
           }
           tc_commit(tc_su32(&aempty[ar.i]));
           tc_commit(tc_su32(&qempty[qr.i]));
-          TC_T(1, p, c);
           ar.next(2);
           qr.next(NSQ);
         }
@@ -395,11 +325,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::NTH, 1)
         // pass 2: D2(chunk) = L_hi Q_hi + L_hi Q_lo + L_lo Q_hi  (B = image 2, K-major)
         tc_wait(tc_su32(lafull), (uint32_t)(p & 1));
         tc_fence_after();
-        for (int c = 0; c < mync; ++c) {
+        for (int c = 0; c < nc; ++c) {
           tc_wait(tc_su32(&qfull[qr.i]), qr.ph);
           tc_wait(tc_su32(&a2empty[cr.i]), cr.ph ^ 1u);
           tc_fence_after();
-          TC_T(0, p, mync + c);
           const uint32_t qa = qs0 + qr.i * QSLOT;
           const uint32_t da = tbase + T_ACC2 + KC * cr.i;
           for (int ks = 0; ks < N1 / 8; ++ks) {
@@ -412,7 +341,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::NTH, 1)
           }
           tc_commit(tc_su32(&qempty[qr.i]));
           tc_commit(tc_su32(&a2full[cr.i]));
-          TC_T(1, p, mync + c);
           qr.next(NSQ);
           cr.next(NACC2);
         }
@@ -427,20 +355,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::NTH, 1)
     const uint32_t tl = tbase + ((uint32_t)(32 * qq) << 16);
     const uint32_t xs0 = tc_su32(xs);
     const int half = N1 / 2;
-    const uint32_t lr_peer = tc_mapa(tc_su32(lrecv), peer);
-    const uint32_t lf_peer = tc_mapa(tc_su32(lfull), peer), le_peer = tc_mapa(tc_su32(lempty), peer);
-    const uint32_t nr_peer = tc_mapa(tc_su32(nrecv), peer), nf_peer = tc_mapa(tc_su32(nfull), peer);
-    const bool st_thr = (w == W_ROW0 && lane == 0);
-    uint64_t pol_st = 0;
-    if (st_thr) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol_st));
     TcRing xr, ar, cr;
     for (int p = 0; p < T; ++p) {
       const int64_t row = row0_of(p) + r;
       const bool vr = row < n;
       // ---- pass 1: split the X chunk into TMEM (A operand)
-      for (int c = 0; c < mync; ++c) {
+      for (int c = 0; c < nc; ++c) {
         tc_wait(tc_su32(&xfull[xr.i]), xr.ph);
-        if (w == W_ROW0 && lane == 0) TC_T(2, p, c);
         const uint32_t xa = xs0 + xr.i * XSLOT + r * 128;
         float v[16];
 #pragma unroll
@@ -459,78 +380,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::NTH, 1)
         for (int i = 0; i < 16; ++i) tc_split(v[i], hi[i], lo[i]);
         tc_wait(tc_su32(&aempty[ar.i]), ar.ph ^ 1u);
         tc_fence_after();
-        if (w == W_ROW0 && lane == 0) TC_T(3, p, c);
         tc_st16(tl + T_XA + 64u * ar.i + 16 * h, hi);
         tc_st16(tl + T_XA + 64u * ar.i + 32 + 16 * h, lo);
         tc_wait_st();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) tc_arrive(tc_su32(&afull[ar.i]));
-        if (w == W_ROW0 && lane == 0) TC_T(4, p, c);
         ar.next(2);
       }
-      // ---- epilogue 1: partial L-hat over this CTA's columns, exchanged with the peer CTA
-      // (DSMEM), L-hat = P_0 + P_1 -> L (rank 0) and its split -> TMEM (pass-2 A)
+      // ---- epilogue 1: L-hat = D1[0:N1) + D1[N1:2N1) -> L, and its split -> TMEM (pass-2 A)
       tc_wait(tc_su32(a1full), (uint32_t)(p & 1));
       tc_fence_after();
-      float P[32];
+      for (int j0 = h * half; j0 < (h + 1) * half; j0 += 8) {
+        float a[8], b[8];
+        tc_ld8(tl + T_ACC1 + j0, a);
+        tc_ld8(tl + T_ACC1 + N1 + j0, b);
+        uint32_t hi[8], lo[8];
 #pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        const int j0 = h * half + 8 * g;
-        if (8 * g < half) {
-          float a[8], b[8];
-          tc_ld8(tl + T_ACC1 + j0, a);
-          tc_ld8(tl + T_ACC1 + N1 + j0, b);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) P[8 * g + j] = a[j] + b[j];
+        for (int j = 0; j < 8; ++j) {
+          const float lv = a[j] + b[j];
+          if (vr && j0 + j < bp) L[row * ldl + k0 + j0 + j] = lv;
+          tc_split(lv, hi[j], lo[j]);
         }
+        tc_st8(tl + T_LA + j0, hi);
+        tc_st8(tl + T_LA + 64 + j0, lo);
       }
-      if (p > 0) tc_wait_cluster(tc_su32(lempty), (uint32_t)((p - 1) & 1));   // peer consumed my last one
-#pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        const int j0 = h * half + 8 * g;
-        if (8 * g < half) {
-          const uint32_t ra = lr_peer + (uint32_t)(r * NMAX + j0) * 4u;
-          tc_st_remote4(ra, P[8 * g], P[8 * g + 1], P[8 * g + 2], P[8 * g + 3]);
-          tc_st_remote4(ra + 16, P[8 * g + 4], P[8 * g + 5], P[8 * g + 6], P[8 * g + 7]);
-        }
-      }
-      __syncwarp();
-      if (lane == 0) tc_arrive_remote(lf_peer);
-      tc_wait_cluster(tc_su32(lfull), (uint32_t)(p & 1));
-#pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        const int j0 = h * half + 8 * g;
-        if (8 * g < half) {
-          const float4 q0 = tc_lds4(tc_su32(lrecv + r * NMAX + j0));
-          const float4 q1 = tc_lds4(tc_su32(lrecv + r * NMAX + j0 + 4));
-          const float R[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
-          uint32_t hi[8], lo[8];
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const float lv = P[8 * g + j] + R[j];   // P_0 + P_1 (addition is commutative)
-            if (rank == 0 && vr && j0 + j < bp) L[row * ldl + k0 + j0 + j] = lv;
-            tc_split(lv, hi[j], lo[j]);
-          }
-          tc_st8(tl + T_LA + j0, hi);
-          tc_st8(tl + T_LA + 64 + j0, lo);
-        }
-      }
-      __syncwarp();
-      if (lane == 0) tc_arrive_remote(le_peer);   // lrecv consumed: the peer may send the next one
       tc_wait_st();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) tc_arrive(tc_su32(lafull));
-      // ---- pass 2: x_res = x - D2, written back into the X slot and stored by one TMA bulk
-      // tensor store per chunk (full 128-byte lines; the slot is released once the store has
-      // read it); fp64 norms of the stored values
+      // ---- pass 2: x_res = x - D2, stored once; fp64 norms of the stored values
       double nr = 0.0;
-      int pend = -1;   // st_thr: X slot of the outstanding store
-      for (int c = 0; c < mync; ++c) {
+      float* xrow = Xr + row * ldx;
+      for (int c = 0; c < nc; ++c) {
         tc_wait(tc_su32(&a2full[cr.i]), cr.ph);
         tc_fence_after();
-        if (w == W_ROW0 && lane == 0) TC_T(5, p, c);
         float a[16];
         tc_ld16(tl + T_ACC2 + KC * cr.i + 16 * h, a);
         tc_fence_before();
@@ -538,76 +422,42 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::NTH, 1)
         if (lane == 0) tc_arrive(tc_su32(&a2empty[cr.i]));
         cr.next(NACC2);
         tc_wait(tc_su32(&xfull[xr.i]), xr.ph);
-        if (w == W_ROW0 && lane == 0) TC_T(6, p, c);
-        const uint32_t xsl = xs0 + xr.i * XSLOT;
-        const uint32_t xa = xsl + r * 128;
+        const uint32_t xa = xs0 + xr.i * XSLOT + r * 128;
+        float4 xv[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) xv[i] = tc_lds4(xa + ((((4 * h + i) ^ (r & 7))) << 4));
+        __syncwarp();
+        if (lane == 0) tc_arrive(tc_su32(&xempty[xr.i]));
+        xr.next(NSX);
+        const int col0 = (nc - 1 - c) * KC + 16 * h;   // reverse chunk order (see the X producer)
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const uint32_t ad = xa + ((((4 * h + i) ^ (r & 7))) << 4);
-          const float4 xv = tc_lds4(ad);
           float4 o;
-          o.x = xv.x - a[4 * i];
-          o.y = xv.y - a[4 * i + 1];
-          o.z = xv.z - a[4 * i + 2];
-          o.w = xv.w - a[4 * i + 3];
+          o.x = xv[i].x - a[4 * i];
+          o.y = xv[i].y - a[4 * i + 1];
+          o.z = xv[i].z - a[4 * i + 2];
+          o.w = xv[i].w - a[4 * i + 3];
           nr = fma((double)o.x, (double)o.x, nr);
           nr = fma((double)o.y, (double)o.y, nr);
           nr = fma((double)o.z, (double)o.z, nr);
           nr = fma((double)o.w, (double)o.w, nr);
-          tc_sts4(ad, o);
+          if (vr && col0 + 4 * i < d) __stcs(reinterpret_cast<float4*>(xrow + col0 + 4 * i), o);
         }
-        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // visible to the TMA store
-        tc_rowbar();
-        if (st_thr) {
-          const int col = gchunk(2 * mync * p + mync + c) * KC;
-          asm volatile(
-              "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2}], [%3], %4;\n" ::"l"(
-                  &xmap),
-              "r"(col), "r"((int)row0_of(p)), "r"(xsl), "l"(pol_st)
-              : "memory");
-          asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
-          if (pend >= 0) {
-            asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
-            tc_arrive_n(tc_su32(&xempty[pend]), NROWW);
-          }
-          pend = xr.i;
-          TC_T(7, p, c);
-        }
-        xr.next(NSX);
       }
-      if (st_thr && pend >= 0) {
-        asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
-        tc_arrive_n(tc_su32(&xempty[pend]), NROWW);
-      }
-      // d(i) = ||x_res,i||^2: the two column halves of this CTA, then rank 1's partial added
-      // by rank 0 (fixed order)
-      nrm[h * M + r] = nr;
+      // d(i) = ||x_res,i||^2: the two column halves summed in a fixed order
+      double* nb = nrm + (size_t)(p & 1) * 2 * M;
+      nb[h * M + r] = nr;
       tc_rowbar();
-      if (h == 0) {
-        const double own = nrm[r] + nrm[M + r];
-        const int nb = p & 1;
-        if (rank == 1) {
-          tc_st_remote_f64(nr_peer + (uint32_t)(nb * M + r) * 8u, own);
-          __syncwarp();
-          if (lane == 0) tc_arrive_remote(nf_peer + 8u * nb);
-        } else {
-          tc_wait_cluster(tc_su32(&nfull[nb]), (uint32_t)((p >> 1) & 1));
-          if (vr) dvec[row] = own + nrecv[nb * M + r];
-        }
-      }
-      tc_rowbar();   // nrm is rewritten at the next tile's end
+      if (h == 0 && vr) dvec[row] = nb[r] + nb[M + r];
     }
   }
-  if (w == W_ROW0 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");   // stores complete
   tc_fence_before();
   __syncthreads();
   if (w == W_MMA) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase) : "memory");
   }
-  tc_cluster_sync();   // the peer may still read / arrive on this CTA's shared memory until here
   proj_end_stamp(st);
-#undef TC_T
 }
 
 // Packed Q_b chunk images for k_proj_tc32 (128-byte swizzle of a 1024-byte-aligned shared-
@@ -657,13 +507,6 @@ __global__ void k_pack_tc32(const float* __restrict__ Qt, int64_t d, float* __re
   }
 }
 
-static long long* g_tc_trace = nullptr;
-extern "C" int rbrp_debug_tc_trace(long long* host, int count) {
-  if (!g_tc_trace) return -1;
-  if (count > 9 * 2 * 128) count = 9 * 2 * 128;
-  return cudaMemcpy(host, g_tc_trace, count * sizeof(long long), cudaMemcpyDeviceToHost) == cudaSuccess ? count : -1;
-}
-
 static PFN_cuTensorMapEncodeTiled_v12000 tc_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -678,7 +521,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 tc_encode() {
 }
 
 bool proj_tc32_supported(const void* X, int64_t ldx, int64_t d) {
-  return d > tc::KC && d % 4 == 0 && ldx % 4 == 0 && ((uintptr_t)X % 16) == 0 && tc_encode() != nullptr;
+  return d >= 8 && d % 4 == 0 && ldx % 4 == 0 && ((uintptr_t)X % 16) == 0 && tc_encode() != nullptr;
 }
 
 size_t tc32_pack_bytes(int64_t d) { return (size_t)((d + tc::KC - 1) / tc::KC) * tc::QIMG; }
@@ -714,23 +557,10 @@ cudaError_t launch_proj_tc32(float* X, int64_t ldx, const float* Qimg, float* L,
   static PerDevice attr;
   cudaError_t e = attr.once(
       [] { return cudaFuncSetAttribute(k_proj_tc32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::SMEM); });
-  long long* tr = nullptr;
-  {   // RBRP_TC_TRACE=1 (profiling only): cycle trace of the first launch
-    static long long* buf = nullptr;
-    static bool traced = false;
-    const char* ev = getenv("RBRP_TC_TRACE");
-    if (ev && ev[0] == '1' && !traced) {
-      if (!buf && cudaMalloc(&buf, 9 * 2 * 128 * sizeof(long long)) == cudaSuccess)
-        cudaMemset(buf, 0, 9 * 2 * 128 * sizeof(long long));
-      tr = buf;
-      traced = true;
-      g_tc_trace = buf;
-    }
-  }
   if (e != cudaSuccess) return e;
   const int nc = (int)((d + tc::KC - 1) / tc::KC);
-  k_proj_tc32<<<device_sms() & ~1, tc::NTH, tc::SMEM, s>>>(map, map0, X0 ? 1 : 0, Qimg, L, ldl, n, (int)d, nc, st,
-                                                            dvec, part, tr);
+  k_proj_tc32<<<device_sms(), tc::NTH, tc::SMEM, s>>>(map, map0, X0 ? 1 : 0, Qimg, L, ldl, n, (int)d, nc, st, X, ldx,
+                                                       dvec, part);
   return cudaGetLastError();
 }
 
