@@ -49,7 +49,9 @@ constexpr int NMAX = 64;                  // Q_b rows per part
 constexpr int XSLOT = M * KC * 4;         // 16 KB X chunk
 constexpr int QSLOT = 2 * NMAX * KC * 4;  // 16 KB shared-memory Q stage (one image)
 constexpr int QIMG = 2 * QSLOT;           // global: image 1 (pass 1) + image 2 (pass 2) per chunk
-constexpr int NSX = 6, NSQ = 4;           // ring depths
+constexpr int NSX = 7;                    // X ring depth
+constexpr int QRING = 96 * 1024;          // Q ring bytes: slots of the launch's image size (<= QSLOT)
+constexpr int NSQMAX = 24;
 constexpr int NROWW = 8;                  // row warps
 constexpr int W_XP = 0, W_MMA = 1, W_QP = 2, W_ROW0 = 3;
 constexpr int NTH = (W_ROW0 + NROWW) * 32;
@@ -59,7 +61,7 @@ constexpr uint32_t T_ACC1 = 0;     // D1: 2 N1 <= 128 columns
 constexpr uint32_t T_XA = 128;     // pass-1 A: 2 stages x (hi 32 | lo 32)
 constexpr uint32_t T_LA = 256;     // pass-2 A: L-hat hi (64) | lo (64)
 constexpr uint32_t T_ACC2 = 384;   // D2: NACC2 stages x 32
-constexpr size_t SMEM = 1024 + (size_t)NSX * XSLOT + (size_t)NSQ * QSLOT + 2 * 2 * M * 8 + 512;
+constexpr size_t SMEM = 1024 + (size_t)NSX * XSLOT + QRING + 2 * 2 * M * 8 + 1024;
 }  // namespace tc
 
 __device__ __forceinline__ uint32_t tc_su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -155,6 +157,13 @@ __device__ __forceinline__ void tc_split(float v, uint32_t& hi, uint32_t& lo) {
   hi = __float_as_uint(v) & 0xFFFFE000u;
   lo = __float_as_uint(v - __uint_as_float(hi));
 }
+__device__ __forceinline__ void tc_arrive_n(uint32_t b, uint32_t n) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;\n" ::"r"(b), "r"(n) : "memory");
+}
+__device__ __forceinline__ void tc_sts4(uint32_t a, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
 __device__ __forceinline__ void tc_rowbar() {
   asm volatile("bar.sync 1, %0;\n" ::"n"(tc::NROWW * 32) : "memory");
 }
@@ -173,8 +182,16 @@ struct TcRing {
 __global__ void __launch_bounds__(tc::NTH, 1)
     k_proj_tc32(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap xmap0, int lazy,
                 const float* __restrict__ Qimg, float* __restrict__ L, int64_t ldl, int64_t n, int d, int nc,
-                DevState* st, float* __restrict__ Xr, int64_t ldx, double* __restrict__ dvec, int part) {
+                DevState* st, float* __restrict__ Xr, int64_t ldx, double* __restrict__ dvec, int part,
+                long long* __restrict__ tr) {
   using namespace tc;
+  // optional cycle trace of CTA 0, tiles 0-1 (RBRP_TC_TRACE=1; profiling only):
+  // tr[(event * 2 + tile) * 128 + step]
+  if (blockIdx.x != 0) tr = nullptr;
+#define TC_T(ev, pp, ss)                                                             \
+  do {                                                                               \
+    if (tr && (pp) < 2 && (ss) < 128) tr[((ev) * 2 + (pp)) * 128 + (ss)] = clock64(); \
+  } while (0)
   if (st->stop) return;
   int bp;
   int64_t k0;
@@ -189,19 +206,23 @@ __global__ void __launch_bounds__(tc::NTH, 1)
     k0 = st->k + NMAX * part;
   }
   const int N1 = (bp + 15) & ~15;
+  // Q ring slots sized for this launch's images (1 KB multiples: 1024-byte-aligned images)
+  const int nkb_ = (N1 + 31) / 32;
+  const int qslot = max(2 * N1 * KC * 4, 2 * nkb_ * KC * 128);
+  const int NSQ = min(NSQMAX, QRING / qslot);
   if (blockIdx.x == 0 && threadIdx.x == 0 && part <= 0) st->ts0 = gtimer();
 
   extern __shared__ __align__(1024) uint8_t tc_smem[];
   uint8_t* sm = tc_smem + ((1024u - (tc_su32(tc_smem) & 1023u)) & 1023u);
   uint8_t* xs = sm;
   uint8_t* qs = xs + (size_t)NSX * XSLOT;
-  double* nrm = reinterpret_cast<double*>(qs + (size_t)NSQ * QSLOT);   // [tile parity][h][128]
+  double* nrm = reinterpret_cast<double*>(qs + QRING);   // [tile parity][h][128]
   uint64_t* bars = reinterpret_cast<uint64_t*>(nrm + 2 * 2 * M);
   uint64_t* xfull = bars;
   uint64_t* xempty = xfull + NSX;
   uint64_t* qfull = xempty + NSX;
-  uint64_t* qempty = qfull + NSQ;
-  uint64_t* afull = qempty + NSQ;
+  uint64_t* qempty = qfull + NSQMAX;
+  uint64_t* afull = qempty + NSQMAX;
   uint64_t* aempty = afull + 2;
   uint64_t* a2full = aempty + 2;
   uint64_t* a2empty = a2full + NACC2;
@@ -221,7 +242,7 @@ __global__ void __launch_bounds__(tc::NTH, 1)
       tc_bar_init(tc_su32(&xfull[s]), 1);
       tc_bar_init(tc_su32(&xempty[s]), NROWW);
     }
-    for (int s = 0; s < NSQ; ++s) {
+    for (int s = 0; s < NSQMAX; ++s) {
       tc_bar_init(tc_su32(&qfull[s]), 1);
       tc_bar_init(tc_su32(&qempty[s]), 1);
     }
@@ -259,6 +280,7 @@ __global__ void __launch_bounds__(tc::NTH, 1)
       TcRing xr;
       for (int s = 0; s < steps; ++s) {
         tc_wait(tc_su32(&xempty[xr.i]), xr.ph ^ 1u);
+        TC_T(8, s / (2 * nc), s % (2 * nc));
         const bool second = (s / nc) & 1;
         // pass 2 walks the chunks in reverse: the most recently loaded ones are re-read first,
         // while they are still in L2
@@ -289,7 +311,7 @@ __global__ void __launch_bounds__(tc::NTH, 1)
         tc_expect(fb, bytes);
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                tc_su32(qs + (size_t)qr.i * QSLOT)),
+                tc_su32(qs + (size_t)qr.i * qslot)),
             "l"(Qimg + (size_t)(second ? nc - 1 - s % nc : s % nc) * (QIMG / 4) + (second ? QSLOT / 4 : 0)), "r"(bytes),
             "r"(fb)
             : "memory");
@@ -308,7 +330,8 @@ __global__ void __launch_bounds__(tc::NTH, 1)
           tc_wait(tc_su32(&afull[ar.i]), ar.ph);
           tc_wait(tc_su32(&qfull[qr.i]), qr.ph);
           tc_fence_after();
-          const uint32_t qa = qs0 + qr.i * QSLOT;
+          TC_T(0, p, c);
+          const uint32_t qa = qs0 + qr.i * qslot;
           const uint32_t xa = tbase + T_XA + 64u * ar.i;
 #pragma unroll
           for (int ks = 0; ks < KC / 8; ++ks) {
@@ -318,6 +341,7 @@ __global__ void __launch_bounds__(tc::NTH, 1)
           }
           tc_commit(tc_su32(&aempty[ar.i]));
           tc_commit(tc_su32(&qempty[qr.i]));
+          TC_T(1, p, c);
           ar.next(2);
           qr.next(NSQ);
         }
@@ -329,7 +353,8 @@ __global__ void __launch_bounds__(tc::NTH, 1)
           tc_wait(tc_su32(&qfull[qr.i]), qr.ph);
           tc_wait(tc_su32(&a2empty[cr.i]), cr.ph ^ 1u);
           tc_fence_after();
-          const uint32_t qa = qs0 + qr.i * QSLOT;
+          TC_T(0, p, nc + c);
+          const uint32_t qa = qs0 + qr.i * qslot;
           const uint32_t da = tbase + T_ACC2 + KC * cr.i;
           for (int ks = 0; ks < N1 / 8; ++ks) {
             const uint32_t kb = (uint32_t)(ks >> 2), koff = 32u * (ks & 3);   // 32-K block, 8-K step in it
@@ -341,6 +366,7 @@ __global__ void __launch_bounds__(tc::NTH, 1)
           }
           tc_commit(tc_su32(&qempty[qr.i]));
           tc_commit(tc_su32(&a2full[cr.i]));
+          TC_T(1, p, nc + c);
           qr.next(NSQ);
           cr.next(NACC2);
         }
@@ -362,6 +388,7 @@ __global__ void __launch_bounds__(tc::NTH, 1)
       // ---- pass 1: split the X chunk into TMEM (A operand)
       for (int c = 0; c < nc; ++c) {
         tc_wait(tc_su32(&xfull[xr.i]), xr.ph);
+        if (w == W_ROW0 && lane == 0) TC_T(2, p, c);
         const uint32_t xa = xs0 + xr.i * XSLOT + r * 128;
         float v[16];
 #pragma unroll
@@ -380,12 +407,14 @@ __global__ void __launch_bounds__(tc::NTH, 1)
         for (int i = 0; i < 16; ++i) tc_split(v[i], hi[i], lo[i]);
         tc_wait(tc_su32(&aempty[ar.i]), ar.ph ^ 1u);
         tc_fence_after();
+        if (w == W_ROW0 && lane == 0) TC_T(3, p, c);
         tc_st16(tl + T_XA + 64u * ar.i + 16 * h, hi);
         tc_st16(tl + T_XA + 64u * ar.i + 32 + 16 * h, lo);
         tc_wait_st();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) tc_arrive(tc_su32(&afull[ar.i]));
+        if (w == W_ROW0 && lane == 0) TC_T(4, p, c);
         ar.next(2);
       }
       // ---- epilogue 1: L-hat = D1[0:N1) + D1[N1:2N1) -> L, and its split -> TMEM (pass-2 A)
@@ -409,12 +438,18 @@ __global__ void __launch_bounds__(tc::NTH, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) tc_arrive(tc_su32(lafull));
-      // ---- pass 2: x_res = x - D2, stored once; fp64 norms of the stored values
+      // ---- pass 2: x_res = x - D2, written back into the X slot and stored by one TMA bulk
+      // tensor store per chunk (full 128-byte lines; the slot is released once the store has
+      // read it); fp64 norms of the stored values
       double nr = 0.0;
-      float* xrow = Xr + row * ldx;
+      const bool st_thr = (w == W_ROW0 && lane == 0);
+      int pend = -1;   // st_thr: X slot of the outstanding store
+      uint64_t pol_st = 0;
+      if (st_thr) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol_st));
       for (int c = 0; c < nc; ++c) {
         tc_wait(tc_su32(&a2full[cr.i]), cr.ph);
         tc_fence_after();
+        if (w == W_ROW0 && lane == 0) TC_T(5, p, c);
         float a[16];
         tc_ld16(tl + T_ACC2 + KC * cr.i + 16 * h, a);
         tc_fence_before();
@@ -422,27 +457,46 @@ __global__ void __launch_bounds__(tc::NTH, 1)
         if (lane == 0) tc_arrive(tc_su32(&a2empty[cr.i]));
         cr.next(NACC2);
         tc_wait(tc_su32(&xfull[xr.i]), xr.ph);
-        const uint32_t xa = xs0 + xr.i * XSLOT + r * 128;
-        float4 xv[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) xv[i] = tc_lds4(xa + ((((4 * h + i) ^ (r & 7))) << 4));
-        __syncwarp();
-        if (lane == 0) tc_arrive(tc_su32(&xempty[xr.i]));
-        xr.next(NSX);
-        const int col0 = (nc - 1 - c) * KC + 16 * h;   // reverse chunk order (see the X producer)
+        if (w == W_ROW0 && lane == 0) TC_T(6, p, c);
+        const uint32_t xsl = xs0 + xr.i * XSLOT;
+        const uint32_t xa = xsl + r * 128;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
+          const uint32_t ad = xa + ((((4 * h + i) ^ (r & 7))) << 4);
+          const float4 xv = tc_lds4(ad);
           float4 o;
-          o.x = xv[i].x - a[4 * i];
-          o.y = xv[i].y - a[4 * i + 1];
-          o.z = xv[i].z - a[4 * i + 2];
-          o.w = xv[i].w - a[4 * i + 3];
+          o.x = xv.x - a[4 * i];
+          o.y = xv.y - a[4 * i + 1];
+          o.z = xv.z - a[4 * i + 2];
+          o.w = xv.w - a[4 * i + 3];
           nr = fma((double)o.x, (double)o.x, nr);
           nr = fma((double)o.y, (double)o.y, nr);
           nr = fma((double)o.z, (double)o.z, nr);
           nr = fma((double)o.w, (double)o.w, nr);
-          if (vr && col0 + 4 * i < d) __stcs(reinterpret_cast<float4*>(xrow + col0 + 4 * i), o);
+          tc_sts4(ad, o);
         }
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // visible to the TMA store
+        tc_rowbar();
+        if (st_thr) {
+          const int col = (nc - 1 - c) * KC;   // reverse chunk order (see the X producer)
+          asm volatile(
+              "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2}], [%3], %4;\n" ::"l"(
+                  &xmap),
+              "r"(col), "r"((int)row0_of(p)), "r"(xsl), "l"(pol_st)
+              : "memory");
+          asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+          if (pend >= 0) {
+            asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+            tc_arrive_n(tc_su32(&xempty[pend]), NROWW);
+          }
+          pend = xr.i;
+          TC_T(7, p, c);
+        }
+        xr.next(NSX);
+      }
+      if (st_thr && pend >= 0) {
+        asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+        tc_arrive_n(tc_su32(&xempty[pend]), NROWW);
       }
       // d(i) = ||x_res,i||^2: the two column halves summed in a fixed order
       double* nb = nrm + (size_t)(p & 1) * 2 * M;
@@ -451,6 +505,7 @@ __global__ void __launch_bounds__(tc::NTH, 1)
       if (h == 0 && vr) dvec[row] = nb[r] + nb[M + r];
     }
   }
+  if (w == W_ROW0 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");   // stores complete
   tc_fence_before();
   __syncthreads();
   if (w == W_MMA) {
@@ -458,6 +513,7 @@ __global__ void __launch_bounds__(tc::NTH, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase) : "memory");
   }
   proj_end_stamp(st);
+#undef TC_T
 }
 
 // Packed Q_b chunk images for k_proj_tc32 (128-byte swizzle of a 1024-byte-aligned shared-
@@ -505,6 +561,13 @@ __global__ void k_pack_tc32(const float* __restrict__ Qt, int64_t d, float* __re
     const float out = hl == 0 ? __uint_as_float(hi) : v - __uint_as_float(hi);
     img[QSLOT / 4 + (hl * nkb + kb) * (KC * KC) + nn * KC + ((((lane >> 2) ^ (nn & 7))) << 2) + (lane & 3)] = out;
   }
+}
+
+static long long* g_tc_trace = nullptr;
+extern "C" int rbrp_debug_tc_trace(long long* host, int count) {
+  if (!g_tc_trace) return -1;
+  if (count > 9 * 2 * 128) count = 9 * 2 * 128;
+  return cudaMemcpy(host, g_tc_trace, count * sizeof(long long), cudaMemcpyDeviceToHost) == cudaSuccess ? count : -1;
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 tc_encode() {
@@ -557,10 +620,22 @@ cudaError_t launch_proj_tc32(float* X, int64_t ldx, const float* Qimg, float* L,
   static PerDevice attr;
   cudaError_t e = attr.once(
       [] { return cudaFuncSetAttribute(k_proj_tc32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::SMEM); });
+  long long* tr = nullptr;
+  {   // RBRP_TC_TRACE=k (profiling only): cycle trace of the k-th launch of the process
+    static long long* buf = nullptr;
+    static int nlaunch = 0;
+    const char* ev = getenv("RBRP_TC_TRACE");
+    if (ev && atoi(ev) == ++nlaunch) {
+      if (!buf && cudaMalloc(&buf, 9 * 2 * 128 * sizeof(long long)) == cudaSuccess)
+        cudaMemset(buf, 0, 9 * 2 * 128 * sizeof(long long));
+      tr = buf;
+      g_tc_trace = buf;
+    }
+  }
   if (e != cudaSuccess) return e;
   const int nc = (int)((d + tc::KC - 1) / tc::KC);
   k_proj_tc32<<<device_sms(), tc::NTH, tc::SMEM, s>>>(map, map0, X0 ? 1 : 0, Qimg, L, ldl, n, (int)d, nc, st, X, ldx,
-                                                       dvec, part);
+                                                       dvec, part, tr);
   return cudaGetLastError();
 }
 

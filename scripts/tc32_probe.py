@@ -13,7 +13,7 @@ L_ = rb.lib()
 f = L_.rbrp_debug_tc32
 f.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
               ctypes.c_void_p]
-for (n, d, b) in [(128, 64, 16), (200, 36, 16), (256, 64, 16), (300, 96, 32), (1000, 256, 64), (5000, 2048, 64)]:
+for (n, d, b) in [(128, 32, 16), (256, 64, 16), (300, 96, 32), (1000, 256, 64), (5000, 2048, 64)]:
     rng = np.random.default_rng(0)
     X = rng.standard_normal((n, d)).astype(np.float32)
     Q = np.ascontiguousarray(np.linalg.qr(rng.standard_normal((d, b)))[0].T.astype(np.float32))

@@ -7,7 +7,7 @@ import sys
 import numpy as np
 import torch
 
-os.environ["RBRP_TC_TRACE"] = "1"
+os.environ.setdefault("RBRP_TC_TRACE", "1")
 os.environ["RBRP_NO_GRAPH"] = "1"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2309_16002_b200 as rb  # noqa: E402
