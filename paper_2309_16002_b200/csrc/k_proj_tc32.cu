@@ -86,20 +86,28 @@ __device__ __forceinline__ void tc_wait(uint32_t b, uint32_t parity) {
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
-// tcgen05.mma kind::tf32, A from TMEM, B from a shared-memory descriptor, D in TMEM
+// tcgen05.mma kind::tf32, A from TMEM, B from a shared-memory descriptor, D in TMEM.  Called
+// by the whole (converged) MMA warp with warp-uniform operands; elect.sync picks the one
+// lane that issues (no per-instruction divergence loop around the uniform-datapath op).
 __device__ __forceinline__ void tc_mma(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
   asm volatile(
-      "{\n .reg .pred p;\n"
+      "{\n .reg .pred p, e;\n"
+      " elect.sync _|e, 0xffffffff;\n"
       " setp.ne.b32 p, %4, 0;\n"
-      " tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n"
+      " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n"
       "}\n" ::"r"(d),
       "r"(a), "l"(bdesc), "r"(idesc), "r"(acc)
       : "memory");
 }
-// arrive on the mbarrier once every tcgen05 operation issued so far by this thread is done
+// arrive on the mbarrier once every tcgen05 operation issued so far by the elected lane
+// (always lane 0 of the converged warp) is done
 __device__ __forceinline__ void tc_commit(uint32_t b) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(b)
-               : "memory");
+  asm volatile(
+      "{\n .reg .pred e;\n"
+      " elect.sync _|e, 0xffffffff;\n"
+      " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+      "}\n" ::"r"(b)
+      : "memory");
 }
 // shared-memory matrix descriptor: 128-byte swizzle, version 1 (sm_100)
 __device__ __forceinline__ uint64_t tc_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -166,6 +174,27 @@ __device__ __forceinline__ void tc_sts4(uint32_t a, float4 v) {
 }
 __device__ __forceinline__ void tc_rowbar() {
   asm volatile("bar.sync 1, %0;\n" ::"n"(tc::NROWW * 32) : "memory");
+}
+
+// dst[0 .. cnt) = v[0 .. cnt), cnt <= 32: PRE scalars up to 16-byte alignment, then float4s
+template <int PRE>
+__device__ __forceinline__ void tc_store_row(float* dst, const float (&v)[32], int cnt) {
+#pragma unroll
+  for (int j = 0; j < PRE; ++j)
+    if (j < cnt) dst[j] = v[j];
+#pragma unroll
+  for (int j = PRE; j + 4 <= 32; j += 4) {
+    if (j + 4 <= cnt) {
+      *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (j + u < cnt) dst[j + u] = v[j + u];
+    }
+  }
+#pragma unroll
+  for (int j = PRE + ((32 - PRE) / 4) * 4; j < 32; ++j)
+    if (j < cnt) dst[j] = v[j];
 }
 
 struct TcRing {
@@ -319,7 +348,7 @@ __global__ void __launch_bounds__(tc::NTH, 1)
       }
     }
   } else if (w == W_MMA) {
-    if (lane == 0) {
+    {   // the whole warp runs the issue loop (uniform control flow); one elected lane issues
       const uint32_t id1a = tc_idesc(2 * N1, 0), id1b = tc_idesc(N1, 0), id2 = tc_idesc(KC, 0);
       const int nkb = (N1 + 31) / 32;
       const uint32_t qs0 = tc_su32(qs);
@@ -330,7 +359,7 @@ __global__ void __launch_bounds__(tc::NTH, 1)
           tc_wait(tc_su32(&afull[ar.i]), ar.ph);
           tc_wait(tc_su32(&qfull[qr.i]), qr.ph);
           tc_fence_after();
-          TC_T(0, p, c);
+          if (lane == 0) TC_T(0, p, c);
           const uint32_t qa = qs0 + qr.i * qslot;
           const uint32_t xa = tbase + T_XA + 64u * ar.i;
 #pragma unroll
@@ -341,7 +370,7 @@ __global__ void __launch_bounds__(tc::NTH, 1)
           }
           tc_commit(tc_su32(&aempty[ar.i]));
           tc_commit(tc_su32(&qempty[qr.i]));
-          TC_T(1, p, c);
+          if (lane == 0) TC_T(1, p, c);
           ar.next(2);
           qr.next(NSQ);
         }
@@ -353,7 +382,7 @@ __global__ void __launch_bounds__(tc::NTH, 1)
           tc_wait(tc_su32(&qfull[qr.i]), qr.ph);
           tc_wait(tc_su32(&a2empty[cr.i]), cr.ph ^ 1u);
           tc_fence_after();
-          TC_T(0, p, nc + c);
+          if (lane == 0) TC_T(0, p, nc + c);
           const uint32_t qa = qs0 + qr.i * qslot;
           const uint32_t da = tbase + T_ACC2 + KC * cr.i;
           for (int ks = 0; ks < N1 / 8; ++ks) {
@@ -366,7 +395,7 @@ __global__ void __launch_bounds__(tc::NTH, 1)
           }
           tc_commit(tc_su32(&qempty[qr.i]));
           tc_commit(tc_su32(&a2full[cr.i]));
-          TC_T(1, p, nc + c);
+          if (lane == 0) TC_T(1, p, nc + c);
           qr.next(NSQ);
           cr.next(NACC2);
         }
@@ -420,24 +449,38 @@ __global__ void __launch_bounds__(tc::NTH, 1)
       // ---- epilogue 1: L-hat = D1[0:N1) + D1[N1:2N1) -> L, and its split -> TMEM (pass-2 A)
       tc_wait(tc_su32(a1full), (uint32_t)(p & 1));
       tc_fence_after();
-      for (int j0 = h * half; j0 < (h + 1) * half; j0 += 8) {
-        float a[8], b[8];
-        tc_ld8(tl + T_ACC1 + j0, a);
-        tc_ld8(tl + T_ACC1 + N1 + j0, b);
-        uint32_t hi[8], lo[8];
+      float P[32];   // L-hat(row, h half .. + half), kept for the L stores below
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float lv = a[j] + b[j];
-          if (vr && j0 + j < bp) L[row * ldl + k0 + j0 + j] = lv;
-          tc_split(lv, hi[j], lo[j]);
+      for (int g = 0; g < 4; ++g) {
+        if (8 * g < half) {
+          const int j0 = h * half + 8 * g;
+          float a[8], b[8];
+          tc_ld8(tl + T_ACC1 + j0, a);
+          tc_ld8(tl + T_ACC1 + N1 + j0, b);
+          uint32_t hi[8], lo[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            P[8 * g + j] = a[j] + b[j];
+            tc_split(P[8 * g + j], hi[j], lo[j]);
+          }
+          tc_st8(tl + T_LA + j0, hi);
+          tc_st8(tl + T_LA + 64 + j0, lo);
         }
-        tc_st8(tl + T_LA + j0, hi);
-        tc_st8(tl + T_LA + 64 + j0, lo);
       }
       tc_wait_st();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) tc_arrive(tc_su32(lafull));
+      if (lane == 0) tc_arrive(tc_su32(lafull));   // pass 2 may start; L is written meanwhile
+      if (vr) {
+        const int cnt = min(half, bp - h * half);
+        float* dst = L + row * ldl + k0 + h * half;
+        switch ((4 - (int)(((uintptr_t)dst >> 2) & 3)) & 3) {   // warp-uniform (ldl % 4 == 0)
+          case 0: tc_store_row<0>(dst, P, cnt); break;
+          case 1: tc_store_row<1>(dst, P, cnt); break;
+          case 2: tc_store_row<2>(dst, P, cnt); break;
+          default: tc_store_row<3>(dst, P, cnt); break;
+        }
+      }
       // ---- pass 2: x_res = x - D2, written back into the X slot and stored by one TMA bulk
       // tensor store per chunk (full 128-byte lines; the slot is released once the store has
       // read it); fp64 norms of the stored values
