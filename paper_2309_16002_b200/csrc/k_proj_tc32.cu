@@ -42,6 +42,9 @@
 
 namespace rbrp {
 
+#ifndef TC_KEEP_FRAC
+#define TC_KEEP_FRAC 0.75
+#endif
 namespace tc {
 constexpr int M = 128;                    // rows per tile (TMEM lanes)
 constexpr int KC = 32;                    // columns per chunk (128-byte swizzle row)
@@ -181,20 +184,20 @@ template <int PRE>
 __device__ __forceinline__ void tc_store_row(float* dst, const float (&v)[32], int cnt) {
 #pragma unroll
   for (int j = 0; j < PRE; ++j)
-    if (j < cnt) dst[j] = v[j];
+    if (j < cnt) __stcs(dst + j, v[j]);
 #pragma unroll
   for (int j = PRE; j + 4 <= 32; j += 4) {
     if (j + 4 <= cnt) {
-      *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+      __stcs(reinterpret_cast<float4*>(dst + j), make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
     } else {
 #pragma unroll
       for (int u = 0; u < 4; ++u)
-        if (j + u < cnt) dst[j + u] = v[j + u];
+        if (j + u < cnt) __stcs(dst + j + u, v[j + u]);
     }
   }
 #pragma unroll
   for (int j = PRE + ((32 - PRE) / 4) * 4; j < 32; ++j)
-    if (j < cnt) dst[j] = v[j];
+    if (j < cnt) __stcs(dst + j, v[j]);
 }
 
 struct TcRing {
@@ -304,6 +307,10 @@ __global__ void __launch_bounds__(tc::NTH, 1)
       // X chunks, pass 1 then pass 2 of every tile.  Lazy X_res copy: block 1 reads X itself
       const CUtensorMap* mp = (lazy && st->t == 1 && part <= 0) ? &xmap0 : &xmap;
       uint64_t pol_keep, pol_drop;
+      // pass-1 chunks below keep_from (the oldest, re-read last in the reversed pass 2) are
+      // not marked evict_last: with 148 x 1 MB tiles in flight the L2 cannot hold them all,
+      // so it keeps the newer ones (TC_KEEP_FRAC, compile time)
+      const int keep_from = (int)(nc * (1.0 - TC_KEEP_FRAC));
       asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol_keep));
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol_drop));
       TcRing xr;
@@ -319,7 +326,7 @@ __global__ void __launch_bounds__(tc::NTH, 1)
         asm volatile(
             "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint "
             "[%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(tc_su32(xs + (size_t)xr.i * XSLOT)),
-            "l"(mp), "r"(c * KC), "r"(y), "r"(fb), "l"(second ? pol_drop : pol_keep)
+            "l"(mp), "r"(c * KC), "r"(y), "r"(fb), "l"((second || c < keep_from) ? pol_drop : pol_keep)
             : "memory");
         xr.next(NSX);
       }
