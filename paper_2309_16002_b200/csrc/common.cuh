@@ -120,6 +120,18 @@ inline int device_sms() {
 
 inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
+// b' > 32 projected in parts (Q_b's rows are orthonormal, so the parts in sequence equal one
+// projection up to rounding): np = ceil(b'/32) balanced parts, part p = rows [r0, r0 + cnt)
+// of Q_b.  Returns false if part p does not exist for this b'.
+__host__ __device__ inline bool part_range(int bpa, int part, int* r0, int* cnt) {
+  if (bpa <= 32) return false;
+  const int np = (bpa + 31) / 32;
+  if (part >= np) return false;
+  *r0 = part * bpa / np;
+  *cnt = (part + 1) * bpa / np - *r0;
+  return true;
+}
+
 // padded block-width bucket used to instantiate the projection kernels
 __host__ __device__ inline int bucket_of(int bp) {
   return bp <= 16 ? 16 : bp <= 32 ? 32 : bp <= 64 ? 64 : 128;

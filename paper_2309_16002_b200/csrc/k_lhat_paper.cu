@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(lp::NTH, 1)
   using namespace lp;
   if (st->stop) return;
   // part < 0: the block's b' columns if b' falls in this bucket.  part >= 0 (b' > 32): the
-  // 32-column part [32 part, min(b', 32 part + 32)) of Q_b; the parts run in order, each
+  // balanced part [r0, r0 + cnt) of Q_b's rows (part_range, <= 32); the parts run in order, each
   // on the residual the previous one left (Q_b's rows are orthonormal, so the sequence
   // equals one projection up to rounding; the paper form downdates per part).
   int bp;
@@ -189,11 +189,12 @@ __global__ void __launch_bounds__(lp::NTH, 1)
     if (bp <= 0 || bucket_of(bp) != BPB) return;
     k0 = st->k;
   } else {
-    const int bpa = st->b_prime;
-    bp = bpa - 32 * part < 32 ? bpa - 32 * part : 32;
-    if (bpa <= 32 || bp <= 0) return;
-    k0 = st->k + 32 * part;
+    int r0;
+    if (!part_range(st->b_prime, part, &r0, &bp)) return;
+    k0 = st->k + r0;
   }
+  // DMMA work only for the 8-column groups that hold a column of Q_b (warp-uniform)
+  const int ntr = (bp + 7) >> 3;
   if (blockIdx.x == 0 && threadIdx.x == 0 && part <= 0) st->ts0 = gtimer();
 
   extern __shared__ __align__(1024) double sm_raw[];
@@ -333,12 +334,14 @@ __global__ void __launch_bounds__(lp::NTH, 1)
           const double2 a1 = LE::ld2(xsl + (int)sizeof(E) * xo[1][h]);
 #pragma unroll
           for (int t = 0; t < NT; ++t) {
-            const int j = 8 * t + g;
-            const double2 b = lp_lds2s(Qs + 8 * (j * KC + lp_qswz(j, 16 * cw + 8 * h + 2 * q)));
-            lp_dmma(acc[0][t], a0.x, b.x);
-            lp_dmma(acc[1][t], a1.x, b.x);
-            lp_dmma(acc[0][t], a0.y, b.y);
-            lp_dmma(acc[1][t], a1.y, b.y);
+            if (t < ntr) {
+              const int j = 8 * t + g;
+              const double2 b = lp_lds2s(Qs + 8 * (j * KC + lp_qswz(j, 16 * cw + 8 * h + 2 * q)));
+              lp_dmma(acc[0][t], a0.x, b.x);
+              lp_dmma(acc[1][t], a1.x, b.x);
+              lp_dmma(acc[0][t], a0.y, b.y);
+              lp_dmma(acc[1][t], a1.y, b.y);
+            }
           }
         }
         release(xr.i, qr.i);
@@ -447,6 +450,7 @@ __global__ void __launch_bounds__(lp::NTH, 1)
           bb[1] = lp_lds2s(qb + 128);
 #pragma unroll
           for (int t = 0; t < NT; ++t) {
+            if (t >= ntr) break;
             if (t + 1 < NT) {
               bn[0] = lp_lds2s(qb + 16 * 4 * KC * (t + 1));
               bn[1] = lp_lds2s(qb + 16 * 4 * KC * (t + 1) + 128);

@@ -21,8 +21,8 @@ __host__ __device__ __forceinline__ int pk_qswz(int j, int col) {
   return col ^ (8 * (j & 1)) ^ (4 * ((j >> 1) & 3));
 }
 
-// part < 0: rows [0, b'), b' <= 64.  part >= 0 (b' > 32 split into 32-row parts, see
-// enqueue_projection): rows [32 part, min(b', 32 part + 32)).
+// part < 0: rows [0, b'), b' <= 64.  part >= 0 (b' > 32 split into balanced parts of <= 32
+// rows, part_range): rows [r0, r0 + cnt).
 template <typename QT>
 __global__ void k_pack_q(const QT* __restrict__ Qt, int64_t d, double* __restrict__ Qp,
                          const DevState* st, int part, int64_t ldq) {
@@ -33,9 +33,7 @@ __global__ void k_pack_q(const QT* __restrict__ Qt, int64_t d, double* __restric
     bp = bpa;
     if (bp <= 0 || bp > pk::PACK_ROWS) return;
   } else {
-    r0 = 32 * part;
-    bp = bpa - r0 < 32 ? bpa - r0 : 32;
-    if (bpa <= 32 || bp <= 0) return;
+    if (!part_range(bpa, part, &r0, &bp)) return;
   }
   const int c = blockIdx.x, j = blockIdx.y, col = threadIdx.x;   // blockDim = KC
   const int64_t gc = (int64_t)c * pk::KC + col;
