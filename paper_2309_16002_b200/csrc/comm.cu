@@ -13,6 +13,7 @@ struct NcclApi {
   decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
   decltype(&ncclCommInitRank) CommInitRank = nullptr;
   decltype(&ncclCommDestroy) CommDestroy = nullptr;
+  decltype(&ncclCommGetAsyncError) GetAsyncError = nullptr;
   decltype(&ncclAllReduce) AllReduce = nullptr;
   decltype(&ncclGroupStart) GroupStart = nullptr;
   decltype(&ncclGroupEnd) GroupEnd = nullptr;
@@ -32,6 +33,7 @@ NcclApi& api() {
   a.AllReduce = (decltype(a.AllReduce))dlsym(h, "ncclAllReduce");
   a.GroupStart = (decltype(a.GroupStart))dlsym(h, "ncclGroupStart");
   a.GroupEnd = (decltype(a.GroupEnd))dlsym(h, "ncclGroupEnd");
+  a.GetAsyncError = (decltype(a.GetAsyncError))dlsym(h, "ncclCommGetAsyncError");
   a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.AllReduce && a.GroupStart &&
          a.GroupEnd;
   return a;
@@ -119,6 +121,15 @@ int comm_allreduce_max_i64(rbrp_comm* c, int64_t* buf, int64_t count, cudaStream
   if (a.AllReduce(buf, buf, count, ncclInt64, ncclMax, (ncclComm_t)c->nccl_comm, s) != ncclSuccess)
     return RBRP_ENCCL;
   return RBRP_OK;
+}
+
+int comm_check(rbrp_comm* c) {
+  NcclApi& a = api();
+  if (!a.ok) return RBRP_ENCCL;
+  if (!a.GetAsyncError) return RBRP_OK;
+  ncclResult_t st = ncclSuccess;
+  if (a.GetAsyncError((ncclComm_t)c->nccl_comm, &st) != ncclSuccess) return RBRP_ENCCL;
+  return (st == ncclSuccess || st == ncclInProgress) ? RBRP_OK : RBRP_ENCCL;
 }
 
 int comm_allreduce_sum_i32(rbrp_comm* c, int32_t* buf, int64_t count, cudaStream_t s) {

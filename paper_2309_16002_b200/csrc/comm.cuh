@@ -20,4 +20,6 @@ int comm_allgather_chunks(rbrp_comm* c, double* ctot, int32_t* cpos, int64_t chu
 int comm_allreduce_f64(rbrp_comm* c, double* buf, int64_t count, cudaStream_t s);
 int comm_allreduce_max_i64(rbrp_comm* c, int64_t* buf, int64_t count, cudaStream_t s);
 int comm_allreduce_sum_i32(rbrp_comm* c, int32_t* buf, int64_t count, cudaStream_t s);
+// ncclCommGetAsyncError: RBRP_ENCCL if a collective of this communicator failed
+int comm_check(rbrp_comm* c);
 }  // namespace rbrp

@@ -319,13 +319,13 @@ void make_ctx(Ctx<T>& c, const rbrp_problem* p, void* Xv, char* ws, const Layout
   // (b' > 32 runs as 32-column parts on the same kernel, enqueue_projection)
   const int lp_need = c.bucketB > 32 && !env_on("RBRP_NO_PARTS") ? 32 : c.bucketB;
   c.lazy = c.tiled && !inplace && c.Xres != c.X && c.lp_max >= lp_need && c.lp_max > 0 &&
-           lp_max_bucket<T>(c.X, p->ld, c.d) >= lp_need && !comm && !env_on("RBRP_EAGER_COPY");
+           lp_max_bucket<T>(c.X, p->ld, c.d) >= lp_need && !env_on("RBRP_EAGER_COPY");
   // fp32 residual form: the tcgen05 3xTF32 kernel (RBRP_FP32_DMMA=1 keeps the fp64-DMMA one)
   if (sizeof(T) == 4 && !c.paper && c.Qtc && !force_simt() && !env_on("RBRP_FP32_DMMA") && !env_on("RBRP_FP32_SIMT") &&
       proj_tc32_supported(c.Xres, c.ldr, c.d)) {
     c.tc32 = true;
     c.tiled = false;
-    c.lazy = !inplace && c.Xres != c.X && proj_tc32_supported(c.X, p->ld, c.d) && !comm && !env_on("RBRP_EAGER_COPY");
+    c.lazy = !inplace && c.Xres != c.X && proj_tc32_supported(c.X, p->ld, c.d) && !env_on("RBRP_EAGER_COPY");
   }
 }
 
@@ -1027,7 +1027,7 @@ int run_dist(int nsh, const rbrp_problem* ps, void* const* Xs, char* const* wss,
   for (int h = 0; h < nsh; ++h) {
     const bool inplace = (ps[h].flags & RBRP_INPLACE) != 0;
     LKD(launch_init_norms<T>(C[h].X, ps[h].ld, C[h].Xres, C[h].n, C[h].d, C[h].dvec, C[h].st,
-                               !inplace && !C[h].paper, s));
+                               !inplace && !C[h].paper && !C[h].lazy, s));
     LKD(launch_chunk_scan(C[h].dvec, C[h].n, C[h].chunk0, C[h].cpre, C[h].ctot, C[h].cpos, s));
   }
   RCD(coll_chunks());
@@ -1094,12 +1094,15 @@ int run_dist(int nsh, const rbrp_problem* ps, void* const* Xs, char* const* wss,
 
   int blk = 0;
   while (!hst->stop) {
-    // a3: V rows from their owners (C3), then the filter on every shard
-    if (comm) CK(cudaMemsetAsync(C[0].Vg, 0, (size_t)RBRP_MAX_B * C[0].d * 8, s));
-    for (int h = 0; h < nsh; ++h)
-      LKD(launch_gather_rows<T>(C[h].Xres, C[h].ldr, C[h].St, C[h].n, ps[h].row_offset, C[h].st, C[h].d,
-                                C[h].Vg, s));
-    if (comm) RCD(comm_allreduce_f64(comm, C[0].Vg, (int64_t)RBRP_MAX_B * C[0].d, s));
+    // a3: V rows from their owners (C3: b x d values, b = the block size), then the filter
+    // on every shard.  Lazy X_res: block 1's rows come from X itself.
+    if (comm) CK(cudaMemsetAsync(C[0].Vg, 0, (size_t)p->b * C[0].d * 8, s));
+    for (int h = 0; h < nsh; ++h) {
+      const bool from_x = C[h].lazy && blk == 0;
+      LKD(launch_gather_rows<T>(from_x ? C[h].X : C[h].Xres, from_x ? ps[h].ld : C[h].ldr, C[h].St, C[h].n,
+                                ps[h].row_offset, C[h].st, C[h].d, C[h].Vg, s));
+    }
+    if (comm) RCD(comm_allreduce_f64(comm, C[0].Vg, (int64_t)p->b * C[0].d, s));
     // paper form, l.6 (CGS2): once per distinct V buffer (in-process shards share one)
     if (C[0].paper) {
       for (int h = 0; h < nsh; ++h) {
@@ -1159,6 +1162,7 @@ int run_dist(int nsh, const rbrp_problem* ps, void* const* Xs, char* const* wss,
     RCD(sample(rl));
     CK(cudaMemcpyAsync(hst, C[0].st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    if (comm) RCD(comm_check(comm));   // a failed collective surfaces as RBRP_ENCCL
   }
   const int64_t k = hst->k;
   const int nblocks = std::min(hst->t, mb);
