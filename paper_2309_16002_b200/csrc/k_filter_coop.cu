@@ -14,10 +14,7 @@
 //   E  G2 = sum_c Gpart[c]
 //   F  every CTA: Cholesky G2 = R2^T R2 (CholQR2) with T2 = R2^{-1}; CTA 0: R_total = R2 R11
 //   G  Q_b(:, cols) = Q1 T2 -> Qt (rows >= b' zero up to bp_pad)
-// b_t <= 64: every CTA sums the partial Grams itself (B, E: same fixed order, bit-identical
-// in every CTA), so only the two barriers after A and D remain; the partials of D go to a
-// second buffer (Tg) because slow CTAs may still be reading those of A.  Larger blocks:
-// four grid-wide barriers.
+// Four grid-wide barriers.
 #include <cooperative_groups.h>
 #include <float.h>
 
@@ -446,27 +443,6 @@ __device__ void slice_gram(const double* S, int nb, double* out) {
   }
 }
 
-// every CTA: G = sum_q Gpart[q] in the same fixed order as reduce_slices (so each CTA holds
-// the bit-identical G without a grid barrier after the reduction); nb <= 64
-__device__ void reduce_slices_local(const double* Gpart, int nsplit, int nb, double* G) {
-  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
-    const int i = e / nb, j = e % nb;
-    const double* src = Gpart + i * kMaxB + j;
-    double s = 0.0;
-    int q = 0;
-    for (; q + 8 <= nsplit; q += 8) {
-      double x[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) x[u] = src[(int64_t)(q + u) * kMaxB * kMaxB];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) s += x[u];
-    }
-    for (; q < nsplit; ++q) s += src[(int64_t)q * kMaxB * kMaxB];
-    G[i * kMaxB + j] = s;
-  }
-  __syncthreads();
-}
-
 __device__ void reduce_slices(const double* Gpart, int nsplit, int nb, double* G) {
   const int64_t per = (int64_t)nb * nb;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < per;
@@ -568,15 +544,9 @@ __global__ void __launch_bounds__(kFiltThreads, 1) k_filter_coop(FilterArgs F) {
   stamp(F.dbg, 1);
   grid.sync();
   stamp(F.dbg, 2);
-  // B: G = sum of the partial Grams -- per CTA (small blocks) or grid-wide
-  double* Gfac = F.G;   // the G the factorizations read (stride kMaxB)
-  if (small) {
-    Gfac = F.Ag + (int64_t)blockIdx.x * kMaxB * kMaxB;
-    reduce_slices_local(F.Gpart, nsplit, nb, Gfac);
-  } else {
-    reduce_slices(F.Gpart, nsplit, nb, F.G);
-    grid.sync();
-  }
+  // B
+  reduce_slices(F.Gpart, nsplit, nb, F.G);
+  grid.sync();
   stamp(F.dbg, 3);
   // C: pivoted Cholesky + filter + T11 = R11^{-1} (redundant in every CTA).  b_t <= 64:
   // register-resident fast path; larger blocks: shared/L2 path + column-parallel inverse.
@@ -588,9 +558,9 @@ __global__ void __launch_bounds__(kFiltThreads, 1) k_filter_coop(FilterArgs F) {
     const double tb = st->tau_b < 0.0 ? 1.0 / nb : st->tau_b;
     int kept;
     if (nb <= 32) {
-      kept = cta_chol_inv<4>(Gfac, nb, 1, F.forced, tb, Rs, ldr, Ts, ldt, perm, s_mass, s_dg, s_ch, &s_rd);
+      kept = cta_chol_inv<4>(F.G, nb, 1, F.forced, tb, Rs, ldr, Ts, ldt, perm, s_mass, s_dg, s_ch, &s_rd);
     } else if (small) {
-      kept = cta_chol_inv<16>(Gfac, nb, 1, F.forced, tb, Rs, ldr, Ts, ldt, perm, s_mass, s_dg, s_ch, &s_rd);
+      kept = cta_chol_inv<16>(F.G, nb, 1, F.forced, tb, Rs, ldr, Ts, ldt, perm, s_mass, s_dg, s_ch, &s_rd);
     } else {
       kept = cta_pivchol_reg(F.G, nb, 1, F.forced, tb, Rs, ldr, perm, s_mass, &s_rd);
       __syncthreads();
@@ -629,19 +599,13 @@ __global__ void __launch_bounds__(kFiltThreads, 1) k_filter_coop(FilterArgs F) {
   // D: Q1(:, cols) = V(:, pi(1:b')) T11, partial Gram of Q1
   apply_T(Ts, ldt, bp, Vs, perm, Q1s);
   __syncthreads();
-  // small blocks: D's partials in a second buffer (other CTAs may still be reading A's)
-  double* const Gpart2 = small ? F.Tg : F.Gpart;
-  slice_gram(Q1s, bp, Gpart2 + (int64_t)blockIdx.x * kMaxB * kMaxB);
+  slice_gram(Q1s, bp, Gp);
   stamp(F.dbg, 5);
   grid.sync();
   stamp(F.dbg, 6);
   // E
-  if (small) {
-    reduce_slices_local(Gpart2, nsplit, bp, Gfac);
-  } else {
-    reduce_slices(F.Gpart, nsplit, bp, F.G);
-    grid.sync();
-  }
+  reduce_slices(F.Gpart, nsplit, bp, F.G);
+  grid.sync();
   stamp(F.dbg, 7);
   // F: CholQR2 pass (R2 into Rs, T2 = R2^{-1} into Ts).  G2 = I + E: if max|E| is small
   // (the usual case) a parallel perturbation expansion, else the exact Cholesky.
@@ -650,7 +614,7 @@ __global__ void __launch_bounds__(kFiltThreads, 1) k_filter_coop(FilterArgs F) {
     double em = 0.0;
     for (int e = tid; e < bp * bp; e += kFiltThreads) {
       const int i = e / bp, j = e - (e / bp) * bp;
-      const double x = Gfac[i * kMaxB + j] - (i == j ? 1.0 : 0.0);
+      const double x = F.G[i * kMaxB + j] - (i == j ? 1.0 : 0.0);
       Gs[i * ldg + j] = x;
       em = fmax(em, fabs(x));
     }
@@ -679,9 +643,9 @@ __global__ void __launch_bounds__(kFiltThreads, 1) k_filter_coop(FilterArgs F) {
   } else {
     int rd2, kept;
     if (bp <= 32) {
-      kept = cta_chol_inv<4>(Gfac, bp, 2, nullptr, 0.0, Rs, ldr, Ts, ldt, perm2, nullptr, s_dg, s_ch, &rd2);
+      kept = cta_chol_inv<4>(F.G, bp, 2, nullptr, 0.0, Rs, ldr, Ts, ldt, perm2, nullptr, s_dg, s_ch, &rd2);
     } else if (small) {
-      kept = cta_chol_inv<16>(Gfac, bp, 2, nullptr, 0.0, Rs, ldr, Ts, ldt, perm2, nullptr, s_dg, s_ch, &rd2);
+      kept = cta_chol_inv<16>(F.G, bp, 2, nullptr, 0.0, Rs, ldr, Ts, ldt, perm2, nullptr, s_dg, s_ch, &rd2);
     } else {
       for (int e = tid; e < bp * bp; e += kFiltThreads) Gs[(e / bp) * ldg + e % bp] = F.G[(e / bp) * kMaxB + e % bp];
       __syncthreads();
