@@ -684,7 +684,9 @@ cudaError_t launch_proj_tc32(float* X, int64_t ldx, const float* Qimg, float* L,
   }
   if (e != cudaSuccess) return e;
   const int nc = (int)((d + tc::KC - 1) / tc::KC);
-  k_proj_tc32<<<device_sms(), tc::NTH, tc::SMEM, s>>>(map, map0, X0 ? 1 : 0, Qimg, L, ldl, n, (int)d, nc, st, X, ldx,
+  int grid = device_sms();
+  if (const char* g = getenv("RBRP_TC_GRID")) grid = atoi(g);   // experiments only (L2 working set)
+  k_proj_tc32<<<grid, tc::NTH, tc::SMEM, s>>>(map, map0, X0 ? 1 : 0, Qimg, L, ldl, n, (int)d, nc, st, X, ldx,
                                                        dvec, part, tr);
   return cudaGetLastError();
 }
