@@ -152,6 +152,8 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample(SampleArgs A) {
     s_bt = bt;
     s_c = 0;
     if (A.cond) cudaGraphSetConditional((cudaGraphConditionalHandle)A.cond, stop ? 0u : 1u);
+    // row-sharded graph loop: the draw rounds run while this block still needs rows
+    if (A.cond2) cudaGraphSetConditional((cudaGraphConditionalHandle)A.cond2, stop ? 0u : 1u);
   }
   __syncthreads();
   if (s_stop) return;
@@ -347,7 +349,10 @@ __global__ void __launch_bounds__(kSampleRound) k_draw_resolve(SampleArgs A) {
 // R6) — the same rule as k_sample's single-GPU loop, so S_t is identical for any sharding.
 __global__ void __launch_bounds__(kSampleRound) k_draw_accept(SampleArgs A) {
   DevState* st = A.st;
-  if (st->stop || st->sample_done) return;
+  if (st->stop || st->sample_done) {
+    if (A.cond2 && threadIdx.x == 0) cudaGraphSetConditional((cudaGraphConditionalHandle)A.cond2, 0u);
+    return;
+  }
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   __shared__ int64_t chosen[kMaxB];
   __shared__ int64_t cand[kSampleRound];
@@ -366,6 +371,7 @@ __global__ void __launch_bounds__(kSampleRound) k_draw_accept(SampleArgs A) {
       st->sample_c = n;
       st->sample_done = 1;
       st->flags |= RBRP_F_SUPPORT_EXHAUSTED;
+      if (A.cond2) cudaGraphSetConditional((cudaGraphConditionalHandle)A.cond2, 0u);
     }
     return;
   }
@@ -385,10 +391,12 @@ __global__ void __launch_bounds__(kSampleRound) k_draw_accept(SampleArgs A) {
     const int nc = min(bt, c + tot);
     st->sample_c = nc;
     st->jb += kSampleRound;
-    if (nc >= bt || st->jb >= kJMax) {
+    const bool done = nc >= bt || st->jb >= kJMax;
+    if (done) {
       st->sample_done = 1;
       st->b_t = nc;
     }
+    if (A.cond2) cudaGraphSetConditional((cudaGraphConditionalHandle)A.cond2, done ? 0u : 1u);
   }
 }
 

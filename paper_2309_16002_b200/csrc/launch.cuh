@@ -29,6 +29,7 @@ struct SampleArgs {
   const int32_t* piv;     // pivots of the block that just finished (logged)
   BlockLog log;
   unsigned long long cond;   // cudaGraphConditionalHandle of the WHILE node (0: none)
+  unsigned long long cond2;  // row-sharded graph loop: handle of the draw-round WHILE node (0: none)
   int dist;               // 1: row-sharded run; this kernel only does the stop test / b_t
   int64_t* cand;          // distributed rounds: candidate rows of kSampleRound draws (-1 = not mine)
   int greedy;             // RBGP (Remark 4.2): S_t = the top b_t rows of d (k_topb), no draw
@@ -52,7 +53,7 @@ cudaError_t launch_topb(const double* dvec, int64_t n, int64_t row_offset, int B
 template <typename T>
 cudaError_t launch_gather_rows(const T* X, int64_t ldx, const int64_t* rows, int64_t n_local,
                                int64_t row_offset, const DevState* st, int64_t d, double* Vg,
-                               cudaStream_t s);
+                               cudaStream_t s, const T* X0 = nullptr, int64_t ldx0 = 0);   // X0: lazy block 1
 // k_filter_coop.cu — the whole a3 step in one cooperative kernel
 struct FilterArgs {
   DevState* st;

@@ -516,6 +516,7 @@ struct GraphKey {
   rbrp_problem p;
   const void* X;
   const void* ws;
+  const void* aux;   // row-sharded graphs: the communicator
   int device, use_mma;
   bool operator==(const GraphKey& o) const { return memcmp(this, &o, sizeof(GraphKey)) == 0; }
 };
@@ -556,7 +557,7 @@ void evict_lru(std::list<std::shared_ptr<E>>& cache, size_t cap) {
   }
 }
 
-GraphKey make_key(const rbrp_problem* p, const void* X, const void* ws, int variant) {
+GraphKey make_key(const rbrp_problem* p, const void* X, const void* ws, int variant, const void* aux = nullptr) {
   GraphKey k;
   memset(&k, 0, sizeof(k));
   k.p = *p;
@@ -567,6 +568,7 @@ GraphKey make_key(const rbrp_problem* p, const void* X, const void* ws, int vari
   k.ws = ws;
   cudaGetDevice(&k.device);
   k.use_mma = variant;
+  k.aux = aux;
   return k;
 }
 
@@ -627,6 +629,108 @@ GraphPtr get_graph(Ctx<T>& c, SampleArgs sa, const GraphKey& key) {
 
 // Remark 5.2 trigger (reading R17): min |diag L_1| < 1e-12 max |diag L_1|
 bool clip_needed(double dmin, double dmax) { return dmax > 0.0 && dmin < 1e-12 * dmax; }
+
+// the nodes of g with no outgoing edge
+std::vector<cudaGraphNode_t> sink_nodes(cudaGraph_t g) {
+  size_t nn = 0, ne = 0;
+  std::vector<cudaGraphNode_t> sinks;
+  if (cudaGraphGetNodes(g, nullptr, &nn) != cudaSuccess) return sinks;
+  std::vector<cudaGraphNode_t> nodes(nn);
+  if (nn && cudaGraphGetNodes(g, nodes.data(), &nn) != cudaSuccess) return sinks;
+  if (cudaGraphGetEdges(g, nullptr, nullptr, &ne) != cudaSuccess) return sinks;
+  std::vector<cudaGraphNode_t> from(ne), to(ne);
+  if (ne && cudaGraphGetEdges(g, from.data(), to.data(), &ne) != cudaSuccess) return sinks;
+  for (auto n : nodes)
+    if (std::find(from.begin(), from.end(), n) == from.end()) sinks.push_back(n);
+  return sinks;
+}
+
+// Row-sharded block loop as one graph: outer WHILE (handle set by k_sample) whose body is
+// [block kernels + collectives, k_sample per shard] followed by an inner WHILE node over the
+// draw rounds (handle set by k_sample and k_draw_accept).  NCCL collectives are captured
+// into the bodies.  nullptr if graphs are not usable here (the caller runs the eager loop).
+template <typename T, class FB, class FS, class FR>
+GraphPtr get_graph_dist(Ctx<T>* C, SampleArgs* SA, int nsh, rbrp_comm* comm, FB& blockf, FS& samplef, FR& roundf,
+                        const GraphKey& key) {
+  (void)C;
+  (void)comm;
+  std::lock_guard<std::mutex> lk(g_graph_mu);
+  for (auto& e : g_graphs)
+    if (e->key == key) {
+      e->stamp = ++g_graph_clock;
+      return e;
+    }
+  cudaStream_t cs = capture_stream();
+  if (!cs) return nullptr;
+  GraphPtr ep = std::make_shared<GraphEntry>();
+  GraphEntry& e = *ep;
+  e.key = key;
+  if (cudaGraphCreate(&e.g, 0) != cudaSuccess) return nullptr;
+  cudaGraphConditionalHandle h = 0, h2 = 0;
+  cudaGraph_t body = nullptr, inner = nullptr;
+  bool ok = cudaGraphConditionalHandleCreate(&h, e.g, 1, cudaGraphCondAssignDefault) == cudaSuccess;
+  if (ok) {
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = h;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    ok = cudaGraphAddNode(&node, e.g, nullptr, 0, &np) == cudaSuccess;
+    if (ok) body = np.conditional.phGraph_out[0];
+    ok = ok && body;
+  }
+  if (ok) ok = cudaGraphConditionalHandleCreate(&h2, body, 0, 0) == cudaSuccess;
+  std::vector<SampleArgs> saved(SA, SA + nsh);
+  for (int i = 0; i < nsh; ++i) {
+    SA[i].cond = (unsigned long long)h;
+    SA[i].cond2 = (unsigned long long)h2;
+    SA[i].first = 0;
+  }
+  int nl = 0;
+  if (ok) {   // outer body: the block, then the stop test / b_t of the next one
+    ok = cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed) == cudaSuccess;
+    if (ok) {
+      int rc = blockf(cs, &nl);
+      if (!rc) rc = samplef(cs, -1, &nl);
+      cudaGraph_t cap = nullptr;
+      const bool endok = cudaStreamEndCapture(cs, &cap) == cudaSuccess;
+      ok = rc == RBRP_OK && endok;
+    }
+  }
+  if (ok) {   // ... then the draw rounds
+    std::vector<cudaGraphNode_t> sinks = sink_nodes(body);
+    cudaGraphNodeParams np2 = {};
+    np2.type = cudaGraphNodeTypeConditional;
+    np2.conditional.handle = h2;
+    np2.conditional.type = cudaGraphCondTypeWhile;
+    np2.conditional.size = 1;
+    cudaGraphNode_t n2;
+    ok = !sinks.empty() && cudaGraphAddNode(&n2, body, sinks.data(), sinks.size(), &np2) == cudaSuccess;
+    if (ok) inner = np2.conditional.phGraph_out[0];
+    ok = ok && inner;
+  }
+  if (ok) {
+    ok = cudaStreamBeginCaptureToGraph(cs, inner, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed) == cudaSuccess;
+    if (ok) {
+      const int rc = roundf(cs, &nl);
+      cudaGraph_t cap = nullptr;
+      const bool endok = cudaStreamEndCapture(cs, &cap) == cudaSuccess;
+      ok = rc == RBRP_OK && endok;
+    }
+  }
+  for (int i = 0; i < nsh; ++i) SA[i] = saved[i];
+  if (ok) ok = cudaGraphInstantiate(&e.exec, e.g, 0) == cudaSuccess;
+  if (!ok) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  e.launches_per_block = nl;   // one draw round per block counted
+  evict_lru(g_graphs, 8);
+  e.stamp = ++g_graph_clock;
+  g_graphs.push_back(ep);
+  return ep;
+}
 
 // a6: W(S,:) = I, W(rest,:) = L_2 L_1^{-1} (Alg. 3; triangular inverse),
 // or L_2 pinv_clip(L_1) when `clip` (Remark 5.2)
@@ -1018,11 +1122,106 @@ int run_dist(int nsh, const rbrp_problem* ps, void* const* Xs, char* const* wss,
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
   CK(cudaEventRecord(e0, s));
-  auto coll_chunks = [&]() -> int {
+  auto coll_chunks = [&](cudaStream_t ss) -> int {
     if (!comm) return RBRP_OK;
     return comm_allgather_chunks(comm, C[0].ctot, C[0].cpos, C[0].chunk0,
-                                 (C[0].n + RBRP_CHUNK - 1) / RBRP_CHUNK, Lys[0].nchunks, s);
+                                 (C[0].n + RBRP_CHUNK - 1) / RBRP_CHUNK, Lys[0].nchunks, ss);
   };
+#define LKS(x)                                 \
+  do {                                         \
+    ++*nlp;                                    \
+    if ((x) != cudaSuccess) return RBRP_ECUDA; \
+  } while (0)
+  // the kernels and collectives of one block on `ss`: a3 (V rows from their owners, C3;
+  // the filter on every shard), a4 + fix-up + chunk scan per shard, C1.  Every kernel reads
+  // its sizes from DevState and is a no-op once stop is set (graph-capturable).
+  auto enqueue_dblock = [&](cudaStream_t ss, int* nlp) -> int {
+    if (comm && cudaMemsetAsync(C[0].Vg, 0, (size_t)p->b * C[0].d * 8, ss) != cudaSuccess) return RBRP_ECUDA;
+    for (int h = 0; h < nsh; ++h)   // lazy X_res: block 1's rows come from X itself (device-side test)
+      LKS(launch_gather_rows<T>(C[h].Xres, C[h].ldr, C[h].St, C[h].n, ps[h].row_offset, C[h].st, C[h].d, C[h].Vg,
+                                ss, C[h].lazy ? (const T*)C[h].X : nullptr, ps[h].ld));
+    if (comm) {
+      const int rc = comm_allreduce_f64(comm, C[0].Vg, (int64_t)p->b * C[0].d, ss);
+      if (rc) return rc;
+    }
+    // paper form, l.6 (CGS2): once per distinct V buffer (in-process shards share one)
+    if (C[0].paper) {
+      for (int h = 0; h < nsh; ++h) {
+        bool seen = false;
+        for (int h2 = 0; h2 < h; ++h2) seen = seen || (C[h2].Vg == C[h].Vg);
+        if (!seen) LKS(launch_cgs2_rows<T>(C[h].Vg, C[h].d, C[h].Qall, C[h].k_cap, C[h].Ccgs, C[h].st, ss));
+      }
+    }
+    for (int h = 0; h < nsh; ++h) {
+      Ctx<T>& c = C[h];
+      FilterArgs fa;
+      fa.st = c.st;
+      fa.X = c.Xres;
+      fa.ldx = c.ldr;
+      fa.X0 = nullptr;
+      fa.ldx0 = 0;
+      fa.Vg = c.Vg;
+      fa.S_t = c.St;
+      fa.row_offset = ps[h].row_offset;
+      fa.d = c.d;
+      fa.Gpart = c.Gpart;
+      fa.G = c.G;
+      fa.forced = (c.use_forced && c.force_blk) ? c.forced : nullptr;
+      if (fa.forced && h == 0) ++c.nforced;
+      fa.piv = c.piv;
+      fa.mass = c.mass;
+      fa.R11 = c.R11;
+      fa.Tg = c.Tg;
+      fa.Ag = c.Ag;
+      fa.Rtot = c.Rtot;
+      fa.S = c.S;
+      fa.Qt = c.Qt;
+      fa.bp_pad = c.bucketB;
+      fa.dbg = nullptr;
+      LKS(launch_filter_coop<T>(fa, ss));
+    }
+    // a4: projection, rank-local
+    for (int h = 0; h < nsh; ++h) {
+      Ctx<T>& c = C[h];
+      {
+        const int rc = enqueue_projection(c, ss, nlp);
+        if (rc) return rc;
+      }
+      LKS(launch_fixup<T>(c.paper ? nullptr : c.Xres, c.ldr, c.dvec, c.Lm, c.k_cap, c.Rtot, c.S, c.n,
+                          ps[h].row_offset, c.d, c.st, ss));
+      if (c.paper) {
+        LKS(launch_zero_prev<T>(c.Lm, c.k_cap, c.S, c.n, ps[h].row_offset, c.st, ss));
+        LKS(launch_append_q<T>(c.Qt, c.d, c.Qall, c.st, ss));
+      }
+      LKS(launch_chunk_scan(c.dvec, c.n, c.chunk0, c.cpre, c.ctot, c.cpos, ss));
+    }
+    return coll_chunks(ss);
+  };
+  // stop test + b_t of the next block (l.3-4) on every shard
+  auto enqueue_dsample = [&](cudaStream_t ss, int rl, int* nlp) -> int {
+    for (int h = 0; h < nsh; ++h) {
+      SA[h].replay_len = rl;
+      if (emul) SA[h].S_rep = C[0].Srep;
+      LKS(launch_sample(SA[h], ss));
+      SA[h].first = 0;
+    }
+    return RBRP_OK;
+  };
+  // one draw round (l.5): kSampleRound draws resolved by their owners (C2: max), accepted
+  // in draw order on every shard
+  auto enqueue_dround = [&](cudaStream_t ss, int* nlp) -> int {
+    const int ncand = emul ? 1 : nsh;
+    for (int h = 0; h < ncand; ++h)
+      if (cudaMemsetAsync(C[h].cand, 0xff, kSampleRound * 8, ss) != cudaSuccess) return RBRP_ECUDA;
+    for (int h = 0; h < nsh; ++h) LKS(launch_draw_resolve(SA[h], ss));
+    if (comm) {
+      const int rc = comm_allreduce_max_i64(comm, C[0].cand, kSampleRound, ss);
+      if (rc) return rc;
+    }
+    for (int h = 0; h < nsh; ++h) LKS(launch_draw_accept(SA[h], ss));
+    return RBRP_OK;
+  };
+#undef LKS
   // a0
   for (int h = 0; h < nsh; ++h) {
     const bool inplace = (ps[h].flags & RBRP_INPLACE) != 0;
@@ -1030,7 +1229,7 @@ int run_dist(int nsh, const rbrp_problem* ps, void* const* Xs, char* const* wss,
                                !inplace && !C[h].paper && !C[h].lazy, s));
     LKD(launch_chunk_scan(C[h].dvec, C[h].n, C[h].chunk0, C[h].cpre, C[h].ctot, C[h].cpos, s));
   }
-  RCD(coll_chunks());
+  RCD(coll_chunks(s));
   // replay ids: one staging buffer (shard 0's Srep; shared in emulation, per rank with NCCL)
   int64_t replay_pos = 0;
   auto stage_replay = [&](int blk) -> int {
@@ -1060,21 +1259,13 @@ int run_dist(int nsh, const rbrp_problem* ps, void* const* Xs, char* const* wss,
     replay_pos += len;
     return len;
   };
-  // stop test + next block (l.3-5); draws resolved by their owners, combined, accepted
+  // eager sampling: stop test, then draw rounds until the block is complete (one host read
+  // of the loop state per round)
   auto sample = [&](int rl) -> int {
-    for (int h = 0; h < nsh; ++h) {
-      SA[h].replay_len = rl;
-      if (emul) SA[h].S_rep = C[0].Srep;
-      LKD(launch_sample(SA[h], s));
-      SA[h].first = 0;
-    }
+    RCD(enqueue_dsample(s, rl, &nl));
     if (rl >= 0 || rl == -2) return RBRP_OK;
     for (int round = 0;; ++round) {
-      const int ncand = emul ? 1 : nsh;
-      for (int h = 0; h < ncand; ++h) CK(cudaMemsetAsync(C[h].cand, 0xff, kSampleRound * 8, s));
-      for (int h = 0; h < nsh; ++h) LKD(launch_draw_resolve(SA[h], s));
-      if (comm) RCD(comm_allreduce_max_i64(comm, C[0].cand, kSampleRound, s));
-      for (int h = 0; h < nsh; ++h) LKD(launch_draw_accept(SA[h], s));
+      RCD(enqueue_dround(s, &nl));
       CK(cudaMemcpyAsync(hst, C[0].st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
       if (hst->stop || hst->sample_done) break;
@@ -1092,70 +1283,27 @@ int run_dist(int nsh, const rbrp_problem* ps, void* const* Xs, char* const* wss,
     if (hst[h].nonfinite) return RBRP_ENONFINITE;
   if (!(hst->D0 > 0.0)) return RBRP_EDEGENERATE;
 
+  // Graph mode (no replay): the whole block loop -- block kernels, collectives, the stop
+  // test and the draw rounds -- is one CUDA-graph launch: an outer conditional WHILE node
+  // (condition set by k_sample) whose body ends in an inner WHILE node over the draw rounds
+  // (condition set by k_sample and k_draw_accept).  No host round trip per block.
+  GraphPtr dg;
+  if (!hst->stop && !p->replay_nblocks && !env_on("RBRP_NO_GRAPH"))
+    dg = get_graph_dist<T>(C.data(), SA.data(), nsh, comm, enqueue_dblock, enqueue_dsample, enqueue_dround,
+                           make_key(p, Xs[0], wss[0], 64 | (nsh << 8) | (C[0].lazy ? 8 : 0) | (C[0].paper ? 16 : 0) |
+                                                           (C[0].tc32 ? 2 : 0) | (C[0].use_mma ? 1 : 0), comm));
+  if (dg) {
+    CK(cudaGraphLaunch(dg->exec, s));
+    CK(cudaMemcpyAsync(hst, C[0].st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (comm) RCD(comm_check(comm));
+    nl += dg->launches_per_block * hst->t;
+    nproj += hst->t;
+  }
   int blk = 0;
   while (!hst->stop) {
-    // a3: V rows from their owners (C3: b x d values, b = the block size), then the filter
-    // on every shard.  Lazy X_res: block 1's rows come from X itself.
-    if (comm) CK(cudaMemsetAsync(C[0].Vg, 0, (size_t)p->b * C[0].d * 8, s));
-    for (int h = 0; h < nsh; ++h) {
-      const bool from_x = C[h].lazy && blk == 0;
-      LKD(launch_gather_rows<T>(from_x ? C[h].X : C[h].Xres, from_x ? ps[h].ld : C[h].ldr, C[h].St, C[h].n,
-                                ps[h].row_offset, C[h].st, C[h].d, C[h].Vg, s));
-    }
-    if (comm) RCD(comm_allreduce_f64(comm, C[0].Vg, (int64_t)p->b * C[0].d, s));
-    // paper form, l.6 (CGS2): once per distinct V buffer (in-process shards share one)
-    if (C[0].paper) {
-      for (int h = 0; h < nsh; ++h) {
-        bool seen = false;
-        for (int h2 = 0; h2 < h; ++h2) seen = seen || (C[h2].Vg == C[h].Vg);
-        if (!seen) LKD(launch_cgs2_rows<T>(C[h].Vg, C[h].d, C[h].Qall, C[h].k_cap, C[h].Ccgs, C[h].st, s));
-      }
-    }
-    for (int h = 0; h < nsh; ++h) {
-      Ctx<T>& c = C[h];
-      FilterArgs fa;
-      fa.st = c.st;
-      fa.X = c.Xres;
-      fa.ldx = c.ldr;
-      fa.X0 = nullptr;
-      fa.ldx0 = 0;
-      fa.Vg = c.Vg;
-      fa.S_t = c.St;
-      fa.row_offset = ps[h].row_offset;
-      fa.d = c.d;
-      fa.Gpart = c.Gpart;
-      fa.G = c.G;
-      fa.forced = (c.use_forced && c.force_blk) ? c.forced : nullptr;
-      if (fa.forced && h == 0) ++c.nforced;
-      fa.piv = c.piv;
-      fa.mass = c.mass;
-      fa.R11 = c.R11;
-      fa.Tg = c.Tg;
-      fa.Ag = c.Ag;
-      fa.Rtot = c.Rtot;
-      fa.S = c.S;
-      fa.Qt = c.Qt;
-      fa.bp_pad = c.bucketB;
-      fa.dbg = nullptr;
-      LKD(launch_filter_coop<T>(fa, s));
-    }
-    // a4: projection, rank-local
-    for (int h = 0; h < nsh; ++h) {
-      Ctx<T>& c = C[h];
-      {
-        int rc = enqueue_projection(c, s, &nl);
-        if (rc) return rc;
-      }
-      LKD(launch_fixup<T>(c.paper ? nullptr : c.Xres, c.ldr, c.dvec, c.Lm, c.k_cap, c.Rtot, c.S, c.n,
-                          ps[h].row_offset, c.d, c.st, s));
-      if (c.paper) {
-        LKD(launch_zero_prev<T>(c.Lm, c.k_cap, c.S, c.n, ps[h].row_offset, c.st, s));
-        LKD(launch_append_q<T>(c.Qt, c.d, c.Qall, c.st, s));
-      }
-      LKD(launch_chunk_scan(c.dvec, c.n, c.chunk0, c.cpre, c.ctot, c.cpos, s));
-    }
+    RCD(enqueue_dblock(s, &nl));
     ++nproj;
-    RCD(coll_chunks());
     ++blk;
     rl = stage_replay(blk);
     if (rl < -100) return rl + 1000;
@@ -1262,7 +1410,7 @@ int run_dist(int nsh, const rbrp_problem* ps, void* const* Xs, char* const* wss,
       }
     }
     rep->proj_ms = (float)proj;
-    rep->graph = 0;
+    rep->graph = dg ? 1 : 0;
   }
 #undef LKD
 #undef RCD

@@ -34,10 +34,15 @@ SCRIPT = textwrap.dedent(r"""
         X = make(cfg, device="cuda")
         a = rb.id(X, tol=1e-12, b=16, seed=3, form=form)
         c = rdist.id_distributed(X, cfg.n, 0, comm, tol=1e-12, b=16, seed=3, form=form)
+        assert c.graph, form        # the loop with its NCCL collectives captured as one graph
         assert a.S.tolist() == c.S.tolist(), form
         assert a.b_prime == c.b_prime and a.rho == c.rho, form
         assert torch.allclose(a.W, c.W, rtol=0, atol=1e-12), form
         assert c.k == 40
+        os.environ["RBRP_NO_GRAPH"] = "1"   # the eager, host-driven loop: same answer
+        e = rdist.id_distributed(X, cfg.n, 0, comm, tol=1e-12, b=16, seed=3, form=form)
+        del os.environ["RBRP_NO_GRAPH"]
+        assert not e.graph and e.S.tolist() == c.S.tolist() and e.rho == c.rho, form
     # replay through the communicator against the oracle
     cfg = small_config("c3", n=12000, d=64, n_heavy_dirs=20, n_heavy_rows=6000, b=16)
     Xnp = make(cfg).numpy()

@@ -297,10 +297,34 @@ def test_shard_invariance(split):
         rows.append(X[off:off + sz])
         off += sz
     res, Ws = rb.rbrp.id_sharded(rows, tol=1e-12, b=16, seed=2)
+    assert res.graph                      # the sharded loop (and its collectives) as one graph
     assert res.S.tolist() == ref.S.tolist() and res.k == 40
     assert res.b_prime == ref.b_prime and res.rho == ref.rho and res.b_t == ref.b_t
     assert res.blocks == ref.blocks
     assert torch.equal(torch.cat(Ws, 0), ref.W)
+
+
+@cuda
+def test_sharded_graph_loop_equals_eager(monkeypatch):
+    """The row-sharded loop as one CUDA graph (outer WHILE over blocks, inner WHILE over the
+    draw rounds) and the host-driven eager loop: bit-identical S, b', rho, W -- also on a
+    support smaller than b (several draw rounds, SUPPORT_EXHAUSTED) and in the paper form."""
+    rb = _rb()
+    cfg = small_config("c2", n=3 * 4096 + 500, d=192, rank=30, b=16)
+    X = make(cfg, device="cuda")
+    shards = [X[:4096], X[4096:8192], X[8192:]]
+    for form in ("residual", "paper"):
+        g, Wg = rb.rbrp.id_sharded(shards, tol=1e-12, b=16, seed=4, form=form)
+        monkeypatch.setenv("RBRP_NO_GRAPH", "1")
+        e, We = rb.rbrp.id_sharded(shards, tol=1e-12, b=16, seed=4, form=form)
+        monkeypatch.delenv("RBRP_NO_GRAPH")
+        assert g.graph and not e.graph
+        assert g.S.tolist() == e.S.tolist() and g.b_prime == e.b_prime and g.rho == e.rho
+        assert all(torch.equal(a, b) for a, b in zip(Wg, We))
+    Z = torch.zeros(2 * 4096 + 10, 12, dtype=torch.float64, device="cuda")
+    Z[[5, 4100, 8195, 8200]] = torch.randn(4, 12, dtype=torch.float64, device="cuda")
+    r, _ = rb.rbrp.id_sharded([Z[:4096], Z[4096:8192], Z[8192:]], tol=1e-14, b=8)
+    assert r.graph and sorted(r.S.tolist()) == [5, 4100, 8195, 8200]
 
 
 @cuda
