@@ -655,6 +655,7 @@ __global__ void __launch_bounds__(kFiltThreads, 1) k_filter_coop(FilterArgs F) {
     }
     if (tid == 0) s_kept = kept;
   }
+  __syncthreads();
   const int bq = s_kept;   // normally bp; smaller only if G2 lost definiteness
   stamp(F.dbg, 8);
   if (blockIdx.x == 0) {
