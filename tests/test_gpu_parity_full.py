@@ -216,3 +216,36 @@ def test_form_w_auto_triggers_on_tiny_diagonal():
     assert np.max(np.abs(Wg - Wo)) <= 1e-8 * np.max(np.abs(Wo))
     Wt, _, _ = O.form_W(L, S, method="trsm")
     assert np.max(np.abs(Wt)) > 1e6 * np.max(np.abs(Wg))     # what the plain solve would give
+
+
+@cuda
+@pytest.mark.parametrize("name,kw,dtype", [
+    ("c3", dict(n=5 * 4096 + 300, d=128, n_heavy_dirs=30, n_heavy_rows=9000, b=32), np.float64),
+    ("c5", dict(n=6 * 4096 + 77, d=160, n_centres=64, b=64), np.float64),
+    ("c4", dict(n=5 * 4096 + 11, d=192, b=32), np.float32),
+])
+def test_same_seed_end_to_end_multichunk(name, kw, dtype):
+    """SURVEY T3 on the other constructions (several 4096-row chunks, the tcgen05 kernel
+    for fp32): same seed -> the same S on >= 8 of 10 seeds, |S| within b on all, both meet
+    the stop rule (Alg. 2 l.3, l.5)."""
+    cfg = small_config(name, **kw)
+    Xnp = make(cfg).numpy()
+    if cfg.tau is not None:
+        tau = cfg.tau
+    else:
+        tau = (1 + cfg.eps) * R.eta(np.asarray(Xnp, np.float64), min(cfg.r, Xnp.shape[1] // 4))
+    Xd = torch.from_numpy(Xnp).cuda()
+    rb = _rb()
+    same = 0
+    for seed in range(10):
+        ores = O.rbrp(Xnp, tau=tau, b=cfg.b, seed=seed)
+        res = rb.id(Xd, tol=tau, b=cfg.b, seed=seed)
+        assert res.blocks[0] == ores.blocks[0].S_t, seed
+        assert abs(res.k - ores.k) <= cfg.b
+        assert res.resid_rel <= tau and ores.rho <= tau
+        if res.S.tolist() == ores.S:
+            same += 1
+            assert res.b_prime == [blk.b_prime for blk in ores.blocks]
+            for a, blk in zip(res.rho, ores.blocks):
+                assert abs(a - blk.rho) <= TOL[dtype]
+    assert same >= 8, same
