@@ -226,8 +226,11 @@ def test_form_w_auto_triggers_on_tiny_diagonal():
 ])
 def test_same_seed_end_to_end_multichunk(name, kw, dtype):
     """SURVEY T3 on the other constructions (several 4096-row chunks, the tcgen05 kernel
-    for fp32): same seed -> the same S on >= 8 of 10 seeds, |S| within b on all, both meet
-    the stop rule (Alg. 2 l.3, l.5)."""
+    for fp32): same seed -> the same skeletons on >= 8 of 10 seeds, |S| within b on all, both
+    meet the stop rule (Alg. 2 l.3, l.5).  "The same" compares what is unique: the skeleton
+    SET of every block.  On c3 the heavy directions all have norm exactly 100, so the pivot
+    ORDER inside a block is decided by rounding (a tie, reading R9 / R27); the kept set, b'
+    and rho_t are not."""
     cfg = small_config(name, **kw)
     Xnp = make(cfg).numpy()
     if cfg.tau is not None:
@@ -243,9 +246,16 @@ def test_same_seed_end_to_end_multichunk(name, kw, dtype):
         assert res.blocks[0] == ores.blocks[0].S_t, seed
         assert abs(res.k - ores.k) <= cfg.b
         assert res.resid_rel <= tau and ores.rho <= tau
-        if res.S.tolist() == ores.S:
+        if _block_sets(res.S.tolist(), res.b_prime) == _block_sets(ores.S, [blk.b_prime for blk in ores.blocks]):
             same += 1
-            assert res.b_prime == [blk.b_prime for blk in ores.blocks]
             for a, blk in zip(res.rho, ores.blocks):
                 assert abs(a - blk.rho) <= TOL[dtype]
     assert same >= 8, same
+
+
+def _block_sets(S, bps):
+    out, o = [], 0
+    for bp in bps:
+        out.append(sorted(S[o:o + bp]))
+        o += bp
+    return out
