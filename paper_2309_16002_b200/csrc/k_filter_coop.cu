@@ -133,21 +133,20 @@ __device__ int cta_chol_inv(const double* __restrict__ Gg, int nb, int mode, con
                             double tau_b, double* R, int ld, double* Tm, int ldt, int* perm,
                             double* mass, double* dg, int* chosen_unused, int* rank_def) {
   const int tid = threadIdx.x, lane = tid & 31;
-  int er[EPT], ec[EPT];
+  __builtin_assume(__isShared(R));    // both in shared memory at every call site
+  __builtin_assume(__isShared(Tm));
+  // element map (blockDim = kFiltThreads): thread t owns column c = t % NBX of rows
+  // t / NBX + (256 / NBX) k, NBX = 32 (EPT 4) or 64 (EPT 16); a warp shares its rows (the
+  // row loads are broadcasts) and a thread its column (R(i, c) loaded once per step)
+  constexpr int NBX = EPT == 4 ? 32 : 64, RSTEP = kFiltThreads / NBX;
+  static_assert(NBX * NBX == EPT * kFiltThreads, "element map");
+  const int ec0 = tid % NBX;
   double a[EPT], ta[EPT];
 #pragma unroll
   for (int k = 0; k < EPT; ++k) {
-    const int e = tid + k * blockDim.x;
-    if (e < nb * nb) {
-      er[k] = e / nb;
-      ec[k] = e - er[k] * nb;
-      a[k] = Gg[er[k] * kMaxB + ec[k]];
-      if (er[k] == ec[k]) dg[er[k]] = a[k];
-    } else {
-      er[k] = -1;
-      ec[k] = -1;
-      a[k] = 0.0;
-    }
+    const int r = tid / NBX + RSTEP * k;
+    a[k] = (r < nb && ec0 < nb) ? Gg[r * kMaxB + ec0] : 0.0;
+    if (r == ec0 && r < nb) dg[r] = a[k];
     ta[k] = 0.0;
   }
   for (int e = tid; e < nb * ldt; e += blockDim.x) Tm[e] = 0.0;
@@ -173,21 +172,31 @@ __device__ int cta_chol_inv(const double* __restrict__ Gg, int nb, int mode, con
         if (x > best) { best = x; bl = l; }
       }
     }
-    ms = warp_sum(ms);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-      const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
-      if (ob > best || (ob == best && ol < bl)) { best = ob; bl = ol; }
+    int p;
+    double dp;
+    if (mode == 1 && !forced) {
+      // pivot search as three warp REDUX ops: a positive double orders as its bit pattern,
+      // so max of the high words, then max of the low words among those leaders, then the
+      // lowest index holding exactly that value (ties -> lowest index, as a butterfly of
+      // (value, index) pairs would give).  A non-positive best maps to key 0: that pivot is
+      // cut below whichever index is returned.
+      const unsigned long long key = best > 0.0 ? (unsigned long long)__double_as_longlong(best) : 0ull;
+      const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+      const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+      const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+      p = __reduce_min_sync(0xffffffffu, (hi == mh && lo == ml) ? bl : (1 << 30));
+      dp = __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml));
+    } else {
+      p = mode == 2 ? i : forced[i];
+      const double dq0 = __shfl_sync(0xffffffffu, dg0, p & 31), dq1 = __shfl_sync(0xffffffffu, dg1, p & 31);
+      dp = p < 32 ? dq0 : dq1;
     }
-    if (i == 0) thr = tau_b * ms;
     int cut = 0;
-    if (mode == 1 && (!(ms > 0.0) || ms < thr)) cut = 1;            // l.8 cut
-    int p = bl;
-    if (mode == 2) p = i;
-    if (mode == 1 && forced) p = forced[i];
-    const double dq0 = __shfl_sync(0xffffffffu, dg0, p & 31), dq1 = __shfl_sync(0xffffffffu, dg1, p & 31);
-    const double dp = p < 32 ? dq0 : dq1;
+    if (mode == 1) {
+      ms = warp_sum(ms);   // fixed butterfly order
+      if (i == 0) thr = tau_b * ms;
+      if (!(ms > 0.0) || ms < thr) cut = 1;                         // l.8 cut
+    }
     if (!cut && !(dp > 0.0)) cut = 2;                               // non-positive pivot
     if (tid == 0 && mode == 1) mass[i] = ms;
     if (cut) {
@@ -201,22 +210,42 @@ __device__ int cta_chol_inv(const double* __restrict__ Gg, int nb, int mode, con
       perm[i] = p;
       Tm[i * ldt + i] = inv;
     }
+    const int c = ec0;
+    {
+      // only the owners write: row p of R is element k = (p - tid / NBX) / RSTEP of the
+      // threads of column c (selected without indexing the register array), column p of
+      // T (rows < i) belongs to the threads with c == p
+      const int rp = p - tid / NBX;
+      if (c < nb && rp >= 0 && rp % RSTEP == 0) {
+        const int kp = rp / RSTEP;
+        double av = a[0];
 #pragma unroll
-    for (int k = 0; k < EPT; ++k) {
-      const int c = ec[k];
-      const double rv = a[k] * inv, tv = -ta[k] * inv;   // computed by every lane
-      if (er[k] == p) R[i * ld + c] = (c == p) ? rii : (((chosen >> c) & 1ull) ? 0.0 : rv);
-      if (c == p && er[k] < i) Tm[er[k] * ldt + i] = tv;
+        for (int k = 1; k < EPT; ++k)
+          if (k == kp) av = a[k];
+        R[i * ld + c] = (c == p) ? rii : (((chosen >> c) & 1ull) ? 0.0 : av * inv);
+      }
+      if (c == p) {
+#pragma unroll
+        for (int k = 0; k < EPT; ++k) {
+          const int r = tid / NBX + RSTEP * k;
+          if (r < i) Tm[r * ldt + i] = -ta[k] * inv;
+        }
+      }
     }
     chosen |= 1ull << p;
     __syncthreads();   // row i of R and column i of T complete; step i+1 writes row / column i+1
-#pragma unroll
-    for (int k = 0; k < EPT; ++k) {
-      const int r = er[k], c = ec[k];
-      if (r < 0) continue;
+    {
+      // branch-free (the loads pipeline): rows r < NBX <= ld exist in R and Tm; an inactive
+      // element (r or c >= nb) only ever updates its own, never-read register, and
+      // T(r, i) = 0 for r > i (zeroed above, written only for r <= i), so the r <= i
+      // guard of the T update is implicit
       const double ric = R[i * ld + c];
-      a[k] = fma(-R[i * ld + r], ric, a[k]);
-      if (r <= i) ta[k] = fma(Tm[r * ldt + i], ric, ta[k]);
+#pragma unroll
+      for (int k = 0; k < EPT; ++k) {
+        const int r = tid / NBX + RSTEP * k;
+        a[k] = fma(-R[i * ld + r], ric, a[k]);
+        ta[k] = fma(Tm[r * ldt + i], ric, ta[k]);
+      }
     }
     if (lane < nb) {
       const double rl = R[i * ld + lane];
@@ -642,7 +671,7 @@ __global__ void __launch_bounds__(kFiltThreads, 1) k_filter_coop(FilterArgs F) {
     if (tid == 0) s_kept = bp;
   } else {
     int rd2, kept;
-    if (bp <= 32) {
+    if (bp <= 32 && small) {
       kept = cta_chol_inv<4>(F.G, bp, 2, nullptr, 0.0, Rs, ldr, Ts, ldt, perm2, nullptr, s_dg, s_ch, &rd2);
     } else if (small) {
       kept = cta_chol_inv<16>(F.G, bp, 2, nullptr, 0.0, Rs, ldr, Ts, ldt, perm2, nullptr, s_dg, s_ch, &rd2);
