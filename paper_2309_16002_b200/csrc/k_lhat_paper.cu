@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(lp::NTH, 1)
     k0 = st->k;
   } else {
     int r0;
-    if (!part_range(st->b_prime, part, &r0, &bp)) return;
+    if (!part_range(st->b_prime, part, &r0, &bp, BPB)) return;
     k0 = st->k + r0;
   }
   // DMMA work only for the 8-column groups that hold a column of Q_b (warp-uniform)
@@ -527,6 +527,318 @@ __global__ void __launch_bounds__(lp::NTH, 1)
   proj_end_stamp(st);
 }
 
+// ------------------------------------------------------------------------------------
+// k_lhat64: the same two passes for 32 < b' <= 64 columns of Q_b in ONE pass over X
+// (fp64).  k_lhat_paper's K-split warps would hold 2 x 64 accumulator columns per row pair
+// (and the update pass the whole -P row block) in registers; here the warps split N:
+// warp (rp, cw) computes L-hat(16 rows of rp, Q_b rows 16 cw .. 16 cw + 15) over every
+// column of each chunk, so a lane holds 8 accumulator doubles and no K fold is needed.
+// At the tile end each warp writes its block of -L-hat into a shared 64 x 64 tile P_s
+// (16-byte units XOR-swizzled by row); the update pass reads its A fragments (-P of its
+// 16 rows, all b' columns) from P_s and its B fragments from the pair image, as
+// k_lhat_paper's update pass does.  Rings: 3 X slots, 2 Q stages of 32 KB (227 KB).
+// The summation order of every output (L-hat: chunk by chunk, 8-column groups in order,
+// x then y halves; update: t in order) is fixed: bitwise reproducible.
+namespace lp64 {
+constexpr int BPB = 64, NT = 2;              // Q_b rows per warp column group: 2 x 8
+constexpr int QSTAGE = BPB * lp::KC;         // doubles per Q stage
+constexpr int PS = lp::R * BPB;              // doubles of the -P tile
+constexpr int NRM = 2 * lp::NRP * lp::NCW * 16;
+__host__ __device__ constexpr size_t smem(int ns, int nq) {
+  return (size_t)ns * lp::SLOT * 8 + (size_t)nq * QSTAGE * 8 + (size_t)(PS + NRM) * 8 + (2 * ns + 2 * nq) * 8 +
+         1024;
+}
+}  // namespace lp64
+
+__global__ void __launch_bounds__(lp::NTH, 1)
+    k_lhat64(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap xmap0, int lazy,
+             const double* __restrict__ Qp, double* __restrict__ L, int64_t ldl, int64_t n, int d, int nc,
+             int NS, int NQ, double* __restrict__ dvec, DevState* st, double* __restrict__ Xr, int64_t ldx,
+             int resid, int part) {
+  using LE = LpE<double>;
+  constexpr int CPB = LE::CPB, NBOX = lp::KC / CPB, BOXE = lp::R * CPB;
+  using namespace lp;
+  using lp64::NT;
+  if (st->stop) return;
+  int bp;
+  int64_t k0;
+  if (part < 0) {
+    bp = st->b_prime;
+    if (bp <= 0 || bucket_of(bp) != lp64::BPB) return;
+    k0 = st->k;
+  } else {
+    int r0;
+    if (!part_range(st->b_prime, part, &r0, &bp, lp64::BPB)) return;
+    k0 = st->k + r0;
+  }
+  const int ntr = (bp + 7) >> 3;   // 8-row groups of Q_b that hold a row (<= 8)
+  if (blockIdx.x == 0 && threadIdx.x == 0 && part <= 0) st->ts0 = gtimer();
+
+  extern __shared__ __align__(1024) double sm_raw[];
+  double* sm = sm_raw + ((1024u - (lp_su32(sm_raw) & 1023u)) & 1023u) / 8;
+  double* xs = sm;                                    // NS x SLOT
+  double* qs = xs + (size_t)NS * SLOT;                // NQ x QSTAGE
+  double* ps = qs + (size_t)NQ * lp64::QSTAGE;        // -P: [64 rows][32 units of 2], swizzled
+  double* nrm = ps + lp64::PS;                        // [tile parity][rp][cw][16]
+  uint64_t* xfull = reinterpret_cast<uint64_t*>(nrm + lp64::NRM);
+  uint64_t* xempty = xfull + NS;
+  uint64_t* qfull = xempty + NS;
+  uint64_t* qempty = qfull + NQ;
+
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int64_t ntiles = (n + R - 1) / R;
+  const int T = ntiles > blockIdx.x ? (int)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+  if (T == 0) {
+    proj_end_stamp(st);
+    return;
+  }
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) {
+      lp_init(&xfull[s], 1);
+      lp_init(&xempty[s], NCONS);
+    }
+    for (int s = 0; s < NQ; ++s) {
+      lp_init(&qfull[s], 1);
+      lp_init(&qempty[s], NCONS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  auto row0_of = [&](int p) { return ((int64_t)blockIdx.x + (int64_t)p * gridDim.x) * R; };
+  const int npass = resid ? 2 : 1;
+  const int steps = T * nc * npass;
+
+  if (w >= NCONS) {
+    if (w == NCONS && lane == 0) {   // X producer (as k_lhat_paper)
+      const CUtensorMap* mp = (lazy && st->t == 1 && part <= 0) ? &xmap0 : &xmap;
+      uint64_t pol_keep, pol_drop;
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol_keep));
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol_drop));
+      LpRing xr;
+      for (int s = 0; s < steps; ++s) {
+        if (s >= NS) lp_wait(&xempty[xr.i], xr.ph ^ 1);
+        const int y = (int)row0_of(s / (nc * npass)), c = s % nc;
+        const bool second = resid && ((s / nc) & 1);
+        lp_expect(&xfull[xr.i], SLOT * 8);
+        double* dst = xs + (size_t)xr.i * SLOT;
+        const uint64_t pol = resid ? (second ? pol_drop : pol_keep) : pol_drop;
+#pragma unroll
+        for (int b = 0; b < NBOX; ++b)
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint "
+              "[%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(lp_su32(dst + b * BOXE)),
+              "l"(mp), "r"(c * KC + CPB * b), "r"(y), "r"(lp_su32(&xfull[xr.i])), "l"(pol)
+              : "memory");
+        xr.next(NS);
+      }
+    } else if (w == NCONS + 1 && lane == 0) {   // Q producer: image 1 (L-hat pass), image 2 (update)
+      LpRing qr;
+      for (int s = 0; s < steps; ++s) {
+        if (s >= NQ) lp_wait(&qempty[qr.i], qr.ph ^ 1);
+        lp_expect(&qfull[qr.i], (uint32_t)(lp64::QSTAGE * 8));
+        const int in = s % (nc * npass);
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                lp_su32(qs + (size_t)qr.i * lp64::QSTAGE)),
+            "l"(Qp + (in >= nc ? (size_t)nc * PACK_ROWS * KC : 0) + (size_t)(in % nc) * PACK_ROWS * KC),
+            "r"((uint32_t)(lp64::QSTAGE * 8)), "r"(lp_su32(&qfull[qr.i]))
+            : "memory");
+        qr.next(NQ);
+      }
+    }
+    __syncwarp();
+  } else {
+    const uint32_t xs_s = lp_su32(xs), qs_s = lp_su32(qs), ps_s = lp_su32(ps);
+    const uint32_t xf_s = lp_su32(xfull), xe_s = lp_su32(xempty), qf_s = lp_su32(qfull), qe_s = lp_su32(qempty);
+    auto release = [&](int xi, int qi) {
+      __syncwarp();
+      if (lane == 0) {
+        lp_arrives(xe_s + 8 * xi);
+        lp_arrives(qe_s + 8 * qi);
+      }
+    };
+    const int rp = w >> 2, cw = w & 3;
+    const int g = lane >> 2, q = lane & 3;
+    const int pg = LE::pg(g);
+    // this lane's tile rows (MMA row g of the two 8-row groups) and their swizzle keys
+    const int ra = 16 * rp + pg, rb = ra + 8;
+    const int sw = ra & 7;   // = rb & 7
+    // L-hat pass, X fragments: row ra / rb, columns 8h + 2q of the chunk (h = 0..7):
+    // lp_xoff_e(row, 8h + 2q) = (h >> 1) * 1024 + row * 16 + (((4 (h & 1) + q) ^ (row & 7)) * 2)
+    const int xa = ra * 16, xb = rb * 16;
+    // update pass, X fragments: columns 16 cw + 8 hh + 2q (k_lhat_paper's layout)
+    int xo[2][2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) xo[r][hh] = lp_xoff_e<double>(r ? rb : ra, 16 * cw + 8 * hh + 2 * q);
+    // Q image 1 rows of this warp: j = 16 cw + 8 t + g
+    int qj[NT], qf[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      qj[t] = 16 * cw + 8 * t + g;
+      qf[t] = (8 * (qj[t] & 1)) ^ (4 * ((qj[t] >> 1) & 3));
+    }
+    const bool on0 = 2 * cw < ntr, on1 = 2 * cw + 1 < ntr;   // warp-uniform
+    LpRing qr, xr;
+    for (int p = 0; p < T; ++p) {
+      double2 acc[2][NT];
+#pragma unroll
+      for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int t = 0; t < NT; ++t) acc[r][t] = make_double2(0.0, 0.0);
+      for (int c = 0; c < nc; ++c) {
+        lp_waits(qf_s + 8 * qr.i, qr.ph);
+        lp_waits(xf_s + 8 * xr.i, xr.ph);
+        const uint32_t xsl = xs_s + xr.i * (SLOT * 8);
+        const uint32_t Qs = qs_s + qr.i * (lp64::QSTAGE * 8);
+        if (on0) {
+#pragma unroll
+          for (int h = 0; h < 8; ++h) {
+            const int cu = 4 * (h & 1) + q, bo = (h >> 1) * 1024;
+            const double2 a0 = lp_lds2s(xsl + 8 * (bo + xa + ((cu ^ sw) * 2)));
+            const double2 a1 = lp_lds2s(xsl + 8 * (bo + xb + ((cu ^ sw) * 2)));
+            const double2 b0 = lp_lds2s(Qs + 8 * (qj[0] * KC + ((8 * h + 2 * q) ^ qf[0])));
+            lp_dmma(acc[0][0], a0.x, b0.x);
+            lp_dmma(acc[1][0], a1.x, b0.x);
+            lp_dmma(acc[0][0], a0.y, b0.y);
+            lp_dmma(acc[1][0], a1.y, b0.y);
+            if (on1) {
+              const double2 b1 = lp_lds2s(Qs + 8 * (qj[1] * KC + ((8 * h + 2 * q) ^ qf[1])));
+              lp_dmma(acc[0][1], a0.x, b1.x);
+              lp_dmma(acc[1][1], a1.x, b1.x);
+              lp_dmma(acc[0][1], a0.y, b1.y);
+              lp_dmma(acc[1][1], a1.y, b1.y);
+            }
+          }
+        }
+        release(xr.i, qr.i);
+        xr.next(NS);
+        qr.next(NQ);
+      }
+      // tile end: L-hat to L; -L-hat into P_s (residual form) or the l.16 downdate (paper)
+      const int64_t r0 = row0_of(p);
+      double ss[2] = {0.0, 0.0};
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int trow = r ? rb : ra;
+        const int64_t row = r0 + trow;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          if (!(t ? on1 : on0)) continue;
+          const double vx = acc[r][t].x, vy = acc[r][t].y;
+          const int j = 16 * cw + 8 * t + 2 * q;
+          if (row < n) {
+            if (j < bp) L[row * ldl + k0 + j] = vx;
+            if (j + 1 < bp) L[row * ldl + k0 + j + 1] = vy;
+          }
+          ss[r] += vx * vx + vy * vy;
+          if (resid) {
+            const int u = 8 * cw + 4 * t + q;   // 16-byte unit (columns 2u, 2u + 1)
+            double* dst = ps + trow * lp64::BPB + 2 * (u ^ sw);
+            dst[0] = -vx;
+            dst[1] = -vy;
+          }
+        }
+      }
+      double* nb = nrm + (size_t)((p & 1) * NRP + rp) * NCW * 16;
+      if (!resid) {
+        // l.16 downdate (paper form): sum over the row's columns, q lanes then cw in order
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          double v = ss[r];
+          v += __shfl_xor_sync(0xffffffffu, v, 1);
+          v += __shfl_xor_sync(0xffffffffu, v, 2);
+          if (q == 0) nb[cw * 16 + 8 * r + pg] = v;
+        }
+        lp_bar();
+        if (cw == 0 && lane < 16 && dvec) {
+          const double v = (nb[lane] + nb[16 + lane]) + (nb[32 + lane] + nb[48 + lane]);
+          const int64_t row = r0 + 16 * rp + lane;
+          if (row < n) dvec[row] = fmax(dvec[row] - v, 0.0);
+        }
+      } else {
+        lp_bar();   // P_s complete
+        // ----- update pass (l.16): X(tile) -= L-hat Q_b, chunk by chunk through L2
+        double nr[2] = {0.0, 0.0};
+        const bool v0 = r0 + ra < n, v1 = r0 + rb < n;
+        double* xp = Xr + (r0 + ra) * ldx + 16 * cw + 2 * q;
+        const int64_t l8 = 8 * ldx;
+        const uint32_t pa = ps_s + 8 * (ra * lp64::BPB), pb = ps_s + 8 * (rb * lp64::BPB);
+        for (int c = 0; c < nc; ++c) {
+          lp_waits(qf_s + 8 * qr.i, qr.ph);
+          lp_waits(xf_s + 8 * xr.i, xr.ph);
+          const uint32_t xsl = xs_s + xr.i * (SLOT * 8);
+          const uint32_t Qs = qs_s + qr.i * (lp64::QSTAGE * 8);
+          double2 xv[2][2];
+#pragma unroll
+          for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) xv[r][hh] = lp_lds2s(xsl + 8 * xo[r][hh]);
+          const uint32_t qb = Qs + 16 * (q * KC + ((16 * cw + g) ^ (2 * q)));
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            if (t >= ntr) break;
+            const double2 b0 = lp_lds2s(qb + 16 * 4 * KC * t);
+            const double2 b1 = lp_lds2s(qb + 16 * 4 * KC * t + 128);
+            const int u = (4 * t + q) ^ sw;
+            const double2 fa = lp_lds2s(pa + 16 * u), fb = lp_lds2s(pb + 16 * u);
+            lp_dmma_v(xv[0][0], fa.x, b0.x);
+            lp_dmma_v(xv[1][0], fb.x, b0.x);
+            lp_dmma_v(xv[0][1], fa.x, b1.x);
+            lp_dmma_v(xv[1][1], fb.x, b1.x);
+            lp_dmma_v(xv[0][0], fa.y, b0.y);
+            lp_dmma_v(xv[1][0], fb.y, b0.y);
+            lp_dmma_v(xv[0][1], fa.y, b1.y);
+            lp_dmma_v(xv[1][1], fb.y, b1.y);
+          }
+          release(xr.i, qr.i);
+          xr.next(NS);
+          qr.next(NQ);
+          double* xc = xp + c * KC;
+          if (c * KC + KC <= d) {
+            if (v0) {
+              LE::st2(xc, xv[0][0]);
+              LE::st2(xc + 8, xv[0][1]);
+            }
+            if (v1) {
+              LE::st2(xc + l8, xv[1][0]);
+              LE::st2(xc + l8 + 8, xv[1][1]);
+            }
+          } else {
+            const int col = c * KC + 16 * cw + 2 * q;
+            if (v0 && col < d) LE::st2(xc, xv[0][0]);
+            if (v0 && col + 8 < d) LE::st2(xc + 8, xv[0][1]);
+            if (v1 && col < d) LE::st2(xc + l8, xv[1][0]);
+            if (v1 && col + 8 < d) LE::st2(xc + l8 + 8, xv[1][1]);
+          }
+#pragma unroll
+          for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) nr[r] += xv[r][hh].x * xv[r][hh].x + xv[r][hh].y * xv[r][hh].y;
+        }
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          double v = nr[r];
+          v += __shfl_xor_sync(0xffffffffu, v, 1);
+          v += __shfl_xor_sync(0xffffffffu, v, 2);
+          if (q == 0) nb[cw * 16 + 8 * r + pg] = v;
+        }
+        lp_bar();
+        if (cw == 0 && lane < 16) {
+          const double v = (nb[lane] + nb[16 + lane]) + (nb[32 + lane] + nb[48 + lane]);
+          const int64_t row = r0 + 16 * rp + lane;
+          if (row < n) dvec[row] = v;
+        }
+      }
+      // P_s and nrm are rewritten one tile later (nc chunk steps); the rings keep every warp
+      // within max(NS, NQ) steps of the others, so a barrier is only needed for short tiles
+      if (nc <= (NS > NQ ? NS : NQ) + 1) lp_bar();
+    }
+  }
+  proj_end_stamp(st);
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 lp_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static bool tried = false;
@@ -567,6 +879,7 @@ int lhat_paper_max_bucket_t(const void* X, int64_t ldx, int64_t d) {
   int ns, nq, best = 0;
   if (LpCfg<16, E>::rings(ns, nq)) best = 16;
   if (LpCfg<32, E>::rings(ns, nq)) best = 32;
+  if (sizeof(E) == 8 && best == 32 && lp64::smem(3, 2) <= (size_t)lp::SMEM_MAX && !getenv("RBRP_NO_LP64")) best = 64;
   return best;
 }
 int lhat_paper_max_bucket(const void* X, int64_t ldx, int64_t d) { return lhat_paper_max_bucket_t<double>(X, ldx, d); }
@@ -595,6 +908,22 @@ static cudaError_t go_lp(const CUtensorMap& map, const CUtensorMap& map0, int la
   return cudaGetLastError();
 }
 
+static cudaError_t go_lp64(const CUtensorMap& map, const CUtensorMap& map0, int lazy, const double* Qp, double* L,
+                           int64_t ldl, int64_t n, int64_t d, double* dvec, DevState* st, double* Xr, int64_t ldx,
+                           int resid, cudaStream_t s, int part) {
+  const int ns = 3, nq = 2;
+  const size_t smem = lp64::smem(ns, nq);
+  static PerDevice attr;
+  const cudaError_t ae = attr.once([smem] {
+    return cudaFuncSetAttribute(k_lhat64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  });
+  if (ae != cudaSuccess) return ae;
+  const int nc = (int)((d + lp::KC - 1) / lp::KC);
+  k_lhat64<<<lp_sms(), lp::NTH, smem, s>>>(map, map0, lazy, Qp, L, ldl, n, (int)d, nc, ns, nq, dvec, st, Xr, ldx,
+                                            resid, part);
+  return cudaGetLastError();
+}
+
 template <typename E>
 static cudaError_t launch_lhat_paper_t(const E* X, int64_t ldx, const double* Qp, E* L, int64_t ldl, int64_t n,
                                        int64_t d, double* dvec, DevState* st, int bucket, bool resid,
@@ -618,6 +947,9 @@ static cudaError_t launch_lhat_paper_t(const E* X, int64_t ldx, const double* Qp
   switch (bucket) {
     case 16: return go_lp<16, E>(map, map0, lazy, Qp, L, ldl, n, d, dvec, st, (E*)X, ldx, resid ? 1 : 0, s, -1);
     case 32: return go_lp<32, E>(map, map0, lazy, Qp, L, ldl, n, d, dvec, st, (E*)X, ldx, resid ? 1 : 0, s, part);
+    case 64:
+      if (sizeof(E) != 8) return cudaErrorInvalidValue;
+      return go_lp64(map, map0, lazy, Qp, (double*)L, ldl, n, d, dvec, st, (double*)X, ldx, resid ? 1 : 0, s, part);
     default: return cudaErrorInvalidValue;
   }
 }

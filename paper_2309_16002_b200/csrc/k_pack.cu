@@ -21,11 +21,11 @@ __host__ __device__ __forceinline__ int pk_qswz(int j, int col) {
   return col ^ (8 * (j & 1)) ^ (4 * ((j >> 1) & 3));
 }
 
-// part < 0: rows [0, b'), b' <= 64.  part >= 0 (b' > 32 split into balanced parts of <= 32
+// part < 0: rows [0, b'), b' <= 64.  part >= 0 (b' > pw split into balanced parts of <= pw
 // rows, part_range): rows [r0, r0 + cnt).
 template <typename QT>
 __global__ void k_pack_q(const QT* __restrict__ Qt, int64_t d, double* __restrict__ Qp,
-                         const DevState* st, int part, int64_t ldq) {
+                         const DevState* st, int part, int64_t ldq, int pw) {
   if (st->stop) return;
   const int bpa = st->b_prime;
   int bp, r0 = 0;
@@ -33,7 +33,7 @@ __global__ void k_pack_q(const QT* __restrict__ Qt, int64_t d, double* __restric
     bp = bpa;
     if (bp <= 0 || bp > pk::PACK_ROWS) return;
   } else {
-    if (!part_range(bpa, part, &r0, &bp)) return;
+    if (!part_range(bpa, part, &r0, &bp, pw)) return;
   }
   const int c = blockIdx.x, j = blockIdx.y, col = threadIdx.x;   // blockDim = KC
   const int64_t gc = (int64_t)c * pk::KC + col;
@@ -49,16 +49,16 @@ static int pk_nc(int64_t d) { return (int)((d + pk::KC - 1) / pk::KC); }
 size_t fused_pack_bytes(int64_t d) { return 2 * (size_t)pk_nc(d) * pk::PACK_ROWS * pk::KC * 8; }   // two images
 
 cudaError_t launch_pack_q(const float* Qt, int64_t d, double* Qp, DevState* st, cudaStream_t s, int part,
-                          int64_t ldq) {
+                          int64_t ldq, int pw) {
   dim3 grid((unsigned)pk_nc(d), pk::PACK_ROWS);
-  k_pack_q<float><<<grid, pk::KC, 0, s>>>(Qt, d, Qp, st, part, ldq > 0 ? ldq : d);
+  k_pack_q<float><<<grid, pk::KC, 0, s>>>(Qt, d, Qp, st, part, ldq > 0 ? ldq : d, pw);
   return cudaGetLastError();
 }
 
 cudaError_t launch_pack_q(const double* Qt, int64_t d, double* Qp, DevState* st, cudaStream_t s, int part,
-                          int64_t ldq) {
+                          int64_t ldq, int pw) {
   dim3 grid((unsigned)pk_nc(d), pk::PACK_ROWS);
-  k_pack_q<double><<<grid, pk::KC, 0, s>>>(Qt, d, Qp, st, part, ldq > 0 ? ldq : d);
+  k_pack_q<double><<<grid, pk::KC, 0, s>>>(Qt, d, Qp, st, part, ldq > 0 ? ldq : d, pw);
   return cudaGetLastError();
 }
 

@@ -104,12 +104,16 @@ cudaError_t launch_update_mma(double* Xres, int64_t ldx, const double* Qt, const
 // k_pack.cu — Q_b packed in the shared-memory image of k_lhat_paper (two images)
 size_t fused_pack_bytes(int64_t d);
 // Qt: rows of Q_b (leading dimension ldq, 0 -> d), d columns packed
+// part >= 0: rows of part_range(b', part, pw)
 cudaError_t launch_pack_q(const double* Qt, int64_t d, double* Qp, DevState* st, cudaStream_t s, int part = -1,
-                          int64_t ldq = 0);
+                          int64_t ldq = 0, int pw = 32);
 cudaError_t launch_pack_q(const float* Qt, int64_t d, double* Qp, DevState* st, cudaStream_t s, int part = -1,
-                          int64_t ldq = 0);
+                          int64_t ldq = 0, int pw = 32);
 
-// k_lhat_paper.cu — paper form, l.13 + l.16: read-only DMMA pass with 64-row tiles
+// k_lhat_paper.cu — paper form, l.13 + l.16: read-only DMMA pass with 64-row tiles.
+// bucket 16 / 32: k_lhat_paper (K-split warps); bucket 64 (fp64): k_lhat64 (N-split warps,
+// L-hat tile shared through shared memory).  part >= 0: the rows part_range(b', part,
+// bucket) of Q_b (b' > bucket)
 int lhat_paper_max_bucket(const void* X, int64_t ldx, int64_t d);
 cudaError_t launch_lhat_paper(const double* X, int64_t ldx, const double* Qp, double* L, int64_t ldl,
                               int64_t n, int64_t d, double* dvec, DevState* st, int bucket, bool resid,

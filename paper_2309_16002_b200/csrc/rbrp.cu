@@ -393,11 +393,11 @@ int enqueue_projection(Ctx<T>& c, cudaStream_t s, int* nl) {
   const int fmax = (c.paper || c.tiled) ? c.lp_max : 0;
   if (fmax > 0 && (rc = lk(launch_pack_q(c.Qt, c.d, c.Qp, c.st, s)))) return rc;
   bool need_downdate = false;
-  // b' > 32 on the 64-row-tile kernel: 32-column parts in sequence (RBRP_NO_PARTS=1: the
-  // two-kernel path instead)
-  const bool parts = (c.paper || c.tiled) && c.lp_max >= 32 && c.bucketB > 32 && !env_on("RBRP_NO_PARTS");
+  // b' above the widest 64-row-tile kernel (64 columns fp64, 32 fp32): balanced parts of
+  // <= lp_max columns in sequence (RBRP_NO_PARTS=1: the two-kernel path instead)
+  const bool parts = (c.paper || c.tiled) && c.lp_max >= 32 && c.bucketB > c.lp_max && !env_on("RBRP_NO_PARTS");
   for (int bk = 16; bk <= c.bucketB; bk *= 2) {
-    if (bk > 32 && parts) continue;
+    if (bk > c.lp_max && parts) continue;
     if (bk <= fmax) {
       rc = lk(launch_lhat_paper((const T*)c.Xres, c.ldr, c.Qp, c.Lm, c.k_cap, c.n, c.d, c.dvec, c.st, bk,
                                 !c.paper, s, c.lazy ? (const T*)c.X : nullptr, c.p->ld));
@@ -416,9 +416,9 @@ int enqueue_projection(Ctx<T>& c, cudaStream_t s, int* nl) {
     }
     if (rc) return rc;
   }
-  for (int part = 0; parts && part < c.bucketB / 32; ++part) {
-    if ((rc = lk(launch_pack_q(c.Qt, c.d, c.Qp, c.st, s, part)))) return rc;
-    if ((rc = lk(launch_lhat_paper((const T*)c.Xres, c.ldr, c.Qp, c.Lm, c.k_cap, c.n, c.d, c.dvec, c.st, 32,
+  for (int part = 0; parts && part < (c.bucketB + c.lp_max - 1) / c.lp_max; ++part) {
+    if ((rc = lk(launch_pack_q(c.Qt, c.d, c.Qp, c.st, s, part, 0, c.lp_max)))) return rc;
+    if ((rc = lk(launch_lhat_paper((const T*)c.Xres, c.ldr, c.Qp, c.Lm, c.k_cap, c.n, c.d, c.dvec, c.st, c.lp_max,
                                    !c.paper, s, c.lazy ? (const T*)c.X : nullptr, c.p->ld, part))))
       return rc;
   }
@@ -517,6 +517,7 @@ struct GraphKey {
   const void* X;
   const void* ws;
   const void* aux;   // row-sharded graphs: the communicator
+  uint64_t shards;   // row-sharded graphs: hash of every shard's X, workspace and rows
   int device, use_mma;
   bool operator==(const GraphKey& o) const { return memcmp(this, &o, sizeof(GraphKey)) == 0; }
 };
@@ -557,7 +558,8 @@ void evict_lru(std::list<std::shared_ptr<E>>& cache, size_t cap) {
   }
 }
 
-GraphKey make_key(const rbrp_problem* p, const void* X, const void* ws, int variant, const void* aux = nullptr) {
+GraphKey make_key(const rbrp_problem* p, const void* X, const void* ws, int variant, const void* aux = nullptr,
+                  uint64_t shards = 0) {
   GraphKey k;
   memset(&k, 0, sizeof(k));
   k.p = *p;
@@ -569,7 +571,28 @@ GraphKey make_key(const rbrp_problem* p, const void* X, const void* ws, int vari
   cudaGetDevice(&k.device);
   k.use_mma = variant;
   k.aux = aux;
+  k.shards = shards;
   return k;
+}
+
+// FNV-1a over the shard pointers and sizes: a graph captured for one set of in-process
+// shards bakes every shard's X and workspace address into its kernels, not only shard 0's
+uint64_t shard_hash(int nsh, const rbrp_problem* ps, void* const* Xs, char* const* wss) {
+  uint64_t h = 1469598103934665603ull;
+  auto mix = [&](uint64_t v) {
+    for (int i = 0; i < 8; ++i) {
+      h ^= (v >> (8 * i)) & 0xffu;
+      h *= 1099511628211ull;
+    }
+  };
+  for (int i = 0; i < nsh; ++i) {
+    mix((uint64_t)(uintptr_t)Xs[i]);
+    mix((uint64_t)(uintptr_t)wss[i]);
+    mix((uint64_t)ps[i].n_local);
+    mix((uint64_t)ps[i].row_offset);
+    mix((uint64_t)ps[i].ld);
+  }
+  return h;
 }
 
 // Returns the cached graph for key, building it if needed; nullptr if graphs are not
@@ -1291,7 +1314,8 @@ int run_dist(int nsh, const rbrp_problem* ps, void* const* Xs, char* const* wss,
   if (!hst->stop && !p->replay_nblocks && !env_on("RBRP_NO_GRAPH"))
     dg = get_graph_dist<T>(C.data(), SA.data(), nsh, comm, enqueue_dblock, enqueue_dsample, enqueue_dround,
                            make_key(p, Xs[0], wss[0], 64 | (nsh << 8) | (C[0].lazy ? 8 : 0) | (C[0].paper ? 16 : 0) |
-                                                           (C[0].tc32 ? 2 : 0) | (C[0].use_mma ? 1 : 0), comm));
+                                                           (C[0].tc32 ? 2 : 0) | (C[0].use_mma ? 1 : 0), comm,
+                                    shard_hash(nsh, ps, Xs, wss)));
   if (dg) {
     CK(cudaGraphLaunch(dg->exec, s));
     CK(cudaMemcpyAsync(hst, C[0].st, sizeof(DevState), cudaMemcpyDeviceToHost, s));

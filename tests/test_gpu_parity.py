@@ -328,6 +328,27 @@ def test_sharded_graph_loop_equals_eager(monkeypatch):
 
 
 @cuda
+def test_sharded_graph_cache_keys_every_shard():
+    """A row-sharded graph bakes every shard's X and workspace into its kernels: a second
+    call that keeps shard 0 (same tensor, same workspace address) but swaps the other shards
+    must not replay the first call's graph."""
+    rb = _rb()
+    dev = torch.device("cuda")
+    Z0 = torch.zeros(4096, 12, dtype=torch.float64, device=dev)
+    Z0[5] = torch.randn(12, dtype=torch.float64, device=dev)
+    keep = []   # the first call's shards stay allocated: the second call's get new addresses
+    for rows in ([100, 4000], [7, 2222]):   # nonzero rows of shard 1 (global 4096 + r)
+        Z1 = torch.zeros(4096, 12, dtype=torch.float64, device=dev)
+        Z1[rows] = torch.randn(2, 12, dtype=torch.float64, device=dev)
+        Z2 = torch.zeros(10, 12, dtype=torch.float64, device=dev)
+        Z2[3] = torch.randn(12, dtype=torch.float64, device=dev)
+        r, _ = rb.rbrp.id_sharded([Z0, Z1, Z2], tol=1e-14, b=8)
+        assert r.graph
+        assert sorted(r.S.tolist()) == [5] + [4096 + x for x in sorted(rows)] + [8192 + 3]
+        keep += [Z1, Z2]
+
+
+@cuda
 def test_sharded_replay_and_c3_duplicates():
     """Sharded run in forced-pivot replay against the oracle on the duplicate
     adversary (c3 construction), 3 shards."""
