@@ -989,29 +989,58 @@ size_t gemm_lp_scratch_bytes(int64_t N, int64_t K) {
   return ((fused_pack_bytes(K) + 255) & ~(size_t)255) + (size_t)G * sizeof(DevState);
 }
 
-// K >= 512: the per-tile fold of the 4-way K split is amortised over >= 8 chunk steps
-// (measured: W = L L_1^{-1} at K = 128 and the OSID W at K = 384 ran slower than k_nt_mma)
-bool gemm_lp_supported(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t K, int64_t min_k) {
-  return K >= min_k && lhat_paper_max_bucket(A, lda, K) >= 32 && ldb == K && ((uintptr_t)B % 16) == 0;
+// min_k: k_lhat_paper's per-tile fold of the 4-way K split needed K >= 512 to beat
+// k_nt_mma; the 64-column groups on k_lhat64 (no fold) win from K = 128 (scripts/w_bench.py)
+template <typename E>
+static int lp_max_bucket_e(const E* A, int64_t lda, int64_t K) {
+  return sizeof(E) == 8 ? lhat_paper_max_bucket(A, lda, K) : lhat_paper_max_bucket_f32(A, lda, K);
 }
 
-cudaError_t gemm_nt_lp(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
-                       int64_t M, int64_t N, int64_t K, void* scratch, cudaStream_t s, bool lower_b, int64_t min_k) {
+template <typename E>
+static bool gemm_lp_supported_t(const E* A, int64_t lda, const E* B, int64_t ldb, int64_t K, int64_t min_k) {
+  return K >= min_k && lp_max_bucket_e(A, lda, K) >= 32 && ldb == K && ((uintptr_t)B % 16) == 0;
+}
+bool gemm_lp_supported(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t K, int64_t min_k) {
+  return gemm_lp_supported_t(A, lda, B, ldb, K, min_k);
+}
+bool gemm_lp_supported(const float* A, int64_t lda, const float* B, int64_t ldb, int64_t K, int64_t min_k) {
+  return gemm_lp_supported_t(A, lda, B, ldb, K, min_k);
+}
+
+// fp32 storage: k_lhat_paper<32, float> groups (fp64 DMMA arithmetic on the fp32 values,
+// the result rounded once to fp32)
+template <typename E>
+static cudaError_t gemm_nt_lp_t(const E* A, int64_t lda, const E* B, int64_t ldb, E* C, int64_t ldc, int64_t M,
+                                int64_t N, int64_t K, void* scratch, cudaStream_t s, bool lower_b, int64_t min_k,
+                                int* nlaunch) {
   if (M <= 0 || N <= 0) return cudaSuccess;
-  if (!gemm_lp_supported(A, lda, B, ldb, K, min_k)) return cudaErrorNotSupported;
+  if (!gemm_lp_supported_t(A, lda, B, ldb, K, min_k)) return cudaErrorNotSupported;
   double* Qp = (double*)scratch;
   DevState* st = (DevState*)((char*)scratch + ((fused_pack_bytes(K) + 255) & ~(size_t)255));
-  const int64_t G = (N + 31) / 32;
-  k_gemm_groups<<<(unsigned)((G + 127) / 128), 128, 0, s>>>(st, N, 32);
+  // groups of 64 columns of C on k_lhat64 (one read of A per 64 columns), else 32
+  const int gw = (lp_max_bucket_e(A, lda, K) >= 64 && !getenv("RBRP_GEMM_GW32")) ? 64 : 32;
+  const int64_t G = (N + gw - 1) / gw;
+  k_gemm_groups<<<(unsigned)((G + 127) / 128), 128, 0, s>>>(st, N, gw);
+  if (nlaunch) *nlaunch += 1 + 2 * (int)G;
   cudaError_t e = cudaGetLastError();
   for (int64_t g = 0; g < G && e == cudaSuccess; ++g) {
-    const int bg = (int)(N - 32 * g < 32 ? N - 32 * g : 32);
-    const int64_t k0 = lower_b ? (32 * g / lp::KC) * lp::KC : 0;   // B(rows of g, m < k0) = 0
-    e = launch_pack_q(B + 32 * g * ldb + k0, K - k0, Qp, st + g, s, -1, ldb);
+    const int bg = (int)(N - gw * g < gw ? N - gw * g : gw);
+    const int64_t k0 = lower_b ? (gw * g / lp::KC) * lp::KC : 0;   // B(rows of g, m < k0) = 0
+    e = launch_pack_q(B + gw * g * ldb + k0, K - k0, Qp, st + g, s, -1, ldb);
     if (e == cudaSuccess)
       e = launch_lhat_paper(A + k0, lda, Qp, C, ldc, M, K - k0, nullptr, st + g, bucket_of(bg), false, s);
   }
   return e;
+}
+cudaError_t gemm_nt_lp(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
+                       int64_t M, int64_t N, int64_t K, void* scratch, cudaStream_t s, bool lower_b, int64_t min_k,
+                       int* nlaunch) {
+  return gemm_nt_lp_t(A, lda, B, ldb, C, ldc, M, N, K, scratch, s, lower_b, min_k, nlaunch);
+}
+cudaError_t gemm_nt_lp(const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
+                       int64_t M, int64_t N, int64_t K, void* scratch, cudaStream_t s, bool lower_b, int64_t min_k,
+                       int* nlaunch) {
+  return gemm_nt_lp_t(A, lda, B, ldb, C, ldc, M, N, K, scratch, s, lower_b, min_k, nlaunch);
 }
 
 }  // namespace rbrp

@@ -52,8 +52,9 @@ constexpr int NMAX = 64;                  // Q_b rows per part
 constexpr int XSLOT = M * KC * 4;         // 16 KB X chunk
 constexpr int QSLOT = 2 * NMAX * KC * 4;  // 16 KB shared-memory Q stage (one image)
 constexpr int QIMG = 2 * QSLOT;           // global: image 1 (pass 1) + image 2 (pass 2) per chunk
-constexpr int NSX = 7;                    // X ring depth
-constexpr int QRING = 96 * 1024;          // Q ring bytes: slots of the launch's image size (<= QSLOT)
+constexpr int NSX = 7;                    // X ring depth (default; RBRP_TC_NSX, <= NSXMAX)
+constexpr int NSXMAX = 12;
+constexpr int QRING = 96 * 1024;          // Q ring bytes (default; RBRP_TC_QRING_KB): slots of the launch's image size (<= QSLOT)
 constexpr int NSQMAX = 24;
 constexpr int NROWW = 8;                  // row warps
 constexpr int W_XP = 0, W_MMA = 1, W_QP = 2, W_ROW0 = 3;
@@ -64,7 +65,9 @@ constexpr uint32_t T_ACC1 = 0;     // D1: 2 N1 <= 128 columns
 constexpr uint32_t T_XA = 128;     // pass-1 A: 2 stages x (hi 32 | lo 32)
 constexpr uint32_t T_LA = 256;     // pass-2 A: L-hat hi (64) | lo (64)
 constexpr uint32_t T_ACC2 = 384;   // D2: NACC2 stages x 32
-constexpr size_t SMEM = 1024 + (size_t)NSX * XSLOT + QRING + 2 * 2 * M * 8 + 1024;
+constexpr size_t smem_bytes(int nsx, int qring) { return 1024 + (size_t)nsx * XSLOT + qring + 2 * 2 * M * 8 + 1024; }
+constexpr size_t SMEM = smem_bytes(NSX, QRING);
+constexpr size_t SMEM_MAX = 232448;
 }  // namespace tc
 
 __device__ __forceinline__ uint32_t tc_su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -215,7 +218,7 @@ __global__ void __launch_bounds__(tc::NTH, 1)
     k_proj_tc32(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap xmap0, int lazy,
                 const float* __restrict__ Qimg, float* __restrict__ L, int64_t ldl, int64_t n, int d, int nc,
                 DevState* st, float* __restrict__ Xr, int64_t ldx, double* __restrict__ dvec, int part,
-                long long* __restrict__ tr) {
+                long long* __restrict__ tr, int nsx, int qring) {
   using namespace tc;
   // optional cycle trace of CTA 0, tiles 0-1 (RBRP_TC_TRACE=1; profiling only):
   // tr[(event * 2 + tile) * 128 + step]
@@ -241,18 +244,18 @@ __global__ void __launch_bounds__(tc::NTH, 1)
   // Q ring slots sized for this launch's images (1 KB multiples: 1024-byte-aligned images)
   const int nkb_ = (N1 + 31) / 32;
   const int qslot = max(2 * N1 * KC * 4, 2 * nkb_ * KC * 128);
-  const int NSQ = min(NSQMAX, QRING / qslot);
+  const int NSQ = min(NSQMAX, qring / qslot);
   if (blockIdx.x == 0 && threadIdx.x == 0 && part <= 0) st->ts0 = gtimer();
 
   extern __shared__ __align__(1024) uint8_t tc_smem[];
   uint8_t* sm = tc_smem + ((1024u - (tc_su32(tc_smem) & 1023u)) & 1023u);
   uint8_t* xs = sm;
-  uint8_t* qs = xs + (size_t)NSX * XSLOT;
-  double* nrm = reinterpret_cast<double*>(qs + QRING);   // [tile parity][h][128]
+  uint8_t* qs = xs + (size_t)nsx * XSLOT;
+  double* nrm = reinterpret_cast<double*>(qs + qring);   // [tile parity][h][128]
   uint64_t* bars = reinterpret_cast<uint64_t*>(nrm + 2 * 2 * M);
   uint64_t* xfull = bars;
-  uint64_t* xempty = xfull + NSX;
-  uint64_t* qfull = xempty + NSX;
+  uint64_t* xempty = xfull + nsx;
+  uint64_t* qfull = xempty + nsx;
   uint64_t* qempty = qfull + NSQMAX;
   uint64_t* afull = qempty + NSQMAX;
   uint64_t* aempty = afull + 2;
@@ -270,7 +273,7 @@ __global__ void __launch_bounds__(tc::NTH, 1)
     return;
   }
   if (tid == 0) {
-    for (int s = 0; s < NSX; ++s) {
+    for (int s = 0; s < nsx; ++s) {
       tc_bar_init(tc_su32(&xfull[s]), 1);
       tc_bar_init(tc_su32(&xempty[s]), NROWW);
     }
@@ -328,7 +331,7 @@ __global__ void __launch_bounds__(tc::NTH, 1)
             "[%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(tc_su32(xs + (size_t)xr.i * XSLOT)),
             "l"(mp), "r"(c * KC), "r"(y), "r"(fb), "l"((second || c < keep_from) ? pol_drop : pol_keep)
             : "memory");
-        xr.next(NSX);
+        xr.next(nsx);
       }
     }
   } else if (w == W_QP) {
@@ -437,7 +440,7 @@ __global__ void __launch_bounds__(tc::NTH, 1)
         }
         __syncwarp();
         if (lane == 0) tc_arrive(tc_su32(&xempty[xr.i]));
-        xr.next(NSX);
+        xr.next(nsx);
         uint32_t hi[16], lo[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) tc_split(v[i], hi[i], lo[i]);
@@ -542,7 +545,7 @@ __global__ void __launch_bounds__(tc::NTH, 1)
           pend = xr.i;
           TC_T(7, p, c);
         }
-        xr.next(NSX);
+        xr.next(nsx);
       }
       if (st_thr && pend >= 0) {
         asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
@@ -667,9 +670,14 @@ cudaError_t launch_proj_tc32(float* X, int64_t ldx, const float* Qimg, float* L,
   } else {
     map0 = map;
   }
+  // ring sizes (experiments: RBRP_TC_NSX X slots, RBRP_TC_QRING_KB of Q ring)
+  int nsx = tc::NSX, qring = tc::QRING;
+  if (const char* e1 = getenv("RBRP_TC_NSX")) nsx = std::max(2, std::min(tc::NSXMAX, atoi(e1)));
+  if (const char* e2 = getenv("RBRP_TC_QRING_KB")) qring = std::max(16, atoi(e2)) * 1024;
+  if (tc::smem_bytes(nsx, qring) > tc::SMEM_MAX) return cudaErrorInvalidValue;
   static PerDevice attr;
   cudaError_t e = attr.once(
-      [] { return cudaFuncSetAttribute(k_proj_tc32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::SMEM); });
+      [] { return cudaFuncSetAttribute(k_proj_tc32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::SMEM_MAX); });
   long long* tr = nullptr;
   {   // RBRP_TC_TRACE=k (profiling only): cycle trace of the k-th launch of the process
     static long long* buf = nullptr;
@@ -686,8 +694,8 @@ cudaError_t launch_proj_tc32(float* X, int64_t ldx, const float* Qimg, float* L,
   const int nc = (int)((d + tc::KC - 1) / tc::KC);
   int grid = device_sms();
   if (const char* g = getenv("RBRP_TC_GRID")) grid = atoi(g);   // experiments only (L2 working set)
-  k_proj_tc32<<<grid, tc::NTH, tc::SMEM, s>>>(map, map0, X0 ? 1 : 0, Qimg, L, ldl, n, (int)d, nc, st, X, ldx,
-                                                       dvec, part, tr);
+  k_proj_tc32<<<grid, tc::NTH, tc::smem_bytes(nsx, qring), s>>>(map, map0, X0 ? 1 : 0, Qimg, L, ldl, n, (int)d, nc,
+                                                                 st, X, ldx, dvec, part, tr, nsx, qring);
   return cudaGetLastError();
 }
 

@@ -149,18 +149,24 @@ cudaError_t launch_downdate(const T* L, int64_t ldl, int64_t n, double* dvec, De
                             int fused_max, cudaStream_t s);
 bool gemm_nt_mma(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
                  int64_t M, int64_t N, int64_t K, cudaStream_t s, cudaError_t* err);
-// k_lhat_paper.cu: C = A B^T by read-only L-hat passes of 32 columns (B: N x K, ldb == K);
-// scratch >= gemm_lp_scratch_bytes(N, K), 256-byte aligned
+// k_lhat_paper.cu: C = A B^T by read-only L-hat passes of 64 (or 32) columns (B: N x K,
+// ldb == K); scratch >= gemm_lp_scratch_bytes(N, K), 256-byte aligned
 size_t gemm_lp_scratch_bytes(int64_t N, int64_t K);
-// min_k: smallest K for which the pass structure beats k_nt_mma (512 for the W GEMMs of
-// the ID, 256 for OSID's W = Y M whose K = l is larger relative to N = k)
+// min_k: smallest K for which the pass structure beats k_nt_mma (128 for the W GEMMs of
+// the ID since k_lhat64 (no K fold), 256 for OSID's W = Y M)
 bool gemm_lp_supported(const double* A, int64_t lda, const double* B, int64_t ldb, int64_t K,
                        int64_t min_k = 512);
-// lower_b: B(j, m) = 0 for m < j (B = L_1^{-T} of W): each 32-column group starts its K
-// range at the 64-column chunk holding its first nonzero (about half the work)
+// Column groups of 64 (k_lhat64; 32 if A's layout only admits k_lhat_paper).  lower_b:
+// B(j, m) = 0 for m < j (B = L_1^{-T} of W): each group starts its K range at the 64-column
+// chunk holding its first nonzero (about half the work).  nlaunch: + kernels launched
 cudaError_t gemm_nt_lp(const double* A, int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
                        int64_t M, int64_t N, int64_t K, void* scratch, cudaStream_t s, bool lower_b = false,
-                       int64_t min_k = 512);
+                       int64_t min_k = 512, int* nlaunch = nullptr);
+// fp32 storage: 32-column groups on k_lhat_paper<32, float> (fp64 DMMA arithmetic)
+bool gemm_lp_supported(const float* A, int64_t lda, const float* B, int64_t ldb, int64_t K, int64_t min_k = 512);
+cudaError_t gemm_nt_lp(const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
+                       int64_t M, int64_t N, int64_t K, void* scratch, cudaStream_t s, bool lower_b = false,
+                       int64_t min_k = 512, int* nlaunch = nullptr);
 
 // k_formw.cu — Alg. 3 by triangular solve
 template <typename T>

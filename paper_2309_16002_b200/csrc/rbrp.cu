@@ -162,6 +162,15 @@ bool env_on(const char* name) {
 // RBRP_FORCE_SIMT=1: CUDA-core projection kernels instead of DMMA.  RBRP_NO_GRAPH=1: eager
 // block loop.  RBRP_DEBUG_STAMPS=1: print the filter phase stamps of every block (eager).
 bool force_simt() { return env_on("RBRP_FORCE_SIMT"); }
+// smallest K (= k rounded up to 8) for which W = L L_1^{-1} runs as k_lhat64 passes
+// rather than k_nt_mma (measured, scripts/w_bench.py: k = 240: 0.66 vs 0.98 ms, k = 128:
+// 0.22 vs 0.25 ms; RBRP_W_MINK overrides)
+// fp32: any K (the alternative is the CUDA-core tile GEMM)
+template <typename T = double>
+int64_t w_min_k() {
+  const char* e = getenv("RBRP_W_MINK");
+  return e ? atoll(e) : (sizeof(T) == 8 ? 128 : 16);
+}
 // RBRP_HOST_TIMING=1: host microseconds between the marks of one rbrp_id (profiling only)
 struct HostMarks {
   bool on = env_on("RBRP_HOST_TIMING");
@@ -783,12 +792,12 @@ int enqueue_W(Ctx<T>& c, const rbrp_problem* p, rbrp_comm* comm, void* W_out, in
     CK(cudaMemset2DAsync(c.Lm + k, (size_t)k_cap * sizeof(T), 0, (size_t)(kp - k) * sizeof(T), (size_t)c.n, s));
   cudaError_t merr = cudaSuccess;
   ++*nl;
-  if (sizeof(T) == 8 && !force_simt() && kp <= k_cap && c.Wsc && !env_on("RBRP_W_NTMMA") &&
-      gemm_lp_supported((const double*)c.Lm, k_cap, (const double*)LinvT, kp, kp)) {
-    // lower_b: L_1^{-T} has zero chunks to skip; the clipped pinv is dense
-    CK(gemm_nt_lp((const double*)c.Lm, k_cap, (const double*)LinvT, kp, (double*)W_out, k_cap, c.n, k, kp, c.Wsc,
-                  s, !clip));
-    *nl += 2 * (int)((k + 31) / 32);
+  if (!force_simt() && kp <= k_cap && c.Wsc && !env_on("RBRP_W_NTMMA") && !env_on("RBRP_W_SIMT") &&
+      gemm_lp_supported(c.Lm, k_cap, LinvT, kp, kp, w_min_k<T>())) {
+    // lower_b: L_1^{-T} has zero chunks to skip; the clipped pinv is dense.  fp32: the same
+    // passes with fp32 storage and fp64 DMMA arithmetic
+    --*nl;
+    CK(gemm_nt_lp(c.Lm, k_cap, LinvT, kp, (T*)W_out, k_cap, c.n, k, kp, c.Wsc, s, !clip, w_min_k<T>(), nl));
   } else if (sizeof(T) == 8 && !force_simt() && kp <= k_cap &&
              gemm_nt_mma((const double*)c.Lm, k_cap, (const double*)LinvT, kp, (double*)W_out, k_cap, c.n, k, kp, s,
                          &merr)) {
@@ -1366,11 +1375,10 @@ int run_dist(int nsh, const rbrp_problem* ps, void* const* Xs, char* const* wss,
         CK(cudaMemset2DAsync(c.Lm + k, (size_t)k_cap * sizeof(T), 0, (size_t)(kp - k) * sizeof(T), (size_t)c.n, s));
       cudaError_t merr = cudaSuccess;
       ++nl;
-      if (sizeof(T) == 8 && !force_simt() && kp <= k_cap && c.Wsc && !env_on("RBRP_W_NTMMA") &&
-          gemm_lp_supported((const double*)c.Lm, k_cap, (const double*)c.LinvT, kp, kp)) {
-        CK(gemm_nt_lp((const double*)c.Lm, k_cap, (const double*)c.LinvT, kp, (double*)W_outs[h], k_cap, c.n, k,
-                      kp, c.Wsc, s, !clip));
-        nl += 2 * (int)((k + 31) / 32);
+      if (!force_simt() && kp <= k_cap && c.Wsc && !env_on("RBRP_W_NTMMA") && !env_on("RBRP_W_SIMT") &&
+          gemm_lp_supported(c.Lm, k_cap, c.LinvT, kp, kp, w_min_k<T>())) {
+        --nl;
+        CK(gemm_nt_lp(c.Lm, k_cap, c.LinvT, kp, (T*)W_outs[h], k_cap, c.n, k, kp, c.Wsc, s, !clip, w_min_k<T>(), &nl));
       } else if (sizeof(T) == 8 && !force_simt() && kp <= k_cap &&
                  gemm_nt_mma((const double*)c.Lm, k_cap, (const double*)c.LinvT, kp, (double*)W_outs[h], k_cap,
                              c.n, k, kp, s, &merr)) {
@@ -1445,7 +1453,7 @@ int run_dist(int nsh, const rbrp_problem* ps, void* const* Xs, char* const* wss,
 
 namespace {
 struct FwLayout {
-  size_t L1, LinvT, Pinv, S, diag, nclip, total;
+  size_t L1, LinvT, Pinv, S, diag, nclip, Wsc, total;
 };
 FwLayout fw_layout(rbrp_dtype dtype, int64_t k) {
   FwLayout f;
@@ -1463,6 +1471,7 @@ FwLayout fw_layout(rbrp_dtype dtype, int64_t k) {
   f.S = take((size_t)k * 8);
   f.diag = take(16);
   f.nclip = take(8);
+  f.Wsc = take(gemm_lp_scratch_bytes(k, kp));
   f.total = off;
   return f;
 }
@@ -1493,7 +1502,17 @@ int form_w_run(const T* L, int64_t ldl, int64_t n, const int64_t* S, int64_t k, 
   } else {
     CK(launch_trinv<T>(L1, k, LinvT, kp, nullptr, s));
   }
-  CK(launch_gemm_nt<T>(L, ldl, LinvT, kp, W, ldw, n, k, k, s));
+  // the ID's W GEMM (k_lhat64 / k_lhat_paper passes, or k_nt_mma for small fp64 k) when L's
+  // rows can be read as k = kp columns (k % 8 == 0), else the CUDA-core tile GEMM
+  cudaError_t merr = cudaSuccess;
+  if (k == kp && !force_simt() && gemm_lp_supported(L, ldl, (const T*)LinvT, kp, kp, w_min_k<T>())) {
+    CK(gemm_nt_lp(L, ldl, (const T*)LinvT, kp, W, ldw, n, k, kp, ws + f.Wsc, s, !clip, w_min_k<T>()));
+  } else if (sizeof(T) == 8 && k == kp && !force_simt() &&
+             gemm_nt_mma((const double*)L, ldl, (const double*)LinvT, kp, (double*)W, ldw, n, k, kp, s, &merr)) {
+    CK(merr);
+  } else {
+    CK(launch_gemm_nt<T>(L, ldl, LinvT, kp, W, ldw, n, k, k, s));
+  }
   CK(launch_w_identity<T>(W, ldw, Sd, k, n, 0, s));
   int hn = 0;
   CK(cudaMemcpyAsync(&hn, ncl, 4, cudaMemcpyDeviceToHost, s));
