@@ -58,7 +58,8 @@ constexpr int QRING = 96 * 1024;          // Q ring bytes (default; RBRP_TC_QRIN
 constexpr int NSQMAX = 24;
 constexpr int NROWW = 8;                  // row warps
 constexpr int W_XP = 0, W_MMA = 1, W_QP = 2, W_ROW0 = 3;
-constexpr int NTH = (W_ROW0 + NROWW) * 32;
+constexpr int W_ST = W_ROW0 + NROWW;      // pass-2 TMA store issuer
+constexpr int NTH = (W_ST + 1) * 32;
 constexpr int NACC2 = 4;
 // TMEM columns (512 allocated)
 constexpr uint32_t T_ACC1 = 0;     // D1: 2 N1 <= 128 columns
@@ -218,7 +219,7 @@ __global__ void __launch_bounds__(tc::NTH, 1)
     k_proj_tc32(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap xmap0, int lazy,
                 const float* __restrict__ Qimg, float* __restrict__ L, int64_t ldl, int64_t n, int d, int nc,
                 DevState* st, float* __restrict__ Xr, int64_t ldx, double* __restrict__ dvec, int part,
-                long long* __restrict__ tr, int nsx, int qring) {
+                long long* __restrict__ tr, int nsx, int qring, int keep_from) {
   using namespace tc;
   // optional cycle trace of CTA 0, tiles 0-1 (RBRP_TC_TRACE=1; profiling only):
   // tr[(event * 2 + tile) * 128 + step]
@@ -263,7 +264,8 @@ __global__ void __launch_bounds__(tc::NTH, 1)
   uint64_t* a2empty = a2full + NACC2;
   uint64_t* a1full = a2empty + NACC2;
   uint64_t* lafull = a1full + 1;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(lafull + 1);
+  uint64_t* xdone = lafull + 1;   // [NSXMAX] pass 2: the row warps have written the slot
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(xdone + NSXMAX);
 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int64_t ntiles = (n + M - 1) / M;
@@ -291,6 +293,7 @@ __global__ void __launch_bounds__(tc::NTH, 1)
     }
     tc_bar_init(tc_su32(a1full), 1);
     tc_bar_init(tc_su32(lafull), NROWW);
+    for (int s = 0; s < nsx; ++s) tc_bar_init(tc_su32(&xdone[s]), NROWW);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (w == W_MMA) {   // the whole warp allocates all 512 TMEM columns (one CTA per SM)
@@ -312,8 +315,7 @@ __global__ void __launch_bounds__(tc::NTH, 1)
       uint64_t pol_keep, pol_drop;
       // pass-1 chunks below keep_from (the oldest, re-read last in the reversed pass 2) are
       // not marked evict_last: with 148 x 1 MB tiles in flight the L2 cannot hold them all,
-      // so it keeps the newer ones (TC_KEEP_FRAC, compile time)
-      const int keep_from = (int)(nc * (1.0 - TC_KEEP_FRAC));
+      // so it keeps the newer ones (keep_from: host, launch_proj_tc32)
       asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol_keep));
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol_drop));
       TcRing xr;
@@ -356,6 +358,46 @@ __global__ void __launch_bounds__(tc::NTH, 1)
             : "memory");
         qr.next(NSQ);
       }
+    }
+  } else if (w == W_ST) {
+    if (lane == 0) {
+      // pass-2 stores: once the 8 row warps have written chunk c's residual into its X slot
+      // (xdone), one TMA bulk tensor store per chunk; the slot is released to the X producer
+      // when the store has read it.  The row warps never wait for a store.
+      uint64_t pol_st;
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol_st));
+      TcRing xr;
+      uint32_t dph = 0;   // per-slot parity of xdone
+      int pend = -1;
+      for (int s = 0; s < steps; ++s) {
+        const int p = s / (2 * nc), in = s % (2 * nc);
+        if (in >= nc) {
+          const int c = in - nc;
+          tc_wait(tc_su32(&xdone[xr.i]), (dph >> xr.i) & 1u);
+          dph ^= 1u << xr.i;
+          const int col = (nc - 1 - c) * KC;   // reverse chunk order (see the X producer)
+          asm volatile(
+              "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2}], [%3], %4;\n" ::"l"(
+                  &xmap),
+              "r"(col), "r"((int)row0_of(p)), "r"(tc_su32(xs + (size_t)xr.i * XSLOT)), "l"(pol_st)
+              : "memory");
+          asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+          if (pend >= 0) {
+            asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+            tc_arrive_n(tc_su32(&xempty[pend]), NROWW);
+          }
+          pend = xr.i;
+          TC_T(7, p, c);
+          if (c == nc - 1) {   // tile end: release the last slot now (the producer reuses it
+            // for the next tile's pass 1, before any further pass-2 store of this warp)
+            asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+            tc_arrive_n(tc_su32(&xempty[pend]), NROWW);
+            pend = -1;
+          }
+        }
+        xr.next(nsx);
+      }
+      asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");   // stores complete
     }
   } else if (w == W_MMA) {
     {   // the whole warp runs the issue loop (uniform control flow); one elected lane issues
@@ -491,14 +533,10 @@ __global__ void __launch_bounds__(tc::NTH, 1)
           default: tc_store_row<3>(dst, P, cnt); break;
         }
       }
-      // ---- pass 2: x_res = x - D2, written back into the X slot and stored by one TMA bulk
-      // tensor store per chunk (full 128-byte lines; the slot is released once the store has
-      // read it); fp64 norms of the stored values
-      double nr = 0.0;
-      const bool st_thr = (w == W_ROW0 && lane == 0);
-      int pend = -1;   // st_thr: X slot of the outstanding store
-      uint64_t pol_st = 0;
-      if (st_thr) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol_st));
+      // ---- pass 2: x_res = x - D2, written back into the X slot and stored by the store warp
+      // (one TMA bulk tensor store per chunk, full 128-byte lines); fp64 norms of the stored
+      // values in four independent accumulators
+      double nq[4] = {0.0, 0.0, 0.0, 0.0};
       for (int c = 0; c < nc; ++c) {
         tc_wait(tc_su32(&a2full[cr.i]), cr.ph);
         tc_fence_after();
@@ -522,35 +560,18 @@ __global__ void __launch_bounds__(tc::NTH, 1)
           o.y = xv.y - a[4 * i + 1];
           o.z = xv.z - a[4 * i + 2];
           o.w = xv.w - a[4 * i + 3];
-          nr = fma((double)o.x, (double)o.x, nr);
-          nr = fma((double)o.y, (double)o.y, nr);
-          nr = fma((double)o.z, (double)o.z, nr);
-          nr = fma((double)o.w, (double)o.w, nr);
+          nq[i] = fma((double)o.x, (double)o.x, nq[i]);
+          nq[i] = fma((double)o.y, (double)o.y, nq[i]);
+          nq[i] = fma((double)o.z, (double)o.z, nq[i]);
+          nq[i] = fma((double)o.w, (double)o.w, nq[i]);
           tc_sts4(ad, o);
         }
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // visible to the TMA store
-        tc_rowbar();
-        if (st_thr) {
-          const int col = (nc - 1 - c) * KC;   // reverse chunk order (see the X producer)
-          asm volatile(
-              "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2}], [%3], %4;\n" ::"l"(
-                  &xmap),
-              "r"(col), "r"((int)row0_of(p)), "r"(xsl), "l"(pol_st)
-              : "memory");
-          asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
-          if (pend >= 0) {
-            asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
-            tc_arrive_n(tc_su32(&xempty[pend]), NROWW);
-          }
-          pend = xr.i;
-          TC_T(7, p, c);
-        }
+        __syncwarp();
+        if (lane == 0) tc_arrive(tc_su32(&xdone[xr.i]));
         xr.next(nsx);
       }
-      if (st_thr && pend >= 0) {
-        asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
-        tc_arrive_n(tc_su32(&xempty[pend]), NROWW);
-      }
+      const double nr = (nq[0] + nq[1]) + (nq[2] + nq[3]);
       // d(i) = ||x_res,i||^2: the two column halves summed in a fixed order
       double* nb = nrm + (size_t)(p & 1) * 2 * M;
       nb[h * M + r] = nr;
@@ -558,7 +579,6 @@ __global__ void __launch_bounds__(tc::NTH, 1)
       if (h == 0 && vr) dvec[row] = nb[r] + nb[M + r];
     }
   }
-  if (w == W_ROW0 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");   // stores complete
   tc_fence_before();
   __syncthreads();
   if (w == W_MMA) {
@@ -692,10 +712,16 @@ cudaError_t launch_proj_tc32(float* X, int64_t ldx, const float* Qimg, float* L,
   }
   if (e != cudaSuccess) return e;
   const int nc = (int)((d + tc::KC - 1) / tc::KC);
+  // pass-1 chunks [0, keep_from) are loaded evict_first: when the 148 tiles in flight
+  // (128 x d x 4 bytes each) exceed about half the L2, the oldest quarter is let go
+  // (RBRP_TC_KEEP = fraction kept, experiments)
+  double keep = (double)device_sms() * tc::M * d * 4 > 64e6 ? TC_KEEP_FRAC : 1.0;
+  if (const char* e3 = getenv("RBRP_TC_KEEP")) keep = atof(e3);
+  const int keep_from = (int)(nc * (1.0 - keep));
   int grid = device_sms();
   if (const char* g = getenv("RBRP_TC_GRID")) grid = atoi(g);   // experiments only (L2 working set)
   k_proj_tc32<<<grid, tc::NTH, tc::smem_bytes(nsx, qring), s>>>(map, map0, X0 ? 1 : 0, Qimg, L, ldl, n, (int)d, nc,
-                                                                 st, X, ldx, dvec, part, tr, nsx, qring);
+                                                                 st, X, ldx, dvec, part, tr, nsx, qring, keep_from);
   return cudaGetLastError();
 }
 

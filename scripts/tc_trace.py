@@ -39,4 +39,16 @@ for p in range(2):
             row.append(f"{(v - t0) if v else -1:7d}")
         print(f" s{s:3d} " + " ".join(row))
 print("cols:", names)
+# per-step intervals over tile 1 (steady state): median cycles between consecutive steps
+for e, nm in enumerate(names):
+    rng = range(0, 2 * nc) if e in (0, 1, 8) else range(0, nc)
+    v = np.array([t[e, 1, i] for i in rng if i < 128])
+    v = v[v > 0]
+    if len(v) > 2:
+        dv = np.diff(v)
+        print(f"{nm:12s} median step {int(np.median(dv)):6d} cyc  mean {int(dv.mean()):6d}  (n={len(dv)})")
+# tile 1 length and phases
+p1 = t[2, 1, 0], t[4, 1, nc - 1], t[5, 1, 0], t[7, 1, nc - 1]
+print("tile1 pass1 start->end", p1[1] - p1[0], " pass1 end->pass2 first a2full", p1[2] - p1[1],
+      " pass2", p1[3] - p1[2], " total", p1[3] - p1[0])
 print("k", r.k, r.b_prime, r.proj_ms_blk)
