@@ -121,15 +121,17 @@ inline int device_sms() {
 inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
 // b' > pw projected in parts (Q_b's rows are orthonormal, so the parts in sequence equal one
-// projection up to rounding): np = ceil(b'/pw) balanced parts, part p = rows [r0, r0 + cnt)
-// of Q_b; pw = the widest projection kernel (64 for fp64, 32 for the fp32 DMMA fallback).
-// Returns false if part p does not exist for this b'.
+// projection up to rounding): full parts of pw rows of Q_b, then the remainder, part p = rows
+// [r0, r0 + cnt) = [p pw, min((p + 1) pw, b')); pw = the widest projection kernel (64 for
+// fp64, 32 for the fp32 DMMA fallback).  The remainder runs on the kernel of its own bucket
+// (a 31-column remainder on the 32-column kernel: balanced parts of 48 would leave a quarter
+// of the 64-column kernel's warps idle).  Returns false if part p does not exist for this b'.
 __host__ __device__ inline bool part_range(int bpa, int part, int* r0, int* cnt, int pw = 32) {
   if (bpa <= pw) return false;
   const int np = (bpa + pw - 1) / pw;
   if (part >= np) return false;
-  *r0 = part * bpa / np;
-  *cnt = (part + 1) * bpa / np - *r0;
+  *r0 = part * pw;
+  *cnt = bpa - *r0 < pw ? bpa - *r0 : pw;
   return true;
 }
 

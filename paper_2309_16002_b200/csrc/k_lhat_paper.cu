@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(lp::NTH, 1)
                  int lazy, const double* __restrict__ Qp,
                  E* __restrict__ L, int64_t ldl, int64_t n, int d, int nc, int NS, int NQ,
                  double* __restrict__ dvec, DevState* st, E* __restrict__ Xr, int64_t ldx, int resid,
-                 long long* __restrict__ tr, int part) {
+                 long long* __restrict__ tr, int part, int pw) {
   using Cf = LpCfg<BPB, E>;
   using LE = LpE<E>;
   constexpr int CPB = LE::CPB, NBOX = lp::KC / CPB, BOXE = lp::R * CPB;
@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(lp::NTH, 1)
     k0 = st->k;
   } else {
     int r0;
-    if (!part_range(st->b_prime, part, &r0, &bp, BPB)) return;
+    if (!part_range(st->b_prime, part, &r0, &bp, pw) || bucket_of(bp) != BPB) return;
     k0 = st->k + r0;
   }
   // DMMA work only for the 8-column groups that hold a column of Q_b (warp-uniform)
@@ -554,7 +554,7 @@ __global__ void __launch_bounds__(lp::NTH, 1)
     k_lhat64(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap xmap0, int lazy,
              const double* __restrict__ Qp, double* __restrict__ L, int64_t ldl, int64_t n, int d, int nc,
              int NS, int NQ, double* __restrict__ dvec, DevState* st, double* __restrict__ Xr, int64_t ldx,
-             int resid, int part) {
+             int resid, int part, int pw) {
   using LE = LpE<double>;
   constexpr int CPB = LE::CPB, NBOX = lp::KC / CPB, BOXE = lp::R * CPB;
   using namespace lp;
@@ -568,7 +568,7 @@ __global__ void __launch_bounds__(lp::NTH, 1)
     k0 = st->k;
   } else {
     int r0;
-    if (!part_range(st->b_prime, part, &r0, &bp, lp64::BPB)) return;
+    if (!part_range(st->b_prime, part, &r0, &bp, pw) || bucket_of(bp) != lp64::BPB) return;
     k0 = st->k + r0;
   }
   const int ntr = (bp + 7) >> 3;   // 8-row groups of Q_b that hold a row (<= 8)
@@ -890,7 +890,7 @@ int lhat_paper_max_bucket_f32(const void* X, int64_t ldx, int64_t d) {
 template <int BPB, typename E>
 static cudaError_t go_lp(const CUtensorMap& map, const CUtensorMap& map0, int lazy, const double* Qp, E* L,
                          int64_t ldl, int64_t n, int64_t d, double* dvec, DevState* st, E* Xr, int64_t ldx,
-                         int resid, cudaStream_t s, int part) {
+                         int resid, cudaStream_t s, int part, int pw) {
   using Cf = LpCfg<BPB, E>;
   int ns, nq;
   if (!Cf::rings(ns, nq)) return cudaErrorInvalidValue;
@@ -904,13 +904,13 @@ static cudaError_t go_lp(const CUtensorMap& map, const CUtensorMap& map0, int la
     traced = 1;
   }
   k_lhat_paper<BPB, E><<<lp_sms(), lp::NTH, smem, s>>>(map, map0, lazy, Qp, L, ldl, n, (int)d, nc, ns, nq, dvec,
-                                                        st, Xr, ldx, resid, tr, part);
+                                                        st, Xr, ldx, resid, tr, part, pw);
   return cudaGetLastError();
 }
 
 static cudaError_t go_lp64(const CUtensorMap& map, const CUtensorMap& map0, int lazy, const double* Qp, double* L,
                            int64_t ldl, int64_t n, int64_t d, double* dvec, DevState* st, double* Xr, int64_t ldx,
-                           int resid, cudaStream_t s, int part) {
+                           int resid, cudaStream_t s, int part, int pw) {
   const int ns = 3, nq = 2;
   const size_t smem = lp64::smem(ns, nq);
   static PerDevice attr;
@@ -920,15 +920,16 @@ static cudaError_t go_lp64(const CUtensorMap& map, const CUtensorMap& map0, int 
   if (ae != cudaSuccess) return ae;
   const int nc = (int)((d + lp::KC - 1) / lp::KC);
   k_lhat64<<<lp_sms(), lp::NTH, smem, s>>>(map, map0, lazy, Qp, L, ldl, n, (int)d, nc, ns, nq, dvec, st, Xr, ldx,
-                                            resid, part);
+                                            resid, part, pw);
   return cudaGetLastError();
 }
 
 template <typename E>
 static cudaError_t launch_lhat_paper_t(const E* X, int64_t ldx, const double* Qp, E* L, int64_t ldl, int64_t n,
                                        int64_t d, double* dvec, DevState* st, int bucket, bool resid,
-                                       cudaStream_t s, const E* X0, int64_t ldx0, int part) {
+                                       cudaStream_t s, const E* X0, int64_t ldx0, int part, int pw) {
   if (n <= 0) return cudaSuccess;
+  if (pw <= 0) pw = bucket;
   auto enc = lp_encode();
   if (!enc) return cudaErrorNotSupported;
   auto make_map = [&](const E* P, int64_t ld, CUtensorMap* map) {
@@ -945,24 +946,25 @@ static cudaError_t launch_lhat_paper_t(const E* X, int64_t ldx, const double* Qp
   const int lazy = X0 != nullptr ? 1 : 0;
   if (!make_map(lazy ? X0 : X, lazy ? ldx0 : ldx, &map0)) return cudaErrorInvalidValue;
   switch (bucket) {
-    case 16: return go_lp<16, E>(map, map0, lazy, Qp, L, ldl, n, d, dvec, st, (E*)X, ldx, resid ? 1 : 0, s, -1);
-    case 32: return go_lp<32, E>(map, map0, lazy, Qp, L, ldl, n, d, dvec, st, (E*)X, ldx, resid ? 1 : 0, s, part);
+    case 16: return go_lp<16, E>(map, map0, lazy, Qp, L, ldl, n, d, dvec, st, (E*)X, ldx, resid ? 1 : 0, s, part, pw);
+    case 32: return go_lp<32, E>(map, map0, lazy, Qp, L, ldl, n, d, dvec, st, (E*)X, ldx, resid ? 1 : 0, s, part, pw);
     case 64:
       if (sizeof(E) != 8) return cudaErrorInvalidValue;
-      return go_lp64(map, map0, lazy, Qp, (double*)L, ldl, n, d, dvec, st, (double*)X, ldx, resid ? 1 : 0, s, part);
+      return go_lp64(map, map0, lazy, Qp, (double*)L, ldl, n, d, dvec, st, (double*)X, ldx, resid ? 1 : 0, s, part,
+                     pw);
     default: return cudaErrorInvalidValue;
   }
 }
 
 cudaError_t launch_lhat_paper(const double* X, int64_t ldx, const double* Qp, double* L, int64_t ldl,
                               int64_t n, int64_t d, double* dvec, DevState* st, int bucket, bool resid,
-                              cudaStream_t s, const double* X0, int64_t ldx0, int part) {
-  return launch_lhat_paper_t<double>(X, ldx, Qp, L, ldl, n, d, dvec, st, bucket, resid, s, X0, ldx0, part);
+                              cudaStream_t s, const double* X0, int64_t ldx0, int part, int pw) {
+  return launch_lhat_paper_t<double>(X, ldx, Qp, L, ldl, n, d, dvec, st, bucket, resid, s, X0, ldx0, part, pw);
 }
 cudaError_t launch_lhat_paper(const float* X, int64_t ldx, const double* Qp, float* L, int64_t ldl,
                               int64_t n, int64_t d, double* dvec, DevState* st, int bucket, bool resid,
-                              cudaStream_t s, const float* X0, int64_t ldx0, int part) {
-  return launch_lhat_paper_t<float>(X, ldx, Qp, L, ldl, n, d, dvec, st, bucket, resid, s, X0, ldx0, part);
+                              cudaStream_t s, const float* X0, int64_t ldx0, int part, int pw) {
+  return launch_lhat_paper_t<float>(X, ldx, Qp, L, ldl, n, d, dvec, st, bucket, resid, s, X0, ldx0, part, pw);
 }
 
 // ------------------------------------------------------------------------------------

@@ -112,16 +112,18 @@ cudaError_t launch_pack_q(const float* Qt, int64_t d, double* Qp, DevState* st, 
 
 // k_lhat_paper.cu — paper form, l.13 + l.16: read-only DMMA pass with 64-row tiles.
 // bucket 16 / 32: k_lhat_paper (K-split warps); bucket 64 (fp64): k_lhat64 (N-split warps,
-// L-hat tile shared through shared memory).  part >= 0: the rows part_range(b', part,
-// bucket) of Q_b (b' > bucket)
+// L-hat tile shared through shared memory).  part >= 0: the rows part_range(b', part, pw) of
+// Q_b (b' > pw, pw = 0: the bucket), run only if their count falls in this bucket
 int lhat_paper_max_bucket(const void* X, int64_t ldx, int64_t d);
 cudaError_t launch_lhat_paper(const double* X, int64_t ldx, const double* Qp, double* L, int64_t ldl,
                               int64_t n, int64_t d, double* dvec, DevState* st, int bucket, bool resid,
-                              cudaStream_t s, const double* X0 = nullptr, int64_t ldx0 = 0, int part = -1);
+                              cudaStream_t s, const double* X0 = nullptr, int64_t ldx0 = 0, int part = -1,
+                              int pw = 0);
 // fp32 storage (X, X_res, L), fp64 DMMA arithmetic, fp64 norms (R19)
 cudaError_t launch_lhat_paper(const float* X, int64_t ldx, const double* Qp, float* L, int64_t ldl,
                               int64_t n, int64_t d, double* dvec, DevState* st, int bucket, bool resid,
-                              cudaStream_t s, const float* X0 = nullptr, int64_t ldx0 = 0, int part = -1);
+                              cudaStream_t s, const float* X0 = nullptr, int64_t ldx0 = 0, int part = -1,
+                              int pw = 0);
 int lhat_paper_max_bucket_f32(const void* X, int64_t ldx, int64_t d);
 // resid: + the update pass (residual form, L2 re-read).  X0 (lazy X_res): in block 1 the
 // tile is read from X0 (the input) and the update is written to X (X_res)

@@ -425,11 +425,16 @@ int enqueue_projection(Ctx<T>& c, cudaStream_t s, int* nl) {
     }
     if (rc) return rc;
   }
-  for (int part = 0; parts && part < (c.bucketB + c.lp_max - 1) / c.lp_max; ++part) {
+  // full parts of lp_max columns, then the remainder on the kernel of its bucket (every bucket
+  // kernel is enqueued for every part; all but one exit at once)
+  const int nparts = parts ? (c.bucketB + c.lp_max - 1) / c.lp_max : 0;
+  for (int part = 0; part < nparts; ++part) {
     if ((rc = lk(launch_pack_q(c.Qt, c.d, c.Qp, c.st, s, part, 0, c.lp_max)))) return rc;
-    if ((rc = lk(launch_lhat_paper((const T*)c.Xres, c.ldr, c.Qp, c.Lm, c.k_cap, c.n, c.d, c.dvec, c.st, c.lp_max,
-                                   !c.paper, s, c.lazy ? (const T*)c.X : nullptr, c.p->ld, part))))
-      return rc;
+    for (int bk = 16; bk <= c.lp_max; bk *= 2) {
+      if ((rc = lk(launch_lhat_paper((const T*)c.Xres, c.ldr, c.Qp, c.Lm, c.k_cap, c.n, c.d, c.dvec, c.st, bk,
+                                     !c.paper, s, c.lazy ? (const T*)c.X : nullptr, c.p->ld, part, c.lp_max))))
+        return rc;
+    }
   }
   // paper form on the two-kernel path: l.16 downdate from the L-hat columns (the kernel
   // skips blocks whose bucket the fused kernel handled, which downdates in its epilogue)
