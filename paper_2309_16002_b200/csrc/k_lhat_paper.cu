@@ -554,7 +554,7 @@ __global__ void __launch_bounds__(lp::NTH, 1)
     k_lhat64(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap xmap0, int lazy,
              const double* __restrict__ Qp, double* __restrict__ L, int64_t ldl, int64_t n, int d, int nc,
              int NS, int NQ, double* __restrict__ dvec, DevState* st, double* __restrict__ Xr, int64_t ldx,
-             int resid, int part, int pw) {
+             int resid, int part, int pw, int bkt) {
   using LE = LpE<double>;
   constexpr int CPB = LE::CPB, NBOX = lp::KC / CPB, BOXE = lp::R * CPB;
   using namespace lp;
@@ -564,11 +564,11 @@ __global__ void __launch_bounds__(lp::NTH, 1)
   int64_t k0;
   if (part < 0) {
     bp = st->b_prime;
-    if (bp <= 0 || bucket_of(bp) != lp64::BPB) return;
+    if (bp <= 0 || bucket_of(bp) != bkt) return;
     k0 = st->k;
   } else {
     int r0;
-    if (!part_range(st->b_prime, part, &r0, &bp, pw) || bucket_of(bp) != lp64::BPB) return;
+    if (!part_range(st->b_prime, part, &r0, &bp, pw) || bucket_of(bp) != bkt) return;
     k0 = st->k + r0;
   }
   const int ntr = (bp + 7) >> 3;   // 8-row groups of Q_b that hold a row (<= 8)
@@ -680,19 +680,49 @@ __global__ void __launch_bounds__(lp::NTH, 1)
       qf[t] = (8 * (qj[t] & 1)) ^ (4 * ((qj[t] >> 1) & 3));
     }
     const bool on0 = 2 * cw < ntr, on1 = 2 * cw + 1 < ntr;   // warp-uniform
+    // L-hat pass work split.  v1 (ntr >= 7): warp (rp, cw) = 2 row groups x the 2 column
+    // tiles 2 cw, 2 cw + 1.  v2 (ntr <= 6, where v1 would idle the cw = 3 warps): warp
+    // (rg, cg) = 1 row group (8 rows) x column tiles [tb, tb + tn) of a 2-way split of the ntr
+    // tiles (at most 3 per warp instead of 4)
+    const bool v2 = ntr <= 6;
+    const int rg = w >> 1, cg = w & 1, T0 = (ntr + 1) >> 1;
+    const int tb = cg ? T0 : 0, tn = cg ? ntr - T0 : T0;   // warp-uniform, tn <= 3
+    const int rr = 8 * rg + pg;                          // v2: this lane's tile row
+    int qj2[3], qf2[3];
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      qj2[t] = 8 * (tb + t) + g;
+      qf2[t] = (8 * (qj2[t] & 1)) ^ (4 * ((qj2[t] >> 1) & 3));
+    }
     LpRing qr, xr;
     for (int p = 0; p < T; ++p) {
-      double2 acc[2][NT];
+      double2 acc[2][NT], acc2[3];
 #pragma unroll
       for (int r = 0; r < 2; ++r)
 #pragma unroll
         for (int t = 0; t < NT; ++t) acc[r][t] = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int t = 0; t < 3; ++t) acc2[t] = make_double2(0.0, 0.0);
       for (int c = 0; c < nc; ++c) {
         lp_waits(qf_s + 8 * qr.i, qr.ph);
         lp_waits(xf_s + 8 * xr.i, xr.ph);
         const uint32_t xsl = xs_s + xr.i * (SLOT * 8);
         const uint32_t Qs = qs_s + qr.i * (lp64::QSTAGE * 8);
-        if (on0) {
+        if (v2) {
+#pragma unroll
+          for (int h = 0; h < 8; ++h) {
+            const int cu = 4 * (h & 1) + q, bo = (h >> 1) * 1024;
+            const double2 a = lp_lds2s(xsl + 8 * (bo + 16 * rr + ((cu ^ pg) * 2)));
+#pragma unroll
+            for (int t = 0; t < 3; ++t) {
+              if (t < tn) {
+                const double2 b = lp_lds2s(Qs + 8 * (qj2[t] * KC + ((8 * h + 2 * q) ^ qf2[t])));
+                lp_dmma(acc2[t], a.x, b.x);
+                lp_dmma(acc2[t], a.y, b.y);
+              }
+            }
+          }
+        } else if (on0) {
 #pragma unroll
           for (int h = 0; h < 8; ++h) {
             const int cu = 4 * (h & 1) + q, bo = (h >> 1) * 1024;
@@ -718,44 +748,71 @@ __global__ void __launch_bounds__(lp::NTH, 1)
       }
       // tile end: L-hat to L; -L-hat into P_s (residual form) or the l.16 downdate (paper)
       const int64_t r0 = row0_of(p);
-      double ss[2] = {0.0, 0.0};
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const int trow = r ? rb : ra;
+      auto put = [&](int trow, int j, double vx, double vy) {   // columns j, j + 1 of row trow
         const int64_t row = r0 + trow;
+        if (row < n) {
+          if (j < bp) L[row * ldl + k0 + j] = vx;
+          if (j + 1 < bp) L[row * ldl + k0 + j + 1] = vy;
+        }
+        if (resid) {
+          const int u = j >> 1;   // 16-byte unit (columns 2u, 2u + 1)
+          double* dst = ps + trow * lp64::BPB + 2 * (u ^ (trow & 7));
+          dst[0] = -vx;
+          dst[1] = -vy;
+        }
+      };
+      double ss[2] = {0.0, 0.0};
+      if (v2) {
 #pragma unroll
-        for (int t = 0; t < NT; ++t) {
-          if (!(t ? on1 : on0)) continue;
-          const double vx = acc[r][t].x, vy = acc[r][t].y;
-          const int j = 16 * cw + 8 * t + 2 * q;
-          if (row < n) {
-            if (j < bp) L[row * ldl + k0 + j] = vx;
-            if (j + 1 < bp) L[row * ldl + k0 + j + 1] = vy;
+        for (int t = 0; t < 3; ++t) {
+          if (t < tn) {
+            const double vx = acc2[t].x, vy = acc2[t].y;
+            put(rr, 8 * (tb + t) + 2 * q, vx, vy);
+            ss[0] += vx * vx + vy * vy;
           }
-          ss[r] += vx * vx + vy * vy;
-          if (resid) {
-            const int u = 8 * cw + 4 * t + q;   // 16-byte unit (columns 2u, 2u + 1)
-            double* dst = ps + trow * lp64::BPB + 2 * (u ^ sw);
-            dst[0] = -vx;
-            dst[1] = -vy;
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+#pragma unroll
+          for (int t = 0; t < NT; ++t) {
+            if (!(t ? on1 : on0)) continue;
+            const double vx = acc[r][t].x, vy = acc[r][t].y;
+            put(r ? rb : ra, 16 * cw + 8 * t + 2 * q, vx, vy);
+            ss[r] += vx * vx + vy * vy;
           }
         }
       }
       double* nb = nrm + (size_t)((p & 1) * NRP + rp) * NCW * 16;
       if (!resid) {
-        // l.16 downdate (paper form): sum over the row's columns, q lanes then cw in order
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-          double v = ss[r];
+        // l.16 downdate (paper form): sum over the row's columns, q lanes then the column
+        // groups in order
+        if (v2) {
+          double* nb2 = nrm + (size_t)(p & 1) * NRP * NCW * 16 + rg * 16;   // [rg][cg][8]
+          double v = ss[0];
           v += __shfl_xor_sync(0xffffffffu, v, 1);
           v += __shfl_xor_sync(0xffffffffu, v, 2);
-          if (q == 0) nb[cw * 16 + 8 * r + pg] = v;
-        }
-        lp_bar();
-        if (cw == 0 && lane < 16 && dvec) {
-          const double v = (nb[lane] + nb[16 + lane]) + (nb[32 + lane] + nb[48 + lane]);
-          const int64_t row = r0 + 16 * rp + lane;
-          if (row < n) dvec[row] = fmax(dvec[row] - v, 0.0);
+          if (q == 0) nb2[cg * 8 + pg] = v;
+          lp_bar();
+          if (cg == 0 && lane < 8 && dvec) {
+            const double vv = nb2[lane] + nb2[8 + lane];
+            const int64_t row = r0 + 8 * rg + lane;
+            if (row < n) dvec[row] = fmax(dvec[row] - vv, 0.0);
+          }
+        } else {
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            double v = ss[r];
+            v += __shfl_xor_sync(0xffffffffu, v, 1);
+            v += __shfl_xor_sync(0xffffffffu, v, 2);
+            if (q == 0) nb[cw * 16 + 8 * r + pg] = v;
+          }
+          lp_bar();
+          if (cw == 0 && lane < 16 && dvec) {
+            const double v = (nb[lane] + nb[16 + lane]) + (nb[32 + lane] + nb[48 + lane]);
+            const int64_t row = r0 + 16 * rp + lane;
+            if (row < n) dvec[row] = fmax(dvec[row] - v, 0.0);
+          }
         }
       } else {
         lp_bar();   // P_s complete
@@ -908,9 +965,16 @@ static cudaError_t go_lp(const CUtensorMap& map, const CUtensorMap& map0, int la
   return cudaGetLastError();
 }
 
+// RBRP_LP64_ALL=1 (experiment): b' <= 32 on k_lhat64 as well.  Measured slower on c2
+// (b' = 31: 0.36 vs 0.32 ms per block): the K-split warps of k_lhat_paper<32> stay the default.
+static bool lp64_all() {
+  const char* e = getenv("RBRP_LP64_ALL");
+  return e && e[0] == '1';
+}
+
 static cudaError_t go_lp64(const CUtensorMap& map, const CUtensorMap& map0, int lazy, const double* Qp, double* L,
                            int64_t ldl, int64_t n, int64_t d, double* dvec, DevState* st, double* Xr, int64_t ldx,
-                           int resid, cudaStream_t s, int part, int pw) {
+                           int resid, cudaStream_t s, int part, int pw, int bkt) {
   const int ns = 3, nq = 2;
   const size_t smem = lp64::smem(ns, nq);
   static PerDevice attr;
@@ -920,7 +984,7 @@ static cudaError_t go_lp64(const CUtensorMap& map, const CUtensorMap& map0, int 
   if (ae != cudaSuccess) return ae;
   const int nc = (int)((d + lp::KC - 1) / lp::KC);
   k_lhat64<<<lp_sms(), lp::NTH, smem, s>>>(map, map0, lazy, Qp, L, ldl, n, (int)d, nc, ns, nq, dvec, st, Xr, ldx,
-                                            resid, part, pw);
+                                            resid, part, pw, bkt);
   return cudaGetLastError();
 }
 
@@ -946,12 +1010,19 @@ static cudaError_t launch_lhat_paper_t(const E* X, int64_t ldx, const double* Qp
   const int lazy = X0 != nullptr ? 1 : 0;
   if (!make_map(lazy ? X0 : X, lazy ? ldx0 : ldx, &map0)) return cudaErrorInvalidValue;
   switch (bucket) {
-    case 16: return go_lp<16, E>(map, map0, lazy, Qp, L, ldl, n, d, dvec, st, (E*)X, ldx, resid ? 1 : 0, s, part, pw);
-    case 32: return go_lp<32, E>(map, map0, lazy, Qp, L, ldl, n, d, dvec, st, (E*)X, ldx, resid ? 1 : 0, s, part, pw);
+    case 16:
+    case 32:
+      // fp64 with RBRP_LP64_ALL=1 (experiment): k_lhat64's split L-hat pass for ntr <= 4 too
+      if (sizeof(E) == 8 && lp64_all())
+        return go_lp64(map, map0, lazy, Qp, (double*)L, ldl, n, d, dvec, st, (double*)X, ldx, resid ? 1 : 0, s,
+                       part, pw, bucket);
+      if (bucket == 16)
+        return go_lp<16, E>(map, map0, lazy, Qp, L, ldl, n, d, dvec, st, (E*)X, ldx, resid ? 1 : 0, s, part, pw);
+      return go_lp<32, E>(map, map0, lazy, Qp, L, ldl, n, d, dvec, st, (E*)X, ldx, resid ? 1 : 0, s, part, pw);
     case 64:
       if (sizeof(E) != 8) return cudaErrorInvalidValue;
       return go_lp64(map, map0, lazy, Qp, (double*)L, ldl, n, d, dvec, st, (double*)X, ldx, resid ? 1 : 0, s, part,
-                     pw);
+                     pw, 64);
     default: return cudaErrorInvalidValue;
   }
 }
