@@ -393,13 +393,116 @@ cudaError_t launch_w_identity(T* W, int64_t ldw, const int64_t* S, int64_t k, in
   return cudaGetLastError();
 }
 
+// W = L L_1^{-T} for small K = kp <= kWsK (Alg. 3): L_1^{-T} (kp x kp, fp64) stays
+// in shared memory for the whole launch, 64-row tiles of L stream through (converted to fp64,
+// prefetched into registers during the previous tile's MMAs), and the product runs on the FP64
+// tensor path (DMMA m8n8k4): warp w owns the tile's rows 8w .. 8w + 7 and walks the 8-column
+// output tiles four at a time (four independent accumulator chains, one A fragment per k-step
+// shared by the four).  Output tile t (columns 8t ..) skips the k-steps with k < 8t, where
+// L_1^{-T}(n, k) = 0 (L_1^{-1} is lower triangular).  One pass over L, one write of W.
+constexpr int kWsK = 128;
+constexpr int kWsRows = 64;
+constexpr int kWsThreads = 256;
+template <typename T>
+__global__ void __launch_bounds__(kWsThreads, 1)
+    k_w_small(const T* __restrict__ L, int64_t ldl, const T* __restrict__ LinvT, int64_t n, int k, int kp,
+              T* __restrict__ W, int64_t ldw, int lower) {
+  extern __shared__ double ws_[];
+  const int ld = kp + 4;                         // conflict-free fragment loads (ld = 4 mod 8)
+  double* Bs = ws_;                              // [kp][ld]: Bs[nn][kk] = L_1^{-T}(nn, kk)
+  double* As = Bs + (size_t)kp * ld;             // [64][ld]
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, q = lane & 3;
+  for (int e = tid; e < kp * kp; e += kWsThreads) {
+    const int nn = e / kp, kk = e - nn * kp;
+    Bs[nn * ld + kk] = (double)LinvT[(int64_t)nn * kp + kk];
+  }
+  const int64_t ntiles = (n + kWsRows - 1) / kWsRows;
+  constexpr int PF = kWsRows * kWsK / kWsThreads;   // prefetched elements per thread (32)
+  T pf[PF];
+  auto fetch = [&](int64_t tile) {
+#pragma unroll
+    for (int u = 0; u < PF; ++u) {
+      const int e = tid + u * kWsThreads, r = e / kWsK, c = e - r * kWsK;
+      const int64_t row = tile * kWsRows + r;
+      pf[u] = (c < kp && row < n) ? L[row * ldl + c] : T(0);
+    }
+  };
+  int64_t tile = blockIdx.x;
+  if (tile < ntiles) fetch(tile);
+  const int ntt = kp / 8;
+  for (; tile < ntiles; tile += gridDim.x) {
+    __syncthreads();   // previous tile's MMAs done with As (and Bs complete, first time)
+#pragma unroll
+    for (int u = 0; u < PF; ++u) {
+      const int e = tid + u * kWsThreads, r = e / kWsK, c = e - r * kWsK;
+      if (c < kp) As[r * ld + c] = (double)pf[u];
+    }
+    __syncthreads();
+    if (tile + gridDim.x < ntiles) fetch(tile + gridDim.x);   // in flight during the MMAs
+    const double* Ar = As + (8 * w + g) * ld + q;
+    const int64_t row = tile * kWsRows + 8 * w + g;
+    for (int t0 = 0; t0 < ntt; t0 += 4) {
+      double2 acc[4] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0),
+                        make_double2(0.0, 0.0)};
+      const int s0 = lower ? 2 * t0 : 0;   // k-steps of 4 below 8 t0 hold only zeros of B
+      for (int s4 = s0; s4 < kp / 4; ++s4) {
+        const double a = Ar[4 * s4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int t = t0 + j;
+          if (t < ntt && (!lower || s4 >= 2 * t)) {
+            const double b = Bs[(8 * t + g) * ld + 4 * s4 + q];
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                         : "+d"(acc[j].x), "+d"(acc[j].y)
+                         : "d"(a), "d"(b));
+          }
+        }
+      }
+      if (row < n) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int col = 8 * (t0 + j) + 2 * q;
+          if (t0 + j < ntt) {
+            if (col < k) W[row * ldw + col] = (T)acc[j].x;
+            if (col + 1 < k) W[row * ldw + col + 1] = (T)acc[j].y;
+          }
+        }
+      }
+    }
+  }
+}
+
+template <typename T>
+bool w_small_supported(int64_t kp) { return kp % 8 == 0 && kp >= 8 && kp <= kWsK; }
+
+template <typename T>
+cudaError_t launch_w_small(const T* L, int64_t ldl, const T* LinvT, int64_t n, int64_t k, int64_t kp, T* W,
+                           int64_t ldw, bool lower, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  if (!w_small_supported<T>(kp)) return cudaErrorInvalidValue;
+  const size_t smem = (size_t)(kp + kWsRows) * (kp + 4) * sizeof(double);
+  static PerDevice attr;
+  const cudaError_t ae = attr.once([] {
+    return cudaFuncSetAttribute(k_w_small<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)((size_t)(kWsK + kWsRows) * (kWsK + 4) * sizeof(double)));
+  });
+  if (ae != cudaSuccess) return ae;
+  const int64_t ntiles = (n + kWsRows - 1) / kWsRows;
+  const int grid = (int)std::min<int64_t>(ntiles, device_sms());
+  k_w_small<T><<<grid, kWsThreads, smem, s>>>(L, ldl, LinvT, n, (int)k, (int)kp, W, ldw, lower ? 1 : 0);
+  return cudaGetLastError();
+}
+
 #define INSTW(T)                                                                                  \
   template cudaError_t launch_gather_L1<T>(const T*, int64_t, const int64_t*, int64_t, int64_t,  \
                                            int64_t, double*, cudaStream_t);                      \
   template cudaError_t launch_trinv<T>(const double*, int64_t, T*, int64_t, DevState*, cudaStream_t); \
   template cudaError_t launch_w_identity<T>(T*, int64_t, const int64_t*, int64_t, int64_t,       \
                                             int64_t, cudaStream_t);                              \
-  template cudaError_t launch_pinv_clip<T>(double*, int64_t, T*, int64_t, void*, int*, cudaStream_t);
+  template cudaError_t launch_pinv_clip<T>(double*, int64_t, T*, int64_t, void*, int*, cudaStream_t); \
+  template bool w_small_supported<T>(int64_t);                                                   \
+  template cudaError_t launch_w_small<T>(const T*, int64_t, const T*, int64_t, int64_t, int64_t, T*, int64_t, \
+                                         bool, cudaStream_t);
 INSTW(double)
 INSTW(float)
 

@@ -171,6 +171,13 @@ cudaError_t gemm_nt_lp(const float* A, int64_t lda, const float* B, int64_t ldb,
                        int64_t min_k = 512, int* nlaunch = nullptr);
 
 // k_formw.cu — Alg. 3 by triangular solve
+// W = L L_1^{-T} for K = kp <= 128 (kp % 8 == 0): L_1^{-T} resident in shared memory, DMMA;
+// lower: skip the zero k-steps of a triangular L_1^{-1}
+template <typename T>
+bool w_small_supported(int64_t kp);
+template <typename T>
+cudaError_t launch_w_small(const T* L, int64_t ldl, const T* LinvT, int64_t n, int64_t k, int64_t kp, T* W,
+                           int64_t ldw, bool lower, cudaStream_t s);
 template <typename T>
 cudaError_t launch_gather_L1(const T* L, int64_t ldl, const int64_t* S, int64_t k, int64_t n_local,
                              int64_t row_offset, double* L1, cudaStream_t s);

@@ -797,7 +797,11 @@ int enqueue_W(Ctx<T>& c, const rbrp_problem* p, rbrp_comm* comm, void* W_out, in
     CK(cudaMemset2DAsync(c.Lm + k, (size_t)k_cap * sizeof(T), 0, (size_t)(kp - k) * sizeof(T), (size_t)c.n, s));
   cudaError_t merr = cudaSuccess;
   ++*nl;
-  if (!force_simt() && kp <= k_cap && c.Wsc && !env_on("RBRP_W_NTMMA") && !env_on("RBRP_W_SIMT") &&
+  if (!force_simt() && kp <= k_cap && w_small_supported<T>(kp) && !env_on("RBRP_W_NOSMALL") &&
+      !env_on("RBRP_W_SIMT")) {
+    // K <= 128: L_1^{-T} resident in shared memory, one pass over L (k_w_small)
+    CK(launch_w_small<T>(c.Lm, k_cap, LinvT, c.n, k, kp, (T*)W_out, k_cap, !clip, s));
+  } else if (!force_simt() && kp <= k_cap && c.Wsc && !env_on("RBRP_W_NTMMA") && !env_on("RBRP_W_SIMT") &&
       gemm_lp_supported(c.Lm, k_cap, LinvT, kp, kp, w_min_k<T>())) {
     // lower_b: L_1^{-T} has zero chunks to skip; the clipped pinv is dense.  fp32: the same
     // passes with fp32 storage and fp64 DMMA arithmetic
@@ -1380,7 +1384,10 @@ int run_dist(int nsh, const rbrp_problem* ps, void* const* Xs, char* const* wss,
         CK(cudaMemset2DAsync(c.Lm + k, (size_t)k_cap * sizeof(T), 0, (size_t)(kp - k) * sizeof(T), (size_t)c.n, s));
       cudaError_t merr = cudaSuccess;
       ++nl;
-      if (!force_simt() && kp <= k_cap && c.Wsc && !env_on("RBRP_W_NTMMA") && !env_on("RBRP_W_SIMT") &&
+      if (!force_simt() && kp <= k_cap && w_small_supported<T>(kp) && !env_on("RBRP_W_NOSMALL") &&
+          !env_on("RBRP_W_SIMT")) {
+        CK(launch_w_small<T>(c.Lm, k_cap, c.LinvT, c.n, k, kp, (T*)W_outs[h], k_cap, !clip, s));
+      } else if (!force_simt() && kp <= k_cap && c.Wsc && !env_on("RBRP_W_NTMMA") && !env_on("RBRP_W_SIMT") &&
           gemm_lp_supported(c.Lm, k_cap, c.LinvT, kp, kp, w_min_k<T>())) {
         --nl;
         CK(gemm_nt_lp(c.Lm, k_cap, c.LinvT, kp, (T*)W_outs[h], k_cap, c.n, k, kp, c.Wsc, s, !clip, w_min_k<T>(), &nl));
@@ -1510,7 +1517,9 @@ int form_w_run(const T* L, int64_t ldl, int64_t n, const int64_t* S, int64_t k, 
   // the ID's W GEMM (k_lhat64 / k_lhat_paper passes, or k_nt_mma for small fp64 k) when L's
   // rows can be read as k = kp columns (k % 8 == 0), else the CUDA-core tile GEMM
   cudaError_t merr = cudaSuccess;
-  if (k == kp && !force_simt() && gemm_lp_supported(L, ldl, (const T*)LinvT, kp, kp, w_min_k<T>())) {
+  if (k == kp && !force_simt() && w_small_supported<T>(kp) && !env_on("RBRP_W_NOSMALL")) {
+    CK(launch_w_small<T>(L, ldl, (const T*)LinvT, n, k, kp, W, ldw, !clip, s));
+  } else if (k == kp && !force_simt() && gemm_lp_supported(L, ldl, (const T*)LinvT, kp, kp, w_min_k<T>())) {
     CK(gemm_nt_lp(L, ldl, (const T*)LinvT, kp, W, ldw, n, k, kp, ws + f.Wsc, s, !clip, w_min_k<T>()));
   } else if (sizeof(T) == 8 && k == kp && !force_simt() &&
              gemm_nt_mma((const double*)L, ldl, (const double*)LinvT, kp, (double*)W, ldw, n, k, kp, s, &merr)) {
