@@ -296,26 +296,29 @@ __device__ int cta_pivchol_reg(const double* __restrict__ Gg, int nb, int mode, 
         if (x > best) { best = x; bl = l; }
       }
     }
-    ms = warp_sum(ms);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-      const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
-      if (ob > best || (ob == best && ol < bl)) { best = ob; bl = ol; }
+    int p;
+    double dp;
+    if (mode == 1 && !forced) {   // REDUX pivot search (as cta_chol_inv)
+      const unsigned long long key = best > 0.0 ? (unsigned long long)__double_as_longlong(best) : 0ull;
+      const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+      const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+      const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+      p = __reduce_min_sync(0xffffffffu, (hi == mh && lo == ml) ? bl : (1 << 30));
+      dp = __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml));
+    } else {
+      p = mode == 2 ? i : forced[i];
+      const double q0 = __shfl_sync(0xffffffffu, dgv[0], p & 31), q1 = __shfl_sync(0xffffffffu, dgv[1], p & 31);
+      const double q2 = __shfl_sync(0xffffffffu, dgv[2], p & 31), q3 = __shfl_sync(0xffffffffu, dgv[3], p & 31);
+      const int pm = (p >> 5) & 3;
+      dp = pm == 0 ? q0 : (pm == 1 ? q1 : (pm == 2 ? q2 : q3));
     }
     int cut = 0;
     if (mode == 1) {
+      ms = warp_sum(ms);
       if (tid == 0) mass[i] = ms;
       if (i == 0) thr = tau_b * ms;
       if (!(ms > 0.0) || ms < thr) cut = 1;                        // l.8 cut
     }
-    int p = bl;
-    if (mode == 2) p = i;
-    if (mode == 1 && forced) p = forced[i];
-    const double q0 = __shfl_sync(0xffffffffu, dgv[0], p & 31), q1 = __shfl_sync(0xffffffffu, dgv[1], p & 31);
-    const double q2 = __shfl_sync(0xffffffffu, dgv[2], p & 31), q3 = __shfl_sync(0xffffffffu, dgv[3], p & 31);
-    const int pm = (p >> 5) & 3;
-    const double dp = pm == 0 ? q0 : (pm == 1 ? q1 : (pm == 2 ? q2 : q3));
     if (!cut && !(dp > 0.0)) cut = 2;                               // non-positive pivot
     if (cut) {
       if (tid == 0 && cut == 2) *rank_def = 1;
