@@ -124,6 +124,43 @@ def test_replay_parity_fp64(name, kw):
 
 
 @cuda
+@pytest.mark.parametrize("rank,b", [(70, 128), (95, 128), (81, 96), (120, 128)])
+def test_replay_parity_projection_parts(rank, b):
+    """b' > 64 runs as a 64-column part on k_lhat64 plus the remainder on the kernel of its own
+    width (R28): exactly rank-r data puts b' = r into the first block, so the remainders are
+    6 (bucket 16), 31 (bucket 32), 17 (bucket 32) and 56 (k_lhat64 again).  Replay parity
+    with the oracle: S, b' exact, rho_t within 1e-10, W within tolerance."""
+    cfg = small_config("c2", n=3 * 4096 + 1234, d=256, rank=rank, b=b)
+    Xnp = make(cfg).numpy()
+    ores = O.rbrp(Xnp, tau=1e-12, b=b, seed=0)
+    assert ores.blocks[0].b_prime > 64   # (the robust filter may stop a few short of rank)
+    _replay(Xnp, ores, np.float64, b)
+
+
+@cuda
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("k", [8, 88, 128, 136, 90])
+def test_form_w_kernels_against_oracle(dtype, k):
+    """rbrp_form_w (Alg. 3 on its own) on every W kernel: k_w_small (k % 8 == 0, k <= 128),
+    the pass GEMM (k = 136), the CUDA-core tile GEMM (k = 90: rows not readable as
+    round8(k) columns); W against the oracle's triangular solve."""
+    rb = _rb()
+    rng = np.random.default_rng(k)
+    n = 5000
+    L = rng.standard_normal((n, k))
+    S = sorted(rng.choice(n, k, replace=False).tolist())
+    L[S] = np.eye(k) + 0.05 * np.tril(rng.standard_normal((k, k)), -1)
+    Lg = torch.from_numpy(L.astype(dtype)).cuda()
+    W, flags, _ = rb.rbrp.form_w(Lg, S, method="trsm")
+    Wo, kappa, _ = O.form_W(Lg.double().cpu().numpy(), S, method="trsm")
+    u = 1.1e-16 if dtype == np.float64 else 6e-8
+    tol = max(_tol(dtype), 10 * kappa * u)
+    Wd = W.double().cpu().numpy()
+    assert np.linalg.norm(Wd - Wo) <= tol * np.linalg.norm(Wo)
+    assert np.array_equal(Wd[S], np.eye(k))
+
+
+@cuda
 @pytest.mark.parametrize("b", [16, 64])
 def test_replay_parity_fp32_c4_small(monkeypatch, b):
     """fp32 (c4-like): the default projection (fp32 storage, fp64 DMMA arithmetic, reading
