@@ -127,9 +127,10 @@ def test_replay_parity_fp64(name, kw):
 @pytest.mark.parametrize("rank,b", [(70, 128), (95, 128), (81, 96), (120, 128)])
 def test_replay_parity_projection_parts(rank, b):
     """b' > 64 runs as a 64-column part on k_lhat64 plus the remainder on the kernel of its own
-    width (R28): exactly rank-r data puts b' = r into the first block, so the remainders are
-    6 (bucket 16), 31 (bucket 32), 17 (bucket 32) and 56 (k_lhat64 again).  Replay parity
-    with the oracle: S, b' exact, rho_t within 1e-10, W within tolerance."""
+    width (R28): exactly rank-r data puts b' ~ r into the first block (the oracle keeps 68,
+    90, 73, 105), so the remainders 4, 26, 9, 41 run on buckets 16, 32, 16 and on k_lhat64
+    again.  Replay parity with the oracle: S, b' exact, rho_t within 1e-10, W within
+    tolerance."""
     cfg = small_config("c2", n=3 * 4096 + 1234, d=256, rank=rank, b=b)
     Xnp = make(cfg).numpy()
     ores = O.rbrp(Xnp, tau=1e-12, b=b, seed=0)
