@@ -479,8 +479,8 @@ def _replay_form(Xnp, ores, dtype, b, form):
     ("c2", dict(n=9000 + 77, d=1024, rank=70, b=32)),     # fused paper pass, nc = 16
     ("c2", dict(n=6000, d=260, rank=24, b=8)),            # partial chunk, bucket 16
     ("c3", dict(n=12000, d=64, n_heavy_dirs=20, n_heavy_rows=6000, b=16)),
-    ("c5", dict(n=12000, d=160, n_centres=120, b=64)),    # b' > 32: two 32-column parts
-    ("c5", dict(n=12000, d=200, n_centres=150, b=96)),    # three parts, downdate per part
+    ("c5", dict(n=12000, d=160, n_centres=120, b=64)),    # 32 < b' <= 64: k_lhat64, read-only
+    ("c5", dict(n=12000, d=200, n_centres=150, b=96)),    # b' > 64: parts, downdate per part
 ])
 def test_paper_form_replay_parity(name, kw):
     """NEXT-1 (RBRP_FORM_PAPER): Alg. 2 literally (CGS2 for l.6, read-only L-hat pass
