@@ -155,9 +155,160 @@ __global__ void __launch_bounds__(32 * kTrinvSmallWarps) k_trinv_small(const dou
   for (int64_t m = lane; m < ldo; m += 32) LinvT[(int64_t)j * ldo + m] = (m < j || m >= kk) ? T(0) : (T)x[m];
 }
 
+// Blocked inversion of the lower-triangular L_1 in place, one cooperative kernel (the
+// substitution kernels above chain k dependent steps; this one chains log2(k / 32) levels
+// of small GEMMs spread over the whole GPU):
+//   phase 0  the strictly upper triangle of L_1 is zeroed; every 32 x 32 diagonal block is
+//            inverted in place (one warp per block, thread j = column j, substitution)
+//   level s  (s = 32, 64, ...) for every pair of inverted diagonal blocks A (rows/cols
+//            [2ps, 2ps + s)) and C (the next s or fewer), with B = L_1(C, A):
+//            T = B A^{-1} (scratch), then L_1(C, A) <- -C^{-1} T   (= the (C, A) block of L_1^{-1})
+//   final    LinvT(j, i) = L_1^{-1}(i, j), zero above the diagonal and in the padding
+// GEMM tiles are 32 x 32 outputs per CTA step (256 threads, 4 outputs each, 32-deep smem
+// panels), taken grid-stride; one grid barrier after each step.  Triangular factors are
+// stored with exact zeros above the diagonal, so the panels need no masks.
+constexpr int kTbThreads = 256;
 template <typename T>
-cudaError_t launch_trinv(const double* L1, int64_t k, T* LinvT, int64_t ldo, DevState* st, cudaStream_t s) {
+__global__ void __launch_bounds__(kTbThreads) k_trinv_blk(double* __restrict__ L1, int k, double* __restrict__ Tsc,
+                                                          T* __restrict__ LinvT, int64_t ldo) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double Ps[32][33], Qs[32][33];
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+  const int64_t kk = k;
+  // phase 0a: zero the strictly upper triangle (one warp per row)
+  for (int64_t i = (int64_t)blockIdx.x * (kTbThreads / 32) + ty; i < kk; i += (int64_t)gridDim.x * (kTbThreads / 32))
+    for (int64_t j = i + 1 + tx; j < kk; j += 32) L1[i * kk + j] = 0.0;
+  // phase 0b: invert the 32 x 32 diagonal blocks in place (lower part only): warp w runs the
+  // columns w, w + 8, w + 16, w + 24 together, column-oriented substitution with lane i
+  // owning row i (step m: x_m = r_m / L(m,m) broadcast by a shuffle, r_i -= L(i,m) x_m for
+  // i > m; for m below a column's start r_m = 0, so every column runs all 32 steps)
+  const int nbk = (k + 31) / 32;
+  for (int b = blockIdx.x; b < nbk; b += gridDim.x) {
+    const int o = 32 * b, cb = min(32, k - o);
+    __syncthreads();
+    for (int e = tid; e < 32 * 32; e += kTbThreads) {
+      const int i = e >> 5, j = e & 31;
+      Ps[i][j] = (i < cb && j <= i) ? L1[(int64_t)(o + i) * kk + o + j] : (i == j ? 1.0 : 0.0);
+    }
+    __syncthreads();
+    const double dl = 1.0 / Ps[tx][tx];   // lane tx: 1 / L(tx, tx)
+    double r[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) r[u] = (tx == ty + 8 * u) ? 1.0 : 0.0;
+    for (int m = 0; m < 32; ++m) {
+      const double dm = __shfl_sync(0xffffffffu, dl, m);
+      const double lim = Ps[tx][m];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double xm = __shfl_sync(0xffffffffu, r[u], m) * dm;
+        r[u] = tx == m ? xm : (tx > m ? fma(-lim, xm, r[u]) : r[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) Qs[tx][ty + 8 * u] = r[u];   // x_i of column j = ty + 8u at row tx
+    __syncthreads();
+    for (int e = tid; e < 32 * 32; e += kTbThreads) {
+      const int i = e >> 5, j = e & 31;
+      if (i < cb && j <= i) L1[(int64_t)(o + i) * kk + o + j] = Qs[i][j];
+    }
+  }
+  grid.sync();
+  for (int sb = 32; sb < k; sb *= 2) {
+    const int npair = (k + 2 * sb - 1) / (2 * sb);
+    const int tps = sb / 32;   // 32-wide tiles per s
+    // step 1: T(p) = B A^{-1}, B = L1(C rows, A cols): cs x s, A^{-1} lower (m >= c)
+    // step 2: L1(C, A) = -C^{-1} T(p): C^{-1} lower (m <= r)
+    for (int step = 0; step < 2; ++step) {
+      for (int64_t w = blockIdx.x;; w += gridDim.x) {
+        // work item w -> (pair p, row tile rt, column tile ct)
+        int p = 0;
+        int64_t ww = w;
+        int cs = 0, rtiles = 0;
+        for (; p < npair; ++p) {
+          const int c0 = 2 * p * sb + sb;
+          cs = c0 < k ? min(sb, k - c0) : 0;
+          rtiles = (cs + 31) / 32;
+          const int64_t items = (int64_t)rtiles * tps;
+          if (ww < items) break;
+          ww -= items;
+        }
+        if (p >= npair) break;
+        const int rt = (int)(ww / tps), ct = (int)(ww - (int64_t)rt * tps);
+        const int a0 = 2 * p * sb, c0 = a0 + sb;
+        double* Tp = Tsc + (int64_t)p * sb * sb;   // [cs][sb]
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        const int c = 32 * ct + tx;
+        // K range: step 1: m in [32 ct, sb) (A^{-1}(m, c) = 0 for m < c);
+        //          step 2: m in [0, 32 rt + 32) (C^{-1}(r, m) = 0 for m > r)
+        const int mlo = step == 0 ? 32 * ct : 0;
+        const int mhi = step == 0 ? sb : min(cs, 32 * rt + 32);
+        for (int m0 = mlo; m0 < mhi; m0 += 32) {
+          __syncthreads();
+          for (int e = tid; e < 32 * 32; e += kTbThreads) {
+            const int i = e >> 5, j = e & 31;
+            const int r = 32 * rt + i, m = m0 + j, mr = m0 + i, cc = 32 * ct + j;
+            double pv = 0.0, qv = 0.0;
+            if (step == 0) {
+              if (r < cs && m < mhi) pv = L1[(int64_t)(c0 + r) * kk + a0 + m];           // B(r, m)
+              if (mr < mhi) qv = L1[(int64_t)(a0 + mr) * kk + a0 + cc];                  // A^{-1}(mr, cc)
+            } else {
+              if (r < cs && m < mhi) pv = L1[(int64_t)(c0 + r) * kk + c0 + m];           // C^{-1}(r, m)
+              if (mr < mhi) qv = Tp[(int64_t)mr * sb + cc];                              // T(mr, cc)
+            }
+            Ps[i][j] = pv;
+            Qs[i][j] = qv;
+          }
+          __syncthreads();
+#pragma unroll 8
+          for (int mm = 0; mm < 32; ++mm) {
+            const double q = Qs[mm][tx];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) acc[u] = fma(Ps[ty + 8 * u][mm], q, acc[u]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int r = 32 * rt + ty + 8 * u;
+          if (r < cs) {
+            if (step == 0) Tp[(int64_t)r * sb + c] = acc[u];
+            else L1[(int64_t)(c0 + r) * kk + a0 + c] = -acc[u];
+          }
+        }
+      }
+      grid.sync();
+    }
+  }
+  // final: LinvT (k x ldo) = L_1^{-T}, zero above the diagonal and in the padding
+  for (int64_t e = (int64_t)blockIdx.x * kTbThreads + tid; e < kk * ldo; e += (int64_t)gridDim.x * kTbThreads) {
+    const int64_t j = e / ldo, i = e - j * ldo;
+    LinvT[e] = (i >= j && i < kk) ? (T)L1[i * kk + j] : T(0);
+  }
+}
+
+template <typename T>
+cudaError_t launch_trinv(const double* L1, int64_t k, T* LinvT, int64_t ldo, DevState* st, cudaStream_t s,
+                         void* scratch) {
   if (k <= 0) return cudaSuccess;
+  if (scratch && k > 32 && !getenv("RBRP_TRINV_SUBST")) {
+    // blocked cooperative inversion (L1 is overwritten by L_1^{-1}; scratch >= k^2 / 2 doubles)
+    int maxit = (int)((k + 31) / 32);
+    for (int64_t sb = 32; sb < k; sb *= 2) {
+      int items = 0;
+      for (int64_t a0 = 0; a0 + sb < k; a0 += 2 * sb) items += (int)(((std::min<int64_t>(sb, k - a0 - sb) + 31) / 32) * (sb / 32));
+      maxit = std::max(maxit, items);
+    }
+    int per = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_trinv_blk<T>, kTbThreads, 0);
+    if (e != cudaSuccess) return e;
+    const int grid = std::max(1, std::min(maxit, device_sms() * std::max(per, 1)));
+    double* L1w = const_cast<double*>(L1);
+    double* Tsc = (double*)scratch;
+    int ki = (int)k;
+    void* args[] = {&L1w, &ki, &Tsc, &LinvT, &ldo};
+    e = cudaLaunchCooperativeKernel((const void*)k_trinv_blk<T>, dim3(grid), dim3(kTbThreads), args, 0, s);
+    return e;
+  }
   if (k <= kTrinvSmallK) {
     const size_t smem = (size_t)(k * k + k + kTrinvSmallWarps * k) * sizeof(double);
     static PerDevice attr;   // once per device, for the largest k of this path
@@ -496,7 +647,7 @@ cudaError_t launch_w_small(const T* L, int64_t ldl, const T* LinvT, int64_t n, i
 #define INSTW(T)                                                                                  \
   template cudaError_t launch_gather_L1<T>(const T*, int64_t, const int64_t*, int64_t, int64_t,  \
                                            int64_t, double*, cudaStream_t);                      \
-  template cudaError_t launch_trinv<T>(const double*, int64_t, T*, int64_t, DevState*, cudaStream_t); \
+  template cudaError_t launch_trinv<T>(const double*, int64_t, T*, int64_t, DevState*, cudaStream_t, void*); \
   template cudaError_t launch_w_identity<T>(T*, int64_t, const int64_t*, int64_t, int64_t,       \
                                             int64_t, cudaStream_t);                              \
   template cudaError_t launch_pinv_clip<T>(double*, int64_t, T*, int64_t, void*, int*, cudaStream_t); \

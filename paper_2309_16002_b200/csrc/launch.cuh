@@ -181,9 +181,11 @@ cudaError_t launch_w_small(const T* L, int64_t ldl, const T* LinvT, int64_t n, i
 template <typename T>
 cudaError_t launch_gather_L1(const T* L, int64_t ldl, const int64_t* S, int64_t k, int64_t n_local,
                              int64_t row_offset, double* L1, cudaStream_t s);
+// LinvT: k x ldo, columns [k, ldo) zero.  scratch (>= k^2/2 doubles, optional): the blocked
+// cooperative inversion k_trinv_blk, which overwrites L1 with L_1^{-1}; without: substitution
 template <typename T>
 cudaError_t launch_trinv(const double* L1, int64_t k, T* LinvT, int64_t ldo, DevState* st,
-                         cudaStream_t s);   // LinvT: k x ldo, columns [k, ldo) zero
+                         cudaStream_t s, void* scratch = nullptr);
 template <typename T>
 cudaError_t launch_gemm_nt(const T* A, int64_t lda, const T* B, int64_t ldb, T* C, int64_t ldc,
                            int64_t M, int64_t N, int64_t K, cudaStream_t s);

@@ -791,7 +791,7 @@ int enqueue_W(Ctx<T>& c, const rbrp_problem* p, rbrp_comm* comm, void* W_out, in
     CK(launch_pinv_clip<T>(L1, k, LinvT, kp, c.Pinv, nullptr, s));   // dense pinv_clip(L_1)^T
   } else {
     ++*nl;
-    CK(launch_trinv<T>(L1, k, LinvT, kp, c.st, s));
+    CK(launch_trinv<T>(L1, k, LinvT, kp, c.st, s, c.Pinv));
   }
   if (kp > k && kp <= k_cap && c.n > 0)
     CK(cudaMemset2DAsync(c.Lm + k, (size_t)k_cap * sizeof(T), 0, (size_t)(kp - k) * sizeof(T), (size_t)c.n, s));
@@ -1364,21 +1364,22 @@ int run_dist(int nsh, const rbrp_problem* ps, void* const* Xs, char* const* wss,
     for (int h = 0; h < nsh; ++h)
       LKD(launch_gather_L1<T>(C[h].Lm, k_cap, C[h].S, k, C[h].n, ps[h].row_offset, C[h].L1, s));
     if (comm) RCD(comm_allreduce_f64(comm, C[0].L1, k * k, s));
+    int lt_src = -1;   // in-process shards: the shard whose L_1^{-T} the others copy
     for (int h = 0; h < nsh; ++h) {
       Ctx<T>& c = C[h];
       if (!W_outs[h]) continue;
       const int64_t kp = (k + 7) / 8 * 8;
-      if (clip) {
-        // the Jacobi SVD rotates L_1 in place: in-process shards (one shared L_1) compute
-        // pinv_clip once and copy it
-        if (emul && h > 0) {
-          CK(cudaMemcpyAsync(c.LinvT, C[0].LinvT, (size_t)k * kp * sizeof(T), cudaMemcpyDeviceToDevice, s));
-        } else {
-          nl += 4;
-          CK(launch_pinv_clip<T>(c.L1, k, c.LinvT, kp, c.Pinv, nullptr, s));
-        }
+      // the Jacobi SVD and the blocked inverse work on L_1 in place: in-process shards (one
+      // shared L_1) compute L_1^{-T} once and copy it
+      if (emul && lt_src >= 0) {
+        CK(cudaMemcpyAsync(c.LinvT, C[lt_src].LinvT, (size_t)k * kp * sizeof(T), cudaMemcpyDeviceToDevice, s));
+      } else if (clip) {
+        nl += 4;
+        CK(launch_pinv_clip<T>(c.L1, k, c.LinvT, kp, c.Pinv, nullptr, s));
+        lt_src = h;
       } else {
-        LKD(launch_trinv<T>(c.L1, k, c.LinvT, kp, c.st, s));
+        LKD(launch_trinv<T>(c.L1, k, c.LinvT, kp, c.st, s, c.Pinv));
+        lt_src = h;
       }
       if (kp > k && kp <= k_cap && c.n > 0)
         CK(cudaMemset2DAsync(c.Lm + k, (size_t)k_cap * sizeof(T), 0, (size_t)(kp - k) * sizeof(T), (size_t)c.n, s));
@@ -1512,7 +1513,7 @@ int form_w_run(const T* L, int64_t ldl, int64_t n, const int64_t* S, int64_t k, 
   if (clip) {
     CK(launch_pinv_clip<T>(L1, k, LinvT, kp, ws + f.Pinv, ncl, s));
   } else {
-    CK(launch_trinv<T>(L1, k, LinvT, kp, nullptr, s));
+    CK(launch_trinv<T>(L1, k, LinvT, kp, nullptr, s, ws + f.Pinv));
   }
   // the ID's W GEMM (k_lhat64 / k_lhat_paper passes, or k_nt_mma for small fp64 k) when L's
   // rows can be read as k = kp columns (k % 8 == 0), else the CUDA-core tile GEMM
