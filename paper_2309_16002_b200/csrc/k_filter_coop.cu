@@ -463,18 +463,38 @@ __device__ void cta_trinv_warp(const double* R, int ldr, const int* perm, int bp
 }
 
 // partial Gram of the nb x 32 slice S (stride kFiltLd) -> out (kMaxB x kMaxB)
+// partial Gram of this CTA's 32 columns: out(i, j) = sum_c S(i, c) S(j, c), i, j < nb, in
+// 4 x 4 register tiles (8 shared loads per 16 fmas, 16 independent chains per thread)
 __device__ void slice_gram(const double* S, int nb, double* out) {
-  for (int p = threadIdx.x; p < nb * nb; p += blockDim.x) {
-    const int i = p / nb, j = p % nb;
-    if (i > j) continue;
-    double s = 0.0;
-#pragma unroll 8
-    for (int c = 0; c < kFiltCW; ++c) s += S[i * kFiltLd + c] * S[j * kFiltLd + c];
-    out[i * kMaxB + j] = s;
-    out[j * kMaxB + i] = s;
+  const int nt = (nb + 3) >> 2;   // 4-row tiles per side
+  for (int t = threadIdx.x; t < nt * nt; t += blockDim.x) {
+    const int ti = t / nt, tj = t - ti * nt;
+    const int i0 = 4 * ti, j0 = 4 * tj;
+    double acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+#pragma unroll 4
+    for (int c = 0; c < kFiltCW; ++c) {
+      double x[4], y[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {   // rows past nb (< kMaxB) feed only unwritten outputs
+        x[a] = S[(i0 + a) * kFiltLd + c];
+        y[a] = S[(j0 + a) * kFiltLd + c];
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = fma(x[a], y[b], acc[a][b]);
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        if (i0 + a < nb && j0 + b < nb) out[(i0 + a) * kMaxB + j0 + b] = acc[a][b];
   }
 }
-
 __device__ void reduce_slices(const double* Gpart, int nsplit, int nb, double* G) {
   const int64_t per = (int64_t)nb * nb;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < per;
@@ -498,16 +518,27 @@ __device__ void reduce_slices(const double* Gpart, int nsplit, int nb, double* G
 // Out(i, c) = sum_{j <= i} T(j, i) In(src(j), c), i < rows (parallel dot products)
 __device__ void apply_T(const double* Tm, int ldt, int rows, const double* In, const int* src,
                         double* Out) {
-  for (int e = threadIdx.x; e < rows * kFiltCW; e += blockDim.x) {
-    const int i = e / kFiltCW, c = e % kFiltCW;
-    double s0 = 0.0, s1 = 0.0;
-    int j = 0;
-    for (; j + 1 <= i; j += 2) {
-      s0 = fma(Tm[j * ldt + i], In[(src ? src[j] : j) * kFiltLd + c], s0);
-      s1 = fma(Tm[(j + 1) * ldt + i], In[(src ? src[j + 1] : j + 1) * kFiltLd + c], s1);
+  // Out(i, c) = sum_{j <= i} T(j, i) In(src(j), c): thread (ty, tx) = column tx of the rows
+  // ty + 8u of a 64-row half, eight independent chains; T(j, i) is a warp-wide broadcast
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // blockDim = kFiltThreads = 256
+  for (int base = 0; base < rows; base += 64) {
+    double acc[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+    const int jmax = min(rows, base + 64);
+    for (int j = 0; j < jmax; ++j) {
+      const double x = In[(src ? src[j] : j) * kFiltLd + tx];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = base + ty + 8 * u;
+        if (i < rows && j <= i) acc[u] = fma(Tm[j * ldt + i], x, acc[u]);
+      }
     }
-    if (j <= i) s0 = fma(Tm[j * ldt + i], In[(src ? src[j] : j) * kFiltLd + c], s0);
-    Out[i * kFiltLd + c] = s0 + s1;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = base + ty + 8 * u;
+      if (i < rows) Out[i * kFiltLd + tx] = acc[u];
+    }
   }
 }
 
@@ -557,19 +588,30 @@ __global__ void __launch_bounds__(kFiltThreads, 1) k_filter_coop(FilterArgs F) {
   const int nsplit = gridDim.x;
   double* Gp = F.Gpart + (int64_t)blockIdx.x * kMaxB * kMaxB;
 
-  // A: gather + partial Gram
-  for (int e = tid; e < nb * kFiltCW; e += kFiltThreads) {
-    const int i = e / kFiltCW, c = e % kFiltCW;
-    double v = 0.0;
-    if (c0 + c < d) {
-      if (F.Vg) {
-        v = F.Vg[(int64_t)i * d + c0 + c];
-      } else {
-        const int64_t r = F.S_t[i] - F.row_offset;
-        v = s_first ? (double)((const T*)F.X0)[r * F.ldx0 + c0 + c] : (double)((const T*)F.X)[r * F.ldx + c0 + c];
+  // A: gather + partial Gram.  All of a thread's loads (rows S_t(i), scattered in HBM) are
+  // issued before any is stored: one memory latency instead of one per element.
+  {
+    constexpr int GPT = kMaxB * kFiltCW / kFiltThreads;   // elements per thread (16)
+    double v[GPT];
+#pragma unroll
+    for (int u = 0; u < GPT; ++u) {
+      const int e = tid + u * kFiltThreads, i = e / kFiltCW, c = e % kFiltCW;
+      double x = 0.0;
+      if (i < nb && c0 + c < d) {
+        if (F.Vg) {
+          x = F.Vg[(int64_t)i * d + c0 + c];
+        } else {
+          const int64_t r = F.S_t[i] - F.row_offset;
+          x = s_first ? (double)((const T*)F.X0)[r * F.ldx0 + c0 + c] : (double)((const T*)F.X)[r * F.ldx + c0 + c];
+        }
       }
+      v[u] = x;
     }
-    Vs[i * kFiltLd + c] = v;
+#pragma unroll
+    for (int u = 0; u < GPT; ++u) {
+      const int e = tid + u * kFiltThreads, i = e / kFiltCW, c = e % kFiltCW;
+      if (i < nb) Vs[i * kFiltLd + c] = v[u];
+    }
   }
   __syncthreads();
   slice_gram(Vs, nb, Gp);
@@ -690,14 +732,23 @@ __global__ void __launch_bounds__(kFiltThreads, 1) k_filter_coop(FilterArgs F) {
   __syncthreads();
   const int bq = s_kept;   // normally bp; smaller only if G2 lost definiteness
   stamp(F.dbg, 8);
-  if (blockIdx.x == 0) {
-    for (int e = tid; e < bq * bq; e += kFiltThreads) {
-      const int i = e / bq, j = e % bq;
-      double s = 0.0;
-      if (i <= j)
-        for (int m = i; m <= j; ++m) s = fma(Rs[i * ldr + m], R11s[m * ld11 + j], s);
-      F.Rtot[i * kMaxB + j] = (i <= j) ? s : 0.0;                      // R_total = R2 R11
+  // R_total = R2 R11 (every CTA holds both factors: the entries are spread over the grid,
+  // each dot product in two chains)
+  for (int64_t e = (int64_t)blockIdx.x * kFiltThreads + tid; e < (int64_t)bq * bq;
+       e += (int64_t)gridDim.x * kFiltThreads) {
+    const int i = (int)(e / bq), j = (int)(e % bq);
+    double s0 = 0.0, s1 = 0.0;
+    if (i <= j) {
+      int m = i;
+      for (; m + 1 <= j; m += 2) {
+        s0 = fma(Rs[i * ldr + m], R11s[m * ld11 + j], s0);
+        s1 = fma(Rs[i * ldr + m + 1], R11s[(m + 1) * ld11 + j], s1);
+      }
+      if (m <= j) s0 = fma(Rs[i * ldr + m], R11s[m * ld11 + j], s0);
     }
+    F.Rtot[i * kMaxB + j] = (i <= j) ? s0 + s1 : 0.0;
+  }
+  if (blockIdx.x == 0) {
     if (tid == 0 && bq < bp) {
       st->b_prime = bq;
       st->rank_def = 1;
