@@ -14,6 +14,7 @@
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
+#include <unistd.h>   // environ
 
 #include <algorithm>
 #include <list>
@@ -532,6 +533,7 @@ struct GraphKey {
   const void* ws;
   const void* aux;   // row-sharded graphs: the communicator
   uint64_t shards;   // row-sharded graphs: hash of every shard's X, workspace and rows
+  uint64_t env;      // hash of the RBRP_* environment (the experiment knobs select kernels)
   int device, use_mma;
   bool operator==(const GraphKey& o) const { return memcmp(this, &o, sizeof(GraphKey)) == 0; }
 };
@@ -572,6 +574,22 @@ void evict_lru(std::list<std::shared_ptr<E>>& cache, size_t cap) {
   }
 }
 
+// FNV-1a over the RBRP_* environment entries: a graph captured under one setting of the
+// experiment knobs (§7.1 of DESIGN.md) is not replayed under another
+uint64_t env_hash() {
+  uint64_t h = 1469598103934665603ull;
+  for (char** e = environ; e && *e; ++e) {
+    if (strncmp(*e, "RBRP_", 5) != 0) continue;
+    for (const char* c = *e; *c; ++c) {
+      h ^= (unsigned char)*c;
+      h *= 1099511628211ull;
+    }
+    h ^= 0xffu;
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+
 GraphKey make_key(const rbrp_problem* p, const void* X, const void* ws, int variant, const void* aux = nullptr,
                   uint64_t shards = 0) {
   GraphKey k;
@@ -586,6 +604,7 @@ GraphKey make_key(const rbrp_problem* p, const void* X, const void* ws, int vari
   k.use_mma = variant;
   k.aux = aux;
   k.shards = shards;
+  k.env = env_hash();
   return k;
 }
 
