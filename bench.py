@@ -360,6 +360,19 @@ def _measure(rb, cfg, X, tau, k_max, n_local, steps, warmup, form, seed, dev, dk
     return ms, res_list, kw
 
 
+def _kernel_label(cfg, bucket, form):
+    """Which kernel(s) run a block of the dominant bucket (R28)."""
+    what = "projection pass a4 (Alg. 2 l.13/l.16)" if form == "residual" else "read-only L-hat pass (l.13, l.16 downdate)"
+    if cfg.dtype == "f32" and form == "residual":
+        k = ("k_proj_tc32 (tcgen05 3xTF32), b' <= 64" if bucket <= 64
+             else "k_proj_tc32 (tcgen05 3xTF32) in 64-column parts, b' > 64")
+    else:
+        k = {16: "k_lhat_paper<16> (FP64 DMMA), b' <= 16", 32: "k_lhat_paper<32> (FP64 DMMA), 16 < b' <= 32",
+             64: "k_lhat64 (FP64 DMMA), 32 < b' <= 64"}.get(
+            bucket, "k_lhat64 on a 64-column part + the remainder on its own kernel (FP64 DMMA), b' > 64")
+    return f"{what}: {k}"
+
+
 def _config_entry(cfg, tau, k_max, ms, res_list, n_local, form, steps):
     r0 = res_list[-1]
     dom = _roofline(cfg, res_list, n_local, form)
@@ -369,8 +382,7 @@ def _config_entry(cfg, tau, k_max, ms, res_list, n_local, form, steps):
             "steps": steps, "k": r0.k, "blocks": r0.nblocks, "b_prime": r0.b_prime, "resid_rel": r0.resid_rel,
             "tau": tau, "projection_share_of_step": proj_ms / steps / ms if ms > 0 else None,
             "gpu_launches_per_step": r0.launches,
-            "roofline": (dict(dom, kernel="projection pass a4 (Alg. 2 l.13/l.16), b' <= %d instantiation"
-                              % dom["bucket"], compute_peak_note=cp_label,
+            "roofline": (dict(dom, kernel=_kernel_label(cfg, dom["bucket"], form), compute_peak_note=cp_label,
                               traffic=_traffic_from_profile(cfg.name)) if dom else None)}
 
 
