@@ -15,10 +15,10 @@ import paper_2309_16002_b200 as rb  # noqa: E402
 from workloads import CONFIGS, make  # noqa: E402
 
 torch.cuda.init()
-mb = int(os.environ.get("PERSIST_MB", "0"))
+mb = int(os.environ.get("PERSIST_MB", "-1"))
 err, prop = cudart.cudaGetDeviceProperties(0)
 print("persistingL2CacheMaxSize MB", prop.persistingL2CacheMaxSize / 2**20, "l2 MB", prop.l2CacheSize / 2**20)
-if mb:
+if mb >= 0:
     print(cudart.cudaDeviceSetLimit(cudart.cudaLimit.cudaLimitPersistingL2CacheSize, mb << 20))
 err, v = cudart.cudaDeviceGetLimit(cudart.cudaLimit.cudaLimitPersistingL2CacheSize)
 print("limit MB", v / 2**20)
