@@ -547,13 +547,18 @@ cudaError_t launch_w_identity(T* W, int64_t ldw, const int64_t* S, int64_t k, in
 // W = L L_1^{-T} for small K = kp <= kWsK (Alg. 3): L_1^{-T} (kp x kp, fp64) stays
 // in shared memory for the whole launch, 64-row tiles of L stream through (converted to fp64,
 // prefetched into registers during the previous tile's MMAs), and the product runs on the FP64
-// tensor path (DMMA m8n8k4): warp w owns the tile's rows 8w .. 8w + 7 and walks the 8-column
-// output tiles four at a time (four independent accumulator chains, one A fragment per k-step
-// shared by the four).  Output tile t (columns 8t ..) skips the k-steps with k < 8t, where
+// tensor path (DMMA m8n8k4): 16 warps, warp w owns the tile's rows 8 (w & 7) .. + 7 and one half
+// of the groups of four 8-column output tiles (four independent accumulator chains, one A
+// fragment per k-step shared by the four).  Output tile t (columns 8t ..) skips the k-steps with k < 8t, where
 // L_1^{-T}(n, k) = 0 (L_1^{-1} is lower triangular).  One pass over L, one write of W.
 constexpr int kWsK = 128;
 constexpr int kWsRows = 64;
-constexpr int kWsThreads = 256;
+constexpr int kWsThreads = 512;
+__device__ __forceinline__ void ws_dmma(double2& d, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d.x), "+d"(d.y)
+      : "d"(a), "d"(b));
+}
 template <typename T>
 __global__ void __launch_bounds__(kWsThreads, 1)
     k_w_small(const T* __restrict__ L, int64_t ldl, const T* __restrict__ LinvT, int64_t n, int k, int kp,
@@ -563,12 +568,16 @@ __global__ void __launch_bounds__(kWsThreads, 1)
   double* Bs = ws_;                              // [kp][ld]: Bs[nn][kk] = L_1^{-T}(nn, kk)
   double* As = Bs + (size_t)kp * ld;             // [64][ld]
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, q = lane & 3;
+  // warp w: row group rg = w & 7 (8 rows of the tile), column half ch = w >> 3 of the groups of
+  // four 8-column output tiles, paired from both ends (0 with the last, 1 with the one before,
+  // ...) so that both halves carry the same triangular work
+  const int rg = w & 7, ch = w >> 3;
   for (int e = tid; e < kp * kp; e += kWsThreads) {
     const int nn = e / kp, kk = e - nn * kp;
     Bs[nn * ld + kk] = (double)LinvT[(int64_t)nn * kp + kk];
   }
   const int64_t ntiles = (n + kWsRows - 1) / kWsRows;
-  constexpr int PF = kWsRows * kWsK / kWsThreads;   // prefetched elements per thread (32)
+  constexpr int PF = kWsRows * kWsK / kWsThreads;   // prefetched elements per thread (16)
   T pf[PF];
   auto fetch = [&](int64_t tile) {
 #pragma unroll
@@ -580,7 +589,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
   };
   int64_t tile = blockIdx.x;
   if (tile < ntiles) fetch(tile);
-  const int ntt = kp / 8;
+  const int ntt = kp / 8, ngr = (ntt + 3) / 4, nk4 = kp / 4;
   for (; tile < ntiles; tile += gridDim.x) {
     __syncthreads();   // previous tile's MMAs done with As (and Bs complete, first time)
 #pragma unroll
@@ -590,30 +599,50 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     }
     __syncthreads();
     if (tile + gridDim.x < ntiles) fetch(tile + gridDim.x);   // in flight during the MMAs
-    const double* Ar = As + (8 * w + g) * ld + q;
-    const int64_t row = tile * kWsRows + 8 * w + g;
-    for (int t0 = 0; t0 < ntt; t0 += 4) {
+    const double* Ar = As + (8 * rg + g) * ld + q;
+    const int64_t row = tile * kWsRows + 8 * rg + g;
+    for (int grp = 0; grp < ngr; ++grp) {
+      // half 0 takes the groups 0, 3, 4, 7, ... and half 1 the groups 1, 2, 5, 6, ...: with the
+      // triangular k ranges shrinking by 8 per group, both halves get the same work
+      const int m4 = grp & 3;
+      if ((m4 == 0 || m4 == 3) != (ch == 0)) continue;
+      const int t0 = 4 * grp;
       double2 acc[4] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0),
                         make_double2(0.0, 0.0)};
-      const int s0 = lower ? 2 * t0 : 0;   // k-steps of 4 below 8 t0 hold only zeros of B
-      for (int s4 = s0; s4 < kp / 4; ++s4) {
+      const double* B0 = Bs + (8 * t0 + g) * ld + q;
+      const int nj = min(4, ntt - t0);
+      int s4 = lower ? 2 * t0 : 0;   // k-steps of 4 below 8 t0 hold only zeros of B
+      // diagonal band (lower): tile t0 + j starts at k-step 2 (t0 + j)
+      const int sfull = lower ? min(nk4, 2 * t0 + 6) : s4;
+      for (; s4 < sfull; ++s4) {
         const double a = Ar[4 * s4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int t = t0 + j;
-          if (t < ntt && (!lower || s4 >= 2 * t)) {
-            const double b = Bs[(8 * t + g) * ld + 4 * s4 + q];
-            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-                         : "+d"(acc[j].x), "+d"(acc[j].y)
-                         : "d"(a), "d"(b));
-          }
+        for (int j = 0; j < 4; ++j)
+          if (j < nj && s4 >= 2 * (t0 + j)) ws_dmma(acc[j], a, B0[8 * j * ld + 4 * s4]);
+      }
+      if (nj == 4) {
+#pragma unroll 2
+        for (; s4 < nk4; ++s4) {
+          const double a = Ar[4 * s4];
+          const double b0 = B0[4 * s4], b1 = B0[8 * ld + 4 * s4], b2 = B0[16 * ld + 4 * s4], b3 = B0[24 * ld + 4 * s4];
+          ws_dmma(acc[0], a, b0);
+          ws_dmma(acc[1], a, b1);
+          ws_dmma(acc[2], a, b2);
+          ws_dmma(acc[3], a, b3);
+        }
+      } else {
+        for (; s4 < nk4; ++s4) {
+          const double a = Ar[4 * s4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (j < nj) ws_dmma(acc[j], a, B0[8 * j * ld + 4 * s4]);
         }
       }
       if (row < n) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const int col = 8 * (t0 + j) + 2 * q;
-          if (t0 + j < ntt) {
+          if (j < nj) {
             if (col < k) W[row * ldw + col] = (T)acc[j].x;
             if (col + 1 < k) W[row * ldw + col + 1] = (T)acc[j].y;
           }
