@@ -286,10 +286,191 @@ __global__ void __launch_bounds__(kTbThreads) k_trinv_blk(double* __restrict__ L
   }
 }
 
+// k <= 128: L_1^{-1} in ONE CTA with L_1 resident in shared memory (padded to kp = 8 ceil(k/8)
+// rows with an identity block, whose inverse is the identity), by recursive doubling: the 8 x 8
+// diagonal blocks by substitution (one thread per column, in registers), then for sb = 8, 16,
+// 32, 64 every pair of inverted sb-blocks A = L(a0.., a0..), C = L(c0.., c0..) (c0 = a0 + sb)
+// with B = L(C, A) becomes the inverse of [[A, 0], [B, C]] by T = B A^{-1} (scratch) and
+// L(C, A) = -C^{-1} T, all pairs of a level together, on the FP64 tensor path (DMMA m8n8k4):
+// a warp owns 2 x 2 output tiles (one 8 x 8 tile while sb = 8), so each fragment load feeds two
+// MMAs; the K loops skip the zero triangles of A^{-1} (T: k >= the first column) and C^{-1}
+// (L: k <= the last row). No grid barriers and no global round trips between the levels; the
+// FP64 work on one SM (kp^3 / 3 FMA) is ~3 us at k = 128.
+constexpr int kT1K = 128;
+constexpr int kT1Threads = 512;
+constexpr int kT1Scratch = 64 * 68 + kT1K;   // level scratch (max np sb (sb + 4)) + reciprocals
+__host__ __device__ constexpr size_t trinv_one_smem(int k) {
+  return ((size_t)((k + 7) & ~7) * (((k + 7) & ~7) + 4) + kT1Scratch) * sizeof(double);
+}
+__device__ __forceinline__ void t1_dmma(double2& d, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d.x), "+d"(d.y)
+      : "d"(a), "d"(b));
+}
+template <typename T>
+__global__ void __launch_bounds__(kT1Threads, 1) k_trinv_one(const double* __restrict__ L1, int k,
+                                                              T* __restrict__ LinvT, int64_t ldo) {
+  extern __shared__ double t1_[];
+  const int kp = (k + 7) & ~7, ld = kp + 4;   // ld = 4 mod 8: conflict-free fragment loads
+  double* Ls = t1_;                           // [kp][ld]
+  double* Tt = Ls + (size_t)kp * ld;          // level scratch [pair][sb][sb + 4]
+  double* Dr = Tt + 64 * 68;                  // 1 / L(i, i)
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, q = lane & 3;
+  constexpr int NW = kT1Threads / 32, RPW = kT1K / NW;
+  {
+    // warp w: rows w + 16 r, lanes over the columns; all loads in flight before the stores
+    double v[RPW][4];
+#pragma unroll
+    for (int r = 0; r < RPW; ++r)
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int i = w + NW * r, jj = lane + 32 * t;
+        v[r][t] = (i < k && jj <= i) ? L1[(int64_t)i * k + jj] : (i == jj ? 1.0 : 0.0);
+      }
+#pragma unroll
+    for (int r = 0; r < RPW; ++r)
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int i = w + NW * r, jj = lane + 32 * t;
+        if (i < kp && jj < kp) {
+          Ls[i * ld + jj] = v[r][t];
+          if (jj == i) Dr[i] = 1.0 / v[r][t];
+        }
+      }
+    // LinvT's zeros (above the diagonal and the padding columns [k, ldo)); every other entry
+    // is written once, when it becomes final
+    for (int j = w; j < k; j += NW)
+      for (int64_t i = lane; i < ldo; i += 32)
+        if (i < j || i >= k) LinvT[(int64_t)j * ldo + i] = T(0);
+  }
+  __syncthreads();
+  {
+    // 8 x 8 diagonal blocks: thread 8 b + j solves L_bb x = e_j
+    const int b = tid >> 3, j = tid & 7;
+    double x[8];
+    double* Lb = Ls + 8 * b * (ld + 1);
+    if (tid < kp) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        double sacc = i == j ? 1.0 : 0.0;
+#pragma unroll
+        for (int m = 0; m < i; ++m) sacc = fma(-Lb[i * ld + m], x[m], sacc);
+        x[i] = sacc * Dr[8 * b + i];
+      }
+    }
+    __syncthreads();
+    if (tid < kp) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (i >= j) {
+          Lb[i * ld + j] = x[i];
+          if (8 * b + i < k) LinvT[(int64_t)(8 * b + j) * ldo + 8 * b + i] = (T)x[i];
+        }
+    }
+  }
+  __syncthreads();
+  for (int sb = 8; sb < kp; sb *= 2) {
+    const int np = (kp - sb + 2 * sb - 1) / (2 * sb), ntc = sb / 8;
+    const int bt = sb >= 16 ? 2 : 1, nub = ntc / bt;   // units of bt x bt tiles, np nub^2 <= 16
+    const int tld = sb + 4;
+    for (int step = 0; step < 2; ++step) {
+      // the coordinate that sets a unit's K extent (T: its first tile column, L: its last tile
+      // row) varies across the four warps of each SM sub-partition (w / 4), the rest (w % 4)
+      const int hv = (w >> 2) % nub, v = (w & 3) + 4 * (w / (4 * nub));
+      const int p = v / nub, ot = v - p * nub;
+      const int trb = step == 0 ? ot : hv, tcb = step == 0 ? hv : ot;
+      const int a0 = 2 * sb * p, c0 = a0 + sb, cs = min(sb, kp - c0);
+      const int tr0 = bt * trb, tc0 = bt * tcb;
+      const bool act = p < np && 8 * tr0 < cs;
+      const bool row1 = bt == 2 && 8 * (tr0 + 1) < cs;   // second tile row inside the block
+      const int rA0 = c0 + 8 * tr0 + g, rA1 = row1 ? rA0 + 8 : rA0;
+      if (act) {
+        double2 acc[2][2];
+#pragma unroll
+        for (int x = 0; x < 2; ++x)
+#pragma unroll
+          for (int y = 0; y < 2; ++y) acc[x][y] = make_double2(0.0, 0.0);
+        if (step == 0) {
+          // T(r, c) = sum_{m >= 8 tc0} B(r, m) A^{-1}(m, c)
+          const double* a_0 = Ls + rA0 * ld + a0 + q;
+          const double* a_1 = Ls + rA1 * ld + a0 + q;
+          const double* b_0 = Ls + (a0 + q) * ld + a0 + 8 * tc0 + g;
+          for (int s4 = 2 * tc0; s4 < sb / 4; ++s4) {
+            const double x0 = a_0[4 * s4], y0 = b_0[4 * s4 * ld];
+            t1_dmma(acc[0][0], x0, y0);
+            if (bt == 2) {
+              const double x1 = a_1[4 * s4], y1 = b_0[4 * s4 * ld + 8];
+              t1_dmma(acc[0][1], x0, y1);
+              t1_dmma(acc[1][0], x1, y0);
+              t1_dmma(acc[1][1], x1, y1);
+            }
+          }
+          double* o = Tt + (size_t)p * sb * tld + (8 * tr0 + g) * tld + 8 * tc0 + 2 * q;
+          *reinterpret_cast<double2*>(o) = acc[0][0];
+          if (bt == 2) {
+            *reinterpret_cast<double2*>(o + 8) = acc[0][1];
+            if (row1) {
+              *reinterpret_cast<double2*>(o + 8 * tld) = acc[1][0];
+              *reinterpret_cast<double2*>(o + 8 * tld + 8) = acc[1][1];
+            }
+          }
+        } else {
+          // L(C, A)(r, c) = -sum_{m < 8 (tr0 + bt)} C^{-1}(r, m) T(m, c)
+          const double* a_0 = Ls + rA0 * ld + c0 + q;
+          const double* a_1 = Ls + rA1 * ld + c0 + q;
+          const double* b_0 = Tt + (size_t)p * sb * tld + q * tld + 8 * tc0 + g;
+          const int kend = min(cs, 8 * (tr0 + bt)) / 4;
+          for (int s4 = 0; s4 < kend; ++s4) {
+            const double x0 = a_0[4 * s4], y0 = b_0[4 * s4 * tld];
+            t1_dmma(acc[0][0], x0, y0);
+            if (bt == 2) {
+              const double x1 = a_1[4 * s4], y1 = b_0[4 * s4 * tld + 8];
+              t1_dmma(acc[0][1], x0, y1);
+              t1_dmma(acc[1][0], x1, y0);
+              t1_dmma(acc[1][1], x1, y1);
+            }
+          }
+          // these entries of L_1^{-1} are final: also straight to LinvT (8 consecutive i per
+          // store group), overlapping the later levels
+#pragma unroll
+          for (int x = 0; x < 2; ++x)
+#pragma unroll
+            for (int y = 0; y < 2; ++y) {
+              if ((x == 1 || y == 1) && bt == 1) continue;
+              if (x == 1 && !row1) continue;
+              const double2 r = make_double2(-acc[x][y].x, -acc[x][y].y);
+              const int i = rA0 + 8 * x, j = a0 + 8 * (tc0 + y) + 2 * q;
+              *reinterpret_cast<double2*>(Ls + i * ld + j) = r;
+              if (i < k) {
+                LinvT[(int64_t)j * ldo + i] = (T)r.x;
+                LinvT[(int64_t)(j + 1) * ldo + i] = (T)r.y;
+              }
+            }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
 template <typename T>
 cudaError_t launch_trinv(const double* L1, int64_t k, T* LinvT, int64_t ldo, DevState* st, cudaStream_t s,
                          void* scratch) {
   if (k <= 0) return cudaSuccess;
+  if (k > 32 && k <= kT1K && !getenv("RBRP_TRINV_SUBST") && !getenv("RBRP_TRINV_GRID")) {
+    const size_t smem = trinv_one_smem((int)k);
+    static PerDevice attr1;
+    const cudaError_t ae = attr1.once([] {
+      const size_t mx = trinv_one_smem(kT1K);
+      cudaError_t r = cudaFuncSetAttribute(k_trinv_one<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
+      if (r == cudaSuccess)
+        r = cudaFuncSetAttribute(k_trinv_one<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
+      return r;
+    });
+    if (ae != cudaSuccess) return ae;
+    k_trinv_one<T><<<1, kT1Threads, smem, s>>>(L1, (int)k, LinvT, ldo);
+    return cudaGetLastError();
+  }
   if (scratch && k > 32 && !getenv("RBRP_TRINV_SUBST")) {
     // blocked cooperative inversion (L1 is overwritten by L_1^{-1}; scratch >= k^2 / 2 doubles)
     int maxit = (int)((k + 31) / 32);
