@@ -16,6 +16,11 @@ namespace rbrp {
 constexpr int kSampleThreads = 256;
 constexpr int kSmemChunks = 2048;   // chunk prefixes searched in shared memory up to 8.4M rows
 
+constexpr int kHashBits = 10;       // repeat-rejection hash set (<= kMaxB + 256 live keys)
+constexpr int kHashSize = 1 << kHashBits;
+static_assert(kMaxB + kSampleThreads <= kHashSize / 2 && kMaxB + kSampleRound <= kHashSize / 2,
+              "hash set load factor");
+
 constexpr int kSkipRows = 64;       // rows per entry of the shared skip table
 constexpr int kSkipMax = 2048;      // skip table in shared memory up to 131072 local rows
 
@@ -27,21 +32,22 @@ constexpr int kSkipMax = 2048;      // skip table in shared memory up to 131072 
 // tq), then over 64 rows -- the same row, 6 global loads on the dependent path, not 12.
 __device__ int64_t resolve_in_chunk(int q, double tq, const double* __restrict__ cpre,
                                     const double* __restrict__ dvec, int64_t n_local,
-                                    int64_t row_offset, const double* skip = nullptr) {
+                                    int64_t row_offset, const double* skip = nullptr, int sg = kSkipRows) {
   int64_t lo = (int64_t)q * kChunk - row_offset;
   int64_t hi = lo + kChunk;
   if (hi > n_local) hi = n_local;
   if (lo < 0 || lo >= n_local) return -1;   // chunk owned by another rank
   int64_t a = lo, b = hi;                    // search in [a, b)
-  if (skip && lo % kSkipRows == 0) {
-    int64_t sa = lo / kSkipRows, sb = (hi + kSkipRows - 1) / kSkipRows;
+  if (skip && lo % sg == 0) {
+    int64_t sa = lo / sg, sb = (hi + sg - 1) / sg;
     while (sa < sb) {
       const int64_t m = (sa + sb) >> 1;
       if (skip[m] > tq) sb = m; else sa = m + 1;
     }
-    a = sa * kSkipRows;
+    a = sa * sg;
     if (a > hi) a = hi;
-    b = a + kSkipRows < hi ? a + kSkipRows : hi;
+    b = a + sg < hi ? a + sg : hi;
+    if (sg == 1) b = a;   // the skip table is cpre itself
   }
   while (a < b) {
     int64_t m = (a + b) >> 1;
@@ -54,6 +60,17 @@ __device__ int64_t resolve_in_chunk(int q, double tq, const double* __restrict__
   return a + row_offset;
 }
 
+// slot of row in the open-addressing set hkey (inserted if absent); rows are distinct keys
+__device__ __forceinline__ int hash_slot(unsigned long long* hkey, int64_t row) {
+  const unsigned long long key = (unsigned long long)row;
+  int h = (int)((uint32_t)((key ^ (key >> 29)) * 2654435761u) >> (32 - kHashBits));
+  while (true) {
+    const unsigned long long old = atomicCAS(&hkey[h], ~0ull, key);
+    if (old == ~0ull || old == key) return h;
+    h = (h + 1) & (kHashSize - 1);
+  }
+}
+
 __global__ void __launch_bounds__(kSampleThreads) k_sample(SampleArgs A) {
   DevState* st = A.st;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -61,7 +78,8 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample(SampleArgs A) {
   __shared__ double s_total;
   __shared__ int64_t s_np;
   __shared__ int64_t chosen[kMaxB];
-  __shared__ int64_t cand[kSampleThreads];
+  __shared__ unsigned long long hkey[kHashSize];
+  __shared__ int hidx[kHashSize];
   __shared__ int wcount[kSampleThreads / 32];
   __shared__ int s_tprev, s_log, s_btprev, s_bpprev;
   __shared__ double s_cpref[kSmemChunks];
@@ -214,15 +232,32 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample(SampleArgs A) {
     return;
   }
   // (3) rejection rounds
-  const int64_t nskip = (A.n_local + kSkipRows - 1) / kSkipRows;
+  // skip granularity: the smallest power of two that fits the table in shared memory (one
+  // row: the whole cpre, no global load on the draw's path), at most 64 rows
+  int sg = 1;
+  while (sg < kSkipRows && (A.n_local + sg - 1) / sg > kSkipMax) sg *= 2;
+  const int64_t nskip = (A.n_local + sg - 1) / sg;
   const bool use_skip = nskip <= kSkipMax;
   if (use_skip) {
-    for (int64_t j = tid; j < nskip; j += kSampleThreads) {
-      const int64_t r = j * kSkipRows + kSkipRows - 1;
-      s_skip[j] = A.cpre[r < A.n_local ? r : A.n_local - 1];
+    constexpr int U = kSkipMax / kSampleThreads;   // all loads in flight before the stores
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t j = tid + (int64_t)u * kSampleThreads, r = j * sg + sg - 1;
+      v[u] = j < nskip ? A.cpre[r < A.n_local ? r : A.n_local - 1] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t j = tid + (int64_t)u * kSampleThreads;
+      if (j < nskip) s_skip[j] = v[u];
     }
     __syncthreads();
   }
+  for (int h = tid; h < kHashSize; h += kSampleThreads) {
+    hkey[h] = ~0ull;
+    hidx[h] = kSampleThreads;
+  }
+  __syncthreads();
   const double total = s_total;
   const uint2 key = make_uint2((uint32_t)(A.seed & 0xffffffffu), (uint32_t)(A.seed >> 32));
   const uint32_t t = (uint32_t)st->t;
@@ -248,20 +283,27 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample(SampleArgs A) {
       row = resolve_in_chunk(q, 1e308, A.cpre, A.dvec, A.n_local, A.row_offset);
     } else {
       const double tq = target - (a > 0 ? cpf[a - 1] : 0.0);
-      row = resolve_in_chunk(a, tq, A.cpre, A.dvec, A.n_local, A.row_offset, use_skip ? s_skip : nullptr);
+      row = resolve_in_chunk(a, tq, A.cpre, A.dvec, A.n_local, A.row_offset, use_skip ? s_skip : nullptr, sg);
     }
-    cand[tid] = row;
+    // repeats: a shared hash set of the rows seen, hidx = the first draw of this round that
+    // hit the row, or -1 once the row is in S_t (reading R6: repeats rejected in draw order)
+    int slot = -1;
+    if (row >= 0) {
+      slot = hash_slot(hkey, row);
+      atomicMin(&hidx[slot], tid);
+    }
     __syncthreads();
-    int isnew = row >= 0;
-    for (int m = 0; m < c && isnew; ++m) isnew = chosen[m] != row;
-    for (int m = 0; m < tid && isnew; ++m) isnew = cand[m] != row;
+    int isnew = slot >= 0 && hidx[slot] == tid;
     unsigned msk = __ballot_sync(0xffffffffu, isnew);
     if (lane == 0) wcount[w] = __popc(msk);
     __syncthreads();
     int off = 0;
     for (int q = 0; q < w; ++q) off += wcount[q];
     off += __popc(msk & ((1u << lane) - 1u));
-    if (isnew && c + off < bt) chosen[c + off] = row;
+    if (isnew && c + off < bt) {
+      chosen[c + off] = row;
+      hidx[slot] = -1;
+    }
     if (isnew && c + off == bt - 1) s_new = (int)(jb + tid + 1);   // draws consumed
     __syncthreads();
     if (tid == 0) {
@@ -357,6 +399,8 @@ __global__ void __launch_bounds__(kSampleRound) k_draw_accept(SampleArgs A) {
   __shared__ int64_t chosen[kMaxB];
   __shared__ int64_t cand[kSampleRound];
   __shared__ int wcount[kSampleRound / 32];
+  __shared__ unsigned long long hkey[kHashSize];
+  __shared__ int hidx[kHashSize];
   const int bt = st->b_t;
   const int c = st->sample_c;
   for (int i = tid; i < c; i += kSampleRound) chosen[i] = A.S_t[i];
@@ -375,9 +419,22 @@ __global__ void __launch_bounds__(kSampleRound) k_draw_accept(SampleArgs A) {
     }
     return;
   }
-  int isnew = row >= 0;
-  for (int m = 0; m < c && isnew; ++m) isnew = chosen[m] != row;
-  for (int m = 0; m < tid && isnew; ++m) isnew = cand[m] != row;
+  // repeats (reading R6, draw order): S_t's rows so far enter the hash set with hidx = -1,
+  // then every draw's row with atomicMin of its index
+  for (int h = tid; h < kHashSize; h += kSampleRound) {
+    hkey[h] = ~0ull;
+    hidx[h] = kSampleRound;
+  }
+  __syncthreads();
+  for (int i = tid; i < c; i += kSampleRound) hidx[hash_slot(hkey, chosen[i])] = -1;
+  __syncthreads();
+  int slot = -1;
+  if (row >= 0) {
+    slot = hash_slot(hkey, row);
+    atomicMin(&hidx[slot], tid);
+  }
+  __syncthreads();
+  const int isnew = slot >= 0 && hidx[slot] == tid;
   const unsigned msk = __ballot_sync(0xffffffffu, isnew);
   if (lane == 0) wcount[w] = __popc(msk);
   __syncthreads();
