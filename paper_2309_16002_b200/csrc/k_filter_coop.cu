@@ -766,6 +766,22 @@ __global__ void __launch_bounds__(kFiltThreads, 1) k_filter_coop(FilterArgs F) {
     if (c0 + c >= d) continue;
     Qt[(int64_t)i * d + c0 + c] = (T)(i < bq ? Vs[i * kFiltLd + c] : 0.0);
   }
+  if (F.Qp && bq <= 64) {
+    // Q_b's two packed images for the 64-row-tile projection (k_pack_q's layout, which the
+    // projection would otherwise build in a launch of its own): this CTA's 32 columns, zero
+    // rows [b', 64), and (last CTA, at a chunk start) the zero columns of its chunk past d
+    const int64_t nc = (d + 63) / 64;
+    double* Q2 = F.Qp + nc * 64 * 64;
+    const int cw = (blockIdx.x == gridDim.x - 1 && c0 % 64 == 0) ? 64 : kFiltCW;
+    for (int e = tid; e < 64 * cw; e += kFiltThreads) {
+      const int j = e / cw, cl = e - (e / cw) * cw;
+      const int64_t gc = c0 + cl, ch = gc / 64;
+      const int col = (int)(gc - ch * 64), pr = j >> 1;
+      const double v = (j < bq && cl < kFiltCW && gc < d) ? Vs[j * kFiltLd + cl] : 0.0;
+      F.Qp[(ch * 64 + j) * 64 + pack_qswz(j, col)] = v;
+      Q2[ch * 64 * 64 + (pr * 64 + (col ^ (2 * (pr & 3)))) * 2 + (j & 1)] = v;
+    }
+  }
   stamp(F.dbg, 9);
 }
 

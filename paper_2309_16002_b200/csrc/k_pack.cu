@@ -17,9 +17,6 @@ constexpr int KC = 64;          // columns per chunk (k_lhat_paper lp::KC)
 constexpr int PACK_ROWS = 64;   // rows of the packed buffer (lp::PACK_ROWS)
 }  // namespace pk
 
-__host__ __device__ __forceinline__ int pk_qswz(int j, int col) {
-  return col ^ (8 * (j & 1)) ^ (4 * ((j >> 1) & 3));
-}
 
 // part < 0: rows [0, b'), b' <= 64.  part >= 0 (b' > pw split into balanced parts of <= pw
 // rows, part_range): rows [r0, r0 + cnt).
@@ -38,7 +35,7 @@ __global__ void k_pack_q(const QT* __restrict__ Qt, int64_t d, double* __restric
   const int c = blockIdx.x, j = blockIdx.y, col = threadIdx.x;   // blockDim = KC
   const int64_t gc = (int64_t)c * pk::KC + col;
   const double v = (j < bp && gc < d) ? (double)Qt[(int64_t)(r0 + j) * ldq + gc] : 0.0;
-  Qp[((int64_t)c * pk::PACK_ROWS + j) * pk::KC + pk_qswz(j, col)] = v;
+  Qp[((int64_t)c * pk::PACK_ROWS + j) * pk::KC + pack_qswz(j, col)] = v;
   const int pr = j >> 1;
   double* Q2 = Qp + (int64_t)gridDim.x * pk::PACK_ROWS * pk::KC + (int64_t)c * pk::PACK_ROWS * pk::KC;
   Q2[(pr * pk::KC + (col ^ (2 * (pr & 3)))) * 2 + (j & 1)] = v;

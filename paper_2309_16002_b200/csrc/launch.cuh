@@ -76,6 +76,7 @@ struct FilterArgs {
   int64_t* S;               // skeleton list: S'_t appended at [k, k+b')
   void* Qt;                 // out: Q_b rows (dtype T), ld d; rows [b', bp_pad) zero
   int bp_pad;
+  double* Qp = nullptr;     // optional: also write Q_b's packed images (k_pack.cu layout) when b' <= 64
   long long* dbg;           // optional: %globaltimer stamps of the phases (CTA 0)
 };
 template <typename T>
@@ -103,6 +104,11 @@ cudaError_t launch_update_mma(double* Xres, int64_t ldx, const double* Qt, const
                               int bucket, cudaStream_t s);
 // k_pack.cu — Q_b packed in the shared-memory image of k_lhat_paper (two images)
 size_t fused_pack_bytes(int64_t d);
+// Q_b image 1 of the packed layout (k_pack.cu): row j, column col of a 64-column chunk at
+// j * 64 + pack_qswz(j, col) (conflict-free B fragments of the L-hat pass)
+__host__ __device__ __forceinline__ int pack_qswz(int j, int col) {
+  return col ^ (8 * (j & 1)) ^ (4 * ((j >> 1) & 3));
+}
 // Qt: rows of Q_b (leading dimension ldq, 0 -> d), d columns packed
 // part >= 0: rows of part_range(b', part, pw)
 cudaError_t launch_pack_q(const double* Qt, int64_t d, double* Qp, DevState* st, cudaStream_t s, int part = -1,

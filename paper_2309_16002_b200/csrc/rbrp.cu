@@ -378,6 +378,14 @@ cudaError_t launch_block_sample(Ctx<T>& c, SampleArgs& sa, cudaStream_t s, int* 
   return launch_sample(sa, s);
 }
 
+// b' <= 64 on the 64-row-tile kernel: the filter writes Q_b's packed images itself (no
+// k_pack_q launch); RBRP_NO_FUSE_PACK=1 restores the separate launch
+template <typename T>
+bool fuse_pack(const Ctx<T>& c) {
+  static const bool off = env_on("RBRP_NO_FUSE_PACK");
+  return !off && !c.tc32 && (c.paper || c.tiled) && c.lp_max > 0;
+}
+
 // a4 (Alg. 2 l.13 + l.16): the 64-row-tile kernel k_lhat_paper (L-hat pass + update pass
 // per tile) for the buckets it supports, else the two-kernel DMMA / CUDA-core path.  Each
 // launch is a no-op unless the block's b' falls in its bucket, so the sequence is
@@ -401,7 +409,7 @@ int enqueue_projection(Ctx<T>& c, cudaStream_t s, int* nl) {
     return RBRP_OK;
   }
   const int fmax = (c.paper || c.tiled) ? c.lp_max : 0;
-  if (fmax > 0 && (rc = lk(launch_pack_q(c.Qt, c.d, c.Qp, c.st, s)))) return rc;
+  if (fmax > 0 && !fuse_pack(c) && (rc = lk(launch_pack_q(c.Qt, c.d, c.Qp, c.st, s)))) return rc;
   bool need_downdate = false;
   // b' above the widest 64-row-tile kernel (64 columns fp64, 32 fp32): balanced parts of
   // <= lp_max columns in sequence (RBRP_NO_PARTS=1: the two-kernel path instead)
@@ -490,6 +498,7 @@ int enqueue_block(Ctx<T>& c, SampleArgs& sa, cudaStream_t s, Prof* prof, int* nl
   fa.S = c.S;
   fa.Qt = c.Qt;
   fa.bp_pad = c.bucketB;
+  fa.Qp = fuse_pack(c) ? c.Qp : nullptr;
   fa.dbg = c.dbg;
   LK(launch_filter_coop<T>(fa, s));
   if (prof) prof->end();
@@ -1237,6 +1246,7 @@ int run_dist(int nsh, const rbrp_problem* ps, void* const* Xs, char* const* wss,
       fa.S = c.S;
       fa.Qt = c.Qt;
       fa.bp_pad = c.bucketB;
+      fa.Qp = fuse_pack(c) ? c.Qp : nullptr;
       fa.dbg = nullptr;
       LKS(launch_filter_coop<T>(fa, ss));
     }
