@@ -465,7 +465,7 @@ __device__ void cta_trinv_warp(const double* R, int ldr, const int* perm, int bp
 // partial Gram of the nb x 32 slice S (stride kFiltLd) -> out (kMaxB x kMaxB)
 // partial Gram of this CTA's 32 columns: out(i, j) = sum_c S(i, c) S(j, c), i, j < nb, in
 // 4 x 4 register tiles (8 shared loads per 16 fmas, 16 independent chains per thread)
-__device__ void slice_gram(const double* S, int nb, double* out) {
+__device__ void slice_gram(const double* S, int nb, double* out, int ldo = kMaxB) {
   const int nt = (nb + 3) >> 2;   // 4-row tiles per side
   for (int t = threadIdx.x; t < nt * nt; t += blockDim.x) {
     const int ti = t / nt, tj = t - ti * nt;
@@ -492,7 +492,7 @@ __device__ void slice_gram(const double* S, int nb, double* out) {
     for (int a = 0; a < 4; ++a)
 #pragma unroll
       for (int b = 0; b < 4; ++b)
-        if (i0 + a < nb && j0 + b < nb) out[(i0 + a) * kMaxB + j0 + b] = acc[a][b];
+        if (i0 + a < nb && j0 + b < nb) out[(i0 + a) * ldo + j0 + b] = acc[a][b];
   }
 }
 __device__ void reduce_slices(const double* Gpart, int nsplit, int nb, double* G) {
@@ -511,6 +511,31 @@ __device__ void reduce_slices(const double* Gpart, int nsplit, int nb, double* G
       for (int u = 0; u < 8; ++u) s += x[u];
     }
     for (; q < nsplit; ++q) s += src[(int64_t)q * kMaxB * kMaxB];
+    G[i * kMaxB + j] = s;
+  }
+}
+
+// cluster mode, nb <= 32: every CTA sums the nsplit partial Grams (nb x nb, stride 32, in
+// the shared memory of the cluster's CTAs, read over DSMEM) in rank order -- the order of
+// reduce_slices -- into its own copy G (stride kMaxB); no second barrier
+__device__ void reduce_dsmem(double* part, int nsplit, int nb, double* G) {
+  cg::cluster_group cl = cg::this_cluster();
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+    const int i = e / nb, j = e - (e / nb) * nb;
+    double x[8];
+    double s = 0.0;
+    int q = 0;
+    for (; q + 8 <= nsplit; q += 8) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) x[u] = cl.map_shared_rank(part, q + u)[i * 32 + j];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s += x[u];
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x[u] = q + u < nsplit ? cl.map_shared_rank(part, q + u)[i * 32 + j] : 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (q + u < nsplit) s += x[u];
     G[i * kMaxB + j] = s;
   }
 }
@@ -542,6 +567,13 @@ __device__ void apply_T(const double* Tm, int ldt, int rows, const double* In, c
   }
 }
 
+// dynamic shared memory: V, Q1, R (and, nb <= 64, G, T, R11) -- then, cluster mode, two
+// 32 x 32 partial Grams read by the other CTAs of the cluster
+constexpr size_t filter_smem_small = 2 * kMaxB * kFiltLd + 4 * kSmallNb * (kSmallNb + 1);
+constexpr size_t filter_smem_large = 2 * kMaxB * kFiltLd + kMaxB * (kMaxB + 1);
+constexpr size_t filter_smem_base =
+    sizeof(double) * (filter_smem_small > filter_smem_large ? filter_smem_small : filter_smem_large);
+
 __device__ __forceinline__ void stamp(long long* dbg, int k) {
   if (dbg && blockIdx.x == 0 && threadIdx.x == 0) {
     unsigned long long t;
@@ -553,6 +585,17 @@ __device__ __forceinline__ void stamp(long long* dbg, int k) {
 template <typename T>
 __global__ void __launch_bounds__(kFiltThreads, 1) k_filter_coop(FilterArgs F) {
   cg::grid_group grid = cg::this_grid();
+  // the grid barrier: a cooperative launch's grid.sync(), or for d <= 8 * 32 a thread-block
+  // cluster of the whole grid and its hardware barrier (release / acquire at cluster scope;
+  // the partial Grams go through global memory either way)
+  auto gsync = [&]() {
+    if (F.cluster) {
+      __threadfence();
+      cg::this_cluster().sync();
+    } else {
+      grid.sync();
+    }
+  };
   stamp(F.dbg, 0);
   extern __shared__ double smd[];
   __shared__ int perm[kMaxB], perm2[kMaxB], s_ch[kMaxB];
@@ -614,13 +657,24 @@ __global__ void __launch_bounds__(kFiltThreads, 1) k_filter_coop(FilterArgs F) {
     }
   }
   __syncthreads();
-  slice_gram(Vs, nb, Gp);
+  // cluster mode with nb <= 32: partial Grams in shared memory, reduced over DSMEM by every
+  // CTA into its own slot of Gpart (no global round trip between CTAs, one barrier per
+  // reduction instead of two)
+  const bool dsm = F.cluster && nb <= 32;
+  double* Gl = smd + filter_smem_base / sizeof(double);   // [2][32 x 32]
+  const double* Gr = dsm ? Gp : F.G;                        // the reduced Gram, stride kMaxB
+  slice_gram(Vs, nb, dsm ? Gl : Gp, dsm ? 32 : kMaxB);
   stamp(F.dbg, 1);
-  grid.sync();
+  gsync();
   stamp(F.dbg, 2);
   // B
-  reduce_slices(F.Gpart, nsplit, nb, F.G);
-  grid.sync();
+  if (dsm) {
+    reduce_dsmem(Gl, nsplit, nb, Gp);
+    __syncthreads();
+  } else {
+    reduce_slices(F.Gpart, nsplit, nb, F.G);
+    gsync();
+  }
   stamp(F.dbg, 3);
   // C: pivoted Cholesky + filter + T11 = R11^{-1} (redundant in every CTA).  b_t <= 64:
   // register-resident fast path; larger blocks: shared/L2 path + column-parallel inverse.
@@ -632,9 +686,9 @@ __global__ void __launch_bounds__(kFiltThreads, 1) k_filter_coop(FilterArgs F) {
     const double tb = st->tau_b < 0.0 ? 1.0 / nb : st->tau_b;
     int kept;
     if (nb <= 32) {
-      kept = cta_chol_inv<4>(F.G, nb, 1, F.forced, tb, Rs, ldr, Ts, ldt, perm, s_mass, s_dg, s_ch, &s_rd);
+      kept = cta_chol_inv<4>(Gr, nb, 1, F.forced, tb, Rs, ldr, Ts, ldt, perm, s_mass, s_dg, s_ch, &s_rd);
     } else if (small) {
-      kept = cta_chol_inv<16>(F.G, nb, 1, F.forced, tb, Rs, ldr, Ts, ldt, perm, s_mass, s_dg, s_ch, &s_rd);
+      kept = cta_chol_inv<16>(Gr, nb, 1, F.forced, tb, Rs, ldr, Ts, ldt, perm, s_mass, s_dg, s_ch, &s_rd);
     } else {
       kept = cta_pivchol_reg(F.G, nb, 1, F.forced, tb, Rs, ldr, perm, s_mass, &s_rd);
       __syncthreads();
@@ -668,18 +722,29 @@ __global__ void __launch_bounds__(kFiltThreads, 1) k_filter_coop(FilterArgs F) {
       }
     }
   }
-  if (bp == 0) return;   // uniform
+  if (bp == 0) {   // uniform
+    if (dsm) cg::this_cluster().sync();   // the peers are done reading this CTA's partial Gram
+    return;
+  }
   __syncthreads();
   // D: Q1(:, cols) = V(:, pi(1:b')) T11, partial Gram of Q1
   apply_T(Ts, ldt, bp, Vs, perm, Q1s);
   __syncthreads();
-  slice_gram(Q1s, bp, Gp);
+  slice_gram(Q1s, bp, dsm ? Gl + 32 * 32 : Gp, dsm ? 32 : kMaxB);
   stamp(F.dbg, 5);
-  grid.sync();
+  gsync();
   stamp(F.dbg, 6);
   // E
-  reduce_slices(F.Gpart, nsplit, bp, F.G);
-  grid.sync();
+  if (dsm) {
+    reduce_dsmem(Gl + 32 * 32, nsplit, bp, Gp);
+    // this CTA is done reading its peers' shared memory; it may not exit before they are
+    // done reading its own (cluster_done() before every exit below)
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    __syncthreads();
+  } else {
+    reduce_slices(F.Gpart, nsplit, bp, F.G);
+    gsync();
+  }
   stamp(F.dbg, 7);
   // F: CholQR2 pass (R2 into Rs, T2 = R2^{-1} into Ts).  G2 = I + E: if max|E| is small
   // (the usual case) a parallel perturbation expansion, else the exact Cholesky.
@@ -688,7 +753,7 @@ __global__ void __launch_bounds__(kFiltThreads, 1) k_filter_coop(FilterArgs F) {
     double em = 0.0;
     for (int e = tid; e < bp * bp; e += kFiltThreads) {
       const int i = e / bp, j = e - (e / bp) * bp;
-      const double x = F.G[i * kMaxB + j] - (i == j ? 1.0 : 0.0);
+      const double x = Gr[i * kMaxB + j] - (i == j ? 1.0 : 0.0);
       Gs[i * ldg + j] = x;
       em = fmax(em, fabs(x));
     }
@@ -717,9 +782,9 @@ __global__ void __launch_bounds__(kFiltThreads, 1) k_filter_coop(FilterArgs F) {
   } else {
     int rd2, kept;
     if (bp <= 32 && small) {
-      kept = cta_chol_inv<4>(F.G, bp, 2, nullptr, 0.0, Rs, ldr, Ts, ldt, perm2, nullptr, s_dg, s_ch, &rd2);
+      kept = cta_chol_inv<4>(Gr, bp, 2, nullptr, 0.0, Rs, ldr, Ts, ldt, perm2, nullptr, s_dg, s_ch, &rd2);
     } else if (small) {
-      kept = cta_chol_inv<16>(F.G, bp, 2, nullptr, 0.0, Rs, ldr, Ts, ldt, perm2, nullptr, s_dg, s_ch, &rd2);
+      kept = cta_chol_inv<16>(Gr, bp, 2, nullptr, 0.0, Rs, ldr, Ts, ldt, perm2, nullptr, s_dg, s_ch, &rd2);
     } else {
       for (int e = tid; e < bp * bp; e += kFiltThreads) Gs[(e / bp) * ldg + e % bp] = F.G[(e / bp) * kMaxB + e % bp];
       __syncthreads();
@@ -755,7 +820,13 @@ __global__ void __launch_bounds__(kFiltThreads, 1) k_filter_coop(FilterArgs F) {
       if (bq == 0) st->stop = 1;
     }
   }
-  if (bq == 0) return;
+  auto cluster_done = [&]() {
+    if (dsm) asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  };
+  if (bq == 0) {
+    cluster_done();
+    return;
+  }
   // G: Q_b(:, cols) = Q1 T2 -> Vs (free now) -> Qt
   apply_T(Ts, ldt, bq, Q1s, nullptr, Vs);
   __syncthreads();
@@ -782,14 +853,11 @@ __global__ void __launch_bounds__(kFiltThreads, 1) k_filter_coop(FilterArgs F) {
       Q2[ch * 64 * 64 + (pr * 64 + (col ^ (2 * (pr & 3)))) * 2 + (j & 1)] = v;
     }
   }
+  cluster_done();
   stamp(F.dbg, 9);
 }
 
-static size_t filter_smem() {
-  const size_t small = 2 * kMaxB * kFiltLd + 4 * kSmallNb * (kSmallNb + 1);
-  const size_t large = 2 * kMaxB * kFiltLd + kMaxB * (kMaxB + 1);
-  return sizeof(double) * (small > large ? small : large);
-}
+static size_t filter_smem() { return filter_smem_base + 2 * 32 * 32 * sizeof(double); }
 
 template <typename T>
 cudaError_t launch_filter_coop(const FilterArgs& a, cudaStream_t s) {
@@ -799,18 +867,30 @@ cudaError_t launch_filter_coop(const FilterArgs& a, cudaStream_t s) {
   cudaError_t ae = attr.once(
       [&] { return cudaFuncSetAttribute(k_filter_coop<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
   if (ae != cudaSuccess) return ae;
-  // cooperative launch through cudaLaunchKernelEx so that it can be captured in a graph
+  // cooperative launch through cudaLaunchKernelEx so that it can be captured in a graph; a
+  // grid of at most 8 CTAs runs as one thread-block cluster instead (hardware cluster barrier
+  // in place of the cooperative grid barrier; RBRP_FILTER_COOP=1 keeps the cooperative launch)
+  static const bool coop_only = getenv("RBRP_FILTER_COOP") && getenv("RBRP_FILTER_COOP")[0] == '1';
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nsplit);
   cfg.blockDim = dim3(kFiltThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute la[1];
-  la[0].id = cudaLaunchAttributeCooperative;
-  la[0].val.cooperative = 1;
+  FilterArgs b = a;
+  b.cluster = !coop_only && nsplit <= 8;
+  if (b.cluster) {
+    la[0].id = cudaLaunchAttributeClusterDimension;
+    la[0].val.clusterDim.x = (unsigned)nsplit;
+    la[0].val.clusterDim.y = 1;
+    la[0].val.clusterDim.z = 1;
+  } else {
+    la[0].id = cudaLaunchAttributeCooperative;
+    la[0].val.cooperative = 1;
+  }
   cfg.attrs = la;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_filter_coop<T>, a);
+  return cudaLaunchKernelEx(&cfg, k_filter_coop<T>, b);
 }
 
 int filter_coop_nsplit(int64_t d) { return ceil_div(d, kFiltCW); }

@@ -76,6 +76,7 @@ struct FilterArgs {
   int64_t* S;               // skeleton list: S'_t appended at [k, k+b')
   void* Qt;                 // out: Q_b rows (dtype T), ld d; rows [b', bp_pad) zero
   int bp_pad;
+  int cluster = 0;          // set by launch_filter_coop: the grid is one thread-block cluster
   double* Qp = nullptr;     // optional: also write Q_b's packed images (k_pack.cu layout) when b' <= 64
   long long* dbg;           // optional: %globaltimer stamps of the phases (CTA 0)
 };
