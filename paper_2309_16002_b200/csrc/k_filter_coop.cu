@@ -870,7 +870,8 @@ cudaError_t launch_filter_coop(const FilterArgs& a, cudaStream_t s) {
   // cooperative launch through cudaLaunchKernelEx so that it can be captured in a graph; a
   // grid of at most 8 CTAs runs as one thread-block cluster instead (hardware cluster barrier
   // in place of the cooperative grid barrier; RBRP_FILTER_COOP=1 keeps the cooperative launch)
-  static const bool coop_only = getenv("RBRP_FILTER_COOP") && getenv("RBRP_FILTER_COOP")[0] == '1';
+  const char* ec = getenv("RBRP_FILTER_COOP");
+  const bool coop_only = ec && ec[0] == '1';
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nsplit);
   cfg.blockDim = dim3(kFiltThreads);

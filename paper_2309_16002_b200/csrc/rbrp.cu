@@ -382,8 +382,7 @@ cudaError_t launch_block_sample(Ctx<T>& c, SampleArgs& sa, cudaStream_t s, int* 
 // k_pack_q launch); RBRP_NO_FUSE_PACK=1 restores the separate launch
 template <typename T>
 bool fuse_pack(const Ctx<T>& c) {
-  static const bool off = env_on("RBRP_NO_FUSE_PACK");
-  return !off && !c.tc32 && (c.paper || c.tiled) && c.lp_max > 0;
+  return !env_on("RBRP_NO_FUSE_PACK") && !c.tc32 && (c.paper || c.tiled) && c.lp_max > 0;
 }
 
 // a4 (Alg. 2 l.13 + l.16): the 64-row-tile kernel k_lhat_paper (L-hat pass + update pass

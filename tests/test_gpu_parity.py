@@ -301,6 +301,28 @@ def test_simt_and_mma_projection_paths_agree(monkeypatch):
 
 
 @cuda
+@pytest.mark.parametrize("b,d", [(16, 200), (32, 256), (16, 1024)])
+def test_filter_variants_bit_identical(monkeypatch, b, d):
+    """The filter's launch variants compute the same numbers in the same order: the
+    thread-block cluster with DSMEM reductions (d <= 256) against the cooperative grid,
+    Q_b's packed images written by the filter against k_pack_q.  Identical S, b', rho, W
+    (bitwise), and the oracle's S on this seed."""
+    rb = _rb()
+    cfg = small_config("c1", n=3000, d=d, b=b)
+    X = make(cfg, device="cuda")
+    base = rb.id(X, k=48, b=b, seed=5)
+    ores = O.rbrp(X.cpu().numpy(), k=48, b=b, seed=5)
+    assert base.S.tolist() == list(ores.S)
+    for env in ("RBRP_FILTER_COOP", "RBRP_NO_FUSE_PACK"):
+        monkeypatch.setenv(env, "1")
+        r = rb.id(X, k=48, b=b, seed=5)
+        monkeypatch.delenv(env)
+        assert r.S.tolist() == base.S.tolist(), env
+        assert r.b_prime == base.b_prime and r.rho == base.rho, env
+        assert torch.equal(r.W, base.W), env
+
+
+@cuda
 def test_graph_loop_equals_eager_loop(monkeypatch):
     """The block loop as one CUDA graph (conditional WHILE node) and the eager,
     host-driven loop launch the same kernels: identical S, b', rho and W."""
