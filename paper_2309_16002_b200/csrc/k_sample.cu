@@ -23,6 +23,7 @@ static_assert(kMaxB + kSampleThreads <= kHashSize / 2 && kMaxB + kSampleRound <=
 
 constexpr int kSkipRows = 64;       // rows per entry of the shared skip table
 constexpr int kSkipMax = 2048;      // skip table in shared memory up to 131072 local rows
+static_assert(kMaxB <= kSampleThreads, "one block-log entry per thread");
 
 // smallest local row r of global chunk q with cpre[r] > tq; falls back to the last
 // positive row of the chunk when tq is past the chunk's end (rounding).  skip (optional):
@@ -71,7 +72,16 @@ __device__ __forceinline__ int hash_slot(unsigned long long* hkey, int64_t row) 
   }
 }
 
+__device__ __forceinline__ void sstamp(long long* dbg, int k) {
+  if (dbg && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    dbg[k] = (long long)t;
+  }
+}
+
 __global__ void __launch_bounds__(kSampleThreads) k_sample(SampleArgs A) {
+  sstamp(A.dbg, 0);
   DevState* st = A.st;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   __shared__ int s_stop, s_bt, s_c, s_new;
@@ -81,34 +91,37 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample(SampleArgs A) {
   __shared__ unsigned long long hkey[kHashSize];
   __shared__ int hidx[kHashSize];
   __shared__ int wcount[kSampleThreads / 32];
-  __shared__ int s_tprev, s_log, s_btprev, s_bpprev;
+  __shared__ int s_tcur;
   __shared__ double s_cpref[kSmemChunks];
   __shared__ double s_skip[kSkipMax];
 
-  // log the block that just finished (device-side, read by the host at the end)
-  if (tid == 0) {
-    s_tprev = st->t;
-    s_btprev = st->b_t;
-    s_bpprev = st->b_prime;
-    s_log = (!A.first && s_tprev >= 1 && s_tprev > st->nlogged && s_tprev <= A.log.maxlog &&
-             A.log.bt != nullptr);
-  }
-  __syncthreads();
-  if (s_log) {
-    const int slot = s_tprev - 1;
-    for (int i = tid; i < A.log.b; i += kSampleThreads) {
-      A.log.St[(int64_t)slot * A.log.b + i] = i < s_btprev ? A.S_t[i] : -1;
-      A.log.piv[(int64_t)slot * A.log.b + i] = i < s_bpprev ? A.piv[i] : -1;
-    }
-    if (tid == 0) {
-      A.log.bt[slot] = s_btprev;
-      A.log.bp[slot] = s_bpprev;
-      A.log.ts[2 * slot] = st->ts0;
-      A.log.ts[2 * slot + 1] = st->ts1;
+  // one round of global loads for the whole prologue: warp 1 snapshots DevState into shared
+  // memory while warp 0 loads the chunk totals (the stop test below reads only the snapshot);
+  // every thread also loads its entries of the skip table and of the block log
+  // skip granularity: the smallest power of two that fits the table in shared memory (one
+  // row: the whole cpre, no global load on the draw's path), at most 64 rows
+  int sg = 1;
+  while (sg < kSkipRows && (A.n_local + sg - 1) / sg > kSkipMax) sg *= 2;
+  const int64_t nskip = (A.n_local + sg - 1) / sg;
+  const bool use_skip = nskip <= kSkipMax && A.replay_len < 0 && !A.greedy && !A.dist;
+  constexpr int kSkipU = kSkipMax / kSampleThreads;
+  double skv[kSkipU];
+  if (use_skip) {
+#pragma unroll
+    for (int u = 0; u < kSkipU; ++u) {
+      const int64_t j = tid + (int64_t)u * kSampleThreads, r = j * sg + sg - 1;
+      skv[u] = j < nskip ? A.cpre[r < A.n_local ? r : A.n_local - 1] : 0.0;
     }
   }
-
-  // the previous block's kept skeletons become part of S (Alg. 2 l.14)
+  const bool may_log = !A.first && A.log.bt != nullptr && tid < A.log.b;
+  const int64_t lg_st = may_log ? A.S_t[tid] : -1;
+  const int32_t lg_pv = may_log ? A.piv[tid] : -1;
+  __shared__ DevState s_st;
+  static_assert(sizeof(DevState) % 8 == 0, "DevState snapshot by 8-byte words");
+  constexpr int kStWords = (int)(sizeof(DevState) / 8);
+  static_assert(kStWords <= 32, "one warp snapshots DevState");
+  if (w == 1 && lane < kStWords)
+    reinterpret_cast<unsigned long long*>(&s_st)[lane] = reinterpret_cast<const unsigned long long*>(st)[lane];
   // (1) chunk prefix, fixed order: lane l sums a contiguous range of chunks
   if (w == 0) {
     const int nch = A.nchunks;
@@ -136,44 +149,69 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample(SampleArgs A) {
     if (lane == 0) s_np = np;
   }
   __syncthreads();
+  sstamp(A.dbg, 1);
+  // log the block that just finished (device-side, read by the host at the end)
+  const int tprev = s_st.t, btprev = s_st.b_t, bpprev = s_st.b_prime;
+  const bool do_log = (!A.first && tprev >= 1 && tprev > s_st.nlogged && tprev <= A.log.maxlog &&
+                    A.log.bt != nullptr);
+  if (do_log) {
+    const int slot = tprev - 1;
+    if (tid < A.log.b) {   // A.log.b = b <= kMaxB <= kSampleThreads
+      A.log.St[(int64_t)slot * A.log.b + tid] = tid < btprev ? lg_st : -1;
+      A.log.piv[(int64_t)slot * A.log.b + tid] = tid < bpprev ? lg_pv : -1;
+    }
+    if (tid == 0) {
+      A.log.bt[slot] = btprev;
+      A.log.bp[slot] = bpprev;
+      A.log.ts[2 * slot] = s_st.ts0;
+      A.log.ts[2 * slot + 1] = s_st.ts1;
+    }
+  }
+  sstamp(A.dbg, 2);
   if (tid == 0) {
     const double total = s_total;
-    st->k += st->b_prime;          // l.14: S <- S u S'_t of the previous block
+    const int64_t k = s_st.k + s_st.b_prime;   // l.14: S <- S u S'_t of the previous block
+    const double D0 = A.first ? total : s_st.D0;
+    uint32_t flags = s_st.flags;
+    st->k = k;
     st->b_prime = 0;
     st->total = total;
     st->npos = s_np;
     if (A.first) st->D0 = total;
-    if (s_log) {
-      A.log.rho[s_tprev - 1] = total / st->D0;
-      st->nlogged = s_tprev;
+    if (do_log) {
+      A.log.rho[tprev - 1] = total / D0;
+      st->nlogged = tprev;
     }
-    const bool fixed = !(st->tau > 0.0);
-    bool stop = st->stop != 0;
-    if (!stop && st->k >= st->k_cap) {
+    const bool fixed = !(s_st.tau > 0.0);
+    bool stop = s_st.stop != 0;
+    if (!stop && k >= s_st.k_cap) {
       stop = true;
-      if (!fixed && total > st->tau * st->D0) st->flags |= RBRP_F_TOL_UNREACHED;
+      if (!fixed && total > s_st.tau * D0) flags |= RBRP_F_TOL_UNREACHED;
     }
-    if (!stop && !fixed && !(total > st->tau * st->D0)) stop = true;   // l.3
+    if (!stop && !fixed && !(total > s_st.tau * D0)) stop = true;   // l.3
     if (!stop && s_np == 0) {
       stop = true;
-      st->flags |= RBRP_F_SUPPORT_EXHAUSTED;
+      flags |= RBRP_F_SUPPORT_EXHAUSTED;
     }
     if (!stop && A.replay_len == -2) stop = true;   // replay log exhausted
     int bt = 0;
     if (!stop) {
-      st->t += 1;                                                     // l.4
-      int64_t room = st->k_cap - st->k;
-      bt = (int)(st->b < room ? st->b : room);
+      st->t = s_st.t + 1;                                             // l.4
+      const int64_t room = s_st.k_cap - k;
+      bt = (int)(s_st.b < room ? s_st.b : room);
     }
+    if (flags != s_st.flags) st->flags = flags;
     st->stop = stop ? 1 : 0;
     s_stop = stop;
     s_bt = bt;
     s_c = 0;
+    s_tcur = stop ? s_st.t : s_st.t + 1;
     if (A.cond) cudaGraphSetConditional((cudaGraphConditionalHandle)A.cond, stop ? 0u : 1u);
     // row-sharded graph loop: the draw rounds run while this block still needs rows
     if (A.cond2) cudaGraphSetConditional((cudaGraphConditionalHandle)A.cond2, stop ? 0u : 1u);
   }
   __syncthreads();
+  sstamp(A.dbg, 3);
   if (s_stop) return;
   if (A.dist && A.replay_len < 0) {   // drawing happens in the resolve / accept rounds
     if (tid == 0) {
@@ -232,24 +270,11 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample(SampleArgs A) {
     return;
   }
   // (3) rejection rounds
-  // skip granularity: the smallest power of two that fits the table in shared memory (one
-  // row: the whole cpre, no global load on the draw's path), at most 64 rows
-  int sg = 1;
-  while (sg < kSkipRows && (A.n_local + sg - 1) / sg > kSkipMax) sg *= 2;
-  const int64_t nskip = (A.n_local + sg - 1) / sg;
-  const bool use_skip = nskip <= kSkipMax;
   if (use_skip) {
-    constexpr int U = kSkipMax / kSampleThreads;   // all loads in flight before the stores
-    double v[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t j = tid + (int64_t)u * kSampleThreads, r = j * sg + sg - 1;
-      v[u] = j < nskip ? A.cpre[r < A.n_local ? r : A.n_local - 1] : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
+    for (int u = 0; u < kSkipU; ++u) {
       const int64_t j = tid + (int64_t)u * kSampleThreads;
-      if (j < nskip) s_skip[j] = v[u];
+      if (j < nskip) s_skip[j] = skv[u];
     }
     __syncthreads();
   }
@@ -258,9 +283,10 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample(SampleArgs A) {
     hidx[h] = kSampleThreads;
   }
   __syncthreads();
+  sstamp(A.dbg, 4);
   const double total = s_total;
   const uint2 key = make_uint2((uint32_t)(A.seed & 0xffffffffu), (uint32_t)(A.seed >> 32));
-  const uint32_t t = (uint32_t)st->t;
+  const uint32_t t = (uint32_t)s_tcur;
   int64_t jb = 0;
   for (; jb < kJMax; jb += kSampleThreads) {
     const int c = s_c;
@@ -313,12 +339,15 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample(SampleArgs A) {
     }
     __syncthreads();
   }
+  sstamp(A.dbg, 5);
+  if (A.dbg && tid == 0) A.dbg[6] = jb / kSampleThreads;   // rounds
   const int c = s_c;
   for (int i = tid; i < c; i += kSampleThreads) A.S_t[i] = chosen[i];
   if (tid == 0) {
     st->b_t = c;
     st->draws = (c == bt) ? s_new : (int)jb;
   }
+  sstamp(A.dbg, 7);
 }
 
 cudaError_t launch_sample(const SampleArgs& a, cudaStream_t s) {

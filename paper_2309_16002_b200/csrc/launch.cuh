@@ -35,6 +35,7 @@ struct SampleArgs {
   int greedy;             // RBGP (Remark 4.2): S_t = the top b_t rows of d (k_topb), no draw
   const int64_t* S_top;   // greedy: top rows of d, in order
   const int* top_cnt;     // greedy: how many of them have d > 0
+  long long* dbg = nullptr;   // optional: %globaltimer stamps of the phases (RBRP_DEBUG_STAMPS)
 };
 cudaError_t launch_sample(const SampleArgs& a, cudaStream_t s);
 // distributed sampling: every rank resolves the draws that land in its

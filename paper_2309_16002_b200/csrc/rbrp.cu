@@ -363,6 +363,7 @@ void make_sample_args(SampleArgs& sa, const Ctx<T>& c, int dist) {
   sa.greedy = c.p->greedy ? 1 : 0;
   sa.S_top = c.p->greedy ? (const int64_t*)((char*)c.ws + c.Ly->Stop) : nullptr;
   sa.top_cnt = c.p->greedy ? (const int*)((char*)c.ws + c.Ly->Tcnt) : nullptr;
+  sa.dbg = c.dbg ? c.dbg + 32 : nullptr;
 }
 
 // l.5: RBRP draw, or (RBGP, Remark 4.2) the top-b rows of d computed first by k_topb
@@ -1025,6 +1026,13 @@ int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* 
           fprintf(stderr, "rbrp filter phases (us):");
           for (int i = 1; i < 11; ++i) fprintf(stderr, " %.2f", (t[i] - t[0]) * 1e-3);
           fprintf(stderr, "\n");
+          long long u[8];
+          if (cudaMemcpy(u, c.dbg + 32, sizeof(u), cudaMemcpyDeviceToHost) == cudaSuccess) {
+            fprintf(stderr, "rbrp sample phases (us):");
+            for (int i = 1; i < 8; ++i)
+              if (i != 6) fprintf(stderr, " %.2f", (u[i] - u[0]) * 1e-3);
+            fprintf(stderr, " rounds %lld\n", u[6]);
+          }
         }
       }
     }
