@@ -605,12 +605,14 @@ __global__ void __launch_bounds__(kFiltThreads, 1) k_filter_coop(FilterArgs F) {
   DevState* st = F.st;
   const int tid = threadIdx.x;
   __shared__ int s_first;
+  __shared__ int64_t s_rows[kMaxB];   // S_t (local rows), loaded together with the state
   if (tid == 0) {
     s_stop = st->stop;
     s_nb = st->b_t;
     s_k = st->k;
     s_first = (F.X0 != nullptr && st->t == 1) ? 1 : 0;   // lazy X_res: block 1 reads X
   }
+  if (!F.Vg && tid < kMaxB) s_rows[tid] = F.S_t[tid] - F.row_offset;   // entries >= b_t unused
   __syncthreads();
   if (s_stop || s_nb <= 0) return;   // uniform over the grid
   const int nb = s_nb;
@@ -644,7 +646,7 @@ __global__ void __launch_bounds__(kFiltThreads, 1) k_filter_coop(FilterArgs F) {
         if (F.Vg) {
           x = F.Vg[(int64_t)i * d + c0 + c];
         } else {
-          const int64_t r = F.S_t[i] - F.row_offset;
+          const int64_t r = s_rows[i];
           x = s_first ? (double)((const T*)F.X0)[r * F.ldx0 + c0 + c] : (double)((const T*)F.X)[r * F.ldx + c0 + c];
         }
       }

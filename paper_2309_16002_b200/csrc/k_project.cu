@@ -267,18 +267,31 @@ __global__ void __launch_bounds__(256) k_fixup(T* __restrict__ X, int64_t ldx,
   const int bp = st->b_prime;
   const int i = blockIdx.x;
   if (i >= bp) return;
-  if (i == 0 && threadIdx.x == 0) {
-    // diag(L_1) of this block = diag(R_V(1:b',1:b')) as stored in L (Remark 5.2 trigger)
-    double mn = st->ldiag_min, mx = st->ldiag_max;
-    for (int j = 0; j < bp; ++j) {
-      const double a = fabs((double)(T)Rtot[j * kMaxB + j]);
-      mn = fmin(mn, a);
-      mx = fmax(mx, a);
-    }
-    st->ldiag_min = mn;
-    st->ldiag_max = mx;
-  }
   const int64_t k0 = st->k;
+  if (i == 0 && threadIdx.x < 32) {
+    // diag(L_1) of this block = diag(R_V(1:b',1:b')) as stored in L (Remark 5.2 trigger):
+    // min / max over the warp (lanes j, j + 32, ...), all loads in flight together
+    const int lane = threadIdx.x;
+    double mn = INFINITY, mx = 0.0;
+#pragma unroll
+    for (int u = 0; u < kMaxB / 32; ++u) {
+      const int j = lane + 32 * u;
+      if (j < bp) {
+        const double a = fabs((double)(T)Rtot[j * kMaxB + j]);
+        mn = fmin(mn, a);
+        mx = fmax(mx, a);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if (lane == 0) {
+      st->ldiag_min = fmin(st->ldiag_min, mn);
+      st->ldiag_max = fmax(st->ldiag_max, mx);
+    }
+  }
   const int64_t r = S[k0 + i] - row_offset;
   if (r < 0 || r >= n_local) return;
   if (X)   // residual form: the skeleton's residual row is 0 (paper form: X is read only)
