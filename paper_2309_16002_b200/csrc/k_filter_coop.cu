@@ -15,6 +15,7 @@
 //   F  every CTA: Cholesky G2 = R2^T R2 (CholQR2) with T2 = R2^{-1}; CTA 0: R_total = R2 R11
 //   G  Q_b(:, cols) = Q1 T2 -> Qt (rows >= b' zero up to bp_pad)
 // Four grid-wide barriers.
+#include <atomic>
 #include <cooperative_groups.h>
 #include <float.h>
 
@@ -861,6 +862,36 @@ __global__ void __launch_bounds__(kFiltThreads, 1) k_filter_coop(FilterArgs F) {
 
 static size_t filter_smem() { return filter_smem_base + 2 * 32 * 32 * sizeof(double); }
 
+// can a cluster of nc CTAs of the filter be resident (one GPC with nc free SMs)?  Cached per
+// device and cluster size; no: the cooperative launch
+template <typename T>
+bool cluster_fits(int nc, size_t smem) {
+  static std::atomic<int> cache[256][9];   // 0 unknown, 1 yes, 2 no
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::atomic<int>& c = cache[dev & 255][nc];
+  int v = c.load(std::memory_order_relaxed);
+  if (v == 0) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nc);
+    cfg.blockDim = dim3(kFiltThreads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute la[1];
+    la[0].id = cudaLaunchAttributeClusterDimension;
+    la[0].val.clusterDim.x = (unsigned)nc;
+    la[0].val.clusterDim.y = 1;
+    la[0].val.clusterDim.z = 1;
+    cfg.attrs = la;
+    cfg.numAttrs = 1;
+    int n = 0;
+    const cudaError_t e = cudaOccupancyMaxActiveClusters(&n, k_filter_coop<T>, &cfg);
+    if (e != cudaSuccess) cudaGetLastError();   // clear; fall back to the cooperative launch
+    v = (e == cudaSuccess && n >= 1) ? 1 : 2;
+    c.store(v, std::memory_order_relaxed);
+  }
+  return v == 1;
+}
+
 template <typename T>
 cudaError_t launch_filter_coop(const FilterArgs& a, cudaStream_t s) {
   const int nsplit = ceil_div(a.d, kFiltCW);
@@ -881,7 +912,7 @@ cudaError_t launch_filter_coop(const FilterArgs& a, cudaStream_t s) {
   cfg.stream = s;
   cudaLaunchAttribute la[1];
   FilterArgs b = a;
-  b.cluster = !coop_only && nsplit <= 8;
+  b.cluster = !coop_only && nsplit <= 8 && cluster_fits<T>(nsplit, smem);
   if (b.cluster) {
     la[0].id = cudaLaunchAttributeClusterDimension;
     la[0].val.clusterDim.x = (unsigned)nsplit;
