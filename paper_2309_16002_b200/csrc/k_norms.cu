@@ -121,7 +121,8 @@ __global__ void __launch_bounds__(1024) k_chunk_scan(const double* __restrict__ 
   if (lane == 0) excl = 0.0;
   if (lane == 31) wsum[w] = incl;
   __syncthreads();
-  if (c) atomicAdd(&cnt, c);
+  const int wc = __reduce_add_sync(0xffffffffu, c);   // one shared atomic per warp
+  if (lane == 0 && wc) atomicAdd(&cnt, wc);
   if (w == 0) {
     double x = wsum[lane];
 #pragma unroll
