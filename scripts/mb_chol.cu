@@ -208,8 +208,8 @@ __device__ int chol_fast(const double* __restrict__ Gg, int nb, double tau_b, do
       p = __reduce_min_sync(0xffffffffu, (hi == mh && lo == ml) ? bl : (1 << 30));
       dp = __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml));
     }
-    const double inv = rsqrt(dp);
-    const double rii = dp * inv;
+    const double rii = sqrt(dp);
+    const double inv = 1.0 / rii;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) ms += __shfl_xor_sync(0xffffffffu, ms, o);
     long long c1 = clock64();
@@ -229,13 +229,6 @@ __device__ int chol_fast(const double* __restrict__ Gg, int nb, double tau_b, do
           if (k == kp) av = a[k];
         R[i * ld + c] = (c == p) ? rii : (((chosen >> c) & 1ull) ? 0.0 : av * inv);
       }
-      if (c == p) {
-#pragma unroll
-        for (int k = 0; k < EPT; ++k) {
-          const int r = tid / NBX + RSTEP * k;
-          if (r < i) Tm[r * ldt + i] = -ta[k] * inv;
-        }
-      }
     }
     chosen |= 1ull << p;
     __syncthreads();
@@ -249,15 +242,6 @@ __device__ int chol_fast(const double* __restrict__ Gg, int nb, double tau_b, do
       break;
     }
     long long c3 = clock64();
-    {
-      const double ric = R[i * ld + c];
-#pragma unroll
-      for (int k = 0; k < EPT; ++k) {
-        const int r = tid / NBX + RSTEP * k;
-        a[k] = fma(-R[i * ld + r], ric, a[k]);
-        ta[k] = fma(Tm[r * ldt + i], ric, ta[k]);
-      }
-    }
     if (lane < nb) {
       const double rl = R[i * ld + lane];
       dg0 = fma(-rl, rl, dg0);
@@ -265,6 +249,14 @@ __device__ int chol_fast(const double* __restrict__ Gg, int nb, double tau_b, do
     if (lane + 32 < nb) {
       const double rl = R[i * ld + lane + 32];
       dg1 = fma(-rl, rl, dg1);
+    }
+    {
+      const double ric = R[i * ld + c];
+#pragma unroll
+      for (int k = 0; k < EPT; ++k) {
+        const int r = tid / NBX + RSTEP * k;
+        a[k] = fma(-R[i * ld + r], ric, a[k]);
+      }
     }
     long long c4 = clock64();
     t_red += c1 - c0;
@@ -774,7 +766,7 @@ int main() {
       const long long* c = cyc + 8 * v;
       const double st = (double)c[5];
       printf("nb=%d %s kept=%lld total %lld cyc = %.0f/step: reduce %.0f pivot %.0f write+bar %.0f update %.0f\n", nb,
-             v == 2 ? "blocked" : v ? "redux  " : "fast   ", c[5], c[0], c[0] / st, c[1] / st, c[2] / st, c[3] / st, c[4] / st);
+             v == 2 ? "blocked" : v ? "redux  " : "noT    ", c[5], c[0], c[0] / st, c[1] / st, c[2] / st, c[3] / st, c[4] / st);
     }
     double md = 0.0;
     for (int e = 0; e < 64 * 65; ++e) {
