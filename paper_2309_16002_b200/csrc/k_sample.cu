@@ -24,6 +24,7 @@ static_assert(kMaxB + kSampleThreads <= kHashSize / 2 && kMaxB + kSampleRound <=
 constexpr int kSkipRows = 64;       // rows per entry of the shared skip table
 constexpr int kSkipMax = 2048;      // skip table in shared memory up to 131072 local rows
 static_assert(kMaxB <= kSampleThreads, "one block-log entry per thread");
+static_assert(kChunk % kSampleThreads == 0 && kChunk / 2 <= kSkipMax, "fused one-chunk scan");
 
 // smallest local row r of global chunk q with cpre[r] > tq; falls back to the last
 // positive row of the chunk when tq is past the chunk's end (rounding).  skip (optional):
@@ -106,11 +107,21 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample(SampleArgs A) {
   const bool use_skip = nskip <= kSkipMax && A.replay_len < 0 && !A.greedy && !A.dist;
   constexpr int kSkipU = kSkipMax / kSampleThreads;
   double skv[kSkipU];
-  if (use_skip) {
+  if (use_skip && !A.fuse_scan) {
 #pragma unroll
     for (int u = 0; u < kSkipU; ++u) {
       const int64_t j = tid + (int64_t)u * kSampleThreads, r = j * sg + sg - 1;
       skv[u] = j < nskip ? A.cpre[r < A.n_local ? r : A.n_local - 1] : 0.0;
+    }
+  }
+  // fused scan (one chunk): thread t owns rows [16 t, 16 t + 16) of d
+  constexpr int kScanR = kChunk / kSampleThreads;
+  double dv[kScanR];
+  if (A.fuse_scan) {
+#pragma unroll
+    for (int u = 0; u < kScanR; ++u) {
+      const int64_t r = (int64_t)kScanR * tid + u;
+      dv[u] = r < A.n_local ? A.dvec[r] : 0.0;
     }
   }
   const bool may_log = !A.first && A.log.bt != nullptr && tid < A.log.b;
@@ -123,7 +134,55 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample(SampleArgs A) {
   if (w == 1 && lane < kStWords)
     reinterpret_cast<unsigned long long*>(&s_st)[lane] = reinterpret_cast<const unsigned long long*>(st)[lane];
   // (1) chunk prefix, fixed order: lane l sums a contiguous range of chunks
-  if (w == 0) {
+  if (A.fuse_scan) {
+    // the chunk-local prefix cpre of k_chunk_scan, computed here (fixed order: rows within a
+    // thread, then a warp scan, then the warp totals): cpre to global memory and, as the skip
+    // table, to shared memory; the chunk's total and positive count
+    __shared__ double s_wsum[kSampleThreads / 32];
+    __shared__ int s_wcnt[kSampleThreads / 32];
+    double sacc = 0.0;
+    int cnt = 0;
+#pragma unroll
+    for (int u = 0; u < kScanR; ++u) {
+      sacc += dv[u];
+      cnt += dv[u] > 0.0;
+    }
+    double incl = sacc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int wc = __reduce_add_sync(0xffffffffu, cnt);
+    if (lane == 31) s_wsum[w] = incl;
+    if (lane == 0) s_wcnt[w] = wc;
+    __syncthreads();
+    double base = 0.0;
+    long long np = 0;
+    for (int q = 0; q < kSampleThreads / 32; ++q) {
+      if (q < w) base += s_wsum[q];
+      np += s_wcnt[q];
+    }
+    double pfx = base + incl - sacc;   // exclusive prefix of this thread's rows
+#pragma unroll
+    for (int u = 0; u < kScanR; ++u) {
+      const int64_t r = (int64_t)kScanR * tid + u;
+      pfx += dv[u];
+      if (r < A.n_local) {
+        A.cpre[r] = pfx;
+        if (sg == 1) s_skip[r] = pfx;
+        else if ((r & 1) || r == A.n_local - 1) s_skip[r >> 1] = pfx;   // sg = 2
+      }
+    }
+    if (tid == kSampleThreads - 1) {
+      s_total = pfx;
+      s_np = np;
+      A.cprefix[0] = pfx;
+      s_cpref[0] = pfx;
+      A.ctot[0] = pfx;
+      A.cpos[0] = (int32_t)np;
+    }
+  } else if (w == 0) {
     const int nch = A.nchunks;
     const int per = (nch + 31) / 32;
     const int c0 = lane * per, c1 = min(nch, c0 + per);
@@ -270,7 +329,7 @@ __global__ void __launch_bounds__(kSampleThreads) k_sample(SampleArgs A) {
     return;
   }
   // (3) rejection rounds
-  if (use_skip) {
+  if (use_skip && !A.fuse_scan) {
 #pragma unroll
     for (int u = 0; u < kSkipU; ++u) {
       const int64_t j = tid + (int64_t)u * kSampleThreads;

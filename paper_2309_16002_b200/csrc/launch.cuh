@@ -14,11 +14,11 @@ cudaError_t launch_chunk_scan(const double* dvec, int64_t n_local, int64_t chunk
 // k_sample.cu — Alg. 2 l.3-5
 struct SampleArgs {
   DevState* st;
-  const double* ctot;     // per-chunk totals (global chunk index)
-  const int32_t* cpos;    // per-chunk positive counts
+  double* ctot;           // per-chunk totals (global chunk index; written by a fused scan)
+  int32_t* cpos;          // per-chunk positive counts
   double* cprefix;        // out: inclusive prefix over chunks
   int nchunks;
-  const double* cpre;     // chunk-local inclusive prefix of d (local rows)
+  double* cpre;           // chunk-local inclusive prefix of d (local rows)
   const double* dvec;
   int64_t n_local, row_offset;
   int64_t* S_t;           // out: candidates (global ids)
@@ -36,6 +36,7 @@ struct SampleArgs {
   const int64_t* S_top;   // greedy: top rows of d, in order
   const int* top_cnt;     // greedy: how many of them have d > 0
   long long* dbg = nullptr;   // optional: %globaltimer stamps of the phases (RBRP_DEBUG_STAMPS)
+  int fuse_scan = 0;          // one chunk, single GPU: the sampler scans d itself (no k_chunk_scan)
 };
 cudaError_t launch_sample(const SampleArgs& a, cudaStream_t s);
 // distributed sampling: every rank resolves the draws that land in its

@@ -339,6 +339,13 @@ void make_ctx(Ctx<T>& c, const rbrp_problem* p, void* Xv, char* ws, const Layout
   }
 }
 
+// one sampling chunk on one GPU: k_sample computes the chunk scan itself (no k_chunk_scan
+// launch; RBRP_NO_FUSE_SCAN=1 keeps the separate kernel)
+template <typename T>
+bool fuse_scan(const Ctx<T>& c) {
+  return !c.comm && c.Ly->nchunks == 1 && c.n <= RBRP_CHUNK && c.chunk0 == 0 && !env_on("RBRP_NO_FUSE_SCAN");
+}
+
 template <typename T>
 void make_sample_args(SampleArgs& sa, const Ctx<T>& c, int dist) {
   memset(&sa, 0, sizeof(sa));
@@ -364,6 +371,7 @@ void make_sample_args(SampleArgs& sa, const Ctx<T>& c, int dist) {
   sa.S_top = c.p->greedy ? (const int64_t*)((char*)c.ws + c.Ly->Stop) : nullptr;
   sa.top_cnt = c.p->greedy ? (const int*)((char*)c.ws + c.Ly->Tcnt) : nullptr;
   sa.dbg = c.dbg ? c.dbg + 32 : nullptr;
+  sa.fuse_scan = (!dist && fuse_scan(c)) ? 1 : 0;
 }
 
 // l.5: RBRP draw, or (RBGP, Remark 4.2) the top-b rows of d computed first by k_topb
@@ -517,7 +525,7 @@ int enqueue_block(Ctx<T>& c, SampleArgs& sa, cudaStream_t s, Prof* prof, int* nl
     LK(launch_zero_prev<T>(c.Lm, c.k_cap, c.S, c.n, p->row_offset, c.st, s));
     LK(launch_append_q<T>(c.Qt, c.d, c.Qall, c.st, s));
   }
-  LK(launch_chunk_scan(c.dvec, c.n, c.chunk0, c.cpre, c.ctot, c.cpos, s));
+  if (!fuse_scan(c)) LK(launch_chunk_scan(c.dvec, c.n, c.chunk0, c.cpre, c.ctot, c.cpos, s));
   if (prof) prof->end();
   if (c.comm) {
     int rc = comm_allgather_chunks(c.comm, c.ctot, c.cpos, c.chunk0, (c.n + RBRP_CHUNK - 1) / RBRP_CHUNK,
@@ -944,8 +952,10 @@ int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* 
   prof.begin(0);
   ++nl;
   CK(launch_init_norms<T>(c.X, p->ld, c.Xres, c.n, c.d, c.dvec, c.st, !inplace && !c.paper && !c.lazy, s));
-  ++nl;
-  CK(launch_chunk_scan(c.dvec, c.n, c.chunk0, c.cpre, c.ctot, c.cpos, s));
+  if (!fuse_scan(c)) {
+    ++nl;
+    CK(launch_chunk_scan(c.dvec, c.n, c.chunk0, c.cpre, c.ctot, c.cpos, s));
+  }
   prof.end();
   if (comm) {
     int rc = comm_allgather_chunks(comm, c.ctot, c.cpos, c.chunk0, (c.n + RBRP_CHUNK - 1) / RBRP_CHUNK,
