@@ -162,6 +162,31 @@ def test_form_w_kernels_against_oracle(dtype, k):
 
 
 @cuda
+@pytest.mark.parametrize("k", [33, 65, 100, 127, 129, 200])
+def test_trinv_paths_edge_sizes(monkeypatch, k):
+    """L_1^{-1} at the edges of its kernels: k_trinv_one (32 < k <= 128; k padded to a
+    multiple of 8 with an identity block) and k_trinv_blk (k > 128), on an L_1 with a
+    non-unit diagonal; W through rbrp_form_w against the oracle's triangular solve, and the
+    one-CTA inverse against the grid one (RBRP_TRINV_GRID=1) within the same bound."""
+    rb = _rb()
+    rng = np.random.default_rng(1000 + k)
+    n = 3000
+    L = rng.standard_normal((n, k))
+    S = sorted(rng.choice(n, k, replace=False).tolist())
+    L[S] = np.diag(rng.uniform(0.5, 2.0, k)) + 0.3 * np.tril(rng.standard_normal((k, k)), -1) / np.sqrt(k)
+    Lg = torch.from_numpy(L).cuda()
+    Wo, kappa, _ = O.form_W(L, S, method="trsm")
+    tol = max(1e-10, 10 * kappa * 1.1e-16)
+    W1, _, _ = rb.rbrp.form_w(Lg, S, method="trsm")
+    monkeypatch.setenv("RBRP_TRINV_GRID", "1")
+    W2, _, _ = rb.rbrp.form_w(Lg, S, method="trsm")
+    for W in (W1, W2):
+        Wd = W.cpu().numpy()
+        assert np.linalg.norm(Wd - Wo) <= tol * np.linalg.norm(Wo)
+        assert np.array_equal(Wd[S], np.eye(k))
+
+
+@cuda
 @pytest.mark.parametrize("b", [16, 64])
 def test_replay_parity_fp32_c4_small(monkeypatch, b):
     """fp32 (c4-like): the default projection (fp32 storage, fp64 DMMA arithmetic, reading
