@@ -86,6 +86,25 @@ def test_c1_first_block_candidates_match_oracle():
         assert res.blocks[0] == ores.blocks[0].S_t
 
 
+@cuda
+@pytest.mark.parametrize("n", [3000, 3 * 4096 + 100])
+def test_candidates_with_many_repeated_draws(n):
+    """Sampling without replacement by rejecting repeats (reading R6) when almost every draw
+    repeats: five rows hold all but ~1e-3 of the mass, so block 1 needs thousands of draws
+    (dozens of 256-draw rounds of the shared hash set) to find b distinct rows.  Block 1's
+    candidates, in draw order, equal the oracle's; one chunk (the sampler's own scan) and
+    several chunks."""
+    rng = np.random.default_rng(n)
+    X = rng.standard_normal((n, 48))
+    X[[7, 100, 1234, 2000, n - 1]] *= 1000.0
+    rb = _rb()
+    Xd = torch.from_numpy(X).cuda()
+    for seed in range(3):
+        ores = O.rbrp(X, k=16, b=16, seed=seed)
+        res = rb.id(Xd, k=16, b=16, seed=seed)
+        assert res.blocks[0] == ores.blocks[0].S_t, seed
+
+
 def _replay(Xnp, ores, dtype, b, with_pivots=True):
     rb = _rb()
     blocks = [blk.S_t for blk in ores.blocks]
