@@ -8,6 +8,8 @@
 //           j * KC + (c ^ f(j)), f(j) = 8 (j & 1) ^ 4 ((j >> 1) & 3)  (conflict-free);
 //   image 2 (update pass, B fragments indexed by (row pair p, column)): the 16-byte unit
 //           (Q(2p, c), Q(2p+1, c)) of pair p and column c at p * KC + (c ^ 2 (p & 3)).
+#include <algorithm>
+
 #include "launch.cuh"
 
 namespace rbrp {
@@ -39,6 +41,33 @@ __global__ void k_pack_q(const QT* __restrict__ Qt, int64_t d, double* __restric
   const int pr = j >> 1;
   double* Q2 = Qp + (int64_t)gridDim.x * pk::PACK_ROWS * pk::KC + (int64_t)c * pk::PACK_ROWS * pk::KC;
   Q2[(pr * pk::KC + (col ^ (2 * (pr & 3)))) * 2 + (j & 1)] = v;
+}
+
+struct CopySegs {
+  CopySeg seg[kMaxCopySegs];
+};
+__global__ void k_copy_segments(CopySegs a) {
+  const CopySeg sg = a.seg[blockIdx.y];
+  const uint32_t* src = (const uint32_t*)sg.src;
+  uint32_t* dst = (uint32_t*)sg.dst;
+  const size_t nw = sg.bytes / 4;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
+cudaError_t launch_copy_segments(const CopySeg* segs, int nseg, cudaStream_t s) {
+  if (nseg <= 0) return cudaSuccess;
+  if (nseg > kMaxCopySegs) return cudaErrorInvalidValue;
+  CopySegs a = {};
+  size_t mx = 0;
+  for (int i = 0; i < nseg; ++i) {
+    if (segs[i].bytes % 4) return cudaErrorInvalidValue;
+    a.seg[i] = segs[i];
+    mx = segs[i].bytes > mx ? segs[i].bytes : mx;
+  }
+  const unsigned gx = (unsigned)std::min<size_t>(std::max<size_t>((mx / 4 + 255) / 256, 1), 64);
+  k_copy_segments<<<dim3(gx, (unsigned)nseg), 256, 0, s>>>(a);
+  return cudaGetLastError();
 }
 
 static int pk_nc(int64_t d) { return (int)((d + pk::KC - 1) / pk::KC); }

@@ -107,6 +107,15 @@ cudaError_t launch_update_mma(double* Xres, int64_t ldx, const double* Qt, const
                               int bucket, cudaStream_t s);
 // k_pack.cu — Q_b packed in the shared-memory image of k_lhat_paper (two images)
 size_t fused_pack_bytes(int64_t d);
+// up to 8 (src, dst, bytes) segments copied by one kernel (4-byte words; bytes % 4 == 0),
+// e.g. device -> pinned (host-mapped) memory: one launch instead of one copy per segment
+struct CopySeg {
+  const void* src;
+  void* dst;
+  size_t bytes;
+};
+constexpr int kMaxCopySegs = 8;
+cudaError_t launch_copy_segments(const CopySeg* segs, int nseg, cudaStream_t s);
 // Q_b image 1 of the packed layout (k_pack.cu): row j, column col of a 64-column chunk at
 // j * 64 + pack_qswz(j, col) (conflict-free B fragments of the L-hat pass)
 __host__ __device__ __forceinline__ int pack_qswz(int j, int col) {

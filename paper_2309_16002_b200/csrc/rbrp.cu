@@ -1079,18 +1079,26 @@ int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* 
     }
     prof.end();
   }
+  // the report (S, state, block log) into the pinned staging buffer: one kernel writing the
+  // host-mapped memory instead of one copy per array
   int64_t* hS = (int64_t*)(hp + o_S);
-  CK(cudaMemcpyAsync(hS, c.S, (size_t)std::max<int64_t>(k, 1) * 8, cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(hst, c.st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
   const int nlog = std::max(nblocks, 1);
-  CK(cudaMemcpyAsync(hp + o_bt, c.log.bt, nlog * 4, cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(hp + o_bp, c.log.bp, nlog * 4, cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(hp + o_rho, c.log.rho, nlog * 8, cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(hp + o_ts, c.log.ts, nlog * 16, cudaMemcpyDeviceToHost, s));
   const bool want_blocks = rep && (rep->block_idx || rep->block_piv);
-  if (want_blocks) {
-    CK(cudaMemcpyAsync(hp + o_lSt, c.log.St, (size_t)nlog * b * 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(hp + o_lpiv, c.log.piv, (size_t)nlog * b * 4, cudaMemcpyDeviceToHost, s));
+  {
+    CopySeg sg[kMaxCopySegs];
+    int ns = 0;
+    sg[ns++] = {c.S, hS, (size_t)std::max<int64_t>(k, 1) * 8};
+    sg[ns++] = {c.st, hst, sizeof(DevState)};
+    sg[ns++] = {c.log.bt, hp + o_bt, (size_t)nlog * 4};
+    sg[ns++] = {c.log.bp, hp + o_bp, (size_t)nlog * 4};
+    sg[ns++] = {c.log.rho, hp + o_rho, (size_t)nlog * 8};
+    sg[ns++] = {c.log.ts, hp + o_ts, (size_t)nlog * 16};
+    if (want_blocks) {
+      sg[ns++] = {c.log.St, hp + o_lSt, (size_t)nlog * b * 8};
+      sg[ns++] = {c.log.piv, hp + o_lpiv, (size_t)nlog * b * 4};
+    }
+    ++nl;
+    CK(launch_copy_segments(sg, ns, s));
   }
   if (rep && rep->d_out && c.n > 0)   // the final d^(t) (residual squared row norms)
     CK(cudaMemcpyAsync(rep->d_out, c.dvec, (size_t)c.n * 8, cudaMemcpyDeviceToDevice, s));
