@@ -936,7 +936,10 @@ int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* 
   hst->b = p->b;
   hst->ldiag_min = DBL_MAX;
   hst->ldiag_max = 0.0;
-  CK(cudaMemcpyAsync(c.st, hst, sizeof(DevState), cudaMemcpyHostToDevice, s));
+  {
+    const CopySeg sg = {hst, c.st, sizeof(DevState)};   // pinned staging -> device, by a kernel
+    CK(launch_copy_segments(&sg, 1, s));
+  }
 
   Prof prof;
   prof.on = rep && rep->profile;
@@ -1048,9 +1051,13 @@ int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* 
     }
   }
 
-  // read the state (k, flags) before W
+  // read the state (k, flags) before W (written into the pinned staging by a kernel)
   hm.mark("loop_enqueued");
-  CK(cudaMemcpyAsync(hst, c.st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+  {
+    const CopySeg sg = {c.st, hst, sizeof(DevState)};
+    ++nl;
+    CK(launch_copy_segments(&sg, 1, s));
+  }
   CK(cudaStreamSynchronize(s));
   hm.mark("loop_done");
   if (hst->nonfinite) return RBRP_ENONFINITE;
