@@ -765,7 +765,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     for (int u = 0; u < PF; ++u) {
       const int e = tid + u * kWsThreads, r = e / kWsK, c = e - r * kWsK;
       const int64_t row = tile * kWsRows + r;
-      pf[u] = (c < kp && row < n) ? L[row * ldl + c] : T(0);
+      pf[u] = (c < k && row < n) ? L[row * ldl + c] : T(0);   // L's columns [k, kp) read as zeros
     }
   };
   int64_t tile = blockIdx.x;

@@ -829,12 +829,13 @@ int enqueue_W(Ctx<T>& c, const rbrp_problem* p, rbrp_comm* comm, void* W_out, in
     ++*nl;
     CK(launch_trinv<T>(L1, k, LinvT, kp, c.st, s, c.Pinv));
   }
-  if (kp > k && kp <= k_cap && c.n > 0)
+  const bool w_small = !force_simt() && kp <= k_cap && w_small_supported<T>(kp) && !env_on("RBRP_W_NOSMALL") &&
+                       !env_on("RBRP_W_SIMT");
+  if (kp > k && kp <= k_cap && c.n > 0 && !w_small)   // k_w_small reads columns [k, kp) as zeros
     CK(cudaMemset2DAsync(c.Lm + k, (size_t)k_cap * sizeof(T), 0, (size_t)(kp - k) * sizeof(T), (size_t)c.n, s));
   cudaError_t merr = cudaSuccess;
   ++*nl;
-  if (!force_simt() && kp <= k_cap && w_small_supported<T>(kp) && !env_on("RBRP_W_NOSMALL") &&
-      !env_on("RBRP_W_SIMT")) {
+  if (w_small) {
     // K <= 128: L_1^{-T} resident in shared memory, one pass over L (k_w_small)
     CK(launch_w_small<T>(c.Lm, k_cap, LinvT, c.n, k, kp, (T*)W_out, k_cap, !clip, s));
   } else if (!force_simt() && kp <= k_cap && c.Wsc && !env_on("RBRP_W_NTMMA") && !env_on("RBRP_W_SIMT") &&
