@@ -70,6 +70,15 @@ cudaError_t launch_copy_segments(const CopySeg* segs, int nseg, cudaStream_t s) 
   return cudaGetLastError();
 }
 
+__global__ void k_set_state(DevState v, DevState* st) {
+  if (threadIdx.x == 0) *st = v;
+}
+
+cudaError_t launch_set_state(const DevState& v, DevState* st, cudaStream_t s) {
+  k_set_state<<<1, 32, 0, s>>>(v, st);
+  return cudaGetLastError();
+}
+
 static int pk_nc(int64_t d) { return (int)((d + pk::KC - 1) / pk::KC); }
 
 size_t fused_pack_bytes(int64_t d) { return 2 * (size_t)pk_nc(d) * pk::PACK_ROWS * pk::KC * 8; }   // two images

@@ -116,6 +116,8 @@ struct CopySeg {
 };
 constexpr int kMaxCopySegs = 8;
 cudaError_t launch_copy_segments(const CopySeg* segs, int nseg, cudaStream_t s);
+// *st = v, the value travelling as a kernel parameter (no copy, no PCIe read)
+cudaError_t launch_set_state(const DevState& v, DevState* st, cudaStream_t s);
 // Q_b image 1 of the packed layout (k_pack.cu): row j, column col of a 64-column chunk at
 // j * 64 + pack_qswz(j, col) (conflict-free B fragments of the L-hat pass)
 __host__ __device__ __forceinline__ int pack_qswz(int j, int col) {

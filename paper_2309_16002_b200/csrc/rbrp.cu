@@ -937,10 +937,7 @@ int run(const rbrp_problem* p, void* Xv, char* ws, const Layout& Ly, rbrp_comm* 
   hst->b = p->b;
   hst->ldiag_min = DBL_MAX;
   hst->ldiag_max = 0.0;
-  {
-    const CopySeg sg = {hst, c.st, sizeof(DevState)};   // pinned staging -> device, by a kernel
-    CK(launch_copy_segments(&sg, 1, s));
-  }
+  CK(launch_set_state(*hst, c.st, s));   // the initial state as a kernel parameter
 
   Prof prof;
   prof.on = rep && rep->profile;
